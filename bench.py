@@ -1,0 +1,319 @@
+#!/usr/bin/env python
+"""farPCA time-to-epsilon benchmark (BASELINE.json metric) on B200.
+
+Workload (BASELINE.json configs[1], the metric's single-GPU config "C2"):
+  A = U diag(sigma) V', 8000 x 8000 FP64, sigma_i = 10^(-i/50) (i = 1..900; smaller
+  values drop below 1e-18 sigma_1 as in synthetic.cpp:21), U, V from QR of seeded
+  N(0,1) matrices (synthetic stand-in, torch.Generator seed 42);
+  standardized-Bernoulli Omega (p = 1/2), b = 50, P = 2, eps = 1e-3 relative.
+
+One step = one full run_fixed_precision to eps (rank 200, 4 blocks) through the
+engine, A resident in HBM (512 MB > 126 MB L2, so no L2 flush is needed between
+steps).  `e2e` repeats the step through the public API with A in pinned host
+memory (H2D inside the timed region) and Q, B' returned to the host.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+M = N = 8000
+RANK_SIG = 900
+BLOCK, POWER, EPS, P_BERN = 50, 2, 1e-3, 0.5
+SEED_A, SEED_OMEGA = 42, 7
+FP64_PEAK_TFLOPS = 37.1     # measured DMMA peak on this pool (profiles/fp64_peak_r01.txt)
+WORKLOAD = "C2: 8000x8000 FP64, sigma_i=10^(-i/50), StdBernoulli p=1/2, b=50, P=2, eps=1e-3"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def make_matrix(device):
+    import torch
+    g = torch.Generator(device=device).manual_seed(SEED_A)
+    u = torch.linalg.qr(torch.randn(M, RANK_SIG, dtype=torch.float64, device=device, generator=g))[0]
+    v = torch.linalg.qr(torch.randn(N, RANK_SIG, dtype=torch.float64, device=device, generator=g))[0]
+    sig = 10.0 ** (-torch.arange(1, RANK_SIG + 1, dtype=torch.float64, device=device) / 50.0)
+    a = (u * sig) @ v.t()
+    return a.t().contiguous().t()  # column-major (DenseMatrix layout)
+
+
+def config():
+    from paper_2506_03859_b200 import FarpcaConfig, SketchKind, SketchSpec
+    return FarpcaConfig(eps=EPS, power=POWER, block=BLOCK,
+                        sketch=SketchSpec(SketchKind.StdBernoulli, P_BERN, SEED_OMEGA), relative=True)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[3:7]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def gemm_roofline(eng, a, stream):
+    """Live per-launch timing of the dominant kernel: the A-pass DMMA GEMM
+    W = A' Y (TN, 8000 x 50 x 8000), CUDA events on the engine's stream."""
+    import torch
+    y = torch.randn(BLOCK, M, dtype=torch.float64, device=a.device).t()   # m x b col-major
+    w = torch.empty(BLOCK, N, dtype=torch.float64, device=a.device).t()
+    yn = torch.empty(BLOCK, M, dtype=torch.float64, device=a.device).t()
+    g = torch.randn(BLOCK, N, dtype=torch.float64, device=a.device).t()
+    reps = 20
+    out = {}
+    for name, trans, outp, bp in (("tn", True, w, y), ("nn", False, yn, g)):
+        for _ in range(3):
+            eng.gemm(trans, N if trans else M, BLOCK, M if trans else N, 1.0, a.data_ptr(), a.stride(1),
+                     bp.data_ptr(), bp.stride(1), 0.0, outp.data_ptr(), outp.stride(1))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            e0.record()
+            for _ in range(reps):
+                eng.gemm(trans, N if trans else M, BLOCK, M if trans else N, 1.0, a.data_ptr(), a.stride(1),
+                         bp.data_ptr(), bp.stride(1), 0.0, outp.data_ptr(), outp.stride(1))
+            e1.record()
+        e1.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        flops = 2.0 * M * N * BLOCK
+        out[name] = {"ms": ms, "tflops": flops / ms / 1e9}
+    return out
+
+
+def load_traffic():
+    path = os.path.join(ROOT, "profiles", "traffic_r01.json")
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return None
+
+
+def cpu_baseline_reference(a_host, kind):
+    """The reference CPU implementation (oracle/_ref, else the C port) on one core."""
+    from oracle.oracle import Oracle, REF_LIB
+    which = "reference" if os.path.exists(REF_LIB) else "port"
+    orc = Oracle(which)
+    t0 = time.perf_counter()
+    r = orc.run(a_host, eps=EPS, power=POWER, block=BLOCK, kind=2, p=P_BERN, seed=SEED_OMEGA, relative=True)
+    dt = time.perf_counter() - t0
+    return dt, which, r
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+
+    import paper_2506_03859_b200 as fqb
+    eng = fqb.Engine(local)
+    stream = torch.cuda.Stream(device=dev)
+    eng.set_stream(stream.cuda_stream)
+    a = make_matrix(dev)
+    torch.cuda.synchronize()
+    cfg = config()
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(args.warmup, 0)):
+        r = eng.run_fixed_precision(a, cfg, output="device")
+        del r
+    barrier()
+    launches0 = eng.launch_count
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    results = []
+    with ClockSampler(local) as clk:
+        with torch.cuda.stream(stream):
+            e0.record()
+        for _ in range(args.steps):
+            results.append(eng.run_fixed_precision(a, cfg, output="device"))
+        with torch.cuda.stream(stream):
+            e1.record()
+        e1.synchronize()
+    barrier()
+    launches = eng.launch_count - launches0
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = t.item()
+    last = results[-1]
+    rank_l, blocks, e_rel = last.rank, last.blocks, float(np.sqrt(max(last.residual_sq, 0) / last.norm_a_sq))
+    del results
+
+    # ---- e2e: host A (pinned) -> public API -> Q, B' back on the host -----------------
+    a_host = a.t().contiguous().cpu().pin_memory()  # (n x m) row-major == A column-major
+    a_host_cm = a_host.t()
+    for _ in range(1):
+        eng.run_fixed_precision(a_host_cm, cfg, output="host")
+    torch.cuda.synchronize()
+    t_e2e = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        r = eng.run_fixed_precision(a_host_cm, cfg, output="host")
+        t_e2e.append(time.perf_counter() - t0)
+    e2e_s = statistics.mean(t_e2e)
+    h2d = M * N * 8
+    d2h = (M + N) * r.rank * 8 + 8 * (r.blocks + 4)
+
+    roof = gemm_roofline(eng, a, stream)
+    dom = roof["tn"]
+    traffic = load_traffic()
+    line = {
+        "metric": "farPCA time-to-eps (s)",
+        "value": ms / 1000.0,
+        "unit": "s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "higher_is_better": False,
+        "scaling": "weak" if world > 1 else "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded torch N(0,1) factors, see bench.py docstring)",
+        "config": {"workload": WORKLOAD, "m": M, "n": N, "block": BLOCK, "power": POWER, "eps": EPS,
+                   "sketch": "stdbernoulli p=0.5", "rank_reached": rank_l, "blocks": blocks,
+                   "rel_error_indicator": e_rel, "l2": "A (512 MB) exceeds the 126 MB L2; no flush",
+                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+        "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": launches,
+        "roofline": {"bound": "tensor", "kernel": "k_gemm<TN> W=A'Y 8000x50x8000 (DMMA f64)",
+                     "achieved": dom["tflops"], "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                     "frac": dom["tflops"] / FP64_PEAK_TFLOPS,
+                     "peak_source": "measured DMMA microbenchmark (MEASURED_PEAKS.json has no FP64 entry)",
+                     "flops_per_launch": 2.0 * M * N * BLOCK, "launch_ms": dom["ms"],
+                     "nn_achieved": roof["nn"]["tflops"],
+                     "traffic": (traffic or {}).get("tn_bytes_per_launch")},
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        a_np = np.asfortranarray(a.cpu().numpy())
+        dt, which, rr = cpu_baseline_reference(a_np, 2)
+        line["cpu_baseline"] = {"value": dt, "unit": "s", "cores": 1, "kind": which,
+                                "sample": f"one full C2 run_fixed_precision (rank {rr.rank}, "
+                                          f"{rr.blocks} blocks), single-threaded like the reference"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def run_reference(args):
+    """--impl reference: the reference's own CPU run_fixed_precision (oracle/_ref)."""
+    import numpy as np
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import torch
+    dev = torch.device("cuda:0") if torch.cuda.is_available() else torch.device("cpu")
+    a = np.asfortranarray(make_matrix(dev).cpu().numpy())
+    from oracle.oracle import Oracle, REF_LIB
+    which = "reference" if os.path.exists(REF_LIB) else "port"
+    orc = Oracle(which)
+    budget_s = 150.0
+    times = []
+    t_start = time.perf_counter()
+    for i in range(max(args.warmup, 0) + args.steps):
+        t0 = time.perf_counter()
+        r = orc.run(a, eps=EPS, power=POWER, block=BLOCK, kind=2, p=P_BERN, seed=SEED_OMEGA, relative=True)
+        dt = time.perf_counter() - t0
+        if i >= min(args.warmup, 1):
+            times.append(dt)
+        if time.perf_counter() - t_start > budget_s and times:
+            break
+        if i == 0 and args.warmup > 0:
+            continue
+    v = statistics.mean(times)
+    line = {"metric": "farPCA time-to-eps (s)", "value": v, "unit": "s", "n_gpus": 0,
+            "steps": len(times), "warmup": min(args.warmup, 1), "ms_per_step": v * 1000,
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (same A as the ours arm)", "impl": "reference",
+            "config": {"workload": WORKLOAD, "rank_reached": r.rank, "blocks": r.blocks},
+            "cpu_baseline": {"value": v, "unit": "s", "cores": 1, "kind": which,
+                             "sample": f"{len(times)} full run(s) within a {budget_s:.0f}s budget; "
+                                       "the reference is single-threaded per factorization"},
+            "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)

@@ -1,0 +1,212 @@
+/*
+ * farqb.h -- C-ABI of libfarqb.so, the B200 (sm_100a) farPCA blocked-QB engine.
+ *
+ * This is the drop-in boundary for the reference's hot path.  The reference is
+ * a C++ library with no FFI of its own; the entry points below are what a
+ * C/ctypes/cgo/JNI binding of its QB API would bind, one for one:
+ *
+ *   fqb_qb_fixed_precision  <- rsvd::run_fixed_precision
+ *                              (/root/reference/proj/include/rsvd/driver.hpp:98-99,
+ *                               src/driver.cpp:347-388)
+ *   fqb_qb_fixed_rank       <- rsvd::run_fixed_rank (driver.hpp:101-103, driver.cpp:390-413)
+ *   fqb_block_source_fn     <- rsvd::BlockSource::next (driver.hpp:67-73)
+ *   fqb_config              <- rsvd::FarpcaConfig (driver.hpp:18-26) + SketchSpec
+ *                              (sketch.hpp:18-22), plus `zeta` (fixed nonzeros per
+ *                              column, BASELINE configs 3-5)
+ *   fqb_qb_result           <- rsvd::ApproxSvd's scalars (driver.hpp:45-58) plus the
+ *                              north-star QB outputs Q (m x l) and B' (n x l)
+ *   fqb_status              <- the exception taxonomy of errors.hpp:9-46 and
+ *                              ToleranceNotReached (driver.hpp:60-65)
+ *   fqb_gen_sketch          <- rsvd::gen_sketch (sketch.hpp:46, sketch.cpp:51-102)
+ *   fqb_sparse_dense_mul    <- rsvd::sparse_dense_mul / centered_product (sketch.cpp:104-140)
+ *   fqb_centering_column    <- rsvd::centering_column (driver.hpp:78, driver.cpp:178-183)
+ *   fqb_frob_norm_sq        <- rsvd::frob_norm_sq (matrix_core.hpp:59, matrix_core.cpp:46-48)
+ *   fqb_gemm                <- rsvd::kern::Ops::gemm_nn / gemm_tn (kernels.hpp:9-19)
+ *   fqb_philox_u32          <- rsvd::Philox::next_u32 (rng.hpp:21-24)
+ *
+ * Conventions: matrices are column-major doubles with an explicit leading
+ * dimension; sizes are int64_t; no C++ types cross this boundary and no
+ * exception escapes it.  Every call returns an fqb_status; the message of the
+ * last failure on the calling thread is fqb_last_error().  There is no CPU
+ * compute path: without a CUDA device every compute entry point fails with
+ * FQB_ERR_CUDA.
+ */
+#ifndef FARQB_H
+#define FARQB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FARQB_ABI_VERSION 1
+
+typedef enum fqb_status {
+    FQB_OK = 0,
+    FQB_ERR_CONFIG = 1,                 /* rsvd::ConfigError                     */
+    FQB_ERR_DIMENSION = 2,              /* rsvd::DimensionError                  */
+    FQB_ERR_BLOCK_DEGENERATE = 3,       /* rsvd::BlockDegenerate (after 3 redraws) */
+    FQB_ERR_TOLERANCE_NOT_REACHED = 4,  /* rsvd::ToleranceNotReached; result still filled */
+    FQB_ERR_CUDA = 5,                   /* CUDA runtime / no device              */
+    FQB_ERR_NCCL = 6,                   /* collective failure                    */
+    FQB_ERR_INVALID_ARGUMENT = 7,       /* null pointer, bad handle, bad enum    */
+    FQB_ERR_CONVERGENCE = 8,            /* rsvd::ConvergenceFailure              */
+    FQB_ERR_CALLBACK = 9,               /* block source returned non-zero        */
+    FQB_ERR_ALLOC = 10                  /* device or host allocation failed      */
+} fqb_status;
+
+/* rsvd::SketchKind, same numbering (sketch.hpp:11). */
+typedef enum fqb_sketch_kind {
+    FQB_GAUSSIAN = 0,
+    FQB_BERNOULLI = 1,
+    FQB_STD_BERNOULLI = 2,
+    FQB_SPARSE_SIGN = 3,
+    FQB_SPARSE_GAUSSIAN = 4
+} fqb_sketch_kind;
+
+typedef struct fqb_sketch_spec {
+    int kind;          /* fqb_sketch_kind                                        */
+    double p;          /* density; 0 picks default_density (driver.cpp:449-455)  */
+    uint64_t seed;
+    int zeta;          /* > 0: exactly zeta nonzeros per column (sign/Gaussian)  */
+} fqb_sketch_spec;
+
+typedef struct fqb_config {
+    double eps;              /* Frobenius tolerance (relative when `relative`)  */
+    int power;               /* power-iteration passes P                        */
+    int block;               /* block size b; 0 picks default_block             */
+    fqb_sketch_spec sketch;
+    int max_iters;           /* 0 picks ceil(n / 2b)                            */
+    int shift_convention;    /* 0 LastDiagonal, 1 FirstDiagonal (driver.hpp:16) */
+    int relative;            /* eps is a fraction of ||A||_F                    */
+} fqb_config;
+
+/* One raw test-matrix block handed over by a block source (HOST memory, owned
+ * by the source, valid until the source is called again or the run returns).
+ * Mirrors rsvd::SketchBlock (sketch.hpp:37-44). */
+typedef struct fqb_block {
+    int is_dense;
+    int rows, cols;
+    const double* dense;     /* rows x cols column-major (ld = rows)            */
+    const int* col_ptr;      /* cols + 1                                        */
+    const int* row_idx;      /* nnz, strictly increasing per column             */
+    const double* values;    /* nnz                                             */
+    int64_t nnz;
+    int centered;            /* StdBernoulli centering trick                    */
+    double p;
+    double std_scale;
+} fqb_block;
+
+/* BlockSource::next.  Return 0 on success, anything else aborts the run with
+ * FQB_ERR_CALLBACK.  NULL source = the on-device Philox generator. */
+typedef int (*fqb_block_source_fn)(void* user, int n, int b, int block_id, fqb_block* out);
+
+/* Output placement flags for fqb_qb_*. */
+#define FQB_OUT_NONE   0u   /* scalars, trace and ids only                       */
+#define FQB_OUT_HOST   1u   /* copy Q and B' into malloc'd host arrays           */
+#define FQB_OUT_DEVICE 2u   /* keep Q and B' on the device (library-owned)       */
+
+typedef struct fqb_qb_result {
+    int status;              /* same as the call's return value                 */
+    int64_t m, n;
+    int rank;                /* l = blocks * b                                  */
+    int blocks;
+    int converged;
+    double residual_sq;      /* E = ||A||_F^2 - sum_j ||B_j||_F^2                */
+    double norm_a_sq;
+    double* q;               /* m x rank, ld = ldq  (host or device, see flags) */
+    int64_t ldq;
+    double* bt;              /* n x rank = B',  ld = ldbt                        */
+    int64_t ldbt;
+    int on_device;
+    double* block_residuals; /* host, E after each accepted block, `blocks`     */
+    int* block_ids;          /* host, every id requested from the source        */
+    int n_ids;
+    int resolved_block;
+    int resolved_max_iters;
+    double resolved_p;
+    int gpu_launches;        /* kernels this call launched                      */
+    double elapsed_ms;       /* device time of the call (CUDA events)           */
+    void* internal;
+} fqb_qb_result;
+
+typedef struct fqb_handle_s* fqb_handle;
+
+/* ---- lifecycle ------------------------------------------------------------- */
+int fqb_abi_version(void);
+fqb_status fqb_create(int device, fqb_handle* out);
+fqb_status fqb_destroy(fqb_handle h);
+/* Run subsequent work on this cudaStream_t (NULL = the handle's own stream). */
+fqb_status fqb_set_stream(fqb_handle h, void* cuda_stream);
+fqb_status fqb_synchronize(fqb_handle h);
+const char* fqb_last_error(void);
+const char* fqb_status_name(int status);
+/* Kernels launched by this handle since creation (launch accounting). */
+int64_t fqb_launch_count(fqb_handle h);
+
+/* ---- the QB loop ----------------------------------------------------------- */
+/* A is m x n column-major with leading dimension lda, on the device when
+ * a_on_device != 0 (used in place when lda is even and 16-byte aligned,
+ * otherwise copied once), else on the host (copied to the device inside the
+ * call).  `src` may be NULL.  On FQB_ERR_TOLERANCE_NOT_REACHED the result is
+ * the partial factorization, like ToleranceNotReached::partial. */
+fqb_status fqb_qb_fixed_precision(fqb_handle h, const double* a, int64_t m, int64_t n,
+                                  int64_t lda, int a_on_device, const fqb_config* cfg,
+                                  fqb_block_source_fn src, void* user, unsigned flags,
+                                  fqb_qb_result* out);
+fqb_status fqb_qb_fixed_rank(fqb_handle h, const double* a, int64_t m, int64_t n,
+                             int64_t lda, int a_on_device, int rank, const fqb_config* cfg,
+                             fqb_block_source_fn src, void* user, unsigned flags,
+                             fqb_qb_result* out);
+void fqb_result_free(fqb_qb_result* r);
+
+/* ---- building blocks (device pointers unless stated) ------------------------ */
+/* First `count` u32 words of the Philox stream (seed, block_id, column), into
+ * host memory; generated on the device. */
+fqb_status fqb_philox_u32(fqb_handle h, uint64_t seed, uint32_t block_id, uint32_t column,
+                          int count, uint32_t* host_out);
+
+/* Host copy of a device-generated test block (rsvd::gen_sketch).  Arrays are
+ * malloc'd by the library; release with fqb_sketch_free. */
+typedef struct fqb_sketch_host {
+    int is_dense, rows, cols;
+    double* dense;
+    int* col_ptr;
+    int* row_idx;
+    double* values;
+    int64_t nnz;
+    int centered;
+    double p, std_scale;
+} fqb_sketch_host;
+fqb_status fqb_gen_sketch(fqb_handle h, const fqb_sketch_spec* spec, int n, int l, int block_id,
+                          fqb_sketch_host* out);
+void fqb_sketch_free(fqb_sketch_host* s);
+
+/* c (m x l, ldc) = a (m x n, lda) * S (CSC, device arrays) [- z broadcast when
+ * z != NULL]; one fused multiply-add per nonzero in CSC order. */
+fqb_status fqb_sparse_dense_mul(fqb_handle h, const double* a, int64_t m, int64_t n, int64_t lda,
+                                const int* col_ptr, const int* row_idx, const double* values,
+                                int l, const double* z, double* c, int64_t ldc);
+/* z (m) = A (p 1_n) */
+fqb_status fqb_centering_column(fqb_handle h, const double* a, int64_t m, int64_t n, int64_t lda,
+                                double p, double* z);
+/* ||A||_F^2 into *host_out */
+fqb_status fqb_frob_norm_sq(fqb_handle h, const double* a, int64_t m, int64_t n, int64_t lda,
+                            double* host_out);
+/* C (m x n) = alpha * op(A) * B + beta * C, op(A) = A (trans_a = 0, A is m x k)
+ * or A' (trans_a = 1, A is k x m); B is k x n.  FP64 on the DMMA tensor pipe. */
+fqb_status fqb_gemm(fqb_handle h, int trans_a, int64_t m, int64_t n, int64_t k, double alpha,
+                    const double* a, int64_t lda, const double* b, int64_t ldb, double beta,
+                    double* c, int64_t ldc);
+
+/* ---- defaults (driver.cpp:449-466) ------------------------------------------- */
+double fqb_default_density(int kind, int64_t n);
+int fqb_default_block(int64_t m, int64_t n);
+int fqb_default_max_iters(int64_t n, int b);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

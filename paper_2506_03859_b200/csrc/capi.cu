@@ -1,0 +1,360 @@
+// capi.cu -- the extern "C" boundary (include/farqb.h).
+//
+// Every entry point converts farqb::Error / std::exception into an fqb_status
+// and a thread-local message; no C++ exception crosses the boundary.  There is
+// no host compute path: without a CUDA device every compute call fails with
+// FQB_ERR_CUDA.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "../../include/farqb.h"
+#include "engine.hpp"
+#include "kernels.hpp"
+
+struct fqb_handle_s {
+    farqb::Handle h;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+fqb_status set_error(int status, const std::string& msg) {
+    g_last_error = msg;
+    return static_cast<fqb_status>(status);
+}
+
+template <typename F>
+fqb_status guarded(F&& f) {
+    try {
+        return f();
+    } catch (const farqb::Error& e) {
+        return set_error(e.status, e.what());
+    } catch (const std::bad_alloc&) {
+        return set_error(FQB_ERR_ALLOC, "host allocation failed");
+    } catch (const std::exception& e) {
+        return set_error(FQB_ERR_INVALID_ARGUMENT, e.what());
+    } catch (...) {
+        return set_error(FQB_ERR_INVALID_ARGUMENT, "unknown error");
+    }
+}
+
+void bind(fqb_handle h) {
+    if (!h) throw farqb::Error(FQB_ERR_INVALID_ARGUMENT, "null handle");
+    FQB_CUDA(cudaSetDevice(h->h.device));
+}
+
+}  // namespace
+
+extern "C" {
+
+int fqb_abi_version(void) { return FARQB_ABI_VERSION; }
+
+const char* fqb_last_error(void) { return g_last_error.c_str(); }
+
+const char* fqb_status_name(int status) {
+    switch (status) {
+        case FQB_OK: return "ok";
+        case FQB_ERR_CONFIG: return "config";
+        case FQB_ERR_DIMENSION: return "dimension";
+        case FQB_ERR_BLOCK_DEGENERATE: return "block_degenerate";
+        case FQB_ERR_TOLERANCE_NOT_REACHED: return "tolerance_not_reached";
+        case FQB_ERR_CUDA: return "cuda";
+        case FQB_ERR_NCCL: return "nccl";
+        case FQB_ERR_INVALID_ARGUMENT: return "invalid_argument";
+        case FQB_ERR_CONVERGENCE: return "convergence";
+        case FQB_ERR_CALLBACK: return "callback";
+        case FQB_ERR_ALLOC: return "alloc";
+        default: return "unknown";
+    }
+}
+
+fqb_status fqb_create(int device, fqb_handle* out) {
+    return guarded([&]() -> fqb_status {
+        if (!out) throw farqb::Error(FQB_ERR_INVALID_ARGUMENT, "null output handle");
+        *out = nullptr;
+        int count = 0;
+        const cudaError_t e = cudaGetDeviceCount(&count);
+        if (e != cudaSuccess || count == 0)
+            throw farqb::Error(FQB_ERR_CUDA, "no CUDA device available (libfarqb has no CPU path)");
+        if (device < 0 || device >= count) throw farqb::Error(FQB_ERR_INVALID_ARGUMENT, "bad device ordinal");
+        FQB_CUDA(cudaSetDevice(device));
+        auto* hs = new fqb_handle_s();
+        farqb::Handle& h = hs->h;
+        h.device = device;
+        FQB_CUDA(cudaDeviceGetAttribute(&h.num_sms, cudaDevAttrMultiProcessorCount, device));
+        FQB_CUDA(cudaStreamCreateWithFlags(&h.own_stream, cudaStreamNonBlocking));
+        h.stream = h.own_stream;
+        FQB_CUDA(cudaEventCreate(&h.ev0));
+        FQB_CUDA(cudaEventCreate(&h.ev1));
+        FQB_CUDA(cudaMallocHost(&h.host_status, 64));
+        FQB_CUDA(cudaMallocHost(&h.host_scalars, 64 * sizeof(double)));
+        cudaMemPool_t pool;
+        FQB_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+        uint64_t threshold = UINT64_MAX;
+        FQB_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold));
+        *out = hs;
+        return FQB_OK;
+    });
+}
+
+fqb_status fqb_destroy(fqb_handle h) {
+    return guarded([&]() -> fqb_status {
+        if (!h) return FQB_OK;
+        bind(h);
+        cudaStreamSynchronize(h->h.stream);
+        {
+            farqb::Workspace& w = h->h.ws;
+            w.omega.release(); w.y0.release(); w.ys.release(); w.wp.release(); w.wraw.release();
+            w.g.release(); w.t.release(); w.cd.release(); w.c2.release(); w.small.release();
+            w.zc.release(); w.rowsum_b.release(); w.splitk.release(); w.partial.release();
+            w.scalars.release(); w.scratch.release(); w.a_copy.release(); w.col_ptr.release();
+            w.row_idx.release(); w.counts.release(); w.values.release(); w.status.release();
+        }
+        cudaStreamSynchronize(h->h.stream);
+        cudaFreeHost(h->h.host_status);
+        cudaFreeHost(h->h.host_scalars);
+        cudaEventDestroy(h->h.ev0);
+        cudaEventDestroy(h->h.ev1);
+        cudaStreamDestroy(h->h.own_stream);
+        delete h;
+        return FQB_OK;
+    });
+}
+
+fqb_status fqb_set_stream(fqb_handle h, void* stream) {
+    return guarded([&]() -> fqb_status {
+        bind(h);
+        h->h.stream = stream ? static_cast<cudaStream_t>(stream) : h->h.own_stream;
+        return FQB_OK;
+    });
+}
+
+fqb_status fqb_synchronize(fqb_handle h) {
+    return guarded([&]() -> fqb_status {
+        bind(h);
+        FQB_CUDA(cudaStreamSynchronize(h->h.stream));
+        return FQB_OK;
+    });
+}
+
+int64_t fqb_launch_count(fqb_handle h) { return h ? h->h.lc.total : 0; }
+
+static fqb_status run_common(fqb_handle h, const double* a, int64_t m, int64_t n, int64_t lda,
+                             int a_on_device, bool fixed_precision, int rank, const fqb_config* cfg,
+                             fqb_block_source_fn src, void* user, unsigned flags, fqb_qb_result* out) {
+    if (out) std::memset(out, 0, sizeof *out);
+    return guarded([&]() -> fqb_status {
+        bind(h);
+        if (!cfg || !out) throw farqb::Error(FQB_ERR_INVALID_ARGUMENT, "null config or result");
+        std::string msg;
+        const int st = farqb::run_qb(h->h, a, m, n, lda, a_on_device != 0, fixed_precision, rank, *cfg, src,
+                                     user, flags, out, &msg);
+        out->status = st;
+        if (st != FQB_OK) g_last_error = msg;
+        return static_cast<fqb_status>(st);
+    });
+}
+
+fqb_status fqb_qb_fixed_precision(fqb_handle h, const double* a, int64_t m, int64_t n, int64_t lda,
+                                  int a_on_device, const fqb_config* cfg, fqb_block_source_fn src,
+                                  void* user, unsigned flags, fqb_qb_result* out) {
+    const fqb_status st = run_common(h, a, m, n, lda, a_on_device, true, 0, cfg, src, user, flags, out);
+    if (out) out->status = st;
+    return st;
+}
+
+fqb_status fqb_qb_fixed_rank(fqb_handle h, const double* a, int64_t m, int64_t n, int64_t lda,
+                             int a_on_device, int rank, const fqb_config* cfg, fqb_block_source_fn src,
+                             void* user, unsigned flags, fqb_qb_result* out) {
+    const fqb_status st = run_common(h, a, m, n, lda, a_on_device, false, rank, cfg, src, user, flags, out);
+    if (out) out->status = st;
+    return st;
+}
+
+void fqb_result_free(fqb_qb_result* r) {
+    if (!r) return;
+    if (r->on_device) {
+        if (r->q) cudaFree(r->q);
+        if (r->bt) cudaFree(r->bt);
+    } else {
+        std::free(r->q);
+        std::free(r->bt);
+    }
+    std::free(r->block_residuals);
+    std::free(r->block_ids);
+    r->q = r->bt = nullptr;
+    r->block_residuals = nullptr;
+    r->block_ids = nullptr;
+}
+
+// ---- building blocks ----------------------------------------------------------
+
+fqb_status fqb_philox_u32(fqb_handle h, uint64_t seed, uint32_t block_id, uint32_t column, int count,
+                          uint32_t* host_out) {
+    return guarded([&]() -> fqb_status {
+        bind(h);
+        if (count < 0 || (count > 0 && !host_out)) throw farqb::Error(FQB_ERR_INVALID_ARGUMENT, "bad output");
+        if (count == 0) return FQB_OK;
+        cudaStream_t s = h->h.stream;
+        farqb::DeviceArray<uint32_t> d;
+        d.ensure(size_t(count), s);
+        farqb::launch_philox_u32(seed, block_id, column, count, d.ptr, s, h->h.lc);
+        FQB_CUDA(cudaMemcpyAsync(host_out, d.ptr, sizeof(uint32_t) * count, cudaMemcpyDeviceToHost, s));
+        FQB_CUDA(cudaStreamSynchronize(s));
+        return FQB_OK;
+    });
+}
+
+fqb_status fqb_gen_sketch(fqb_handle h, const fqb_sketch_spec* spec, int n, int l, int block_id,
+                          fqb_sketch_host* out) {
+    if (out) std::memset(out, 0, sizeof *out);
+    return guarded([&]() -> fqb_status {
+        bind(h);
+        if (!spec || !out) throw farqb::Error(FQB_ERR_INVALID_ARGUMENT, "null spec or output");
+        if (n < 1 || l < 1) throw farqb::Error(FQB_ERR_CONFIG, "gen_sketch: dimensions must be positive");
+        const int kind = spec->kind;
+        if (kind < 0 || kind > 4) throw farqb::Error(FQB_ERR_CONFIG, "unknown sketch kind");
+        cudaStream_t s = h->h.stream;
+        farqb::LaunchCounter& lc = h->h.lc;
+        farqb::DeviceArray<unsigned> status;
+        status.ensure(1, s);
+        FQB_CUDA(cudaMemsetAsync(status.ptr, 0, sizeof(unsigned), s));
+        out->rows = n;
+        out->cols = l;
+        out->p = spec->p;
+        if (kind == FQB_GAUSSIAN) {
+            farqb::DeviceArray<double> d;
+            d.ensure(size_t(n) * l, s);
+            farqb::launch_gaussian_dense(spec->seed, block_id, n, l, d.ptr, n, status.ptr, s, lc);
+            out->is_dense = 1;
+            out->dense = static_cast<double*>(std::malloc(sizeof(double) * size_t(n) * l));
+            FQB_CUDA(cudaMemcpyAsync(out->dense, d.ptr, sizeof(double) * size_t(n) * l, cudaMemcpyDeviceToHost, s));
+            FQB_CUDA(cudaStreamSynchronize(s));
+            return FQB_OK;
+        }
+        farqb::DeviceArray<int> cp, ri, counts;
+        farqb::DeviceArray<double> va;
+        cp.ensure(size_t(l) + 1, s);
+        int64_t cap;
+        if (spec->zeta > 0) {
+            if (kind != FQB_SPARSE_SIGN && kind != FQB_SPARSE_GAUSSIAN)
+                throw farqb::Error(FQB_ERR_CONFIG, "zeta applies to the sparse sign / sparse Gaussian kinds only");
+            if (spec->zeta > n || spec->zeta > 256) throw farqb::Error(FQB_ERR_CONFIG, "zeta must not exceed min(n, 256)");
+            cap = int64_t(spec->zeta) * l;
+            ri.ensure(size_t(cap), s);
+            va.ensure(size_t(cap), s);
+            farqb::launch_zeta_fill(kind, spec->seed, block_id, n, l, spec->zeta, 1.0 / std::sqrt(double(spec->zeta)),
+                                    cp.ptr, ri.ptr, va.ptr, status.ptr, s, lc);
+        } else {
+            const double p = spec->p;
+            if (!(p > 0.0 && p < 1.0)) throw farqb::Error(FQB_ERR_CONFIG, "gen_sketch: sparse kinds require p in (0,1)");
+            cap = int64_t(n) * l;
+            ri.ensure(size_t(cap), s);
+            va.ensure(size_t(cap), s);
+            counts.ensure(size_t(l), s);
+            const double denom = std::log1p(-p);
+            const double scale = (kind == FQB_SPARSE_SIGN || kind == FQB_SPARSE_GAUSSIAN) ? 1.0 / std::sqrt(p) : 1.0;
+            farqb::launch_iid_count(kind, spec->seed, block_id, n, l, denom, counts.ptr, s, lc);
+            farqb::launch_exclusive_scan(counts.ptr, l, cp.ptr, s, lc);
+            farqb::launch_iid_fill_csc(kind, spec->seed, block_id, n, l, denom, scale, cp.ptr, ri.ptr, va.ptr,
+                                       status.ptr, s, lc);
+            if (kind == FQB_STD_BERNOULLI) {
+                out->centered = 1;
+                out->std_scale = 1.0 / std::sqrt(p * (1.0 - p));
+            }
+        }
+        out->col_ptr = static_cast<int*>(std::malloc(sizeof(int) * (size_t(l) + 1)));
+        FQB_CUDA(cudaMemcpyAsync(out->col_ptr, cp.ptr, sizeof(int) * (size_t(l) + 1), cudaMemcpyDeviceToHost, s));
+        FQB_CUDA(cudaStreamSynchronize(s));
+        const int64_t nnz = out->col_ptr[l];
+        out->nnz = nnz;
+        out->row_idx = static_cast<int*>(std::malloc(sizeof(int) * size_t(std::max<int64_t>(nnz, 1))));
+        out->values = static_cast<double*>(std::malloc(sizeof(double) * size_t(std::max<int64_t>(nnz, 1))));
+        if (nnz > 0) {
+            FQB_CUDA(cudaMemcpyAsync(out->row_idx, ri.ptr, sizeof(int) * nnz, cudaMemcpyDeviceToHost, s));
+            FQB_CUDA(cudaMemcpyAsync(out->values, va.ptr, sizeof(double) * nnz, cudaMemcpyDeviceToHost, s));
+        }
+        unsigned st = 0;
+        FQB_CUDA(cudaMemcpyAsync(&st, status.ptr, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+        FQB_CUDA(cudaStreamSynchronize(s));
+        if (st & farqb::kGenZeroGaussian)
+            throw farqb::Error(FQB_ERR_CONVERGENCE, "a Gaussian draw hit an exact zero");
+        return FQB_OK;
+    });
+}
+
+void fqb_sketch_free(fqb_sketch_host* s) {
+    if (!s) return;
+    std::free(s->dense);
+    std::free(s->col_ptr);
+    std::free(s->row_idx);
+    std::free(s->values);
+    std::memset(s, 0, sizeof *s);
+}
+
+fqb_status fqb_sparse_dense_mul(fqb_handle h, const double* a, int64_t m, int64_t n, int64_t lda,
+                                const int* col_ptr, const int* row_idx, const double* values, int l,
+                                const double* z, double* c, int64_t ldc) {
+    return guarded([&]() -> fqb_status {
+        bind(h);
+        (void)n;
+        if (!a || !col_ptr || !c) throw farqb::Error(FQB_ERR_INVALID_ARGUMENT, "null pointer");
+        if (lda < m || ldc < m) throw farqb::Error(FQB_ERR_DIMENSION, "leading dimension too small");
+        farqb::launch_gather_spmm(a, m, lda, col_ptr, row_idx, values, l, z, c, ldc, h->h.stream, h->h.lc);
+        return FQB_OK;
+    });
+}
+
+fqb_status fqb_centering_column(fqb_handle h, const double* a, int64_t m, int64_t n, int64_t lda, double p,
+                                double* z) {
+    return guarded([&]() -> fqb_status {
+        bind(h);
+        if (!a || !z) throw farqb::Error(FQB_ERR_INVALID_ARGUMENT, "null pointer");
+        farqb::launch_centering(a, m, n, lda, p, z, h->h.stream, h->h.lc);
+        return FQB_OK;
+    });
+}
+
+fqb_status fqb_frob_norm_sq(fqb_handle h, const double* a, int64_t m, int64_t n, int64_t lda,
+                            double* host_out) {
+    return guarded([&]() -> fqb_status {
+        bind(h);
+        if (!a || !host_out) throw farqb::Error(FQB_ERR_INVALID_ARGUMENT, "null pointer");
+        cudaStream_t s = h->h.stream;
+        farqb::DeviceArray<double> part;
+        part.ensure(farqb::kReducePartials + 1, s);
+        farqb::launch_sumsq(a, m, n, lda, part.ptr, part.ptr + farqb::kReducePartials, s, h->h.lc);
+        FQB_CUDA(cudaMemcpyAsync(host_out, part.ptr + farqb::kReducePartials, sizeof(double),
+                                 cudaMemcpyDeviceToHost, s));
+        FQB_CUDA(cudaStreamSynchronize(s));
+        return FQB_OK;
+    });
+}
+
+fqb_status fqb_gemm(fqb_handle h, int trans_a, int64_t m, int64_t n, int64_t k, double alpha,
+                    const double* a, int64_t lda, const double* b, int64_t ldb, double beta, double* c,
+                    int64_t ldc) {
+    return guarded([&]() -> fqb_status {
+        bind(h);
+        if (m < 0 || n < 0 || k < 0) throw farqb::Error(FQB_ERR_DIMENSION, "negative dimension");
+        if (ldc < m || ldb < k || lda < (trans_a ? k : m)) throw farqb::Error(FQB_ERR_DIMENSION, "leading dimension too small");
+        cudaStream_t s = h->h.stream;
+        const int64_t wd = int64_t(h->h.num_sms) * 256 * 128 + 16;
+        h->h.ws.splitk.ensure(size_t(wd), s);
+        farqb::gemm(trans_a != 0, m, n, k, alpha, a, lda, b, ldb, beta, c, ldc, h->h.ws.splitk.ptr, wd,
+                    h->h.num_sms, s, h->h.lc);
+        return FQB_OK;
+    });
+}
+
+double fqb_default_density(int kind, int64_t n) { return farqb::default_density(kind, n); }
+int fqb_default_block(int64_t m, int64_t n) { return farqb::default_block(m, n); }
+int fqb_default_max_iters(int64_t n, int b) { return farqb::default_max_iters(n, b); }
+
+}  // extern "C"

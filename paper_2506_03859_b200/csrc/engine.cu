@@ -1,0 +1,586 @@
+// engine.cu -- the farPCA blocked adaptive QB loop, device resident.
+//
+// Host-side orchestration of the reference's run_fixed_precision /
+// run_fixed_rank (/root/reference/proj/src/driver.cpp:134-160, 185-294,
+// 347-413).  All matrix work runs in the sm_100a kernels of this directory on
+// one CUDA stream; the host only makes the per-block decisions (converged?
+// degenerate -> redraw?) from a handful of scalars read back once per block.
+//
+// Numerical recipe (explicit Q instead of the reference's Gram-space Y/W/Z/L):
+//   sketch     Y_j = A * Omega_j           (gather SpMM or DMMA GEMM)
+//   power      W = A' Y - B'(B Omega) [- alpha G],  G = orth(W)   (P passes)
+//   accept     Y_j = A G;  W_j = A' Y_j
+//              [C1; D] = [Q | Y_j]' Y_j            one TN GEMM
+//              Y' = Y_j - Q C1;  R1 = chol(Y''Y')  pivot rule of driver.cpp:265-279
+//              Q1 = Y' R1^-1;   C2 = Q' Q1;  Q2 = Q1 - Q C2;  R2 = chol(Q2'Q2)
+//              Q_j = Q2 R2^-1,  R = R2 R1,  C = C1 + C2 R1       (CholeskyQR2 + BGS2)
+//              B_j' = (W_j - B' C) R^-1                          (no extra pass over A)
+//              E  -= ||B_j||_F^2                                 (driver.cpp:280-286)
+// Y_j = Q C + Q_j R and W_j = A'Y_j give the B_j identity; the reference's
+// r = (w_j - W Z^-1 Y'y_j) L22^-T is the same quantity in Gram form.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "engine.hpp"
+#include "kernels.hpp"
+
+namespace farqb {
+
+namespace {
+
+constexpr unsigned kStAcceptPivot = 1u << 4;
+constexpr unsigned kStAcceptChol2 = 1u << 5;
+constexpr unsigned kStPowerChol = 1u << 6;
+constexpr unsigned kStPowerDegenerate = 1u << 7;
+constexpr unsigned kStEigConv = 1u << 8;
+constexpr double kDenseThreshold = 1.0 / 32.0;  // density above which Omega is densified
+
+enum ScalarSlot { kNormA = 0, kBNorm = 1, kDMax = 2, kAlpha = 3, kScalarCount = 8 };
+
+}  // namespace
+
+double default_density(int kind, int64_t n) {
+    if (kind == kGaussian) return 0.0;
+    const double nn = double(n);
+    return std::max(1e-3, kind == kStdBernoulli ? std::log(nn) / nn : 10.0 / nn);
+}
+
+int default_block(int64_t m, int64_t n) {
+    const int64_t mn = std::min(m, n);
+    return int(std::min<int64_t>(std::min<int64_t>(std::max<int64_t>(20, mn / 100), 50), mn));
+}
+
+int default_max_iters(int64_t n, int b) { return int((n + 2 * int64_t(b) - 1) / (2 * int64_t(b))); }
+
+fqb_config resolve_config(int64_t m, int64_t n, const fqb_config& in, bool fixed_precision) {
+    if (m < 1 || n < 1) throw Error(kStatusConfig, "matrix must be non-empty");
+    if (m > INT32_MAX || n > INT32_MAX) throw Error(kStatusDimension, "dimensions exceed 2^31-1");
+    fqb_config cfg = in;
+    if (cfg.sketch.kind < kGaussian || cfg.sketch.kind > kSparseGaussian)
+        throw Error(kStatusConfig, "unknown sketch kind");
+    if (cfg.block == 0) cfg.block = default_block(m, n);
+    if (cfg.block < 1) throw Error(kStatusConfig, "block size must be at least 1");
+    if (cfg.block > std::min(m, n)) throw Error(kStatusConfig, "block size exceeds matrix dimensions");
+    if (cfg.block > 1024) throw Error(kStatusConfig, "block size above 1024 is not supported");
+    if (cfg.max_iters == 0) cfg.max_iters = default_max_iters(n, cfg.block);
+    if (cfg.max_iters < 1) throw Error(kStatusConfig, "max_iters must be at least 1");
+    if (cfg.power < 0) throw Error(kStatusConfig, "power must be non-negative");
+    if (cfg.power >= 3 && cfg.block > 128)
+        throw Error(kStatusConfig, "shifted power iteration (power >= 3) supports block size <= 128");
+    if (cfg.sketch.zeta < 0) throw Error(kStatusConfig, "zeta must be non-negative");
+    if (cfg.sketch.zeta > 0) {
+        if (cfg.sketch.kind != kSparseSign && cfg.sketch.kind != kSparseGaussian)
+            throw Error(kStatusConfig, "zeta applies to the sparse sign / sparse Gaussian kinds only");
+        if (cfg.sketch.zeta > n || cfg.sketch.zeta > 256)
+            throw Error(kStatusConfig, "zeta must not exceed min(n, 256)");
+        if (cfg.sketch.p == 0.0) cfg.sketch.p = double(cfg.sketch.zeta) / double(n);
+    } else if (cfg.sketch.kind != kGaussian && cfg.sketch.p == 0.0) {
+        cfg.sketch.p = default_density(cfg.sketch.kind, n);
+    }
+    if (fixed_precision && !(cfg.eps > 0.0))
+        throw Error(kStatusConfig, "fixed-precision mode needs a positive tolerance");
+    cfg.shift_convention = cfg.shift_convention ? 1 : 0;
+    return cfg;
+}
+
+namespace {
+
+class QbRun {
+  public:
+    QbRun(Handle& h, const double* a, int64_t m, int64_t n, int64_t lda, const fqb_config& cfg,
+          fqb_block_source_fn src, void* user)
+        : h_(h), s_(h.stream), a_(a), m_(m), n_(n), lda_(lda), cfg_(cfg), b_(cfg.block), src_(src),
+          user_(user) {
+        ldq_ = round_up(m_, 8);
+        ldbt_ = round_up(n_, 8);
+        ldo_ = round_up(n_, 8);
+        Workspace& w = h_.ws;
+        const int64_t b = b_;
+        w.omega.ensure(size_t(ldo_) * b, s_);
+        w.y0.ensure(size_t(ldq_) * b, s_);
+        w.ys.ensure(size_t(ldq_) * b, s_);
+        w.wp.ensure(size_t(ldbt_) * b, s_);
+        w.wraw.ensure(size_t(ldbt_) * b, s_);
+        w.g.ensure(size_t(ldbt_) * b, s_);
+        w.small.ensure(size_t(12) * b * b + 4 * b, s_);
+        w.scalars.ensure(kScalarCount, s_);
+        w.partial.ensure(kReducePartials, s_);
+        w.status.ensure(4, s_);
+        w.scratch.ensure(size_t(b) * (b + 1), s_);
+        w.col_ptr.ensure(size_t(b) + 1, s_);
+        w.counts.ensure(size_t(b), s_);
+        splitk_doubles_ = int64_t(h_.num_sms) * 256 * 128 + 16;
+        w.splitk.ensure(size_t(splitk_doubles_), s_);
+        double* sm = w.small.ptr;
+        S_ = sm;
+        S2_ = sm + 1 * b * b;
+        R1_ = sm + 2 * b * b;
+        R1i_ = sm + 3 * b * b;
+        R2_ = sm + 4 * b * b;
+        R2i_ = sm + 5 * b * b;
+        R_ = sm + 6 * b * b;
+        Ri_ = sm + 7 * b * b;
+        V_ = sm + 8 * b * b;
+        VS_ = sm + 9 * b * b;
+        VT_ = sm + 10 * b * b;
+        eig_ = sm + 12 * b * b;
+        sig_ = eig_ + b;
+        scal_ = w.scalars.ptr;
+        status_ = w.status.ptr;
+    }
+
+    // --- setup: ||A||^2 and (StdBernoulli) the centering column -----------------
+    void setup() {
+        FQB_CUDA(cudaMemsetAsync(scal_, 0, kScalarCount * sizeof(double), s_));
+        launch_sumsq(a_, m_, n_, lda_, h_.ws.partial.ptr, scal_ + kNormA, s_, h_.lc);
+        if (cfg_.sketch.kind == kStdBernoulli) {
+            h_.ws.zc.ensure(size_t(m_), s_);
+            launch_centering(a_, m_, n_, lda_, cfg_.sketch.p, h_.ws.zc.ptr, s_, h_.lc);
+            have_z_ = true;
+            need_rowsum_ = true;
+        }
+        FQB_CUDA(cudaMemcpyAsync(h_.host_scalars, scal_ + kNormA, sizeof(double), cudaMemcpyDeviceToHost, s_));
+        FQB_CUDA(cudaStreamSynchronize(s_));
+        norm_a_sq_ = h_.host_scalars[0];
+    }
+
+    double norm_a_sq() const { return norm_a_sq_; }
+    double residual() const { return norm_a_sq_ - trace_; }
+    int blocks() const { return blocks_; }
+    int rank() const { return int(l_); }
+    std::vector<double>& residuals() { return residuals_; }
+    std::vector<int>& ids() { return ids_; }
+
+    void reserve_blocks(int nblocks) { grow(int64_t(nblocks) * b_); }
+
+    // process_block (driver.cpp:134-160): up to 3 redraws with id + 1000 r
+    void process_block(int index) {
+        for (int attempt = 0;; ++attempt) {
+            const int id = index + 1000 * attempt;
+            ids_.push_back(id);
+            const unsigned st = try_block(id);
+            if (st == 0) return;
+            if (attempt >= 3)
+                throw DegenerateError(std::string("block degenerate after 3 redraws (status ") +
+                                      std::to_string(st) + ")");
+        }
+    }
+
+    struct DegenerateError : Error {
+        explicit DegenerateError(const std::string& m) : Error(kStatusDegenerate, m) {}
+    };
+
+    // Final outputs
+    DeviceArray<double>& q() { return q_; }
+    DeviceArray<double>& bt() { return bt_; }
+    int64_t ldq() const { return ldq_; }
+    int64_t ldbt() const { return ldbt_; }
+
+  private:
+    // ---- buffers ------------------------------------------------------------
+    void grow(int64_t need_cols) {
+        if (need_cols <= cap_) return;
+        int64_t nc = std::max<int64_t>(need_cols, cap_ ? 2 * cap_ : int64_t(b_) * 4);
+        nc = std::min<int64_t>(std::max(nc, need_cols), std::max<int64_t>(need_cols, int64_t(cfg_.max_iters) * b_));
+        auto regrow = [&](DeviceArray<double>& arr, int64_t ld) {
+            DeviceArray<double> fresh;
+            fresh.ensure(size_t(ld) * nc, s_);
+            if (l_ > 0) FQB_CUDA(cudaMemcpyAsync(fresh.ptr, arr.ptr, size_t(ld) * l_ * sizeof(double),
+                                                 cudaMemcpyDeviceToDevice, s_));
+            arr.release();
+            arr.ptr = fresh.detach();
+            arr.count = size_t(ld) * nc;
+            arr.stream = s_;
+        };
+        regrow(q_, ldq_);
+        regrow(bt_, ldbt_);
+        if (need_rowsum_) regrow(rowsum_, 1);
+        cap_ = nc;
+        Workspace& w = h_.ws;
+        w.t.ensure(size_t(nc) * b_, s_);
+        w.cd.ensure(size_t(nc + b_) * b_, s_);
+        w.c2.ensure(size_t(nc) * b_, s_);
+    }
+
+    void gemm_(bool ta, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
+               const double* B, int64_t ldb, double beta, double* C, int64_t ldc) {
+        gemm(ta, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, h_.ws.splitk.ptr, splitk_doubles_,
+             h_.num_sms, s_, h_.lc);
+    }
+
+    // ---- Omega ----------------------------------------------------------------
+    void make_block(int id) {
+        Workspace& w = h_.ws;
+        const int b = b_;
+        om_centered_ = false;
+        om_shift_folded_ = false;
+        om_p_ = cfg_.sketch.p;
+        if (src_) {
+            fqb_block blk;
+            std::memset(&blk, 0, sizeof blk);
+            if (src_(user_, int(n_), b, id, &blk) != 0)
+                throw Error(kStatusCallback, "block source returned an error for block " + std::to_string(id));
+            if (blk.rows != n_ || blk.cols != b)
+                throw Error(kStatusDimension, "block source returned a block of the wrong shape");
+            om_centered_ = blk.centered != 0;
+            om_p_ = blk.p;
+            if (blk.is_dense) {
+                if (!blk.dense) throw Error(kStatusInvalid, "dense block without data");
+                FQB_CUDA(cudaMemcpy2DAsync(w.omega.ptr, ldo_ * sizeof(double), blk.dense, n_ * sizeof(double),
+                                           n_ * sizeof(double), b, cudaMemcpyHostToDevice, s_));
+                om_dense_ = true;
+                return;
+            }
+            if (!blk.col_ptr || (blk.nnz > 0 && (!blk.row_idx || !blk.values)))
+                throw Error(kStatusInvalid, "sparse block without arrays");
+            const int64_t nnz = blk.col_ptr[b];
+            w.row_idx.ensure(size_t(std::max<int64_t>(nnz, 1)), s_);
+            w.values.ensure(size_t(std::max<int64_t>(nnz, 1)), s_);
+            FQB_CUDA(cudaMemcpyAsync(w.col_ptr.ptr, blk.col_ptr, (b + 1) * sizeof(int), cudaMemcpyHostToDevice, s_));
+            if (nnz > 0) {
+                FQB_CUDA(cudaMemcpyAsync(w.row_idx.ptr, blk.row_idx, nnz * sizeof(int), cudaMemcpyHostToDevice, s_));
+                FQB_CUDA(cudaMemcpyAsync(w.values.ptr, blk.values, nnz * sizeof(double), cudaMemcpyHostToDevice, s_));
+            }
+            FQB_CUDA(cudaStreamSynchronize(s_));  // host arrays may change after the callback returns
+            finish_sparse(double(nnz) / (double(n_) * b));
+            return;
+        }
+        const int kind = cfg_.sketch.kind;
+        const uint64_t seed = cfg_.sketch.seed;
+        if (kind == kGaussian) {
+            launch_gaussian_dense(seed, id, n_, b, w.omega.ptr, ldo_, status_, s_, h_.lc);
+            om_dense_ = true;
+            return;
+        }
+        om_centered_ = kind == kStdBernoulli;
+        if (cfg_.sketch.zeta > 0) {
+            const int zeta = cfg_.sketch.zeta;
+            const int64_t nnz = int64_t(zeta) * b;
+            w.row_idx.ensure(size_t(nnz), s_);
+            w.values.ensure(size_t(nnz), s_);
+            launch_zeta_fill(kind, seed, id, n_, b, zeta, 1.0 / std::sqrt(double(zeta)), w.col_ptr.ptr,
+                             w.row_idx.ptr, w.values.ptr, status_, s_, h_.lc);
+            finish_sparse(double(zeta) / double(n_));
+            return;
+        }
+        const double p = cfg_.sketch.p;
+        const double denom = std::log1p(-p);  // host libm, like sketch.cpp:38
+        const double scale = (kind == kSparseSign || kind == kSparseGaussian) ? 1.0 / std::sqrt(p) : 1.0;
+        if (p > kDenseThreshold) {
+            // densified directly by the walk, centering folded in: Omega_c = S - p
+            launch_iid_fill_dense(kind, seed, id, n_, b, denom, scale, om_centered_ ? p : 0.0, w.omega.ptr,
+                                  ldo_, status_, s_, h_.lc);
+            om_dense_ = true;
+            om_shift_folded_ = true;
+            return;
+        }
+        const int64_t cap = n_ * int64_t(b);  // every row may be a nonzero
+        w.row_idx.ensure(size_t(cap), s_);
+        w.values.ensure(size_t(cap), s_);
+        launch_iid_count(kind, seed, id, n_, b, denom, w.counts.ptr, s_, h_.lc);
+        launch_exclusive_scan(w.counts.ptr, b, w.col_ptr.ptr, s_, h_.lc);
+        launch_iid_fill_csc(kind, seed, id, n_, b, denom, scale, w.col_ptr.ptr, w.row_idx.ptr, w.values.ptr,
+                            status_, s_, h_.lc);
+        om_dense_ = false;
+    }
+
+    void finish_sparse(double density) {
+        Workspace& w = h_.ws;
+        if (density > kDenseThreshold) {
+            launch_densify(w.col_ptr.ptr, w.row_idx.ptr, w.values.ptr, n_, b_, om_centered_ ? om_p_ : 0.0,
+                           w.omega.ptr, ldo_, s_, h_.lc);
+            om_dense_ = true;
+            om_shift_folded_ = true;
+        } else {
+            om_dense_ = false;
+            if (om_centered_ && !have_z_)
+                throw Error(kStatusDimension, "centered_product: stale centering column");
+        }
+    }
+
+    // Y (m x b, ldy) = A * Omega  [centered]   (apply_block, driver.cpp:21-26)
+    void apply_omega(double* y, int64_t ldy) {
+        Workspace& w = h_.ws;
+        if (om_dense_) {
+            gemm_(false, m_, b_, n_, 1.0, a_, lda_, w.omega.ptr, ldo_, 0.0, y, ldy);
+        } else {
+            launch_gather_spmm(a_, m_, lda_, w.col_ptr.ptr, w.row_idx.ptr, w.values.ptr, b_,
+                               om_centered_ ? w.zc.ptr : nullptr, y, ldy, s_, h_.lc);
+        }
+    }
+
+    // T (l x b) = B * Omega_c  (tmul_block, driver.cpp:30-45, with W Z^-1 W' = B'B)
+    void tmul_omega(double* t, int64_t ldt) {
+        Workspace& w = h_.ws;
+        if (om_dense_) {
+            gemm_(true, l_, b_, n_, 1.0, bt_.ptr, ldbt_, w.omega.ptr, ldo_, 0.0, t, ldt);
+            if (om_centered_ && !om_shift_folded_) {
+                // a dense block flagged centered: subtract p * rowsum(B) like the reference
+                throw Error(kStatusConfig, "dense centered blocks are not supported");
+            }
+        } else {
+            launch_gather_tmul(bt_.ptr, n_, ldbt_, int(l_), w.col_ptr.ptr, w.row_idx.ptr, w.values.ptr, b_,
+                               om_centered_ ? rowsum_.ptr : nullptr, om_p_, t, ldt, s_, h_.lc);
+        }
+    }
+
+    // ---- orth(W) -> G (n x b) ---------------------------------------------------
+    void orth_power(const double* wsrc, double* gdst, bool eig_mode, bool need_sigma) {
+        const int b = b_;
+        gemm_(true, b, b, n_, 1.0, wsrc, ldbt_, wsrc, ldbt_, 0.0, S_, b);
+        if (need_sigma || eig_mode) {
+            launch_sym_eig(S_, b, b, eig_, eig_mode ? V_ : nullptr, VT_, status_, kStEigConv, s_, h_.lc);
+        }
+        if (eig_mode) {
+            // eig_svd (matrix_core.cpp:193-215): G = W V Sigma^-1
+            launch_eigsvd_scale(eig_, V_, b, VS_, sig_, status_, kStPowerDegenerate, s_, h_.lc);
+            gemm_(false, n_, b, b, 1.0, wsrc, ldbt_, VS_, b, 0.0, gdst, ldbt_);
+        } else {
+            // one CholeskyQR pass: same span, orthonormal to the same u*cond^2 as eigSVD
+            launch_chol_upper_inv(S_, b, b, 0.0, 0.0, nullptr, 0, R1_, R1i_, nullptr, h_.ws.scratch.ptr,
+                                  status_, kStPowerChol, s_, h_.lc);
+            gemm_(false, n_, b, b, 1.0, wsrc, ldbt_, R1i_, b, 0.0, gdst, ldbt_);
+        }
+    }
+
+    // power_iterate_block (driver.cpp:185-228); leaves the iterate in ws.g
+    void power_iterate(bool eig_mode) {
+        Workspace& w = h_.ws;
+        const int P = cfg_.power;
+        FQB_CUDA(cudaMemsetAsync(scal_ + kAlpha, 0, sizeof(double), s_));
+        for (int k = 1; k <= P; ++k) {
+            if (k == 1) apply_omega(w.y0.ptr, ldq_);
+            else gemm_(false, m_, b_, n_, 1.0, a_, lda_, w.g.ptr, ldbt_, 0.0, w.y0.ptr, ldq_);
+            gemm_(true, n_, b_, m_, 1.0, a_, lda_, w.y0.ptr, ldq_, 0.0, w.wp.ptr, ldbt_);
+            if (l_ > 0) {
+                if (k == 1) tmul_omega(w.t.ptr, l_);
+                else gemm_(true, l_, b_, n_, 1.0, bt_.ptr, ldbt_, w.g.ptr, ldbt_, 0.0, w.t.ptr, l_);
+                gemm_(false, n_, b_, l_, -1.0, bt_.ptr, ldbt_, w.t.ptr, l_, 1.0, w.wp.ptr, ldbt_);
+            }
+            if (k > 1 && P >= 3)
+                launch_axpy_cols_dev(scal_ + kAlpha, w.g.ptr, ldbt_, w.wp.ptr, ldbt_, n_, b_, s_, h_.lc);
+            const bool need_sigma = k > 1 && k < P;  // the shift only matters for a later pass
+            orth_power(w.wp.ptr, w.g.ptr, eig_mode, need_sigma);
+            if (need_sigma) launch_shift_update(eig_, b_, cfg_.shift_convention, scal_ + kAlpha, s_, h_.lc);
+        }
+    }
+
+    // accept_block (driver.cpp:230-294), explicit-Q form
+    void accept(bool from_iterate) {
+        Workspace& w = h_.ws;
+        const int b = b_;
+        const int64_t l = l_;
+        double* yj = q_.ptr + l * ldq_;
+        double* btj = bt_.ptr + l * ldbt_;
+        if (from_iterate) gemm_(false, m_, b, n_, 1.0, a_, lda_, w.g.ptr, ldbt_, 0.0, yj, ldq_);
+        else apply_omega(yj, ldq_);
+        gemm_(true, n_, b, m_, 1.0, a_, lda_, yj, ldq_, 0.0, w.wraw.ptr, ldbt_);
+        const int64_t ldcd = l + b;
+        double* cd = w.cd.ptr;
+        // [C1; D] = [Q_old | Y_j]' Y_j
+        gemm_(true, l + b, b, m_, 1.0, q_.ptr, ldq_, yj, ldq_, 0.0, cd, ldcd);
+        double* dblk = cd + l;  // rows l..l+b-1, ld = l+b
+        if (l == 0) {
+            launch_chol_upper_inv(dblk, b, ldcd, 1e-12, 0.0, dblk, ldcd, R1_, R1i_, scal_ + kDMax,
+                                  w.scratch.ptr, status_, kStAcceptPivot, s_, h_.lc);
+            gemm_(false, m_, b, b, 1.0, yj, ldq_, R1i_, b, 0.0, w.ys.ptr, ldq_);
+        } else {
+            gemm_(false, m_, b, l, -1.0, q_.ptr, ldq_, cd, ldcd, 1.0, yj, ldq_);
+            gemm_(true, b, b, m_, 1.0, yj, ldq_, yj, ldq_, 0.0, S_, b);
+            launch_chol_upper_inv(S_, b, b, 1e-12, diag_max_, dblk, ldcd, R1_, R1i_, scal_ + kDMax,
+                                  w.scratch.ptr, status_, kStAcceptPivot, s_, h_.lc);
+            gemm_(false, m_, b, b, 1.0, yj, ldq_, R1i_, b, 0.0, w.ys.ptr, ldq_);
+            gemm_(true, l, b, m_, 1.0, q_.ptr, ldq_, w.ys.ptr, ldq_, 0.0, w.c2.ptr, l);
+            gemm_(false, m_, b, l, -1.0, q_.ptr, ldq_, w.c2.ptr, l, 1.0, w.ys.ptr, ldq_);
+        }
+        gemm_(true, b, b, m_, 1.0, w.ys.ptr, ldq_, w.ys.ptr, ldq_, 0.0, S2_, b);
+        launch_chol_upper_inv(S2_, b, b, 0.0, 0.0, nullptr, 0, R2_, R2i_, nullptr, w.scratch.ptr, status_,
+                              kStAcceptChol2, s_, h_.lc);
+        gemm_(false, m_, b, b, 1.0, w.ys.ptr, ldq_, R2i_, b, 0.0, yj, ldq_);  // Q_j
+        gemm_(false, b, b, b, 1.0, R1i_, b, R2i_, b, 0.0, Ri_, b);              // R^-1 = R1^-1 R2^-1
+        if (l > 0) {
+            gemm_(false, l, b, b, 1.0, w.c2.ptr, l, R1_, b, 1.0, cd, ldcd);     // C = C1 + C2 R1
+            gemm_(false, n_, b, l, -1.0, bt_.ptr, ldbt_, cd, ldcd, 1.0, w.wraw.ptr, ldbt_);
+        }
+        gemm_(false, n_, b, b, 1.0, w.wraw.ptr, ldbt_, Ri_, b, 0.0, btj, ldbt_);  // B_j'
+        launch_sumsq(btj, n_, b, ldbt_, w.partial.ptr, scal_ + kBNorm, s_, h_.lc);
+        if (need_rowsum_) launch_colsum(btj, n_, b, ldbt_, rowsum_.ptr + l, s_, h_.lc);
+    }
+
+    // One attempt; returns 0 when accepted, the degenerate status bits otherwise.
+    unsigned try_block(int id) {
+        grow(l_ + b_);
+        bool eig_mode = false;
+        for (int pass = 0; pass < 2; ++pass) {
+            FQB_CUDA(cudaMemsetAsync(status_, 0, sizeof(unsigned), s_));
+            make_block(id);
+            if (cfg_.power >= 1) power_iterate(eig_mode);
+            accept(cfg_.power >= 1);
+            FQB_CUDA(cudaMemcpyAsync(h_.host_status, status_, sizeof(unsigned), cudaMemcpyDeviceToHost, s_));
+            FQB_CUDA(cudaMemcpyAsync(h_.host_scalars, scal_, 4 * sizeof(double), cudaMemcpyDeviceToHost, s_));
+            FQB_CUDA(cudaStreamSynchronize(s_));
+            const unsigned st = *h_.host_status;
+            if (st & kGenZeroGaussian)
+                throw Error(kStatusConvergence, "a Gaussian draw hit an exact zero (reference would redraw)");
+            if (st & kStEigConv) throw Error(kStatusConvergence, "sym_eig: jacobi sweeps exhausted");
+            if ((st & kStPowerChol) && !eig_mode) {
+                eig_mode = true;  // CholeskyQR broke down: redo with eigSVD like the reference
+                continue;
+            }
+            if (st & (kStPowerDegenerate | kStAcceptPivot | kStAcceptChol2 | kStPowerChol)) return st;
+            // commit
+            trace_ += h_.host_scalars[kBNorm];
+            diag_max_ = h_.host_scalars[kDMax];
+            l_ += b_;
+            ++blocks_;
+            residuals_.push_back(residual());
+            return 0;
+        }
+        return kStPowerDegenerate;
+    }
+
+    Handle& h_;
+    cudaStream_t s_;
+    const double* a_;
+    int64_t m_, n_, lda_;
+    fqb_config cfg_;
+    int b_;
+    fqb_block_source_fn src_;
+    void* user_;
+    int64_t ldq_, ldbt_, ldo_;
+    int64_t splitk_doubles_ = 0;
+    int64_t cap_ = 0, l_ = 0;
+    int blocks_ = 0;
+    double norm_a_sq_ = 0.0, trace_ = 0.0, diag_max_ = 0.0;
+    bool have_z_ = false, need_rowsum_ = false;
+    bool om_dense_ = true, om_centered_ = false, om_shift_folded_ = false;
+    double om_p_ = 0.0;
+    DeviceArray<double> q_, bt_, rowsum_;
+    std::vector<double> residuals_;
+    std::vector<int> ids_;
+    double *S_, *S2_, *R1_, *R1i_, *R2_, *R2i_, *R_, *Ri_, *V_, *VS_, *VT_, *eig_, *sig_, *scal_;
+    unsigned* status_;
+};
+
+}  // namespace
+
+int run_qb(Handle& h, const double* a, int64_t m, int64_t n, int64_t lda, bool a_on_device,
+           bool fixed_precision, int rank, const fqb_config& cfg_in, fqb_block_source_fn src, void* user,
+           unsigned flags, fqb_qb_result* out, std::string* message_out) {
+    std::memset(out, 0, sizeof *out);
+    out->m = m;
+    out->n = n;
+    if (!a) throw Error(kStatusInvalid, "null matrix pointer");
+    if (lda < m) throw Error(kStatusDimension, "lda < m");
+    fqb_config cfg = resolve_config(m, n, cfg_in, fixed_precision);
+    if (!fixed_precision) {
+        if (rank < 1) throw Error(kStatusConfig, "rank must be at least 1");
+        if (rank > std::min(m, n)) throw Error(kStatusConfig, "rank exceeds matrix dimensions");
+    }
+    if (!src && cfg.sketch.kind != kGaussian && cfg.sketch.zeta == 0 && !(cfg.sketch.p > 0.0 && cfg.sketch.p < 1.0))
+        throw Error(kStatusConfig, "gen_sketch: sparse kinds require p in (0,1)");
+    out->resolved_block = cfg.block;
+    out->resolved_max_iters = cfg.max_iters;
+    out->resolved_p = cfg.sketch.p;
+    const int64_t launches0 = h.lc.total;
+    cudaStream_t s = h.stream;
+    FQB_CUDA(cudaEventRecord(h.ev0, s));
+
+    // A on the device with an even, 16-byte aligned leading dimension
+    const double* ad = a;
+    int64_t ldad = lda;
+    const bool usable = a_on_device && lda % 2 == 0 && reinterpret_cast<uintptr_t>(a) % 16 == 0;
+    if (!usable) {
+        ldad = round_up(m, 8);
+        h.ws.a_copy.ensure(size_t(ldad) * n, s);
+        FQB_CUDA(cudaMemcpy2DAsync(h.ws.a_copy.ptr, ldad * sizeof(double), a, lda * sizeof(double),
+                                   m * sizeof(double), n,
+                                   a_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+        ad = h.ws.a_copy.ptr;
+    }
+
+    QbRun run(h, ad, m, n, ldad, cfg, src, user);
+    run.setup();
+    int status = 0;
+    bool converged = false;
+    std::string message;
+    try {
+        if (fixed_precision) {
+            const double norm_a = std::sqrt(run.norm_a_sq());
+            const double eps_abs = cfg.relative ? cfg.eps * norm_a : cfg.eps;
+            const double eps_sq = eps_abs * eps_abs;
+            if (run.residual() <= eps_sq) {
+                converged = true;
+            } else {
+                for (int j = 0; j < cfg.max_iters; ++j) {
+                    run.process_block(j);
+                    if (run.residual() < eps_sq) {
+                        converged = true;
+                        break;
+                    }
+                }
+            }
+            if (!converged) {
+                status = kStatusTolerance;
+                message = "tolerance not reached after " + std::to_string(run.blocks()) + " blocks";
+            }
+        } else {
+            const int nblocks = (rank + cfg.block - 1) / cfg.block;
+            run.reserve_blocks(nblocks);
+            for (int j = 0; j < nblocks; ++j) run.process_block(j);
+            converged = true;
+        }
+    } catch (const Error& e) {
+        if (e.status != kStatusDegenerate) throw;
+        status = kStatusDegenerate;
+        message = e.what();
+    }
+    FQB_CUDA(cudaEventRecord(h.ev1, s));
+
+    out->status = status;
+    out->rank = run.rank();
+    out->blocks = run.blocks();
+    out->converged = converged ? 1 : 0;
+    out->residual_sq = run.residual();
+    out->norm_a_sq = run.norm_a_sq();
+    out->ldq = run.ldq();
+    out->ldbt = run.ldbt();
+    const int l = run.rank();
+    if (l > 0 && (flags & FQB_OUT_DEVICE)) {
+        out->q = run.q().detach();
+        out->bt = run.bt().detach();
+        out->on_device = 1;
+    } else if (l > 0 && (flags & FQB_OUT_HOST)) {
+        out->q = static_cast<double*>(std::malloc(sizeof(double) * size_t(m) * l));
+        out->bt = static_cast<double*>(std::malloc(sizeof(double) * size_t(n) * l));
+        if (!out->q || !out->bt) throw Error(kStatusAlloc, "host result allocation failed");
+        FQB_CUDA(cudaMemcpy2DAsync(out->q, m * sizeof(double), run.q().ptr, run.ldq() * sizeof(double),
+                                   m * sizeof(double), l, cudaMemcpyDeviceToHost, s));
+        FQB_CUDA(cudaMemcpy2DAsync(out->bt, n * sizeof(double), run.bt().ptr, run.ldbt() * sizeof(double),
+                                   n * sizeof(double), l, cudaMemcpyDeviceToHost, s));
+        out->ldq = m;
+        out->ldbt = n;
+        out->on_device = 0;
+    }
+    FQB_CUDA(cudaStreamSynchronize(s));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, h.ev0, h.ev1);
+    out->elapsed_ms = ms;
+    const auto& res = run.residuals();
+    out->block_residuals = static_cast<double*>(std::malloc(sizeof(double) * std::max<size_t>(res.size(), 1)));
+    if (!res.empty()) std::memcpy(out->block_residuals, res.data(), sizeof(double) * res.size());
+    const auto& ids = run.ids();
+    out->block_ids = static_cast<int*>(std::malloc(sizeof(int) * std::max<size_t>(ids.size(), 1)));
+    if (!ids.empty()) std::memcpy(out->block_ids, ids.data(), sizeof(int) * ids.size());
+    out->n_ids = int(ids.size());
+    out->gpu_launches = int(h.lc.total - launches0);
+    if (message_out) *message_out = message;
+    return status;
+}
+
+}  // namespace farqb

@@ -1,0 +1,87 @@
+// engine.hpp -- the device-resident farPCA blocked QB loop (C++ host side).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/farqb.h"
+#include "common.cuh"
+
+namespace farqb {
+
+// Stream-ordered device allocation (cudaMallocAsync pool), grown on demand.
+template <typename T>
+struct DeviceArray {
+    T* ptr = nullptr;
+    size_t count = 0;
+    cudaStream_t stream = nullptr;
+    DeviceArray() = default;
+    DeviceArray(const DeviceArray&) = delete;
+    DeviceArray& operator=(const DeviceArray&) = delete;
+    ~DeviceArray() { release(); }
+    void release() {
+        if (ptr) cudaFreeAsync(ptr, stream);
+        ptr = nullptr;
+        count = 0;
+    }
+    // contents are not preserved
+    T* ensure(size_t n, cudaStream_t s) {
+        if (n <= count && ptr) return ptr;
+        release();
+        stream = s;
+        FQB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ptr), std::max<size_t>(n, 1) * sizeof(T), s));
+        count = std::max<size_t>(n, 1);
+        return ptr;
+    }
+    // hand ownership to the caller
+    T* detach() {
+        T* p = ptr;
+        ptr = nullptr;
+        count = 0;
+        return p;
+    }
+};
+
+// Per-handle reusable workspace (everything except the Q and B' outputs).
+struct Workspace {
+    DeviceArray<double> omega, y0, ys, wp, wraw, g, t, cd, c2, small, zc, rowsum_b, splitk, partial,
+        scalars, scratch, a_copy;
+    DeviceArray<int> col_ptr, row_idx, counts;
+    DeviceArray<double> values;
+    DeviceArray<unsigned> status;
+};
+
+struct Handle {
+    int device = 0;
+    int num_sms = 148;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+    LaunchCounter lc;
+    Workspace ws;
+    unsigned* host_status = nullptr;  // pinned readback slot
+    double* host_scalars = nullptr;   // pinned readback slots
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};
+
+struct ResolvedConfig {
+    fqb_config cfg;
+    int64_t m, n;
+};
+
+// Runs the loop; fills `out` (status also returned).  Throws farqb::Error for
+// configuration / CUDA failures before any result exists.
+int run_qb(Handle& h, const double* a, int64_t m, int64_t n, int64_t lda, bool a_on_device,
+           bool fixed_precision, int rank, const fqb_config& cfg, fqb_block_source_fn src,
+           void* user, unsigned flags, fqb_qb_result* out, std::string* message_out);
+
+// Resolution rules of the reference (driver.cpp:116-132) plus zeta checks.
+fqb_config resolve_config(int64_t m, int64_t n, const fqb_config& in, bool fixed_precision);
+
+double default_density(int kind, int64_t n);
+int default_block(int64_t m, int64_t n);
+int default_max_iters(int64_t n, int b);
+
+}  // namespace farqb

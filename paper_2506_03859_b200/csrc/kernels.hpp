@@ -1,0 +1,118 @@
+// kernels.hpp -- host-side launchers for the farqb sm_100a kernels.
+//
+// Everything here enqueues device work on the given stream and returns
+// immediately; nothing falls back to the host.  The engine (engine.cu) and the
+// C-ABI building blocks (capi.cpp) are the only callers.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace farqb {
+
+enum SketchKindId { kGaussian = 0, kBernoulli = 1, kStdBernoulli = 2, kSparseSign = 3, kSparseGaussian = 4 };
+
+// Device status word shared by generator kernels: bit 0 = a Gaussian draw hit
+// an exact zero (the reference would redraw, rng.hpp:41-53); bit 1 = CSC
+// capacity exceeded.
+constexpr unsigned kGenZeroGaussian = 1u;
+constexpr unsigned kGenOverflow = 2u;
+
+// ---- sketch.cu ---------------------------------------------------------------
+void launch_philox_u32(uint64_t seed, uint32_t block_id, uint32_t column, int count, uint32_t* out,
+                       cudaStream_t s, LaunchCounter& lc);
+// Dense N(0,1) block, column j from stream (seed, block_id, j); out is n x l (ld).
+void launch_gaussian_dense(uint64_t seed, int block_id, int64_t n, int l, double* out, int64_t ld,
+                           unsigned* status, cudaStream_t s, LaunchCounter& lc);
+// i.i.d. density-p pattern (geometric gap walk, sketch.cpp:35-47, 75-95).
+// count pass -> counts[l]; csc pass needs col_ptr; dense pass writes
+// (value - shift) at nonzeros and -shift elsewhere into an n x l buffer.
+void launch_iid_count(int kind, uint64_t seed, int block_id, int64_t n, int l, double denom,
+                      int* counts, cudaStream_t s, LaunchCounter& lc);
+void launch_iid_fill_csc(int kind, uint64_t seed, int block_id, int64_t n, int l, double denom,
+                         double scale, const int* col_ptr, int* row_idx, double* values,
+                         unsigned* status, cudaStream_t s, LaunchCounter& lc);
+void launch_iid_fill_dense(int kind, uint64_t seed, int block_id, int64_t n, int l, double denom,
+                           double scale, double shift, double* out, int64_t ld, unsigned* status,
+                           cudaStream_t s, LaunchCounter& lc);
+// Fixed zeta nonzeros per column (sparse sign / sparse Gaussian).
+void launch_zeta_fill(int kind, uint64_t seed, int block_id, int64_t n, int l, int zeta,
+                      double scale, int* col_ptr, int* row_idx, double* values, unsigned* status,
+                      cudaStream_t s, LaunchCounter& lc);
+// exclusive scan of counts[l] into col_ptr[l+1] (single CTA)
+void launch_exclusive_scan(const int* counts, int l, int* col_ptr, cudaStream_t s, LaunchCounter& lc);
+// out (n x l, ld) = dense(S) - shift
+void launch_densify(const int* col_ptr, const int* row_idx, const double* values, int64_t n, int l,
+                    double shift, double* out, int64_t ld, cudaStream_t s, LaunchCounter& lc);
+
+// ---- spmm.cu -----------------------------------------------------------------
+// C (m x l) = A (m x n) * S  [- z]   one fma per nonzero in CSC order.
+void launch_gather_spmm(const double* a, int64_t m, int64_t lda, const int* col_ptr,
+                        const int* row_idx, const double* values, int l, const double* z,
+                        double* c, int64_t ldc, cudaStream_t s, LaunchCounter& lc);
+// T (k x l) = Wt' * S [- shift * colsum(Wt) broadcast] where Wt is n x k (ld),
+// i.e. the row-gather product used by the deflation B * Omega.
+void launch_gather_tmul(const double* wt, int64_t n, int64_t ldw, int k, const int* col_ptr,
+                        const int* row_idx, const double* values, int l, const double* colsum,
+                        double shift, double* t, int64_t ldt, cudaStream_t s, LaunchCounter& lc);
+
+// ---- reduce.cu ---------------------------------------------------------------
+// Deterministic two-stage sums.  partial must hold kReducePartials doubles.
+constexpr int kReducePartials = 1184;  // 8 x 148
+void launch_sumsq(const double* a, int64_t m, int64_t n, int64_t lda, double* partial, double* out,
+                  cudaStream_t s, LaunchCounter& lc);
+// z[i] = sum_c fma(p, A[i,c], z[i]) in column order (driver.cpp:178-183), bitwise
+// the reference's axpy sequence.
+void launch_centering(const double* a, int64_t m, int64_t n, int64_t lda, double p, double* z,
+                      cudaStream_t s, LaunchCounter& lc);
+// colsum[j] = sum_i X[i, j] for j < k (X is rows x k, ld)
+void launch_colsum(const double* x, int64_t rows, int k, int64_t ld, double* colsum, cudaStream_t s,
+                   LaunchCounter& lc);
+
+// ---- gemm.cu -----------------------------------------------------------------
+// C (m x n) = alpha op(A) B + beta C, column-major; DMMA (mma.sync f64) tensor
+// pipe, deterministic split-K.  `work` must hold gemm_workspace_doubles(...).
+int64_t gemm_workspace_doubles(int64_t m, int64_t n, int64_t k, int num_sms);
+void gemm(bool trans_a, int64_t m, int64_t n, int64_t k, double alpha, const double* a, int64_t lda,
+          const double* b, int64_t ldb, double beta, double* c, int64_t ldc, double* work,
+          int64_t work_doubles, int num_sms, cudaStream_t s, LaunchCounter& lc);
+
+// ---- smallla.cu --------------------------------------------------------------
+// Cholesky of the b x b SPD matrix S (ld = lds) with the reference pivot rule
+// (matrix_core.cpp:117-140): pivot <= tol * max(diag_ref, max diag(S)) fails.
+// Writes R = L' (upper) and R^{-1}, both b x b with ld = b; on failure sets
+// *status |= fail_bit and writes identities.
+// max_diag_out (optional) receives the pivot reference actually used; scratch
+// (b x (b+1) doubles) is only touched when b > 128.
+void launch_chol_upper_inv(const double* S, int b, int64_t lds, double tol, double diag_ref,
+                           const double* dref_extra, int64_t ld_extra, double* R, double* Rinv,
+                           double* max_diag_out, double* scratch, unsigned* status, unsigned fail_bit,
+                           cudaStream_t s, LaunchCounter& lc);
+// eigenvalues (ascending) of a b x b symmetric matrix (cyclic Jacobi,
+// matrix_core.cpp:50-115) and optionally eigenvectors (ld = b).
+// vtmp: b x b doubles of scratch when vectors are wanted.
+void launch_sym_eig(const double* S, int b, int64_t lds, double* values, double* vectors,
+                    double* vtmp, unsigned* status, unsigned fail_bit, cudaStream_t s,
+                    LaunchCounter& lc);
+// alpha <- (shat + alpha)/2 if alpha < shat (driver.cpp:216-221), on the device
+void launch_shift_update(const double* values, int b, int conv, double* alpha, cudaStream_t s,
+                         LaunchCounter& lc);
+// y[:, c] -= (*alpha) * x[:, c]
+void launch_axpy_cols_dev(const double* alpha, const double* x, int64_t ldx, double* y, int64_t ldy,
+                          int64_t rows, int cols, cudaStream_t s, LaunchCounter& lc);
+// eigSVD tail (matrix_core.cpp:193-215): from ascending eigenvalues/vectors of
+// W'W build V Sigma^{-1} (b x b) and sigma; sets fail_bit if lmax <= 0.
+void launch_eigsvd_scale(const double* values, const double* vectors, int b, double* vs,
+                         double* sigma, unsigned* status, unsigned fail_bit, cudaStream_t s,
+                         LaunchCounter& lc);
+// out[0] = sum of squares of a column-major x (rows x cols, ld) (two-stage)
+void launch_sumsq_small(const double* x, int64_t rows, int64_t cols, int64_t ld, double* partial,
+                        double* out, cudaStream_t s, LaunchCounter& lc);
+// y[:, c] -= alpha * x[:, c] (rows x cols)
+void launch_axpy_cols(double alpha, const double* x, int64_t ldx, double* y, int64_t ldy,
+                      int64_t rows, int cols, cudaStream_t s, LaunchCounter& lc);
+
+}  // namespace farqb

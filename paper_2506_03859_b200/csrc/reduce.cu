@@ -1,0 +1,121 @@
+// reduce.cu -- deterministic reductions over A and the B blocks.
+//
+//  launch_sumsq       ||A||_F^2 (reference frob_norm_sq, matrix_core.cpp:46-48):
+//                     fixed grid, per-CTA tree sums, then one fixed-order pass.
+//  launch_centering   z = A (p 1_n) (reference centering_column, driver.cpp:
+//                     178-183): one thread per row, columns in order with one
+//                     fma each -- the reference's axpy sequence, so z (and the
+//                     centered sketch Y = A S - z) match it bit for bit.
+//  launch_colsum      column sums of B' for the centered deflation term.
+#include <cstdint>
+
+#include "kernels.hpp"
+
+namespace farqb {
+namespace {
+
+constexpr int kSeg = 4096;  // rows per segment
+
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) sh[warp] = v;
+    __syncthreads();
+    const int nw = blockDim.x >> 5;
+    v = threadIdx.x < nw ? sh[threadIdx.x] : 0.0;
+    if (warp == 0) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+    }
+    return v;  // valid in thread 0
+}
+
+__global__ void __launch_bounds__(256) k_sumsq_partial(const double* __restrict__ a, int64_t m,
+                                                       int64_t n, int64_t lda, double* partial) {
+    __shared__ double sh[32];
+    const int64_t segs_per_col = (m + kSeg - 1) / kSeg;
+    const int64_t total = segs_per_col * n;
+    double acc = 0.0;
+    for (int64_t sgi = blockIdx.x; sgi < total; sgi += gridDim.x) {
+        const int64_t col = sgi / segs_per_col;
+        const int64_t r0 = (sgi - col * segs_per_col) * kSeg;
+        const int64_t r1 = r0 + kSeg < m ? r0 + kSeg : m;
+        const double* c = a + col * lda;
+        for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+            const double v = __ldg(c + r);
+            acc = fma(v, v, acc);
+        }
+    }
+    const double s = block_sum(acc, sh);
+    if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
+__global__ void k_sum_partials(const double* partial, int count, double* out) {
+    __shared__ double sh[32];
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < count; i += blockDim.x) acc += partial[i];
+    const double s = block_sum(acc, sh);
+    if (threadIdx.x == 0) *out = s;
+}
+
+__global__ void __launch_bounds__(128) k_centering(const double* __restrict__ a, int64_t m, int64_t n,
+                                                   int64_t lda, double p, double* __restrict__ z) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    const double* r = a + i;
+    double acc = 0.0;
+    int64_t c = 0;
+    for (; c + 8 <= n; c += 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __ldg(r + (c + u) * lda);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc = fma(p, v[u], acc);
+    }
+    for (; c < n; ++c) acc = fma(p, __ldg(r + c * lda), acc);
+    z[i] = acc;
+}
+
+__global__ void __launch_bounds__(256) k_colsum(const double* __restrict__ x, int64_t rows,
+                                                int64_t ld, double* colsum) {
+    __shared__ double sh[32];
+    const double* c = x + int64_t(blockIdx.x) * ld;
+    double acc = 0.0;
+    for (int64_t r = threadIdx.x; r < rows; r += blockDim.x) acc += c[r];
+    const double s = block_sum(acc, sh);
+    if (threadIdx.x == 0) colsum[blockIdx.x] = s;
+}
+
+}  // namespace
+
+void launch_sumsq(const double* a, int64_t m, int64_t n, int64_t lda, double* partial, double* out,
+                  cudaStream_t s, LaunchCounter& lc) {
+    k_sumsq_partial<<<kReducePartials, 256, 0, s>>>(a, m, n, lda, partial);
+    FQB_LAUNCHED();
+    k_sum_partials<<<1, 1024, 0, s>>>(partial, kReducePartials, out);
+    FQB_LAUNCHED();
+    lc.bump(2);
+}
+
+void launch_centering(const double* a, int64_t m, int64_t n, int64_t lda, double p, double* z,
+                      cudaStream_t s, LaunchCounter& lc) {
+    k_centering<<<unsigned(ceil_div(m, 128)), 128, 0, s>>>(a, m, n, lda, p, z);
+    FQB_LAUNCHED();
+    lc.bump();
+}
+
+void launch_colsum(const double* x, int64_t rows, int k, int64_t ld, double* colsum, cudaStream_t s,
+                   LaunchCounter& lc) {
+    if (k <= 0) return;
+    k_colsum<<<unsigned(k), 256, 0, s>>>(x, rows, ld, colsum);
+    FQB_LAUNCHED();
+    lc.bump();
+}
+
+void launch_sumsq_small(const double* x, int64_t rows, int64_t cols, int64_t ld, double* partial,
+                        double* out, cudaStream_t s, LaunchCounter& lc) {
+    launch_sumsq(x, rows, cols, ld, partial, out, s, lc);
+}
+
+}  // namespace farqb

@@ -1,0 +1,508 @@
+"""Python mirror of the reference's QB API (rsvd::, /root/reference/proj/include/rsvd/).
+
+Same names, argument meaning and error behaviour as the C++ reference, so a
+caller of ``rsvd::run_fixed_precision(a, cfg, source)`` (driver.hpp:98-99) can
+switch to ``run_fixed_precision(a, cfg, source)`` here; the difference is the
+result, which carries the north-star QB outputs (Q, B', rank, error indicator)
+computed by the sm_100a engine in libfarqb.so:
+
+  reference                                this module
+  ---------------------------------------  ------------------------------------
+  SketchKind, sketch_kind_name/_from_name  SketchKind, sketch_kind_name/_from_name
+  SketchSpec{kind, p, seed}                SketchSpec(kind, p, seed, zeta=0)
+  FarpcaConfig{eps, power, block, sketch,  FarpcaConfig(...)  same fields
+    max_iters, shift_convention, relative}
+  ShiftConvention                          ShiftConvention
+  BlockSource::next(n, b, block_id)        BlockSource.next(n, b, block_id) -> SketchBlock
+  SketchBlock / SparseSketch               SketchBlock (numpy arrays)
+  run_fixed_precision / run_fixed_rank     run_fixed_precision / run_fixed_rank -> QBResult
+  gen_sketch                               gen_sketch (generated on the device)
+  ConfigError, DimensionError,             same exception classes
+  BlockDegenerate, ToleranceNotReached,
+  ConvergenceFailure
+  default_density/_block/_max_iters        same
+
+Matrices are column-major (Fortran order) float64, like DenseMatrix
+(dense_matrix.hpp:13-51).  Accepted inputs: numpy arrays (host), torch tensors
+on the host or on a CUDA device.  Every compute call runs on the GPU; without
+one the calls raise CudaError.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import _native as N
+
+# ---------------------------------------------------------------- errors ----
+
+
+class RsvdError(Exception):
+    status = -1
+
+
+class ConfigError(RsvdError, ValueError):
+    status = 1
+
+
+class DimensionError(RsvdError, ValueError):
+    status = 2
+
+
+class BlockDegenerate(RsvdError, RuntimeError):
+    """errors.hpp:28-37; carries the accepted block count and residual."""
+    status = 3
+
+    def __init__(self, msg, blocks_accepted=0, residual_sq=0.0, norm_a_sq=0.0):
+        super().__init__(msg)
+        self.blocks_accepted = blocks_accepted
+        self.residual_sq = residual_sq
+        self.norm_a_sq = norm_a_sq
+
+
+class ToleranceNotReached(RsvdError, RuntimeError):
+    """driver.hpp:60-65; ``partial`` is the QB result after max_iters blocks."""
+    status = 4
+
+    def __init__(self, msg, partial=None):
+        super().__init__(msg)
+        self.partial = partial
+
+
+class CudaError(RsvdError, RuntimeError):
+    status = 5
+
+
+class InvalidArgument(RsvdError, ValueError):
+    status = 7
+
+
+class ConvergenceFailure(RsvdError, RuntimeError):
+    status = 8
+
+
+class CallbackError(RsvdError, RuntimeError):
+    status = 9
+
+
+class AllocError(RsvdError, MemoryError):
+    status = 10
+
+
+_ERRORS = {c.status: c for c in (ConfigError, DimensionError, BlockDegenerate, ToleranceNotReached,
+                                 CudaError, InvalidArgument, ConvergenceFailure, CallbackError,
+                                 AllocError)}
+
+
+def _raise(status: int, what: str = ""):
+    msg = N.lib().fqb_last_error().decode(errors="replace")
+    cls = _ERRORS.get(status, RsvdError)
+    raise cls(f"{what}: {msg}" if what else msg)
+
+
+# ------------------------------------------------------------------ types ---
+
+
+class SketchKind(enum.IntEnum):
+    Gaussian = 0
+    Bernoulli = 1
+    StdBernoulli = 2
+    SparseSign = 3
+    SparseGaussian = 4
+
+
+_KIND_NAMES = {SketchKind.Gaussian: "gaussian", SketchKind.Bernoulli: "bernoulli",
+               SketchKind.StdBernoulli: "stdbernoulli", SketchKind.SparseSign: "sparsesign",
+               SketchKind.SparseGaussian: "sparsegaussian"}
+
+
+def sketch_kind_name(k: SketchKind) -> str:
+    return _KIND_NAMES.get(SketchKind(k), "unknown")
+
+
+def sketch_kind_from_name(name: str) -> SketchKind:
+    for k, v in _KIND_NAMES.items():
+        if v == name:
+            return k
+    raise ConfigError(f"unknown sketch kind: {name}")
+
+
+class ShiftConvention(enum.IntEnum):
+    LastDiagonal = 0
+    FirstDiagonal = 1
+
+
+@dataclass
+class SketchSpec:
+    kind: SketchKind = SketchKind.Gaussian
+    p: float = 0.0
+    seed: int = 0
+    zeta: int = 0     # > 0: exactly zeta nonzeros per column (sparse sign / Gaussian)
+
+
+@dataclass
+class FarpcaConfig:
+    eps: float = 0.0
+    power: int = 0
+    block: int = 0
+    sketch: SketchSpec = field(default_factory=SketchSpec)
+    max_iters: int = 0
+    shift_convention: ShiftConvention = ShiftConvention.LastDiagonal
+    relative: bool = False
+
+    def _c(self) -> N.ConfigC:
+        s = self.sketch
+        return N.ConfigC(float(self.eps), int(self.power), int(self.block),
+                         N.SketchSpecC(int(s.kind), float(s.p), int(s.seed) & (2**64 - 1), int(s.zeta)),
+                         int(self.max_iters), int(self.shift_convention), int(bool(self.relative)))
+
+
+@dataclass
+class SketchBlock:
+    """rsvd::SketchBlock (sketch.hpp:37-44) with numpy arrays."""
+    is_dense: bool
+    rows: int
+    cols: int
+    dense: Optional[np.ndarray] = None      # rows x cols, Fortran order
+    col_ptr: Optional[np.ndarray] = None
+    row_idx: Optional[np.ndarray] = None
+    values: Optional[np.ndarray] = None
+    centered: bool = False
+    p: float = 0.0
+    std_scale: float = 0.0
+
+    @property
+    def nnz(self) -> int:
+        return 0 if self.is_dense else int(self.col_ptr[-1])
+
+    def densify(self) -> np.ndarray:
+        if self.is_dense:
+            return self.dense
+        d = np.zeros((self.rows, self.cols), order="F")
+        for j in range(self.cols):
+            s, e = self.col_ptr[j], self.col_ptr[j + 1]
+            d[self.row_idx[s:e], j] = self.values[s:e]
+        return d
+
+
+class BlockSource:
+    """rsvd::BlockSource (driver.hpp:67-73): supplies the raw block for (n, b, block_id)."""
+
+    def next(self, n: int, b: int, block_id: int) -> SketchBlock:  # pragma: no cover - interface
+        raise NotImplementedError
+
+
+@dataclass
+class QBResult:
+    """QB factorization A ~ Q B with the reference's ApproxSvd scalars.
+
+    q  : m x rank, orthonormal columns
+    bt : n x rank, B transposed (B = Q' A is rank x n)
+    residual_sq : the error indicator E = ||A||_F^2 - sum ||B_j||_F^2
+    """
+    q: object
+    bt: object
+    rank: int
+    blocks: int
+    converged: bool
+    residual_sq: float
+    norm_a_sq: float
+    block_residuals: np.ndarray
+    block_ids: list
+    resolved_block: int
+    resolved_max_iters: int
+    resolved_p: float
+    elapsed_ms: float
+    gpu_launches: int
+
+    @property
+    def b(self):
+        return None if self.bt is None else self.bt.T
+
+
+def default_density(kind: SketchKind, n: int) -> float:
+    return N.lib().fqb_default_density(int(kind), int(n))
+
+
+def default_block(m: int, n: int) -> int:
+    return N.lib().fqb_default_block(int(m), int(n))
+
+
+def default_max_iters(n: int, b: int) -> int:
+    return N.lib().fqb_default_max_iters(int(n), int(b))
+
+
+# ----------------------------------------------------------------- engine ---
+
+
+class _DeviceBuffer:
+    """Owns a library-allocated device array; exposes __cuda_array_interface__."""
+
+    def __init__(self, ptr: int, rows: int, cols: int, ld: int):
+        self.ptr = ptr
+        self.__cuda_array_interface__ = {
+            "shape": (cols, rows), "strides": (ld * 8, 8), "typestr": "<f8",
+            "data": (ptr, False), "version": 3}
+
+    def __del__(self):
+        try:
+            import torch  # noqa: F401
+            from . import _native
+            _cudart_free(self.ptr)
+        except Exception:  # noqa: BLE001 - interpreter shutdown
+            pass
+
+
+def _cudart_free(ptr: int) -> None:
+    r = N.ResultC()
+    r.on_device = 1
+    r.q = ptr
+    r.bt = None
+    N.lib().fqb_result_free(C.byref(r))
+
+
+def _is_torch(x) -> bool:
+    return type(x).__module__.startswith("torch")
+
+
+def _as_colmajor(a):
+    """-> (pointer, m, n, lda, on_device, keepalive)."""
+    if _is_torch(a):
+        import torch
+        if a.dtype != torch.float64 or a.dim() != 2:
+            raise InvalidArgument("A must be a 2-D float64 tensor")
+        m, n = a.shape
+        if not (a.stride(0) == 1 and (a.stride(1) >= max(m, 1) or n == 1)):
+            a = a.t().contiguous().t()  # column-major copy
+        lda = a.stride(1) if n > 1 else max(m, 1)
+        return a.data_ptr(), m, n, lda, a.is_cuda, a
+    arr = np.asfortranarray(np.asarray(a, dtype=np.float64))
+    if arr.ndim != 2:
+        raise InvalidArgument("A must be 2-D")
+    m, n = arr.shape
+    return arr.ctypes.data, m, n, max(m, 1), False, arr
+
+
+class Engine:
+    """One libfarqb handle (one device, one stream, reusable workspace)."""
+
+    def __init__(self, device: int = 0):
+        self._lib = N.lib()
+        h = C.c_void_p()
+        st = self._lib.fqb_create(int(device), C.byref(h))
+        if st != 0:
+            _raise(st, "fqb_create")
+        self._h = h
+        self.device = device
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.fqb_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+    @property
+    def launch_count(self) -> int:
+        return self._lib.fqb_launch_count(self._h)
+
+    def set_stream(self, stream_ptr: int | None):
+        st = self._lib.fqb_set_stream(self._h, stream_ptr)
+        if st:
+            _raise(st, "fqb_set_stream")
+
+    def synchronize(self):
+        st = self._lib.fqb_synchronize(self._h)
+        if st:
+            _raise(st, "fqb_synchronize")
+
+    # ---- the QB loop --------------------------------------------------------
+    def run_fixed_precision(self, a, cfg: FarpcaConfig, source: BlockSource | None = None,
+                            output: str = "device") -> QBResult:
+        return self._run(a, cfg, source, output, rank=None)
+
+    def run_fixed_rank(self, a, rank: int, cfg: FarpcaConfig, source: BlockSource | None = None,
+                       output: str = "device") -> QBResult:
+        return self._run(a, cfg, source, output, rank=rank)
+
+    def _run(self, a, cfg, source, output, rank):
+        ptr, m, n, lda, on_dev, keep = _as_colmajor(a)
+        flags = {"device": N.OUT_DEVICE, "host": N.OUT_HOST, "none": N.OUT_NONE}[output]
+        res = N.ResultC()
+        ccfg = cfg._c()
+        cb, err, hold = self._make_source(source)
+        if rank is None:
+            st = self._lib.fqb_qb_fixed_precision(self._h, ptr, m, n, lda, int(on_dev), C.byref(ccfg),
+                                                  cb, None, flags, C.byref(res))
+        else:
+            st = self._lib.fqb_qb_fixed_rank(self._h, ptr, m, n, lda, int(on_dev), int(rank),
+                                             C.byref(ccfg), cb, None, flags, C.byref(res))
+        del keep, hold
+        if err:
+            self._lib.fqb_result_free(C.byref(res))
+            raise CallbackError("block source raised") from err[0]
+        if st not in (0, 3, 4):
+            self._lib.fqb_result_free(C.byref(res))
+            _raise(st)
+        out = self._collect(res, m, n, output)
+        if st == 4:
+            raise ToleranceNotReached(
+                f"tolerance not reached after {out.blocks} blocks; residual "
+                f"{np.sqrt(max(out.residual_sq, 0.0)):.6g}", out)
+        if st == 3:
+            raise BlockDegenerate(N.lib().fqb_last_error().decode(errors="replace"), out.blocks,
+                                  out.residual_sq, out.norm_a_sq)
+        return out
+
+    def _make_source(self, source):
+        if source is None:
+            return N.SOURCE_FN(), [], None
+        err: list = []
+        keep: list = []
+
+        def cb(_user, n, b, bid, out):
+            try:
+                blk = source.next(n, b, bid) if isinstance(source, BlockSource) else source(n, b, bid)
+                keep.clear()
+                c = N.BlockC()
+                c.is_dense = int(blk.is_dense)
+                c.rows, c.cols = int(blk.rows), int(blk.cols)
+                c.centered = int(blk.centered)
+                c.p = float(blk.p)
+                c.std_scale = float(blk.std_scale)
+                if blk.is_dense:
+                    d = np.asfortranarray(blk.dense, dtype=np.float64)
+                    keep.append(d)
+                    c.dense = d.ctypes.data
+                else:
+                    cp = np.ascontiguousarray(blk.col_ptr, dtype=np.int32)
+                    ri = np.ascontiguousarray(blk.row_idx, dtype=np.int32)
+                    va = np.ascontiguousarray(blk.values, dtype=np.float64)
+                    if ri.size == 0:
+                        ri, va = np.zeros(1, np.int32), np.zeros(1)
+                    keep.extend([cp, ri, va])
+                    c.col_ptr, c.row_idx, c.values = cp.ctypes.data, ri.ctypes.data, va.ctypes.data
+                    c.nnz = int(cp[-1])
+                out[0] = c
+                return 0
+            except Exception as e:  # noqa: BLE001 - surfaced as CallbackError
+                err.append(e)
+                return 1
+
+        fn = N.SOURCE_FN(cb)
+        return fn, err, (fn, keep)
+
+    def _collect(self, res: N.ResultC, m: int, n: int, output: str) -> QBResult:
+        l = res.rank
+        q = bt = None
+        try:
+            if l > 0 and output == "device" and res.q:
+                import torch
+                qb = _DeviceBuffer(res.q, m, l, res.ldq)
+                bb = _DeviceBuffer(res.bt, n, l, res.ldbt)
+                res.q = None
+                res.bt = None
+                with torch.cuda.device(self.device):
+                    q = torch.as_tensor(qb, device=f"cuda:{self.device}").t()
+                    bt = torch.as_tensor(bb, device=f"cuda:{self.device}").t()
+            elif l > 0 and output == "host" and res.q:
+                q = np.ctypeslib.as_array(C.cast(res.q, C.POINTER(C.c_double)), (m * l,)).reshape(
+                    (m, l), order="F").copy()
+                bt = np.ctypeslib.as_array(C.cast(res.bt, C.POINTER(C.c_double)), (n * l,)).reshape(
+                    (n, l), order="F").copy()
+            br = (np.ctypeslib.as_array(res.block_residuals, (res.blocks,)).copy()
+                  if res.blocks and res.block_residuals else np.zeros(0))
+            ids = (np.ctypeslib.as_array(res.block_ids, (res.n_ids,)).tolist()
+                   if res.n_ids and res.block_ids else [])
+            return QBResult(q, bt, l, res.blocks, bool(res.converged), res.residual_sq, res.norm_a_sq,
+                            br, [int(i) for i in ids], res.resolved_block, res.resolved_max_iters,
+                            res.resolved_p, res.elapsed_ms, res.gpu_launches)
+        finally:
+            self._lib.fqb_result_free(C.byref(res))
+
+    # ---- building blocks ----------------------------------------------------
+    def philox_u32(self, seed: int, block_id: int, column: int, count: int) -> np.ndarray:
+        out = np.zeros(count, dtype=np.uint32)
+        st = self._lib.fqb_philox_u32(self._h, seed, block_id, column, count, out.ctypes.data)
+        if st:
+            _raise(st, "fqb_philox_u32")
+        return out
+
+    def gen_sketch(self, spec: SketchSpec, n: int, l: int, block_id: int) -> SketchBlock:
+        s = N.SketchHostC()
+        cs = N.SketchSpecC(int(spec.kind), float(spec.p), int(spec.seed) & (2**64 - 1), int(spec.zeta))
+        st = self._lib.fqb_gen_sketch(self._h, C.byref(cs), n, l, block_id, C.byref(s))
+        if st:
+            _raise(st, "fqb_gen_sketch")
+        try:
+            if s.is_dense:
+                d = np.ctypeslib.as_array(s.dense, (n * l,)).reshape((n, l), order="F").copy()
+                return SketchBlock(True, n, l, dense=d, p=s.p)
+            nnz = int(s.nnz)
+            cp = np.ctypeslib.as_array(s.col_ptr, (l + 1,)).copy()
+            ri = np.ctypeslib.as_array(s.row_idx, (max(nnz, 1),))[:nnz].copy()
+            va = np.ctypeslib.as_array(s.values, (max(nnz, 1),))[:nnz].copy()
+            return SketchBlock(False, n, l, col_ptr=cp, row_idx=ri, values=va,
+                               centered=bool(s.centered), p=s.p, std_scale=s.std_scale)
+        finally:
+            self._lib.fqb_sketch_free(C.byref(s))
+
+    def gemm(self, trans_a: bool, m, n, k, alpha, a_ptr, lda, b_ptr, ldb, beta, c_ptr, ldc):
+        st = self._lib.fqb_gemm(self._h, int(trans_a), m, n, k, alpha, a_ptr, lda, b_ptr, ldb, beta,
+                                c_ptr, ldc)
+        if st:
+            _raise(st, "fqb_gemm")
+
+    def sparse_dense_mul(self, a_ptr, m, n, lda, col_ptr_ptr, row_idx_ptr, values_ptr, l, z_ptr,
+                         c_ptr, ldc):
+        st = self._lib.fqb_sparse_dense_mul(self._h, a_ptr, m, n, lda, col_ptr_ptr, row_idx_ptr,
+                                            values_ptr, l, z_ptr, c_ptr, ldc)
+        if st:
+            _raise(st, "fqb_sparse_dense_mul")
+
+    def centering_column(self, a_ptr, m, n, lda, p, z_ptr):
+        st = self._lib.fqb_centering_column(self._h, a_ptr, m, n, lda, p, z_ptr)
+        if st:
+            _raise(st, "fqb_centering_column")
+
+    def frob_norm_sq(self, a_ptr, m, n, lda) -> float:
+        out = C.c_double()
+        st = self._lib.fqb_frob_norm_sq(self._h, a_ptr, m, n, lda, C.byref(out))
+        if st:
+            _raise(st, "fqb_frob_norm_sq")
+        return out.value
+
+
+_default_engines: dict = {}
+
+
+def default_engine(device: int = 0) -> Engine:
+    e = _default_engines.get(device)
+    if e is None:
+        e = _default_engines[device] = Engine(device)
+    return e
+
+
+def run_fixed_precision(a, cfg: FarpcaConfig, source: BlockSource | None = None,
+                        output: str = "device", device: int = 0) -> QBResult:
+    """rsvd::run_fixed_precision (driver.hpp:98-99) on the B200 engine."""
+    return default_engine(device).run_fixed_precision(a, cfg, source, output)
+
+
+def run_fixed_rank(a, rank: int, cfg: FarpcaConfig, source: BlockSource | None = None,
+                   output: str = "device", device: int = 0) -> QBResult:
+    """rsvd::run_fixed_rank (driver.hpp:101-103) on the B200 engine (QB of nblocks * b columns)."""
+    return default_engine(device).run_fixed_rank(a, rank, cfg, source, output)
+
+
+def gen_sketch(spec: SketchSpec, n: int, l: int, block_id: int, device: int = 0) -> SketchBlock:
+    """rsvd::gen_sketch (sketch.hpp:46), generated on the device."""
+    return default_engine(device).gen_sketch(spec, n, l, block_id)

@@ -1,0 +1,345 @@
+"""GPU parity: libfarqb (sm_100a) against the CPU oracle and the reference's golden vectors.
+
+Every call goes through the C-ABI (include/farqb.h) via paper_2506_03859_b200.
+Tolerances (BASELINE north star):
+  integer / index work (rank, blocks, redraw ids, CSC arrays, Philox words): exact
+  sparse gather product, centering column: bitwise (same fma sequence)
+  error indicator E: |E_gpu - E_ref| <= 1e-10 ||A||_F^2
+  top singular values (sigma >= 1e-3 sigma_max): 1e-10 sigma_max for P >= 1,
+      1e-7 for P = 0 (the reference's Gram-space assembly is only that accurate)
+  Gaussian Omega values: 4 ulp (CUDA vs glibc log/sin/cos)
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover - CPU container
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2506_03859_b200 as fqb  # noqa: E402
+from oracle.oracle import SketchArrays  # noqa: E402
+from paper_2506_03859_b200 import FarpcaConfig, SketchKind, SketchSpec  # noqa: E402
+
+KINDS = {"gaussian": 0, "bernoulli": 1, "stdbernoulli": 2, "sparsesign": 3, "sparsegaussian": 4}
+
+
+@pytest.fixture(scope="module")
+def eng():
+    return fqb.default_engine(0)
+
+
+def _arr(s) -> SketchArrays:
+    if s.is_dense:
+        return SketchArrays(True, s.rows, s.cols, dense=s.dense, p=s.p)
+    return SketchArrays(False, s.rows, s.cols, col_ptr=s.col_ptr, row_idx=s.row_idx, values=s.values,
+                        centered=s.centered, p=s.p, std_scale=s.std_scale)
+
+
+def _sigma(bt: np.ndarray) -> np.ndarray:
+    return np.sort(np.linalg.svd(bt, compute_uv=False))
+
+
+def _lowrank(m, n, sig, seed):
+    rng = np.random.default_rng(seed)
+    r = len(sig)
+    u, _ = np.linalg.qr(rng.standard_normal((m, r)))
+    v, _ = np.linalg.qr(rng.standard_normal((n, r)))
+    return np.asfortranarray((u * sig) @ v.T)
+
+
+# ---------------------------------------------------------------- Philox / Omega
+
+def test_philox_words_match_golden(eng, golden):
+    for e in golden["philox"]:
+        got = eng.philox_u32(e["seed"], e["block_id"], e["column"], 16)
+        assert got.tolist() == e["u32"]
+
+
+def test_device_sketch_matches_golden(eng, golden):
+    for e in golden["sketch"]:
+        s = eng.gen_sketch(SketchSpec(KINDS[e["kind"]], e["p"], e["seed"]), e["n"], e["l"], e["block_id"])
+        if "dense" in e:
+            want = np.array(e["dense"])
+            np.testing.assert_allclose(s.dense.flatten(order="F"), want, rtol=4 * 2.2e-16, atol=0)
+        else:
+            assert s.col_ptr.tolist() == e["col_ptr"]
+            assert s.row_idx.tolist() == e["row_idx"]
+            if e["kind"] == "sparsegaussian":
+                np.testing.assert_allclose(s.values, e["values"], rtol=4 * 2.2e-16, atol=0)
+            else:
+                assert s.values.tolist() == e["values"]
+            assert s.centered == e["centered"]
+
+
+@pytest.mark.parametrize("kind", [1, 2, 3, 4])
+@pytest.mark.parametrize("p,n,l", [(0.002, 20000, 64), (0.05, 3000, 50), (0.5, 8000, 50)])
+def test_device_iid_sketch_matches_oracle(eng, port, kind, p, n, l):
+    for bid in (0, 1000, 7):
+        s = eng.gen_sketch(SketchSpec(kind, p, 7), n, l, bid)
+        o = port.gen_sketch(kind, p, 7, n, l, bid)
+        assert np.array_equal(s.col_ptr, o.col_ptr)
+        assert np.array_equal(s.row_idx, o.row_idx)
+        if kind == 4:
+            np.testing.assert_allclose(s.values, o.values, rtol=4 * 2.2e-16, atol=0)
+        else:
+            assert np.array_equal(s.values, o.values)
+
+
+@pytest.mark.parametrize("kind", [3, 4])
+@pytest.mark.parametrize("zeta,n,l", [(8, 20000, 64), (8, 20000, 100), (4, 50000, 128), (1, 50, 7)])
+def test_device_zeta_sketch_matches_oracle(eng, port, kind, zeta, n, l):
+    for bid in (0, 3, 2000):
+        s = eng.gen_sketch(SketchSpec(kind, 0.0, 42, zeta=zeta), n, l, bid)
+        o = port.gen_sketch(kind, 0.0, 42, n, l, bid, zeta=zeta)
+        assert np.array_equal(s.col_ptr, o.col_ptr)
+        assert np.array_equal(s.row_idx, o.row_idx)
+        if kind == 3:
+            assert np.array_equal(s.values, o.values)
+        else:
+            np.testing.assert_allclose(s.values, o.values, rtol=4 * 2.2e-16, atol=0)
+
+
+def test_dense_gaussian_block_matches_oracle(eng, port):
+    s = eng.gen_sketch(SketchSpec(0, 0.0, 7), 2001, 20, 5)
+    o = port.gen_sketch(0, 0.0, 7, 2001, 20, 5)
+    np.testing.assert_allclose(s.dense, o.dense, rtol=8 * 2.2e-16, atol=1e-300)
+
+
+# ---------------------------------------------------------------- kernels
+
+@pytest.mark.parametrize("trans", [False, True])
+@pytest.mark.parametrize("m,n,k", [(8000, 50, 8000), (257, 20, 1999), (100, 104, 3000), (33, 7, 5),
+                                   (5000, 128, 700), (64, 160, 999), (1, 1, 1)])
+def test_gemm_matches_fp64_reference(eng, trans, m, n, k):
+    g = torch.Generator(device="cpu").manual_seed(m * 7 + n + k)
+    a = torch.randn((k, m) if trans else (m, k), dtype=torch.float64, generator=g)
+    b = torch.randn((k, n), dtype=torch.float64, generator=g)
+    c0 = torch.randn((m, n), dtype=torch.float64, generator=g)
+    ad = a.t().contiguous().t().cuda() if False else a.cuda().t().contiguous().t()
+    bd = b.cuda().t().contiguous().t()
+    cd = c0.cuda().t().contiguous().t()
+    eng.gemm(trans, m, n, k, 0.75, ad.data_ptr(), ad.stride(1), bd.data_ptr(), bd.stride(1), -0.5,
+             cd.data_ptr(), cd.stride(1))
+    torch.cuda.synchronize()
+    want = 0.75 * ((a.t() if trans else a) @ b) - 0.5 * c0
+    err = (cd.cpu() - want).abs().max().item()
+    scale = (a.abs().max() * b.abs().max() * k + c0.abs().max()).item()
+    assert err <= 1e-14 * scale, (err, scale)
+
+
+def test_gemm_odd_leading_dimension(eng):
+    m, n, k = 301, 13, 257
+    g = torch.Generator(device="cpu").manual_seed(3)
+    big = torch.randn((k, m + 1), dtype=torch.float64, generator=g).cuda()   # lda = m+1 (even)
+    big2 = torch.randn((n, k + 2), dtype=torch.float64, generator=g).cuda()  # ldb = k+2 (odd)
+    c = torch.zeros((n, m), dtype=torch.float64, device="cuda")
+    eng.gemm(False, m, n, k, 1.0, big.data_ptr(), m + 1, big2.data_ptr(), k + 2, 0.0, c.data_ptr(), m)
+    torch.cuda.synchronize()
+    A = big[:, :m].t()
+    B = big2[:, :k].t()
+    want = A @ B
+    assert (c.t() - want).abs().max().item() < 1e-12
+
+
+def test_gather_spmm_is_bitwise_the_reference_axpy(eng, port):
+    m, n, l = 4099, 3000, 37
+    rng = np.random.default_rng(1)
+    a = np.asfortranarray(rng.standard_normal((m, n)))
+    for kind, p, zeta in ((3, 0.0, 8), (4, 0.0, 8), (2, 0.01, 0)):
+        s = port.gen_sketch(kind, p, 9, n, l, 2, zeta=zeta)
+        want = port.sparse_dense_mul(a, s)
+        ad = torch.from_numpy(a).cuda().t().contiguous().t()
+        out = torch.empty((l, m), dtype=torch.float64, device="cuda")
+        cp = torch.from_numpy(s.col_ptr.astype(np.int32)).cuda()
+        ri = torch.from_numpy(s.row_idx.astype(np.int32)).cuda()
+        va = torch.from_numpy(s.values).cuda()
+        eng.sparse_dense_mul(ad.data_ptr(), m, n, m, cp.data_ptr(), ri.data_ptr(), va.data_ptr(), l, None,
+                             out.data_ptr(), m)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.t().cpu().numpy(), want)
+        # centered: A S - z with the reference's z (bitwise too)
+        z = port.centering_column(a, 0.01)
+        zd = torch.from_numpy(z).cuda()
+        eng.sparse_dense_mul(ad.data_ptr(), m, n, m, cp.data_ptr(), ri.data_ptr(), va.data_ptr(), l,
+                             zd.data_ptr(), out.data_ptr(), m)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.t().cpu().numpy(), want - z[:, None])
+
+
+def test_centering_column_bitwise(eng, port):
+    m, n = 1001, 777
+    a = np.asfortranarray(np.random.default_rng(2).standard_normal((m, n)))
+    ad = torch.from_numpy(a).cuda().t().contiguous().t()
+    z = torch.empty(m, dtype=torch.float64, device="cuda")
+    eng.centering_column(ad.data_ptr(), m, n, m, 0.3, z.data_ptr())
+    torch.cuda.synchronize()
+    assert np.array_equal(z.cpu().numpy(), port.centering_column(a, 0.3))
+
+
+def test_frob_norm(eng):
+    a = torch.randn(3001, 257, dtype=torch.float64, device="cuda")
+    got = eng.frob_norm_sq(a.data_ptr(), 257, 3001, 257)
+    want = (a.double() ** 2).sum().item()
+    assert abs(got - want) <= 1e-13 * want
+
+
+# ---------------------------------------------------------------- the QB loop
+
+def _check_run(res, ref, power, tag):
+    assert res.blocks == ref.blocks, tag
+    assert res.block_ids == ref.block_ids, tag
+    na = ref.norm_a_sq
+    assert abs(res.residual_sq - ref.residual_sq) <= 1e-10 * na, (tag, res.residual_sq, ref.residual_sq)
+    assert np.max(np.abs(res.block_residuals - np.asarray(ref.block_residuals))) <= 1e-10 * na, tag
+    if res.rank:
+        sig = _sigma(res.bt)
+        rs = np.asarray(ref.sigma)
+        top = rs >= 1e-3 * rs[-1]
+        k = min(len(sig), len(rs))
+        tol = 1e-10 if power >= 1 else 1e-7
+        assert np.max(np.abs(sig[-k:][top[-k:]] - rs[-k:][top[-k:]])) <= tol * rs[-1], tag
+        q = res.q
+        assert np.abs(q.T @ q - np.eye(res.rank)).max() < 1e-12, tag
+
+
+def test_qb_matches_golden_reference_runs(golden, golden_mats):
+    """Device-generated Omega, same seeds as the reference's own gen_sketch."""
+    for r in golden["runs"]:
+        a = golden_mats[r["matrix"]]
+        spec = SketchSpec(KINDS[r["kind"]], r["p"], r["seed"])
+        cfg = FarpcaConfig(eps=r["eps"], power=r["power"], block=r["block"], sketch=spec,
+                           max_iters=r.get("max_iters", 0), relative=r["relative"])
+        tag = f"{r['matrix']} {r['kind']} P={r['power']} rank={r['rank']}"
+        try:
+            if r["rank"] is None:
+                res = fqb.run_fixed_precision(a, cfg, output="host")
+                status = 0
+            else:
+                res = fqb.run_fixed_rank(a, r["rank"], cfg, output="host")
+                status = 0
+        except fqb.ToleranceNotReached as e:
+            res, status = e.partial, 4
+        assert status == r["status"], tag
+        if r["rank"] is not None:
+            # fixed rank returns the QB of nblocks*b columns; the reference drops the overshoot
+            continue
+
+        class R:  # golden as an oracle-like record
+            pass
+        ref = R()
+        ref.blocks, ref.block_ids, ref.norm_a_sq = r["blocks"], r["block_ids"], r["norm_a_sq"]
+        ref.residual_sq, ref.block_residuals, ref.sigma = r["residual_sq"], r["block_residuals"], r["sigma"]
+        assert res.rank == r["out_rank"], tag
+        _check_run(res, ref, r["power"], tag)
+
+
+@pytest.mark.parametrize("kind,zeta", [(0, 0), (2, 0), (3, 8), (4, 8), (3, 0), (1, 0)])
+@pytest.mark.parametrize("power", [0, 1, 2, 3])
+def test_qb_matches_oracle_same_omega(eng, port, kind, zeta, power):
+    """GPU engine with its on-device generator vs the oracle fed the identical Omega."""
+    a = _lowrank(700, 500, 1.0 / np.arange(1, 201) ** 1.5, seed=kind * 10 + power)
+    p = 0.0 if kind == 0 or zeta else (0.5 if kind == 2 else 0.02)
+    spec = SketchSpec(kind, p, 11, zeta=zeta)
+    cfg = FarpcaConfig(eps=1e-2, power=power, block=20, sketch=spec, relative=True)
+    res = eng.run_fixed_precision(a, cfg, output="host")
+
+    def src(n, b, bid):
+        return _arr(eng.gen_sketch(spec, n, b, bid))
+    ref = port.run(a, eps=1e-2, power=power, block=20, kind=kind, p=p, seed=11, zeta=zeta, relative=True,
+                   source=src)
+    assert ref.status == 0 and res.converged
+    assert res.rank == ref.rank
+    _check_run(res, ref, power, f"kind={kind} zeta={zeta} P={power}")
+
+
+def test_qb_injected_block_source_matches_reference(reference, port):
+    """BlockSource plugin: host-supplied fixed-zeta blocks, identical on GPU and reference."""
+    a = _lowrank(900, 600, 1.0 / np.arange(1, 301), seed=5)
+
+    def src(n, b, bid):
+        return port.gen_sketch(4, 0.0, 3, n, b, bid, zeta=8)
+
+    for power in (0, 1, 2):
+        cfg = FarpcaConfig(eps=3e-2, power=power, block=32, sketch=SketchSpec(4, 0.0, 3, zeta=8), relative=True)
+        res = fqb.run_fixed_precision(a, cfg, source=src, output="host")
+        ref = reference.run(a, eps=3e-2, power=power, block=32, kind=4, seed=3, zeta=0, relative=True,
+                            source=src, traced=True)
+        assert ref.status == 0 and res.rank == ref.rank
+        _check_run(res, ref, power, f"injected P={power}")
+
+
+def test_c1_reference_matrix(reference):
+    """BASELINE config 1 exactly: gen_synthetic(SlowDecay, 2000, seed 42), Gaussian, b=20, P=1, eps=1e-2."""
+    a = reference.gen_synthetic(0, 2000, 42)
+    cfg = FarpcaConfig(eps=1e-2, power=1, block=20, sketch=SketchSpec(0, 0.0, 7), relative=True)
+    res = fqb.run_fixed_precision(a, cfg, output="host")
+    ref = reference.run(a, eps=1e-2, power=1, block=20, kind=0, seed=7, relative=True, traced=True)
+    assert res.rank == ref.rank == 20 and res.blocks == 1
+    _check_run(res, ref, 1, "C1")
+
+
+def test_redraw_ids_and_block_degenerate():
+    a = _lowrank(60, 60, np.ones(60), seed=1)
+
+    def make(bad_below):
+        def src(n, b, bid):
+            if bid < bad_below:
+                return fqb.SketchBlock(True, n, b, dense=np.ones((n, b), order="F"))
+            return fqb.SketchBlock(True, n, b, dense=np.asfortranarray(
+                np.random.default_rng(bid).standard_normal((n, b))))
+        return src
+    res = fqb.run_fixed_rank(a, 10, FarpcaConfig(block=10), source=make(1), output="host")
+    assert res.block_ids == [0, 1000] and res.rank == 10
+    with pytest.raises(fqb.BlockDegenerate):
+        fqb.run_fixed_rank(a, 10, FarpcaConfig(block=10), source=make(100000))
+
+
+def test_tolerance_not_reached_carries_partial(golden_mats):
+    a = golden_mats["slow128"]
+    cfg = FarpcaConfig(eps=1e-6, power=1, block=10, sketch=SketchSpec(0, 0.0, 77), max_iters=2, relative=True)
+    with pytest.raises(fqb.ToleranceNotReached) as ei:
+        fqb.run_fixed_precision(a, cfg, output="host")
+    part = ei.value.partial
+    assert part.blocks == 2 and part.rank == 20 and not part.converged
+    assert np.sqrt(part.residual_sq) > 1e-6 * np.sqrt(part.norm_a_sq)
+
+
+def test_config_errors():
+    a = np.asfortranarray(np.random.default_rng(0).standard_normal((30, 30)))
+    with pytest.raises(fqb.ConfigError):
+        fqb.run_fixed_rank(a, 10, FarpcaConfig(block=40))
+    with pytest.raises(fqb.ConfigError):
+        fqb.run_fixed_rank(a, 0, FarpcaConfig(block=10))
+    with pytest.raises(fqb.ConfigError):
+        fqb.run_fixed_rank(a, 31, FarpcaConfig(block=10))
+    with pytest.raises(fqb.ConfigError):
+        fqb.run_fixed_rank(a, 10, FarpcaConfig(block=10, power=-1))
+    with pytest.raises(fqb.ConfigError):
+        fqb.run_fixed_precision(a, FarpcaConfig(block=10))
+    with pytest.raises(fqb.ConfigError):
+        fqb.run_fixed_precision(a, FarpcaConfig(eps=0.1, block=10, sketch=SketchSpec(1, 0.1, 1, zeta=4)))
+
+
+def test_deterministic_and_device_input_identical():
+    a = _lowrank(1500, 900, 10.0 ** (-np.arange(900) / 100), seed=9)   # full rank, eps reachable
+    cfg = FarpcaConfig(eps=1e-3, power=2, block=32, sketch=SketchSpec(3, 0.0, 5, zeta=8), relative=True)
+    r1 = fqb.run_fixed_precision(a, cfg, output="host")
+    r2 = fqb.run_fixed_precision(a, cfg, output="host")
+    ad = torch.from_numpy(a).cuda().t().contiguous().t()
+    r3 = fqb.run_fixed_precision(ad, cfg, output="device")
+    assert r1.residual_sq == r2.residual_sq == r3.residual_sq
+    assert np.array_equal(r1.q, r2.q) and np.array_equal(r1.bt, r2.bt)
+    assert np.array_equal(r1.q, r3.q.cpu().numpy())
+
+
+def test_indicator_equals_true_residual():
+    """E = ||A||^2 - ||Q'A||^2 = ||A - QB||^2 (test_driver.cpp:77-92, acceptance C4)."""
+    a = _lowrank(2500, 1800, 10.0 ** (-np.arange(600) / 100), seed=4)
+    for kind, zeta, p in ((0, 0, 0.0), (2, 0, 0.5), (3, 8, 0.0), (4, 8, 0.0)):
+        cfg = FarpcaConfig(eps=1e-4, power=1, block=40, sketch=SketchSpec(kind, p, 1, zeta=zeta), relative=True)
+        res = fqb.run_fixed_precision(a, cfg, output="host")
+        true = np.linalg.norm(a - res.q @ res.bt.T) ** 2
+        assert abs(res.residual_sq - true) <= 1e-10 * res.norm_a_sq
+        assert np.all(np.diff(res.block_residuals) <= 1e-12 * res.norm_a_sq)
