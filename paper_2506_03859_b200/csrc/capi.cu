@@ -115,6 +115,7 @@ fqb_status fqb_destroy(fqb_handle h) {
             w.zc.release(); w.rowsum_b.release(); w.splitk.release(); w.partial.release();
             w.scalars.release(); w.scratch.release(); w.a_copy.release(); w.col_ptr.release();
             w.row_idx.release(); w.counts.release(); w.values.release(); w.status.release();
+            w.gemm_flags.release();
         }
         cudaStreamSynchronize(h->h.stream);
         cudaFreeHost(h->h.host_status);
@@ -345,10 +346,9 @@ fqb_status fqb_gemm(fqb_handle h, int trans_a, int64_t m, int64_t n, int64_t k, 
         if (m < 0 || n < 0 || k < 0) throw farqb::Error(FQB_ERR_DIMENSION, "negative dimension");
         if (ldc < m || ldb < k || lda < (trans_a ? k : m)) throw farqb::Error(FQB_ERR_DIMENSION, "leading dimension too small");
         cudaStream_t s = h->h.stream;
-        const int64_t wd = int64_t(h->h.num_sms) * 256 * 128 + 16;
-        h->h.ws.splitk.ensure(size_t(wd), s);
-        farqb::gemm(trans_a != 0, m, n, k, alpha, a, lda, b, ldb, beta, c, ldc, h->h.ws.splitk.ptr, wd,
-                    h->h.num_sms, s, h->h.lc);
+        farqb::ensure_gemm_workspace(h->h);
+        farqb::gemm(trans_a != 0, m, n, k, alpha, a, lda, b, ldb, beta, c, ldc, h->h.gws, h->h.num_sms, s,
+                    h->h.lc);
         return FQB_OK;
     });
 }

@@ -22,6 +22,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -43,6 +44,23 @@ constexpr double kDenseThreshold = 1.0 / 32.0;  // density above which Omega is 
 enum ScalarSlot { kNormA = 0, kBNorm = 1, kDMax = 2, kAlpha = 3, kScalarCount = 8 };
 
 }  // namespace
+
+void ensure_gemm_workspace(Handle& h) {
+    const int64_t need = std::max<int64_t>(int64_t(h.num_sms) * 256 * 128 + 16, gemm_tma_workspace_doubles(h.num_sms));
+    if (h.ws.splitk.count < size_t(need)) {
+        h.ws.splitk.ensure(size_t(need), h.stream);
+        h.gws.work = h.ws.splitk.ptr;
+        h.gws.work_doubles = need;
+    }
+    if (!h.ws.gemm_flags.ptr) {
+        h.ws.gemm_flags.ensure(size_t(h.num_sms) + 16, h.stream);
+        FQB_CUDA(cudaMemsetAsync(h.ws.gemm_flags.ptr, 0, sizeof(unsigned) * (h.num_sms + 16), h.stream));
+        h.gws.flags = h.ws.gemm_flags.ptr;
+        h.gws.epoch = 0;
+    }
+    const char* env = std::getenv("FQB_GEMM_TMA");
+    h.gws.use_tma = !(env && env[0] == '0');
+}
 
 double default_density(int kind, int64_t n) {
     if (kind == kGaussian) return 0.0;
@@ -114,8 +132,7 @@ class QbRun {
         w.scratch.ensure(size_t(b) * (b + 1), s_);
         w.col_ptr.ensure(size_t(b) + 1, s_);
         w.counts.ensure(size_t(b), s_);
-        splitk_doubles_ = int64_t(h_.num_sms) * 256 * 128 + 16;
-        w.splitk.ensure(size_t(splitk_doubles_), s_);
+        ensure_gemm_workspace(h_);
         double* sm = w.small.ptr;
         S_ = sm;
         S2_ = sm + 1 * b * b;
@@ -209,8 +226,7 @@ class QbRun {
 
     void gemm_(bool ta, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
                const double* B, int64_t ldb, double beta, double* C, int64_t ldc) {
-        gemm(ta, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, h_.ws.splitk.ptr, splitk_doubles_,
-             h_.num_sms, s_, h_.lc);
+        gemm(ta, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, h_.gws, h_.num_sms, s_, h_.lc);
     }
 
     // ---- Omega ----------------------------------------------------------------
@@ -453,7 +469,6 @@ class QbRun {
     fqb_block_source_fn src_;
     void* user_;
     int64_t ldq_, ldbt_, ldo_;
-    int64_t splitk_doubles_ = 0;
     int64_t cap_ = 0, l_ = 0;
     int blocks_ = 0;
     double norm_a_sq_ = 0.0, trace_ = 0.0, diag_max_ = 0.0;

@@ -9,6 +9,7 @@
 
 #include "../../include/farqb.h"
 #include "common.cuh"
+#include "kernels.hpp"
 
 namespace farqb {
 
@@ -52,6 +53,7 @@ struct Workspace {
     DeviceArray<int> col_ptr, row_idx, counts;
     DeviceArray<double> values;
     DeviceArray<unsigned> status;
+    DeviceArray<unsigned> gemm_flags;
 };
 
 struct Handle {
@@ -61,6 +63,7 @@ struct Handle {
     cudaStream_t stream = nullptr;
     LaunchCounter lc;
     Workspace ws;
+    GemmWorkspace gws;                // views into ws.splitk / ws.gemm_flags
     unsigned* host_status = nullptr;  // pinned readback slot
     double* host_scalars = nullptr;   // pinned readback slots
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -70,6 +73,9 @@ struct ResolvedConfig {
     fqb_config cfg;
     int64_t m, n;
 };
+
+// Sizes the GEMM scratch (split-K partials, stream-K flags) on the handle.
+void ensure_gemm_workspace(Handle& h);
 
 // Runs the loop; fills `out` (status also returned).  Throws farqb::Error for
 // configuration / CUDA failures before any result exists.

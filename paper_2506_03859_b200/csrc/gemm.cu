@@ -340,8 +340,8 @@ int64_t gemm_workspace_doubles(int64_t m, int64_t n, int64_t k, int num_sms) {
 }
 
 void gemm(bool trans_a, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
-          const double* B, int64_t ldb, double beta, double* C, int64_t ldc, double* work,
-          int64_t work_doubles, int num_sms, cudaStream_t s, LaunchCounter& lc) {
+          const double* B, int64_t ldb, double beta, double* C, int64_t ldc, GemmWorkspace& ws,
+          int num_sms, cudaStream_t s, LaunchCounter& lc) {
     if (M <= 0 || N <= 0) return;
     if (K <= 0 || alpha == 0.0) {
         k_scale<<<unsigned(ceil_div(M * N, 256)), 256, 0, s>>>(C, M, N, ldc, beta);
@@ -349,6 +349,16 @@ void gemm(bool trans_a, int64_t M, int64_t N, int64_t K, double alpha, const dou
         lc.bump();
         return;
     }
+    if (ws.use_tma && ws.flags && gemm_tma_supported(trans_a, M, N, K, lda, ldb, A, B, num_sms) &&
+        ws.work_doubles >= gemm_tma_workspace_doubles(num_sms)) {
+        if (++ws.epoch == 0) ws.epoch = 1;
+        gemm_tma(trans_a, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ws.work, ws.flags, ws.epoch, num_sms, s,
+                 false);
+        lc.bump();
+        return;
+    }
+    double* work = ws.work;
+    const int64_t work_doubles = ws.work_doubles;
     const bool vec2 = (lda % 2 == 0) && (ldb % 2 == 0) && (reinterpret_cast<uintptr_t>(A) % 16 == 0) &&
                       (reinterpret_cast<uintptr_t>(B) % 16 == 0);
     Plan pl = make_plan(trans_a, vec2, M, N, K, num_sms);

@@ -75,10 +75,29 @@ void launch_colsum(const double* x, int64_t rows, int k, int64_t ld, double* col
 // ---- gemm.cu -----------------------------------------------------------------
 // C (m x n) = alpha op(A) B + beta C, column-major; DMMA (mma.sync f64) tensor
 // pipe, deterministic split-K.  `work` must hold gemm_workspace_doubles(...).
+// Split-K / stream-K scratch: `work` doubles of partials plus `flags` (num_sms
+// unsigned, zero-initialised once) and a per-stream epoch for the stream-K fixup.
+struct GemmWorkspace {
+    double* work = nullptr;
+    int64_t work_doubles = 0;
+    unsigned* flags = nullptr;
+    unsigned epoch = 0;
+    bool use_tma = true;
+};
 int64_t gemm_workspace_doubles(int64_t m, int64_t n, int64_t k, int num_sms);
 void gemm(bool trans_a, int64_t m, int64_t n, int64_t k, double alpha, const double* a, int64_t lda,
-          const double* b, int64_t ldb, double beta, double* c, int64_t ldc, double* work,
-          int64_t work_doubles, int num_sms, cudaStream_t s, LaunchCounter& lc);
+          const double* b, int64_t ldb, double beta, double* c, int64_t ldc, GemmWorkspace& ws,
+          int num_sms, cudaStream_t s, LaunchCounter& lc);
+// gemm_tma.cu: TMA + mbarrier + stream-K variant (used by gemm() when the
+// operands have even leading dimensions and 16-byte aligned bases)
+int64_t gemm_tma_workspace_doubles(int num_sms);
+bool gemm_tma_supported(bool trans_a, int64_t M, int64_t N, int64_t K, int64_t lda, int64_t ldb, const double* A,
+                        const double* B, int num_sms);
+// a3d_slack: the caller guarantees 16 readable doubles past the end of A
+// (engine-owned buffers), so the NN 3-D box may overrun the last row block.
+void gemm_tma(bool trans_a, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
+              const double* B, int64_t ldb, double beta, double* C, int64_t ldc, double* work, unsigned* flags,
+              unsigned epoch, int num_sms, cudaStream_t s, bool a3d_slack = false);
 
 // ---- smallla.cu --------------------------------------------------------------
 // Cholesky of the b x b SPD matrix S (ld = lds) with the reference pivot rule
