@@ -21,7 +21,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -155,12 +157,9 @@ class QbRun {
     void setup() {
         FQB_CUDA(cudaMemsetAsync(scal_, 0, kScalarCount * sizeof(double), s_));
         launch_sumsq(a_, m_, n_, lda_, h_.ws.partial.ptr, scal_ + kNormA, s_, h_.lc);
-        if (cfg_.sketch.kind == kStdBernoulli) {
-            h_.ws.zc.ensure(size_t(m_), s_);
-            launch_centering(a_, m_, n_, lda_, cfg_.sketch.p, h_.ws.zc.ptr, s_, h_.lc);
-            have_z_ = true;
-            need_rowsum_ = true;
-        }
+        // z = A (p 1_n) exists when the reference would build it (driver.cpp:364-365);
+        // it is only computed once a sparse centered block actually needs it.
+        z_allowed_ = cfg_.sketch.kind == kStdBernoulli;
         FQB_CUDA(cudaMemcpyAsync(h_.host_scalars, scal_ + kNormA, sizeof(double), cudaMemcpyDeviceToHost, s_));
         FQB_CUDA(cudaStreamSynchronize(s_));
         norm_a_sq_ = h_.host_scalars[0];
@@ -216,7 +215,7 @@ class QbRun {
         };
         regrow(q_, ldq_);
         regrow(bt_, ldbt_);
-        if (need_rowsum_) regrow(rowsum_, 1);
+        if (z_allowed_) regrow(rowsum_, 1);
         cap_ = nc;
         Workspace& w = h_.ws;
         w.t.ensure(size_t(nc) * b_, s_);
@@ -314,9 +313,24 @@ class QbRun {
             om_shift_folded_ = true;
         } else {
             om_dense_ = false;
-            if (om_centered_ && !have_z_)
-                throw Error(kStatusDimension, "centered_product: stale centering column");
+            if (om_centered_) ensure_centering();
         }
+    }
+
+    void ensure_centering() {
+        if (!z_allowed_) throw Error(kStatusDimension, "centered_product: stale centering column");
+        if (!have_z_) {
+            h_.ws.zc.ensure(size_t(m_), s_);
+            launch_centering(a_, m_, n_, lda_, cfg_.sketch.p, h_.ws.zc.ptr, s_, h_.lc);
+            have_z_ = true;
+        }
+        // B row sums for the centered deflation term, for every accepted column
+        if (rowsum_cols_ < l_) {
+            launch_colsum(bt_.ptr + rowsum_cols_ * ldbt_, n_, int(l_ - rowsum_cols_), ldbt_, rowsum_.ptr + rowsum_cols_,
+                          s_, h_.lc);
+            rowsum_cols_ = l_;
+        }
+        need_rowsum_ = true;
     }
 
     // Y (m x b, ldy) = A * Omega  [centered]   (apply_block, driver.cpp:21-26)
@@ -425,7 +439,10 @@ class QbRun {
         }
         gemm_(false, n_, b, b, 1.0, w.wraw.ptr, ldbt_, Ri_, b, 0.0, btj, ldbt_);  // B_j'
         launch_sumsq(btj, n_, b, ldbt_, w.partial.ptr, scal_ + kBNorm, s_, h_.lc);
-        if (need_rowsum_) launch_colsum(btj, n_, b, ldbt_, rowsum_.ptr + l, s_, h_.lc);
+        if (need_rowsum_ && rowsum_cols_ == l) {
+            launch_colsum(btj, n_, b, ldbt_, rowsum_.ptr + l, s_, h_.lc);
+            pending_rowsum_ = true;
+        }
     }
 
     // One attempt; returns 0 when accepted, the degenerate status bits otherwise.
@@ -433,13 +450,16 @@ class QbRun {
         grow(l_ + b_);
         bool eig_mode = false;
         for (int pass = 0; pass < 2; ++pass) {
+            pending_rowsum_ = false;
             FQB_CUDA(cudaMemsetAsync(status_, 0, sizeof(unsigned), s_));
             make_block(id);
             if (cfg_.power >= 1) power_iterate(eig_mode);
             accept(cfg_.power >= 1);
             FQB_CUDA(cudaMemcpyAsync(h_.host_status, status_, sizeof(unsigned), cudaMemcpyDeviceToHost, s_));
             FQB_CUDA(cudaMemcpyAsync(h_.host_scalars, scal_, 4 * sizeof(double), cudaMemcpyDeviceToHost, s_));
+            const auto tw0 = std::chrono::steady_clock::now();
             FQB_CUDA(cudaStreamSynchronize(s_));
+            host_wait_s_ += std::chrono::duration<double>(std::chrono::steady_clock::now() - tw0).count();
             const unsigned st = *h_.host_status;
             if (st & kGenZeroGaussian)
                 throw Error(kStatusConvergence, "a Gaussian draw hit an exact zero (reference would redraw)");
@@ -453,6 +473,8 @@ class QbRun {
             trace_ += h_.host_scalars[kBNorm];
             diag_max_ = h_.host_scalars[kDMax];
             l_ += b_;
+            if (pending_rowsum_) rowsum_cols_ = l_;
+            pending_rowsum_ = false;
             ++blocks_;
             residuals_.push_back(residual());
             return 0;
@@ -472,7 +494,10 @@ class QbRun {
     int64_t cap_ = 0, l_ = 0;
     int blocks_ = 0;
     double norm_a_sq_ = 0.0, trace_ = 0.0, diag_max_ = 0.0;
-    bool have_z_ = false, need_rowsum_ = false;
+    bool have_z_ = false, need_rowsum_ = false, z_allowed_ = false, pending_rowsum_ = false;
+    int64_t rowsum_cols_ = 0;  // B' columns whose row sums are in rowsum_
+  public:
+    double host_wait_s_ = 0.0;  // time the host spent blocked on the device (FQB_HOST_STATS)
     bool om_dense_ = true, om_centered_ = false, om_shift_folded_ = false;
     double om_p_ = 0.0;
     DeviceArray<double> q_, bt_, rowsum_;
@@ -519,6 +544,7 @@ int run_qb(Handle& h, const double* a, int64_t m, int64_t n, int64_t lda, bool a
         ad = h.ws.a_copy.ptr;
     }
 
+    const auto t_host0 = std::chrono::steady_clock::now();
     QbRun run(h, ad, m, n, ldad, cfg, src, user);
     run.setup();
     int status = 0;
@@ -594,6 +620,11 @@ int run_qb(Handle& h, const double* a, int64_t m, int64_t n, int64_t lda, bool a
     if (!ids.empty()) std::memcpy(out->block_ids, ids.data(), sizeof(int) * ids.size());
     out->n_ids = int(ids.size());
     out->gpu_launches = int(h.lc.total - launches0);
+    if (const char* e = std::getenv("FQB_HOST_STATS"); e && e[0] == '1') {
+        const double tot = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_host0).count();
+        std::fprintf(stderr, "[farqb] host %.3f ms, blocked on device %.3f ms, device %.3f ms, launches %d\n",
+                     tot * 1e3, run.host_wait_s_ * 1e3, double(ms), out->gpu_launches);
+    }
     if (message_out) *message_out = message;
     return status;
 }

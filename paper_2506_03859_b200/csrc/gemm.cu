@@ -254,12 +254,8 @@ __global__ void k_scale(double* C, int64_t M, int64_t N, int64_t ldc, double bet
 
 using KernelFn = void (*)(const GemmArgs);
 
-template <bool TRANS_A, int NT, int VEC>
-constexpr int wm_for() { return NT <= 8 ? 32 : 16; }
-
-template <bool TRANS_A, int NT, int VEC>
+template <bool TRANS_A, int NT, int WM, int VEC>
 KernelFn kernel_for(size_t& smem, int& bm, int& bn) {
-    constexpr int WM = wm_for<TRANS_A, NT, VEC>();
     using C = Cfg<TRANS_A, NT, WM, VEC>;
     smem = C::SMEM;
     bm = C::BM;
@@ -275,25 +271,35 @@ KernelFn kernel_for(size_t& smem, int& bm, int& bn) {
     return k_gemm<TRANS_A, NT, WM, VEC>;
 }
 
+// WM = rows per warp (8, 16 or 32; 32 only while the accumulators fit, NT <= 8)
+template <bool TRANS_A, int NT>
+KernelFn pick_wm(int wm, size_t& smem, int& bm, int& bn) {
+    if constexpr (NT <= 8) {
+        if (wm >= 32) return kernel_for<TRANS_A, NT, 32, 2>(smem, bm, bn);
+    }
+    if (wm >= 16) return kernel_for<TRANS_A, NT, 16, 2>(smem, bm, bn);
+    return kernel_for<TRANS_A, NT, 8, 2>(smem, bm, bn);
+}
+
 template <bool TRANS_A>
-KernelFn pick_vec2(int nt, size_t& smem, int& bm, int& bn) {
+KernelFn pick_vec2(int nt, int wm, size_t& smem, int& bm, int& bn) {
     switch (nt) {
-        case 1: return kernel_for<TRANS_A, 1, 2>(smem, bm, bn);
-        case 2: return kernel_for<TRANS_A, 2, 2>(smem, bm, bn);
-        case 3: return kernel_for<TRANS_A, 3, 2>(smem, bm, bn);
-        case 4: return kernel_for<TRANS_A, 4, 2>(smem, bm, bn);
-        case 5: return kernel_for<TRANS_A, 5, 2>(smem, bm, bn);
-        case 6: return kernel_for<TRANS_A, 6, 2>(smem, bm, bn);
-        case 7: return kernel_for<TRANS_A, 7, 2>(smem, bm, bn);
-        case 8: return kernel_for<TRANS_A, 8, 2>(smem, bm, bn);
-        case 9: return kernel_for<TRANS_A, 9, 2>(smem, bm, bn);
-        case 10: return kernel_for<TRANS_A, 10, 2>(smem, bm, bn);
-        case 11: return kernel_for<TRANS_A, 11, 2>(smem, bm, bn);
-        case 12: return kernel_for<TRANS_A, 12, 2>(smem, bm, bn);
-        case 13: return kernel_for<TRANS_A, 13, 2>(smem, bm, bn);
-        case 14: return kernel_for<TRANS_A, 14, 2>(smem, bm, bn);
-        case 15: return kernel_for<TRANS_A, 15, 2>(smem, bm, bn);
-        default: return kernel_for<TRANS_A, 16, 2>(smem, bm, bn);
+        case 1: return pick_wm<TRANS_A, 1>(wm, smem, bm, bn);
+        case 2: return pick_wm<TRANS_A, 2>(wm, smem, bm, bn);
+        case 3: return pick_wm<TRANS_A, 3>(wm, smem, bm, bn);
+        case 4: return pick_wm<TRANS_A, 4>(wm, smem, bm, bn);
+        case 5: return pick_wm<TRANS_A, 5>(wm, smem, bm, bn);
+        case 6: return pick_wm<TRANS_A, 6>(wm, smem, bm, bn);
+        case 7: return pick_wm<TRANS_A, 7>(wm, smem, bm, bn);
+        case 8: return pick_wm<TRANS_A, 8>(wm, smem, bm, bn);
+        case 9: return pick_wm<TRANS_A, 9>(wm, smem, bm, bn);
+        case 10: return pick_wm<TRANS_A, 10>(wm, smem, bm, bn);
+        case 11: return pick_wm<TRANS_A, 11>(wm, smem, bm, bn);
+        case 12: return pick_wm<TRANS_A, 12>(wm, smem, bm, bn);
+        case 13: return pick_wm<TRANS_A, 13>(wm, smem, bm, bn);
+        case 14: return pick_wm<TRANS_A, 14>(wm, smem, bm, bn);
+        case 15: return pick_wm<TRANS_A, 15>(wm, smem, bm, bn);
+        default: return pick_wm<TRANS_A, 16>(wm, smem, bm, bn);
     }
 }
 
@@ -309,11 +315,15 @@ struct Plan {
 Plan make_plan(bool trans_a, bool vec2, int64_t M, int64_t N, int64_t K, int num_sms) {
     Plan pl{};
     const int nt = int(std::min<int64_t>(16, ceil_div(std::max<int64_t>(N, 1), 8)));
+    // the largest warp tile that still yields half a wave of CTAs without split-K
+    int wm = nt <= 8 ? 32 : 16;
+    while (wm > 8 && ceil_div(M, int64_t(wm) * WARPS) * ceil_div(N, 8 * nt) < num_sms / 2) wm /= 2;
     if (vec2) {
-        pl.fn = trans_a ? pick_vec2<true>(nt, pl.smem, pl.bm, pl.bn) : pick_vec2<false>(nt, pl.smem, pl.bm, pl.bn);
+        pl.fn = trans_a ? pick_vec2<true>(nt, wm, pl.smem, pl.bm, pl.bn)
+                        : pick_vec2<false>(nt, wm, pl.smem, pl.bm, pl.bn);
     } else {
-        pl.fn = trans_a ? kernel_for<true, 16, 1>(pl.smem, pl.bm, pl.bn)
-                        : kernel_for<false, 16, 1>(pl.smem, pl.bm, pl.bn);
+        pl.fn = trans_a ? kernel_for<true, 16, 16, 1>(pl.smem, pl.bm, pl.bn)
+                        : kernel_for<false, 16, 16, 1>(pl.smem, pl.bm, pl.bn);
     }
     pl.mt = ceil_div(M, pl.bm);
     pl.nt_tiles = ceil_div(N, pl.bn);
@@ -322,7 +332,7 @@ Plan make_plan(bool trans_a, bool vec2, int64_t M, int64_t N, int64_t K, int num
     int64_t splits = 1;
     if (tiles < num_sms) {
         splits = std::max<int64_t>(1, num_sms / tiles);
-        splits = std::min<int64_t>(splits, std::max<int64_t>(1, ktiles / 8));
+        splits = std::min<int64_t>(splits, std::max<int64_t>(1, ktiles / 4));
     }
     pl.splits = int(splits);
     pl.kchunk = ceil_div(ktiles, splits) * BK;

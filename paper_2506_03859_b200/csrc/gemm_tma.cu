@@ -447,7 +447,9 @@ bool gemm_tma_supported(bool trans_a, int64_t M, int64_t N, int64_t K, int64_t l
     const int64_t iters = tiles * ceil_div(K, BK);
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(num_sms, iters / 8));
     (void)trans_a;
-    return grid <= 6 * tiles;
+    // enough k-tiles per CTA to keep the TMA ring busy, and at most ~8 segments
+    // per tile for the serial fixup; otherwise the split-K kernel is faster.
+    return iters >= 16 * int64_t(num_sms) && grid <= 8 * tiles;
 }
 
 void gemm_tma(bool trans_a, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,

@@ -14,6 +14,7 @@
 //  * fixed zeta (new): one thread per column, same rule as the oracle
 //    (oracle/farqb_oracle.c fqo_gen_sketch): rows r = (u32 * n) >> 32 with
 //    duplicates skipped, then one sign bit / Gaussian per row, sorted by row.
+#include <cmath>
 #include <cstdint>
 
 #include "kernels.hpp"
@@ -113,6 +114,66 @@ __global__ void __launch_bounds__(256) k_iid_walk(int kind, PhiloxKey key, uint3
         }
         row = __shfl_sync(0xffffffffu, r, 31);
         t_base += 32;
+    }
+}
+
+// One CTA (1024 threads) per column for dense patterns (n p >> 32): 1024
+// candidate gaps per round, block-wide prefix sum, first invalid candidate found
+// with a block min.  Same draws and the same rows as k_iid_walk.
+template <int MODE>
+__global__ void __launch_bounds__(1024) k_iid_walk_cta(int kind, PhiloxKey key, uint32_t blk, int64_t n,
+                                                       double denom, double scale, double shift, int* counts,
+                                                       const int* col_ptr, int* row_idx, double* values,
+                                                       double* dense, int64_t ld, unsigned* status) {
+    __shared__ long long warp_tot[32];
+    __shared__ int first_bad_s;
+    __shared__ long long row_s;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int col = blockIdx.x;
+    long long row = -1;
+    uint64_t t_base = 0;
+    const int base_out = MODE == kFillCsc ? col_ptr[col] : 0;
+    const double nd = double(n);
+    for (;;) {
+        const uint64_t t = t_base + tid;
+        const double u = stream_unit(key, blk, uint32_t(col), gap_unit(kind, t));
+        const double ratio = log(u) / denom;
+        const bool stop = ratio >= nd;
+        const long long gap = stop ? (long long)n : 1 + (long long)ratio;
+        long long x = warp_incl_scan(gap, lane);
+        if (lane == 31) warp_tot[warp] = x;
+        if (tid == 0) first_bad_s = 1024;
+        __syncthreads();
+        if (warp == 0) {
+            long long w = warp_tot[lane];
+            w = warp_incl_scan(w, lane);
+            warp_tot[lane] = w;
+        }
+        __syncthreads();
+        const long long r = row + x + (warp > 0 ? warp_tot[warp - 1] : 0);
+        const bool bad = stop || r >= n;
+        if (bad) atomicMin(&first_bad_s, tid);
+        __syncthreads();
+        const int first_bad = first_bad_s;
+        if (tid < first_bad && MODE != kCount) {
+            double v;
+            if (!nonzero_value(kind, key, blk, uint32_t(col), t, scale, v)) atomicOr(status, kGenZeroGaussian);
+            if (MODE == kFillCsc) {
+                row_idx[base_out + t] = int(r);
+                values[base_out + t] = v;
+            } else {
+                dense[int64_t(col) * ld + r] = v - shift;
+            }
+        }
+        if (first_bad < 1024) {
+            if (MODE == kCount && tid == 0) counts[col] = int(t_base + first_bad);
+            return;
+        }
+        if (tid == 1023) row_s = r;
+        __syncthreads();
+        row = row_s;
+        t_base += 1024;
+        __syncthreads();
     }
 }
 
@@ -257,8 +318,19 @@ void launch_gaussian_dense(uint64_t seed, int block_id, int64_t n, int l, double
     lc.bump();
 }
 
+// expected nonzeros per column from the walk's own constant denom = log1p(-p)
+static bool dense_columns(int64_t n, double denom) { return double(n) * -std::expm1(denom) > 256.0; }
+
 void launch_iid_count(int kind, uint64_t seed, int block_id, int64_t n, int l, double denom,
                       int* counts, cudaStream_t s, LaunchCounter& lc) {
+    if (dense_columns(n, denom)) {
+        k_iid_walk_cta<kCount><<<unsigned(l), 1024, 0, s>>>(kind, philox_key(seed), uint32_t(block_id), n, denom,
+                                                          0.0, 0.0, counts, nullptr, nullptr, nullptr, nullptr, 0,
+                                                          nullptr);
+        FQB_LAUNCHED();
+        lc.bump();
+        return;
+    }
     k_iid_walk<kCount><<<unsigned(ceil_div(l, 8)), 256, 0, s>>>(
         kind, philox_key(seed), uint32_t(block_id), n, l, denom, 0.0, 0.0, counts, nullptr, nullptr,
         nullptr, nullptr, 0, nullptr);
@@ -269,6 +341,14 @@ void launch_iid_count(int kind, uint64_t seed, int block_id, int64_t n, int l, d
 void launch_iid_fill_csc(int kind, uint64_t seed, int block_id, int64_t n, int l, double denom,
                          double scale, const int* col_ptr, int* row_idx, double* values,
                          unsigned* status, cudaStream_t s, LaunchCounter& lc) {
+    if (dense_columns(n, denom)) {
+        k_iid_walk_cta<kFillCsc><<<unsigned(l), 1024, 0, s>>>(kind, philox_key(seed), uint32_t(block_id), n, denom,
+                                                            scale, 0.0, nullptr, col_ptr, row_idx, values, nullptr,
+                                                            0, status);
+        FQB_LAUNCHED();
+        lc.bump();
+        return;
+    }
     k_iid_walk<kFillCsc><<<unsigned(ceil_div(l, 8)), 256, 0, s>>>(
         kind, philox_key(seed), uint32_t(block_id), n, l, denom, scale, 0.0, nullptr, col_ptr,
         row_idx, values, nullptr, 0, status);
@@ -282,6 +362,14 @@ void launch_iid_fill_dense(int kind, uint64_t seed, int block_id, int64_t n, int
     dim3 g0(unsigned(ceil_div(n, 256)), unsigned(l));
     k_fill_const<<<g0, 256, 0, s>>>(out, n, l, ld, -shift);
     FQB_LAUNCHED();
+    if (dense_columns(n, denom)) {
+        k_iid_walk_cta<kFillDense><<<unsigned(l), 1024, 0, s>>>(kind, philox_key(seed), uint32_t(block_id), n,
+                                                              denom, scale, shift, nullptr, nullptr, nullptr,
+                                                              nullptr, out, ld, status);
+        FQB_LAUNCHED();
+        lc.bump(2);
+        return;
+    }
     k_iid_walk<kFillDense><<<unsigned(ceil_div(l, 8)), 256, 0, s>>>(
         kind, philox_key(seed), uint32_t(block_id), n, l, denom, scale, shift, nullptr, nullptr,
         nullptr, nullptr, out, ld, status);

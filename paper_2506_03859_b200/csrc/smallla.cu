@@ -59,25 +59,28 @@ __device__ __forceinline__ double block_reduce_sum(double v, double* sh) {
     return r;
 }
 
-// M is b x b row-major with pitch ld (shared memory for b <= 128, else global scratch)
-__global__ void __launch_bounds__(kCholThreads) k_chol_inv(const double* __restrict__ S, int b, int64_t lds,
-                                                          double tol, double diag_ref,
-                                                          const double* __restrict__ dref_extra,
-                                                          int64_t ld_extra, double* __restrict__ R,
-                                                          double* __restrict__ Rinv,
-                                                          double* __restrict__ max_diag_out,
-                                                          unsigned* status, unsigned fail_bit,
-                                                          double* gscratch) {
+// M is b x b row-major with pitch ld (shared memory for b <= 128, else global
+// scratch).  Warp w eliminates rows i = j+1+w, j+1+w+nwarps, ... of step j, lanes
+// sweep the columns, so a step needs a single __syncthreads (row j+1 must be
+// final before it becomes the next pivot row).
+__global__ void __launch_bounds__(1024) k_chol_inv(const double* __restrict__ S, int b, int64_t lds,
+                                                   double tol, double diag_ref,
+                                                   const double* __restrict__ dref_extra,
+                                                   int64_t ld_extra, double* __restrict__ R,
+                                                   double* __restrict__ Rinv,
+                                                   double* __restrict__ max_diag_out,
+                                                   unsigned* status, unsigned fail_bit,
+                                                   double* gscratch) {
     extern __shared__ double smem[];
-    __shared__ double fvec[1024];
     __shared__ double red[32];
-    __shared__ int failed;
+    __shared__ double sd[1024];
     const int ld = b + 1;
     double* M = b <= kSmemMaxB ? smem : gscratch;
     const int tid = threadIdx.x, nt = blockDim.x;
+    const int warp = tid >> 5, lane = tid & 31, nwarps = nt >> 5;
     for (int e = tid; e < b * b; e += nt) {
-        const int i = e / b, c = e - i * b;
-        M[i * ld + c] = S[int64_t(c) * lds + i];  // column-major -> row-major (symmetric anyway)
+        const int c = e / b, i = e - c * b;
+        M[i * ld + c] = S[int64_t(c) * lds + i];
     }
     // pivot reference (matrix_core.cpp:121-123, driver.cpp:270-275)
     double local = 0.0;
@@ -86,31 +89,28 @@ __global__ void __launch_bounds__(kCholThreads) k_chol_inv(const double* __restr
     } else if (!(diag_ref > 0.0)) {
         for (int i = tid; i < b; i += nt) local = fmax(local, S[int64_t(i) * lds + i]);
     }
-    if (tid == 0) failed = 0;
-    double max_diag = block_reduce_max(local, red);
+    double max_diag = block_reduce_max(local, red);  // contains __syncthreads
     if (dref_extra) max_diag = fmax(max_diag, diag_ref);
     else if (diag_ref > 0.0) max_diag = diag_ref;
     const double thresh = tol * max_diag;
     if (tid == 0 && max_diag_out) *max_diag_out = max_diag;
-    __syncthreads();
 
+    bool failed = false;
     for (int j = 0; j < b; ++j) {
+        __syncthreads();
         const double d = M[j * ld + j];
-        if (!(d > thresh)) {
-            if (tid == 0) failed = 1;
-            break;  // uniform: every thread reads the same d
+        if (!(d > thresh)) {  // uniform: every thread reads the same pivot
+            failed = true;
+            break;
         }
         const double invd = 1.0 / d;
-        for (int i = j + 1 + tid; i < b; i += nt) fvec[i] = M[i * ld + j] * invd;
-        __syncthreads();
-        const int rows = b - j - 1;
-        for (int e = tid; e < rows * b; e += nt) {
-            const int i = j + 1 + e / b, c = e % b;
-            const double f = fvec[i];
-            if (c == j) M[i * ld + c] = -f;
-            else M[i * ld + c] = fma(-f, M[j * ld + c], M[i * ld + c]);
+        const double* pivot_row = M + j * ld;
+        for (int i = j + 1 + warp; i < b; i += nwarps) {
+            double* row = M + i * ld;
+            const double f = row[j] * invd;
+            __syncwarp();
+            for (int c = lane; c < b; c += 32) row[c] = c == j ? -f : fma(-f, pivot_row[c], row[c]);
         }
-        __syncthreads();
     }
     __syncthreads();
     if (failed) {
@@ -122,14 +122,107 @@ __global__ void __launch_bounds__(kCholThreads) k_chol_inv(const double* __restr
         }
         return;
     }
-    // R (col-major b x b): R[r, c] = U[r][c] / sqrt(d_r) for c >= r
-    // Rinv[k, j] = M[j][k] / sqrt(d_j) for k < j, 1/sqrt(d_j) on the diagonal
+    for (int i = tid; i < b; i += nt) sd[i] = sqrt(M[i * ld + i]);
+    __syncthreads();
+    // R[r, c] = U[r][c] / sqrt(d_r) (c >= r);  Rinv[k, j] = M[j][k] / sqrt(d_j) (k < j)
     for (int e = tid; e < b * b; e += nt) {
         const int r = e % b, c = e / b;
-        const double sr = sqrt(M[r * ld + r]);
-        R[e] = c >= r ? M[r * ld + c] / sr : 0.0;
-        const double sc = sqrt(M[c * ld + c]);
-        Rinv[e] = r < c ? M[c * ld + r] / sc : (r == c ? 1.0 / sc : 0.0);
+        R[e] = c >= r ? M[r * ld + c] / sd[r] : 0.0;
+        Rinv[e] = r < c ? M[c * ld + r] / sd[c] : (r == c ? 1.0 / sd[c] : 0.0);
+    }
+}
+
+// Register-resident variant for b <= 128: thread t owns column c = t % b and
+// rows rg, rg + 8, rg + 16, ... (rg = t / b), held in registers.  At step j the
+// owners of row j publish it to shared memory (by symmetry of the trailing
+// Schur complement it is also pivot column j), one barrier, then every thread
+// updates its rows: M[i][c] -= (M[j][i] / d) M[j][c]  (c != j),  M[i][j] = -f.
+// The published rows are double buffered, so each step costs one barrier.
+template <int MAXS>
+__global__ void __launch_bounds__(1024) k_chol_inv_reg(const double* __restrict__ S, int b, int64_t lds,
+                                                       double tol, double diag_ref,
+                                                       const double* __restrict__ dref_extra, int64_t ld_extra,
+                                                       double* __restrict__ R, double* __restrict__ Rinv,
+                                                       double* __restrict__ max_diag_out, unsigned* status,
+                                                       unsigned fail_bit) {
+    extern __shared__ double smem[];        // final M, b x (b+1), row-major
+    __shared__ double prow[2][kSmemMaxB];
+    __shared__ double red[32];
+    __shared__ double sd[kSmemMaxB];
+    constexpr int RG = 8;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int c = tid % b, rg = tid / b;
+    const bool active = tid < RG * b;
+    double v[MAXS];
+#pragma unroll
+    for (int s = 0; s < MAXS; ++s) {
+        const int i = rg + s * RG;
+        v[s] = (active && i < b) ? S[int64_t(c) * lds + i] : 0.0;   // M[i][c] = S[i][c]
+    }
+    double local = 0.0;
+    if (dref_extra) {
+        for (int i = tid; i < b; i += nt) local = fmax(local, dref_extra[int64_t(i) * ld_extra + i]);
+    } else if (!(diag_ref > 0.0)) {
+        for (int i = tid; i < b; i += nt) local = fmax(local, S[int64_t(i) * lds + i]);
+    }
+    double max_diag = block_reduce_max(local, red);
+    if (dref_extra) max_diag = fmax(max_diag, diag_ref);
+    else if (diag_ref > 0.0) max_diag = diag_ref;
+    const double thresh = tol * max_diag;
+    if (tid == 0 && max_diag_out) *max_diag_out = max_diag;
+
+    bool failed = false;
+    for (int j = 0; j < b; ++j) {
+        double* pr = prow[j & 1];
+        if (active && rg == (j % RG)) {
+            const int sj = j / RG;
+#pragma unroll
+            for (int s = 0; s < MAXS; ++s)
+                if (s == sj) pr[c] = v[s];
+        }
+        __syncthreads();
+        const double d = pr[j];
+        if (!(d > thresh)) {
+            failed = true;
+            break;
+        }
+        const double invd = 1.0 / d;
+        const double pc = pr[c];
+        if (active) {
+#pragma unroll
+            for (int s = 0; s < MAXS; ++s) {
+                const int i = rg + s * RG;
+                if (i > j && i < b) {
+                    const double f = pr[i] * invd;
+                    v[s] = c == j ? -f : fma(-f, pc, v[s]);
+                }
+            }
+        }
+    }
+    if (failed) {
+        if (tid == 0) atomicOr(status, fail_bit);
+        for (int e = tid; e < b * b; e += nt) {
+            const int r = e % b, cc = e / b;
+            R[e] = r == cc ? 1.0 : 0.0;
+            Rinv[e] = r == cc ? 1.0 : 0.0;
+        }
+        return;
+    }
+    const int ld = b + 1;
+    if (active) {
+#pragma unroll
+        for (int s = 0; s < MAXS; ++s) {
+            const int i = rg + s * RG;
+            if (i < b) smem[i * ld + c] = v[s];
+        }
+    }
+    __syncthreads();
+    for (int i = tid; i < b; i += nt) sd[i] = sqrt(smem[i * ld + i]);
+    __syncthreads();
+    for (int e = tid; e < b * b; e += nt) {
+        const int r = e % b, cc = e / b;
+        R[e] = cc >= r ? smem[r * ld + cc] / sd[r] : 0.0;
+        Rinv[e] = r < cc ? smem[cc * ld + r] / sd[cc] : (r == cc ? 1.0 / sd[cc] : 0.0);
     }
 }
 
@@ -329,12 +422,31 @@ void launch_chol_upper_inv(const double* S, int b, int64_t lds, double tol, doub
         int dev = 0;
         FQB_CUDA(cudaGetDevice(&dev));
         if (dev < 0 || dev >= 64 || !configured[dev]) {
-            FQB_CUDA(cudaFuncSetAttribute(k_chol_inv, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          int(size_t(kSmemMaxB) * (kSmemMaxB + 1) * sizeof(double))));
+            const int bytes = int(size_t(kSmemMaxB) * (kSmemMaxB + 1) * sizeof(double));
+            FQB_CUDA(cudaFuncSetAttribute(k_chol_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+            FQB_CUDA(cudaFuncSetAttribute(k_chol_inv_reg<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+            FQB_CUDA(cudaFuncSetAttribute(k_chol_inv_reg<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+            FQB_CUDA(cudaFuncSetAttribute(k_chol_inv_reg<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
             if (dev >= 0 && dev < 64) configured[dev] = true;
         }
     }
-    k_chol_inv<<<1, kCholThreads, smem, s>>>(S, b, lds, tol, diag_ref, dref_extra, ld_extra, R, Rinv,
+    if (b <= kSmemMaxB) {
+        const int threads = int(ceil_div(8 * b, 32) * 32);
+        if (b <= 32)
+            k_chol_inv_reg<4><<<1, threads, smem, s>>>(S, b, lds, tol, diag_ref, dref_extra, ld_extra, R, Rinv,
+                                                      max_diag_out, status, fail_bit);
+        else if (b <= 64)
+            k_chol_inv_reg<8><<<1, threads, smem, s>>>(S, b, lds, tol, diag_ref, dref_extra, ld_extra, R, Rinv,
+                                                      max_diag_out, status, fail_bit);
+        else
+            k_chol_inv_reg<16><<<1, threads, smem, s>>>(S, b, lds, tol, diag_ref, dref_extra, ld_extra, R, Rinv,
+                                                       max_diag_out, status, fail_bit);
+        FQB_LAUNCHED();
+        lc.bump();
+        return;
+    }
+    const int threads = 1024;
+    k_chol_inv<<<1, threads, smem, s>>>(S, b, lds, tol, diag_ref, dref_extra, ld_extra, R, Rinv,
                                              max_diag_out, status, fail_bit, scratch);
     FQB_LAUNCHED();
     lc.bump();
