@@ -162,6 +162,18 @@ fqb_status fqb_qb_fixed_rank(fqb_handle h, const double* a, int64_t m, int64_t n
                              fqb_qb_result* out);
 void fqb_result_free(fqb_qb_result* r);
 
+/* ---- row-sharded multi-GPU (one rank per GPU, NCCL over NVLink) ------------- */
+/* Rank 0 creates a 128-byte id, the caller distributes it (e.g. with
+ * torch.distributed or MPI), every rank attaches.  With a communicator attached,
+ * the `a, m, lda` passed to fqb_qb_* are this rank's contiguous row block of A;
+ * Q comes back as this rank's rows, B' (and every scalar) is replicated.  The
+ * sums over rows (||A||^2, A'Y and the Gram blocks) are NCCL all-reduces. */
+fqb_status fqb_comm_unique_id(void* out128);
+fqb_status fqb_comm_attach(fqb_handle h, const void* id128, int nranks, int rank);
+fqb_status fqb_comm_detach(fqb_handle h);
+/* collectives issued by this handle since creation */
+int64_t fqb_collective_count(fqb_handle h);
+
 /* ---- building blocks (device pointers unless stated) ------------------------ */
 /* First `count` u32 words of the Philox stream (seed, block_id, column), into
  * host memory; generated on the device. */

@@ -69,6 +69,10 @@ SIGNATURES = [
                                     C.POINTER(ConfigC), SOURCE_FN, C.c_void_p, C.c_uint,
                                     C.POINTER(ResultC)]),
     ("fqb_result_free", None, [C.POINTER(ResultC)]),
+    ("fqb_comm_unique_id", C.c_int, [C.c_void_p]),
+    ("fqb_comm_attach", C.c_int, [_H, C.c_void_p, C.c_int, C.c_int]),
+    ("fqb_comm_detach", C.c_int, [_H]),
+    ("fqb_collective_count", C.c_int64, [_H]),
     ("fqb_philox_u32", C.c_int, [_H, C.c_uint64, C.c_uint32, C.c_uint32, C.c_int, C.c_void_p]),
     ("fqb_gen_sketch", C.c_int, [_H, C.POINTER(SketchSpecC), C.c_int, C.c_int, C.c_int,
                                  C.POINTER(SketchHostC)]),

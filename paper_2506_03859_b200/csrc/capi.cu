@@ -108,6 +108,7 @@ fqb_status fqb_destroy(fqb_handle h) {
         if (!h) return FQB_OK;
         bind(h);
         cudaStreamSynchronize(h->h.stream);
+        farqb::comm_detach(h->h);
         {
             farqb::Workspace& w = h->h.ws;
             w.omega.release(); w.y0.release(); w.ys.release(); w.wp.release(); w.wraw.release();
@@ -145,6 +146,33 @@ fqb_status fqb_synchronize(fqb_handle h) {
 }
 
 int64_t fqb_launch_count(fqb_handle h) { return h ? h->h.lc.total : 0; }
+
+int64_t fqb_collective_count(fqb_handle h) { return h ? h->h.collectives : 0; }
+
+fqb_status fqb_comm_unique_id(void* out128) {
+    return guarded([&]() -> fqb_status {
+        if (!out128) throw farqb::Error(FQB_ERR_INVALID_ARGUMENT, "null id buffer");
+        farqb::comm_unique_id(out128);
+        return FQB_OK;
+    });
+}
+
+fqb_status fqb_comm_attach(fqb_handle h, const void* id128, int nranks, int rank) {
+    return guarded([&]() -> fqb_status {
+        bind(h);
+        if (!id128) throw farqb::Error(FQB_ERR_INVALID_ARGUMENT, "null id");
+        farqb::comm_attach(h->h, id128, nranks, rank);
+        return FQB_OK;
+    });
+}
+
+fqb_status fqb_comm_detach(fqb_handle h) {
+    return guarded([&]() -> fqb_status {
+        bind(h);
+        farqb::comm_detach(h->h);
+        return FQB_OK;
+    });
+}
 
 static fqb_status run_common(fqb_handle h, const double* a, int64_t m, int64_t n, int64_t lda,
                              int a_on_device, bool fixed_precision, int rank, const fqb_config* cfg,

@@ -157,6 +157,7 @@ class QbRun {
     void setup() {
         FQB_CUDA(cudaMemsetAsync(scal_, 0, kScalarCount * sizeof(double), s_));
         launch_sumsq(a_, m_, n_, lda_, h_.ws.partial.ptr, scal_ + kNormA, s_, h_.lc);
+        comm_allreduce_sum(h_, scal_ + kNormA, 1, s_);
         // z = A (p 1_n) exists when the reference would build it (driver.cpp:364-365);
         // it is only computed once a sparse centered block actually needs it.
         z_allowed_ = cfg_.sketch.kind == kStdBernoulli;
@@ -387,6 +388,7 @@ class QbRun {
             if (k == 1) apply_omega(w.y0.ptr, ldq_);
             else gemm_(false, m_, b_, n_, 1.0, a_, lda_, w.g.ptr, ldbt_, 0.0, w.y0.ptr, ldq_);
             gemm_(true, n_, b_, m_, 1.0, a_, lda_, w.y0.ptr, ldq_, 0.0, w.wp.ptr, ldbt_);
+            comm_allreduce_sum(h_, w.wp.ptr, size_t(ldbt_) * b_, s_);   // W = sum_g A_g' Y_g
             if (l_ > 0) {
                 if (k == 1) tmul_omega(w.t.ptr, l_);
                 else gemm_(true, l_, b_, n_, 1.0, bt_.ptr, ldbt_, w.g.ptr, ldbt_, 0.0, w.t.ptr, l_);
@@ -410,10 +412,12 @@ class QbRun {
         if (from_iterate) gemm_(false, m_, b, n_, 1.0, a_, lda_, w.g.ptr, ldbt_, 0.0, yj, ldq_);
         else apply_omega(yj, ldq_);
         gemm_(true, n_, b, m_, 1.0, a_, lda_, yj, ldq_, 0.0, w.wraw.ptr, ldbt_);
+        comm_allreduce_sum(h_, w.wraw.ptr, size_t(ldbt_) * b, s_);
         const int64_t ldcd = l + b;
         double* cd = w.cd.ptr;
         // [C1; D] = [Q_old | Y_j]' Y_j
         gemm_(true, l + b, b, m_, 1.0, q_.ptr, ldq_, yj, ldq_, 0.0, cd, ldcd);
+        comm_allreduce_sum(h_, cd, size_t(ldcd) * b, s_);
         double* dblk = cd + l;  // rows l..l+b-1, ld = l+b
         if (l == 0) {
             launch_chol_upper_inv(dblk, b, ldcd, 1e-12, 0.0, dblk, ldcd, R1_, R1i_, scal_ + kDMax,
@@ -422,13 +426,16 @@ class QbRun {
         } else {
             gemm_(false, m_, b, l, -1.0, q_.ptr, ldq_, cd, ldcd, 1.0, yj, ldq_);
             gemm_(true, b, b, m_, 1.0, yj, ldq_, yj, ldq_, 0.0, S_, b);
+            comm_allreduce_sum(h_, S_, size_t(b) * b, s_);
             launch_chol_upper_inv(S_, b, b, 1e-12, diag_max_, dblk, ldcd, R1_, R1i_, scal_ + kDMax,
                                   w.scratch.ptr, status_, kStAcceptPivot, s_, h_.lc);
             gemm_(false, m_, b, b, 1.0, yj, ldq_, R1i_, b, 0.0, w.ys.ptr, ldq_);
             gemm_(true, l, b, m_, 1.0, q_.ptr, ldq_, w.ys.ptr, ldq_, 0.0, w.c2.ptr, l);
+            comm_allreduce_sum(h_, w.c2.ptr, size_t(l) * b, s_);
             gemm_(false, m_, b, l, -1.0, q_.ptr, ldq_, w.c2.ptr, l, 1.0, w.ys.ptr, ldq_);
         }
         gemm_(true, b, b, m_, 1.0, w.ys.ptr, ldq_, w.ys.ptr, ldq_, 0.0, S2_, b);
+        comm_allreduce_sum(h_, S2_, size_t(b) * b, s_);
         launch_chol_upper_inv(S2_, b, b, 0.0, 0.0, nullptr, 0, R2_, R2i_, nullptr, w.scratch.ptr, status_,
                               kStAcceptChol2, s_, h_.lc);
         gemm_(false, m_, b, b, 1.0, w.ys.ptr, ldq_, R2i_, b, 0.0, yj, ldq_);  // Q_j
@@ -515,12 +522,24 @@ int run_qb(Handle& h, const double* a, int64_t m, int64_t n, int64_t lda, bool a
     std::memset(out, 0, sizeof *out);
     out->m = m;
     out->n = n;
-    if (!a) throw Error(kStatusInvalid, "null matrix pointer");
+    if (!a && !(h.comm && m == 0)) throw Error(kStatusInvalid, "null matrix pointer");
     if (lda < m) throw Error(kStatusDimension, "lda < m");
-    fqb_config cfg = resolve_config(m, n, cfg_in, fixed_precision);
+    // with a communicator, (a, m, lda) is this rank's row block of A
+    int64_t m_global = m;
+    if (h.comm) {
+        h.ws.scalars.ensure(8, h.stream);
+        const double local = double(m);
+        FQB_CUDA(cudaMemcpyAsync(h.ws.scalars.ptr, &local, sizeof(double), cudaMemcpyHostToDevice, h.stream));
+        comm_allreduce_sum(h, h.ws.scalars.ptr, 1, h.stream);
+        double total = 0.0;
+        FQB_CUDA(cudaMemcpyAsync(&total, h.ws.scalars.ptr, sizeof(double), cudaMemcpyDeviceToHost, h.stream));
+        FQB_CUDA(cudaStreamSynchronize(h.stream));
+        m_global = int64_t(total);
+    }
+    fqb_config cfg = resolve_config(m_global, n, cfg_in, fixed_precision);
     if (!fixed_precision) {
         if (rank < 1) throw Error(kStatusConfig, "rank must be at least 1");
-        if (rank > std::min(m, n)) throw Error(kStatusConfig, "rank exceeds matrix dimensions");
+        if (rank > std::min(m_global, n)) throw Error(kStatusConfig, "rank exceeds matrix dimensions");
     }
     if (!src && cfg.sketch.kind != kGaussian && cfg.sketch.zeta == 0 && !(cfg.sketch.p > 0.0 && cfg.sketch.p < 1.0))
         throw Error(kStatusConfig, "gen_sketch: sparse kinds require p in (0,1)");

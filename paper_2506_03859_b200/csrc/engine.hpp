@@ -67,7 +67,17 @@ struct Handle {
     unsigned* host_status = nullptr;  // pinned readback slot
     double* host_scalars = nullptr;   // pinned readback slots
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // row-sharded multi-GPU (comm.cu); nullptr = single GPU
+    void* comm = nullptr;
+    int nranks = 1, rank = 0;
+    int64_t collectives = 0;
 };
+
+// comm.cu
+void comm_unique_id(void* out128);
+void comm_attach(Handle& h, const void* id128, int nranks, int rank);
+void comm_detach(Handle& h);
+void comm_allreduce_sum(Handle& h, double* buf, size_t count, cudaStream_t s);
 
 struct ResolvedConfig {
     fqb_config cfg;

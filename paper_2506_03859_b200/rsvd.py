@@ -314,6 +314,21 @@ class Engine:
     def launch_count(self) -> int:
         return self._lib.fqb_launch_count(self._h)
 
+    @property
+    def collective_count(self) -> int:
+        return self._lib.fqb_collective_count(self._h)
+
+    def attach_comm(self, group=None) -> None:
+        """Row-sharded mode: subsequent runs take this rank's row block of A
+        (see paper_2506_03859_b200.dist.partition_rows)."""
+        from . import dist
+        dist.attach(self, group)
+
+    def detach_comm(self) -> None:
+        st = self._lib.fqb_comm_detach(self._h)
+        if st:
+            _raise(st, "fqb_comm_detach")
+
     def set_stream(self, stream_ptr: int | None):
         st = self._lib.fqb_set_stream(self._h, stream_ptr)
         if st:
