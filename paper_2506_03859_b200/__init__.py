@@ -13,4 +13,6 @@ from .rsvd import (  # noqa: F401
     default_density, default_engine, default_max_iters, gen_sketch, run_fixed_precision,
     run_fixed_rank, sketch_kind_from_name, sketch_kind_name)
 
+from . import dist  # noqa: F401,E402  (row-sharded multi-GPU helpers)
+
 __all__ = [n for n in dir() if not n.startswith("_")]

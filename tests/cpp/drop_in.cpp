@@ -60,7 +60,7 @@ static int gpu_checks() {
     const rb::DenseMatrix a = lowrank(600, 400, 120, 7);
     for (int kind = 0; kind < 5; ++kind) {
         rb::FarpcaConfig cfg;
-        cfg.eps = 1e-6;
+        cfg.eps = 1e-4;  // rank ~42 of 120: well above the 1e-12 relative pivot floor
         cfg.relative = true;
         cfg.power = 1;
         cfg.block = 16;
@@ -89,7 +89,7 @@ static int gpu_checks() {
     ZetaSource src;
     src.eng = &eng;
     rb::FarpcaConfig cfg;
-    cfg.eps = 1e-6;
+    cfg.eps = 1e-4;
     cfg.relative = true;
     cfg.block = 16;
     cfg.power = 2;

@@ -9,7 +9,7 @@ rows = list(csv.reader(open(path)))
 h = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
 hdr, data = rows[h], rows[h + 1:]
 ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
-scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}
+scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6, "s": 1e6}
 ours = [r for r in data if "farqb" in r[ki]]
 run = ours[-per_run:] if per_run else ours
 agg = collections.defaultdict(lambda: [0, 0.0])
