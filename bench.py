@@ -33,6 +33,7 @@ RANK_SIG = 900
 BLOCK, POWER, EPS, P_BERN = 50, 2, 1e-3, 0.5
 SEED_A, SEED_OMEGA = 42, 7
 FP64_PEAK_TFLOPS = 37.1     # measured DMMA peak on this pool (profiles/fp64_peak_r01.txt)
+HBM_PEAK_GBS = 6550.4       # MEASURED_PEAKS.json hbm_gbs (copy)
 WORKLOAD = "C2: 8000x8000 FP64, sigma_i=10^(-i/50), StdBernoulli p=1/2, b=50, P=2, eps=1e-3"
 
 
@@ -143,6 +144,55 @@ def gemm_roofline(eng, a, stream):
     return out
 
 
+def sketch_roofline(eng, dev):
+    """Sparse-sign sketch Y = A*Omega at BASELINE config 3 shape (A 20000 x 20000 FP64,
+    b = 64, zeta = 8): HBM GB/s of the gather SpMM against the measured copy peak.
+    32 different Omega blocks are cycled so consecutive launches touch different
+    columns of A (each block reads 512 of 20000 columns, 82 MB, < L2 otherwise)."""
+    import numpy as np
+    import torch
+    from paper_2506_03859_b200 import SketchKind, SketchSpec
+    m = n = 20000
+    b, zeta, nblk = 64, 8, 32
+    a = torch.randn(n, m, dtype=torch.float64, device=dev).t()      # m x n column-major
+    spec = SketchSpec(SketchKind.SparseSign, 0.0, 7, zeta=zeta)
+    blocks, alg_bytes = [], []
+    for j in range(nblk):
+        s = eng.gen_sketch(spec, n, b, j)
+        u = len(np.unique(s.row_idx))
+        blocks.append((torch.from_numpy(s.col_ptr.astype(np.int32)).to(dev),
+                       torch.from_numpy(s.row_idx.astype(np.int32)).to(dev),
+                       torch.from_numpy(s.values).to(dev)))
+        alg_bytes.append(8 * m * (u + b) + 12 * s.nnz + 4 * (b + 1))
+    y = torch.empty(b, m, dtype=torch.float64, device=dev).t()
+    stream = torch.cuda.Stream(device=dev)   # a real stream: handle 0 would mean the engine's own
+    eng.set_stream(stream.cuda_stream)
+
+    def launch(j):
+        cp, ri, va = blocks[j]
+        eng.sparse_dense_mul(a.data_ptr(), m, n, m, cp.data_ptr(), ri.data_ptr(), va.data_ptr(), b, None,
+                             y.data_ptr(), m)
+    for j in range(nblk):
+        launch(j)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 4
+    e0.record(stream)
+    for _ in range(reps):
+        for j in range(nblk):
+            launch(j)
+    e1.record(stream)
+    e1.synchronize()
+    ms = e0.elapsed_time(e1) / (reps * nblk)
+    gbs = (sum(alg_bytes) / nblk) / (ms * 1e-3) / 1e9
+    del a
+    torch.cuda.empty_cache()
+    return {"kernel": "k_gather_spmm (sparse sign, zeta=8) Y = A*Omega, A 20000x20000, b=64",
+            "achieved": gbs, "peak": HBM_PEAK_GBS, "unit": "GB/s", "frac": gbs / HBM_PEAK_GBS,
+            "launch_us": ms * 1e3, "bytes_per_launch": sum(alg_bytes) / nblk,
+            "bytes_formula": "8*m*(u+b) + 12*nnz + 4*(b+1), u = distinct rows of the block"}
+
+
 def load_traffic():
     path = os.path.join(ROOT, "profiles", "traffic_r01.json")
     try:
@@ -186,7 +236,7 @@ def run_ours(args):
         # strong scaling: one problem, rows of A sharded over the GPUs, NCCL all-reduce
         r0, r1 = partition_rows(M, world, rank)
         a = a_full[r0:r1, :].t().contiguous().t()
-        del a_full
+        a_full = None
         eng.attach_comm()
     else:
         a = a_full
@@ -199,18 +249,22 @@ def run_ours(args):
         torch.cuda.synchronize()
 
     clk = ClockSampler(local).__enter__()
-    time.sleep(0.3)   # let the sampler start before the timed region
+    t_wait = time.time()
+    while not clk.lines and time.time() - t_wait < 10.0:   # NVML start-up must not overlap the timing
+        time.sleep(0.05)
     for _ in range(max(args.warmup, 0)):
         r = eng.run_fixed_precision(a, cfg, output="device")
         del r
     barrier()
     launches0 = eng.launch_count
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    results = []
+    step_ms = []
     with torch.cuda.stream(stream):
         e0.record()
     for _ in range(args.steps):
-        results.append(eng.run_fixed_precision(a, cfg, output="device"))
+        r = eng.run_fixed_precision(a, cfg, output="device")   # Q, B' produced on the device
+        step_ms.append(r.elapsed_ms)
+        last = r
     with torch.cuda.stream(stream):
         e1.record()
     e1.synchronize()
@@ -221,9 +275,8 @@ def run_ours(args):
         t = torch.tensor([ms], device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = t.item()
-    last = results[-1]
+
     rank_l, blocks, e_rel = last.rank, last.blocks, float(np.sqrt(max(last.residual_sq, 0) / last.norm_a_sq))
-    del results
 
     # ---- e2e: host A (pinned) -> public API -> Q, B' back on the host -----------------
     a_host = a.t().contiguous().cpu().pin_memory()  # (n x m_local) row-major == A column-major
@@ -246,6 +299,9 @@ def run_ours(args):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_s = t.item()
     roof = gemm_roofline(eng, a_full if world == 1 else make_matrix(dev), stream)
+    a_full = None
+    torch.cuda.empty_cache()
+    sketch = sketch_roofline(eng, dev)
     dom = roof["tn"]
     traffic = load_traffic()
     line = {
@@ -263,7 +319,7 @@ def run_ours(args):
         "data": "synthetic (seeded torch N(0,1) factors, see bench.py docstring)",
         "config": {"workload": WORKLOAD, "m": M, "n": N, "block": BLOCK, "power": POWER, "eps": EPS,
                    "sketch": "stdbernoulli p=0.5", "rank_reached": rank_l, "blocks": blocks,
-                   "rel_error_indicator": e_rel, "l2": "A (512 MB) exceeds the 126 MB L2; no flush",
+                   "rel_error_indicator": e_rel, "step_device_ms": step_ms, "l2": "A (512 MB) exceeds the 126 MB L2; no flush",
                    "parallelism": f"rows of A sharded over {world} GPUs, NCCL all-reduce" if world > 1
                    else "single GPU"},
         "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
@@ -275,6 +331,7 @@ def run_ours(args):
                      "flops_per_launch": 2.0 * M * N * BLOCK, "launch_ms": dom["ms"],
                      "nn_achieved": roof["nn"]["tflops"],
                      "traffic": (traffic or {}).get("tn_bytes_per_launch")},
+        "sketch_roofline": sketch,
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

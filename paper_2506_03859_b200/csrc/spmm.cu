@@ -3,76 +3,98 @@
 //  launch_gather_spmm:  Y = A * S [- z]      (reference: sparse_dense_mul,
 //      centered_product, /root/reference/proj/src/sketch.cpp:104-140).  Each
 //      output column gathers the zeta columns of A that its nonzeros name.  A
-//      warp owns 64 consecutive rows (one 16-byte load per lane per nonzero),
-//      so every A column segment is read once, fully coalesced, and the
+//      warp owns 64*VPL consecutive rows (VPL 16-byte loads per lane per
+//      nonzero), so every A column segment is read once, fully coalesced, and the
 //      nonzeros are accumulated in CSC order with one fma each -- the same
 //      operation sequence as the reference's axpy loop (kernels_avx2.cpp:
 //      220-231), hence bitwise-identical output.
 //  launch_gather_tmul:  T = Wt' * S [- shift * colsum(Wt)]  (reference:
 //      dense_sparse_tmul + the centering in tmul_block, sketch.cpp:116-130,
 //      driver.cpp:30-45); the deflation product B * Omega with Wt = B'.
+#include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "kernels.hpp"
 
 namespace farqb {
 namespace {
 
-constexpr int kRowsPerWarp = 64;
 constexpr int kWarpsPerCta = 8;
 constexpr int kUnroll = 8;
 
-template <bool VEC2>
+// VPL double2 vectors per lane: a warp owns 64*VPL consecutive rows, so every
+// gathered column of A is read as one 512*VPL-byte contiguous run.
+template <bool VEC2, int VPL>
 __global__ void __launch_bounds__(256) k_gather_spmm(const double* __restrict__ a, int64_t m,
                                                      int64_t lda, const int* __restrict__ col_ptr,
                                                      const int* __restrict__ row_idx,
                                                      const double* __restrict__ values,
                                                      const double* __restrict__ z,
                                                      double* __restrict__ c, int64_t ldc) {
+    constexpr int ROWS = 64 * VPL;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int j = blockIdx.y;
-    const int64_t r0 = (int64_t(blockIdx.x) * kWarpsPerCta + warp) * kRowsPerWarp + 2 * lane;
-    if (r0 >= m) return;
-    const bool two = r0 + 1 < m;
+    const int64_t base = (int64_t(blockIdx.x) * kWarpsPerCta + warp) * ROWS + 2 * lane;
+    if (base >= m) return;
     const int beg = col_ptr[j], end = col_ptr[j + 1];
-    double acc0 = 0.0, acc1 = 0.0;
-    int idx = beg;
-    for (; idx + kUnroll <= end; idx += kUnroll) {
-        double2 av[kUnroll];
-        double vv[kUnroll];
+    double acc[VPL][2];
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-            const double* col = a + int64_t(row_idx[idx + u]) * lda + r0;
+    for (int v = 0; v < VPL; ++v) acc[v][0] = acc[v][1] = 0.0;
+    int idx = beg;
+    constexpr int U = kUnroll / VPL > 0 ? kUnroll / VPL : 1;
+    for (; idx + U <= end; idx += U) {
+        double2 av[U][VPL];
+        double vv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const double* col = a + int64_t(row_idx[idx + u]) * lda;
             vv[u] = values[idx + u];
-            if (VEC2 && two) {
-                av[u] = __ldg(reinterpret_cast<const double2*>(col));
-            } else {
-                av[u].x = __ldg(col);
-                av[u].y = two ? __ldg(col + 1) : 0.0;
+#pragma unroll
+            for (int v = 0; v < VPL; ++v) {
+                const int64_t r = base + 64 * v;
+                if (VEC2 && r + 1 < m) {
+                    av[u][v] = __ldg(reinterpret_cast<const double2*>(col + r));
+                } else {
+                    av[u][v].x = r < m ? __ldg(col + r) : 0.0;
+                    av[u][v].y = r + 1 < m ? __ldg(col + r + 1) : 0.0;
+                }
             }
         }
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-            acc0 = fma(vv[u], av[u].x, acc0);
-            acc1 = fma(vv[u], av[u].y, acc1);
-        }
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int v = 0; v < VPL; ++v) {
+                acc[v][0] = fma(vv[u], av[u][v].x, acc[v][0]);
+                acc[v][1] = fma(vv[u], av[u][v].y, acc[v][1]);
+            }
     }
     for (; idx < end; ++idx) {
-        const double* col = a + int64_t(row_idx[idx]) * lda + r0;
-        const double v = values[idx];
-        acc0 = fma(v, __ldg(col), acc0);
-        if (two) acc1 = fma(v, __ldg(col + 1), acc1);
+        const double* col = a + int64_t(row_idx[idx]) * lda;
+        const double vv = values[idx];
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) {
+            const int64_t r = base + 64 * v;
+            if (r < m) acc[v][0] = fma(vv, __ldg(col + r), acc[v][0]);
+            if (r + 1 < m) acc[v][1] = fma(vv, __ldg(col + r + 1), acc[v][1]);
+        }
     }
-    if (z) {
-        acc0 -= z[r0];
-        if (two) acc1 -= z[r0 + 1];
-    }
-    double* out = c + int64_t(j) * ldc + r0;
-    if (VEC2 && two) {
-        *reinterpret_cast<double2*>(out) = make_double2(acc0, acc1);
-    } else {
-        out[0] = acc0;
-        if (two) out[1] = acc1;
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) {
+        const int64_t r = base + 64 * v;
+        if (r >= m) continue;
+        double y0 = acc[v][0], y1 = acc[v][1];
+        if (z) {
+            y0 -= z[r];
+            if (r + 1 < m) y1 -= z[r + 1];
+        }
+        double* out = c + int64_t(j) * ldc + r;
+        if (VEC2 && r + 1 < m) {
+            *reinterpret_cast<double2*>(out) = make_double2(y0, y1);
+        } else {
+            out[0] = y0;
+            if (r + 1 < m) out[1] = y1;
+        }
     }
 }
 
@@ -102,11 +124,23 @@ void launch_gather_spmm(const double* a, int64_t m, int64_t lda, const int* col_
     if (m <= 0 || l <= 0) return;
     const bool vec2 = (lda % 2 == 0) && (ldc % 2 == 0) && (reinterpret_cast<uintptr_t>(a) % 16 == 0) &&
                       (reinterpret_cast<uintptr_t>(c) % 16 == 0);
-    dim3 grid(unsigned(ceil_div(m, int64_t(kRowsPerWarp) * kWarpsPerCta)), unsigned(l));
-    if (vec2)
-        k_gather_spmm<true><<<grid, 256, 0, s>>>(a, m, lda, col_ptr, row_idx, values, z, c, ldc);
-    else
-        k_gather_spmm<false><<<grid, 256, 0, s>>>(a, m, lda, col_ptr, row_idx, values, z, c, ldc);
+    static int vpl_env = [] {
+        const char* e = std::getenv("FQB_SPMM_VPL");
+        return e ? std::atoi(e) : 0;
+    }();
+    // 1 KB runs per gathered column (VPL = 2) once that still leaves >= 4 CTAs per
+    // SM; measured on the C3 sketch (20000^2, b = 64, zeta = 8): VPL 1/2/4 ->
+    // 4376 / 4932 / 4816 GB/s (profiles/sketch_sweep_r01.txt)
+    int vpl = vpl_env ? vpl_env : (ceil_div(m, 1024) * l >= 4 * 148 ? 2 : 1);
+    if (vpl != 1 && vpl != 2 && vpl != 4) vpl = 1;
+    dim3 grid(unsigned(ceil_div(m, int64_t(64 * vpl) * kWarpsPerCta)), unsigned(l));
+    if (vec2) {
+        if (vpl == 4) k_gather_spmm<true, 4><<<grid, 256, 0, s>>>(a, m, lda, col_ptr, row_idx, values, z, c, ldc);
+        else if (vpl == 2) k_gather_spmm<true, 2><<<grid, 256, 0, s>>>(a, m, lda, col_ptr, row_idx, values, z, c, ldc);
+        else k_gather_spmm<true, 1><<<grid, 256, 0, s>>>(a, m, lda, col_ptr, row_idx, values, z, c, ldc);
+    } else {
+        k_gather_spmm<false, 1><<<grid, 256, 0, s>>>(a, m, lda, col_ptr, row_idx, values, z, c, ldc);
+    }
     FQB_LAUNCHED();
     lc.bump();
 }
