@@ -8,8 +8,9 @@ Workload (BASELINE.json configs[1], the metric's single-GPU config "C2"):
   standardized-Bernoulli Omega (p = 1/2), b = 50, P = 2, eps = 1e-3 relative.
 
 One step = one full run_fixed_precision to eps (rank 200, 4 blocks) through the
-engine, A resident in HBM (512 MB > 126 MB L2, so no L2 flush is needed between
-steps).  `e2e` repeats the step through the public API with A in pinned host
+engine -- the blocked QB loop plus the assembly of U, sigma, V, exactly what the
+reference's run_fixed_precision times -- with A resident in HBM (512 MB > 126 MB
+L2, so no L2 flush is needed between steps).  `e2e` repeats the step through the public API with A in pinned host
 memory (H2D inside the timed region) and Q, B' returned to the host.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
@@ -253,7 +254,7 @@ def run_ours(args):
     while not clk.lines and time.time() - t_wait < 10.0:   # NVML start-up must not overlap the timing
         time.sleep(0.05)
     for _ in range(max(args.warmup, 0)):
-        r = eng.run_fixed_precision(a, cfg, output="device")
+        r = eng.run_fixed_precision(a, cfg, output="device", svd=True)
         del r
     barrier()
     launches0 = eng.launch_count
@@ -262,7 +263,8 @@ def run_ours(args):
     with torch.cuda.stream(stream):
         e0.record()
     for _ in range(args.steps):
-        r = eng.run_fixed_precision(a, cfg, output="device")   # Q, B' produced on the device
+        # like rsvd::run_fixed_precision: QB loop + assemble_svd (U, sigma, V), all on the device
+        r = eng.run_fixed_precision(a, cfg, output="device", svd=True)
         step_ms.append(r.elapsed_ms)
         last = r
     with torch.cuda.stream(stream):
@@ -282,17 +284,18 @@ def run_ours(args):
     a_host = a.t().contiguous().cpu().pin_memory()  # (n x m_local) row-major == A column-major
     a_host_cm = a_host.t()
     for _ in range(1):
-        eng.run_fixed_precision(a_host_cm, cfg, output="host")
+        eng.run_fixed_precision(a_host_cm, cfg, output="host", svd=True)
     torch.cuda.synchronize()
     t_e2e = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        r = eng.run_fixed_precision(a_host_cm, cfg, output="host")
+        r = eng.run_fixed_precision(a_host_cm, cfg, output="host", svd=True)
         t_e2e.append(time.perf_counter() - t0)
     e2e_s = statistics.mean(t_e2e)
     clk.__exit__(None, None, None)
     h2d = a.shape[0] * N * 8
-    d2h = (a.shape[0] + N) * r.rank * 8 + 8 * (r.blocks + 4)
+    # Q, B' and U, V (m x l, n x l each), sigma, flags and the per-block trace
+    d2h = 2 * (a.shape[0] + N) * r.rank * 8 + 9 * r.rank + 8 * (r.blocks + 4)
 
     if world > 1:
         t = torch.tensor([e2e_s], device=dev)

@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define FARQB_ABI_VERSION 1
+#define FARQB_ABI_VERSION 2
 
 typedef enum fqb_status {
     FQB_OK = 0,
@@ -107,6 +107,9 @@ typedef int (*fqb_block_source_fn)(void* user, int n, int b, int block_id, fqb_b
 #define FQB_OUT_NONE   0u   /* scalars, trace and ids only                       */
 #define FQB_OUT_HOST   1u   /* copy Q and B' into malloc'd host arrays           */
 #define FQB_OUT_DEVICE 2u   /* keep Q and B' on the device (library-owned)       */
+#define FQB_OUT_SVD    4u   /* also assemble U, sigma, V like rsvd::ApproxSvd     */
+                            /* (assemble_svd, driver.cpp:296-345); fixed-rank runs */
+                            /* drop the overshoot like drop_smallest (:85-106)     */
 
 typedef struct fqb_qb_result {
     int status;              /* same as the call's return value                 */
@@ -129,6 +132,15 @@ typedef struct fqb_qb_result {
     double resolved_p;
     int gpu_launches;        /* kernels this call launched                      */
     double elapsed_ms;       /* device time of the call (CUDA events)           */
+    /* ApproxSvd fields (driver.hpp:45-58), filled with FQB_OUT_SVD: */
+    int svd_rank;            /* r (fixed rank: the requested rank)               */
+    double* sigma;           /* host, ascending, r                               */
+    char* v_flagged;         /* host, r                                          */
+    double* u;               /* m x r (this rank's rows), placement as q         */
+    int64_t ldu;
+    double* v;               /* n x r                                            */
+    int64_t ldv;
+    double svd_residual_sq;  /* residual_sq plus the dropped energy (fixed rank) */
     void* internal;
 } fqb_qb_result;
 

@@ -19,6 +19,7 @@
 // rank l, block count and the error indicator E = ||A||_F^2 - sum ||B_j||_F^2.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 #include <memory>
@@ -86,17 +87,24 @@ class BlockSource {
     virtual SketchBlock next(int n, int b, int block_id) = 0;
 };
 
+// QB factors plus the reference's ApproxSvd fields (driver.hpp:45-58).
 struct QbResult {
     DenseMatrix q;   // m x rank
     DenseMatrix bt;  // n x rank  (B = bt')
-    int rank = 0;
+    int rank = 0;    // QB rank l = blocks * b
     int blocks = 0;
     bool converged = false;
-    double residual_sq = 0.0;
+    double residual_sq = 0.0;  // ApproxSvd::residual_sq (includes a fixed-rank drop)
     double norm_a_sq = 0.0;
+    DenseMatrix u;                 // m x r
+    std::vector<double> sigma;     // ascending
+    DenseMatrix v;                 // n x r
+    std::vector<char> v_flagged;
+    double qb_residual_sq = 0.0;   // E of the QB factors themselves
     std::vector<double> block_residuals;
     std::vector<int> block_ids;
     double device_ms = 0.0;
+    int svd_rank() const { return int(sigma.size()); }
 };
 
 // ---- exceptions (errors.hpp:9-46, driver.hpp:60-65) -------------------------
@@ -239,9 +247,11 @@ class Engine {
         const int m = a.rows, n = a.cols;
         const fqb_status st =
             rank < 0 ? fqb_qb_fixed_precision(h_, a.data.data(), m, n, m, 0, &c,
-                                              source ? detail::source_trampoline : nullptr, &ctx, FQB_OUT_HOST, &r)
+                                              source ? detail::source_trampoline : nullptr, &ctx,
+                                              FQB_OUT_HOST | FQB_OUT_SVD, &r)
                      : fqb_qb_fixed_rank(h_, a.data.data(), m, n, m, 0, rank, &c,
-                                         source ? detail::source_trampoline : nullptr, &ctx, FQB_OUT_HOST, &r);
+                                         source ? detail::source_trampoline : nullptr, &ctx,
+                                         FQB_OUT_HOST | FQB_OUT_SVD, &r);
         if (ctx.error) {
             fqb_result_free(&r);
             std::rethrow_exception(ctx.error);
@@ -262,6 +272,18 @@ class Engine {
             out.q.data.assign(r.q, r.q + std::size_t(m) * r.rank);
             out.bt = DenseMatrix(n, r.rank);
             out.bt.data.assign(r.bt, r.bt + std::size_t(n) * r.rank);
+        }
+        out.qb_residual_sq = r.residual_sq;
+        if (r.sigma) {
+            out.sigma.assign(r.sigma, r.sigma + r.svd_rank);
+            out.v_flagged.assign(r.v_flagged, r.v_flagged + r.svd_rank);
+            out.residual_sq = r.svd_residual_sq;
+            if (r.svd_rank > 0 && r.u) {
+                out.u = DenseMatrix(m, r.svd_rank);
+                out.u.data.assign(r.u, r.u + std::size_t(m) * r.svd_rank);
+                out.v = DenseMatrix(n, r.svd_rank);
+                out.v.data.assign(r.v, r.v + std::size_t(n) * r.svd_rank);
+            }
         }
         out.block_residuals.assign(r.block_residuals, r.block_residuals + r.blocks);
         out.block_ids.assign(r.block_ids, r.block_ids + r.n_ids);
@@ -293,6 +315,35 @@ QbResult run_fixed_rank(const Matrix& a, int rank, const FarpcaConfig& cfg, Bloc
 
 inline SketchBlock gen_sketch(const SketchSpec& spec, int n, int l, int block_id) {
     return default_engine().gen_sketch(spec, n, l, block_id);
+}
+
+// truncate_to_tolerance (driver.cpp:415-433)
+inline QbResult truncate_to_tolerance(const QbResult& svd, double eps_rel, double norm_a) {
+    if (eps_rel < 0.0 || norm_a < 0.0) throw ConfigError("truncate_to_tolerance: negative tolerance or norm");
+    const double target = eps_rel * norm_a;
+    const double budget = target * target * (1.0 + 1e-12);
+    const int l = svd.svd_rank();
+    double acc = svd.residual_sq;
+    int drop = 0;
+    while (drop < l) {
+        const double next = acc + svd.sigma[drop] * svd.sigma[drop];
+        if (next > budget) break;
+        acc = next;
+        ++drop;
+    }
+    if (drop == 0) return svd;
+    QbResult out = svd;
+    out.residual_sq = acc;
+    out.sigma.assign(svd.sigma.begin() + drop, svd.sigma.end());
+    out.v_flagged.assign(svd.v_flagged.begin() + drop, svd.v_flagged.end());
+    const int r = l - drop;
+    out.u = DenseMatrix(svd.u.rows, r);
+    out.v = DenseMatrix(svd.v.rows, r);
+    for (int j = 0; j < r; ++j) {
+        std::copy(svd.u.col(drop + j), svd.u.col(drop + j) + svd.u.rows, out.u.col(j));
+        std::copy(svd.v.col(drop + j), svd.v.col(drop + j) + svd.v.rows, out.v.col(j));
+    }
+    return out;
 }
 
 inline double default_density(SketchKind kind, int n) { return fqb_default_density(static_cast<int>(kind), n); }

@@ -10,8 +10,8 @@ from .rsvd import (  # noqa: F401
     AllocError, BlockDegenerate, BlockSource, CallbackError, ConfigError, ConvergenceFailure,
     CudaError, DimensionError, Engine, FarpcaConfig, InvalidArgument, QBResult, RsvdError,
     ShiftConvention, SketchBlock, SketchKind, SketchSpec, ToleranceNotReached, default_block,
-    default_density, default_engine, default_max_iters, gen_sketch, run_fixed_precision,
-    run_fixed_rank, sketch_kind_from_name, sketch_kind_name)
+    default_density, default_engine, default_max_iters, estimate_cost, gen_sketch,
+    run_fixed_precision, run_fixed_rank, sketch_kind_from_name, sketch_kind_name, truncate_to_tolerance)
 
 from . import dist  # noqa: F401,E402  (row-sharded multi-GPU helpers)
 

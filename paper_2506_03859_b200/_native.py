@@ -36,7 +36,9 @@ class ResultC(C.Structure):
                 ("block_residuals", C.POINTER(C.c_double)), ("block_ids", C.POINTER(C.c_int)),
                 ("n_ids", C.c_int), ("resolved_block", C.c_int), ("resolved_max_iters", C.c_int),
                 ("resolved_p", C.c_double), ("gpu_launches", C.c_int), ("elapsed_ms", C.c_double),
-                ("internal", C.c_void_p)]
+                ("svd_rank", C.c_int), ("sigma", C.POINTER(C.c_double)), ("v_flagged", C.POINTER(C.c_char)),
+                ("u", C.c_void_p), ("ldu", C.c_int64), ("v", C.c_void_p), ("ldv", C.c_int64),
+                ("svd_residual_sq", C.c_double), ("internal", C.c_void_p)]
 
 
 class SketchHostC(C.Structure):
@@ -49,7 +51,7 @@ class SketchHostC(C.Structure):
 
 SOURCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_int, C.POINTER(BlockC))
 
-OUT_NONE, OUT_HOST, OUT_DEVICE = 0, 1, 2
+OUT_NONE, OUT_HOST, OUT_DEVICE, OUT_SVD = 0, 1, 2, 4
 
 # every function include/farqb.h declares: (name, restype, argtypes)
 _H = C.c_void_p

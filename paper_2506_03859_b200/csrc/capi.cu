@@ -109,6 +109,7 @@ fqb_status fqb_destroy(fqb_handle h) {
         bind(h);
         cudaStreamSynchronize(h->h.stream);
         farqb::comm_detach(h->h);
+        farqb::destroy_cusolver(h->h);
         {
             farqb::Workspace& w = h->h.ws;
             w.omega.release(); w.y0.release(); w.ys.release(); w.wp.release(); w.wraw.release();
@@ -170,6 +171,7 @@ fqb_status fqb_comm_detach(fqb_handle h) {
     return guarded([&]() -> fqb_status {
         bind(h);
         farqb::comm_detach(h->h);
+        farqb::destroy_cusolver(h->h);
         return FQB_OK;
     });
 }
@@ -215,6 +217,17 @@ void fqb_result_free(fqb_qb_result* r) {
         std::free(r->q);
         std::free(r->bt);
     }
+    if (r->on_device) {
+        if (r->u) cudaFree(r->u);
+        if (r->v) cudaFree(r->v);
+    } else {
+        std::free(r->u);
+        std::free(r->v);
+    }
+    std::free(r->sigma);
+    std::free(r->v_flagged);
+    r->u = r->v = r->sigma = nullptr;
+    r->v_flagged = nullptr;
     std::free(r->block_residuals);
     std::free(r->block_ids);
     r->q = r->bt = nullptr;

@@ -55,10 +55,14 @@ void ensure_gemm_workspace(Handle& h) {
         h.gws.work_doubles = need;
     }
     if (!h.ws.gemm_flags.ptr) {
-        h.ws.gemm_flags.ensure(size_t(h.num_sms) + 16, h.stream);
-        FQB_CUDA(cudaMemsetAsync(h.ws.gemm_flags.ptr, 0, sizeof(unsigned) * (h.num_sms + 16), h.stream));
+        // [0, num_sms): stream-K partial flags; then 4*num_sms split-K tile counters
+        const size_t count = size_t(h.num_sms) * 5 + 16;
+        h.ws.gemm_flags.ensure(count, h.stream);
+        FQB_CUDA(cudaMemsetAsync(h.ws.gemm_flags.ptr, 0, sizeof(unsigned) * count, h.stream));
         h.gws.flags = h.ws.gemm_flags.ptr;
         h.gws.epoch = 0;
+        h.gws.counters = h.ws.gemm_flags.ptr + h.num_sms + 16;
+        h.gws.counter_count = int64_t(h.num_sms) * 4;
     }
     const char* env = std::getenv("FQB_GEMM_TMA");
     h.gws.use_tma = !(env && env[0] == '0');
@@ -600,6 +604,23 @@ int run_qb(Handle& h, const double* a, int64_t m, int64_t n, int64_t lda, bool a
         status = kStatusDegenerate;
         message = e.what();
     }
+    // ApproxSvd (assemble_svd, driver.cpp:296-345): also for the partial result of
+    // ToleranceNotReached; BlockDegenerate carries no factorization (errors.hpp:28-37)
+    std::vector<double> sig;
+    std::vector<char> flg;
+    DeviceArray<double> u_dev, v_dev;
+    int svd_r = 0, drop = 0;
+    double svd_res = run.residual();
+    const int l_final = run.rank();
+    if ((flags & FQB_OUT_SVD) && status != kStatusDegenerate && l_final > 0) {
+        u_dev.ensure(size_t(run.ldq()) * l_final, s);
+        v_dev.ensure(size_t(run.ldbt()) * l_final, s);
+        assemble_svd(h, run.q().ptr, run.ldq(), run.bt().ptr, run.ldbt(), m, n, l_final, u_dev.ptr, run.ldq(),
+                     v_dev.ptr, run.ldbt(), sig, flg);
+        if (!fixed_precision) drop = std::max(0, l_final - rank);  // drop_smallest (driver.cpp:85-106)
+        for (int i = 0; i < drop; ++i) svd_res += sig[i] * sig[i];
+        svd_r = l_final - drop;
+    }
     FQB_CUDA(cudaEventRecord(h.ev1, s));
 
     out->status = status;
@@ -626,6 +647,41 @@ int run_qb(Handle& h, const double* a, int64_t m, int64_t n, int64_t lda, bool a
         out->ldq = m;
         out->ldbt = n;
         out->on_device = 0;
+    }
+    if (flags & FQB_OUT_SVD) {
+        out->svd_rank = svd_r;
+        out->svd_residual_sq = svd_res;
+        out->sigma = static_cast<double*>(std::malloc(sizeof(double) * std::max(svd_r, 1)));
+        out->v_flagged = static_cast<char*>(std::malloc(std::max(svd_r, 1)));
+        for (int i = 0; i < svd_r; ++i) {
+            out->sigma[i] = sig[drop + i];
+            out->v_flagged[i] = flg[drop + i];
+        }
+        if (svd_r > 0 && (flags & FQB_OUT_DEVICE)) {
+            // the kept columns are the last svd_r (ascending order): move them to the front
+            if (drop > 0) {
+                FQB_CUDA(cudaMemcpyAsync(u_dev.ptr, u_dev.ptr + int64_t(drop) * run.ldq(),
+                                         sizeof(double) * run.ldq() * svd_r, cudaMemcpyDeviceToDevice, s));
+                FQB_CUDA(cudaMemcpyAsync(v_dev.ptr, v_dev.ptr + int64_t(drop) * run.ldbt(),
+                                         sizeof(double) * run.ldbt() * svd_r, cudaMemcpyDeviceToDevice, s));
+            }
+            out->u = u_dev.detach();
+            out->v = v_dev.detach();
+            out->ldu = run.ldq();
+            out->ldv = run.ldbt();
+        } else if (svd_r > 0 && (flags & FQB_OUT_HOST)) {
+            out->u = static_cast<double*>(std::malloc(sizeof(double) * size_t(m) * svd_r));
+            out->v = static_cast<double*>(std::malloc(sizeof(double) * size_t(n) * svd_r));
+            if (!out->u || !out->v) throw Error(kStatusAlloc, "host result allocation failed");
+            FQB_CUDA(cudaMemcpy2DAsync(out->u, m * sizeof(double), u_dev.ptr + int64_t(drop) * run.ldq(),
+                                       run.ldq() * sizeof(double), m * sizeof(double), svd_r,
+                                       cudaMemcpyDeviceToHost, s));
+            FQB_CUDA(cudaMemcpy2DAsync(out->v, n * sizeof(double), v_dev.ptr + int64_t(drop) * run.ldbt(),
+                                       run.ldbt() * sizeof(double), n * sizeof(double), svd_r,
+                                       cudaMemcpyDeviceToHost, s));
+            out->ldu = m;
+            out->ldv = n;
+        }
     }
     FQB_CUDA(cudaStreamSynchronize(s));
     float ms = 0.f;

@@ -71,7 +71,14 @@ struct Handle {
     void* comm = nullptr;
     int nranks = 1, rank = 0;
     int64_t collectives = 0;
+    void* cusolver = nullptr;  // svd.cu
 };
+
+// svd.cu: U = Q U~, V = Bt U~ Sigma^-1 from eig(B B'); sigma ascending
+void assemble_svd(Handle& h, const double* q, int64_t ldq, const double* bt, int64_t ldbt, int64_t m, int64_t n,
+                  int l, double* u, int64_t ldu, double* v, int64_t ldv, std::vector<double>& sigma,
+                  std::vector<char>& flagged);
+void destroy_cusolver(Handle& h);
 
 // comm.cu
 void comm_unique_id(void* out128);

@@ -44,6 +44,7 @@ struct GemmArgs {
     double* work;     // split-K partials: splits x (M x N), ld = M
     int64_t kchunk;   // K per split, multiple of BK
     int splits;
+    unsigned* counters;  // per-tile arrival counters (zero between launches)
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
@@ -231,14 +232,24 @@ __global__ void __launch_bounds__(THREADS, 1) k_gemm(const GemmArgs p) {
     }
 }
 
-// C = alpha * sum_z work[z] + beta * C, fixed summation order.
-__global__ void k_splitk_reduce(const double* work, int splits, int64_t M, int64_t N, double alpha,
-                                double beta, double* C, int64_t ldc) {
-    const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (idx >= M * N) return;
-    const int64_t col = idx / M, row = idx - col * M;
+// C = alpha * sum_z work[z] + beta * C.  A CTA covers 32 outputs x 8 split
+// lanes: lane q sums splits q, q+8, q+16, ... in order, then the 8 lane sums are
+// combined by a fixed shuffle tree -- deterministic, and only splits/8 dependent
+// loads per thread instead of `splits`.
+__global__ void __launch_bounds__(256) k_splitk_reduce(const double* __restrict__ work, int splits, int64_t M,
+                                                       int64_t N, double alpha, double beta, double* C,
+                                                       int64_t ldc) {
+    const int q = threadIdx.x & 7;
+    const int64_t idx = int64_t(blockIdx.x) * 32 + (threadIdx.x >> 3);
+    const int64_t total = M * N;
     double s = 0.0;
-    for (int z = 0; z < splits; ++z) s += work[int64_t(z) * M * N + idx];
+    if (idx < total)
+        for (int z = q; z < splits; z += 8) s += __ldcg(work + int64_t(z) * total + idx);
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    s += __shfl_xor_sync(0xffffffffu, s, 4);
+    if (q != 0 || idx >= total) return;
+    const int64_t col = idx / M, row = idx - col * M;
     double* cp = C + col * ldc + row;
     const double v = alpha * s;
     *cp = beta != 0.0 ? fma(beta, *cp, v) : v;
@@ -384,13 +395,13 @@ void gemm(bool trans_a, int64_t M, int64_t N, int64_t K, double alpha, const dou
             pl.splits = int(ceil_div(K, pl.kchunk));
         }
     }
-    GemmArgs a{M, N, K, alpha, beta, A, lda, B, ldb, C, ldc, work, pl.kchunk, pl.splits};
+    GemmArgs a{M, N, K, alpha, beta, A, lda, B, ldb, C, ldc, work, pl.kchunk, pl.splits, nullptr};
     dim3 grid(unsigned(pl.mt), unsigned(pl.nt_tiles), unsigned(pl.splits));
     pl.fn<<<grid, THREADS, pl.smem, s>>>(a);
     FQB_LAUNCHED();
     lc.bump();
     if (pl.splits > 1) {
-        k_splitk_reduce<<<unsigned(ceil_div(M * N, 256)), 256, 0, s>>>(work, pl.splits, M, N, alpha, beta, C, ldc);
+        k_splitk_reduce<<<unsigned(ceil_div(M * N, 32)), 256, 0, s>>>(work, pl.splits, M, N, alpha, beta, C, ldc);
         FQB_LAUNCHED();
         lc.bump();
     }

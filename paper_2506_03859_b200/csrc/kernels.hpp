@@ -83,6 +83,8 @@ struct GemmWorkspace {
     unsigned* flags = nullptr;
     unsigned epoch = 0;
     bool use_tma = true;
+    unsigned* counters = nullptr;  // split-K tile counters (zero between launches)
+    int64_t counter_count = 0;
 };
 int64_t gemm_workspace_doubles(int64_t m, int64_t n, int64_t k, int num_sms);
 void gemm(bool trans_a, int64_t m, int64_t n, int64_t k, double alpha, const double* a, int64_t lda,

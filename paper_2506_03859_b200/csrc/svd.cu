@@ -1,0 +1,140 @@
+// svd.cu -- assemble U, sigma, V from the device QB factors.
+//
+// The reference's assemble_svd (/root/reference/proj/src/driver.cpp:296-345)
+// works in Gram space (eig(Z), then eig(D'TD)).  With Q and B explicit the
+// same quantities come from one l x l symmetric eigenproblem:
+//     B B' = U~ diag(lambda) U~'   (B = Bt', l x l, eigenvalues ascending)
+//     sigma = sqrt(max(lambda, 0))              ascending, like ApproxSvd
+//     U = Q U~,   V = B' U~ diag(1/sigma)       (sigma <= 1e-14 sigma_max: zero
+//                                                column, v_flagged, driver.cpp:331-341)
+// B B' is a DMMA GEMM; the l x l eigensolver is cuSOLVER's syevd (dlopen()ed,
+// like NCCL: a library call for a once-per-run O(l^3) step, not the hot loop).
+#include <cusolverDn.h>
+#include <dlfcn.h>
+
+#include <cmath>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "engine.hpp"
+#include "kernels.hpp"
+
+namespace farqb {
+namespace {
+
+struct CusolverApi {
+    decltype(&cusolverDnCreate) create = nullptr;
+    decltype(&cusolverDnDestroy) destroy = nullptr;
+    decltype(&cusolverDnSetStream) set_stream = nullptr;
+    decltype(&cusolverDnDsyevd_bufferSize) syevd_buffer = nullptr;
+    decltype(&cusolverDnDsyevd) syevd = nullptr;
+    bool ok = false;
+    std::string why;
+};
+
+CusolverApi& cusolver() {
+    static CusolverApi api;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* h = dlopen("libcusolver.so.11", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+        if (!h) h = dlopen("libcusolver.so.11", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("/usr/local/cuda/lib64/libcusolver.so.11", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            api.why = std::string("cannot load libcusolver.so.11: ") + dlerror();
+            return;
+        }
+        api.create = reinterpret_cast<decltype(&cusolverDnCreate)>(dlsym(h, "cusolverDnCreate"));
+        api.destroy = reinterpret_cast<decltype(&cusolverDnDestroy)>(dlsym(h, "cusolverDnDestroy"));
+        api.set_stream = reinterpret_cast<decltype(&cusolverDnSetStream)>(dlsym(h, "cusolverDnSetStream"));
+        api.syevd_buffer =
+            reinterpret_cast<decltype(&cusolverDnDsyevd_bufferSize)>(dlsym(h, "cusolverDnDsyevd_bufferSize"));
+        api.syevd = reinterpret_cast<decltype(&cusolverDnDsyevd)>(dlsym(h, "cusolverDnDsyevd"));
+        api.ok = api.create && api.destroy && api.set_stream && api.syevd_buffer && api.syevd;
+        if (!api.ok) api.why = "libcusolver.so.11 lacks a required symbol";
+    });
+    if (!api.ok) throw Error(kStatusCuda, api.why);
+    return api;
+}
+
+void cs_check(cusolverStatus_t st, const char* what) {
+    if (st != CUSOLVER_STATUS_SUCCESS) throw Error(kStatusCuda, std::string(what) + " failed (cusolver status " +
+                                                                    std::to_string(int(st)) + ")");
+}
+
+__global__ void k_scale_cols(const double* src, int64_t lds, const double* scale, int rows, int cols, double* dst,
+                             int64_t ldd) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int c = blockIdx.y;
+    if (i < rows && c < cols) dst[int64_t(c) * ldd + i] = src[int64_t(c) * lds + i] * scale[c];
+}
+
+}  // namespace
+
+void assemble_svd(Handle& h, const double* q, int64_t ldq, const double* bt, int64_t ldbt, int64_t m, int64_t n,
+                  int l, double* u, int64_t ldu, double* v, int64_t ldv, std::vector<double>& sigma,
+                  std::vector<char>& flagged) {
+    sigma.assign(l, 0.0);
+    flagged.assign(l, 0);
+    if (l == 0) return;
+    cudaStream_t s = h.stream;
+    CusolverApi& api = cusolver();
+    if (!h.cusolver) {
+        cusolverDnHandle_t ch = nullptr;
+        cs_check(api.create(&ch), "cusolverDnCreate");
+        h.cusolver = ch;
+    }
+    auto ch = static_cast<cusolverDnHandle_t>(h.cusolver);
+    cs_check(api.set_stream(ch, s), "cusolverDnSetStream");
+    ensure_gemm_workspace(h);
+
+    DeviceArray<double> mat, w, work, scale, us;
+    DeviceArray<int> info;
+    mat.ensure(size_t(l) * l, s);
+    w.ensure(size_t(l), s);
+    info.ensure(1, s);
+    // B B' = Bt' Bt  (l x l)
+    gemm(true, l, l, n, 1.0, bt, ldbt, bt, ldbt, 0.0, mat.ptr, l, h.gws, h.num_sms, s, h.lc);
+    int lwork = 0;
+    cs_check(api.syevd_buffer(ch, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, l, mat.ptr, l, w.ptr, &lwork),
+             "cusolverDnDsyevd_bufferSize");
+    work.ensure(size_t(std::max(lwork, 1)), s);
+    cs_check(api.syevd(ch, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, l, mat.ptr, l, w.ptr, work.ptr, lwork,
+                       info.ptr),
+             "cusolverDnDsyevd");
+    std::vector<double> lam(l);
+    int hinfo = 0;
+    FQB_CUDA(cudaMemcpyAsync(lam.data(), w.ptr, sizeof(double) * l, cudaMemcpyDeviceToHost, s));
+    FQB_CUDA(cudaMemcpyAsync(&hinfo, info.ptr, sizeof(int), cudaMemcpyDeviceToHost, s));
+    FQB_CUDA(cudaStreamSynchronize(s));
+    if (hinfo != 0) throw Error(kStatusConvergence, "syevd did not converge (info " + std::to_string(hinfo) + ")");
+    std::vector<double> inv(l);
+    for (int j = 0; j < l; ++j) sigma[j] = std::sqrt(std::max(lam[j], 0.0));
+    const double smax = sigma[l - 1];
+    for (int j = 0; j < l; ++j) {
+        if (sigma[j] > 1e-14 * smax) {
+            inv[j] = 1.0 / sigma[j];
+        } else {
+            inv[j] = 0.0;  // pseudo-inverse convention, v column zeroed and flagged
+            flagged[j] = 1;
+        }
+    }
+    scale.ensure(size_t(l), s);
+    us.ensure(size_t(l) * l, s);
+    FQB_CUDA(cudaMemcpyAsync(scale.ptr, inv.data(), sizeof(double) * l, cudaMemcpyHostToDevice, s));
+    dim3 grid(unsigned(ceil_div(l, 256)), unsigned(l));
+    k_scale_cols<<<grid, 256, 0, s>>>(mat.ptr, l, scale.ptr, l, l, us.ptr, l);
+    FQB_LAUNCHED();
+    h.lc.bump();
+    // U = Q U~ (this rank's rows), V = Bt (U~ Sigma^-1)
+    gemm(false, m, l, l, 1.0, q, ldq, mat.ptr, l, 0.0, u, ldu, h.gws, h.num_sms, s, h.lc);
+    gemm(false, n, l, l, 1.0, bt, ldbt, us.ptr, l, 0.0, v, ldv, h.gws, h.num_sms, s, h.lc);
+    FQB_CUDA(cudaStreamSynchronize(s));  // the temporaries above are released on return
+}
+
+void destroy_cusolver(Handle& h) {
+    if (h.cusolver) cusolver().destroy(static_cast<cusolverDnHandle_t>(h.cusolver));
+    h.cusolver = nullptr;
+}
+
+}  // namespace farqb

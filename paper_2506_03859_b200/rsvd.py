@@ -218,10 +218,19 @@ class QBResult:
     resolved_p: float
     elapsed_ms: float
     gpu_launches: int
+    # rsvd::ApproxSvd fields (driver.hpp:45-58), present when svd=True
+    u: object = None
+    sigma: Optional[np.ndarray] = None
+    v: object = None
+    v_flagged: Optional[np.ndarray] = None
+    svd_residual_sq: Optional[float] = None
 
     @property
     def b(self):
         return None if self.bt is None else self.bt.T
+
+    def svd_rank(self) -> int:
+        return 0 if self.sigma is None else len(self.sigma)
 
 
 def default_density(kind: SketchKind, n: int) -> float:
@@ -341,16 +350,20 @@ class Engine:
 
     # ---- the QB loop --------------------------------------------------------
     def run_fixed_precision(self, a, cfg: FarpcaConfig, source: BlockSource | None = None,
-                            output: str = "device") -> QBResult:
-        return self._run(a, cfg, source, output, rank=None)
+                            output: str = "device", svd: bool = False) -> QBResult:
+        """svd=True also assembles U, sigma, V (rsvd::ApproxSvd, assemble_svd)."""
+        return self._run(a, cfg, source, output, rank=None, svd=svd)
 
     def run_fixed_rank(self, a, rank: int, cfg: FarpcaConfig, source: BlockSource | None = None,
-                       output: str = "device") -> QBResult:
-        return self._run(a, cfg, source, output, rank=rank)
+                       output: str = "device", svd: bool = False) -> QBResult:
+        """svd=True returns exactly `rank` triplets (drop_smallest, driver.cpp:85-106)."""
+        return self._run(a, cfg, source, output, rank=rank, svd=svd)
 
-    def _run(self, a, cfg, source, output, rank):
+    def _run(self, a, cfg, source, output, rank, svd=False):
         ptr, m, n, lda, on_dev, keep = _as_colmajor(a)
         flags = {"device": N.OUT_DEVICE, "host": N.OUT_HOST, "none": N.OUT_NONE}[output]
+        if svd:
+            flags |= N.OUT_SVD
         res = N.ResultC()
         ccfg = cfg._c()
         cb, err, hold = self._make_source(source)
@@ -437,9 +450,29 @@ class Engine:
                   if res.blocks and res.block_residuals else np.zeros(0))
             ids = (np.ctypeslib.as_array(res.block_ids, (res.n_ids,)).tolist()
                    if res.n_ids and res.block_ids else [])
-            return QBResult(q, bt, l, res.blocks, bool(res.converged), res.residual_sq, res.norm_a_sq,
-                            br, [int(i) for i in ids], res.resolved_block, res.resolved_max_iters,
-                            res.resolved_p, res.elapsed_ms, res.gpu_launches)
+            out = QBResult(q, bt, l, res.blocks, bool(res.converged), res.residual_sq, res.norm_a_sq,
+                           br, [int(i) for i in ids], res.resolved_block, res.resolved_max_iters,
+                           res.resolved_p, res.elapsed_ms, res.gpu_launches)
+            if res.sigma:
+                r = res.svd_rank
+                out.sigma = np.ctypeslib.as_array(res.sigma, (max(r, 1),))[:r].copy()
+                out.v_flagged = np.frombuffer(C.string_at(res.v_flagged, r), dtype=np.int8).astype(bool)
+                out.svd_residual_sq = res.svd_residual_sq
+                if r > 0 and res.u and output == "device":
+                    import torch
+                    ub = _DeviceBuffer(res.u, m, r, res.ldu)
+                    vb = _DeviceBuffer(res.v, n, r, res.ldv)
+                    res.u = None
+                    res.v = None
+                    with torch.cuda.device(self.device):
+                        out.u = torch.as_tensor(ub, device=f"cuda:{self.device}").t()
+                        out.v = torch.as_tensor(vb, device=f"cuda:{self.device}").t()
+                elif r > 0 and res.u and output == "host":
+                    out.u = np.ctypeslib.as_array(C.cast(res.u, C.POINTER(C.c_double)), (m * r,)).reshape(
+                        (m, r), order="F").copy()
+                    out.v = np.ctypeslib.as_array(C.cast(res.v, C.POINTER(C.c_double)), (n * r,)).reshape(
+                        (n, r), order="F").copy()
+            return out
         finally:
             self._lib.fqb_result_free(C.byref(res))
 
@@ -507,15 +540,60 @@ def default_engine(device: int = 0) -> Engine:
 
 
 def run_fixed_precision(a, cfg: FarpcaConfig, source: BlockSource | None = None,
-                        output: str = "device", device: int = 0) -> QBResult:
-    """rsvd::run_fixed_precision (driver.hpp:98-99) on the B200 engine."""
-    return default_engine(device).run_fixed_precision(a, cfg, source, output)
+                        output: str = "device", device: int = 0, svd: bool = True) -> QBResult:
+    """rsvd::run_fixed_precision (driver.hpp:98-99) on the B200 engine: the QB factors
+    plus, like the reference's ApproxSvd, U, sigma (ascending) and V."""
+    return default_engine(device).run_fixed_precision(a, cfg, source, output, svd=svd)
 
 
 def run_fixed_rank(a, rank: int, cfg: FarpcaConfig, source: BlockSource | None = None,
-                   output: str = "device", device: int = 0) -> QBResult:
-    """rsvd::run_fixed_rank (driver.hpp:101-103) on the B200 engine (QB of nblocks * b columns)."""
-    return default_engine(device).run_fixed_rank(a, rank, cfg, source, output)
+                   output: str = "device", device: int = 0, svd: bool = True) -> QBResult:
+    """rsvd::run_fixed_rank (driver.hpp:101-103): QB of ceil(rank/b)*b columns and an
+    ApproxSvd of exactly `rank` triplets (the overshoot dropped like drop_smallest)."""
+    return default_engine(device).run_fixed_rank(a, rank, cfg, source, output, svd=svd)
+
+
+def truncate_to_tolerance(res: QBResult, eps_rel: float, norm_a: float) -> QBResult:
+    """rsvd::truncate_to_tolerance (driver.cpp:415-433) on an assembled result:
+    drop the smallest triplets while the residual stays within (eps_rel*norm_a)^2."""
+    import copy
+    if eps_rel < 0.0 or norm_a < 0.0:
+        raise ConfigError("truncate_to_tolerance: negative tolerance or norm")
+    if res.sigma is None:
+        raise InvalidArgument("truncate_to_tolerance needs an assembled SVD (svd=True)")
+    target = eps_rel * norm_a
+    budget = target * target * (1.0 + 1e-12)
+    acc = res.svd_residual_sq
+    drop = 0
+    while drop < len(res.sigma):
+        nxt = acc + res.sigma[drop] * res.sigma[drop]
+        if nxt > budget:
+            break
+        acc = nxt
+        drop += 1
+    if drop == 0:
+        return res
+    out = copy.copy(res)
+    out.sigma = res.sigma[drop:].copy()
+    out.v_flagged = res.v_flagged[drop:].copy()
+    out.u = res.u[:, drop:] if res.u is not None else None
+    out.v = res.v[:, drop:] if res.v is not None else None
+    out.svd_residual_sq = acc
+    return out
+
+
+def estimate_cost(m: float, n: float, l: float, power: int, block: int, p: float, kind: SketchKind):
+    """rsvd::estimate_cost (driver.cpp:435-447): multiply-add counts of the dense
+    (Gaussian) loop and the accelerated (sparse) loop, and their ratio."""
+    if m < 1 or n < 1 or l < 1 or block < 1 or power < 0:
+        raise ConfigError("estimate_cost: arguments must be positive")
+    pw, b = float(power), float(block)
+    common = 1.5 * (m + n) * l * l + pw * (2.0 * m * n * l + n * l * l + 2.0 * n * l * b)
+    dense = 2.0 * m * n * l + common
+    accel = dense
+    if SketchKind(kind) != SketchKind.Gaussian:
+        accel = m * n * l + m * n * l * p + m * np.sqrt(n * l) + common
+    return dense, accel, accel / dense
 
 
 def gen_sketch(spec: SketchSpec, n: int, l: int, block_id: int, device: int = 0) -> SketchBlock:

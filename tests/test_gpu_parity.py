@@ -214,16 +214,27 @@ def test_qb_matches_golden_reference_runs(golden, golden_mats):
         tag = f"{r['matrix']} {r['kind']} P={r['power']} rank={r['rank']}"
         try:
             if r["rank"] is None:
-                res = fqb.run_fixed_precision(a, cfg, output="host")
+                res = fqb.run_fixed_precision(a, cfg, output="host", svd=True)
                 status = 0
             else:
-                res = fqb.run_fixed_rank(a, r["rank"], cfg, output="host")
+                res = fqb.run_fixed_rank(a, r["rank"], cfg, output="host", svd=True)
                 status = 0
         except fqb.ToleranceNotReached as e:
             res, status = e.partial, 4
         assert status == r["status"], tag
+        # ApproxSvd parity: sigma ascending, rank after the fixed-rank drop, residual incl. dropped energy
+        sig = np.array(r["sigma"])
+        assert res.svd_rank() == r["out_rank"], tag
+        assert abs(res.svd_residual_sq - r["residual_sq"]) <= 1e-10 * r["norm_a_sq"], tag
+        top = sig >= 1e-3 * sig[-1]
+        tol = 1e-10 if r["power"] >= 1 else 1e-7
+        assert np.max(np.abs(res.sigma[top] - sig[top])) <= tol * sig[-1], tag
+        # U, V reproduce B: A ~ U diag(sigma) V' equals Q B to rounding
+        recon = (res.u * res.sigma) @ res.v.T
+        if r["rank"] is None:
+            assert np.linalg.norm(recon - res.q @ res.bt.T) <= 1e-10 * np.sqrt(r["norm_a_sq"]), tag
         if r["rank"] is not None:
-            # fixed rank returns the QB of nblocks*b columns; the reference drops the overshoot
+            assert res.blocks == r["blocks"] and res.block_ids == r["block_ids"], tag
             continue
 
         class R:  # golden as an oracle-like record
@@ -343,3 +354,27 @@ def test_indicator_equals_true_residual():
         true = np.linalg.norm(a - res.q @ res.bt.T) ** 2
         assert abs(res.residual_sq - true) <= 1e-10 * res.norm_a_sq
         assert np.all(np.diff(res.block_residuals) <= 1e-12 * res.norm_a_sq)
+
+
+def test_truncate_to_tolerance_and_estimate_cost(golden_mats):
+    """driver.cpp:415-447 on an assembled GPU result (test_driver.cpp:273-297, 357-382)."""
+    a = golden_mats["slow128"]
+    cfg = FarpcaConfig(power=1, block=10, sketch=SketchSpec(0, 0.0, 81))
+    svd = fqb.run_fixed_rank(a, 40, cfg, output="host", svd=True)
+    norm_a = np.sqrt(svd.norm_a_sq)
+    assert fqb.truncate_to_tolerance(svd, 0.0, norm_a).svd_rank() == 40
+    none = fqb.truncate_to_tolerance(svd, 1.0, norm_a)
+    assert none.svd_rank() == 0 and abs(none.svd_residual_sq - svd.norm_a_sq) <= 1e-10 * svd.norm_a_sq
+    eps = 5e-3
+    cut = fqb.truncate_to_tolerance(svd, eps, norm_a)
+    budget = (eps * norm_a) ** 2 * (1 + 1e-12)
+    assert cut.svd_residual_sq <= budget
+    if 0 < cut.svd_rank() < 40:
+        assert cut.svd_residual_sq + cut.sigma[0] ** 2 > budget
+    with pytest.raises(fqb.ConfigError):
+        fqb.truncate_to_tolerance(svd, -1.0, norm_a)
+    d, acc, ratio = fqb.estimate_cost(1000, 1000, 100, 2, 20, 0.01, SketchKind.SparseSign)
+    common = 1.5 * 2000 * 100 ** 2 + 2 * (2 * 1e6 * 100 + 1000 * 100 ** 2 + 2 * 1000 * 100 * 20)
+    assert d == 2 * 1e6 * 100 + common
+    assert acc == 1e6 * 100 + 1e6 * 100 * 0.01 + 1000 * np.sqrt(1000 * 100) + common
+    assert fqb.estimate_cost(1000, 1000, 100, 2, 20, 0.01, SketchKind.Gaussian)[2] == 1.0
