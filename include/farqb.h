@@ -150,7 +150,9 @@ typedef struct fqb_handle_s* fqb_handle;
 int fqb_abi_version(void);
 fqb_status fqb_create(int device, fqb_handle* out);
 fqb_status fqb_destroy(fqb_handle h);
-/* Run subsequent work on this cudaStream_t (NULL = the handle's own stream). */
+/* Run subsequent work on this cudaStream_t (NULL = the handle's own stream, which
+ * is a blocking stream: it waits for work queued on the legacy default stream).
+ * Device inputs must be complete in the order of the stream the handle uses. */
 fqb_status fqb_set_stream(fqb_handle h, void* cuda_stream);
 fqb_status fqb_synchronize(fqb_handle h);
 const char* fqb_last_error(void);

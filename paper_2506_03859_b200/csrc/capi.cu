@@ -88,7 +88,11 @@ fqb_status fqb_create(int device, fqb_handle* out) {
         farqb::Handle& h = hs->h;
         h.device = device;
         FQB_CUDA(cudaDeviceGetAttribute(&h.num_sms, cudaDevAttrMultiProcessorCount, device));
-        FQB_CUDA(cudaStreamCreateWithFlags(&h.own_stream, cudaStreamNonBlocking));
+        // A blocking stream: work on it is ordered after work the caller queued on the
+        // legacy default stream (e.g. PyTorch producing A), so a device-resident A is
+        // always complete when the engine reads it.  Callers on other streams pass
+        // their stream with fqb_set_stream.
+        FQB_CUDA(cudaStreamCreateWithFlags(&h.own_stream, cudaStreamDefault));
         h.stream = h.own_stream;
         FQB_CUDA(cudaEventCreate(&h.ev0));
         FQB_CUDA(cudaEventCreate(&h.ev1));
