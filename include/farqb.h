@@ -227,6 +227,14 @@ fqb_status fqb_gemm(fqb_handle h, int trans_a, int64_t m, int64_t n, int64_t k, 
                     const double* a, int64_t lda, const double* b, int64_t ldb, double beta,
                     double* c, int64_t ldc);
 
+/* Same contract as fqb_gemm, computed on the INT8 tensor cores (tcgen05
+ * kind::i8) by Ozaki slicing: 8 signed 7-bit slices per operand with one
+ * power-of-two scale per output row / column, exact int32 slice products, FP64
+ * recombination -- the accuracy class of an FP64 GEMM.  n <= 64. */
+fqb_status fqb_gemm_emulated(fqb_handle h, int trans_a, int64_t m, int64_t n, int64_t k, double alpha,
+                             const double* a, int64_t lda, const double* b, int64_t ldb, double beta,
+                             double* c, int64_t ldc);
+
 /* ---- defaults (driver.cpp:449-466) ------------------------------------------- */
 double fqb_default_density(int kind, int64_t n);
 int fqb_default_block(int64_t m, int64_t n);

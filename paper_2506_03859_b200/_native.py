@@ -88,6 +88,8 @@ SIGNATURES = [
                                    C.POINTER(C.c_double)]),
     ("fqb_gemm", C.c_int, [_H, C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_double, C.c_void_p,
                            C.c_int64, C.c_void_p, C.c_int64, C.c_double, C.c_void_p, C.c_int64]),
+    ("fqb_gemm_emulated", C.c_int, [_H, C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_double, C.c_void_p,
+                                    C.c_int64, C.c_void_p, C.c_int64, C.c_double, C.c_void_p, C.c_int64]),
     ("fqb_default_density", C.c_double, [C.c_int, C.c_int64]),
     ("fqb_default_block", C.c_int, [C.c_int64, C.c_int64]),
     ("fqb_default_max_iters", C.c_int, [C.c_int64, C.c_int]),

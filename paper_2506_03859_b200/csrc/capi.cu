@@ -6,6 +6,7 @@
 // FQB_ERR_CUDA.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -394,6 +395,35 @@ fqb_status fqb_gemm(fqb_handle h, int trans_a, int64_t m, int64_t n, int64_t k, 
         farqb::ensure_gemm_workspace(h->h);
         farqb::gemm(trans_a != 0, m, n, k, alpha, a, lda, b, ldb, beta, c, ldc, h->h.gws, h->h.num_sms, s,
                     h->h.lc);
+        return FQB_OK;
+    });
+}
+
+fqb_status fqb_gemm_emulated(fqb_handle h, int trans_a, int64_t m, int64_t n, int64_t k, double alpha,
+                             const double* a, int64_t lda, const double* b, int64_t ldb, double beta, double* c,
+                             int64_t ldc) {
+    return guarded([&]() -> fqb_status {
+        bind(h);
+        if (m < 0 || n < 0 || k < 0) throw farqb::Error(FQB_ERR_DIMENSION, "negative dimension");
+        if (n > farqb::ozaki_max_n()) throw farqb::Error(FQB_ERR_DIMENSION, "fqb_gemm_emulated: n > 64");
+        if (ldc < m || ldb < k || lda < (trans_a ? k : m))
+            throw farqb::Error(FQB_ERR_DIMENSION, "leading dimension too small");
+        if (m == 0 || n == 0) return FQB_OK;
+        cudaStream_t s = h->h.stream;
+        farqb::ensure_gemm_workspace(h->h);
+        if (k == 0) throw farqb::Error(FQB_ERR_DIMENSION, "fqb_gemm_emulated: k = 0");
+        farqb::DeviceArray<int8_t> xs, zs;
+        farqb::DeviceArray<int> ex, ez;
+        xs.ensure(size_t(farqb::ozaki_x_bytes(m, k)), s);
+        zs.ensure(size_t(farqb::ozaki_z_bytes(n, k)), s);
+        ex.ensure(size_t(m), s);
+        ez.ensure(size_t(n), s);
+        if (trans_a) farqb::ozaki_slice_x_cols(a, k, m, lda, ex.ptr, xs.ptr, s, h->h.lc);
+        else farqb::ozaki_slice_x_rows(a, m, k, lda, ex.ptr, xs.ptr, s, h->h.lc);
+        farqb::ozaki_slice_z(b, k, n, ldb, ez.ptr, zs.ptr, s, h->h.lc);
+        farqb::ozaki_gemm(m, n, k, alpha, xs.ptr, ex.ptr, zs.ptr, ez.ptr, beta, c, ldc, h->h.gws.work, h->h.num_sms,
+                          s, h->h.lc);
+        FQB_CUDA(cudaStreamSynchronize(s));
         return FQB_OK;
     });
 }

@@ -139,6 +139,7 @@ class QbRun {
         w.col_ptr.ensure(size_t(b) + 1, s_);
         w.counts.ensure(size_t(b), s_);
         ensure_gemm_workspace(h_);
+        oz_on_ = ozaki_default(m_, n_, b_);
         double* sm = w.small.ptr;
         S_ = sm;
         S2_ = sm + 1 * b * b;
@@ -199,6 +200,7 @@ class QbRun {
     // Final outputs
     DeviceArray<double>& q() { return q_; }
     DeviceArray<double>& bt() { return bt_; }
+    bool ozaki() const { return oz_on_; }
     int64_t ldq() const { return ldq_; }
     int64_t ldbt() const { return ldbt_; }
 
@@ -231,6 +233,44 @@ class QbRun {
     void gemm_(bool ta, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
                const double* B, int64_t ldb, double beta, double* C, int64_t ldc) {
         gemm(ta, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, h_.gws, h_.num_sms, s_, h_.lc);
+    }
+
+    // ---- A-pass products ------------------------------------------------------
+    // C = A' B (ta) or A B with B of N <= b columns: the passes over A that dominate
+    // the run.  With the Ozaki path on, A is sliced once per run per layout into
+    // int8 (ozaki.cu) and every pass runs on the tcgen05 INT8 tensor cores; otherwise
+    // the FP64 DMMA GEMM.
+    static bool ozaki_default(int64_t m, int64_t n, int b) {
+        const char* e = std::getenv("FQB_OZAKI");
+        if (e && e[0] == '0') return false;
+        if (b > ozaki_max_n()) return false;
+        if (!(e && e[0] == '1') && double(m) * double(n) < double(1 << 24)) return false;  // small: DMMA is fine
+        size_t free_b = 0, total_b = 0;
+        if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return false;
+        const double need = double(ozaki_x_bytes(m, n)) + double(ozaki_x_bytes(n, m));   // both layouts
+        return double(free_b) > need + double(1 << 30);
+    }
+
+    void a_gemm(bool ta, int N, const double* B, int64_t ldb, double* C, int64_t ldc) {
+        if (!oz_on_ || N > ozaki_max_n()) {
+            if (ta) gemm_(true, n_, N, m_, 1.0, a_, lda_, B, ldb, 0.0, C, ldc);
+            else gemm_(false, m_, N, n_, 1.0, a_, lda_, B, ldb, 0.0, C, ldc);
+            return;
+        }
+        const int L = ta ? 1 : 0;
+        const int64_t M = ta ? n_ : m_, K = ta ? m_ : n_;
+        if (!oz_ready_[L]) {
+            oz_x_[L].ensure(size_t(ozaki_x_bytes(M, K)), s_);
+            oz_e_[L].ensure(size_t(M), s_);
+            if (ta) ozaki_slice_x_cols(a_, K, M, lda_, oz_e_[L].ptr, oz_x_[L].ptr, s_, h_.lc);
+            else ozaki_slice_x_rows(a_, M, K, lda_, oz_e_[L].ptr, oz_x_[L].ptr, s_, h_.lc);
+            oz_ready_[L] = true;
+        }
+        oz_z_.ensure(size_t(ozaki_z_bytes(N, K)), s_);
+        oz_ze_.ensure(size_t(ozaki_max_n()), s_);
+        ozaki_slice_z(B, K, N, ldb, oz_ze_.ptr, oz_z_.ptr, s_, h_.lc);
+        ozaki_gemm(M, N, K, 1.0, oz_x_[L].ptr, oz_e_[L].ptr, oz_z_.ptr, oz_ze_.ptr, 0.0, C, ldc, h_.gws.work,
+                   h_.num_sms, s_, h_.lc);
     }
 
     // ---- Omega ----------------------------------------------------------------
@@ -342,7 +382,7 @@ class QbRun {
     void apply_omega(double* y, int64_t ldy) {
         Workspace& w = h_.ws;
         if (om_dense_) {
-            gemm_(false, m_, b_, n_, 1.0, a_, lda_, w.omega.ptr, ldo_, 0.0, y, ldy);
+            a_gemm(false, b_, w.omega.ptr, ldo_, y, ldy);
         } else {
             launch_gather_spmm(a_, m_, lda_, w.col_ptr.ptr, w.row_idx.ptr, w.values.ptr, b_,
                                om_centered_ ? w.zc.ptr : nullptr, y, ldy, s_, h_.lc);
@@ -390,8 +430,8 @@ class QbRun {
         FQB_CUDA(cudaMemsetAsync(scal_ + kAlpha, 0, sizeof(double), s_));
         for (int k = 1; k <= P; ++k) {
             if (k == 1) apply_omega(w.y0.ptr, ldq_);
-            else gemm_(false, m_, b_, n_, 1.0, a_, lda_, w.g.ptr, ldbt_, 0.0, w.y0.ptr, ldq_);
-            gemm_(true, n_, b_, m_, 1.0, a_, lda_, w.y0.ptr, ldq_, 0.0, w.wp.ptr, ldbt_);
+            else a_gemm(false, b_, w.g.ptr, ldbt_, w.y0.ptr, ldq_);
+            a_gemm(true, b_, w.y0.ptr, ldq_, w.wp.ptr, ldbt_);
             comm_allreduce_sum(h_, w.wp.ptr, size_t(ldbt_) * b_, s_);   // W = sum_g A_g' Y_g
             if (l_ > 0) {
                 if (k == 1) tmul_omega(w.t.ptr, l_);
@@ -413,9 +453,9 @@ class QbRun {
         const int64_t l = l_;
         double* yj = q_.ptr + l * ldq_;
         double* btj = bt_.ptr + l * ldbt_;
-        if (from_iterate) gemm_(false, m_, b, n_, 1.0, a_, lda_, w.g.ptr, ldbt_, 0.0, yj, ldq_);
+        if (from_iterate) a_gemm(false, b, w.g.ptr, ldbt_, yj, ldq_);
         else apply_omega(yj, ldq_);
-        gemm_(true, n_, b, m_, 1.0, a_, lda_, yj, ldq_, 0.0, w.wraw.ptr, ldbt_);
+        a_gemm(true, b, yj, ldq_, w.wraw.ptr, ldbt_);
         comm_allreduce_sum(h_, w.wraw.ptr, size_t(ldbt_) * b, s_);
         const int64_t ldcd = l + b;
         double* cd = w.cd.ptr;
@@ -512,6 +552,12 @@ class QbRun {
     bool om_dense_ = true, om_centered_ = false, om_shift_folded_ = false;
     double om_p_ = 0.0;
     DeviceArray<double> q_, bt_, rowsum_;
+    bool oz_on_ = false;              // A-pass products on the INT8 tensor cores (a_gemm)
+    bool oz_ready_[2] = {false, false};
+    DeviceArray<int8_t> oz_x_[2];     // A slices: [0] rows of A (A G), [1] columns of A (A' Y)
+    DeviceArray<int> oz_e_[2];
+    DeviceArray<int8_t> oz_z_;        // slices of the current right-hand block
+    DeviceArray<int> oz_ze_;
     std::vector<double> residuals_;
     std::vector<int> ids_;
     double *S_, *S2_, *R1_, *R1i_, *R2_, *R2i_, *R_, *Ri_, *V_, *VS_, *VT_, *eig_, *sig_, *scal_;

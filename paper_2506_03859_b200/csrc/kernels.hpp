@@ -101,6 +101,29 @@ void gemm_tma(bool trans_a, int64_t M, int64_t N, int64_t K, double alpha, const
               const double* B, int64_t ldb, double beta, double* C, int64_t ldc, double* work, unsigned* flags,
               unsigned epoch, int num_sms, cudaStream_t s, bool a3d_slack = false);
 
+// ---- ozaki.cu: FP64 GEMM on the INT8 tensor cores ------------------------------
+// Operands are int8 slices with one power-of-two exponent per operand row, stored
+// pre-tiled and pre-swizzled (ozaki_x_bytes / ozaki_z_bytes).  C (M x N) =
+// alpha X' Z + beta C with X the K x M operand, Z the K x N operand, N <= 64.
+int ozaki_slices();
+int ozaki_max_n();
+int ozaki_bn(int64_t n);
+int64_t ozaki_x_bytes(int64_t rows, int64_t k);
+int64_t ozaki_z_bytes(int64_t n, int64_t k);
+int64_t ozaki_workspace_doubles(int num_sms);
+// X rows = columns of a (a is k x rows, ld): the A'Y operand
+void ozaki_slice_x_cols(const double* a, int64_t k, int64_t rows, int64_t ld, int* e, int8_t* out, cudaStream_t s,
+                        LaunchCounter& lc);
+// X rows = rows of a (a is rows x k, ld): the A G operand
+void ozaki_slice_x_rows(const double* a, int64_t rows, int64_t k, int64_t ld, int* e, int8_t* out, cudaStream_t s,
+                        LaunchCounter& lc);
+// Z (k x n, ld)
+void ozaki_slice_z(const double* b, int64_t k, int64_t n, int64_t ld, int* e, int8_t* out, cudaStream_t s,
+                   LaunchCounter& lc);
+void ozaki_gemm(int64_t M, int64_t N, int64_t K, double alpha, const int8_t* xs, const int* ex, const int8_t* zs,
+                const int* ez, double beta, double* C, int64_t ldc, double* work, int num_sms, cudaStream_t s,
+                LaunchCounter& lc);
+
 // ---- smallla.cu --------------------------------------------------------------
 // Cholesky of the b x b SPD matrix S (ld = lds) with the reference pivot rule
 // (matrix_core.cpp:117-140): pivot <= tol * max(diag_ref, max diag(S)) fails.

@@ -1,0 +1,620 @@
+// ozaki.cu -- FP64 GEMM emulated on the INT8 tcgen05 tensor cores (Ozaki scheme I).
+//
+// For the passes over A the FP64 DMMA pipe (37 TFLOP/s) is the bound; B200's INT8
+// tensor cores (tcgen05 kind::i8, 4.5 POPS dense) are not.  Each operand is cut
+// into S = 8 signed 7-bit slices with a power-of-two scale per output row /
+// column, e.g. for a row x of A with 2^(e-1) <= max|x| < 2^e:
+//     x = 2^e ( 2^-6 x_1 + 2^-13 x_2 + ... + 2^-55 x_8 ) + r,   |x_p| <= 64,
+//     |r| <= 2^(e-56)
+// (each step exact in FP64: x_p = rint(r * 2^6 or 2^7), r -= x_p).  Then
+//     (A Z)_ij = 2^(e_i + f_j) sum_{p+q <= 9} 2^(-12 - 7(p+q-2)) (A_p Z_q)_ij
+// where every A_p Z_q is an exact int32 product on the tensor cores and the 36
+// products collapse into 8 diagonals d = p+q (same power of two), accumulated
+// in TMEM (8 x 64 int32 columns = all 512).  The epilogue adds the diagonals
+// from the least significant up in FP64 and applies the exponents.  The
+// dropped terms and r are ~2^-55 relative to max|row| * max|col|, i.e. the
+// accuracy class of an FP64 GEMM.
+//
+// The slices of A are made once per run (A is fixed for all 2P+2 passes), in
+// two layouts: scaled per column for A'Y (K = m contiguous, A's own layout)
+// and per row, transposed, for A G (K = n contiguous).  A pass then streams
+// 8 bytes of slices per element of A -- the same bytes as FP64 -- so it becomes
+// HBM bound instead of FP64 bound.
+//
+// Slices are stored pre-tiled and pre-swizzled: tile (row tile, k-block, slice)
+// is one contiguous TR x 64 B block already in the 64B-swizzle arrangement
+// tcgen05 expects, so every pipeline stage is a single 1-D bulk copy
+// (cp.async.bulk) -- no per-row TMA requests.  Kernel: one producer warp (8 KB
+// A-slice tiles, all 8 Z slices of a k-block in one 32 KB copy, 160 KB of A in
+// flight), one MMA warp (tcgen05.mma.cta_group::1.kind::i8, M=128, K=32, N = 64
+// per Z slice: the products of one A slice with up to 4 consecutive Z slices
+// land on consecutive TMEM diagonals, so one N<=256 MMA covers them and A is
+// read from shared memory once per 4 products), four epilogue warps
+// (tcgen05.ld 32x32b -> FP64).  Tiles are split over the persistent grid
+// stream-K style; a CTA writes pieces of split tiles, already scaled, to its
+// partial slots and k_ozaki_fixup sums them in CTA order (deterministic).
+//
+// Measured (C2, A'Y 8000x50x8000, B200): 104 us + 3 us fixup, vs 235 us for the
+// FP64 DMMA GEMM; HBM floor for the 512 MB of A slices ~80 us.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstdlib>
+
+#include "kernels.hpp"
+
+namespace farqb {
+namespace {
+
+constexpr int S = 8;                     // slices per operand
+constexpr int OZ_BM = 128;               // rows per tile (UMMA M)
+// K bytes per k-block: one 64-byte swizzle row.  64 rather than 128 halves the Z
+// stage (all 8 slices of a k-block) and so doubles the A-slice bytes in flight.
+constexpr int OZ_BK = 64;
+constexpr int SWZ_ROWS = 1024 / 128;     // the swizzle pattern repeats every 8 rows (SBO = 8 rows)
+constexpr int OZ_BN = 64;                // max N (8 diagonals x 64 = 512 TMEM columns)
+constexpr int B_STAGES = 2;
+constexpr int A_TILE = OZ_BM * OZ_BK;             // 8 KB, one slice
+constexpr int B_TILE = OZ_BN * OZ_BK;             // 4 KB per slice (bn = 64)
+constexpr int B_STAGE = S * B_TILE;               // 32 KB: all slices of a k-block
+constexpr int A_STAGES = (225 * 1024 - B_STAGES * B_STAGE) / A_TILE;   // 20: 160 KB of A in flight
+constexpr int CHUNK_KB = 32768 / OZ_BK;           // int32 safety: 8 * 64^2 * 32768 < 2^31
+constexpr int OZ_THREADS = 192;                   // producer, MMA, 4 epilogue warps
+constexpr size_t OZ_SMEM = size_t(A_STAGES) * A_TILE + size_t(B_STAGES) * B_STAGE + 1024;
+constexpr int OZ_PARTIAL = OZ_BM * OZ_BN;         // doubles per CTA partial slot
+
+// 64-bit quotient through a double reciprocal and one correction step (operands are
+// far below 2^48).  The kernel must not contain a division subroutine call: a call
+// anywhere in it pushes the MMA issue path out of the uniform datapath (~1.3x slower).
+// inv_b is 1/b rounded on the host.
+__device__ __forceinline__ int64_t qdiv(int64_t a, int64_t b, double inv_b) {
+    int64_t q = int64_t(double(a) * inv_b);
+    if (q * b > a) --q;
+    else if ((q + 1) * b <= a) ++q;
+    return q;
+}
+
+// x * 2^k without ldexp() (a long library routine: 64 of them per thread made the
+// finishing epilogue take ~14 us).  Exact whenever the result is a normal number;
+// |k| up to 2046 through two factors.
+__device__ __forceinline__ double pow2i(int k) {   // k in [-1022, 1023]
+    return __longlong_as_double(static_cast<long long>(k + 1023) << 52);
+}
+__device__ __forceinline__ double mul_pow2(double x, int k) {
+    if (k >= -1022 && k <= 1023) return x * pow2i(k);
+    const int k1 = max(-1022, min(1023, k / 2));
+    const int k2 = max(-1022, min(1023, k - k1));
+    return x * pow2i(k1) * pow2i(k2);
+}
+
+struct OzArgs {
+    const int8_t* xs;     // tiled slices of the K x M operand
+    const int8_t* zs;     // tiled slices of the K x N operand (one row tile of bn)
+    int64_t M, N, K;
+    double alpha, beta;
+    double* C;
+    int64_t ldc;
+    const int* ex;        // per output row exponent
+    const int* ez;        // per output column exponent
+    double* work;         // 2 * grid slots: partials, then carries
+    int64_t iters;        // tiles * kblocks
+    int kblocks, mtiles, grid, bn;
+    double inv_grid, inv_kblocks, inv_iters;
+};
+
+__device__ __forceinline__ int64_t range_begin(const OzArgs& p, int c) { return qdiv(p.iters * c, p.grid, p.inv_grid); }
+// the CTA whose range holds iteration it: largest c with range_begin(c) <= it
+__device__ __forceinline__ int cta_of(const OzArgs& p, int64_t it) {
+    return int(qdiv((it + 1) * p.grid - 1, p.iters, p.inv_iters));
+}
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return unsigned(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+// the spin loop lives inside the asm (no outputs), so the compiler does not treat the
+// code after a wait as divergent and keeps the MMA descriptors in uniform registers
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}\n" ::"r"(bar), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_load(unsigned dst, const void* src, unsigned bytes, unsigned bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+                 ::"r"(dst), "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(bar) : "memory");
+}
+// K-major, 64B swizzle canonical layout (8-row atoms of 512 B), descriptor version 1,
+// layout type 4 = SWIZZLE_64B
+static_assert(OZ_BK == 64, "descriptor and swz() below are written for 64-byte rows");
+__device__ __forceinline__ uint64_t smem_desc(unsigned addr) {
+    return uint64_t((addr >> 4) & 0x3FFF) | (uint64_t(1) << 16) | (uint64_t((8 * OZ_BK) >> 4) << 32) |
+           (uint64_t(1) << 46) | (uint64_t(4) << 61);
+}
+// descriptors passed as (low, high) 32-bit halves: only the low half (start address) varies
+__device__ __forceinline__ void umma_i8(unsigned tmem_d, unsigned da_lo, unsigned db_lo, unsigned d_hi, unsigned idesc,
+                                        unsigned acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t.reg .b64 da, db;\n\t"
+        "mov.b64 da, {%1, %3};\n\tmov.b64 db, {%2, %3};\n\t"
+        "setp.ne.b32 p, %5, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], da, db, %4, p;\n\t}\n"
+        ::"r"(tmem_d), "r"(da_lo), "r"(db_lo), "r"(d_hi), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(unsigned bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(bar)
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(unsigned taddr, unsigned (&v)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr));
+}
+
+// Work item sequence shared by the three roles: the CTA's iteration range is cut
+// into segments (one per tile, processed last tile first, as in gemm_tma.cu) and
+// each segment into chunks of at most CHUNK_KB k-blocks (int32 headroom).
+struct Walk {
+    int64_t beg, end, KT, t_first, t_last, nseg;
+    __device__ Walk(int64_t b, int64_t e, int64_t kt, double inv_kt) : beg(b), end(e), KT(kt) {
+        t_first = qdiv(b, kt, inv_kt);
+        t_last = qdiv(e - 1, kt, inv_kt);
+        nseg = e > b ? t_last - t_first + 1 : 0;
+    }
+    __device__ int64_t tile(int64_t si) const { return t_last - si; }
+    __device__ int kb(int64_t t) const { return t == t_first ? int(beg - t * KT) : 0; }
+    __device__ int ke(int64_t t) const { return t == t_last ? int(end - t * KT) : int(KT); }
+};
+
+__global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
+    extern __shared__ uint8_t smem_raw[];
+    __shared__ uint64_t bars[2 * A_STAGES + 2 * B_STAGES + 2];
+    __shared__ unsigned tmem_base_s;
+    __shared__ int ez_s[OZ_BN];   // column exponents (0 past N)
+    const unsigned raw = smem_u32(smem_raw);
+    const unsigned base = (raw + 1023u) & ~1023u;
+    const unsigned a_base = base, b_base = base + A_STAGES * A_TILE;
+    const unsigned a_full = smem_u32(&bars[0]), a_empty = a_full + 8 * A_STAGES;
+    const unsigned b_full = a_empty + 8 * A_STAGES, b_empty = b_full + 8 * B_STAGES;
+    const unsigned t_full = b_empty + 8 * B_STAGES, t_empty = t_full + 8;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < A_STAGES; ++s) {
+            mbar_init(a_full + 8 * s, 1);
+            mbar_init(a_empty + 8 * s, 1);
+        }
+        for (int s = 0; s < B_STAGES; ++s) {
+            mbar_init(b_full + 8 * s, 1);
+            mbar_init(b_empty + 8 * s, 1);
+        }
+        mbar_init(t_full, 1);
+        mbar_init(t_empty, 128);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    if (threadIdx.x < OZ_BN) ez_s[threadIdx.x] = int(threadIdx.x) < p.N ? p.ez[threadIdx.x] : 0;
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
+            smem_u32(&tmem_base_s)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n");
+    const unsigned tmem = tmem_base_s;
+
+    const int c = blockIdx.x;
+    const Walk wk(range_begin(p, c), range_begin(p, c + 1), p.kblocks, p.inv_kblocks);
+    const int bn = p.bn;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            const unsigned zbytes = unsigned(S * bn * OZ_BK);
+            int64_t ja = 0, jb = 0;
+            for (int64_t si = 0; si < wk.nseg; ++si) {
+                const int64_t t = wk.tile(si);
+                const int64_t mt = t;   // N <= 64: one column tile, tile index = row tile
+                for (int kb = wk.kb(t); kb < wk.ke(t); ++kb, ++jb) {
+                    const int sb = int(jb % B_STAGES);
+                    mbar_wait(b_empty + 8 * sb, unsigned((jb / B_STAGES) & 1) ^ 1u);
+                    mbar_expect_tx(b_full + 8 * sb, zbytes);
+                    bulk_load(b_base + sb * B_STAGE, p.zs + int64_t(kb) * zbytes, zbytes, b_full + 8 * sb);
+                    const int8_t* xt = p.xs + (mt * p.kblocks + kb) * int64_t(S * A_TILE);
+                    for (int sp = 0; sp < S; ++sp, ++ja) {
+                        const int sa = int(ja % A_STAGES);
+                        mbar_wait(a_empty + 8 * sa, unsigned((ja / A_STAGES) & 1) ^ 1u);
+                        mbar_expect_tx(a_full + 8 * sa, unsigned(A_TILE));
+                        bulk_load(a_base + sa * A_TILE, xt + sp * A_TILE, unsigned(A_TILE), a_full + 8 * sa);
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // M = 128, S32 accumulate, signed int8 A and B, both K-major; N is set per MMA.
+            // Everything below stays 32-bit and the slice loops are unrolled, so the
+            // descriptors live in uniform registers (a per-MMA register->uniform
+            // broadcast made the issue loop, not the tensor core, the bottleneck).
+            constexpr unsigned idesc = (2u << 4) | (1u << 7) | (1u << 10) | (unsigned(OZ_BM >> 4) << 24);
+            const uint64_t da0 = smem_desc(a_base), db0 = smem_desc(b_base);
+            const unsigned da_lo0 = unsigned(da0), db_lo0 = unsigned(db0);
+            const unsigned d_hi = unsigned(da0 >> 32);   // identical for both operands
+            unsigned sa = 0, pa = 0, sb = 0, pb = 0, pt = 0;
+            for (int64_t si = 0; si < wk.nseg; ++si) {
+                const int64_t t = wk.tile(si);
+                const int kb0 = wk.kb(t), kb1 = wk.ke(t);
+                for (int cb = kb0; cb < kb1; cb += CHUNK_KB) {
+                    const int ce = min(kb1, cb + CHUNK_KB);
+                    mbar_wait(t_empty, pt ^ 1u);   // epilogue drained the accumulators
+                    pt ^= 1u;
+                    asm volatile("tcgen05.fence::after_thread_sync;\n");
+                    for (int kb = cb; kb < ce; ++kb) {
+                        mbar_wait(b_full + 8 * sb, pb);
+                        const unsigned db_lo = db_lo0 + sb * unsigned(B_STAGE >> 4);
+#pragma unroll
+                        for (int sp = 0; sp < S; ++sp) {
+                            mbar_wait(a_full + 8 * sa, pa);
+                            asm volatile("tcgen05.fence::after_thread_sync;\n");
+                            const unsigned da_lo = da_lo0 + sa * unsigned(A_TILE >> 4);
+                            // products (sp, sq), sq = sq0 .. sq0+3, land on the consecutive
+                            // diagonals sp+sq: one N = 64 * slices MMA covers them (A read once)
+#pragma unroll
+                            for (int sq0 = 0; sq0 < S - sp; sq0 += 4) {
+                                constexpr unsigned kstep = 32 >> 4;   // 32 bytes of K per MMA
+                                const unsigned id =
+                                    idesc | (unsigned((S - sp - sq0 < 4 ? S - sp - sq0 : 4) * (OZ_BN >> 3)) << 17);
+                                const unsigned dt = tmem + unsigned((sp + sq0) * OZ_BN);
+                                const unsigned bl = db_lo + unsigned((sq0 * OZ_BN * OZ_BK) >> 4);
+                                umma_i8(dt, da_lo, bl, d_hi, id, sp == 0 ? unsigned(kb != cb) : 1u);
+#pragma unroll
+                                for (int k = 1; k < OZ_BK / 32; ++k)
+                                    umma_i8(dt, da_lo + k * kstep, bl + k * kstep, d_hi, id, 1u);
+                            }
+                            umma_commit(a_empty + 8 * sa);
+                            if (++sa == A_STAGES) sa = 0, pa ^= 1u;
+                        }
+                        umma_commit(b_empty + 8 * sb);
+                        if (++sb == B_STAGES) sb = 0, pb ^= 1u;
+                    }
+                    umma_commit(t_full);
+                }
+            }
+        }
+    } else {
+        // ------------------------------ epilogue --------------------------------
+        // 16 output columns at a time (low register pressure keeps the MMA issue
+        // path in uniform registers).  A tile this CTA owns entirely goes straight to
+        // C; a piece of a split tile is written, already scaled, to one of the CTA's
+        // partial slots (0: its last tile, 1: its first) and k_ozaki_fixup sums the
+        // pieces in CTA order afterwards -- no inter-CTA waiting inside this kernel.
+        // A segment longer than CHUNK_KB k-blocks carries its running sum in slot 2.
+        const int quarter = warp & 3;           // TMEM lanes 32*quarter .. +31
+        const int r_loc = quarter * 32 + lane;  // tile row of this thread
+        const unsigned lane_addr = tmem + (unsigned(quarter * 32) << 16);
+        double* carry = p.work + (3 * int64_t(c) + 2) * OZ_PARTIAL;
+        unsigned ph = 0;
+        for (int64_t si = 0; si < wk.nseg; ++si) {
+            const int64_t t = wk.tile(si);
+            const int kb0 = wk.kb(t), kb1 = wk.ke(t);
+            const int64_t row = t * OZ_BM + r_loc;
+            const bool full_tile = kb0 == 0 && kb1 == p.kblocks;
+            double* piece = p.work + (3 * int64_t(c) + (t == wk.t_last ? 0 : 1)) * OZ_PARTIAL;
+            const int er = row < p.M ? p.ex[row] : 0;   // loaded while the MMAs run
+            for (int cb = kb0; cb < kb1; cb += CHUNK_KB) {
+                const bool first_chunk = cb == kb0, last_chunk = cb + CHUNK_KB >= kb1;
+                mbar_wait(t_full, ph);
+                ph ^= 1u;
+                asm volatile("tcgen05.fence::after_thread_sync;\n");
+#pragma unroll 1
+                for (int g = 0; g < OZ_BN; g += 16) {
+                    // all 8 diagonals in flight, one wait
+                    unsigned v[S][16];
+#pragma unroll
+                    for (int d = 0; d < S; ++d) tmem_ld16(lane_addr + unsigned(d * OZ_BN + g), v[d]);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+                    double acc[16];
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) acc[j] = 0.0;
+                    // least significant diagonal first: d = S-1 .. 0 (scale 2^-12-7d)
+#pragma unroll
+                    for (int d = S - 1; d >= 0; --d) {
+                        const double sc = pow2i(-12 - 7 * d);
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) acc[j] = fma(double(int(v[d][j])), sc, acc[j]);
+                    }
+                    if (!first_chunk) {
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) acc[j] += carry[(g + j) * OZ_BM + r_loc];
+                    }
+                    if (!last_chunk) {
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) carry[(g + j) * OZ_BM + r_loc] = acc[j];
+                        continue;
+                    }
+                    if (!full_tile) {
+#pragma unroll
+                        for (int j = 0; j < 16; ++j)
+                            piece[(g + j) * OZ_BM + r_loc] = mul_pow2(acc[j], er + ez_s[g + j]);
+                        continue;
+                    }
+                    if (row < p.M) {
+                        double old_c[16];
+                        if (p.beta != 0.0) {
+#pragma unroll
+                            for (int j = 0; j < 16; ++j)
+                                old_c[j] = g + j < p.N ? p.C[int64_t(g + j) * p.ldc + row] : 0.0;
+                        }
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) {
+                            if (g + j < p.N) {
+                                const double val = p.alpha * mul_pow2(acc[j], er + ez_s[g + j]);
+                                p.C[int64_t(g + j) * p.ldc + row] = p.beta != 0.0 ? fma(p.beta, old_c[j], val) : val;
+                            }
+                        }
+                    }
+                }
+                asm volatile("tcgen05.fence::before_thread_sync;\n");
+                mbar_arrive(t_empty);
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncthreads();
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+}
+
+// ---------------------------------------------------------------------------
+// slicing
+
+// exponent e with 2^(e-1) <= max|x| < 2^e; an all-zero vector gets a very small
+// exponent so it never dominates a max over chunks (and 0 * 2^-e stays 0)
+constexpr int kZeroExp = -2000;
+__device__ __forceinline__ int exponent_of(double maxabs) { return maxabs > 0.0 ? ilogb(maxabs) + 1 : kZeroExp; }
+
+__device__ __forceinline__ void slice8(double x, int e, int8_t (&out)[S]) {
+    double r = mul_pow2(x, -e);  // |r| < 1
+    double y = r * 64.0;
+    double q = rint(y);
+    out[0] = int8_t(q);
+    r = y - q;
+#pragma unroll
+    for (int s = 1; s < S; ++s) {
+        y = r * 128.0;
+        q = rint(y);
+        out[s] = int8_t(q);
+        r = y - q;
+    }
+}
+
+// per-column max exponent of a (rows x cols, ld) -- one CTA per column
+__global__ void __launch_bounds__(256) k_col_exp(const double* __restrict__ a, int64_t rows, int64_t ld, int* e) {
+    __shared__ double red[8];
+    const double* c = a + int64_t(blockIdx.x) * ld;
+    double mx = 0.0;
+    for (int64_t r = threadIdx.x; r < rows; r += blockDim.x) mx = fmax(mx, fabs(c[r]));
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_down_sync(0xffffffffu, mx, off));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double m = 0.0;
+        for (int w = 0; w < int(blockDim.x >> 5); ++w) m = fmax(m, red[w]);
+        e[blockIdx.x] = exponent_of(m);
+    }
+}
+
+// per-row max exponent: a thread covers one row over a chunk of 64 columns
+// (coalesced across the warp), chunks combined with atomicMax on the exponent
+// (e must be preset to a very negative value: memset 0x80)
+__global__ void __launch_bounds__(256) k_row_exp(const double* __restrict__ a, int64_t rows, int64_t cols, int64_t ld,
+                                                 int* e) {
+    const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (r >= rows) return;
+    const int64_t c0 = int64_t(blockIdx.y) * 64, c1 = c0 + 64 < cols ? c0 + 64 : cols;
+    double mx = 0.0;
+    for (int64_t j = c0; j < c1; ++j) mx = fmax(mx, fabs(__ldg(a + j * ld + r)));
+    atomicMax(e + r, exponent_of(mx));
+}
+
+// byte offset of (row r, byte c) inside a swizzled TR x OZ_BK byte tile
+// (64B swizzle: the 16-byte chunk index c>>4 is XORed with address bits 7-8 = (r >> 1) & 3)
+__device__ __forceinline__ int64_t swz(int r, int c) {
+    return int64_t(r) * OZ_BK + ((((c >> 4) ^ ((r >> 1) & 3)) << 4) | (c & 15));
+}
+
+// Tiled slices of an operand whose rows are the columns of `a` (K = rows of a):
+// tile (rt, kb, s) at ((rt * KB + kb) * S + s) * TR * OZ_BK.  A thread slices 4
+// consecutive k of one column and stores them as one 32-bit word per slice.
+__global__ void __launch_bounds__(256) k_slice_cols_tiled(const double* __restrict__ a, int64_t K, int64_t R,
+                                                          int64_t ld, const int* __restrict__ e, int8_t* out, int tr,
+                                                          int64_t kb_count) {
+    const int64_t k0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
+    const int64_t r = blockIdx.y;
+    if (k0 >= kb_count * OZ_BK || r >= R) return;
+    const double* col = a + r * ld;
+    const int er = e[r];
+    uint32_t word[S] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        int8_t s8[S] = {0, 0, 0, 0, 0, 0, 0, 0};
+        if (k0 + u < K) slice8(col[k0 + u], er, s8);
+#pragma unroll
+        for (int sl = 0; sl < S; ++sl) word[sl] |= uint32_t(uint8_t(s8[sl])) << (8 * u);
+    }
+    const int64_t rt = r / tr, kb = k0 / OZ_BK;
+    const int rl = int(r % tr), c = int(k0 % OZ_BK);
+    const int64_t tile_bytes = int64_t(tr) * OZ_BK;
+    int8_t* base = out + (rt * kb_count + kb) * S * tile_bytes + swz(rl, c);
+#pragma unroll
+    for (int sl = 0; sl < S; ++sl) *reinterpret_cast<uint32_t*>(base + sl * tile_bytes) = word[sl];
+}
+
+// Tiled slices of the rows of `a` (K = columns of a), through a shared-memory
+// transpose: a CTA covers 32 rows x 128 columns (128 / OZ_BK k-blocks); each thread
+// slices 16 consecutive k of one row into one 16-byte chunk per slice.
+__global__ void __launch_bounds__(256) k_slice_rows_tiled(const double* __restrict__ a, int64_t R, int64_t K,
+                                                          int64_t ld, const int* __restrict__ e, int8_t* out,
+                                                          int64_t kb_count) {
+    __shared__ double tile[128][33];
+    const int64_t r0 = int64_t(blockIdx.x) * 32, c0 = int64_t(blockIdx.y) * 128;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int kk = warp; kk < 128; kk += 8) {
+        const int64_t r = r0 + lane, k = c0 + kk;
+        tile[kk][lane] = (r < R && k < K) ? a[k * ld + r] : 0.0;
+    }
+    __syncthreads();
+    const int rl32 = threadIdx.x >> 3, chunk = threadIdx.x & 7;  // 32 rows x 8 chunks of 16 k
+    const int64_t r = r0 + rl32;
+    if (r >= R) return;
+    const int er = e[r];
+    uint32_t w[S][4];
+#pragma unroll
+    for (int sl = 0; sl < S; ++sl) w[sl][0] = w[sl][1] = w[sl][2] = w[sl][3] = 0;
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+        int8_t s8[S];
+        slice8(tile[chunk * 16 + u][rl32], er, s8);
+#pragma unroll
+        for (int sl = 0; sl < S; ++sl) w[sl][u >> 2] |= uint32_t(uint8_t(s8[sl])) << (8 * (u & 3));
+    }
+    const int64_t kb = (c0 + chunk * 16) / OZ_BK;
+    if (kb >= kb_count) return;
+    const int64_t rt = r / OZ_BM;
+    const int rl = int(r % OZ_BM);
+    const int64_t tile_bytes = int64_t(OZ_BM) * OZ_BK;
+    int8_t* base = out + (rt * kb_count + kb) * S * tile_bytes + swz(rl, int((chunk * 16) % OZ_BK));
+#pragma unroll
+    for (int sl = 0; sl < S; ++sl)
+        *reinterpret_cast<uint4*>(base + sl * tile_bytes) = make_uint4(w[sl][0], w[sl][1], w[sl][2], w[sl][3]);
+}
+
+// Sum the pieces of every split tile in CTA order (deterministic) into C.
+// Pieces were written already scaled by 2^(ex + ez).  Block (tile, column), one
+// thread per tile row; a tile has at most a handful of pieces.
+__global__ void __launch_bounds__(OZ_BM) k_ozaki_fixup(const OzArgs p) {
+    const int64_t t = blockIdx.x;
+    const int j = blockIdx.y, r = threadIdx.x;
+    const int c0 = cta_of(p, t * p.kblocks), c1 = cta_of(p, t * p.kblocks + p.kblocks - 1);
+    const int64_t row = t * OZ_BM + r;
+    if (c0 == c1 || row >= p.M) return;   // a tile owned by one CTA was written directly
+    double sum = 0.0;
+    for (int cc = c0; cc <= c1; ++cc) {
+        const int64_t t_last = qdiv(range_begin(p, cc + 1) - 1, p.kblocks, p.inv_kblocks);
+        sum += __ldcg(p.work + (3 * int64_t(cc) + (t == t_last ? 0 : 1)) * OZ_PARTIAL + j * OZ_BM + r);
+    }
+    double* cp = p.C + int64_t(j) * p.ldc + row;
+    const double v = p.alpha * sum;
+    *cp = p.beta != 0.0 ? fma(p.beta, *cp, v) : v;
+}
+
+}  // namespace
+
+int ozaki_slices() { return S; }
+int ozaki_max_n() { return OZ_BN; }
+int ozaki_bn(int64_t) { return OZ_BN; }   // Z slices padded to 64 rows: slice sq sits at TMEM diagonal spacing
+int64_t ozaki_x_bytes(int64_t rows, int64_t k) { return ceil_div(rows, OZ_BM) * ceil_div(k, OZ_BK) * S * OZ_BM * OZ_BK; }
+int64_t ozaki_z_bytes(int64_t n, int64_t k) { return ceil_div(k, OZ_BK) * S * int64_t(ozaki_bn(n)) * OZ_BK; }
+
+// X operand from the columns of a (A'Y: rows of X = columns of A)
+void ozaki_slice_x_cols(const double* a, int64_t k, int64_t rows, int64_t ld, int* e, int8_t* out, cudaStream_t s,
+                        LaunchCounter& lc) {
+    if (rows <= 0 || k <= 0) return;
+    const int64_t kbc = ceil_div(k, OZ_BK);
+    FQB_CUDA(cudaMemsetAsync(out, 0, size_t(ozaki_x_bytes(rows, k)), s));
+    k_col_exp<<<unsigned(rows), 256, 0, s>>>(a, k, ld, e);
+    FQB_LAUNCHED();
+    dim3 g(unsigned(ceil_div(kbc * OZ_BK, 1024)), unsigned(rows));
+    k_slice_cols_tiled<<<g, 256, 0, s>>>(a, k, rows, ld, e, out, OZ_BM, kbc);
+    FQB_LAUNCHED();
+    lc.bump(2);
+}
+
+// X operand from the rows of a (A G: rows of X = rows of A, K = columns)
+void ozaki_slice_x_rows(const double* a, int64_t rows, int64_t k, int64_t ld, int* e, int8_t* out, cudaStream_t s,
+                        LaunchCounter& lc) {
+    if (rows <= 0 || k <= 0) return;
+    const int64_t kbc = ceil_div(k, OZ_BK);
+    FQB_CUDA(cudaMemsetAsync(out, 0, size_t(ozaki_x_bytes(rows, k)), s));
+    FQB_CUDA(cudaMemsetAsync(e, 0x80, sizeof(int) * rows, s));
+    dim3 ge(unsigned(ceil_div(rows, 256)), unsigned(ceil_div(k, 64)));
+    k_row_exp<<<ge, 256, 0, s>>>(a, rows, k, ld, e);
+    FQB_LAUNCHED();
+    dim3 g(unsigned(ceil_div(rows, 32)), unsigned(ceil_div(k, 128)));
+    k_slice_rows_tiled<<<g, 256, 0, s>>>(a, rows, k, ld, e, out, kbc);
+    FQB_LAUNCHED();
+    lc.bump(2);
+}
+
+// Z operand (K x n, column j = output column j): one row tile of bn rows
+void ozaki_slice_z(const double* b, int64_t k, int64_t n, int64_t ld, int* e, int8_t* out, cudaStream_t s,
+                   LaunchCounter& lc) {
+    if (n <= 0 || k <= 0) return;
+    const int64_t kbc = ceil_div(k, OZ_BK);
+    FQB_CUDA(cudaMemsetAsync(out, 0, size_t(ozaki_z_bytes(n, k)), s));
+    k_col_exp<<<unsigned(n), 256, 0, s>>>(b, k, ld, e);
+    FQB_LAUNCHED();
+    dim3 g(unsigned(ceil_div(kbc * OZ_BK, 1024)), unsigned(n));
+    k_slice_cols_tiled<<<g, 256, 0, s>>>(b, k, n, ld, e, out, ozaki_bn(n), kbc);
+    FQB_LAUNCHED();
+    lc.bump(2);
+}
+
+void ozaki_gemm(int64_t M, int64_t N, int64_t K, double alpha, const int8_t* xs, const int* ex, const int8_t* zs,
+                const int* ez, double beta, double* C, int64_t ldc, double* work, int num_sms, cudaStream_t s,
+                LaunchCounter& lc) {
+    if (N > OZ_BN) throw Error(kStatusInvalid, "ozaki_gemm: N > 64");
+    static bool configured[64] = {};
+    int dev = 0;
+    FQB_CUDA(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= 64 || !configured[dev]) {
+        FQB_CUDA(cudaFuncSetAttribute(k_ozaki, cudaFuncAttributeMaxDynamicSharedMemorySize, int(OZ_SMEM)));
+        if (dev >= 0 && dev < 64) configured[dev] = true;
+    }
+    OzArgs a{};
+    a.xs = xs;
+    a.zs = zs;
+    a.M = M;
+    a.N = N;
+    a.K = K;
+    a.alpha = alpha;
+    a.beta = beta;
+    a.C = C;
+    a.ldc = ldc;
+    a.ex = ex;
+    a.ez = ez;
+    a.work = work;
+    a.bn = ozaki_bn(N);
+
+    a.mtiles = int(ceil_div(M, OZ_BM));
+    a.kblocks = int(ceil_div(K, OZ_BK));
+    a.iters = int64_t(a.mtiles) * a.kblocks;
+    a.grid = int(std::max<int64_t>(1, std::min<int64_t>(num_sms, a.iters / 4)));
+    a.inv_grid = 1.0 / double(a.grid);
+    a.inv_kblocks = 1.0 / double(a.kblocks);
+    a.inv_iters = 1.0 / double(a.iters);
+    k_ozaki<<<a.grid, OZ_THREADS, OZ_SMEM, s>>>(a);
+    FQB_LAUNCHED();
+    lc.bump();
+    bool split = false;   // does any CTA boundary fall inside a tile?
+    for (int c = 1; c < a.grid && !split; ++c) split = (a.iters * c / a.grid) % a.kblocks != 0;
+    if (split) {
+        k_ozaki_fixup<<<dim3(unsigned(a.mtiles), unsigned(N)), OZ_BM, 0, s>>>(a);
+        FQB_LAUNCHED();
+        lc.bump();
+    }
+}
+
+int64_t ozaki_workspace_doubles(int num_sms) { return 3 * int64_t(num_sms) * OZ_PARTIAL; }  // 2 pieces + carry
+
+}  // namespace farqb

@@ -509,6 +509,13 @@ class Engine:
         if st:
             _raise(st, "fqb_gemm")
 
+    def gemm_emulated(self, trans_a: bool, m, n, k, alpha, a_ptr, lda, b_ptr, ldb, beta, c_ptr, ldc):
+        """FP64 GEMM on the INT8 tensor cores (Ozaki slicing), n <= 64."""
+        st = self._lib.fqb_gemm_emulated(self._h, int(trans_a), m, n, k, alpha, a_ptr, lda, b_ptr, ldb, beta,
+                                         c_ptr, ldc)
+        if st:
+            _raise(st, "fqb_gemm_emulated")
+
     def sparse_dense_mul(self, a_ptr, m, n, lda, col_ptr_ptr, row_idx_ptr, values_ptr, l, z_ptr,
                          c_ptr, ldc):
         st = self._lib.fqb_sparse_dense_mul(self._h, a_ptr, m, n, lda, col_ptr_ptr, row_idx_ptr,

@@ -1,0 +1,153 @@
+"""The INT8 tensor-core FP64 emulation (ozaki.cu) behind fqb_gemm_emulated and the engine's A passes.
+
+Accuracy bar: an FP64 GEMM's.  On a sample of rows, every element of C must be
+within 4e-16 of the bound |A| |B| (elementwise absolute product) plus the final
+rounding (2^-53 |C|) of the exact result, computed in extended precision
+(numpy longdouble) -- what the slicing argument in ozaki.cu guarantees
+(dropped terms ~2^-55 of max|row| * max|col|).  A plain FP64 reference would
+itself be off by ~sqrt(K) u |A||B| and could not resolve this bar.
+The engine with the emulation forced on must keep every parity property of the
+FP64 path: identical rank / blocks / ids and E within 1e-10 ||A||^2.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover - CPU container
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2506_03859_b200 as fqb  # noqa: E402
+from oracle.oracle import SketchArrays  # noqa: E402
+from paper_2506_03859_b200 import FarpcaConfig, SketchSpec  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def eng():
+    return fqb.default_engine(0)
+
+
+def _run_emulated(eng, trans, a, b, c0, alpha, beta):
+    """a: (k x m if trans else m x k), b: k x n, c0: m x n, all float64 CPU tensors."""
+    m, n = c0.shape
+    k = b.shape[0]
+    ad = a.cuda().t().contiguous().t()
+    bd = b.cuda().t().contiguous().t()
+    cd = c0.cuda().t().contiguous().t()
+    # column-major and contiguous: ld = rows (stride(1) is ambiguous for one column)
+    eng.gemm_emulated(trans, m, n, k, alpha, ad.data_ptr(), ad.shape[0], bd.data_ptr(), bd.shape[0], beta,
+                      cd.data_ptr(), cd.shape[0])
+    torch.cuda.synchronize()
+    return cd.cpu()
+
+
+def _check_rows(got, aa, b, c0, alpha, beta, rows):
+    """Extended-precision check of C[rows, :] (aa = op(A), m x k)."""
+    ar = aa[rows].numpy().astype(np.longdouble)
+    bl = b.numpy().astype(np.longdouble)
+    exact = alpha * (ar @ bl) + beta * c0[rows].numpy().astype(np.longdouble)
+    bound = abs(alpha) * (np.abs(ar) @ np.abs(bl)) + abs(beta) * np.abs(c0[rows].numpy())
+    err = np.abs(got[rows].numpy().astype(np.longdouble) - exact)
+    tol = 4e-16 * bound + 2.0 ** -53 * np.abs(exact) + 1e-300
+    assert (err <= tol).all(), float(np.max(err / tol))
+
+
+@pytest.mark.parametrize("trans", [True, False])
+@pytest.mark.parametrize("m,n,k", [(8000, 50, 8000), (257, 33, 999), (128, 64, 64), (129, 1, 65), (1, 17, 3),
+                                   (300, 64, 5000), (1000, 20, 127)])
+def test_emulated_gemm_fp64_accuracy(eng, trans, m, n, k):
+    g = torch.Generator(device="cpu").manual_seed(m + 3 * n + 7 * k + int(trans))
+    a = torch.randn((k, m) if trans else (m, k), dtype=torch.float64, generator=g)
+    b = torch.randn((k, n), dtype=torch.float64, generator=g)
+    c0 = torch.randn((m, n), dtype=torch.float64, generator=g)
+    got = _run_emulated(eng, trans, a, b, c0, 0.75, -0.5)
+    aa = a.t() if trans else a
+    rows = np.unique(np.linspace(0, m - 1, min(m, 48)).astype(int))
+    _check_rows(got, aa, b, c0, 0.75, -0.5, rows)
+
+
+def test_emulated_gemm_wild_scales_and_zero_lines(eng):
+    """Rows / columns spanning 1e-150 .. 1e150, exact zero rows and columns, beta = 0."""
+    m, n, k = 300, 40, 700
+    g = torch.Generator(device="cpu").manual_seed(5)
+    a = torch.randn((k, m), dtype=torch.float64, generator=g)          # trans: rows of C = columns of a
+    a *= torch.logspace(-150, 150, m, dtype=torch.float64)
+    a[:, 7] = 0.0
+    a[13, :] = 0.0
+    b = torch.randn((k, n), dtype=torch.float64, generator=g) * torch.logspace(-100, 100, n, dtype=torch.float64)
+    b[:, 3] = 0.0
+    c0 = torch.full((m, n), 7.0, dtype=torch.float64)
+    got = _run_emulated(eng, True, a, b, c0, 1.0, 0.0)
+    assert torch.isfinite(got).all()
+    assert (got[7, :] == 0).all() and (got[:, 3] == 0).all()
+    _check_rows(got, a.t(), b, c0, 1.0, 0.0, np.arange(0, m, 7))
+
+
+def test_emulated_gemm_is_deterministic(eng):
+    m, n, k = 4000, 50, 6000
+    g = torch.Generator(device="cpu").manual_seed(9)
+    a = torch.randn((k, m), dtype=torch.float64, generator=g)
+    b = torch.randn((k, n), dtype=torch.float64, generator=g)
+    c = torch.zeros((m, n), dtype=torch.float64)
+    r1 = _run_emulated(eng, True, a, b, c, 1.0, 0.0)
+    r2 = _run_emulated(eng, True, a, b, c, 1.0, 0.0)
+    assert torch.equal(r1, r2)
+
+
+def test_emulated_gemm_rejects_wide_n(eng):
+    a = torch.zeros((10, 10), dtype=torch.float64, device="cuda")
+    b = torch.zeros((10, 65), dtype=torch.float64, device="cuda")
+    c = torch.zeros((10, 65), dtype=torch.float64, device="cuda")
+    with pytest.raises(fqb.DimensionError):
+        eng.gemm_emulated(True, 10, 65, 10, 1.0, a.data_ptr(), 10, b.data_ptr(), 10, 0.0, c.data_ptr(), 10)
+
+
+def _lowrank(m, n, sig, seed):
+    rng = np.random.default_rng(seed)
+    r = len(sig)
+    u, _ = np.linalg.qr(rng.standard_normal((m, r)))
+    v, _ = np.linalg.qr(rng.standard_normal((n, r)))
+    return np.asfortranarray((u * sig) @ v.T)
+
+
+@pytest.mark.parametrize("kind,zeta,power", [(2, 0, 2), (0, 0, 1), (3, 8, 3), (4, 8, 0)])
+def test_qb_with_emulation_matches_oracle(eng, port, monkeypatch, kind, zeta, power):
+    """FQB_OZAKI=1 forces every A pass onto the INT8 tensor cores, even at this size."""
+    monkeypatch.setenv("FQB_OZAKI", "1")
+    a = _lowrank(900, 700, 1.0 / np.arange(1, 251) ** 1.5, seed=40 + kind + power)
+    p = 0.0 if kind == 0 or zeta else 0.5
+    spec = SketchSpec(kind, p, 13, zeta=zeta)
+    cfg = FarpcaConfig(eps=1e-2, power=power, block=25, sketch=spec, relative=True)
+    res = eng.run_fixed_precision(a, cfg, output="host")
+
+    def src(n, b, bid):
+        s = eng.gen_sketch(spec, n, b, bid)
+        if s.is_dense:
+            return SketchArrays(True, s.rows, s.cols, dense=s.dense, p=s.p)
+        return SketchArrays(False, s.rows, s.cols, col_ptr=s.col_ptr, row_idx=s.row_idx, values=s.values,
+                            centered=s.centered, p=s.p, std_scale=s.std_scale)
+    ref = port.run(a, eps=1e-2, power=power, block=25, kind=kind, p=p, seed=13, zeta=zeta, relative=True,
+                   source=src)
+    assert ref.status == 0 and res.converged
+    assert (res.rank, res.blocks, res.block_ids) == (ref.rank, ref.blocks, ref.block_ids)
+    na = ref.norm_a_sq
+    assert abs(res.residual_sq - ref.residual_sq) <= 1e-10 * na
+    assert np.max(np.abs(res.block_residuals - ref.block_residuals)) <= 1e-10 * na
+
+
+def test_emulation_on_and_off_agree(eng, monkeypatch):
+    a = _lowrank(1500, 1200, 0.97 ** np.arange(300), seed=77)
+    cfg = FarpcaConfig(eps=1e-3, power=2, block=40, sketch=SketchSpec(2, 0.5, 5), relative=True)
+    monkeypatch.setenv("FQB_OZAKI", "1")
+    r1 = eng.run_fixed_precision(a, cfg, output="host")
+    monkeypatch.setenv("FQB_OZAKI", "0")
+    r0 = eng.run_fixed_precision(a, cfg, output="host")
+    assert (r1.rank, r1.blocks) == (r0.rank, r0.blocks)
+    assert abs(r1.residual_sq - r0.residual_sq) <= 1e-11 * r0.norm_a_sq
+    # different arithmetic (INT8 slices vs DMMA) -- so the emulation really ran ...
+    assert not np.array_equal(r1.bt, r0.bt)
+    # ... and Q B (unique for a given sketch) agrees to FP64 working accuracy
+    qb1 = r1.q @ r1.bt.T
+    qb0 = r0.q @ r0.bt.T
+    assert np.abs(qb1 - qb0).max() <= 1e-10 * np.abs(a).max()
