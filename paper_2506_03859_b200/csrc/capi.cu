@@ -115,15 +115,7 @@ fqb_status fqb_destroy(fqb_handle h) {
         cudaStreamSynchronize(h->h.stream);
         farqb::comm_detach(h->h);
         farqb::destroy_cusolver(h->h);
-        {
-            farqb::Workspace& w = h->h.ws;
-            w.omega.release(); w.y0.release(); w.ys.release(); w.wp.release(); w.wraw.release();
-            w.g.release(); w.t.release(); w.cd.release(); w.c2.release(); w.small.release();
-            w.zc.release(); w.rowsum_b.release(); w.splitk.release(); w.partial.release();
-            w.scalars.release(); w.scratch.release(); w.a_copy.release(); w.col_ptr.release();
-            w.row_idx.release(); w.counts.release(); w.values.release(); w.status.release();
-            w.gemm_flags.release();
-        }
+        h->h.ws.release_all();
         cudaStreamSynchronize(h->h.stream);
         cudaFreeHost(h->h.host_status);
         cudaFreeHost(h->h.host_scalars);
@@ -418,8 +410,10 @@ fqb_status fqb_gemm_emulated(fqb_handle h, int trans_a, int64_t m, int64_t n, in
         zs.ensure(size_t(farqb::ozaki_z_bytes(n, k)), s);
         ex.ensure(size_t(m), s);
         ez.ensure(size_t(n), s);
-        if (trans_a) farqb::ozaki_slice_x_cols(a, k, m, lda, ex.ptr, xs.ptr, s, h->h.lc);
-        else farqb::ozaki_slice_x_rows(a, m, k, lda, ex.ptr, xs.ptr, s, h->h.lc);
+        farqb::DeviceArray<unsigned> line_max;
+        line_max.ensure(size_t(farqb::ozaki_line_max_words(m, k)), s);
+        if (trans_a) farqb::ozaki_slice_a(a, k, m, lda, line_max.ptr, xs.ptr, ex.ptr, nullptr, nullptr, s, h->h.lc);
+        else farqb::ozaki_slice_a(a, m, k, lda, line_max.ptr, nullptr, nullptr, xs.ptr, ex.ptr, s, h->h.lc);
         farqb::ozaki_slice_z(b, k, n, ldb, ez.ptr, zs.ptr, s, h->h.lc);
         farqb::ozaki_gemm(m, n, k, alpha, xs.ptr, ex.ptr, zs.ptr, ez.ptr, beta, c, ldc, h->h.gws.work, h->h.num_sms,
                           s, h->h.lc);

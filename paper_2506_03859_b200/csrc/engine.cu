@@ -244,11 +244,28 @@ class QbRun {
         const char* e = std::getenv("FQB_OZAKI");
         if (e && e[0] == '0') return false;
         if (b > ozaki_max_n()) return false;
-        if (!(e && e[0] == '1') && double(m) * double(n) < double(1 << 24)) return false;  // small: DMMA is fine
-        size_t free_b = 0, total_b = 0;
-        if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return false;
-        const double need = double(ozaki_x_bytes(m, n)) + double(ozaki_x_bytes(n, m));   // both layouts
-        return double(free_b) > need + double(1 << 30);
+        return (e && e[0] == '1') || double(m) * double(n) >= double(1 << 24);   // small: DMMA is fine
+    }
+
+    // Slice A once per run into the handle's buffers; false (and DMMA from then on)
+    // when the two slice layouts do not fit in device memory.
+    bool prepare_ozaki() {
+        Workspace& w = h_.ws;
+        try {
+            w.oz_x_nn.ensure(size_t(ozaki_x_bytes(m_, n_)), s_);
+            w.oz_x_tn.ensure(size_t(ozaki_x_bytes(n_, m_)), s_);
+        } catch (const Error&) {
+            cudaGetLastError();   // clear the allocation failure
+            w.oz_x_nn.release();
+            w.oz_x_tn.release();
+            return false;
+        }
+        w.oz_e_nn.ensure(size_t(m_), s_);
+        w.oz_e_tn.ensure(size_t(n_), s_);
+        w.oz_line_max.ensure(size_t(ozaki_line_max_words(m_, n_)), s_);
+        ozaki_slice_a(a_, m_, n_, lda_, w.oz_line_max.ptr, w.oz_x_tn.ptr, w.oz_e_tn.ptr, w.oz_x_nn.ptr, w.oz_e_nn.ptr,
+                      s_, h_.lc);
+        return true;
     }
 
     void a_gemm(bool ta, int N, const double* B, int64_t ldb, double* C, int64_t ldc) {
@@ -257,20 +274,21 @@ class QbRun {
             else gemm_(false, m_, N, n_, 1.0, a_, lda_, B, ldb, 0.0, C, ldc);
             return;
         }
-        const int L = ta ? 1 : 0;
         const int64_t M = ta ? n_ : m_, K = ta ? m_ : n_;
-        if (!oz_ready_[L]) {
-            oz_x_[L].ensure(size_t(ozaki_x_bytes(M, K)), s_);
-            oz_e_[L].ensure(size_t(M), s_);
-            if (ta) ozaki_slice_x_cols(a_, K, M, lda_, oz_e_[L].ptr, oz_x_[L].ptr, s_, h_.lc);
-            else ozaki_slice_x_rows(a_, M, K, lda_, oz_e_[L].ptr, oz_x_[L].ptr, s_, h_.lc);
-            oz_ready_[L] = true;
+        if (!oz_ready_) {
+            oz_ready_ = true;
+            if (!prepare_ozaki()) {
+                oz_on_ = false;
+                a_gemm(ta, N, B, ldb, C, ldc);
+                return;
+            }
         }
-        oz_z_.ensure(size_t(ozaki_z_bytes(N, K)), s_);
-        oz_ze_.ensure(size_t(ozaki_max_n()), s_);
-        ozaki_slice_z(B, K, N, ldb, oz_ze_.ptr, oz_z_.ptr, s_, h_.lc);
-        ozaki_gemm(M, N, K, 1.0, oz_x_[L].ptr, oz_e_[L].ptr, oz_z_.ptr, oz_ze_.ptr, 0.0, C, ldc, h_.gws.work,
-                   h_.num_sms, s_, h_.lc);
+        Workspace& w = h_.ws;
+        w.oz_z.ensure(size_t(ozaki_z_bytes(N, K)), s_);
+        w.oz_ez.ensure(size_t(ozaki_max_n()), s_);
+        ozaki_slice_z(B, K, N, ldb, w.oz_ez.ptr, w.oz_z.ptr, s_, h_.lc);
+        ozaki_gemm(M, N, K, 1.0, ta ? w.oz_x_tn.ptr : w.oz_x_nn.ptr, ta ? w.oz_e_tn.ptr : w.oz_e_nn.ptr, w.oz_z.ptr,
+                   w.oz_ez.ptr, 0.0, C, ldc, h_.gws.work, h_.num_sms, s_, h_.lc);
     }
 
     // ---- Omega ----------------------------------------------------------------
@@ -553,11 +571,7 @@ class QbRun {
     double om_p_ = 0.0;
     DeviceArray<double> q_, bt_, rowsum_;
     bool oz_on_ = false;              // A-pass products on the INT8 tensor cores (a_gemm)
-    bool oz_ready_[2] = {false, false};
-    DeviceArray<int8_t> oz_x_[2];     // A slices: [0] rows of A (A G), [1] columns of A (A' Y)
-    DeviceArray<int> oz_e_[2];
-    DeviceArray<int8_t> oz_z_;        // slices of the current right-hand block
-    DeviceArray<int> oz_ze_;
+    bool oz_ready_ = false;           // A sliced for this run (buffers live in the handle workspace)
     std::vector<double> residuals_;
     std::vector<int> ids_;
     double *S_, *S2_, *R1_, *R1i_, *R2_, *R2i_, *R_, *Ri_, *V_, *VS_, *VT_, *eig_, *sig_, *scal_;

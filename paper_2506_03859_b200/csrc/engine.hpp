@@ -54,6 +54,21 @@ struct Workspace {
     DeviceArray<double> values;
     DeviceArray<unsigned> status;
     DeviceArray<unsigned> gemm_flags;
+    // Ozaki slices of A (both layouts), kept across runs so a run does not pay
+    // for two large allocations; released with the handle
+    DeviceArray<int8_t> oz_x_nn, oz_x_tn, oz_z;
+    DeviceArray<int> oz_e_nn, oz_e_tn, oz_ez;
+    DeviceArray<unsigned> oz_line_max;
+
+    // every member, while the stream the frees are ordered on still exists
+    void release_all() {
+        for (auto* d : {&omega, &y0, &ys, &wp, &wraw, &g, &t, &cd, &c2, &small, &zc, &rowsum_b, &splitk, &partial,
+                        &scalars, &scratch, &a_copy, &values})
+            d->release();
+        for (auto* d : {&col_ptr, &row_idx, &counts, &oz_e_nn, &oz_e_tn, &oz_ez}) d->release();
+        for (auto* d : {&status, &gemm_flags, &oz_line_max}) d->release();
+        for (auto* d : {&oz_x_nn, &oz_x_tn, &oz_z}) d->release();
+    }
 };
 
 struct Handle {

@@ -111,12 +111,13 @@ int ozaki_bn(int64_t n);
 int64_t ozaki_x_bytes(int64_t rows, int64_t k);
 int64_t ozaki_z_bytes(int64_t n, int64_t k);
 int64_t ozaki_workspace_doubles(int num_sms);
-// X rows = columns of a (a is k x rows, ld): the A'Y operand
-void ozaki_slice_x_cols(const double* a, int64_t k, int64_t rows, int64_t ld, int* e, int8_t* out, cudaStream_t s,
-                        LaunchCounter& lc);
-// X rows = rows of a (a is rows x k, ld): the A G operand
-void ozaki_slice_x_rows(const double* a, int64_t rows, int64_t k, int64_t ld, int* e, int8_t* out, cudaStream_t s,
-                        LaunchCounter& lc);
+// Slices of A (m x n, ld) in both layouts from one pass (either may be null):
+//   x_tn / e_tn: operand rows = columns of A, K = m   (A' Y)
+//   x_nn / e_nn: operand rows = rows of A,    K = n   (A G)
+// line_max: ozaki_line_max_words(m, n) words of scratch.
+int64_t ozaki_line_max_words(int64_t m, int64_t n);
+void ozaki_slice_a(const double* a, int64_t m, int64_t n, int64_t ld, unsigned* line_max, int8_t* x_tn, int* e_tn,
+                   int8_t* x_nn, int* e_nn, cudaStream_t s, LaunchCounter& lc);
 // Z (k x n, ld)
 void ozaki_slice_z(const double* b, int64_t k, int64_t n, int64_t ld, int* e, int8_t* out, cudaStream_t s,
                    LaunchCounter& lc);

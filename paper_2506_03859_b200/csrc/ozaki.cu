@@ -80,6 +80,7 @@ __device__ __forceinline__ int64_t qdiv(int64_t a, int64_t b, double inv_b) {
 // x * 2^k without ldexp() (a long library routine: 64 of them per thread made the
 // finishing epilogue take ~14 us).  Exact whenever the result is a normal number;
 // |k| up to 2046 through two factors.
+__device__ __forceinline__ int64_t round_up_dev(int64_t x, int64_t r) { return (x + r - 1) / r * r; }
 __device__ __forceinline__ double pow2i(int k) {   // k in [-1022, 1023]
     return __longlong_as_double(static_cast<long long>(k + 1023) << 52);
 }
@@ -376,127 +377,166 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
 
 // ---------------------------------------------------------------------------
 // slicing
+//
+// A line (row or column) x with max|x| in [2^(e-1), 2^e) becomes the 55-bit
+// integer R = rint(x 2^(55-e)) (|R| < 2^55, one FP64 multiply and one
+// conversion), and R is written in balanced base 128 with a base-64 top digit:
+//     R = sum_p d_p 2^(49-7p),  d_0 in [-64, 64],  d_1..d_7 in [-64, 63]
+// read off as the 7-bit fields of R + sum_p 64 2^(49-7p) minus 64 (integer ops
+// only).  So x = 2^e sum_p d_p 2^(-6-7p) up to the rounding of R, the weights
+// the kernel's epilogue applies.  Line maxima only need the exponent, which
+// lives in the high word of |x|: they are reduced as 32-bit integers.
 
-// exponent e with 2^(e-1) <= max|x| < 2^e; an all-zero vector gets a very small
-// exponent so it never dominates a max over chunks (and 0 * 2^-e stays 0)
-constexpr int kZeroExp = -2000;
-__device__ __forceinline__ int exponent_of(double maxabs) { return maxabs > 0.0 ? ilogb(maxabs) + 1 : kZeroExp; }
+constexpr long long kDigitBias = (64LL << 49) + (64LL << 42) + (64LL << 35) + (64LL << 28) + (64LL << 21) +
+                                 (64LL << 14) + (64LL << 7) + 64LL;
 
-__device__ __forceinline__ void slice8(double x, int e, int8_t (&out)[S]) {
-    double r = mul_pow2(x, -e);  // |r| < 1
-    double y = r * 64.0;
-    double q = rint(y);
-    out[0] = int8_t(q);
-    r = y - q;
-#pragma unroll
-    for (int s = 1; s < S; ++s) {
-        y = r * 128.0;
-        q = rint(y);
-        out[s] = int8_t(q);
-        r = y - q;
-    }
+// high word of |x|: monotone in |x|, exponent in bits 20..30
+__device__ __forceinline__ unsigned abs_hi(double x) {
+    return unsigned(static_cast<unsigned long long>(__double_as_longlong(x)) >> 32) & 0x7FFFFFFFu;
 }
+// e with 2^(e-1) <= max|x| < 2^e from the max high word.  All-zero lines and
+// subnormal maxima get e = -1021 (their digits are 0 or just coarser).
+__device__ __forceinline__ int exp_of_hi(unsigned hi) { return hi >= 0x00100000u ? int(hi >> 20) - 1022 : -1021; }
 
-// per-column max exponent of a (rows x cols, ld) -- one CTA per column
-__global__ void __launch_bounds__(256) k_col_exp(const double* __restrict__ a, int64_t rows, int64_t ld, int* e) {
-    __shared__ double red[8];
-    const double* c = a + int64_t(blockIdx.x) * ld;
-    double mx = 0.0;
-    for (int64_t r = threadIdx.x; r < rows; r += blockDim.x) mx = fmax(mx, fabs(c[r]));
+// the 8 digits of x in line scale e, as bytes
+__device__ __forceinline__ void digits8(double x, int e, unsigned (&d)[S]) {
+    const long long R = __double2ll_rn(mul_pow2(x, 55 - e));
+    const unsigned long long U = static_cast<unsigned long long>(R + kDigitBias);
+    d[0] = unsigned(int(U >> 49) - 64) & 0xFFu;
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_down_sync(0xffffffffu, mx, off));
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double m = 0.0;
-        for (int w = 0; w < int(blockDim.x >> 5); ++w) m = fmax(m, red[w]);
-        e[blockIdx.x] = exponent_of(m);
-    }
-}
-
-// per-row max exponent: a thread covers one row over a chunk of 64 columns
-// (coalesced across the warp), chunks combined with atomicMax on the exponent
-// (e must be preset to a very negative value: memset 0x80)
-__global__ void __launch_bounds__(256) k_row_exp(const double* __restrict__ a, int64_t rows, int64_t cols, int64_t ld,
-                                                 int* e) {
-    const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (r >= rows) return;
-    const int64_t c0 = int64_t(blockIdx.y) * 64, c1 = c0 + 64 < cols ? c0 + 64 : cols;
-    double mx = 0.0;
-    for (int64_t j = c0; j < c1; ++j) mx = fmax(mx, fabs(__ldg(a + j * ld + r)));
-    atomicMax(e + r, exponent_of(mx));
+    for (int p = 1; p < S; ++p) d[p] = unsigned(int((U >> (49 - 7 * p)) & 127u) - 64) & 0xFFu;
 }
 
 // byte offset of (row r, byte c) inside a swizzled TR x OZ_BK byte tile
 // (64B swizzle: the 16-byte chunk index c>>4 is XORed with address bits 7-8 = (r >> 1) & 3)
-__device__ __forceinline__ int64_t swz(int r, int c) {
-    return int64_t(r) * OZ_BK + ((((c >> 4) ^ ((r >> 1) & 3)) << 4) | (c & 15));
-}
+__device__ __forceinline__ int swz(int r, int c) { return r * OZ_BK + ((((c >> 4) ^ ((r >> 1) & 3)) << 4) | (c & 15)); }
 
-// Tiled slices of an operand whose rows are the columns of `a` (K = rows of a):
-// tile (rt, kb, s) at ((rt * KB + kb) * S + s) * TR * OZ_BK.  A thread slices 4
-// consecutive k of one column and stores them as one 32-bit word per slice.
-__global__ void __launch_bounds__(256) k_slice_cols_tiled(const double* __restrict__ a, int64_t K, int64_t R,
-                                                          int64_t ld, const int* __restrict__ e, int8_t* out, int tr,
-                                                          int64_t kb_count) {
-    const int64_t k0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
-    const int64_t r = blockIdx.y;
-    if (k0 >= kb_count * OZ_BK || r >= R) return;
-    const double* col = a + r * ld;
-    const int er = e[r];
-    uint32_t word[S] = {0, 0, 0, 0, 0, 0, 0, 0};
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-        int8_t s8[S] = {0, 0, 0, 0, 0, 0, 0, 0};
-        if (k0 + u < K) slice8(col[k0 + u], er, s8);
-#pragma unroll
-        for (int sl = 0; sl < S; ++sl) word[sl] |= uint32_t(uint8_t(s8[sl])) << (8 * u);
-    }
-    const int64_t rt = r / tr, kb = k0 / OZ_BK;
-    const int rl = int(r % tr), c = int(k0 % OZ_BK);
-    const int64_t tile_bytes = int64_t(tr) * OZ_BK;
-    int8_t* base = out + (rt * kb_count + kb) * S * tile_bytes + swz(rl, c);
-#pragma unroll
-    for (int sl = 0; sl < S; ++sl) *reinterpret_cast<uint32_t*>(base + sl * tile_bytes) = word[sl];
-}
-
-// Tiled slices of the rows of `a` (K = columns of a), through a shared-memory
-// transpose: a CTA covers 32 rows x 128 columns (128 / OZ_BK k-blocks); each thread
-// slices 16 consecutive k of one row into one 16-byte chunk per slice.
-__global__ void __launch_bounds__(256) k_slice_rows_tiled(const double* __restrict__ a, int64_t R, int64_t K,
-                                                          int64_t ld, const int* __restrict__ e, int8_t* out,
-                                                          int64_t kb_count) {
-    __shared__ double tile[128][33];
-    const int64_t r0 = int64_t(blockIdx.x) * 32, c0 = int64_t(blockIdx.y) * 128;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int kk = warp; kk < 128; kk += 8) {
-        const int64_t r = r0 + lane, k = c0 + kk;
-        tile[kk][lane] = (r < R && k < K) ? a[k * ld + r] : 0.0;
-    }
-    __syncthreads();
-    const int rl32 = threadIdx.x >> 3, chunk = threadIdx.x & 7;  // 32 rows x 8 chunks of 16 k
-    const int64_t r = r0 + rl32;
-    if (r >= R) return;
-    const int er = e[r];
+// 16 consecutive K-values of one operand row -> one 16-byte chunk per slice
+__device__ __forceinline__ void put_chunk16(const double (&v)[16], int e, int8_t* tile0, int64_t slice_stride, int r,
+                                            int c) {
     uint32_t w[S][4];
 #pragma unroll
     for (int sl = 0; sl < S; ++sl) w[sl][0] = w[sl][1] = w[sl][2] = w[sl][3] = 0;
 #pragma unroll
     for (int u = 0; u < 16; ++u) {
-        int8_t s8[S];
-        slice8(tile[chunk * 16 + u][rl32], er, s8);
+        unsigned d[S];
+        digits8(v[u], e, d);
 #pragma unroll
-        for (int sl = 0; sl < S; ++sl) w[sl][u >> 2] |= uint32_t(uint8_t(s8[sl])) << (8 * (u & 3));
+        for (int sl = 0; sl < S; ++sl) w[sl][u >> 2] |= d[sl] << (8 * (u & 3));
     }
-    const int64_t kb = (c0 + chunk * 16) / OZ_BK;
-    if (kb >= kb_count) return;
-    const int64_t rt = r / OZ_BM;
-    const int rl = int(r % OZ_BM);
-    const int64_t tile_bytes = int64_t(OZ_BM) * OZ_BK;
-    int8_t* base = out + (rt * kb_count + kb) * S * tile_bytes + swz(rl, int((chunk * 16) % OZ_BK));
+    int8_t* dst = tile0 + swz(r, c);
 #pragma unroll
     for (int sl = 0; sl < S; ++sl)
-        *reinterpret_cast<uint4*>(base + sl * tile_bytes) = make_uint4(w[sl][0], w[sl][1], w[sl][2], w[sl][3]);
+        *reinterpret_cast<uint4*>(dst + sl * slice_stride) = make_uint4(w[sl][0], w[sl][1], w[sl][2], w[sl][3]);
+}
+
+// Row and column maxima (high words) of A (m x n, ld) in one pass; rmax / cmax
+// must be zeroed.  CTA: 256 rows x 128 columns, a thread walks one row.
+__global__ void __launch_bounds__(256) k_line_max(const double* __restrict__ a, int64_t m, int64_t n, int64_t ld,
+                                                  unsigned* rmax, unsigned* cmax) {
+    __shared__ unsigned cm[8][128];
+    const int64_t i = int64_t(blockIdx.x) * 256 + threadIdx.x;
+    const int64_t j0 = int64_t(blockIdx.y) * 128;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned rm = 0;
+#pragma unroll 4
+    for (int c = 0; c < 128; ++c) {
+        const int64_t j = j0 + c;
+        const unsigned h = (i < m && j < n) ? abs_hi(a[j * ld + i]) : 0u;
+        rm = max(rm, h);
+        const unsigned wm = __reduce_max_sync(0xFFFFFFFFu, h);
+        if (lane == 0) cm[warp][c] = wm;
+    }
+    if (i < m && rm) atomicMax(rmax + i, rm);
+    __syncthreads();
+    if (threadIdx.x < 128 && j0 + threadIdx.x < n) {
+        unsigned v = 0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) v = max(v, cm[w][threadIdx.x]);
+        if (v) atomicMax(cmax + j0 + threadIdx.x, v);
+    }
+}
+
+// Both layouts of A's slices from one read of a 64 x 64 block (staged in shared
+// memory); also turns the line maxima into the exponents the GEMM epilogue uses.
+//   x_tn: operand rows = columns of A, K = m (A' Y),  e_tn per column
+//   x_nn: operand rows = rows of A,    K = n (A G),   e_nn per row
+// Either may be null.  The grid covers the padded operand rows, so every byte of
+// both slice buffers is written (zeros outside A) and no memset is needed.
+__global__ void __launch_bounds__(256) k_slice_a(const double* __restrict__ a, int64_t m, int64_t n, int64_t ld,
+                                                 const unsigned* __restrict__ rmax, const unsigned* __restrict__ cmax,
+                                                 int8_t* x_tn, int* e_tn, int8_t* x_nn, int* e_nn) {
+    __shared__ double t[64][65];   // t[j][i]
+    const int64_t i0 = int64_t(blockIdx.x) * 64, j0 = int64_t(blockIdx.y) * 64;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int jj = warp; jj < 64; jj += 8) {
+        const int64_t j = j0 + jj;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int64_t i = i0 + lane + 32 * h;
+            t[jj][lane + 32 * h] = (i < m && j < n) ? a[j * ld + i] : 0.0;
+        }
+    }
+    __syncthreads();
+    const int line = threadIdx.x >> 2, q = threadIdx.x & 3;   // 64 lines x 4 chunks of 16
+    if (x_tn && i0 < round_up_dev(m, OZ_BK)) {                  // columns of A: rows j, K = i
+        const int64_t j = j0 + line;
+        const int e = j < n ? exp_of_hi(cmax[j]) : -1021;
+        if (e_tn && blockIdx.x == 0 && j < n && q == 0) e_tn[j] = e;
+        double v[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) v[u] = t[line][q * 16 + u];
+        const int64_t kb_count = (m + OZ_BK - 1) / OZ_BK;
+        int8_t* tile0 = x_tn + ((j / OZ_BM) * kb_count + i0 / OZ_BK) * S * int64_t(A_TILE);
+        put_chunk16(v, e, tile0, A_TILE, int(j % OZ_BM), q * 16);
+    }
+    if (x_nn && j0 < round_up_dev(n, OZ_BK)) {                  // rows of A: rows i, K = j
+        const int64_t i = i0 + line;
+        const int e = i < m ? exp_of_hi(rmax[i]) : -1021;
+        if (e_nn && blockIdx.y == 0 && i < m && q == 0) e_nn[i] = e;
+        double v[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) v[u] = t[q * 16 + u][line];
+        const int64_t kb_count = (n + OZ_BK - 1) / OZ_BK;
+        int8_t* tile0 = x_nn + ((i / OZ_BM) * kb_count + j0 / OZ_BK) * S * int64_t(A_TILE);
+        put_chunk16(v, e, tile0, A_TILE, int(i % OZ_BM), q * 16);
+    }
+}
+
+// Z (k x n, ld, n <= 64): CTA (j, y) slices 16-row chunks y*256 .. y*256+255 of
+// column j (padded to 64 columns: zeros).  Every CTA of a column first takes the
+// column max itself (the column is small and L2-resident), so one launch does it.
+__global__ void __launch_bounds__(256) k_slice_z(const double* __restrict__ b, int64_t k, int64_t n, int64_t ld,
+                                                 int* ez, int8_t* out) {
+    __shared__ unsigned wmax[8];
+    const int j = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const double* col = b + int64_t(j) * ld;
+    const bool live = j < n;
+    unsigned h = 0;
+    if (live) {
+        int64_t r = threadIdx.x;
+        for (; r + 3 * 256 < k; r += 4 * 256)
+            h = max(max(max(h, abs_hi(col[r])), abs_hi(col[r + 256])), max(abs_hi(col[r + 512]), abs_hi(col[r + 768])));
+        for (; r < k; r += 256) h = max(h, abs_hi(col[r]));
+    }
+    h = __reduce_max_sync(0xFFFFFFFFu, h);
+    if (lane == 0) wmax[warp] = h;
+    __syncthreads();
+    unsigned mx = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) mx = max(mx, wmax[w]);
+    const int e = exp_of_hi(mx);
+    if (live && blockIdx.y == 0 && threadIdx.x == 0) ez[j] = e;
+    const int64_t kb_count = (k + OZ_BK - 1) / OZ_BK;
+    const int64_t z_tile = int64_t(OZ_BN) * OZ_BK;
+    const int64_t c16 = int64_t(blockIdx.y) * 256 + threadIdx.x;
+    if (c16 >= kb_count * (OZ_BK / 16)) return;
+    const int64_t k0 = c16 * 16;
+    double v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) v[u] = (live && k0 + u < k) ? col[k0 + u] : 0.0;
+    put_chunk16(v, e, out + (k0 / OZ_BK) * S * z_tile, z_tile, j, int(k0 % OZ_BK));
 }
 
 // Sum the pieces of every split tile in CTA order (deterministic) into C.
@@ -508,10 +548,23 @@ __global__ void __launch_bounds__(OZ_BM) k_ozaki_fixup(const OzArgs p) {
     const int c0 = cta_of(p, t * p.kblocks), c1 = cta_of(p, t * p.kblocks + p.kblocks - 1);
     const int64_t row = t * OZ_BM + r;
     if (c0 == c1 || row >= p.M) return;   // a tile owned by one CTA was written directly
+    // all piece loads in flight at once, then the sum in CTA order
+    constexpr int kMaxBatch = 8;
     double sum = 0.0;
-    for (int cc = c0; cc <= c1; ++cc) {
-        const int64_t t_last = qdiv(range_begin(p, cc + 1) - 1, p.kblocks, p.inv_kblocks);
-        sum += __ldcg(p.work + (3 * int64_t(cc) + (t == t_last ? 0 : 1)) * OZ_PARTIAL + j * OZ_BM + r);
+    for (int cb = c0; cb <= c1; cb += kMaxBatch) {
+        double v[kMaxBatch];
+#pragma unroll
+        for (int u = 0; u < kMaxBatch; ++u) {
+            const int cc = cb + u;
+            v[u] = 0.0;
+            if (cc <= c1) {
+                const int64_t t_last = qdiv(range_begin(p, cc + 1) - 1, p.kblocks, p.inv_kblocks);
+                v[u] = __ldcg(p.work + (3 * int64_t(cc) + (t == t_last ? 0 : 1)) * OZ_PARTIAL + j * OZ_BM + r);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kMaxBatch; ++u)
+            if (cb + u <= c1) sum += v[u];
     }
     double* cp = p.C + int64_t(j) * p.ldc + row;
     const double v = p.alpha * sum;
@@ -526,48 +579,30 @@ int ozaki_bn(int64_t) { return OZ_BN; }   // Z slices padded to 64 rows: slice s
 int64_t ozaki_x_bytes(int64_t rows, int64_t k) { return ceil_div(rows, OZ_BM) * ceil_div(k, OZ_BK) * S * OZ_BM * OZ_BK; }
 int64_t ozaki_z_bytes(int64_t n, int64_t k) { return ceil_div(k, OZ_BK) * S * int64_t(ozaki_bn(n)) * OZ_BK; }
 
-// X operand from the columns of a (A'Y: rows of X = columns of A)
-void ozaki_slice_x_cols(const double* a, int64_t k, int64_t rows, int64_t ld, int* e, int8_t* out, cudaStream_t s,
-                        LaunchCounter& lc) {
-    if (rows <= 0 || k <= 0) return;
-    const int64_t kbc = ceil_div(k, OZ_BK);
-    FQB_CUDA(cudaMemsetAsync(out, 0, size_t(ozaki_x_bytes(rows, k)), s));
-    k_col_exp<<<unsigned(rows), 256, 0, s>>>(a, k, ld, e);
+int64_t ozaki_line_max_words(int64_t m, int64_t n) { return m + n; }
+
+void ozaki_slice_a(const double* a, int64_t m, int64_t n, int64_t ld, unsigned* line_max, int8_t* x_tn, int* e_tn,
+                   int8_t* x_nn, int* e_nn, cudaStream_t s, LaunchCounter& lc) {
+    if (m <= 0 || n <= 0) return;
+    unsigned* rmax = line_max;
+    unsigned* cmax = line_max + m;
+    FQB_CUDA(cudaMemsetAsync(line_max, 0, sizeof(unsigned) * size_t(m + n), s));
+    k_line_max<<<dim3(unsigned(ceil_div(m, 256)), unsigned(ceil_div(n, 128))), 256, 0, s>>>(a, m, n, ld, rmax, cmax);
     FQB_LAUNCHED();
-    dim3 g(unsigned(ceil_div(kbc * OZ_BK, 1024)), unsigned(rows));
-    k_slice_cols_tiled<<<g, 256, 0, s>>>(a, k, rows, ld, e, out, OZ_BM, kbc);
+    // cover the padded operand rows of both layouts (multiples of OZ_BM)
+    const dim3 g(unsigned(ceil_div(m, OZ_BM) * (OZ_BM / 64)), unsigned(ceil_div(n, OZ_BM) * (OZ_BM / 64)));
+    k_slice_a<<<g, 256, 0, s>>>(a, m, n, ld, rmax, cmax, x_tn, e_tn, x_nn, e_nn);
     FQB_LAUNCHED();
     lc.bump(2);
 }
 
-// X operand from the rows of a (A G: rows of X = rows of A, K = columns)
-void ozaki_slice_x_rows(const double* a, int64_t rows, int64_t k, int64_t ld, int* e, int8_t* out, cudaStream_t s,
-                        LaunchCounter& lc) {
-    if (rows <= 0 || k <= 0) return;
-    const int64_t kbc = ceil_div(k, OZ_BK);
-    FQB_CUDA(cudaMemsetAsync(out, 0, size_t(ozaki_x_bytes(rows, k)), s));
-    FQB_CUDA(cudaMemsetAsync(e, 0x80, sizeof(int) * rows, s));
-    dim3 ge(unsigned(ceil_div(rows, 256)), unsigned(ceil_div(k, 64)));
-    k_row_exp<<<ge, 256, 0, s>>>(a, rows, k, ld, e);
-    FQB_LAUNCHED();
-    dim3 g(unsigned(ceil_div(rows, 32)), unsigned(ceil_div(k, 128)));
-    k_slice_rows_tiled<<<g, 256, 0, s>>>(a, rows, k, ld, e, out, kbc);
-    FQB_LAUNCHED();
-    lc.bump(2);
-}
-
-// Z operand (K x n, column j = output column j): one row tile of bn rows
 void ozaki_slice_z(const double* b, int64_t k, int64_t n, int64_t ld, int* e, int8_t* out, cudaStream_t s,
                    LaunchCounter& lc) {
     if (n <= 0 || k <= 0) return;
-    const int64_t kbc = ceil_div(k, OZ_BK);
-    FQB_CUDA(cudaMemsetAsync(out, 0, size_t(ozaki_z_bytes(n, k)), s));
-    k_col_exp<<<unsigned(n), 256, 0, s>>>(b, k, ld, e);
+    const int64_t chunks = ceil_div(k, OZ_BK) * (OZ_BK / 16);
+    k_slice_z<<<dim3(OZ_BN, unsigned(ceil_div(chunks, 256))), 256, 0, s>>>(b, k, n, ld, e, out);
     FQB_LAUNCHED();
-    dim3 g(unsigned(ceil_div(kbc * OZ_BK, 1024)), unsigned(n));
-    k_slice_cols_tiled<<<g, 256, 0, s>>>(b, k, n, ld, e, out, ozaki_bn(n), kbc);
-    FQB_LAUNCHED();
-    lc.bump(2);
+    lc.bump();
 }
 
 void ozaki_gemm(int64_t M, int64_t N, int64_t K, double alpha, const int8_t* xs, const int* ex, const int8_t* zs,

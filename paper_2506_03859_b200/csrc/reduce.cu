@@ -14,7 +14,10 @@
 namespace farqb {
 namespace {
 
-constexpr int kSeg = 4096;  // rows per segment
+// rows per segment: long segments for A (streaming), short ones for the n x b
+// blocks so their few segments still spread over many CTAs.  A function of the
+// shape only, so the summation order (and result) is reproducible.
+__host__ __device__ __forceinline__ int64_t seg_rows(int64_t m, int64_t n) { return m * n >= (int64_t(1) << 26) ? 4096 : 512; }
 
 __device__ __forceinline__ double block_sum(double v, double* sh) {
 #pragma unroll
@@ -34,13 +37,14 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
 __global__ void __launch_bounds__(256) k_sumsq_partial(const double* __restrict__ a, int64_t m,
                                                        int64_t n, int64_t lda, double* partial) {
     __shared__ double sh[32];
-    const int64_t segs_per_col = (m + kSeg - 1) / kSeg;
+    const int64_t seg = seg_rows(m, n);
+    const int64_t segs_per_col = (m + seg - 1) / seg;
     const int64_t total = segs_per_col * n;
     double acc = 0.0;
     for (int64_t sgi = blockIdx.x; sgi < total; sgi += gridDim.x) {
         const int64_t col = sgi / segs_per_col;
-        const int64_t r0 = (sgi - col * segs_per_col) * kSeg;
-        const int64_t r1 = r0 + kSeg < m ? r0 + kSeg : m;
+        const int64_t r0 = (sgi - col * segs_per_col) * seg;
+        const int64_t r1 = r0 + seg < m ? r0 + seg : m;
         const double* c = a + col * lda;
         for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
             const double v = __ldg(c + r);

@@ -14,6 +14,7 @@
 //      ascending output.  Disjoint rotations of a round are applied in parallel.
 //  launch_eigsvd_scale: eigSVD tail (matrix_core.cpp:193-215).
 #include <cstdint>
+#include <cstdlib>
 
 #include "kernels.hpp"
 
