@@ -117,9 +117,14 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def gemm_roofline(eng, a, stream):
-    """Live per-launch timing of the dominant kernel: the A-pass DMMA GEMM
-    W = A' Y (TN, 8000 x 50 x 8000), CUDA events on the engine's stream."""
+def apass_roofline(eng, a, stream):
+    """Live per-launch timing of the dominant kernel: one A pass of the QB loop,
+    W = A' Y (TN) and Y = A G (NN) at 8000 x 50 x 8000, as the engine runs it --
+    k_slice_z + k_ozaki (INT8 tcgen05 FP64 emulation) + k_ozaki_fixup on a
+    persistent sliced A (fqb_slice_operand / fqb_sliced_gemm), CUDA events on the
+    stream the kernels are launched on.  HBM bound: the A slices are 8 bytes per
+    element of A, streamed once per pass.  The FP64 DMMA GEMM of the same product
+    is timed beside it for reference."""
     import torch
     y = torch.randn(BLOCK, M, dtype=torch.float64, device=a.device).t()   # m x b col-major
     w = torch.empty(BLOCK, N, dtype=torch.float64, device=a.device).t()
@@ -127,21 +132,30 @@ def gemm_roofline(eng, a, stream):
     g = torch.randn(BLOCK, N, dtype=torch.float64, device=a.device).t()
     reps = 20
     out = {}
+    sl = eng.slice_operand(a.data_ptr(), M, N, a.stride(1))
     for name, trans, outp, bp in (("tn", True, w, y), ("nn", False, yn, g)):
-        for _ in range(3):
-            eng.gemm(trans, N if trans else M, BLOCK, M if trans else N, 1.0, a.data_ptr(), a.stride(1),
-                     bp.data_ptr(), bp.stride(1), 0.0, outp.data_ptr(), outp.stride(1))
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        with torch.cuda.stream(stream):
-            e0.record()
-            for _ in range(reps):
-                eng.gemm(trans, N if trans else M, BLOCK, M if trans else N, 1.0, a.data_ptr(), a.stride(1),
-                         bp.data_ptr(), bp.stride(1), 0.0, outp.data_ptr(), outp.stride(1))
-            e1.record()
-        e1.synchronize()
-        ms = e0.elapsed_time(e1) / reps
-        flops = 2.0 * M * N * BLOCK
-        out[name] = {"ms": ms, "tflops": flops / ms / 1e9}
+        k, rows = (M, N) if trans else (N, M)
+        for kind in ("ozaki", "dmma"):
+            def call():
+                if kind == "ozaki":
+                    sl.gemm(trans, BLOCK, 1.0, bp.data_ptr(), bp.stride(1), 0.0, outp.data_ptr(), outp.stride(1))
+                else:
+                    eng.gemm(trans, rows, BLOCK, k, 1.0, a.data_ptr(), a.stride(1), bp.data_ptr(), bp.stride(1),
+                             0.0, outp.data_ptr(), outp.stride(1))
+            for _ in range(3):
+                call()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(stream):
+                e0.record()
+                for _ in range(reps):
+                    call()
+                e1.record()
+            e1.synchronize()
+            ms = e0.elapsed_time(e1) / reps
+            alg_bytes = 8.0 * M * N + 8.0 * k * BLOCK + 8.0 * rows * BLOCK   # A (as slices), B, C
+            out[f"{name}_{kind}"] = {"ms": ms, "gbs": alg_bytes / ms / 1e6, "bytes": alg_bytes,
+                                     "tflops": 2.0 * M * N * BLOCK / ms / 1e9}
+    sl.free()
     return out
 
 
@@ -195,7 +209,7 @@ def sketch_roofline(eng, dev):
 
 
 def load_traffic():
-    path = os.path.join(ROOT, "profiles", "traffic_r01.json")
+    path = os.path.join(ROOT, "profiles", "traffic_r02.json")
     try:
         with open(path) as f:
             return json.load(f)
@@ -301,11 +315,11 @@ def run_ours(args):
         t = torch.tensor([e2e_s], device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_s = t.item()
-    roof = gemm_roofline(eng, a_full if world == 1 else make_matrix(dev), stream)
+    roof = apass_roofline(eng, a_full if world == 1 else make_matrix(dev), stream)
     a_full = None
     torch.cuda.empty_cache()
     sketch = sketch_roofline(eng, dev)
-    dom = roof["tn"]
+    dom = roof["tn_ozaki"]
     traffic = load_traffic()
     line = {
         "metric": "farPCA time-to-eps (s)",
@@ -327,13 +341,17 @@ def run_ours(args):
                    else "single GPU"},
         "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,
-        "roofline": {"bound": "tensor", "kernel": "k_gemm<TN> W=A'Y 8000x50x8000 (DMMA f64)",
-                     "achieved": dom["tflops"], "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                     "frac": dom["tflops"] / FP64_PEAK_TFLOPS,
-                     "peak_source": "measured DMMA microbenchmark (MEASURED_PEAKS.json has no FP64 entry)",
-                     "flops_per_launch": 2.0 * M * N * BLOCK, "launch_ms": dom["ms"],
-                     "nn_achieved": roof["nn"]["tflops"],
-                     "traffic": (traffic or {}).get("tn_bytes_per_launch")},
+        "roofline": {"bound": "hbm",
+                     "kernel": "A pass W=A'Y 8000x50x8000: k_slice_z + k_ozaki (tcgen05 kind::i8 FP64 emulation) "
+                               "+ k_ozaki_fixup",
+                     "achieved": dom["gbs"], "peak": HBM_PEAK_GBS, "unit": "GB/s", "frac": dom["gbs"] / HBM_PEAK_GBS,
+                     "bytes_per_launch": dom["bytes"], "bytes_formula": "8*m*n (A slices) + 8*m*b (Y) + 8*n*b (W)",
+                     "launch_ms": dom["ms"], "nn_achieved": roof["nn_ozaki"]["gbs"],
+                     "nn_launch_ms": roof["nn_ozaki"]["ms"],
+                     "fp64_tflops_equiv": dom["tflops"],
+                     "dmma_same_product": {"tn_ms": roof["tn_dmma"]["ms"], "tn_tflops": roof["tn_dmma"]["tflops"],
+                                           "nn_ms": roof["nn_dmma"]["ms"], "peak_tflops": FP64_PEAK_TFLOPS},
+                     "traffic": (traffic or {}).get("ozaki_tn_bytes_per_launch")},
         "sketch_roofline": sketch,
         "clocks": clk.summary(),
     }

@@ -235,6 +235,20 @@ fqb_status fqb_gemm_emulated(fqb_handle h, int trans_a, int64_t m, int64_t n, in
                              const double* a, int64_t lda, const double* b, int64_t ldb, double beta,
                              double* c, int64_t ldc);
 
+/* Persistent sliced operand: A (m x n, lda, device memory) cut once into the Ozaki
+ * slices of both layouts (16 m n bytes of device memory), then any number of
+ *     C = alpha op(A) B + beta C,   op(A) = A' (trans_a: B m x nb, C n x nb)
+ *                                   op(A) = A  (B n x nb, C m x nb),   nb <= 64
+ * products on the INT8 tensor cores -- the engine's A-pass path, exposed for
+ * callers that apply one matrix many times (and used by bench.py to time it).
+ * A must stay unchanged while the slices are in use only in the sense that the
+ * slices are a snapshot of it.  Asynchronous on the handle's stream. */
+typedef struct fqb_sliced_s* fqb_sliced;
+fqb_status fqb_slice_operand(fqb_handle h, const double* a, int64_t m, int64_t n, int64_t lda, fqb_sliced* out);
+fqb_status fqb_sliced_gemm(fqb_handle h, fqb_sliced s, int trans_a, int64_t nb, double alpha, const double* b,
+                           int64_t ldb, double beta, double* c, int64_t ldc);
+fqb_status fqb_sliced_free(fqb_handle h, fqb_sliced s);
+
 /* ---- defaults (driver.cpp:449-466) ------------------------------------------- */
 double fqb_default_density(int kind, int64_t n);
 int fqb_default_block(int64_t m, int64_t n);

@@ -417,7 +417,75 @@ fqb_status fqb_gemm_emulated(fqb_handle h, int trans_a, int64_t m, int64_t n, in
         farqb::ozaki_slice_z(b, k, n, ldb, ez.ptr, zs.ptr, s, h->h.lc);
         farqb::ozaki_gemm(m, n, k, alpha, xs.ptr, ex.ptr, zs.ptr, ez.ptr, beta, c, ldc, h->h.gws.work, h->h.num_sms,
                           s, h->h.lc);
-        FQB_CUDA(cudaStreamSynchronize(s));
+        return FQB_OK;   // temporaries are freed stream-ordered, after the kernels
+    });
+}
+
+}  // extern "C"
+
+struct fqb_sliced_s {
+    int64_t m = 0, n = 0;
+    farqb::DeviceArray<int8_t> x_nn, x_tn, z;
+    farqb::DeviceArray<int> e_nn, e_tn, ez;
+};
+
+extern "C" {
+
+fqb_status fqb_slice_operand(fqb_handle h, const double* a, int64_t m, int64_t n, int64_t lda, fqb_sliced* out) {
+    return guarded([&]() -> fqb_status {
+        bind(h);
+        if (!out) throw farqb::Error(FQB_ERR_INVALID_ARGUMENT, "null output");
+        *out = nullptr;
+        if (m <= 0 || n <= 0) throw farqb::Error(FQB_ERR_DIMENSION, "fqb_slice_operand: empty operand");
+        if (lda < m) throw farqb::Error(FQB_ERR_DIMENSION, "leading dimension too small");
+        if (!a) throw farqb::Error(FQB_ERR_INVALID_ARGUMENT, "null operand");
+        cudaStream_t s = h->h.stream;
+        auto* sl = new fqb_sliced_s();
+        try {
+            sl->m = m;
+            sl->n = n;
+            sl->x_nn.ensure(size_t(farqb::ozaki_x_bytes(m, n)), s);
+            sl->x_tn.ensure(size_t(farqb::ozaki_x_bytes(n, m)), s);
+            sl->e_nn.ensure(size_t(m), s);
+            sl->e_tn.ensure(size_t(n), s);
+            sl->ez.ensure(size_t(farqb::ozaki_max_n()), s);
+            farqb::DeviceArray<unsigned> line_max;
+            line_max.ensure(size_t(farqb::ozaki_line_max_words(m, n)), s);
+            farqb::ozaki_slice_a(a, m, n, lda, line_max.ptr, sl->x_tn.ptr, sl->e_tn.ptr, sl->x_nn.ptr, sl->e_nn.ptr, s,
+                                 h->h.lc);
+        } catch (...) {
+            delete sl;
+            throw;
+        }
+        *out = sl;
+        return FQB_OK;
+    });
+}
+
+fqb_status fqb_sliced_gemm(fqb_handle h, fqb_sliced sl, int trans_a, int64_t nb, double alpha, const double* b,
+                           int64_t ldb, double beta, double* c, int64_t ldc) {
+    return guarded([&]() -> fqb_status {
+        bind(h);
+        if (!sl) throw farqb::Error(FQB_ERR_INVALID_ARGUMENT, "null sliced operand");
+        if (nb < 0 || nb > farqb::ozaki_max_n()) throw farqb::Error(FQB_ERR_DIMENSION, "fqb_sliced_gemm: nb > 64");
+        const int64_t M = trans_a ? sl->n : sl->m, K = trans_a ? sl->m : sl->n;
+        if (ldb < K || ldc < M) throw farqb::Error(FQB_ERR_DIMENSION, "leading dimension too small");
+        if (nb == 0) return FQB_OK;
+        cudaStream_t s = h->h.stream;
+        farqb::ensure_gemm_workspace(h->h);
+        sl->z.ensure(size_t(farqb::ozaki_z_bytes(nb, K)), s);
+        farqb::ozaki_slice_z(b, K, nb, ldb, sl->ez.ptr, sl->z.ptr, s, h->h.lc);
+        farqb::ozaki_gemm(M, nb, K, alpha, trans_a ? sl->x_tn.ptr : sl->x_nn.ptr, trans_a ? sl->e_tn.ptr : sl->e_nn.ptr,
+                          sl->z.ptr, sl->ez.ptr, beta, c, ldc, h->h.gws.work, h->h.num_sms, s, h->h.lc);
+        return FQB_OK;
+    });
+}
+
+fqb_status fqb_sliced_free(fqb_handle h, fqb_sliced sl) {
+    return guarded([&]() -> fqb_status {
+        if (!sl) return FQB_OK;
+        bind(h);
+        delete sl;   // device memory returns to the pool, ordered after the handle's queued work
         return FQB_OK;
     });
 }

@@ -296,6 +296,40 @@ def _as_colmajor(a):
     return arr.ctypes.data, m, n, max(m, 1), False, arr
 
 
+class SlicedOperand:
+    """A matrix held as Ozaki slices on the device (both layouts); products with
+    up to 64 right-hand columns run on the INT8 tensor cores (fqb_sliced_gemm)."""
+
+    def __init__(self, engine, handle, m, n):
+        self._eng, self._s, self.m, self.n = engine, handle, m, n
+
+    def gemm(self, trans_a: bool, nb, alpha, b_ptr, ldb, beta, c_ptr, ldc):
+        """C = alpha op(A) B + beta C; op(A) = A' if trans_a (C is n x nb) else A (C is m x nb)."""
+        if self._s is None:
+            raise InvalidArgument("sliced operand was freed")
+        st = self._eng._lib.fqb_sliced_gemm(self._eng._h, self._s, int(trans_a), nb, alpha, b_ptr, ldb, beta,
+                                            c_ptr, ldc)
+        if st:
+            _raise(st, "fqb_sliced_gemm")
+
+    def free(self):
+        if self._s is not None:
+            self._eng._lib.fqb_sliced_free(self._eng._h, self._s)
+            self._s = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.free()
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:  # pragma: no cover - interpreter teardown
+            pass
+
+
 class Engine:
     """One libfarqb handle (one device, one stream, reusable workspace)."""
 
@@ -515,6 +549,14 @@ class Engine:
                                          c_ptr, ldc)
         if st:
             _raise(st, "fqb_gemm_emulated")
+
+    def slice_operand(self, a_ptr, m, n, lda) -> "SlicedOperand":
+        """Cut A (m x n, device, column-major) once into Ozaki slices (fqb_slice_operand)."""
+        out = C.c_void_p()
+        st = self._lib.fqb_slice_operand(self._h, a_ptr, m, n, lda, C.byref(out))
+        if st:
+            _raise(st, "fqb_slice_operand")
+        return SlicedOperand(self, out, m, n)
 
     def sparse_dense_mul(self, a_ptr, m, n, lda, col_ptr_ptr, row_idx_ptr, values_ptr, l, z_ptr,
                          c_ptr, ldc):

@@ -151,3 +151,26 @@ def test_emulation_on_and_off_agree(eng, monkeypatch):
     qb1 = r1.q @ r1.bt.T
     qb0 = r0.q @ r0.bt.T
     assert np.abs(qb1 - qb0).max() <= 1e-10 * np.abs(a).max()
+
+
+def test_sliced_operand_matches_one_shot_emulation(eng):
+    """fqb_slice_operand + fqb_sliced_gemm (both layouts, repeated use) == fqb_gemm_emulated bit for bit."""
+    m, n, nb = 1100, 900, 37
+    g = torch.Generator(device="cpu").manual_seed(21)
+    a = torch.randn((n, m), dtype=torch.float64, generator=g).cuda().t()        # m x n column-major
+    with eng.slice_operand(a.data_ptr(), m, n, m) as sl:
+        for trans in (True, False):
+            k, rows = (m, n) if trans else (n, m)
+            b = torch.randn((nb, k), dtype=torch.float64, generator=g).cuda().t()
+            c0 = torch.randn((nb, rows), dtype=torch.float64, generator=g).cuda().t()
+            c1, c2 = c0.clone(), c0.clone()
+            for _ in range(2):
+                c1.copy_(c0)
+                sl.gemm(trans, nb, 0.5, b.data_ptr(), k, 2.0, c1.data_ptr(), rows)
+            eng.gemm_emulated(trans, rows, nb, k, 0.5, a.data_ptr(), m, b.data_ptr(), k, 2.0, c2.data_ptr(), rows)
+            torch.cuda.synchronize()
+            assert torch.equal(c1, c2)
+            want = 0.5 * ((a.t() if trans else a).cpu() @ b.cpu()) + 2.0 * c0.cpu()
+            assert (c1.cpu() - want).abs().max().item() < 1e-12
+    with pytest.raises(fqb.InvalidArgument):
+        sl.gemm(True, nb, 1.0, b.data_ptr(), m, 0.0, c1.data_ptr(), n)
