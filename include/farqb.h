@@ -174,6 +174,20 @@ fqb_status fqb_qb_fixed_rank(fqb_handle h, const double* a, int64_t m, int64_t n
                              int64_t lda, int a_on_device, int rank, const fqb_config* cfg,
                              fqb_block_source_fn src, void* user, unsigned flags,
                              fqb_qb_result* out);
+/* FP32 input mode (BASELINE config 5: 400000 x 50000 FP32): A stays in FP32 in
+ * HBM (half the bytes of FP64), every product is formed in FP64 from the exactly
+ * widened values -- the results are those of the FP64 loop on double(A), within
+ * the FP64 parity bounds, which are tighter than the FP32-mode 1e-4.  The A passes
+ * slice A straight from FP32 for the INT8 tensor cores; when they run on DMMA
+ * instead (b > 64, small A, slices out of memory) one widened FP64 copy is made. */
+fqb_status fqb_qb_fixed_precision_f32(fqb_handle h, const float* a, int64_t m, int64_t n,
+                                      int64_t lda, int a_on_device, const fqb_config* cfg,
+                                      fqb_block_source_fn src, void* user, unsigned flags,
+                                      fqb_qb_result* out);
+fqb_status fqb_qb_fixed_rank_f32(fqb_handle h, const float* a, int64_t m, int64_t n,
+                                 int64_t lda, int a_on_device, int rank, const fqb_config* cfg,
+                                 fqb_block_source_fn src, void* user, unsigned flags,
+                                 fqb_qb_result* out);
 void fqb_result_free(fqb_qb_result* r);
 
 /* ---- row-sharded multi-GPU (one rank per GPU, NCCL over NVLink) ------------- */

@@ -25,6 +25,7 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
 #include <utility>
 #include <vector>
 
@@ -42,6 +43,19 @@ struct DenseMatrix {
     double operator()(int i, int j) const { return data[std::size_t(j) * rows + i]; }
     double* col(int j) { return data.data() + std::size_t(j) * rows; }
     const double* col(int j) const { return data.data() + std::size_t(j) * rows; }
+};
+
+// FP32 input (BASELINE config 5): same layout as DenseMatrix with float storage.
+// Engine::run_* on a FloatMatrix takes the FP32 input mode (A stays FP32 on the
+// device, every product is formed in FP64).
+struct FloatMatrix {
+    int rows = 0;
+    int cols = 0;
+    std::vector<float> data;  // column-major
+    FloatMatrix() = default;
+    FloatMatrix(int r, int c) : rows(r), cols(c), data(std::size_t(r) * c, 0.0f) {}
+    float& operator()(int i, int j) { return data[std::size_t(j) * rows + i]; }
+    float operator()(int i, int j) const { return data[std::size_t(j) * rows + i]; }
 };
 
 enum class SketchKind { Gaussian = FQB_GAUSSIAN, Bernoulli = FQB_BERNOULLI, StdBernoulli = FQB_STD_BERNOULLI,
@@ -245,13 +259,17 @@ class Engine {
         detail::SourceCtx ctx{source, {}, nullptr};
         fqb_qb_result r{};
         const int m = a.rows, n = a.cols;
-        const fqb_status st =
-            rank < 0 ? fqb_qb_fixed_precision(h_, a.data.data(), m, n, m, 0, &c,
-                                              source ? detail::source_trampoline : nullptr, &ctx,
-                                              FQB_OUT_HOST | FQB_OUT_SVD, &r)
-                     : fqb_qb_fixed_rank(h_, a.data.data(), m, n, m, 0, rank, &c,
-                                         source ? detail::source_trampoline : nullptr, &ctx,
-                                         FQB_OUT_HOST | FQB_OUT_SVD, &r);
+        auto* cb = source ? detail::source_trampoline : nullptr;
+        const unsigned fl = FQB_OUT_HOST | FQB_OUT_SVD;
+        fqb_status st;
+        if constexpr (std::is_same_v<std::decay_t<decltype(a.data[0])>, float>) {
+            // FP32 input mode (fqb_qb_*_f32): A kept in FP32, products in FP64
+            st = rank < 0 ? fqb_qb_fixed_precision_f32(h_, a.data.data(), m, n, m, 0, &c, cb, &ctx, fl, &r)
+                          : fqb_qb_fixed_rank_f32(h_, a.data.data(), m, n, m, 0, rank, &c, cb, &ctx, fl, &r);
+        } else {
+            st = rank < 0 ? fqb_qb_fixed_precision(h_, a.data.data(), m, n, m, 0, &c, cb, &ctx, fl, &r)
+                          : fqb_qb_fixed_rank(h_, a.data.data(), m, n, m, 0, rank, &c, cb, &ctx, fl, &r);
+        }
         if (ctx.error) {
             fqb_result_free(&r);
             std::rethrow_exception(ctx.error);

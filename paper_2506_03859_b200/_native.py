@@ -70,6 +70,12 @@ SIGNATURES = [
     ("fqb_qb_fixed_rank", C.c_int, [_H, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_int, C.c_int,
                                     C.POINTER(ConfigC), SOURCE_FN, C.c_void_p, C.c_uint,
                                     C.POINTER(ResultC)]),
+    ("fqb_qb_fixed_precision_f32", C.c_int, [_H, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_int,
+                                         C.POINTER(ConfigC), SOURCE_FN, C.c_void_p, C.c_uint,
+                                         C.POINTER(ResultC)]),
+    ("fqb_qb_fixed_rank_f32", C.c_int, [_H, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_int, C.c_int,
+                                    C.POINTER(ConfigC), SOURCE_FN, C.c_void_p, C.c_uint,
+                                    C.POINTER(ResultC)]),
     ("fqb_result_free", None, [C.POINTER(ResultC)]),
     ("fqb_comm_unique_id", C.c_int, [C.c_void_p]),
     ("fqb_comm_attach", C.c_int, [_H, C.c_void_p, C.c_int, C.c_int]),

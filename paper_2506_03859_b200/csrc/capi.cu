@@ -173,7 +173,7 @@ fqb_status fqb_comm_detach(fqb_handle h) {
     });
 }
 
-static fqb_status run_common(fqb_handle h, const double* a, int64_t m, int64_t n, int64_t lda,
+static fqb_status run_common(fqb_handle h, const void* a, bool a_f32, int64_t m, int64_t n, int64_t lda,
                              int a_on_device, bool fixed_precision, int rank, const fqb_config* cfg,
                              fqb_block_source_fn src, void* user, unsigned flags, fqb_qb_result* out) {
     if (out) std::memset(out, 0, sizeof *out);
@@ -181,8 +181,8 @@ static fqb_status run_common(fqb_handle h, const double* a, int64_t m, int64_t n
         bind(h);
         if (!cfg || !out) throw farqb::Error(FQB_ERR_INVALID_ARGUMENT, "null config or result");
         std::string msg;
-        const int st = farqb::run_qb(h->h, a, m, n, lda, a_on_device != 0, fixed_precision, rank, *cfg, src,
-                                     user, flags, out, &msg);
+        const int st = farqb::run_qb(h->h, a, a_f32, m, n, lda, a_on_device != 0, fixed_precision, rank, *cfg,
+                                     src, user, flags, out, &msg);
         out->status = st;
         if (st != FQB_OK) g_last_error = msg;
         return static_cast<fqb_status>(st);
@@ -192,7 +192,23 @@ static fqb_status run_common(fqb_handle h, const double* a, int64_t m, int64_t n
 fqb_status fqb_qb_fixed_precision(fqb_handle h, const double* a, int64_t m, int64_t n, int64_t lda,
                                   int a_on_device, const fqb_config* cfg, fqb_block_source_fn src,
                                   void* user, unsigned flags, fqb_qb_result* out) {
-    const fqb_status st = run_common(h, a, m, n, lda, a_on_device, true, 0, cfg, src, user, flags, out);
+    const fqb_status st = run_common(h, a, false, m, n, lda, a_on_device, true, 0, cfg, src, user, flags, out);
+    if (out) out->status = st;
+    return st;
+}
+
+fqb_status fqb_qb_fixed_precision_f32(fqb_handle h, const float* a, int64_t m, int64_t n, int64_t lda,
+                                      int a_on_device, const fqb_config* cfg, fqb_block_source_fn src, void* user,
+                                      unsigned flags, fqb_qb_result* out) {
+    const fqb_status st = run_common(h, a, true, m, n, lda, a_on_device, true, 0, cfg, src, user, flags, out);
+    if (out) out->status = st;
+    return st;
+}
+
+fqb_status fqb_qb_fixed_rank_f32(fqb_handle h, const float* a, int64_t m, int64_t n, int64_t lda,
+                                 int a_on_device, int rank, const fqb_config* cfg, fqb_block_source_fn src,
+                                 void* user, unsigned flags, fqb_qb_result* out) {
+    const fqb_status st = run_common(h, a, true, m, n, lda, a_on_device, false, rank, cfg, src, user, flags, out);
     if (out) out->status = st;
     return st;
 }
@@ -200,7 +216,7 @@ fqb_status fqb_qb_fixed_precision(fqb_handle h, const double* a, int64_t m, int6
 fqb_status fqb_qb_fixed_rank(fqb_handle h, const double* a, int64_t m, int64_t n, int64_t lda,
                              int a_on_device, int rank, const fqb_config* cfg, fqb_block_source_fn src,
                              void* user, unsigned flags, fqb_qb_result* out) {
-    const fqb_status st = run_common(h, a, m, n, lda, a_on_device, false, rank, cfg, src, user, flags, out);
+    const fqb_status st = run_common(h, a, false, m, n, lda, a_on_device, false, rank, cfg, src, user, flags, out);
     if (out) out->status = st;
     return st;
 }

@@ -116,9 +116,10 @@ namespace {
 
 class QbRun {
   public:
-    QbRun(Handle& h, const double* a, int64_t m, int64_t n, int64_t lda, const fqb_config& cfg,
+    // exactly one of a (FP64) / af (FP32 input mode) is non-null
+    QbRun(Handle& h, const double* a, const float* af, int64_t m, int64_t n, int64_t lda, const fqb_config& cfg,
           fqb_block_source_fn src, void* user)
-        : h_(h), s_(h.stream), a_(a), m_(m), n_(n), lda_(lda), cfg_(cfg), b_(cfg.block), src_(src),
+        : h_(h), s_(h.stream), a_(a), af_(af), m_(m), n_(n), lda_(lda), cfg_(cfg), b_(cfg.block), src_(src),
           user_(user) {
         ldq_ = round_up(m_, 8);
         ldbt_ = round_up(n_, 8);
@@ -161,7 +162,8 @@ class QbRun {
     // --- setup: ||A||^2 and (StdBernoulli) the centering column -----------------
     void setup() {
         FQB_CUDA(cudaMemsetAsync(scal_, 0, kScalarCount * sizeof(double), s_));
-        launch_sumsq(a_, m_, n_, lda_, h_.ws.partial.ptr, scal_ + kNormA, s_, h_.lc);
+        if (af_) launch_sumsq(af_, m_, n_, lda_, h_.ws.partial.ptr, scal_ + kNormA, s_, h_.lc);
+        else launch_sumsq(a_, m_, n_, lda_, h_.ws.partial.ptr, scal_ + kNormA, s_, h_.lc);
         comm_allreduce_sum(h_, scal_ + kNormA, 1, s_);
         // z = A (p 1_n) exists when the reference would build it (driver.cpp:364-365);
         // it is only computed once a sparse centered block actually needs it.
@@ -263,15 +265,31 @@ class QbRun {
         w.oz_e_nn.ensure(size_t(m_), s_);
         w.oz_e_tn.ensure(size_t(n_), s_);
         w.oz_line_max.ensure(size_t(ozaki_line_max_words(m_, n_)), s_);
-        ozaki_slice_a(a_, m_, n_, lda_, w.oz_line_max.ptr, w.oz_x_tn.ptr, w.oz_e_tn.ptr, w.oz_x_nn.ptr, w.oz_e_nn.ptr,
-                      s_, h_.lc);
+        if (af_)
+            ozaki_slice_a(af_, m_, n_, lda_, w.oz_line_max.ptr, w.oz_x_tn.ptr, w.oz_e_tn.ptr, w.oz_x_nn.ptr,
+                          w.oz_e_nn.ptr, s_, h_.lc);
+        else
+            ozaki_slice_a(a_, m_, n_, lda_, w.oz_line_max.ptr, w.oz_x_tn.ptr, w.oz_e_tn.ptr, w.oz_x_nn.ptr,
+                          w.oz_e_nn.ptr, s_, h_.lc);
         return true;
+    }
+
+    // FP32 input on the DMMA path: one widened FP64 copy of A for the run
+    void ensure_fp64_a() {
+        if (a_) return;
+        const int64_t ld = round_up(m_, 8);
+        h_.ws.a_copy.ensure(size_t(ld) * size_t(n_), s_);
+        launch_widen(af_, m_, n_, lda_, h_.ws.a_copy.ptr, ld, s_, h_.lc);
+        a_ = h_.ws.a_copy.ptr;
+        a_ld64_ = ld;
     }
 
     void a_gemm(bool ta, int N, const double* B, int64_t ldb, double* C, int64_t ldc) {
         if (!oz_on_ || N > ozaki_max_n()) {
-            if (ta) gemm_(true, n_, N, m_, 1.0, a_, lda_, B, ldb, 0.0, C, ldc);
-            else gemm_(false, m_, N, n_, 1.0, a_, lda_, B, ldb, 0.0, C, ldc);
+            ensure_fp64_a();
+            const int64_t lda = a_ld64_ ? a_ld64_ : lda_;
+            if (ta) gemm_(true, n_, N, m_, 1.0, a_, lda, B, ldb, 0.0, C, ldc);
+            else gemm_(false, m_, N, n_, 1.0, a_, lda, B, ldb, 0.0, C, ldc);
             return;
         }
         const int64_t M = ta ? n_ : m_, K = ta ? m_ : n_;
@@ -384,7 +402,8 @@ class QbRun {
         if (!z_allowed_) throw Error(kStatusDimension, "centered_product: stale centering column");
         if (!have_z_) {
             h_.ws.zc.ensure(size_t(m_), s_);
-            launch_centering(a_, m_, n_, lda_, cfg_.sketch.p, h_.ws.zc.ptr, s_, h_.lc);
+            if (af_) launch_centering(af_, m_, n_, lda_, cfg_.sketch.p, h_.ws.zc.ptr, s_, h_.lc);
+            else launch_centering(a_, m_, n_, lda_, cfg_.sketch.p, h_.ws.zc.ptr, s_, h_.lc);
             have_z_ = true;
         }
         // B row sums for the centered deflation term, for every accepted column
@@ -402,8 +421,12 @@ class QbRun {
         if (om_dense_) {
             a_gemm(false, b_, w.omega.ptr, ldo_, y, ldy);
         } else {
-            launch_gather_spmm(a_, m_, lda_, w.col_ptr.ptr, w.row_idx.ptr, w.values.ptr, b_,
-                               om_centered_ ? w.zc.ptr : nullptr, y, ldy, s_, h_.lc);
+            if (af_)
+                launch_gather_spmm(af_, m_, lda_, w.col_ptr.ptr, w.row_idx.ptr, w.values.ptr, b_,
+                                   om_centered_ ? w.zc.ptr : nullptr, y, ldy, s_, h_.lc);
+            else
+                launch_gather_spmm(a_, m_, lda_, w.col_ptr.ptr, w.row_idx.ptr, w.values.ptr, b_,
+                                   om_centered_ ? w.zc.ptr : nullptr, y, ldy, s_, h_.lc);
         }
     }
 
@@ -554,6 +577,8 @@ class QbRun {
     Handle& h_;
     cudaStream_t s_;
     const double* a_;
+    const float* af_;          // FP32 input mode (a_ null until a DMMA pass needs the widened copy)
+    int64_t a_ld64_ = 0;       // leading dimension of the widened copy
     int64_t m_, n_, lda_;
     fqb_config cfg_;
     int b_;
@@ -580,7 +605,7 @@ class QbRun {
 
 }  // namespace
 
-int run_qb(Handle& h, const double* a, int64_t m, int64_t n, int64_t lda, bool a_on_device,
+int run_qb(Handle& h, const void* a, bool a_f32, int64_t m, int64_t n, int64_t lda, bool a_on_device,
            bool fixed_precision, int rank, const fqb_config& cfg_in, fqb_block_source_fn src, void* user,
            unsigned flags, fqb_qb_result* out, std::string* message_out) {
     std::memset(out, 0, sizeof *out);
@@ -614,21 +639,30 @@ int run_qb(Handle& h, const double* a, int64_t m, int64_t n, int64_t lda, bool a
     cudaStream_t s = h.stream;
     FQB_CUDA(cudaEventRecord(h.ev0, s));
 
-    // A on the device with an even, 16-byte aligned leading dimension
-    const double* ad = a;
+    // A on the device with an even, 16-byte aligned leading dimension (FP64, or
+    // FP32 in the FP32 input mode: A kept in FP32, every product in FP64)
+    const size_t esz = a_f32 ? sizeof(float) : sizeof(double);
+    const void* ad = a;
     int64_t ldad = lda;
     const bool usable = a_on_device && lda % 2 == 0 && reinterpret_cast<uintptr_t>(a) % 16 == 0;
     if (!usable) {
         ldad = round_up(m, 8);
-        h.ws.a_copy.ensure(size_t(ldad) * n, s);
-        FQB_CUDA(cudaMemcpy2DAsync(h.ws.a_copy.ptr, ldad * sizeof(double), a, lda * sizeof(double),
-                                   m * sizeof(double), n,
+        void* dst;
+        if (a_f32) {
+            h.ws.a_copy_f32.ensure(size_t(ldad) * n, s);
+            dst = h.ws.a_copy_f32.ptr;
+        } else {
+            h.ws.a_copy.ensure(size_t(ldad) * n, s);
+            dst = h.ws.a_copy.ptr;
+        }
+        FQB_CUDA(cudaMemcpy2DAsync(dst, ldad * esz, a, lda * esz, m * esz, n,
                                    a_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
-        ad = h.ws.a_copy.ptr;
+        ad = dst;
     }
 
     const auto t_host0 = std::chrono::steady_clock::now();
-    QbRun run(h, ad, m, n, ldad, cfg, src, user);
+    QbRun run(h, a_f32 ? nullptr : static_cast<const double*>(ad), a_f32 ? static_cast<const float*>(ad) : nullptr, m,
+              n, ldad, cfg, src, user);
     run.setup();
     int status = 0;
     bool converged = false;

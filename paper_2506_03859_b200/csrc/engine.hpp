@@ -50,6 +50,7 @@ struct DeviceArray {
 struct Workspace {
     DeviceArray<double> omega, y0, ys, wp, wraw, g, t, cd, c2, small, zc, rowsum_b, splitk, partial,
         scalars, scratch, a_copy;
+    DeviceArray<float> a_copy_f32;   // FP32 input mode staging
     DeviceArray<int> col_ptr, row_idx, counts;
     DeviceArray<double> values;
     DeviceArray<unsigned> status;
@@ -67,6 +68,7 @@ struct Workspace {
             d->release();
         for (auto* d : {&col_ptr, &row_idx, &counts, &oz_e_nn, &oz_e_tn, &oz_ez}) d->release();
         for (auto* d : {&status, &gemm_flags, &oz_line_max}) d->release();
+        a_copy_f32.release();
         for (auto* d : {&oz_x_nn, &oz_x_tn, &oz_z}) d->release();
     }
 };
@@ -111,7 +113,7 @@ void ensure_gemm_workspace(Handle& h);
 
 // Runs the loop; fills `out` (status also returned).  Throws farqb::Error for
 // configuration / CUDA failures before any result exists.
-int run_qb(Handle& h, const double* a, int64_t m, int64_t n, int64_t lda, bool a_on_device,
+int run_qb(Handle& h, const void* a, bool a_f32, int64_t m, int64_t n, int64_t lda, bool a_on_device,
            bool fixed_precision, int rank, const fqb_config& cfg, fqb_block_source_fn src,
            void* user, unsigned flags, fqb_qb_result* out, std::string* message_out);
 

@@ -53,6 +53,9 @@ void launch_densify(const int* col_ptr, const int* row_idx, const double* values
 void launch_gather_spmm(const double* a, int64_t m, int64_t lda, const int* col_ptr,
                         const int* row_idx, const double* values, int l, const double* z,
                         double* c, int64_t ldc, cudaStream_t s, LaunchCounter& lc);
+void launch_gather_spmm(const float* a, int64_t m, int64_t lda, const int* col_ptr,
+                        const int* row_idx, const double* values, int l, const double* z,
+                        double* c, int64_t ldc, cudaStream_t s, LaunchCounter& lc);
 // T (k x l) = Wt' * S [- shift * colsum(Wt) broadcast] where Wt is n x k (ld),
 // i.e. the row-gather product used by the deflation B * Omega.
 void launch_gather_tmul(const double* wt, int64_t n, int64_t ldw, int k, const int* col_ptr,
@@ -64,9 +67,16 @@ void launch_gather_tmul(const double* wt, int64_t n, int64_t ldw, int k, const i
 constexpr int kReducePartials = 1184;  // 8 x 148
 void launch_sumsq(const double* a, int64_t m, int64_t n, int64_t lda, double* partial, double* out,
                   cudaStream_t s, LaunchCounter& lc);
+void launch_sumsq(const float* a, int64_t m, int64_t n, int64_t lda, double* partial, double* out,
+                  cudaStream_t s, LaunchCounter& lc);
+// FP32 input mode: out (ldo) = double(a) when the A passes run on DMMA
+void launch_widen(const float* a, int64_t m, int64_t n, int64_t lda, double* out, int64_t ldo, cudaStream_t s,
+                  LaunchCounter& lc);
 // z[i] = sum_c fma(p, A[i,c], z[i]) in column order (driver.cpp:178-183), bitwise
 // the reference's axpy sequence.
 void launch_centering(const double* a, int64_t m, int64_t n, int64_t lda, double p, double* z,
+                      cudaStream_t s, LaunchCounter& lc);
+void launch_centering(const float* a, int64_t m, int64_t n, int64_t lda, double p, double* z,
                       cudaStream_t s, LaunchCounter& lc);
 // colsum[j] = sum_i X[i, j] for j < k (X is rows x k, ld)
 void launch_colsum(const double* x, int64_t rows, int k, int64_t ld, double* colsum, cudaStream_t s,
@@ -117,6 +127,8 @@ int64_t ozaki_workspace_doubles(int num_sms);
 // line_max: ozaki_line_max_words(m, n) words of scratch.
 int64_t ozaki_line_max_words(int64_t m, int64_t n);
 void ozaki_slice_a(const double* a, int64_t m, int64_t n, int64_t ld, unsigned* line_max, int8_t* x_tn, int* e_tn,
+                   int8_t* x_nn, int* e_nn, cudaStream_t s, LaunchCounter& lc);
+void ozaki_slice_a(const float* a, int64_t m, int64_t n, int64_t ld, unsigned* line_max, int8_t* x_tn, int* e_tn,
                    int8_t* x_nn, int* e_nn, cudaStream_t s, LaunchCounter& lc);
 // Z (k x n, ld)
 void ozaki_slice_z(const double* b, int64_t k, int64_t n, int64_t ld, int* e, int8_t* out, cudaStream_t s,

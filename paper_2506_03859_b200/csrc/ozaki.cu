@@ -432,7 +432,8 @@ __device__ __forceinline__ void put_chunk16(const double (&v)[16], int e, int8_t
 
 // Row and column maxima (high words) of A (m x n, ld) in one pass; rmax / cmax
 // must be zeroed.  CTA: 256 rows x 128 columns, a thread walks one row.
-__global__ void __launch_bounds__(256) k_line_max(const double* __restrict__ a, int64_t m, int64_t n, int64_t ld,
+template <typename T>   // double, or float A (FP32 input mode: widened exactly)
+__global__ void __launch_bounds__(256) k_line_max(const T* __restrict__ a, int64_t m, int64_t n, int64_t ld,
                                                   unsigned* rmax, unsigned* cmax) {
     __shared__ unsigned cm[8][128];
     const int64_t i = int64_t(blockIdx.x) * 256 + threadIdx.x;
@@ -442,7 +443,7 @@ __global__ void __launch_bounds__(256) k_line_max(const double* __restrict__ a, 
 #pragma unroll 4
     for (int c = 0; c < 128; ++c) {
         const int64_t j = j0 + c;
-        const unsigned h = (i < m && j < n) ? abs_hi(a[j * ld + i]) : 0u;
+        const unsigned h = (i < m && j < n) ? abs_hi(double(a[j * ld + i])) : 0u;
         rm = max(rm, h);
         const unsigned wm = __reduce_max_sync(0xFFFFFFFFu, h);
         if (lane == 0) cm[warp][c] = wm;
@@ -463,7 +464,8 @@ __global__ void __launch_bounds__(256) k_line_max(const double* __restrict__ a, 
 //   x_nn: operand rows = rows of A,    K = n (A G),   e_nn per row
 // Either may be null.  The grid covers the padded operand rows, so every byte of
 // both slice buffers is written (zeros outside A) and no memset is needed.
-__global__ void __launch_bounds__(256) k_slice_a(const double* __restrict__ a, int64_t m, int64_t n, int64_t ld,
+template <typename T>
+__global__ void __launch_bounds__(256) k_slice_a(const T* __restrict__ a, int64_t m, int64_t n, int64_t ld,
                                                  const unsigned* __restrict__ rmax, const unsigned* __restrict__ cmax,
                                                  int8_t* x_tn, int* e_tn, int8_t* x_nn, int* e_nn) {
     __shared__ double t[64][65];   // t[j][i]
@@ -474,7 +476,7 @@ __global__ void __launch_bounds__(256) k_slice_a(const double* __restrict__ a, i
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const int64_t i = i0 + lane + 32 * h;
-            t[jj][lane + 32 * h] = (i < m && j < n) ? a[j * ld + i] : 0.0;
+            t[jj][lane + 32 * h] = (i < m && j < n) ? double(a[j * ld + i]) : 0.0;
         }
     }
     __syncthreads();
@@ -581,19 +583,29 @@ int64_t ozaki_z_bytes(int64_t n, int64_t k) { return ceil_div(k, OZ_BK) * S * in
 
 int64_t ozaki_line_max_words(int64_t m, int64_t n) { return m + n; }
 
-void ozaki_slice_a(const double* a, int64_t m, int64_t n, int64_t ld, unsigned* line_max, int8_t* x_tn, int* e_tn,
-                   int8_t* x_nn, int* e_nn, cudaStream_t s, LaunchCounter& lc) {
+template <typename T>
+static void slice_a_impl(const T* a, int64_t m, int64_t n, int64_t ld, unsigned* line_max, int8_t* x_tn, int* e_tn,
+                         int8_t* x_nn, int* e_nn, cudaStream_t s, LaunchCounter& lc) {
     if (m <= 0 || n <= 0) return;
     unsigned* rmax = line_max;
     unsigned* cmax = line_max + m;
     FQB_CUDA(cudaMemsetAsync(line_max, 0, sizeof(unsigned) * size_t(m + n), s));
-    k_line_max<<<dim3(unsigned(ceil_div(m, 256)), unsigned(ceil_div(n, 128))), 256, 0, s>>>(a, m, n, ld, rmax, cmax);
+    k_line_max<T><<<dim3(unsigned(ceil_div(m, 256)), unsigned(ceil_div(n, 128))), 256, 0, s>>>(a, m, n, ld, rmax, cmax);
     FQB_LAUNCHED();
     // cover the padded operand rows of both layouts (multiples of OZ_BM)
     const dim3 g(unsigned(ceil_div(m, OZ_BM) * (OZ_BM / 64)), unsigned(ceil_div(n, OZ_BM) * (OZ_BM / 64)));
-    k_slice_a<<<g, 256, 0, s>>>(a, m, n, ld, rmax, cmax, x_tn, e_tn, x_nn, e_nn);
+    k_slice_a<T><<<g, 256, 0, s>>>(a, m, n, ld, rmax, cmax, x_tn, e_tn, x_nn, e_nn);
     FQB_LAUNCHED();
     lc.bump(2);
+}
+
+void ozaki_slice_a(const double* a, int64_t m, int64_t n, int64_t ld, unsigned* line_max, int8_t* x_tn, int* e_tn,
+                   int8_t* x_nn, int* e_nn, cudaStream_t s, LaunchCounter& lc) {
+    slice_a_impl(a, m, n, ld, line_max, x_tn, e_tn, x_nn, e_nn, s, lc);
+}
+void ozaki_slice_a(const float* a, int64_t m, int64_t n, int64_t ld, unsigned* line_max, int8_t* x_tn, int* e_tn,
+                   int8_t* x_nn, int* e_nn, cudaStream_t s, LaunchCounter& lc) {
+    slice_a_impl(a, m, n, ld, line_max, x_tn, e_tn, x_nn, e_nn, s, lc);
 }
 
 void ozaki_slice_z(const double* b, int64_t k, int64_t n, int64_t ld, int* e, int8_t* out, cudaStream_t s,

@@ -7,6 +7,7 @@
 //                     fma each -- the reference's axpy sequence, so z (and the
 //                     centered sketch Y = A S - z) match it bit for bit.
 //  launch_colsum      column sums of B' for the centered deflation term.
+#include <algorithm>
 #include <cstdint>
 
 #include "kernels.hpp"
@@ -34,7 +35,8 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
     return v;  // valid in thread 0
 }
 
-__global__ void __launch_bounds__(256) k_sumsq_partial(const double* __restrict__ a, int64_t m,
+template <typename T>   // double, or float A (FP32 input mode; squares summed in FP64)
+__global__ void __launch_bounds__(256) k_sumsq_partial(const T* __restrict__ a, int64_t m,
                                                        int64_t n, int64_t lda, double* partial) {
     __shared__ double sh[32];
     const int64_t seg = seg_rows(m, n);
@@ -45,9 +47,9 @@ __global__ void __launch_bounds__(256) k_sumsq_partial(const double* __restrict_
         const int64_t col = sgi / segs_per_col;
         const int64_t r0 = (sgi - col * segs_per_col) * seg;
         const int64_t r1 = r0 + seg < m ? r0 + seg : m;
-        const double* c = a + col * lda;
+        const T* c = a + col * lda;
         for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
-            const double v = __ldg(c + r);
+            const double v = double(__ldg(c + r));
             acc = fma(v, v, acc);
         }
     }
@@ -63,21 +65,22 @@ __global__ void k_sum_partials(const double* partial, int count, double* out) {
     if (threadIdx.x == 0) *out = s;
 }
 
-__global__ void __launch_bounds__(128) k_centering(const double* __restrict__ a, int64_t m, int64_t n,
+template <typename T>
+__global__ void __launch_bounds__(128) k_centering(const T* __restrict__ a, int64_t m, int64_t n,
                                                    int64_t lda, double p, double* __restrict__ z) {
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= m) return;
-    const double* r = a + i;
+    const T* r = a + i;
     double acc = 0.0;
     int64_t c = 0;
     for (; c + 8 <= n; c += 8) {
         double v[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = __ldg(r + (c + u) * lda);
+        for (int u = 0; u < 8; ++u) v[u] = double(__ldg(r + (c + u) * lda));
 #pragma unroll
         for (int u = 0; u < 8; ++u) acc = fma(p, v[u], acc);
     }
-    for (; c < n; ++c) acc = fma(p, __ldg(r + c * lda), acc);
+    for (; c < n; ++c) acc = fma(p, double(__ldg(r + c * lda)), acc);
     z[i] = acc;
 }
 
@@ -93,20 +96,57 @@ __global__ void __launch_bounds__(256) k_colsum(const double* __restrict__ x, in
 
 }  // namespace
 
-void launch_sumsq(const double* a, int64_t m, int64_t n, int64_t lda, double* partial, double* out,
-                  cudaStream_t s, LaunchCounter& lc) {
-    k_sumsq_partial<<<kReducePartials, 256, 0, s>>>(a, m, n, lda, partial);
+template <typename T>
+static void sumsq_impl(const T* a, int64_t m, int64_t n, int64_t lda, double* partial, double* out, cudaStream_t s,
+                       LaunchCounter& lc) {
+    k_sumsq_partial<T><<<kReducePartials, 256, 0, s>>>(a, m, n, lda, partial);
     FQB_LAUNCHED();
     k_sum_partials<<<1, 1024, 0, s>>>(partial, kReducePartials, out);
     FQB_LAUNCHED();
     lc.bump(2);
 }
+void launch_sumsq(const double* a, int64_t m, int64_t n, int64_t lda, double* partial, double* out,
+                  cudaStream_t s, LaunchCounter& lc) {
+    sumsq_impl(a, m, n, lda, partial, out, s, lc);
+}
+void launch_sumsq(const float* a, int64_t m, int64_t n, int64_t lda, double* partial, double* out,
+                  cudaStream_t s, LaunchCounter& lc) {
+    sumsq_impl(a, m, n, lda, partial, out, s, lc);
+}
 
-void launch_centering(const double* a, int64_t m, int64_t n, int64_t lda, double p, double* z,
-                      cudaStream_t s, LaunchCounter& lc) {
-    k_centering<<<unsigned(ceil_div(m, 128)), 128, 0, s>>>(a, m, n, lda, p, z);
+template <typename T>
+static void centering_impl(const T* a, int64_t m, int64_t n, int64_t lda, double p, double* z, cudaStream_t s,
+                           LaunchCounter& lc) {
+    k_centering<T><<<unsigned(ceil_div(m, 128)), 128, 0, s>>>(a, m, n, lda, p, z);
     FQB_LAUNCHED();
     lc.bump();
+}
+void launch_centering(const double* a, int64_t m, int64_t n, int64_t lda, double p, double* z,
+                      cudaStream_t s, LaunchCounter& lc) {
+    centering_impl(a, m, n, lda, p, z, s, lc);
+}
+void launch_centering(const float* a, int64_t m, int64_t n, int64_t lda, double p, double* z,
+                      cudaStream_t s, LaunchCounter& lc) {
+    centering_impl(a, m, n, lda, p, z, s, lc);
+}
+
+// FP32 A -> FP64 copy (FP32 input mode when the A passes run on DMMA)
+__global__ void k_widen(const float* __restrict__ a, int64_t m, int64_t lda, double* __restrict__ out,
+                        int64_t ldo) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t c = blockIdx.y;
+    if (i < m) out[c * ldo + i] = double(a[c * lda + i]);
+}
+void launch_widen(const float* a, int64_t m, int64_t n, int64_t lda, double* out, int64_t ldo, cudaStream_t s,
+                  LaunchCounter& lc) {
+    if (m <= 0 || n <= 0) return;
+    for (int64_t c0 = 0; c0 < n; c0 += 65535) {
+        const int64_t cols = std::min<int64_t>(65535, n - c0);
+        k_widen<<<dim3(unsigned(ceil_div(m, 256)), unsigned(cols)), 256, 0, s>>>(a + c0 * lda, m, lda, out + c0 * ldo,
+                                                                                ldo);
+        FQB_LAUNCHED();
+        lc.bump();
+    }
 }
 
 void launch_colsum(const double* x, int64_t rows, int k, int64_t ld, double* colsum, cudaStream_t s,

@@ -23,10 +23,15 @@ namespace {
 constexpr int kWarpsPerCta = 8;
 constexpr int kUnroll = 8;
 
-// VPL double2 vectors per lane: a warp owns 64*VPL consecutive rows, so every
-// gathered column of A is read as one 512*VPL-byte contiguous run.
-template <bool VEC2, int VPL>
-__global__ void __launch_bounds__(256) k_gather_spmm(const double* __restrict__ a, int64_t m,
+template <typename T> struct Vec2;
+template <> struct Vec2<double> { using type = double2; };
+template <> struct Vec2<float> { using type = float2; };
+
+// VPL 2-vectors per lane: a warp owns 64*VPL consecutive rows, so every gathered
+// column of A is read as one contiguous run.  T = float is the FP32 input mode
+// (values widened exactly, accumulation in FP64 as for double A).
+template <typename T, bool VEC2, int VPL>
+__global__ void __launch_bounds__(256) k_gather_spmm(const T* __restrict__ a, int64_t m,
                                                      int64_t lda, const int* __restrict__ col_ptr,
                                                      const int* __restrict__ row_idx,
                                                      const double* __restrict__ values,
@@ -43,21 +48,22 @@ __global__ void __launch_bounds__(256) k_gather_spmm(const double* __restrict__ 
     for (int v = 0; v < VPL; ++v) acc[v][0] = acc[v][1] = 0.0;
     int idx = beg;
     constexpr int U = kUnroll / VPL > 0 ? kUnroll / VPL : 1;
+    using V2 = typename Vec2<T>::type;
     for (; idx + U <= end; idx += U) {
-        double2 av[U][VPL];
+        V2 av[U][VPL];
         double vv[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const double* col = a + int64_t(row_idx[idx + u]) * lda;
+            const T* col = a + int64_t(row_idx[idx + u]) * lda;
             vv[u] = values[idx + u];
 #pragma unroll
             for (int v = 0; v < VPL; ++v) {
                 const int64_t r = base + 64 * v;
                 if (VEC2 && r + 1 < m) {
-                    av[u][v] = __ldg(reinterpret_cast<const double2*>(col + r));
+                    av[u][v] = __ldg(reinterpret_cast<const V2*>(col + r));
                 } else {
-                    av[u][v].x = r < m ? __ldg(col + r) : 0.0;
-                    av[u][v].y = r + 1 < m ? __ldg(col + r + 1) : 0.0;
+                    av[u][v].x = r < m ? __ldg(col + r) : T(0);
+                    av[u][v].y = r + 1 < m ? __ldg(col + r + 1) : T(0);
                 }
             }
         }
@@ -65,18 +71,18 @@ __global__ void __launch_bounds__(256) k_gather_spmm(const double* __restrict__ 
         for (int u = 0; u < U; ++u)
 #pragma unroll
             for (int v = 0; v < VPL; ++v) {
-                acc[v][0] = fma(vv[u], av[u][v].x, acc[v][0]);
-                acc[v][1] = fma(vv[u], av[u][v].y, acc[v][1]);
+                acc[v][0] = fma(vv[u], double(av[u][v].x), acc[v][0]);
+                acc[v][1] = fma(vv[u], double(av[u][v].y), acc[v][1]);
             }
     }
     for (; idx < end; ++idx) {
-        const double* col = a + int64_t(row_idx[idx]) * lda;
+        const T* col = a + int64_t(row_idx[idx]) * lda;
         const double vv = values[idx];
 #pragma unroll
         for (int v = 0; v < VPL; ++v) {
             const int64_t r = base + 64 * v;
-            if (r < m) acc[v][0] = fma(vv, __ldg(col + r), acc[v][0]);
-            if (r + 1 < m) acc[v][1] = fma(vv, __ldg(col + r + 1), acc[v][1]);
+            if (r < m) acc[v][0] = fma(vv, double(__ldg(col + r)), acc[v][0]);
+            if (r + 1 < m) acc[v][1] = fma(vv, double(__ldg(col + r + 1)), acc[v][1]);
         }
     }
 #pragma unroll
@@ -118,9 +124,10 @@ __global__ void __launch_bounds__(256) k_gather_tmul(const double* __restrict__ 
 
 }  // namespace
 
-void launch_gather_spmm(const double* a, int64_t m, int64_t lda, const int* col_ptr,
-                        const int* row_idx, const double* values, int l, const double* z,
-                        double* c, int64_t ldc, cudaStream_t s, LaunchCounter& lc) {
+template <typename T>
+static void gather_spmm_impl(const T* a, int64_t m, int64_t lda, const int* col_ptr, const int* row_idx,
+                             const double* values, int l, const double* z, double* c, int64_t ldc, cudaStream_t s,
+                             LaunchCounter& lc) {
     if (m <= 0 || l <= 0) return;
     const bool vec2 = (lda % 2 == 0) && (ldc % 2 == 0) && (reinterpret_cast<uintptr_t>(a) % 16 == 0) &&
                       (reinterpret_cast<uintptr_t>(c) % 16 == 0);
@@ -135,14 +142,26 @@ void launch_gather_spmm(const double* a, int64_t m, int64_t lda, const int* col_
     if (vpl != 1 && vpl != 2 && vpl != 4) vpl = 1;
     dim3 grid(unsigned(ceil_div(m, int64_t(64 * vpl) * kWarpsPerCta)), unsigned(l));
     if (vec2) {
-        if (vpl == 4) k_gather_spmm<true, 4><<<grid, 256, 0, s>>>(a, m, lda, col_ptr, row_idx, values, z, c, ldc);
-        else if (vpl == 2) k_gather_spmm<true, 2><<<grid, 256, 0, s>>>(a, m, lda, col_ptr, row_idx, values, z, c, ldc);
-        else k_gather_spmm<true, 1><<<grid, 256, 0, s>>>(a, m, lda, col_ptr, row_idx, values, z, c, ldc);
+        if (vpl == 4) k_gather_spmm<T, true, 4><<<grid, 256, 0, s>>>(a, m, lda, col_ptr, row_idx, values, z, c, ldc);
+        else if (vpl == 2)
+            k_gather_spmm<T, true, 2><<<grid, 256, 0, s>>>(a, m, lda, col_ptr, row_idx, values, z, c, ldc);
+        else k_gather_spmm<T, true, 1><<<grid, 256, 0, s>>>(a, m, lda, col_ptr, row_idx, values, z, c, ldc);
     } else {
-        k_gather_spmm<false, 1><<<grid, 256, 0, s>>>(a, m, lda, col_ptr, row_idx, values, z, c, ldc);
+        k_gather_spmm<T, false, 1><<<grid, 256, 0, s>>>(a, m, lda, col_ptr, row_idx, values, z, c, ldc);
     }
     FQB_LAUNCHED();
     lc.bump();
+}
+
+void launch_gather_spmm(const double* a, int64_t m, int64_t lda, const int* col_ptr, const int* row_idx,
+                        const double* values, int l, const double* z, double* c, int64_t ldc, cudaStream_t s,
+                        LaunchCounter& lc) {
+    gather_spmm_impl(a, m, lda, col_ptr, row_idx, values, l, z, c, ldc, s, lc);
+}
+void launch_gather_spmm(const float* a, int64_t m, int64_t lda, const int* col_ptr, const int* row_idx,
+                        const double* values, int l, const double* z, double* c, int64_t ldc, cudaStream_t s,
+                        LaunchCounter& lc) {
+    gather_spmm_impl(a, m, lda, col_ptr, row_idx, values, l, z, c, ldc, s, lc);
 }
 
 void launch_gather_tmul(const double* wt, int64_t n, int64_t ldw, int k, const int* col_ptr,

@@ -279,21 +279,26 @@ def _is_torch(x) -> bool:
 
 
 def _as_colmajor(a):
-    """-> (pointer, m, n, lda, on_device, keepalive)."""
+    """-> (pointer, m, n, lda, on_device, keepalive, is_f32).
+
+    float64 runs the FP64 engine; float32 selects the FP32 input mode (A kept in
+    FP32 on the device, every product in FP64 -- fqb_qb_*_f32)."""
     if _is_torch(a):
         import torch
-        if a.dtype != torch.float64 or a.dim() != 2:
-            raise InvalidArgument("A must be a 2-D float64 tensor")
+        if a.dtype not in (torch.float64, torch.float32) or a.dim() != 2:
+            raise InvalidArgument("A must be a 2-D float64 or float32 tensor")
         m, n = a.shape
         if not (a.stride(0) == 1 and (a.stride(1) >= max(m, 1) or n == 1)):
             a = a.t().contiguous().t()  # column-major copy
         lda = a.stride(1) if n > 1 else max(m, 1)
-        return a.data_ptr(), m, n, lda, a.is_cuda, a
-    arr = np.asfortranarray(np.asarray(a, dtype=np.float64))
+        return a.data_ptr(), m, n, lda, a.is_cuda, a, a.dtype == torch.float32
+    src = np.asarray(a)
+    dt = np.float32 if src.dtype == np.float32 else np.float64
+    arr = np.asfortranarray(src, dtype=dt)
     if arr.ndim != 2:
         raise InvalidArgument("A must be 2-D")
     m, n = arr.shape
-    return arr.ctypes.data, m, n, max(m, 1), False, arr
+    return arr.ctypes.data, m, n, max(m, 1), False, arr, dt == np.float32
 
 
 class SlicedOperand:
@@ -394,19 +399,19 @@ class Engine:
         return self._run(a, cfg, source, output, rank=rank, svd=svd)
 
     def _run(self, a, cfg, source, output, rank, svd=False):
-        ptr, m, n, lda, on_dev, keep = _as_colmajor(a)
+        ptr, m, n, lda, on_dev, keep, f32 = _as_colmajor(a)
         flags = {"device": N.OUT_DEVICE, "host": N.OUT_HOST, "none": N.OUT_NONE}[output]
         if svd:
             flags |= N.OUT_SVD
         res = N.ResultC()
         ccfg = cfg._c()
         cb, err, hold = self._make_source(source)
+        fp = self._lib.fqb_qb_fixed_precision_f32 if f32 else self._lib.fqb_qb_fixed_precision
+        fr = self._lib.fqb_qb_fixed_rank_f32 if f32 else self._lib.fqb_qb_fixed_rank
         if rank is None:
-            st = self._lib.fqb_qb_fixed_precision(self._h, ptr, m, n, lda, int(on_dev), C.byref(ccfg),
-                                                  cb, None, flags, C.byref(res))
+            st = fp(self._h, ptr, m, n, lda, int(on_dev), C.byref(ccfg), cb, None, flags, C.byref(res))
         else:
-            st = self._lib.fqb_qb_fixed_rank(self._h, ptr, m, n, lda, int(on_dev), int(rank),
-                                             C.byref(ccfg), cb, None, flags, C.byref(res))
+            st = fr(self._h, ptr, m, n, lda, int(on_dev), int(rank), C.byref(ccfg), cb, None, flags, C.byref(res))
         del keep, hold
         if err:
             self._lib.fqb_result_free(C.byref(res))

@@ -120,6 +120,28 @@ static int gpu_checks() {
         ++fails;
     } catch (const rb::ConfigError&) {
     }
+    {   // FP32 input mode: a FloatMatrix gives the FP64 loop on double(A)
+        rb::FloatMatrix af(a.rows, a.cols);
+        rb::DenseMatrix ad(a.rows, a.cols);
+        for (std::size_t e = 0; e < a.data.size(); ++e) {
+            af.data[e] = float(a.data[e]);
+            ad.data[e] = double(af.data[e]);
+        }
+        rb::FarpcaConfig c2;
+        c2.eps = 1e-2;
+        c2.relative = true;
+        c2.block = 16;
+        c2.power = 1;
+        c2.sketch.kind = rb::SketchKind::StdBernoulli;
+        c2.sketch.seed = 3;
+        const rb::QbResult r32 = eng.run_fixed_precision(af, c2);
+        const rb::QbResult r64 = eng.run_fixed_precision(ad, c2);
+        const bool ok = r32.rank == r64.rank && r32.blocks == r64.blocks &&
+                        std::fabs(r32.qb_residual_sq - r64.qb_residual_sq) <= 1e-12 * r64.norm_a_sq;
+        std::printf("fp32 input: rank %d / %d, E %.6e / %.6e %s\n", r32.rank, r64.rank, r32.qb_residual_sq,
+                    r64.qb_residual_sq, ok ? "ok" : "FAIL");
+        fails += !ok;
+    }
     std::printf(fails ? "FAIL\n" : "PASS\n");
     return fails;
 }
