@@ -21,6 +21,7 @@
  *   fqb_sparse_dense_mul    <- rsvd::sparse_dense_mul / centered_product (sketch.cpp:104-140)
  *   fqb_centering_column    <- rsvd::centering_column (driver.hpp:78, driver.cpp:178-183)
  *   fqb_frob_norm_sq        <- rsvd::frob_norm_sq (matrix_core.hpp:59, matrix_core.cpp:46-48)
+ *   fqb_relative_error      <- rsvd::relative_error (experiment.hpp, experiment.cpp:317-342)
  *   fqb_gemm                <- rsvd::kern::Ops::gemm_nn / gemm_tn (kernels.hpp:9-19)
  *   fqb_philox_u32          <- rsvd::Philox::next_u32 (rng.hpp:21-24)
  *
@@ -235,6 +236,14 @@ fqb_status fqb_centering_column(fqb_handle h, const double* a, int64_t m, int64_
 /* ||A||_F^2 into *host_out */
 fqb_status fqb_frob_norm_sq(fqb_handle h, const double* a, int64_t m, int64_t n, int64_t lda,
                             double* host_out);
+/* Exact relative error ||A - U diag(sigma) V'||_F / ||A||_F (experiment.cpp:317-342),
+ * one pass over A in column strips on the device.  U is m x r (ldu), V is n x r (ldv);
+ * sigma (host, r values) may be NULL for a QB pair (U = Q, V = B').  A and the factors
+ * are on the device when the *_on_device flags are set, else copied in.  0 for A = 0,
+ * 1 for r = 0, like the reference. */
+fqb_status fqb_relative_error(fqb_handle h, const double* a, int64_t m, int64_t n, int64_t lda, int a_on_device,
+                              const double* u, int64_t ldu, const double* sigma, const double* v, int64_t ldv,
+                              int r, int factors_on_device, double* host_out);
 /* C (m x n) = alpha * op(A) * B + beta * C, op(A) = A (trans_a = 0, A is m x k)
  * or A' (trans_a = 1, A is k x m); B is k x n.  FP64 on the DMMA tensor pipe. */
 fqb_status fqb_gemm(fqb_handle h, int trans_a, int64_t m, int64_t n, int64_t k, double alpha,

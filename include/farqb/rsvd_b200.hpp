@@ -22,6 +22,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
+#include <cstring>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -362,6 +363,69 @@ inline QbResult truncate_to_tolerance(const QbResult& svd, double eps_rel, doubl
         std::copy(svd.v.col(drop + j), svd.v.col(drop + j) + svd.v.rows, out.v.col(j));
     }
     return out;
+}
+
+// relative_error (experiment.cpp:317-342): exact ||A - U diag(sigma) V'||_F / ||A||_F on the
+// device (one pass over A in column strips); a QB result without the SVD uses Q and B.
+inline double relative_error(const DenseMatrix& a, const QbResult& res, Engine& eng = default_engine()) {
+    const bool svd = !res.sigma.empty();
+    const DenseMatrix& u = svd ? res.u : res.q;
+    const DenseMatrix& v = svd ? res.v : res.bt;
+    const int r = svd ? res.svd_rank() : res.rank;
+    if (r > 0 && (u.rows != a.rows || v.rows != a.cols)) throw DimensionError("relative_error: factor shape mismatch");
+    double out = 0.0;
+    const fqb_status st = fqb_relative_error(eng.handle(), a.data.data(), a.rows, a.cols, std::max(a.rows, 1), 0,
+                                             u.data.data(), std::max(u.rows, 1), svd ? res.sigma.data() : nullptr,
+                                             v.data.data(), std::max(v.rows, 1), r, 0, &out);
+    if (st != FQB_OK) detail::raise(st, "relative_error");
+    return out;
+}
+
+// RawF64 interchange format (matrix_io.cpp:141-200): "SKLR", u32 rows, u32 cols,
+// u32 reserved, then column-major little-endian f64.
+struct FormatError : std::runtime_error {
+    std::size_t offset;
+    FormatError(const std::string& m, std::size_t off) : std::runtime_error(m), offset(off) {}
+};
+
+inline DenseMatrix load_raw(const std::string& buf) {
+    auto u32 = [&](std::size_t at) {
+        const auto* b = reinterpret_cast<const unsigned char*>(buf.data()) + at;
+        return std::uint32_t(b[0]) | (std::uint32_t(b[1]) << 8) | (std::uint32_t(b[2]) << 16) |
+               (std::uint32_t(b[3]) << 24);
+    };
+    if (buf.size() < 16) throw FormatError("truncated header, need 16 bytes", buf.size());
+    if (buf.compare(0, 4, "SKLR") != 0) throw FormatError("bad magic, expected SKLR", 0);
+    const std::uint64_t rows = u32(4), cols = u32(8);
+    if (rows > 0x7FFFFFFFull) throw FormatError("dimension overflow in row count", 4);
+    if (cols > 0x7FFFFFFFull) throw FormatError("dimension overflow in column count", 8);
+    const std::uint64_t need = rows * cols * 8;
+    if (buf.size() - 16 < need) throw FormatError("truncated payload", buf.size());
+    if (buf.size() - 16 > need) throw FormatError("trailing bytes after payload", std::size_t(16 + need));
+    DenseMatrix a(static_cast<int>(rows), static_cast<int>(cols));
+    for (std::size_t k = 0; k < a.data.size(); ++k) {   // little-endian payload, any host byte order
+        std::uint64_t bits = 0;
+        const auto* q = reinterpret_cast<const unsigned char*>(buf.data()) + 16 + 8 * k;
+        for (int i = 7; i >= 0; --i) bits = (bits << 8) | q[i];
+        std::memcpy(&a.data[k], &bits, 8);
+    }
+    return a;
+}
+
+inline void save_raw(const DenseMatrix& a, std::string& out) {
+    auto put = [&](std::uint32_t v) {
+        for (int i = 0; i < 4; ++i) out.push_back(char((v >> (8 * i)) & 0xFF));
+    };
+    out.reserve(out.size() + 16 + 8 * a.data.size());
+    out += "SKLR";
+    put(std::uint32_t(a.rows));
+    put(std::uint32_t(a.cols));
+    put(0);
+    for (double x : a.data) {
+        std::uint64_t bits;
+        std::memcpy(&bits, &x, 8);
+        for (int i = 0; i < 8; ++i) out.push_back(char((bits >> (8 * i)) & 0xFF));
+    }
 }
 
 inline double default_density(SketchKind kind, int n) { return fqb_default_density(static_cast<int>(kind), n); }

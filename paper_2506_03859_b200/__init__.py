@@ -11,8 +11,9 @@ from .rsvd import (  # noqa: F401
     CudaError, DimensionError, Engine, FarpcaConfig, InvalidArgument, QBResult, RsvdError,
     ShiftConvention, SketchBlock, SketchKind, SketchSpec, ToleranceNotReached, default_block,
     default_density, default_engine, default_max_iters, estimate_cost, gen_sketch,
-    run_fixed_precision, run_fixed_rank, sketch_kind_from_name, sketch_kind_name, truncate_to_tolerance)
+    relative_error, run_fixed_precision, run_fixed_rank, sketch_kind_from_name, sketch_kind_name, truncate_to_tolerance)
 
 from . import dist  # noqa: F401,E402  (row-sharded multi-GPU helpers)
+from .matrix_io import FormatError, dumps_raw, load_raw, loads_raw, save_raw  # noqa: F401,E402
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -392,6 +392,21 @@ fqb_status fqb_frob_norm_sq(fqb_handle h, const double* a, int64_t m, int64_t n,
     });
 }
 
+fqb_status fqb_relative_error(fqb_handle h, const double* a, int64_t m, int64_t n, int64_t lda, int a_on_device,
+                              const double* u, int64_t ldu, const double* sigma, const double* v, int64_t ldv,
+                              int r, int factors_on_device, double* host_out) {
+    return guarded([&]() -> fqb_status {
+        bind(h);
+        if (!a || !host_out) throw farqb::Error(FQB_ERR_INVALID_ARGUMENT, "null pointer");
+        if (m < 0 || n < 0 || r < 0) throw farqb::Error(FQB_ERR_DIMENSION, "negative dimension");
+        if (lda < m || (r > 0 && (!u || !v || ldu < m || ldv < n)))
+            throw farqb::Error(FQB_ERR_DIMENSION, "relative_error: factor shape mismatch");
+        *host_out = farqb::relative_error(h->h, a, m, n, lda, a_on_device != 0, u, ldu, sigma, v, ldv, r,
+                                          factors_on_device != 0);
+        return FQB_OK;
+    });
+}
+
 fqb_status fqb_gemm(fqb_handle h, int trans_a, int64_t m, int64_t n, int64_t k, double alpha,
                     const double* a, int64_t lda, const double* b, int64_t ldb, double beta, double* c,
                     int64_t ldc) {

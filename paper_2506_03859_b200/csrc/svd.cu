@@ -85,7 +85,103 @@ __global__ void k_scale_cols(const double* src, int64_t lds, const double* scale
     if (i < rows && c < cols) dst[int64_t(c) * ldd + i] = src[int64_t(c) * lds + i] * scale[c];
 }
 
+// T (r x w, ld r) = (V[s:s+w, :] diag(sigma))'   (sigma null: unscaled)
+__global__ void k_strip_t(const double* v, int64_t ldv, const double* sigma, int r, int64_t s, int w, double* t) {
+    const int k = blockIdx.y;
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < w && k < r) t[int64_t(j) * r + k] = v[int64_t(k) * ldv + s + j] * (sigma ? sigma[k] : 1.0);
+}
+
 }  // namespace
+
+// rsvd::relative_error (experiment.cpp:317-342): strips of w columns of A,
+// D = A_strip - U T with T = (V_strip diag(sigma))', err^2 += ||D||^2 (fixed
+// strip order, each strip a deterministic tree sum), then sqrt(err^2 / ||A||^2).
+double relative_error(Handle& h, const double* a, int64_t m, int64_t n, int64_t lda, bool a_on_device,
+                      const double* u, int64_t ldu, const double* sigma, const double* v, int64_t ldv, int r,
+                      bool factors_on_device) {
+    cudaStream_t s = h.stream;
+    ensure_gemm_workspace(h);
+    if (m == 0 || n == 0) return 0.0;
+    // strips sized to ~256 MB of A
+    const int64_t w = std::max<int64_t>(1, std::min<int64_t>(n, (int64_t(1) << 25) / std::max<int64_t>(m, 1)));
+    const int64_t nstrips = ceil_div(n, w);
+    DeviceArray<double> part, sums, d, t, ud, vd, sd, astrip;
+    part.ensure(kReducePartials, s);
+    sums.ensure(size_t(nstrips + 1), s);
+    d.ensure(size_t(m) * w, s);
+    if (!a_on_device) astrip.ensure(size_t(m) * w, s);
+    const double *U = u, *V = v, *SIG = nullptr;
+    if (r > 0) {
+        if (!factors_on_device) {
+            ud.ensure(size_t(m) * r, s);
+            vd.ensure(size_t(n) * r, s);
+            FQB_CUDA(cudaMemcpy2DAsync(ud.ptr, m * sizeof(double), u, ldu * sizeof(double), m * sizeof(double), r,
+                                       cudaMemcpyHostToDevice, s));
+            FQB_CUDA(cudaMemcpy2DAsync(vd.ptr, n * sizeof(double), v, ldv * sizeof(double), n * sizeof(double), r,
+                                       cudaMemcpyHostToDevice, s));
+            U = ud.ptr;
+            V = vd.ptr;
+            ldu = m;
+            ldv = n;
+        }
+        if (sigma) {
+            sd.ensure(size_t(r), s);
+            FQB_CUDA(cudaMemcpyAsync(sd.ptr, sigma, sizeof(double) * r, cudaMemcpyHostToDevice, s));
+            SIG = sd.ptr;
+        }
+        t.ensure(size_t(r) * w, s);
+    }
+    for (int64_t k = 0; k < nstrips; ++k) {
+        const int64_t c0 = k * w, wc = std::min(w, n - c0);
+        const double* ak = a + c0 * lda;
+        int64_t ldak = lda;
+        if (!a_on_device) {   // stream the host strip in
+            FQB_CUDA(cudaMemcpy2DAsync(astrip.ptr, m * sizeof(double), ak, lda * sizeof(double), m * sizeof(double), wc,
+                                       cudaMemcpyHostToDevice, s));
+            ak = astrip.ptr;
+            ldak = m;
+        }
+        // ||A||^2 strip by strip (slot nstrips accumulates on the host below)
+        FQB_CUDA(cudaMemcpy2DAsync(d.ptr, m * sizeof(double), ak, ldak * sizeof(double), m * sizeof(double), wc,
+                                   cudaMemcpyDeviceToDevice, s));
+        if (r > 0) {
+            dim3 g(unsigned(ceil_div(wc, 256)), unsigned(r));
+            k_strip_t<<<g, 256, 0, s>>>(V, ldv, SIG, r, c0, int(wc), t.ptr);
+            FQB_LAUNCHED();
+            h.lc.bump();
+            gemm(false, m, wc, r, -1.0, U, ldu, t.ptr, r, 1.0, d.ptr, m, h.gws, h.num_sms, s, h.lc);
+        }
+        launch_sumsq(d.ptr, m, wc, m, part.ptr, sums.ptr + k, s, h.lc);
+    }
+    std::vector<double> hs(static_cast<size_t>(nstrips));
+    FQB_CUDA(cudaMemcpyAsync(hs.data(), sums.ptr, sizeof(double) * nstrips, cudaMemcpyDeviceToHost, s));
+    // ||A||^2 with the same strip order
+    double norm_sq = 0.0;
+    {
+        std::vector<double> hn(static_cast<size_t>(nstrips));
+        for (int64_t k = 0; k < nstrips; ++k) {
+            const int64_t c0 = k * w, wc = std::min(w, n - c0);
+            const double* ak = a + c0 * lda;
+            int64_t ldak = lda;
+            if (!a_on_device) {
+                FQB_CUDA(cudaMemcpy2DAsync(astrip.ptr, m * sizeof(double), ak, lda * sizeof(double),
+                                           m * sizeof(double), wc, cudaMemcpyHostToDevice, s));
+                ak = astrip.ptr;
+                ldak = m;
+            }
+            launch_sumsq(ak, m, wc, ldak, part.ptr, sums.ptr + nstrips, s, h.lc);
+            FQB_CUDA(cudaMemcpyAsync(&hn[size_t(k)], sums.ptr + nstrips, sizeof(double), cudaMemcpyDeviceToHost, s));
+        }
+        FQB_CUDA(cudaStreamSynchronize(s));
+        for (double x : hn) norm_sq += x;
+    }
+    if (norm_sq == 0.0) return 0.0;
+    if (r == 0) return 1.0;
+    double err_sq = 0.0;
+    for (double x : hs) err_sq += x;
+    return std::sqrt(err_sq / norm_sq);
+}
 
 void assemble_svd(Handle& h, const double* q, int64_t ldq, const double* bt, int64_t ldbt, int64_t m, int64_t n,
                   int l, double* u, int64_t ldu, double* v, int64_t ldv, std::vector<double>& sigma,

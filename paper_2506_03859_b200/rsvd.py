@@ -555,6 +555,42 @@ class Engine:
         if st:
             _raise(st, "fqb_gemm_emulated")
 
+    def relative_error(self, a, res: "QBResult") -> float:
+        """rsvd::relative_error (experiment.cpp:317-342): ||A - U diag(sigma) V'||_F / ||A||_F on the
+        device, one pass over A.  Uses the ApproxSvd factors when res has them, else Q and B."""
+        ptr, m, n, lda, on_dev, keep, f32 = _as_colmajor(a)
+        if f32:
+            raise InvalidArgument("relative_error takes a float64 A")
+        if res.sigma is not None and res.u is not None:
+            fu, fv, sig = res.u, res.v, np.ascontiguousarray(res.sigma, dtype=np.float64)
+        else:
+            fu, fv, sig = res.q, res.bt, None
+        r = 0 if fu is None else int(fu.shape[1])
+        keep_f = []
+
+        def fptr(x, rows):
+            if x is None:
+                return None, rows, False
+            if _is_torch(x):
+                xc = x if x.stride(0) == 1 else x.t().contiguous().t()
+                keep_f.append(xc)
+                return xc.data_ptr(), (xc.stride(1) if xc.shape[1] > 1 else rows), xc.is_cuda
+            xa = np.asfortranarray(x, dtype=np.float64)
+            keep_f.append(xa)
+            return xa.ctypes.data, rows, False
+        up, ldu, udev = fptr(fu, m)
+        vp, ldv, vdev = fptr(fv, n)
+        if r > 0 and udev != vdev:
+            raise InvalidArgument("U and V must both be on the host or both on the device")
+        out = C.c_double()
+        st = self._lib.fqb_relative_error(self._h, ptr, m, n, lda, int(on_dev), up, max(ldu, 1),
+                                          None if sig is None else sig.ctypes.data, vp, max(ldv, 1), r,
+                                          int(bool(udev)), C.byref(out))
+        del keep, keep_f
+        if st:
+            _raise(st, "fqb_relative_error")
+        return out.value
+
     def slice_operand(self, a_ptr, m, n, lda) -> "SlicedOperand":
         """Cut A (m x n, device, column-major) once into Ozaki slices (fqb_slice_operand)."""
         out = C.c_void_p()
@@ -653,3 +689,8 @@ def estimate_cost(m: float, n: float, l: float, power: int, block: int, p: float
 def gen_sketch(spec: SketchSpec, n: int, l: int, block_id: int, device: int = 0) -> SketchBlock:
     """rsvd::gen_sketch (sketch.hpp:46), generated on the device."""
     return default_engine(device).gen_sketch(spec, n, l, block_id)
+
+
+def relative_error(a, res: QBResult, device: int = 0) -> float:
+    """rsvd::relative_error: exact ||A - U diag(sigma) V'||_F / ||A||_F (or ||A - Q B|| for a QB result)."""
+    return default_engine(device).relative_error(a, res)

@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstring>
 #include <random>
+#include <string>
 
 #include "farqb/rsvd_b200.hpp"
 
@@ -44,6 +45,20 @@ static int cpu_checks() {
     fails += rb::default_block(20000, 20000) != 50;
     fails += rb::default_max_iters(401, 20) != 11;
     fails += std::fabs(rb::default_density(rb::SketchKind::SparseSign, 1000) - 0.01) > 1e-15;
+    {   // RawF64 round trip and a malformed file (matrix_io.cpp:141-200)
+        rb::DenseMatrix a(3, 2);
+        for (int k = 0; k < 6; ++k) a.data[k] = 0.5 * k - 1.0;
+        std::string buf;
+        rb::save_raw(a, buf);
+        const rb::DenseMatrix b = rb::load_raw(buf);
+        fails += buf.size() != 16 + 48 || b.rows != 3 || b.cols != 2 || b.data != a.data;
+        try {
+            rb::load_raw(buf + "x");
+            ++fails;
+        } catch (const rb::FormatError& e) {
+            fails += e.offset != 64;
+        }
+    }
     try {
         rb::Engine e(0);
         std::printf("unexpected: a device is present\n");
@@ -141,6 +156,12 @@ static int gpu_checks() {
         std::printf("fp32 input: rank %d / %d, E %.6e / %.6e %s\n", r32.rank, r64.rank, r32.qb_residual_sq,
                     r64.qb_residual_sq, ok ? "ok" : "FAIL");
         fails += !ok;
+        // exact error of the SVD (experiment.cpp:317-342) vs the indicator
+        const double rel = rb::relative_error(ad, r64, eng);
+        const bool ok2 = std::fabs(rel * rel * r64.norm_a_sq - r64.residual_sq) <= 1e-10 * r64.norm_a_sq;
+        std::printf("relative_error %.6e vs sqrt(E/|A|^2) %.6e %s\n", rel, std::sqrt(r64.residual_sq / r64.norm_a_sq),
+                    ok2 ? "ok" : "FAIL");
+        fails += !ok2;
     }
     std::printf(fails ? "FAIL\n" : "PASS\n");
     return fails;

@@ -378,3 +378,19 @@ def test_truncate_to_tolerance_and_estimate_cost(golden_mats):
     assert d == 2 * 1e6 * 100 + common
     assert acc == 1e6 * 100 + 1e6 * 100 * 0.01 + 1000 * np.sqrt(1000 * 100) + common
     assert fqb.estimate_cost(1000, 1000, 100, 2, 20, 0.01, SketchKind.Gaussian)[2] == 1.0
+
+
+def test_relative_error_matches_numpy_and_the_indicator(eng):
+    """fqb_relative_error (experiment.cpp:317-342) for SVD and QB results, host and device."""
+    a = _lowrank(1500, 1100, 0.93 ** np.arange(300), seed=31)
+    cfg = FarpcaConfig(eps=1e-3, power=1, block=30, sketch=SketchSpec(2, 0.5, 3), relative=True)
+    r_svd = eng.run_fixed_precision(a, cfg, output="host", svd=True)
+    want = np.linalg.norm(a - (r_svd.u * r_svd.sigma) @ r_svd.v.T) / np.linalg.norm(a)
+    got = eng.relative_error(a, r_svd)
+    assert abs(got - want) <= 1e-12
+    assert abs(got ** 2 * r_svd.norm_a_sq - r_svd.residual_sq) <= 1e-10 * r_svd.norm_a_sq
+    r_dev = eng.run_fixed_precision(torch.from_numpy(a).cuda(), cfg, output="device")
+    got_dev = eng.relative_error(torch.from_numpy(a).cuda(), r_dev)
+    assert abs(got_dev - np.sqrt(r_dev.residual_sq / r_dev.norm_a_sq)) <= 1e-10
+    r0 = eng.run_fixed_precision(np.zeros((40, 30)), cfg, output="host")
+    assert eng.relative_error(np.zeros((40, 30)), r0) == 0.0
