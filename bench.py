@@ -276,11 +276,15 @@ def run_ours(args):
     step_ms = []
     with torch.cuda.stream(stream):
         e0.record()
+    last = None
     for _ in range(args.steps):
-        # like rsvd::run_fixed_precision: QB loop + assemble_svd (U, sigma, V), all on the device
+        # like rsvd::run_fixed_precision: QB loop + assemble_svd (U, sigma, V), all on the device.
+        # The previous step's factors are released first (as a caller that consumed them
+        # would), so every step allocates its outputs from the warm pool.
+        last = None
         r = eng.run_fixed_precision(a, cfg, output="device", svd=True)
         step_ms.append(r.elapsed_ms)
-        last = r
+        last, r = r, None
     with torch.cuda.stream(stream):
         e1.record()
     e1.synchronize()

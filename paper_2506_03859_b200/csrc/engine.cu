@@ -47,6 +47,14 @@ enum ScalarSlot { kNormA = 0, kBNorm = 1, kDMax = 2, kAlpha = 3, kScalarCount = 
 
 }  // namespace
 
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("FQB_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 void ensure_gemm_workspace(Handle& h) {
     const int64_t need = std::max<int64_t>(int64_t(h.num_sms) * 256 * 128 + 16, gemm_tma_workspace_doubles(h.num_sms));
     if (h.ws.splitk.count < size_t(need)) {

@@ -140,6 +140,7 @@ __device__ __forceinline__ void load_stage(const GemmArgs& p, double* As, double
 
 template <bool TRANS_A, int NT, int WM, int VEC>
 __global__ void __launch_bounds__(THREADS, 1) k_gemm(const GemmArgs p) {
+    FQB_PDL_ENTRY();
     using C = Cfg<TRANS_A, NT, WM, VEC>;
     extern __shared__ __align__(16) double smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -239,6 +240,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_gemm(const GemmArgs p) {
 __global__ void __launch_bounds__(256) k_splitk_reduce(const double* __restrict__ work, int splits, int64_t M,
                                                        int64_t N, double alpha, double beta, double* C,
                                                        int64_t ldc) {
+    FQB_PDL_ENTRY();
     const int q = threadIdx.x & 7;
     const int64_t idx = int64_t(blockIdx.x) * 32 + (threadIdx.x >> 3);
     const int64_t total = M * N;
@@ -256,6 +258,7 @@ __global__ void __launch_bounds__(256) k_splitk_reduce(const double* __restrict_
 }
 
 __global__ void k_scale(double* C, int64_t M, int64_t N, int64_t ldc, double beta) {
+    FQB_PDL_ENTRY();
     const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (idx >= M * N) return;
     const int64_t col = idx / M, row = idx - col * M;
@@ -365,7 +368,7 @@ void gemm(bool trans_a, int64_t M, int64_t N, int64_t K, double alpha, const dou
           int num_sms, cudaStream_t s, LaunchCounter& lc) {
     if (M <= 0 || N <= 0) return;
     if (K <= 0 || alpha == 0.0) {
-        k_scale<<<unsigned(ceil_div(M * N, 256)), 256, 0, s>>>(C, M, N, ldc, beta);
+        launch_k(k_scale, unsigned(ceil_div(M * N, 256)), 256, 0, s, C, M, N, ldc, beta);
         FQB_LAUNCHED();
         lc.bump();
         return;
@@ -397,11 +400,11 @@ void gemm(bool trans_a, int64_t M, int64_t N, int64_t K, double alpha, const dou
     }
     GemmArgs a{M, N, K, alpha, beta, A, lda, B, ldb, C, ldc, work, pl.kchunk, pl.splits, nullptr};
     dim3 grid(unsigned(pl.mt), unsigned(pl.nt_tiles), unsigned(pl.splits));
-    pl.fn<<<grid, THREADS, pl.smem, s>>>(a);
+    launch_k(pl.fn, grid, THREADS, pl.smem, s, a);
     FQB_LAUNCHED();
     lc.bump();
     if (pl.splits > 1) {
-        k_splitk_reduce<<<unsigned(ceil_div(M * N, 32)), 256, 0, s>>>(work, pl.splits, M, N, alpha, beta, C, ldc);
+        launch_k(k_splitk_reduce, unsigned(ceil_div(M * N, 32)), 256, 0, s, work, pl.splits, M, N, alpha, beta, C, ldc);
         FQB_LAUNCHED();
         lc.bump();
     }

@@ -156,6 +156,7 @@ template <bool TRANS_A, int NT, int WM>
 __global__ void __launch_bounds__(TMA_THREADS, 1)
     k_gemm_tma(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                const TmaArgs p) {
+    FQB_PDL_ENTRY();
     using Cf = TCfg<TRANS_A, NT, WM>;
     extern __shared__ uint8_t smem_raw[];
     const unsigned raw = smem_u32(smem_raw);
@@ -400,7 +401,7 @@ void launch_nt(const double* A, int64_t lda, const double* B, int64_t ldb, TmaAr
     a.ktiles = int(ceil_div(a.K, BK));
     a.iters = int64_t(a.mtiles) * ntiles * a.ktiles;
     a.grid = int(std::max<int64_t>(1, std::min<int64_t>(num_sms, a.iters / 8)));
-    k_gemm_tma<TRANS_A, NT, WM><<<a.grid, TMA_THREADS, Cf::SMEM, s>>>(ma, mb, a);
+    launch_k(k_gemm_tma<TRANS_A, NT, WM>, a.grid, TMA_THREADS, Cf::SMEM, s, ma, mb, a);
     FQB_LAUNCHED();
 }
 

@@ -180,6 +180,7 @@ struct Walk {
 };
 
 __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
+    FQB_PDL_ENTRY();
     extern __shared__ uint8_t smem_raw[];
     __shared__ uint64_t bars[2 * A_STAGES + 2 * B_STAGES + 2];
     __shared__ unsigned tmem_base_s;
@@ -435,6 +436,7 @@ __device__ __forceinline__ void put_chunk16(const double (&v)[16], int e, int8_t
 template <typename T>   // double, or float A (FP32 input mode: widened exactly)
 __global__ void __launch_bounds__(256) k_line_max(const T* __restrict__ a, int64_t m, int64_t n, int64_t ld,
                                                   unsigned* rmax, unsigned* cmax) {
+    FQB_PDL_ENTRY();
     __shared__ unsigned cm[8][128];
     const int64_t i = int64_t(blockIdx.x) * 256 + threadIdx.x;
     const int64_t j0 = int64_t(blockIdx.y) * 128;
@@ -468,6 +470,7 @@ template <typename T>
 __global__ void __launch_bounds__(256) k_slice_a(const T* __restrict__ a, int64_t m, int64_t n, int64_t ld,
                                                  const unsigned* __restrict__ rmax, const unsigned* __restrict__ cmax,
                                                  int8_t* x_tn, int* e_tn, int8_t* x_nn, int* e_nn) {
+    FQB_PDL_ENTRY();
     __shared__ double t[64][65];   // t[j][i]
     const int64_t i0 = int64_t(blockIdx.x) * 64, j0 = int64_t(blockIdx.y) * 64;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -512,6 +515,7 @@ __global__ void __launch_bounds__(256) k_slice_a(const T* __restrict__ a, int64_
 constexpr int ZT = 256;
 __global__ void __launch_bounds__(ZT) k_slice_z(const double* __restrict__ b, int64_t k, int64_t n, int64_t ld,
                                                 int* ez, int8_t* out) {
+    FQB_PDL_ENTRY();
     __shared__ unsigned wmax[ZT / 32];
     const int j = blockIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -548,6 +552,7 @@ __global__ void __launch_bounds__(ZT) k_slice_z(const double* __restrict__ b, in
 // one thread per tile row; up to 4 pieces x 8 columns of loads in flight.
 constexpr int FIX_COLS = 8;
 __global__ void __launch_bounds__(OZ_BM) k_ozaki_fixup(const OzArgs p) {
+    FQB_PDL_ENTRY();
     const int64_t t = blockIdx.x;
     const int j0 = blockIdx.y * FIX_COLS, r = threadIdx.x;
     const int c0 = cta_of(p, t * p.kblocks), c1 = cta_of(p, t * p.kblocks + p.kblocks - 1);
@@ -602,11 +607,11 @@ static void slice_a_impl(const T* a, int64_t m, int64_t n, int64_t ld, unsigned*
     unsigned* rmax = line_max;
     unsigned* cmax = line_max + m;
     FQB_CUDA(cudaMemsetAsync(line_max, 0, sizeof(unsigned) * size_t(m + n), s));
-    k_line_max<T><<<dim3(unsigned(ceil_div(m, 256)), unsigned(ceil_div(n, 128))), 256, 0, s>>>(a, m, n, ld, rmax, cmax);
+    launch_k(k_line_max<T>, dim3(unsigned(ceil_div(m, 256)), unsigned(ceil_div(n, 128))), 256, 0, s, a, m, n, ld, rmax, cmax);
     FQB_LAUNCHED();
     // cover the padded operand rows of both layouts (multiples of OZ_BM)
     const dim3 g(unsigned(ceil_div(m, OZ_BM) * (OZ_BM / 64)), unsigned(ceil_div(n, OZ_BM) * (OZ_BM / 64)));
-    k_slice_a<T><<<g, 256, 0, s>>>(a, m, n, ld, rmax, cmax, x_tn, e_tn, x_nn, e_nn);
+    launch_k(k_slice_a<T>, g, 256, 0, s, a, m, n, ld, rmax, cmax, x_tn, e_tn, x_nn, e_nn);
     FQB_LAUNCHED();
     lc.bump(2);
 }
@@ -624,7 +629,7 @@ void ozaki_slice_z(const double* b, int64_t k, int64_t n, int64_t ld, int* e, in
                    LaunchCounter& lc) {
     if (n <= 0 || k <= 0) return;
     const int64_t chunks = ceil_div(k, OZ_BK) * (OZ_BK / 16);
-    k_slice_z<<<dim3(OZ_BN, unsigned(ceil_div(chunks, ZT))), ZT, 0, s>>>(b, k, n, ld, e, out);
+    launch_k(k_slice_z, dim3(OZ_BN, unsigned(ceil_div(chunks, ZT))), ZT, 0, s, b, k, n, ld, e, out);
     FQB_LAUNCHED();
     lc.bump();
 }
@@ -662,13 +667,13 @@ void ozaki_gemm(int64_t M, int64_t N, int64_t K, double alpha, const int8_t* xs,
     a.inv_grid = 1.0 / double(a.grid);
     a.inv_kblocks = 1.0 / double(a.kblocks);
     a.inv_iters = 1.0 / double(a.iters);
-    k_ozaki<<<a.grid, OZ_THREADS, OZ_SMEM, s>>>(a);
+    launch_k(k_ozaki, a.grid, OZ_THREADS, OZ_SMEM, s, a);
     FQB_LAUNCHED();
     lc.bump();
     bool split = false;   // does any CTA boundary fall inside a tile?
     for (int c = 1; c < a.grid && !split; ++c) split = (a.iters * c / a.grid) % a.kblocks != 0;
     if (split) {
-        k_ozaki_fixup<<<dim3(unsigned(a.mtiles), unsigned(ceil_div(N, FIX_COLS))), OZ_BM, 0, s>>>(a);
+        launch_k(k_ozaki_fixup, dim3(unsigned(a.mtiles), unsigned(ceil_div(N, FIX_COLS))), OZ_BM, 0, s, a);
         FQB_LAUNCHED();
         lc.bump();
     }

@@ -38,6 +38,7 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
 template <typename T>   // double, or float A (FP32 input mode; squares summed in FP64)
 __global__ void __launch_bounds__(256) k_sumsq_partial(const T* __restrict__ a, int64_t m,
                                                        int64_t n, int64_t lda, double* partial) {
+    FQB_PDL_ENTRY();
     __shared__ double sh[32];
     const int64_t seg = seg_rows(m, n);
     const int64_t segs_per_col = (m + seg - 1) / seg;
@@ -58,6 +59,7 @@ __global__ void __launch_bounds__(256) k_sumsq_partial(const T* __restrict__ a, 
 }
 
 __global__ void k_sum_partials(const double* partial, int count, double* out) {
+    FQB_PDL_ENTRY();
     __shared__ double sh[32];
     double acc = 0.0;
     for (int i = threadIdx.x; i < count; i += blockDim.x) acc += partial[i];
@@ -68,6 +70,7 @@ __global__ void k_sum_partials(const double* partial, int count, double* out) {
 template <typename T>
 __global__ void __launch_bounds__(128) k_centering(const T* __restrict__ a, int64_t m, int64_t n,
                                                    int64_t lda, double p, double* __restrict__ z) {
+    FQB_PDL_ENTRY();
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= m) return;
     const T* r = a + i;
@@ -86,6 +89,7 @@ __global__ void __launch_bounds__(128) k_centering(const T* __restrict__ a, int6
 
 __global__ void __launch_bounds__(256) k_colsum(const double* __restrict__ x, int64_t rows,
                                                 int64_t ld, double* colsum) {
+    FQB_PDL_ENTRY();
     __shared__ double sh[32];
     const double* c = x + int64_t(blockIdx.x) * ld;
     double acc = 0.0;
@@ -99,9 +103,9 @@ __global__ void __launch_bounds__(256) k_colsum(const double* __restrict__ x, in
 template <typename T>
 static void sumsq_impl(const T* a, int64_t m, int64_t n, int64_t lda, double* partial, double* out, cudaStream_t s,
                        LaunchCounter& lc) {
-    k_sumsq_partial<T><<<kReducePartials, 256, 0, s>>>(a, m, n, lda, partial);
+    launch_k(k_sumsq_partial<T>, kReducePartials, 256, 0, s, a, m, n, lda, partial);
     FQB_LAUNCHED();
-    k_sum_partials<<<1, 1024, 0, s>>>(partial, kReducePartials, out);
+    launch_k(k_sum_partials, 1, 1024, 0, s, partial, kReducePartials, out);
     FQB_LAUNCHED();
     lc.bump(2);
 }
@@ -117,7 +121,7 @@ void launch_sumsq(const float* a, int64_t m, int64_t n, int64_t lda, double* par
 template <typename T>
 static void centering_impl(const T* a, int64_t m, int64_t n, int64_t lda, double p, double* z, cudaStream_t s,
                            LaunchCounter& lc) {
-    k_centering<T><<<unsigned(ceil_div(m, 128)), 128, 0, s>>>(a, m, n, lda, p, z);
+    launch_k(k_centering<T>, unsigned(ceil_div(m, 128)), 128, 0, s, a, m, n, lda, p, z);
     FQB_LAUNCHED();
     lc.bump();
 }
@@ -133,6 +137,7 @@ void launch_centering(const float* a, int64_t m, int64_t n, int64_t lda, double 
 // FP32 A -> FP64 copy (FP32 input mode when the A passes run on DMMA)
 __global__ void k_widen(const float* __restrict__ a, int64_t m, int64_t lda, double* __restrict__ out,
                         int64_t ldo) {
+    FQB_PDL_ENTRY();
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     const int64_t c = blockIdx.y;
     if (i < m) out[c * ldo + i] = double(a[c * lda + i]);
@@ -142,7 +147,7 @@ void launch_widen(const float* a, int64_t m, int64_t n, int64_t lda, double* out
     if (m <= 0 || n <= 0) return;
     for (int64_t c0 = 0; c0 < n; c0 += 65535) {
         const int64_t cols = std::min<int64_t>(65535, n - c0);
-        k_widen<<<dim3(unsigned(ceil_div(m, 256)), unsigned(cols)), 256, 0, s>>>(a + c0 * lda, m, lda, out + c0 * ldo,
+        launch_k(k_widen, dim3(unsigned(ceil_div(m, 256)), unsigned(cols)), 256, 0, s, a + c0 * lda, m, lda, out + c0 * ldo,
                                                                                 ldo);
         FQB_LAUNCHED();
         lc.bump();
@@ -152,7 +157,7 @@ void launch_widen(const float* a, int64_t m, int64_t n, int64_t lda, double* out
 void launch_colsum(const double* x, int64_t rows, int k, int64_t ld, double* colsum, cudaStream_t s,
                    LaunchCounter& lc) {
     if (k <= 0) return;
-    k_colsum<<<unsigned(k), 256, 0, s>>>(x, rows, ld, colsum);
+    launch_k(k_colsum, unsigned(k), 256, 0, s, x, rows, ld, colsum);
     FQB_LAUNCHED();
     lc.bump();
 }

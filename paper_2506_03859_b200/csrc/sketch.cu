@@ -78,6 +78,7 @@ __global__ void __launch_bounds__(256) k_iid_walk(int kind, PhiloxKey key, uint3
                                                   int* counts, const int* col_ptr, int* row_idx,
                                                   double* values, double* dense, int64_t ld,
                                                   unsigned* status) {
+    FQB_PDL_ENTRY();
     const int lane = threadIdx.x & 31;
     const int col = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (col >= l) return;
@@ -125,6 +126,7 @@ __global__ void __launch_bounds__(1024) k_iid_walk_cta(int kind, PhiloxKey key, 
                                                        double denom, double scale, double shift, int* counts,
                                                        const int* col_ptr, int* row_idx, double* values,
                                                        double* dense, int64_t ld, unsigned* status) {
+    FQB_PDL_ENTRY();
     __shared__ long long warp_tot[32];
     __shared__ int first_bad_s;
     __shared__ long long row_s;
@@ -178,6 +180,7 @@ __global__ void __launch_bounds__(1024) k_iid_walk_cta(int kind, PhiloxKey key, 
 }
 
 __global__ void k_philox_u32(PhiloxKey key, uint32_t blk, uint32_t col, int count, uint32_t* out) {
+    FQB_PDL_ENTRY();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < count) out[i] = philox_word(key, blk, col, uint64_t(i));
 }
@@ -185,6 +188,7 @@ __global__ void k_philox_u32(PhiloxKey key, uint32_t blk, uint32_t col, int coun
 // one thread per (pair, column): gaussians 2k and 2k+1 of the column
 __global__ void k_gaussian_dense(PhiloxKey key, uint32_t blk, int64_t n, int l, double* out,
                                  int64_t ld, unsigned* status) {
+    FQB_PDL_ENTRY();
     const int64_t pairs = (n + 1) >> 1;
     const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     const int col = blockIdx.y;
@@ -205,6 +209,7 @@ constexpr int kMaxZeta = 256;
 __global__ void k_zeta_fill(int kind, PhiloxKey key, uint32_t blk, int64_t n, int l, int zeta,
                             double scale, int* col_ptr, int* row_idx, double* values,
                             unsigned* status) {
+    FQB_PDL_ENTRY();
     const int col = blockIdx.x * blockDim.x + threadIdx.x;
     if (col > l) return;
     col_ptr[col] = col * zeta;
@@ -250,6 +255,7 @@ __global__ void k_zeta_fill(int kind, PhiloxKey key, uint32_t blk, int64_t n, in
 
 // single-CTA exclusive scan (l is at most a few thousand)
 __global__ void k_exclusive_scan(const int* counts, int l, int* col_ptr) {
+    FQB_PDL_ENTRY();
     __shared__ int carry;
     __shared__ int warp_sums[32];
     if (threadIdx.x == 0) carry = 0;
@@ -286,6 +292,7 @@ __global__ void k_exclusive_scan(const int* counts, int l, int* col_ptr) {
 }
 
 __global__ void k_fill_const(double* out, int64_t rows, int cols, int64_t ld, double v) {
+    FQB_PDL_ENTRY();
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     const int c = blockIdx.y;
     if (i < rows && c < cols) out[int64_t(c) * ld + i] = v;
@@ -293,6 +300,7 @@ __global__ void k_fill_const(double* out, int64_t rows, int cols, int64_t ld, do
 
 __global__ void k_scatter(const int* col_ptr, const int* row_idx, const double* values, int l,
                           double shift, double* out, int64_t ld) {
+    FQB_PDL_ENTRY();
     const int c = blockIdx.x;
     for (int idx = col_ptr[c] + threadIdx.x; idx < col_ptr[c + 1]; idx += blockDim.x)
         out[int64_t(c) * ld + row_idx[idx]] = values[idx] - shift;
@@ -303,7 +311,7 @@ __global__ void k_scatter(const int* col_ptr, const int* row_idx, const double* 
 void launch_philox_u32(uint64_t seed, uint32_t block_id, uint32_t column, int count, uint32_t* out,
                        cudaStream_t s, LaunchCounter& lc) {
     if (count <= 0) return;
-    k_philox_u32<<<unsigned(ceil_div(count, 256)), 256, 0, s>>>(philox_key(seed), block_id, column,
+    launch_k(k_philox_u32, unsigned(ceil_div(count, 256)), 256, 0, s, philox_key(seed), block_id, column,
                                                                 count, out);
     FQB_LAUNCHED();
     lc.bump();
@@ -313,7 +321,7 @@ void launch_gaussian_dense(uint64_t seed, int block_id, int64_t n, int l, double
                            unsigned* status, cudaStream_t s, LaunchCounter& lc) {
     const int64_t pairs = (n + 1) / 2;
     dim3 grid(unsigned(ceil_div(pairs, 256)), unsigned(l));
-    k_gaussian_dense<<<grid, 256, 0, s>>>(philox_key(seed), uint32_t(block_id), n, l, out, ld, status);
+    launch_k(k_gaussian_dense, grid, 256, 0, s, philox_key(seed), uint32_t(block_id), n, l, out, ld, status);
     FQB_LAUNCHED();
     lc.bump();
 }
@@ -324,14 +332,14 @@ static bool dense_columns(int64_t n, double denom) { return double(n) * -std::ex
 void launch_iid_count(int kind, uint64_t seed, int block_id, int64_t n, int l, double denom,
                       int* counts, cudaStream_t s, LaunchCounter& lc) {
     if (dense_columns(n, denom)) {
-        k_iid_walk_cta<kCount><<<unsigned(l), 1024, 0, s>>>(kind, philox_key(seed), uint32_t(block_id), n, denom,
+        launch_k(k_iid_walk_cta<kCount>, unsigned(l), 1024, 0, s, kind, philox_key(seed), uint32_t(block_id), n, denom,
                                                           0.0, 0.0, counts, nullptr, nullptr, nullptr, nullptr, 0,
                                                           nullptr);
         FQB_LAUNCHED();
         lc.bump();
         return;
     }
-    k_iid_walk<kCount><<<unsigned(ceil_div(l, 8)), 256, 0, s>>>(
+    launch_k(k_iid_walk<kCount>, unsigned(ceil_div(l, 8)), 256, 0, s, 
         kind, philox_key(seed), uint32_t(block_id), n, l, denom, 0.0, 0.0, counts, nullptr, nullptr,
         nullptr, nullptr, 0, nullptr);
     FQB_LAUNCHED();
@@ -342,14 +350,14 @@ void launch_iid_fill_csc(int kind, uint64_t seed, int block_id, int64_t n, int l
                          double scale, const int* col_ptr, int* row_idx, double* values,
                          unsigned* status, cudaStream_t s, LaunchCounter& lc) {
     if (dense_columns(n, denom)) {
-        k_iid_walk_cta<kFillCsc><<<unsigned(l), 1024, 0, s>>>(kind, philox_key(seed), uint32_t(block_id), n, denom,
+        launch_k(k_iid_walk_cta<kFillCsc>, unsigned(l), 1024, 0, s, kind, philox_key(seed), uint32_t(block_id), n, denom,
                                                             scale, 0.0, nullptr, col_ptr, row_idx, values, nullptr,
                                                             0, status);
         FQB_LAUNCHED();
         lc.bump();
         return;
     }
-    k_iid_walk<kFillCsc><<<unsigned(ceil_div(l, 8)), 256, 0, s>>>(
+    launch_k(k_iid_walk<kFillCsc>, unsigned(ceil_div(l, 8)), 256, 0, s, 
         kind, philox_key(seed), uint32_t(block_id), n, l, denom, scale, 0.0, nullptr, col_ptr,
         row_idx, values, nullptr, 0, status);
     FQB_LAUNCHED();
@@ -360,17 +368,17 @@ void launch_iid_fill_dense(int kind, uint64_t seed, int block_id, int64_t n, int
                            double scale, double shift, double* out, int64_t ld, unsigned* status,
                            cudaStream_t s, LaunchCounter& lc) {
     dim3 g0(unsigned(ceil_div(n, 256)), unsigned(l));
-    k_fill_const<<<g0, 256, 0, s>>>(out, n, l, ld, -shift);
+    launch_k(k_fill_const, g0, 256, 0, s, out, n, l, ld, -shift);
     FQB_LAUNCHED();
     if (dense_columns(n, denom)) {
-        k_iid_walk_cta<kFillDense><<<unsigned(l), 1024, 0, s>>>(kind, philox_key(seed), uint32_t(block_id), n,
+        launch_k(k_iid_walk_cta<kFillDense>, unsigned(l), 1024, 0, s, kind, philox_key(seed), uint32_t(block_id), n,
                                                               denom, scale, shift, nullptr, nullptr, nullptr,
                                                               nullptr, out, ld, status);
         FQB_LAUNCHED();
         lc.bump(2);
         return;
     }
-    k_iid_walk<kFillDense><<<unsigned(ceil_div(l, 8)), 256, 0, s>>>(
+    launch_k(k_iid_walk<kFillDense>, unsigned(ceil_div(l, 8)), 256, 0, s, 
         kind, philox_key(seed), uint32_t(block_id), n, l, denom, scale, shift, nullptr, nullptr,
         nullptr, nullptr, out, ld, status);
     FQB_LAUNCHED();
@@ -381,7 +389,7 @@ void launch_zeta_fill(int kind, uint64_t seed, int block_id, int64_t n, int l, i
                       double scale, int* col_ptr, int* row_idx, double* values, unsigned* status,
                       cudaStream_t s, LaunchCounter& lc) {
     if (zeta > kMaxZeta) throw Error(kStatusConfig, "zeta exceeds 256");
-    k_zeta_fill<<<unsigned(ceil_div(l + 1, 64)), 64, 0, s>>>(kind, philox_key(seed), uint32_t(block_id),
+    launch_k(k_zeta_fill, unsigned(ceil_div(l + 1, 64)), 64, 0, s, kind, philox_key(seed), uint32_t(block_id),
                                                              n, l, zeta, scale, col_ptr, row_idx,
                                                              values, status);
     FQB_LAUNCHED();
@@ -389,7 +397,7 @@ void launch_zeta_fill(int kind, uint64_t seed, int block_id, int64_t n, int l, i
 }
 
 void launch_exclusive_scan(const int* counts, int l, int* col_ptr, cudaStream_t s, LaunchCounter& lc) {
-    k_exclusive_scan<<<1, 1024, 0, s>>>(counts, l, col_ptr);
+    launch_k(k_exclusive_scan, 1, 1024, 0, s, counts, l, col_ptr);
     FQB_LAUNCHED();
     lc.bump();
 }
@@ -397,9 +405,9 @@ void launch_exclusive_scan(const int* counts, int l, int* col_ptr, cudaStream_t 
 void launch_densify(const int* col_ptr, const int* row_idx, const double* values, int64_t n, int l,
                     double shift, double* out, int64_t ld, cudaStream_t s, LaunchCounter& lc) {
     dim3 g0(unsigned(ceil_div(n, 256)), unsigned(l));
-    k_fill_const<<<g0, 256, 0, s>>>(out, n, l, ld, -shift);
+    launch_k(k_fill_const, g0, 256, 0, s, out, n, l, ld, -shift);
     FQB_LAUNCHED();
-    k_scatter<<<unsigned(l), 128, 0, s>>>(col_ptr, row_idx, values, l, shift, out, ld);
+    launch_k(k_scatter, unsigned(l), 128, 0, s, col_ptr, row_idx, values, l, shift, out, ld);
     FQB_LAUNCHED();
     lc.bump(2);
 }

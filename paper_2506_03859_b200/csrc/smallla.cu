@@ -72,6 +72,7 @@ __global__ void __launch_bounds__(1024) k_chol_inv(const double* __restrict__ S,
                                                    double* __restrict__ max_diag_out,
                                                    unsigned* status, unsigned fail_bit,
                                                    double* gscratch) {
+    FQB_PDL_ENTRY();
     extern __shared__ double smem[];
     __shared__ double red[32];
     __shared__ double sd[1024];
@@ -146,6 +147,7 @@ __global__ void __launch_bounds__(1024) k_chol_inv_reg(const double* __restrict_
                                                        double* __restrict__ R, double* __restrict__ Rinv,
                                                        double* __restrict__ max_diag_out, unsigned* status,
                                                        unsigned fail_bit) {
+    FQB_PDL_ENTRY();
     extern __shared__ double smem[];        // final M, b x (b+1), row-major
     __shared__ double prow[2][kSmemMaxB];
     __shared__ double red[32];
@@ -232,6 +234,7 @@ __global__ void __launch_bounds__(1024) k_sym_eig(const double* __restrict__ S, 
                                                   double* __restrict__ values,
                                                   double* __restrict__ vectors, double* __restrict__ vtmp,
                                                   unsigned* status, unsigned fail_bit) {
+    FQB_PDL_ENTRY();
     extern __shared__ double A[];
     __shared__ double cs[64], sn[64];
     __shared__ int pp[64], qq[64];
@@ -353,6 +356,7 @@ __global__ void __launch_bounds__(1024) k_sym_eig(const double* __restrict__ S, 
 
 __global__ void k_eigsvd_scale(const double* values, const double* vectors, int b, double* vs,
                                double* sigma, unsigned* status, unsigned fail_bit) {
+    FQB_PDL_ENTRY();
     const double lmax = values[b - 1];
     if (!(lmax > 0.0)) {
         if (threadIdx.x == 0) atomicOr(status, fail_bit);
@@ -369,6 +373,7 @@ __global__ void k_eigsvd_scale(const double* values, const double* vectors, int 
 
 __global__ void k_axpy_cols(double alpha, const double* x, int64_t ldx, double* y, int64_t ldy,
                             int64_t rows, int cols) {
+    FQB_PDL_ENTRY();
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     const int c = blockIdx.y;
     if (i < rows && c < cols) y[int64_t(c) * ldy + i] = fma(-alpha, x[int64_t(c) * ldx + i], y[int64_t(c) * ldy + i]);
@@ -377,6 +382,7 @@ __global__ void k_axpy_cols(double alpha, const double* x, int64_t ldx, double* 
 // reference halving rule (driver.cpp:216-221) on the eigSVD sigma (floored like
 // matrix_core.cpp:203-206); alpha lives on the device so no host sync is needed.
 __global__ void k_shift_update(const double* values, int b, int conv, double* alpha) {
+    FQB_PDL_ENTRY();
     const double lmax = values[b - 1];
     const double fl = lmax * 1e-31;
     const double v = conv == 0 ? values[b - 1] : values[0];
@@ -386,6 +392,7 @@ __global__ void k_shift_update(const double* values, int b, int conv, double* al
 
 __global__ void k_axpy_cols_dev(const double* alpha, const double* x, int64_t ldx, double* y, int64_t ldy,
                                 int64_t rows, int cols) {
+    FQB_PDL_ENTRY();
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     const int c = blockIdx.y;
     const double a = *alpha;
@@ -397,7 +404,7 @@ __global__ void k_axpy_cols_dev(const double* alpha, const double* x, int64_t ld
 
 void launch_shift_update(const double* values, int b, int conv, double* alpha, cudaStream_t s,
                          LaunchCounter& lc) {
-    k_shift_update<<<1, 1, 0, s>>>(values, b, conv, alpha);
+    launch_k(k_shift_update, 1, 1, 0, s, values, b, conv, alpha);
     FQB_LAUNCHED();
     lc.bump();
 }
@@ -406,7 +413,7 @@ void launch_axpy_cols_dev(const double* alpha, const double* x, int64_t ldx, dou
                           int64_t rows, int cols, cudaStream_t s, LaunchCounter& lc) {
     if (rows <= 0 || cols <= 0) return;
     dim3 grid(unsigned(ceil_div(rows, 256)), unsigned(cols));
-    k_axpy_cols_dev<<<grid, 256, 0, s>>>(alpha, x, ldx, y, ldy, rows, cols);
+    launch_k(k_axpy_cols_dev, grid, 256, 0, s, alpha, x, ldx, y, ldy, rows, cols);
     FQB_LAUNCHED();
     lc.bump();
 }
@@ -434,20 +441,20 @@ void launch_chol_upper_inv(const double* S, int b, int64_t lds, double tol, doub
     if (b <= kSmemMaxB) {
         const int threads = int(ceil_div(8 * b, 32) * 32);
         if (b <= 32)
-            k_chol_inv_reg<4><<<1, threads, smem, s>>>(S, b, lds, tol, diag_ref, dref_extra, ld_extra, R, Rinv,
+            launch_k(k_chol_inv_reg<4>, 1, threads, smem, s, S, b, lds, tol, diag_ref, dref_extra, ld_extra, R, Rinv,
                                                       max_diag_out, status, fail_bit);
         else if (b <= 64)
-            k_chol_inv_reg<8><<<1, threads, smem, s>>>(S, b, lds, tol, diag_ref, dref_extra, ld_extra, R, Rinv,
+            launch_k(k_chol_inv_reg<8>, 1, threads, smem, s, S, b, lds, tol, diag_ref, dref_extra, ld_extra, R, Rinv,
                                                       max_diag_out, status, fail_bit);
         else
-            k_chol_inv_reg<16><<<1, threads, smem, s>>>(S, b, lds, tol, diag_ref, dref_extra, ld_extra, R, Rinv,
+            launch_k(k_chol_inv_reg<16>, 1, threads, smem, s, S, b, lds, tol, diag_ref, dref_extra, ld_extra, R, Rinv,
                                                        max_diag_out, status, fail_bit);
         FQB_LAUNCHED();
         lc.bump();
         return;
     }
     const int threads = 1024;
-    k_chol_inv<<<1, threads, smem, s>>>(S, b, lds, tol, diag_ref, dref_extra, ld_extra, R, Rinv,
+    launch_k(k_chol_inv, 1, threads, smem, s, S, b, lds, tol, diag_ref, dref_extra, ld_extra, R, Rinv,
                                              max_diag_out, status, fail_bit, scratch);
     FQB_LAUNCHED();
     lc.bump();
@@ -466,7 +473,7 @@ void launch_sym_eig(const double* S, int b, int64_t lds, double* values, double*
                                       int(size_t(kSmemMaxB) * (kSmemMaxB + 1) * sizeof(double))));
         if (dev >= 0 && dev < 64) configured[dev] = true;
     }
-    k_sym_eig<<<1, 1024, smem, s>>>(S, b, lds, values, vectors, vectors ? vtmp : nullptr, status, fail_bit);
+    launch_k(k_sym_eig, 1, 1024, smem, s, S, b, lds, values, vectors, vectors ? vtmp : nullptr, status, fail_bit);
     FQB_LAUNCHED();
     lc.bump();
 }
@@ -474,7 +481,7 @@ void launch_sym_eig(const double* S, int b, int64_t lds, double* values, double*
 void launch_eigsvd_scale(const double* values, const double* vectors, int b, double* vs,
                          double* sigma, unsigned* status, unsigned fail_bit, cudaStream_t s,
                          LaunchCounter& lc) {
-    k_eigsvd_scale<<<1, 1024, 0, s>>>(values, vectors, b, vs, sigma, status, fail_bit);
+    launch_k(k_eigsvd_scale, 1, 1024, 0, s, values, vectors, b, vs, sigma, status, fail_bit);
     FQB_LAUNCHED();
     lc.bump();
 }
@@ -483,7 +490,7 @@ void launch_axpy_cols(double alpha, const double* x, int64_t ldx, double* y, int
                       int64_t rows, int cols, cudaStream_t s, LaunchCounter& lc) {
     if (rows <= 0 || cols <= 0) return;
     dim3 grid(unsigned(ceil_div(rows, 256)), unsigned(cols));
-    k_axpy_cols<<<grid, 256, 0, s>>>(alpha, x, ldx, y, ldy, rows, cols);
+    launch_k(k_axpy_cols, grid, 256, 0, s, alpha, x, ldx, y, ldy, rows, cols);
     FQB_LAUNCHED();
     lc.bump();
 }

@@ -37,6 +37,7 @@ __global__ void __launch_bounds__(256) k_gather_spmm(const T* __restrict__ a, in
                                                      const double* __restrict__ values,
                                                      const double* __restrict__ z,
                                                      double* __restrict__ c, int64_t ldc) {
+    FQB_PDL_ENTRY();
     constexpr int ROWS = 64 * VPL;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int j = blockIdx.y;
@@ -111,6 +112,7 @@ __global__ void __launch_bounds__(256) k_gather_tmul(const double* __restrict__ 
                                                      const double* __restrict__ values,
                                                      const double* __restrict__ colsum, double shift,
                                                      double* __restrict__ t, int64_t ldt) {
+    FQB_PDL_ENTRY();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const int j = blockIdx.y;
     if (i >= k) return;
@@ -142,12 +144,12 @@ static void gather_spmm_impl(const T* a, int64_t m, int64_t lda, const int* col_
     if (vpl != 1 && vpl != 2 && vpl != 4) vpl = 1;
     dim3 grid(unsigned(ceil_div(m, int64_t(64 * vpl) * kWarpsPerCta)), unsigned(l));
     if (vec2) {
-        if (vpl == 4) k_gather_spmm<T, true, 4><<<grid, 256, 0, s>>>(a, m, lda, col_ptr, row_idx, values, z, c, ldc);
+        if (vpl == 4) launch_k(k_gather_spmm<T, true, 4>, grid, 256, 0, s, a, m, lda, col_ptr, row_idx, values, z, c, ldc);
         else if (vpl == 2)
-            k_gather_spmm<T, true, 2><<<grid, 256, 0, s>>>(a, m, lda, col_ptr, row_idx, values, z, c, ldc);
-        else k_gather_spmm<T, true, 1><<<grid, 256, 0, s>>>(a, m, lda, col_ptr, row_idx, values, z, c, ldc);
+            launch_k(k_gather_spmm<T, true, 2>, grid, 256, 0, s, a, m, lda, col_ptr, row_idx, values, z, c, ldc);
+        else launch_k(k_gather_spmm<T, true, 1>, grid, 256, 0, s, a, m, lda, col_ptr, row_idx, values, z, c, ldc);
     } else {
-        k_gather_spmm<T, false, 1><<<grid, 256, 0, s>>>(a, m, lda, col_ptr, row_idx, values, z, c, ldc);
+        launch_k(k_gather_spmm<T, false, 1>, grid, 256, 0, s, a, m, lda, col_ptr, row_idx, values, z, c, ldc);
     }
     FQB_LAUNCHED();
     lc.bump();
@@ -170,7 +172,7 @@ void launch_gather_tmul(const double* wt, int64_t n, int64_t ldw, int k, const i
     (void)n;
     if (k <= 0 || l <= 0) return;
     dim3 grid(unsigned(ceil_div(k, 256)), unsigned(l));
-    k_gather_tmul<<<grid, 256, 0, s>>>(wt, ldw, k, col_ptr, row_idx, values, colsum, shift, t, ldt);
+    launch_k(k_gather_tmul, grid, 256, 0, s, wt, ldw, k, col_ptr, row_idx, values, colsum, shift, t, ldt);
     FQB_LAUNCHED();
     lc.bump();
 }

@@ -80,6 +80,7 @@ void cs_check(cusolverStatus_t st, const char* what) {
 
 __global__ void k_scale_cols(const double* src, int64_t lds, const double* scale, int rows, int cols, double* dst,
                              int64_t ldd) {
+    FQB_PDL_ENTRY();
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     const int c = blockIdx.y;
     if (i < rows && c < cols) dst[int64_t(c) * ldd + i] = src[int64_t(c) * lds + i] * scale[c];
@@ -87,6 +88,7 @@ __global__ void k_scale_cols(const double* src, int64_t lds, const double* scale
 
 // T (r x w, ld r) = (V[s:s+w, :] diag(sigma))'   (sigma null: unscaled)
 __global__ void k_strip_t(const double* v, int64_t ldv, const double* sigma, int r, int64_t s, int w, double* t) {
+    FQB_PDL_ENTRY();
     const int k = blockIdx.y;
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j < w && k < r) t[int64_t(j) * r + k] = v[int64_t(k) * ldv + s + j] * (sigma ? sigma[k] : 1.0);
@@ -147,7 +149,7 @@ double relative_error(Handle& h, const double* a, int64_t m, int64_t n, int64_t 
                                    cudaMemcpyDeviceToDevice, s));
         if (r > 0) {
             dim3 g(unsigned(ceil_div(wc, 256)), unsigned(r));
-            k_strip_t<<<g, 256, 0, s>>>(V, ldv, SIG, r, c0, int(wc), t.ptr);
+            launch_k(k_strip_t, g, 256, 0, s, V, ldv, SIG, r, c0, int(wc), t.ptr);
             FQB_LAUNCHED();
             h.lc.bump();
             gemm(false, m, wc, r, -1.0, U, ldu, t.ptr, r, 1.0, d.ptr, m, h.gws, h.num_sms, s, h.lc);
@@ -256,7 +258,7 @@ void assemble_svd(Handle& h, const double* q, int64_t ldq, const double* bt, int
     us.ensure(size_t(l) * l, s);
     FQB_CUDA(cudaMemcpyAsync(scale.ptr, inv.data(), sizeof(double) * l, cudaMemcpyHostToDevice, s));
     dim3 grid(unsigned(ceil_div(l, 256)), unsigned(l));
-    k_scale_cols<<<grid, 256, 0, s>>>(mat.ptr, l, scale.ptr, l, l, us.ptr, l);
+    launch_k(k_scale_cols, grid, 256, 0, s, mat.ptr, l, scale.ptr, l, l, us.ptr, l);
     FQB_LAUNCHED();
     h.lc.bump();
     // U = Q U~ (this rank's rows), V = Bt (U~ Sigma^-1)
