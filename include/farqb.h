@@ -190,6 +190,10 @@ fqb_status fqb_qb_fixed_rank_f32(fqb_handle h, const float* a, int64_t m, int64_
                                  fqb_block_source_fn src, void* user, unsigned flags,
                                  fqb_qb_result* out);
 void fqb_result_free(fqb_qb_result* r);
+/* Host results (Q, B', U, V) live in pinned, pooled memory (fast D2H, no page
+ * faults).  A caller that keeps one of those arrays beyond the result frees it
+ * with fqb_host_free and sets the field to NULL before fqb_result_free. */
+void fqb_host_free(void* p);
 
 /* ---- row-sharded multi-GPU (one rank per GPU, NCCL over NVLink) ------------- */
 /* Rank 0 creates a 128-byte id, the caller distributes it (e.g. with

@@ -76,6 +76,7 @@ SIGNATURES = [
     ("fqb_qb_fixed_rank_f32", C.c_int, [_H, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_int, C.c_int,
                                     C.POINTER(ConfigC), SOURCE_FN, C.c_void_p, C.c_uint,
                                     C.POINTER(ResultC)]),
+    ("fqb_host_free", None, [C.c_void_p]),
     ("fqb_result_free", None, [C.POINTER(ResultC)]),
     ("fqb_comm_unique_id", C.c_int, [C.c_void_p]),
     ("fqb_comm_attach", C.c_int, [_H, C.c_void_p, C.c_int, C.c_int]),

@@ -221,21 +221,23 @@ fqb_status fqb_qb_fixed_rank(fqb_handle h, const double* a, int64_t m, int64_t n
     return st;
 }
 
+void fqb_host_free(void* p) { farqb::host_free(p); }
+
 void fqb_result_free(fqb_qb_result* r) {
     if (!r) return;
     if (r->on_device) {
         if (r->q) cudaFree(r->q);
         if (r->bt) cudaFree(r->bt);
     } else {
-        std::free(r->q);
-        std::free(r->bt);
+        farqb::host_free(r->q);
+        farqb::host_free(r->bt);
     }
     if (r->on_device) {
         if (r->u) cudaFree(r->u);
         if (r->v) cudaFree(r->v);
     } else {
-        std::free(r->u);
-        std::free(r->v);
+        farqb::host_free(r->u);
+        farqb::host_free(r->v);
     }
     std::free(r->sigma);
     std::free(r->v_flagged);

@@ -739,8 +739,8 @@ int run_qb(Handle& h, const void* a, bool a_f32, int64_t m, int64_t n, int64_t l
         out->bt = run.bt().detach();
         out->on_device = 1;
     } else if (l > 0 && (flags & FQB_OUT_HOST)) {
-        out->q = static_cast<double*>(std::malloc(sizeof(double) * size_t(m) * l));
-        out->bt = static_cast<double*>(std::malloc(sizeof(double) * size_t(n) * l));
+        out->q = static_cast<double*>(host_alloc(sizeof(double) * size_t(m) * l));
+        out->bt = static_cast<double*>(host_alloc(sizeof(double) * size_t(n) * l));
         if (!out->q || !out->bt) throw Error(kStatusAlloc, "host result allocation failed");
         FQB_CUDA(cudaMemcpy2DAsync(out->q, m * sizeof(double), run.q().ptr, run.ldq() * sizeof(double),
                                    m * sizeof(double), l, cudaMemcpyDeviceToHost, s));
@@ -772,8 +772,8 @@ int run_qb(Handle& h, const void* a, bool a_f32, int64_t m, int64_t n, int64_t l
             out->ldu = run.ldq();
             out->ldv = run.ldbt();
         } else if (svd_r > 0 && (flags & FQB_OUT_HOST)) {
-            out->u = static_cast<double*>(std::malloc(sizeof(double) * size_t(m) * svd_r));
-            out->v = static_cast<double*>(std::malloc(sizeof(double) * size_t(n) * svd_r));
+            out->u = static_cast<double*>(host_alloc(sizeof(double) * size_t(m) * svd_r));
+            out->v = static_cast<double*>(host_alloc(sizeof(double) * size_t(n) * svd_r));
             if (!out->u || !out->v) throw Error(kStatusAlloc, "host result allocation failed");
             FQB_CUDA(cudaMemcpy2DAsync(out->u, m * sizeof(double), u_dev.ptr + int64_t(drop) * run.ldq(),
                                        run.ldq() * sizeof(double), m * sizeof(double), svd_r,

@@ -96,6 +96,9 @@ void assemble_svd(Handle& h, const double* q, int64_t ldq, const double* bt, int
                   int l, double* u, int64_t ldu, double* v, int64_t ldv, std::vector<double>& sigma,
                   std::vector<char>& flagged);
 void destroy_cusolver(Handle& h);
+// hostmem.cu: pinned, pooled host arrays for results returned on the host
+void* host_alloc(size_t bytes);
+void host_free(void* ptr);
 // ||A - U diag(sigma) V'||_F / ||A||_F (sigma host or null = unscaled), strips of A on the device
 double relative_error(Handle& h, const double* a, int64_t m, int64_t n, int64_t lda, bool a_on_device,
                       const double* u, int64_t ldu, const double* sigma, const double* v, int64_t ldv, int r,

@@ -266,6 +266,27 @@ class _DeviceBuffer:
             pass
 
 
+class _HostBuffer:
+    """Owns a library-allocated pinned host array (fqb_host_free on release); a
+    column-major rows x cols float64 view via __array_interface__ -- no copy."""
+
+    def __init__(self, ptr: int, rows: int, cols: int):
+        self.ptr = ptr
+        self.__array_interface__ = {
+            "shape": (rows, cols), "strides": (8, rows * 8), "typestr": "<f8",
+            "data": (ptr, False), "version": 3}
+
+    def __del__(self):
+        try:
+            N.lib().fqb_host_free(self.ptr)
+        except Exception:  # noqa: BLE001 - interpreter shutdown
+            pass
+
+
+def _host_array(ptr: int, rows: int, cols: int) -> np.ndarray:
+    return np.asarray(_HostBuffer(ptr, rows, cols))
+
+
 def _cudart_free(ptr: int) -> None:
     r = N.ResultC()
     r.on_device = 1
@@ -481,10 +502,11 @@ class Engine:
                     q = torch.as_tensor(qb, device=f"cuda:{self.device}").t()
                     bt = torch.as_tensor(bb, device=f"cuda:{self.device}").t()
             elif l > 0 and output == "host" and res.q:
-                q = np.ctypeslib.as_array(C.cast(res.q, C.POINTER(C.c_double)), (m * l,)).reshape(
-                    (m, l), order="F").copy()
-                bt = np.ctypeslib.as_array(C.cast(res.bt, C.POINTER(C.c_double)), (n * l,)).reshape(
-                    (n, l), order="F").copy()
+                # zero-copy: the arrays own the library's pinned buffers
+                q = _host_array(res.q, m, l)
+                bt = _host_array(res.bt, n, l)
+                res.q = None
+                res.bt = None
             br = (np.ctypeslib.as_array(res.block_residuals, (res.blocks,)).copy()
                   if res.blocks and res.block_residuals else np.zeros(0))
             ids = (np.ctypeslib.as_array(res.block_ids, (res.n_ids,)).tolist()
@@ -507,10 +529,10 @@ class Engine:
                         out.u = torch.as_tensor(ub, device=f"cuda:{self.device}").t()
                         out.v = torch.as_tensor(vb, device=f"cuda:{self.device}").t()
                 elif r > 0 and res.u and output == "host":
-                    out.u = np.ctypeslib.as_array(C.cast(res.u, C.POINTER(C.c_double)), (m * r,)).reshape(
-                        (m, r), order="F").copy()
-                    out.v = np.ctypeslib.as_array(C.cast(res.v, C.POINTER(C.c_double)), (n * r,)).reshape(
-                        (n, r), order="F").copy()
+                    out.u = _host_array(res.u, m, r)
+                    out.v = _host_array(res.v, n, r)
+                    res.u = None
+                    res.v = None
             return out
         finally:
             self._lib.fqb_result_free(C.byref(res))
