@@ -121,6 +121,8 @@ fqb_status fqb_destroy(fqb_handle h) {
         cudaFreeHost(h->h.host_scalars);
         cudaEventDestroy(h->h.ev0);
         cudaEventDestroy(h->h.ev1);
+        if (h->h.copy_stream) cudaStreamDestroy(h->h.copy_stream);
+        if (h->h.ev_qb) cudaEventDestroy(h->h.ev_qb);
         cudaStreamDestroy(h->h.own_stream);
         delete h;
         return FQB_OK;

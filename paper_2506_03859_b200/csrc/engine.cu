@@ -706,6 +706,35 @@ int run_qb(Handle& h, const void* a, bool a_f32, int64_t m, int64_t n, int64_t l
         status = kStatusDegenerate;
         message = e.what();
     }
+    // Host Q, B' are final now: copy them out on a second stream while the SVD
+    // assembly runs (the assembly only reads them)
+    const int l_qb = run.rank();
+    double *host_q = nullptr, *host_bt = nullptr;
+    struct HostGuard {   // returns the blocks to the pool if the assembly below throws
+        double** a;
+        double** b;
+        ~HostGuard() {
+            if (*a) host_free(*a);
+            if (*b) host_free(*b);
+        }
+    } host_guard{&host_q, &host_bt};
+    const bool host_out = l_qb > 0 && !(flags & FQB_OUT_DEVICE) && (flags & FQB_OUT_HOST);
+    if (host_out) {
+        host_q = static_cast<double*>(host_alloc(sizeof(double) * size_t(m) * l_qb));
+        host_bt = static_cast<double*>(host_alloc(sizeof(double) * size_t(n) * l_qb));
+        if (!host_q || !host_bt) throw Error(kStatusAlloc, "host result allocation failed");
+        if (!h.copy_stream) {
+            FQB_CUDA(cudaStreamCreateWithFlags(&h.copy_stream, cudaStreamNonBlocking));
+            FQB_CUDA(cudaEventCreateWithFlags(&h.ev_qb, cudaEventDisableTiming));
+        }
+        FQB_CUDA(cudaEventRecord(h.ev_qb, s));
+        FQB_CUDA(cudaStreamWaitEvent(h.copy_stream, h.ev_qb, 0));
+        FQB_CUDA(cudaMemcpy2DAsync(host_q, m * sizeof(double), run.q().ptr, run.ldq() * sizeof(double),
+                                   m * sizeof(double), l_qb, cudaMemcpyDeviceToHost, h.copy_stream));
+        FQB_CUDA(cudaMemcpy2DAsync(host_bt, n * sizeof(double), run.bt().ptr, run.ldbt() * sizeof(double),
+                                   n * sizeof(double), l_qb, cudaMemcpyDeviceToHost, h.copy_stream));
+    }
+
     // ApproxSvd (assemble_svd, driver.cpp:296-345): also for the partial result of
     // ToleranceNotReached; BlockDegenerate carries no factorization (errors.hpp:28-37)
     std::vector<double> sig;
@@ -738,14 +767,10 @@ int run_qb(Handle& h, const void* a, bool a_f32, int64_t m, int64_t n, int64_t l
         out->q = run.q().detach();
         out->bt = run.bt().detach();
         out->on_device = 1;
-    } else if (l > 0 && (flags & FQB_OUT_HOST)) {
-        out->q = static_cast<double*>(host_alloc(sizeof(double) * size_t(m) * l));
-        out->bt = static_cast<double*>(host_alloc(sizeof(double) * size_t(n) * l));
-        if (!out->q || !out->bt) throw Error(kStatusAlloc, "host result allocation failed");
-        FQB_CUDA(cudaMemcpy2DAsync(out->q, m * sizeof(double), run.q().ptr, run.ldq() * sizeof(double),
-                                   m * sizeof(double), l, cudaMemcpyDeviceToHost, s));
-        FQB_CUDA(cudaMemcpy2DAsync(out->bt, n * sizeof(double), run.bt().ptr, run.ldbt() * sizeof(double),
-                                   n * sizeof(double), l, cudaMemcpyDeviceToHost, s));
+    } else if (host_out) {
+        out->q = host_q;     // copied on the copy stream above
+        out->bt = host_bt;
+        host_q = host_bt = nullptr;   // owned by the result now
         out->ldq = m;
         out->ldbt = n;
         out->on_device = 0;
@@ -786,6 +811,7 @@ int run_qb(Handle& h, const void* a, bool a_f32, int64_t m, int64_t n, int64_t l
         }
     }
     FQB_CUDA(cudaStreamSynchronize(s));
+    if (host_out) FQB_CUDA(cudaStreamSynchronize(h.copy_stream));
     float ms = 0.f;
     cudaEventElapsedTime(&ms, h.ev0, h.ev1);
     out->elapsed_ms = ms;

@@ -89,6 +89,9 @@ struct Handle {
     int nranks = 1, rank = 0;
     int64_t collectives = 0;
     void* cusolver = nullptr;  // svd.cu
+    // D2H of host results overlapped with the SVD assembly (created on first use)
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t ev_qb = nullptr;
 };
 
 // svd.cu: U = Q U~, V = Bt U~ Sigma^-1 from eig(B B'); sigma ascending
