@@ -9,6 +9,7 @@
 //  launch_colsum      column sums of B' for the centered deflation term.
 #include <algorithm>
 #include <cstdint>
+#include <type_traits>
 
 #include "kernels.hpp"
 
@@ -43,18 +44,78 @@ __global__ void __launch_bounds__(256) k_sumsq_partial(const T* __restrict__ a, 
     const int64_t seg = seg_rows(m, n);
     const int64_t segs_per_col = (m + seg - 1) / seg;
     const int64_t total = segs_per_col * n;
-    double acc = 0.0;
+    // four independent loads / accumulators per thread step (memory-level
+    // parallelism), combined in a fixed order: deterministic for a given shape
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    const int bd = blockDim.x;
     for (int64_t sgi = blockIdx.x; sgi < total; sgi += gridDim.x) {
         const int64_t col = sgi / segs_per_col;
         const int64_t r0 = (sgi - col * segs_per_col) * seg;
         const int64_t r1 = r0 + seg < m ? r0 + seg : m;
         const T* c = a + col * lda;
-        for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+        int64_t r = r0 + threadIdx.x;
+        for (; r + 3 * bd < r1; r += 4 * bd) {
+            double v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] = double(__ldcs(c + r + u * bd));   // streaming: read once
+#pragma unroll
+            for (int u = 0; u < 4; ++u) acc[u] = fma(v[u], v[u], acc[u]);
+        }
+        for (; r < r1; r += bd) {
             const double v = double(__ldg(c + r));
-            acc = fma(v, v, acc);
+            acc[0] = fma(v, v, acc[0]);
         }
     }
-    const double s = block_sum(acc, sh);
+    const double s = block_sum((acc[0] + acc[1]) + (acc[2] + acc[3]), sh);
+    if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
+// Contiguous A (lda == m): the m*n values as one array, CTA c sums the fixed chunk
+// [c*len/P, (c+1)*len/P) with 16-byte loads -- deterministic for a given shape.
+template <typename T>
+__global__ void __launch_bounds__(256) k_sumsq_flat(const T* __restrict__ a, int64_t len, double* partial) {
+    FQB_PDL_ENTRY();
+    __shared__ double sh[32];
+    const int64_t c0 = len * blockIdx.x / gridDim.x, c1 = len * (blockIdx.x + 1) / gridDim.x;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    constexpr int VEC = 16 / sizeof(T);   // elements per 16-byte load
+    // head up to 16-byte alignment, then vector body, then tail
+    int64_t i = c0;
+    const int64_t mis = (reinterpret_cast<uintptr_t>(a + c0) & 15) / sizeof(T);
+    const int64_t head = mis ? std::min<int64_t>(c1 - c0, VEC - mis) : 0;
+    if (threadIdx.x < head) {
+        const double v = double(a[c0 + threadIdx.x]);
+        acc[0] = fma(v, v, acc[0]);
+    }
+    i = c0 + head;
+    const int64_t nvec = (c1 - i) / VEC;
+    const T* base = a + i;
+    using V = typename std::conditional<sizeof(T) == 8, double2, float4>::type;
+    const V* vb = reinterpret_cast<const V*>(base);
+    auto sq = [](const V& v) -> double {
+        if constexpr (sizeof(T) == 8) {
+            return fma(v.x, v.x, v.y * v.y);
+        } else {
+            double s2 = fma(double(v.x), double(v.x), double(v.y) * double(v.y));
+            s2 = fma(double(v.z), double(v.z), s2);
+            return fma(double(v.w), double(v.w), s2);
+        }
+    };
+    const int64_t bd = blockDim.x;
+    int64_t k = threadIdx.x;
+    for (; k + 3 * bd < nvec; k += 4 * bd) {   // four 16-byte loads in flight per thread
+        V v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = __ldcs(vb + k + u * bd);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc[u] += sq(v[u]);
+    }
+    for (; k < nvec; k += bd) acc[0] += sq(__ldcs(vb + k));
+    for (int64_t k = i + nvec * VEC + threadIdx.x; k < c1; k += blockDim.x) {
+        const double v = double(a[k]);
+        acc[1] = fma(v, v, acc[1]);
+    }
+    const double s = block_sum((acc[0] + acc[1]) + (acc[2] + acc[3]), sh);
     if (threadIdx.x == 0) partial[blockIdx.x] = s;
 }
 
@@ -103,7 +164,9 @@ __global__ void __launch_bounds__(256) k_colsum(const double* __restrict__ x, in
 template <typename T>
 static void sumsq_impl(const T* a, int64_t m, int64_t n, int64_t lda, double* partial, double* out, cudaStream_t s,
                        LaunchCounter& lc) {
-    launch_k(k_sumsq_partial<T>, kReducePartials, 256, 0, s, a, m, n, lda, partial);
+    if (lda == m && m * n >= (int64_t(1) << 22))   // big contiguous A: 16-byte streaming loads (C2: 141 -> 84 us)
+        launch_k(k_sumsq_flat<T>, kReducePartials, 256, 0, s, a, m * n, partial);
+    else launch_k(k_sumsq_partial<T>, kReducePartials, 256, 0, s, a, m, n, lda, partial);
     FQB_LAUNCHED();
     launch_k(k_sum_partials, 1, 1024, 0, s, partial, kReducePartials, out);
     FQB_LAUNCHED();
