@@ -257,7 +257,8 @@ fqb_status fqb_gemm(fqb_handle h, int trans_a, int64_t m, int64_t n, int64_t k, 
 /* Same contract as fqb_gemm, computed on the INT8 tensor cores (tcgen05
  * kind::i8) by Ozaki slicing: 8 signed 7-bit slices per operand with one
  * power-of-two scale per output row / column, exact int32 slice products, FP64
- * recombination -- the accuracy class of an FP64 GEMM.  n <= 64. */
+ * recombination -- the accuracy class of an FP64 GEMM.  Any n (B is sliced in chunks
+ * of <= 64 columns, one pass over the slices of A each). */
 fqb_status fqb_gemm_emulated(fqb_handle h, int trans_a, int64_t m, int64_t n, int64_t k, double alpha,
                              const double* a, int64_t lda, const double* b, int64_t ldb, double beta,
                              double* c, int64_t ldc);
@@ -265,7 +266,8 @@ fqb_status fqb_gemm_emulated(fqb_handle h, int trans_a, int64_t m, int64_t n, in
 /* Persistent sliced operand: A (m x n, lda, device memory) cut once into the Ozaki
  * slices of both layouts (16 m n bytes of device memory), then any number of
  *     C = alpha op(A) B + beta C,   op(A) = A' (trans_a: B m x nb, C n x nb)
- *                                   op(A) = A  (B n x nb, C m x nb),   nb <= 64
+ *                                   op(A) = A  (B n x nb, C m x nb)
+ * (nb > 64 in chunks of <= 64 columns)
  * products on the INT8 tensor cores -- the engine's A-pass path, exposed for
  * callers that apply one matrix many times (and used by bench.py to time it).
  * A must stay unchanged while the slices are in use only in the sense that the

@@ -432,26 +432,24 @@ fqb_status fqb_gemm_emulated(fqb_handle h, int trans_a, int64_t m, int64_t n, in
     return guarded([&]() -> fqb_status {
         bind(h);
         if (m < 0 || n < 0 || k < 0) throw farqb::Error(FQB_ERR_DIMENSION, "negative dimension");
-        if (n > farqb::ozaki_max_n()) throw farqb::Error(FQB_ERR_DIMENSION, "fqb_gemm_emulated: n > 64");
         if (ldc < m || ldb < k || lda < (trans_a ? k : m))
             throw farqb::Error(FQB_ERR_DIMENSION, "leading dimension too small");
         if (m == 0 || n == 0) return FQB_OK;
+        if (k == 0) throw farqb::Error(FQB_ERR_DIMENSION, "fqb_gemm_emulated: k = 0");
         cudaStream_t s = h->h.stream;
         farqb::ensure_gemm_workspace(h->h);
-        if (k == 0) throw farqb::Error(FQB_ERR_DIMENSION, "fqb_gemm_emulated: k = 0");
         farqb::DeviceArray<int8_t> xs, zs;
         farqb::DeviceArray<int> ex, ez;
         xs.ensure(size_t(farqb::ozaki_x_bytes(m, k)), s);
-        zs.ensure(size_t(farqb::ozaki_z_bytes(n, k)), s);
+        zs.ensure(size_t(farqb::ozaki_z_bytes(farqb::ozaki_max_n(), k)), s);
         ex.ensure(size_t(m), s);
-        ez.ensure(size_t(n), s);
+        ez.ensure(size_t(farqb::ozaki_max_n()), s);
         farqb::DeviceArray<unsigned> line_max;
         line_max.ensure(size_t(farqb::ozaki_line_max_words(m, k)), s);
         if (trans_a) farqb::ozaki_slice_a(a, k, m, lda, line_max.ptr, xs.ptr, ex.ptr, nullptr, nullptr, s, h->h.lc);
         else farqb::ozaki_slice_a(a, m, k, lda, line_max.ptr, nullptr, nullptr, xs.ptr, ex.ptr, s, h->h.lc);
-        farqb::ozaki_slice_z(b, k, n, ldb, ez.ptr, zs.ptr, s, h->h.lc);
-        farqb::ozaki_gemm(m, n, k, alpha, xs.ptr, ex.ptr, zs.ptr, ez.ptr, beta, c, ldc, h->h.gws.work, h->h.num_sms,
-                          s, h->h.lc);
+        farqb::ozaki_apply(m, n, k, alpha, xs.ptr, ex.ptr, b, ldb, beta, c, ldc, zs.ptr, ez.ptr, h->h.gws.work,
+                           h->h.num_sms, s, h->h.lc);
         return FQB_OK;   // temporaries are freed stream-ordered, after the kernels
     });
 }
@@ -502,16 +500,16 @@ fqb_status fqb_sliced_gemm(fqb_handle h, fqb_sliced sl, int trans_a, int64_t nb,
     return guarded([&]() -> fqb_status {
         bind(h);
         if (!sl) throw farqb::Error(FQB_ERR_INVALID_ARGUMENT, "null sliced operand");
-        if (nb < 0 || nb > farqb::ozaki_max_n()) throw farqb::Error(FQB_ERR_DIMENSION, "fqb_sliced_gemm: nb > 64");
+        if (nb < 0) throw farqb::Error(FQB_ERR_DIMENSION, "fqb_sliced_gemm: negative nb");
         const int64_t M = trans_a ? sl->n : sl->m, K = trans_a ? sl->m : sl->n;
         if (ldb < K || ldc < M) throw farqb::Error(FQB_ERR_DIMENSION, "leading dimension too small");
         if (nb == 0) return FQB_OK;
         cudaStream_t s = h->h.stream;
         farqb::ensure_gemm_workspace(h->h);
-        sl->z.ensure(size_t(farqb::ozaki_z_bytes(nb, K)), s);
-        farqb::ozaki_slice_z(b, K, nb, ldb, sl->ez.ptr, sl->z.ptr, s, h->h.lc);
-        farqb::ozaki_gemm(M, nb, K, alpha, trans_a ? sl->x_tn.ptr : sl->x_nn.ptr, trans_a ? sl->e_tn.ptr : sl->e_nn.ptr,
-                          sl->z.ptr, sl->ez.ptr, beta, c, ldc, h->h.gws.work, h->h.num_sms, s, h->h.lc);
+        sl->z.ensure(size_t(farqb::ozaki_z_bytes(farqb::ozaki_max_n(), K)), s);
+        farqb::ozaki_apply(M, nb, K, alpha, trans_a ? sl->x_tn.ptr : sl->x_nn.ptr,
+                           trans_a ? sl->e_tn.ptr : sl->e_nn.ptr, b, ldb, beta, c, ldc, sl->z.ptr, sl->ez.ptr,
+                           h->h.gws.work, h->h.num_sms, s, h->h.lc);
         return FQB_OK;
     });
 }

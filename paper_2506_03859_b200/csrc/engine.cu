@@ -253,8 +253,9 @@ class QbRun {
     static bool ozaki_default(int64_t m, int64_t n, int b) {
         const char* e = std::getenv("FQB_OZAKI");
         if (e && e[0] == '0') return false;
-        if (b > ozaki_max_n()) return false;
-        return (e && e[0] == '1') || double(m) * double(n) >= double(1 << 24);   // small: DMMA is fine
+        // b > 64 runs in column chunks of <= 64, each one more pass over the slices:
+        // still 1.5-3x ahead of DMMA for b in (64, 128]
+        return (e && e[0] == '1') || (double(m) * double(n) >= double(1 << 24) && b >= 16);   // small: DMMA is fine
     }
 
     // Slice A once per run into the handle's buffers; false (and DMMA from then on)
@@ -293,7 +294,7 @@ class QbRun {
     }
 
     void a_gemm(bool ta, int N, const double* B, int64_t ldb, double* C, int64_t ldc) {
-        if (!oz_on_ || N > ozaki_max_n()) {
+        if (!oz_on_) {
             ensure_fp64_a();
             const int64_t lda = a_ld64_ ? a_ld64_ : lda_;
             if (ta) gemm_(true, n_, N, m_, 1.0, a_, lda, B, ldb, 0.0, C, ldc);
@@ -310,11 +311,10 @@ class QbRun {
             }
         }
         Workspace& w = h_.ws;
-        w.oz_z.ensure(size_t(ozaki_z_bytes(N, K)), s_);
+        w.oz_z.ensure(size_t(ozaki_z_bytes(ozaki_max_n(), K)), s_);
         w.oz_ez.ensure(size_t(ozaki_max_n()), s_);
-        ozaki_slice_z(B, K, N, ldb, w.oz_ez.ptr, w.oz_z.ptr, s_, h_.lc);
-        ozaki_gemm(M, N, K, 1.0, ta ? w.oz_x_tn.ptr : w.oz_x_nn.ptr, ta ? w.oz_e_tn.ptr : w.oz_e_nn.ptr, w.oz_z.ptr,
-                   w.oz_ez.ptr, 0.0, C, ldc, h_.gws.work, h_.num_sms, s_, h_.lc);
+        ozaki_apply(M, N, K, 1.0, ta ? w.oz_x_tn.ptr : w.oz_x_nn.ptr, ta ? w.oz_e_tn.ptr : w.oz_e_nn.ptr, B, ldb, 0.0,
+                    C, ldc, w.oz_z.ptr, w.oz_ez.ptr, h_.gws.work, h_.num_sms, s_, h_.lc);
     }
 
     // ---- Omega ----------------------------------------------------------------

@@ -133,6 +133,11 @@ void ozaki_slice_a(const float* a, int64_t m, int64_t n, int64_t ld, unsigned* l
 // Z (k x n, ld)
 void ozaki_slice_z(const double* b, int64_t k, int64_t n, int64_t ld, int* e, int8_t* out, cudaStream_t s,
                    LaunchCounter& lc);
+// C = alpha X' B + beta C for any N: B (K x N, ld, FP64) sliced in chunks of <= 64
+// columns into z (ozaki_z_bytes(64, K)) / ez (64)
+void ozaki_apply(int64_t M, int64_t N, int64_t K, double alpha, const int8_t* xs, const int* ex, const double* b,
+                 int64_t ldb, double beta, double* C, int64_t ldc, int8_t* z, int* ez, double* work, int num_sms,
+                 cudaStream_t s, LaunchCounter& lc);
 void ozaki_gemm(int64_t M, int64_t N, int64_t K, double alpha, const int8_t* xs, const int* ex, const int8_t* zs,
                 const int* ez, double beta, double* C, int64_t ldc, double* work, int num_sms, cudaStream_t s,
                 LaunchCounter& lc);

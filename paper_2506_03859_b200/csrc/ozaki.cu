@@ -679,6 +679,20 @@ void ozaki_gemm(int64_t M, int64_t N, int64_t K, double alpha, const int8_t* xs,
     }
 }
 
+// N > 64 right-hand columns: balanced chunks of <= 64 (one pass over the A slices each)
+void ozaki_apply(int64_t M, int64_t N, int64_t K, double alpha, const int8_t* xs, const int* ex, const double* b,
+                 int64_t ldb, double beta, double* C, int64_t ldc, int8_t* z, int* ez, double* work, int num_sms,
+                 cudaStream_t s, LaunchCounter& lc) {
+    if (N <= 0) return;
+    const int64_t chunks = ceil_div(N, OZ_BN);
+    const int64_t cw = ceil_div(N, chunks);
+    for (int64_t c0 = 0; c0 < N; c0 += cw) {
+        const int64_t nb = std::min(cw, N - c0);
+        ozaki_slice_z(b + c0 * ldb, K, nb, ldb, ez, z, s, lc);
+        ozaki_gemm(M, nb, K, alpha, xs, ex, z, ez, beta, C + c0 * ldc, ldc, work, num_sms, s, lc);
+    }
+}
+
 int64_t ozaki_workspace_doubles(int num_sms) { return 3 * int64_t(num_sms) * OZ_PARTIAL; }  // 2 pieces + carry
 
 }  // namespace farqb

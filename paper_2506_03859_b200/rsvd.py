@@ -571,7 +571,7 @@ class Engine:
             _raise(st, "fqb_gemm")
 
     def gemm_emulated(self, trans_a: bool, m, n, k, alpha, a_ptr, lda, b_ptr, ldb, beta, c_ptr, ldc):
-        """FP64 GEMM on the INT8 tensor cores (Ozaki slicing), n <= 64."""
+        """FP64 GEMM on the INT8 tensor cores (Ozaki slicing); n > 64 runs in chunks of <= 64 columns."""
         st = self._lib.fqb_gemm_emulated(self._h, int(trans_a), m, n, k, alpha, a_ptr, lda, b_ptr, ldb, beta,
                                          c_ptr, ldc)
         if st:

@@ -95,12 +95,16 @@ def test_emulated_gemm_is_deterministic(eng):
     assert torch.equal(r1, r2)
 
 
-def test_emulated_gemm_rejects_wide_n(eng):
-    a = torch.zeros((10, 10), dtype=torch.float64, device="cuda")
-    b = torch.zeros((10, 65), dtype=torch.float64, device="cuda")
-    c = torch.zeros((10, 65), dtype=torch.float64, device="cuda")
-    with pytest.raises(fqb.DimensionError):
-        eng.gemm_emulated(True, 10, 65, 10, 1.0, a.data_ptr(), 10, b.data_ptr(), 10, 0.0, c.data_ptr(), 10)
+@pytest.mark.parametrize("n", [65, 100, 128, 200])
+def test_emulated_gemm_wide_n_in_chunks(eng, n):
+    """n > 64 runs as balanced chunks of <= 64 columns (config 4 has b = 100)."""
+    m, k = 700, 900
+    g = torch.Generator(device="cpu").manual_seed(n)
+    a = torch.randn((k, m), dtype=torch.float64, generator=g)
+    b = torch.randn((k, n), dtype=torch.float64, generator=g)
+    c0 = torch.randn((m, n), dtype=torch.float64, generator=g)
+    got = _run_emulated(eng, True, a, b, c0, 1.5, 0.25)
+    _check_rows(got, a.t(), b, c0, 1.5, 0.25, np.arange(0, m, 13))
 
 
 def _lowrank(m, n, sig, seed):
@@ -111,14 +115,15 @@ def _lowrank(m, n, sig, seed):
     return np.asfortranarray((u * sig) @ v.T)
 
 
-@pytest.mark.parametrize("kind,zeta,power", [(2, 0, 2), (0, 0, 1), (3, 8, 3), (4, 8, 0)])
-def test_qb_with_emulation_matches_oracle(eng, port, monkeypatch, kind, zeta, power):
-    """FQB_OZAKI=1 forces every A pass onto the INT8 tensor cores, even at this size."""
+@pytest.mark.parametrize("kind,zeta,power,block", [(2, 0, 2, 25), (0, 0, 1, 25), (3, 8, 3, 25), (4, 8, 0, 25),
+                                                  (4, 8, 2, 100)])
+def test_qb_with_emulation_matches_oracle(eng, port, monkeypatch, kind, zeta, power, block):
+    """FQB_OZAKI=1 forces every A pass onto the INT8 tensor cores, even at this size (block 100: chunked)."""
     monkeypatch.setenv("FQB_OZAKI", "1")
     a = _lowrank(900, 700, 1.0 / np.arange(1, 251) ** 1.5, seed=40 + kind + power)
     p = 0.0 if kind == 0 or zeta else 0.5
     spec = SketchSpec(kind, p, 13, zeta=zeta)
-    cfg = FarpcaConfig(eps=1e-2, power=power, block=25, sketch=spec, relative=True)
+    cfg = FarpcaConfig(eps=1e-2, power=power, block=block, sketch=spec, relative=True)
     res = eng.run_fixed_precision(a, cfg, output="host")
 
     def src(n, b, bid):
@@ -127,7 +132,7 @@ def test_qb_with_emulation_matches_oracle(eng, port, monkeypatch, kind, zeta, po
             return SketchArrays(True, s.rows, s.cols, dense=s.dense, p=s.p)
         return SketchArrays(False, s.rows, s.cols, col_ptr=s.col_ptr, row_idx=s.row_idx, values=s.values,
                             centered=s.centered, p=s.p, std_scale=s.std_scale)
-    ref = port.run(a, eps=1e-2, power=power, block=25, kind=kind, p=p, seed=13, zeta=zeta, relative=True,
+    ref = port.run(a, eps=1e-2, power=power, block=block, kind=kind, p=p, seed=13, zeta=zeta, relative=True,
                    source=src)
     assert ref.status == 0 and res.converged
     assert (res.rank, res.blocks, res.block_ids) == (ref.rank, ref.blocks, ref.block_ids)
