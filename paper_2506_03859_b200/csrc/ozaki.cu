@@ -399,13 +399,19 @@ __device__ __forceinline__ unsigned abs_hi(double x) {
 // subnormal maxima get e = -1021 (their digits are 0 or just coarser).
 __device__ __forceinline__ int exp_of_hi(unsigned hi) { return hi >= 0x00100000u ? int(hi >> 20) - 1022 : -1021; }
 
-// the 8 digits of x in line scale e, as bytes
+// the 8 digits of x in line scale e, as raw fields d_p + 64 in [0, 128]: the 7-bit
+// fields of U = R + sum_p 64 2^(49-7p), read from its two 32-bit halves
 __device__ __forceinline__ void digits8(double x, int e, unsigned (&d)[S]) {
-    const long long R = __double2ll_rn(mul_pow2(x, 55 - e));
-    const unsigned long long U = static_cast<unsigned long long>(R + kDigitBias);
-    d[0] = unsigned(int(U >> 49) - 64) & 0xFFu;
-#pragma unroll
-    for (int p = 1; p < S; ++p) d[p] = unsigned(int((U >> (49 - 7 * p)) & 127u) - 64) & 0xFFu;
+    const unsigned long long U = static_cast<unsigned long long>(__double2ll_rn(mul_pow2(x, 55 - e)) + kDigitBias);
+    const unsigned hi = unsigned(U >> 32), lo = unsigned(U);
+    d[0] = hi >> 17;
+    d[1] = (hi >> 10) & 127u;
+    d[2] = (hi >> 3) & 127u;
+    d[3] = __funnelshift_r(lo, hi, 28) & 127u;
+    d[4] = (lo >> 21) & 127u;
+    d[5] = (lo >> 14) & 127u;
+    d[6] = (lo >> 7) & 127u;
+    d[7] = lo & 127u;
 }
 
 // byte offset of (row r, byte c) inside a swizzled TR x OZ_BK byte tile
@@ -425,6 +431,11 @@ __device__ __forceinline__ void put_chunk16(const double (&v)[16], int e, int8_t
 #pragma unroll
         for (int sl = 0; sl < S; ++sl) w[sl][u >> 2] |= d[sl] << (8 * (u & 3));
     }
+    // raw fields -> signed digits: (d - 64) mod 256 per byte, four at a time
+#pragma unroll
+    for (int sl = 0; sl < S; ++sl)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) w[sl][q] = __vadd4(w[sl][q], 0xC0C0C0C0u);
     int8_t* dst = tile0 + swz(r, c);
 #pragma unroll
     for (int sl = 0; sl < S; ++sl)
