@@ -49,13 +49,14 @@ def parse():
 
 
 def make_matrix(device):
-    import torch
-    g = torch.Generator(device=device).manual_seed(SEED_A)
-    u = torch.linalg.qr(torch.randn(M, RANK_SIG, dtype=torch.float64, device=device, generator=g))[0]
-    v = torch.linalg.qr(torch.randn(N, RANK_SIG, dtype=torch.float64, device=device, generator=g))[0]
-    sig = 10.0 ** (-torch.arange(1, RANK_SIG + 1, dtype=torch.float64, device=device) / 50.0)
-    a = (u * sig) @ v.t()
-    return a.t().contiguous().t()  # column-major (DenseMatrix layout)
+    """C2's A on the device with the engine's own generator (fqb_gen_lowrank): U, V =
+    random_orthonormal(8000, 900, seed 42) on the reference's factor streams
+    0xFA000001 / 0xFA000002 (SURVEY.md section 8(d) convention), sigma_i = 10^(-i/50)."""
+    import numpy as np
+    import paper_2506_03859_b200 as fqb
+    idx = device.index if getattr(device, "index", None) is not None else 0
+    sig = 10.0 ** (-np.arange(1, RANK_SIG + 1, dtype=np.float64) / 50.0)
+    return fqb.default_engine(idx).gen_lowrank(M, N, sig, seed=SEED_A)   # column-major (DenseMatrix layout)
 
 
 def config():
@@ -339,7 +340,7 @@ def run_ours(args):
         "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f64",
-        "data": "synthetic (seeded torch N(0,1) factors, see bench.py docstring)",
+        "data": "synthetic: A = U diag(sigma) V' from fqb_gen_lowrank (Philox factor streams, seed 42), see make_matrix",
         "config": {"workload": WORKLOAD, "m": M, "n": N, "block": BLOCK, "power": POWER, "eps": EPS,
                    "sketch": "stdbernoulli p=0.5", "rank_reached": rank_l, "blocks": blocks,
                    "rel_error_indicator": e_rel, "step_device_ms": step_ms, "l2": "A (512 MB) exceeds the 126 MB L2; no flush",

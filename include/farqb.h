@@ -278,6 +278,23 @@ fqb_status fqb_sliced_gemm(fqb_handle h, fqb_sliced s, int trans_a, int64_t nb, 
                            int64_t ldb, double beta, double* c, int64_t ldc);
 fqb_status fqb_sliced_free(fqb_handle h, fqb_sliced s);
 
+/* ---- test matrices on the device (reference synthetic.cpp) ----- */
+/* rsvd::random_orthonormal (synthetic.cpp:121-126): n x r orthonormal columns from
+ * Philox(seed, stream, column) Gaussian panels of 64, block Gram-Schmidt + CholeskyQR
+ * twice per panel (bcgs2_step, :36-53).  q is device memory (ldq >= n). */
+fqb_status fqb_random_orthonormal(fqb_handle h, int64_t n, int r, uint64_t seed, uint32_t stream, double* q,
+                                  int64_t ldq);
+/* rsvd::gen_synthetic (synthetic.cpp:159-180) into device memory: kind 0 slow decay
+ * (1/j^2), 1 fast decay (e^{-j/20}), 2 block-diagonal V with d blocks; *rank_out = the
+ * kept rank (sigma < 1e-18 sigma_1 dropped). */
+fqb_status fqb_gen_synthetic(fqb_handle h, int kind, int n, int d, uint64_t seed, double* a, int64_t lda,
+                             int* rank_out);
+/* Rectangular low-rank-plus-noise inputs (BASELINE configs 2-5):
+ * A = U diag(sigma) V' + noise N(0,1)/sqrt(n), U m x r on stream 0xFA000001, V n x r on
+ * 0xFA000002, noise on 0xFA000003 keyed by column; sigma on the host. */
+fqb_status fqb_gen_lowrank(fqb_handle h, int64_t m, int64_t n, int r, const double* sigma, uint64_t seed,
+                           double noise, double* a, int64_t lda);
+
 /* ---- defaults (driver.cpp:449-466) ------------------------------------------- */
 double fqb_default_density(int kind, int64_t n);
 int fqb_default_block(int64_t m, int64_t n);

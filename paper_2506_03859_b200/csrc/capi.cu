@@ -523,6 +523,38 @@ fqb_status fqb_sliced_free(fqb_handle h, fqb_sliced sl) {
     });
 }
 
+fqb_status fqb_random_orthonormal(fqb_handle h, int64_t n, int r, uint64_t seed, uint32_t stream, double* q,
+                                  int64_t ldq) {
+    return guarded([&]() -> fqb_status {
+        bind(h);
+        if (!q) throw farqb::Error(FQB_ERR_INVALID_ARGUMENT, "null output");
+        if (ldq < n) throw farqb::Error(FQB_ERR_DIMENSION, "ldq < n");
+        farqb::random_orthonormal_dev(h->h, n, r, seed, stream, 0, q, ldq);
+        return FQB_OK;
+    });
+}
+
+fqb_status fqb_gen_synthetic(fqb_handle h, int kind, int n, int d, uint64_t seed, double* a, int64_t lda,
+                             int* rank_out) {
+    return guarded([&]() -> fqb_status {
+        bind(h);
+        if (!a) throw farqb::Error(FQB_ERR_INVALID_ARGUMENT, "null output");
+        const int r = farqb::gen_synthetic_dev(h->h, kind, n, d, seed, a, lda);
+        if (rank_out) *rank_out = r;
+        return FQB_OK;
+    });
+}
+
+fqb_status fqb_gen_lowrank(fqb_handle h, int64_t m, int64_t n, int r, const double* sigma, uint64_t seed,
+                           double noise, double* a, int64_t lda) {
+    return guarded([&]() -> fqb_status {
+        bind(h);
+        if (!a || !sigma) throw farqb::Error(FQB_ERR_INVALID_ARGUMENT, "null pointer");
+        farqb::gen_lowrank_dev(h->h, m, n, r, sigma, seed, noise, a, lda);
+        return FQB_OK;
+    });
+}
+
 double fqb_default_density(int kind, int64_t n) { return farqb::default_density(kind, n); }
 int fqb_default_block(int64_t m, int64_t n) { return farqb::default_block(m, n); }
 int fqb_default_max_iters(int64_t n, int b) { return farqb::default_max_iters(n, b); }

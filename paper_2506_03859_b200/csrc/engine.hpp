@@ -99,6 +99,12 @@ void assemble_svd(Handle& h, const double* q, int64_t ldq, const double* bt, int
                   int l, double* u, int64_t ldu, double* v, int64_t ldv, std::vector<double>& sigma,
                   std::vector<char>& flagged);
 void destroy_cusolver(Handle& h);
+// synthetic.cu: test matrices on the device (reference synthetic.cpp)
+void random_orthonormal_dev(Handle& h, int64_t n, int r, uint64_t seed, uint32_t stream, int first_col, double* q,
+                            int64_t ldq);
+int gen_synthetic_dev(Handle& h, int kind, int n, int d, uint64_t seed, double* a, int64_t lda);
+void gen_lowrank_dev(Handle& h, int64_t m, int64_t n, int r, const double* sigma, uint64_t seed, double noise,
+                     double* a, int64_t lda);
 // hostmem.cu: pinned, pooled host arrays for results returned on the host
 void* host_alloc(size_t bytes);
 void host_free(void* ptr);

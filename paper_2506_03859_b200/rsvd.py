@@ -613,6 +613,37 @@ class Engine:
             _raise(st, "fqb_relative_error")
         return out.value
 
+    # ---- test matrices on the device (reference synthetic.cpp) -------------------
+    def random_orthonormal(self, n: int, r: int, seed: int, stream: int = 0xFA000001):
+        """rsvd::random_orthonormal on the device -> torch float64 n x r (column-major)."""
+        import torch
+        q = torch.empty((r, n), dtype=torch.float64, device=f"cuda:{self.device}").t()
+        st = self._lib.fqb_random_orthonormal(self._h, n, r, seed, stream, q.data_ptr(), max(n, 1))
+        if st:
+            _raise(st, "fqb_random_orthonormal")
+        return q
+
+    def gen_synthetic(self, kind: int, n: int, seed: int, d: int = 1):
+        """rsvd::gen_synthetic on the device (kind 0 slow, 1 fast, 2 block-V) -> (A torch n x n, rank)."""
+        import torch
+        a = torch.empty((n, n), dtype=torch.float64, device=f"cuda:{self.device}").t()
+        r = C.c_int()
+        st = self._lib.fqb_gen_synthetic(self._h, int(kind), n, d, seed, a.data_ptr(), max(n, 1), C.byref(r))
+        if st:
+            _raise(st, "fqb_gen_synthetic")
+        return a, r.value
+
+    def gen_lowrank(self, m: int, n: int, sigma, seed: int, noise: float = 0.0):
+        """A = U diag(sigma) V' + noise N(0,1)/sqrt(n) on the device (BASELINE configs 2-5)."""
+        import torch
+        sig = np.ascontiguousarray(np.asarray(sigma, dtype=np.float64))
+        a = torch.empty((n, m), dtype=torch.float64, device=f"cuda:{self.device}").t()
+        st = self._lib.fqb_gen_lowrank(self._h, m, n, len(sig), sig.ctypes.data, seed, float(noise), a.data_ptr(),
+                                       max(m, 1))
+        if st:
+            _raise(st, "fqb_gen_lowrank")
+        return a
+
     def slice_operand(self, a_ptr, m, n, lda) -> "SlicedOperand":
         """Cut A (m x n, device, column-major) once into Ozaki slices (fqb_slice_operand)."""
         out = C.c_void_p()
