@@ -24,6 +24,13 @@
  *   fqb_relative_error      <- rsvd::relative_error (experiment.hpp, experiment.cpp:317-342)
  *   fqb_gemm                <- rsvd::kern::Ops::gemm_nn / gemm_tn (kernels.hpp:9-19)
  *   fqb_philox_u32          <- rsvd::Philox::next_u32 (rng.hpp:21-24)
+ *   fqb_random_orthonormal  <- rsvd::random_orthonormal (synthetic.hpp, synthetic.cpp:121-126)
+ *   fqb_gen_synthetic       <- rsvd::gen_synthetic (synthetic.hpp, synthetic.cpp:159-180)
+ *
+ * Beyond the reference: fqb_qb_*_f32 (FP32 input, BASELINE config 5), the INT8
+ * tensor-core FP64 emulation of the A passes (fqb_gemm_emulated, fqb_slice_operand /
+ * fqb_sliced_gemm), fqb_gen_lowrank (configs 2-5 inputs), row-sharded multi-GPU
+ * (fqb_comm_*).
  *
  * Conventions: matrices are column-major doubles with an explicit leading
  * dimension; sizes are int64_t; no C++ types cross this boundary and no
@@ -42,7 +49,7 @@
 extern "C" {
 #endif
 
-#define FARQB_ABI_VERSION 2
+#define FARQB_ABI_VERSION 3
 
 typedef enum fqb_status {
     FQB_OK = 0,

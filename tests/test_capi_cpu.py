@@ -29,7 +29,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version_and_defaults():
     L = _native.lib()
-    assert L.fqb_abi_version() == 2
+    assert L.fqb_abi_version() == 3
     # driver.cpp:449-466 heuristics, same numbers as test_driver.cpp:384-401
     assert L.fqb_default_block(100, 100) == 20
     assert L.fqb_default_block(3000, 3000) == 30
