@@ -38,3 +38,20 @@ for name, tr, M, N, K in shapes:
     e1.synchronize()
     us = e0.elapsed_time(e1) / 50 * 1e3
     print(f"{name:18s} {'TN' if tr else 'NN'} {M}x{N}x{K}: {us:6.1f} us  {2*M*N*K/us/1e6:6.2f} TF/s")
+
+print("--- cuBLAS (torch.matmul) on the same shapes ---")
+for name, tr, M, N, K in shapes:
+    a = torch.randn((K, M) if tr else (M, K), dtype=torch.float64, device="cuda")
+    bb = torch.randn((K, N), dtype=torch.float64, device="cuda")
+    op = (lambda: a.t() @ bb) if tr else (lambda: a @ bb)
+    for _ in range(5):
+        op()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(50):
+        op()
+    e1.record()
+    e1.synchronize()
+    us = e0.elapsed_time(e1) / 50 * 1e3
+    print(f"{name:18s} {'TN' if tr else 'NN'} {M}x{N}x{K}: {us:6.1f} us  {2*M*N*K/us/1e6:6.2f} TF/s")
