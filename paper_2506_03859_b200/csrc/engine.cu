@@ -304,7 +304,8 @@ class QbRun {
         const int64_t M = ta ? n_ : m_, K = ta ? m_ : n_;
         if (!oz_ready_) {
             oz_ready_ = true;
-            if (!prepare_ozaki()) {
+            // non-finite A: DMMA, whose Inf/NaN propagation is the reference's
+            if (!std::isfinite(norm_a_sq_) || !prepare_ozaki()) {
                 oz_on_ = false;
                 a_gemm(ta, N, B, ldb, C, ldc);
                 return;

@@ -84,8 +84,11 @@ __device__ __forceinline__ int64_t round_up_dev(int64_t x, int64_t r) { return (
 __device__ __forceinline__ double pow2i(int k) {   // k in [-1022, 1023]
     return __longlong_as_double(static_cast<long long>(k + 1023) << 52);
 }
+constexpr int kNonFiniteE = 1 << 20;   // line exponent of a line holding Inf/NaN
 __device__ __forceinline__ double mul_pow2(double x, int k) {
     if (k >= -1022 && k <= 1023) return x * pow2i(k);
+    // an output touching a non-finite input line is NaN (the digits are meaningless)
+    if (k > kNonFiniteE / 2) return __longlong_as_double(0x7FF8000000000000LL);
     const int k1 = max(-1022, min(1023, k / 2));
     const int k2 = max(-1022, min(1023, k - k1));
     return x * pow2i(k1) * pow2i(k2);
@@ -396,8 +399,11 @@ __device__ __forceinline__ unsigned abs_hi(double x) {
     return unsigned(static_cast<unsigned long long>(__double_as_longlong(x)) >> 32) & 0x7FFFFFFFu;
 }
 // e with 2^(e-1) <= max|x| < 2^e from the max high word.  All-zero lines and
-// subnormal maxima get e = -1021 (their digits are 0 or just coarser).
-__device__ __forceinline__ int exp_of_hi(unsigned hi) { return hi >= 0x00100000u ? int(hi >> 20) - 1022 : -1021; }
+// subnormal maxima get e = -1021 (their digits are 0 or just coarser); a line
+// holding Inf or NaN gets kNonFiniteE, which turns its outputs into NaN.
+__device__ __forceinline__ int exp_of_hi(unsigned hi) {
+    return hi >= 0x7FF00000u ? kNonFiniteE : hi >= 0x00100000u ? int(hi >> 20) - 1022 : -1021;
+}
 
 // the 8 digits of x in line scale e, as raw fields d_p + 64 in [0, 128]: the 7-bit
 // fields of U = R + sum_p 64 2^(49-7p), read from its two 32-bit halves

@@ -84,6 +84,37 @@ def test_emulated_gemm_wild_scales_and_zero_lines(eng):
     _check_rows(got, a.t(), b, c0, 1.0, 0.0, np.arange(0, m, 7))
 
 
+@pytest.mark.parametrize("bad", [float("nan"), float("inf"), -float("inf")])
+def test_emulated_gemm_non_finite_lines_give_nan(eng, bad):
+    """An Inf/NaN in a row of op(A) or a column of B makes that row / column of C NaN (its
+    digits are meaningless); every other element keeps the FP64 bar."""
+    m, n, k = 260, 20, 300
+    g = torch.Generator(device="cpu").manual_seed(11)
+    a = torch.randn((k, m), dtype=torch.float64, generator=g)
+    b = torch.randn((k, n), dtype=torch.float64, generator=g)
+    a[17, 200] = bad        # row 200 of op(A) = A^T
+    b[5, 4] = bad           # column 4 of B
+    c0 = torch.zeros((m, n), dtype=torch.float64)
+    got = _run_emulated(eng, True, a, b, c0, 1.0, 0.0)
+    assert torch.isnan(got[200, :]).all() and torch.isnan(got[:, 4]).all()
+    keep_r = np.array([r for r in range(0, m, 9) if r != 200])
+    keep_c = [j for j in range(n) if j != 4]
+    _check_rows(got[:, keep_c], a.t(), b[:, keep_c], c0[:, keep_c], 1.0, 0.0, keep_r)
+
+
+def test_qb_non_finite_input_propagates(eng, monkeypatch):
+    """Non-finite A: the engine stays on DMMA (the reference's Inf/NaN behaviour); no garbage result."""
+    monkeypatch.setenv("FQB_OZAKI", "1")
+    a = _lowrank(400, 300, 1.0 / np.arange(1, 41), seed=3)
+    a[10, 20] = np.nan
+    cfg = FarpcaConfig(eps=1e-2, power=1, block=20, sketch=SketchSpec(0, 0.0, 1), relative=True, max_iters=3)
+    try:
+        res = eng.run_fixed_precision(a, cfg, output="host")
+    except fqb.RsvdError:
+        return   # an error status (e.g. degenerate / tolerance) is acceptable
+    assert not res.converged or not np.isfinite(res.residual_sq)
+
+
 def test_emulated_gemm_is_deterministic(eng):
     m, n, k = 4000, 50, 6000
     g = torch.Generator(device="cpu").manual_seed(9)
