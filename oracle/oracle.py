@@ -153,6 +153,15 @@ class Oracle:
                                          C.POINTER(Result)]
             L.ref_gen_synthetic.argtypes = [C.c_int, C.c_int, C.c_uint64, C.c_void_p]
             L.ref_random_orthonormal.argtypes = [C.c_int, C.c_int, C.c_uint64, C.c_uint32, C.c_void_p]
+            L.ref_load_matrix.argtypes = [C.c_char_p, C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                          C.POINTER(C.POINTER(C.c_double)), C.c_char_p, C.c_int,
+                                          C.POINTER(C.c_longlong)]
+            L.ref_save_matrix.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_char_p, C.c_char_p, C.c_char_p,
+                                          C.c_int]
+            L.ref_free.argtypes = [C.c_void_p]
+            L.ref_run_experiment.argtypes = [C.c_char_p, C.c_char_p, C.c_int]
+            L.ref_check_experiment_config.argtypes = [C.c_char_p, C.c_char_p, C.c_int]
+            L.ref_read_report_csv.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.POINTER(C.c_longlong)]
         else:
             L.fqo_gemm_nn.argtypes = [C.c_int] * 3 + [C.c_void_p, C.c_int, C.c_void_p, C.c_int,
                                                       C.c_void_p, C.c_int]
@@ -284,6 +293,47 @@ class Oracle:
         if rc != 0:
             raise ValueError("random_orthonormal failed")
         return out
+
+
+    # ---- matrix files / experiment driver (reference only) -------------------------
+    # Errors come back as (status, message, offset): status 1 FormatError, 2 ConfigError,
+    # 3 DimensionError, 4 other (ref_shim.cpp).
+    def load_matrix(self, path, fmt):
+        rows, cols, off = C.c_int(), C.c_int(), C.c_longlong(-1)
+        data = C.POINTER(C.c_double)()
+        err = C.create_string_buffer(512)
+        st = self.lib.ref_load_matrix(os.fsencode(path), fmt.encode(), C.byref(rows), C.byref(cols),
+                                      C.byref(data), err, 512, C.byref(off))
+        if st:
+            return None, (st, err.value.decode(), off.value)
+        try:
+            n = rows.value * cols.value
+            flat = np.ctypeslib.as_array(data, shape=(max(n, 1),))[:n].copy()
+        finally:
+            self.lib.ref_free(data)
+        return np.asfortranarray(flat.reshape((cols.value, rows.value)).T), None
+
+    def save_matrix(self, a, path, fmt):
+        a = np.asfortranarray(a, dtype=np.float64)
+        err = C.create_string_buffer(512)
+        st = self.lib.ref_save_matrix(a.ctypes.data, a.shape[0], a.shape[1], os.fsencode(path), fmt.encode(),
+                                      err, 512)
+        return None if st == 0 else (st, err.value.decode())
+
+    def run_experiment(self, config_path):
+        err = C.create_string_buffer(512)
+        st = self.lib.ref_run_experiment(os.fsencode(config_path), err, 512)
+        return None if st == 0 else (st, err.value.decode())
+
+    def check_experiment_config(self, config_path):
+        err = C.create_string_buffer(512)
+        st = self.lib.ref_check_experiment_config(os.fsencode(config_path), err, 512)
+        return None if st == 0 else (st, err.value.decode())
+
+    def read_report_csv(self, path):
+        err, off = C.create_string_buffer(512), C.c_longlong(-1)
+        n = self.lib.ref_read_report_csv(os.fsencode(path), err, 512, C.byref(off))
+        return (n, None) if n >= 0 else (None, (-n, err.value.decode(), off.value))
 
 
 def _block_to_arrays(blk: Block) -> SketchArrays:

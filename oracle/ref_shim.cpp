@@ -22,6 +22,8 @@
 
 #include "rsvd/driver.hpp"
 #include "rsvd/errors.hpp"
+#include "rsvd/experiment.hpp"
+#include "rsvd/matrix_io.hpp"
 #include "rsvd/matrix_core.hpp"
 #include "rsvd/rng.hpp"
 #include "rsvd/sketch.hpp"
@@ -380,6 +382,80 @@ int ref_random_orthonormal(int n, int r, uint64_t seed, uint32_t stream, double*
         return FQO_OK;
     } catch (const std::exception&) {
         return FQO_ERR_CONFIG;
+    }
+}
+
+// ---- matrix files and the experiment driver (callers of the path) -----------
+// Status: 0 ok, 1 FormatError (offset set), 2 ConfigError, 3 DimensionError,
+// 4 other; message into err.
+
+static int io_status(const std::exception& e, char* err, int errlen, long long* offset) {
+    if (err && errlen > 0) std::snprintf(err, size_t(errlen), "%s", e.what());
+    if (auto* f = dynamic_cast<const FormatError*>(&e)) {
+        if (offset) *offset = (long long)f->byte_offset;
+        return 1;
+    }
+    if (dynamic_cast<const ConfigError*>(&e)) return 2;
+    if (dynamic_cast<const DimensionError*>(&e)) return 3;
+    return 4;
+}
+
+// load_matrix (matrix_io.cpp); *data is malloc'ed (free with ref_free).
+int ref_load_matrix(const char* path, const char* format, int* rows, int* cols, double** data, char* err,
+                    int errlen, long long* offset) {
+    try {
+        DenseMatrix a = load_matrix(path, matrix_format_from_name(format));
+        *rows = a.rows;
+        *cols = a.cols;
+        *data = static_cast<double*>(std::malloc(sizeof(double) * (a.data.size() ? a.data.size() : 1)));
+        if (!a.data.empty()) std::memcpy(*data, a.data.data(), sizeof(double) * a.data.size());
+        return 0;
+    } catch (const std::exception& e) {
+        return io_status(e, err, errlen, offset);
+    }
+}
+
+int ref_save_matrix(const double* data, int rows, int cols, const char* path, const char* format, char* err,
+                    int errlen) {
+    try {
+        DenseMatrix a(rows, cols);
+        if (!a.data.empty()) std::memcpy(a.data.data(), data, sizeof(double) * a.data.size());
+        save_matrix(a, path, matrix_format_from_name(format));
+        return 0;
+    } catch (const std::exception& e) {
+        return io_status(e, err, errlen, nullptr);
+    }
+}
+
+void ref_free(void* p) { std::free(p); }
+
+// load_experiment_config + run_experiment (experiment.cpp): the reference's own
+// experiment grid on this host, files under the config's out_prefix.
+int ref_run_experiment(const char* config_path, char* err, int errlen) {
+    try {
+        run_experiment(load_experiment_config(config_path));
+        return 0;
+    } catch (const std::exception& e) {
+        return io_status(e, err, errlen, nullptr);
+    }
+}
+
+// load_experiment_config alone (validation errors)
+int ref_check_experiment_config(const char* config_path, char* err, int errlen) {
+    try {
+        load_experiment_config(config_path);
+        return 0;
+    } catch (const std::exception& e) {
+        return io_status(e, err, errlen, nullptr);
+    }
+}
+
+// read_report_csv: record count (>= 0) or -status
+int ref_read_report_csv(const char* path, char* err, int errlen, long long* offset) {
+    try {
+        return int(read_report_csv(path).size());
+    } catch (const std::exception& e) {
+        return -io_status(e, err, errlen, offset);
     }
 }
 

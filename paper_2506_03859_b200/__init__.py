@@ -14,6 +14,9 @@ from .rsvd import (  # noqa: F401
     relative_error, run_fixed_precision, run_fixed_rank, sketch_kind_from_name, sketch_kind_name, truncate_to_tolerance)
 
 from . import dist  # noqa: F401,E402  (row-sharded multi-GPU helpers)
-from .matrix_io import FormatError, dumps_raw, load_raw, loads_raw, save_raw  # noqa: F401,E402
+from .matrix_io import (  # noqa: F401,E402
+    FormatError, dumps_mm, dumps_ppm, dumps_raw, load_matrix, load_raw, loads_mm, loads_ppm, loads_raw,
+    matrix_format_from_name, matrix_format_name, save_matrix, save_raw)
 
 __all__ = [n for n in dir() if not n.startswith("_")]
+from . import experiment  # noqa: F401,E402

@@ -40,3 +40,121 @@ def test_loader_rejects_malformed_input(mutate, offset):
         fqb.loads_raw(mutate(raw))
     if offset is not None:
         assert e.value.offset == offset
+
+
+# ---- MatrixMarket array / PPM, pinned against the reference's own loader and writer ----------
+MM = b"%%MatrixMarket matrix array real general\n"
+MM_CASES = {
+    "plain": MM + b"2 3\n1\n2\n3\n4\n5\n6\n",
+    "comments_case_crlf": b"%%MatrixMarket MATRIX Array real GENERAL\r\n% c1\r\n2 2\r\n1.5 % inline\r\n-2e3\r\n.5\r\n7.\r\n",
+    "hex_inf_nan": MM + b"1 4\n0x1.8p1\ninf\n-Infinity\nnan\n",
+    "empty": MM + b"0 5\n",
+    "glued_size": MM + b"2 1.5\n3\n",
+    "zeros": MM + b"1 3\n0e5\n-0.000\n0x0p0\n",
+    "subnormal": MM + b"1 1\n1e-310\n",
+    "underflow": MM + b"1 1\n1e-400\n",
+    "overflow": MM + b"1 2\n1\n1e400\n",
+    "no_banner": b"%%MatrixMarkex matrix array real general\n1 1\n1\n",
+    "coordinate": b"%%MatrixMarket matrix coordinate real general\n1 1\n1\n",
+    "missing_rows": MM,
+    "bad_dims": MM + b"abc 2\n",
+    "negative_dim": MM + b"-1 2\n",
+    "huge_dim": MM + b"3000000000 1\n",
+    "too_few": MM + b"2 2\n1\n2\n3\n",
+    "trailing": MM + b"1 1\n1\n2\n",
+    "garbage_entry": MM + b"2 1\n1\nx\n",
+    "underscore": MM + b"2 1\n1_0\n",
+    "exp_no_digits": MM + b"1 2\n1e\n",
+    "nan_payload": MM + b"1 1\nnan(0x1)\n",
+}
+
+
+def _ppm(w, h, maxval, pix, head=None):
+    return (head if head is not None else b"P6\n%d %d\n%d\n" % (w, h, maxval)) + pix
+
+
+_rng = np.random.default_rng(3)
+PPM_CASES = {
+    "8bit": _ppm(3, 2, 255, _rng.integers(0, 256, 18, dtype=np.uint8).tobytes()),
+    "8bit_maxval_100_comment": _ppm(2, 2, 100, bytes(range(12)), b"P6 # hdr\n2 2 # size\n100\n"),
+    "16bit": _ppm(2, 1, 1000, np.array([0, 1, 999, 1000, 500, 7], dtype=">u2").tobytes()),
+    "not_p6": b"P3\n1 1\n255\n" + b"\0" * 3,
+    "no_width": b"P6\n",
+    "zero_width": _ppm(0, 1, 255, b""),
+    "maxval_big": _ppm(1, 1, 70000, b"\0" * 6),
+    "no_separator": b"P6 1 1 255",
+    "truncated": _ppm(2, 2, 255, b"\0" * 11),
+    "trailing": _ppm(1, 1, 255, b"\0" * 4),
+    "height_overflow": b"P6\n1 999999999\n255\n",
+    "digits_overflow": b"P6\n99999999999 1\n255\n",
+}
+
+
+def _ours(buf, fmt):
+    try:
+        return (fqb.loads_mm if fmt == "mm" else fqb.loads_ppm)(buf), None
+    except fqb.FormatError as e:
+        return None, (1, e.msg, e.offset)
+
+
+@pytest.mark.parametrize("case", sorted(MM_CASES))
+def test_matrix_market_loader_matches_reference(reference, tmp_path, case):
+    _compare_loader(reference, tmp_path, MM_CASES[case], "mm")
+
+
+@pytest.mark.parametrize("case", sorted(PPM_CASES))
+def test_ppm_loader_matches_reference(reference, tmp_path, case):
+    _compare_loader(reference, tmp_path, PPM_CASES[case], "ppm")
+
+
+def _compare_loader(reference, tmp_path, buf, fmt):
+    p = tmp_path / ("m." + fmt)
+    p.write_bytes(buf)
+    ref, ref_err = reference.load_matrix(p, fmt)
+    got, err = _ours(buf, fmt)
+    assert err == ref_err
+    if ref is not None:
+        assert got.shape == ref.shape and got.flags.f_contiguous
+        assert np.array_equal(got.view(np.uint64), ref.view(np.uint64)) or \
+            np.array_equal(np.isnan(got), np.isnan(ref)) and np.array_equal(got[~np.isnan(got)], ref[~np.isnan(ref)])
+
+
+@pytest.mark.parametrize("fmt", ["mm", "raw", "ppm"])
+def test_writers_match_reference_bytes(reference, tmp_path, fmt):
+    if fmt == "ppm":
+        a = np.array([[0.5, 254.5, -3.0], [300.0, np.nan, 2.4999999999999996], [1.5, 0.49999999999999994, 17.0],
+                      [255.0, 128.25, 99.5], [3.5, 4.5, 5.5], [0.0, 1.0, 2.0]])
+    else:
+        a = np.array([[np.pi, -0.0, 1e-300], [1.0 / 3.0, np.inf, 12345678901234567.0]])
+    ours, theirs = tmp_path / "o", tmp_path / "t"
+    fqb.save_matrix(a, ours, fmt)
+    assert reference.save_matrix(a, theirs, fmt) is None
+    assert ours.read_bytes() == theirs.read_bytes()
+
+
+def test_ppm_save_rejects_bad_rows():
+    with pytest.raises(fqb.DimensionError):
+        fqb.dumps_ppm(np.zeros((4, 2)))
+
+
+def test_matrix_market_round_trip_large():
+    a = np.random.default_rng(1).standard_normal((300, 40))
+    b = fqb.loads_mm(fqb.dumps_mm(a))
+    assert np.array_equal(a, b)
+
+
+def test_format_names():
+    assert fqb.matrix_format_from_name("MTX") == "matrixmarket"
+    assert fqb.matrix_format_from_name("RawF64") == "rawf64"
+    with pytest.raises(fqb.ConfigError):
+        fqb.matrix_format_from_name("csv")
+
+
+def test_raw_payload_size_overflow_matches_reference(reference, tmp_path):
+    buf = b"SKLR" + struct.pack("<III", 2**31 - 1, 2**31 - 1, 0)
+    p = tmp_path / "big.raw"
+    p.write_bytes(buf)
+    _, ref_err = reference.load_matrix(p, "raw")
+    with pytest.raises(fqb.FormatError) as e:
+        fqb.loads_raw(buf)
+    assert (1, e.value.msg, e.value.offset) == ref_err
