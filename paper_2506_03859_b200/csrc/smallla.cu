@@ -15,6 +15,7 @@
 //  launch_eigsvd_scale: eigSVD tail (matrix_core.cpp:193-215).
 #include <cstdint>
 #include <cstdlib>
+#include <utility>
 
 #include "kernels.hpp"
 
@@ -135,11 +136,62 @@ __global__ void __launch_bounds__(1024) k_chol_inv(const double* __restrict__ S,
 }
 
 // Register-resident variant for b <= 128: thread t owns column c = t % b and
-// rows rg, rg + 8, rg + 16, ... (rg = t / b), held in registers.  At step j the
-// owners of row j publish it to shared memory (by symmetry of the trailing
-// Schur complement it is also pivot column j), one barrier, then every thread
-// updates its rows: M[i][c] -= (M[j][i] / d) M[j][c]  (c != j),  M[i][j] = -f.
-// The published rows are double buffered, so each step costs one barrier.
+// rows rg, rg + 8, rg + 16, ... (rg = t / b), held in registers (slot s = row
+// rg + 8 s).  At step j the owners of row j publish it to shared memory (by
+// symmetry of the trailing Schur complement it is also pivot column j), one
+// barrier, then every thread updates its rows: M[i][c] -= (M[j][i] / d) M[j][c]
+// (c != j), M[i][j] = -f.  The published rows are double buffered, so a step
+// costs one barrier.
+//
+// Steps run in groups of 8 (j = 8Q .. 8Q+7) instantiated per Q: in group Q the
+// pivot row lives in slot Q and every slot below Q is finished, so the slot range
+// is a compile-time constant -- no per-slot predicates, no jump table for the
+// publication, the loads of a step issued together -- and the pivot column's
+// "store -f" is folded into the FMA (v keep + (-f) pc with keep = 0, pc = 1
+// there).  b = 50: 34.8 -> 18.3 us per call, b = 100: 125 -> 86 us
+// (tools/microbench/chol_bench.cu); a two-columns-per-thread form was slower.
+template <int MAXS, int Q>
+__device__ __forceinline__ bool chol_group(double (&v)[MAXS], int b, double thresh, int rg, int c, bool active,
+                                           double (*prow)[kSmemMaxB]) {
+#pragma unroll 1
+    for (int r = 0; r < 8; ++r) {
+        const int j = 8 * Q + r;
+        if (j >= b) return true;
+        double* pr = prow[j & 1];
+        if (active && rg == r) pr[c] = v[Q];
+#ifdef FQB_CHOL_PROBE
+        if (threadIdx.x == FQB_CHOL_PROBE) chol_probe_stamp(2 * j);
+#endif
+        __syncthreads();
+#ifdef FQB_CHOL_PROBE
+        if (threadIdx.x == FQB_CHOL_PROBE) chol_probe_stamp(2 * j + 1);
+#endif
+        const double d = pr[j];
+        if (!(d > thresh)) return false;   // uniform: every thread reads the same pivot
+        double pv[MAXS - Q];
+#pragma unroll
+        for (int s = Q; s < MAXS; ++s) pv[s - Q] = pr[min(rg + 8 * s, b - 1)];
+        const bool piv = c == j;
+        const double pc = piv ? 1.0 : pr[c];
+        const double keep = piv ? 0.0 : 1.0;
+        const double invd = 1.0 / d;
+#pragma unroll
+        for (int s = Q; s < MAXS; ++s) {
+            const double nv = fma(-(pv[s - Q] * invd), pc, v[s] * keep);
+            // slots past row b - 1 collect garbage that is never published or stored
+            if (s == Q) v[s] = rg > r ? nv : v[s];
+            else v[s] = nv;
+        }
+    }
+    return true;
+}
+
+template <int MAXS, int... Qs>
+__device__ __forceinline__ bool chol_groups(double (&v)[MAXS], int b, double thresh, int rg, int c, bool active,
+                                            double (*prow)[kSmemMaxB], std::integer_sequence<int, Qs...>) {
+    return (chol_group<MAXS, Qs>(v, b, thresh, rg, c, active, prow) && ...);
+}
+
 template <int MAXS>
 __global__ void __launch_bounds__(1024) k_chol_inv_reg(const double* __restrict__ S, int b, int64_t lds,
                                                        double tol, double diag_ref,
@@ -151,7 +203,7 @@ __global__ void __launch_bounds__(1024) k_chol_inv_reg(const double* __restrict_
     extern __shared__ double smem[];        // final M, b x (b+1), row-major
     __shared__ double prow[2][kSmemMaxB];
     __shared__ double red[32];
-    __shared__ double sd[kSmemMaxB];
+    __shared__ double isd[kSmemMaxB];
     constexpr int RG = 8;
     const int tid = threadIdx.x, nt = blockDim.x;
     const int c = tid % b, rg = tid / b;
@@ -174,35 +226,8 @@ __global__ void __launch_bounds__(1024) k_chol_inv_reg(const double* __restrict_
     const double thresh = tol * max_diag;
     if (tid == 0 && max_diag_out) *max_diag_out = max_diag;
 
-    bool failed = false;
-    for (int j = 0; j < b; ++j) {
-        double* pr = prow[j & 1];
-        if (active && rg == (j % RG)) {
-            const int sj = j / RG;
-#pragma unroll
-            for (int s = 0; s < MAXS; ++s)
-                if (s == sj) pr[c] = v[s];
-        }
-        __syncthreads();
-        const double d = pr[j];
-        if (!(d > thresh)) {
-            failed = true;
-            break;
-        }
-        const double invd = 1.0 / d;
-        const double pc = pr[c];
-        if (active) {
-#pragma unroll
-            for (int s = 0; s < MAXS; ++s) {
-                const int i = rg + s * RG;
-                if (i > j && i < b) {
-                    const double f = pr[i] * invd;
-                    v[s] = c == j ? -f : fma(-f, pc, v[s]);
-                }
-            }
-        }
-    }
-    if (failed) {
+    const bool ok = chol_groups<MAXS>(v, b, thresh, rg, c, active, prow, std::make_integer_sequence<int, MAXS>{});
+    if (!ok) {
         if (tid == 0) atomicOr(status, fail_bit);
         for (int e = tid; e < b * b; e += nt) {
             const int r = e % b, cc = e / b;
@@ -220,12 +245,13 @@ __global__ void __launch_bounds__(1024) k_chol_inv_reg(const double* __restrict_
         }
     }
     __syncthreads();
-    for (int i = tid; i < b; i += nt) sd[i] = sqrt(smem[i * ld + i]);
+    for (int i = tid; i < b; i += nt) isd[i] = 1.0 / sqrt(smem[i * ld + i]);
     __syncthreads();
+    // R[r, c] = U[r][c] / sqrt(d_r) (c >= r);  Rinv[k, j] = M[j][k] / sqrt(d_j) (k < j)
     for (int e = tid; e < b * b; e += nt) {
-        const int r = e % b, cc = e / b;
-        R[e] = cc >= r ? smem[r * ld + cc] / sd[r] : 0.0;
-        Rinv[e] = r < cc ? smem[cc * ld + r] / sd[cc] : (r == cc ? 1.0 / sd[cc] : 0.0);
+        const int cc = e / b, r = e - cc * b;
+        R[e] = cc >= r ? smem[r * ld + cc] * isd[r] : 0.0;
+        Rinv[e] = r < cc ? smem[cc * ld + r] * isd[cc] : (r == cc ? isd[cc] : 0.0);
     }
 }
 

@@ -5,10 +5,18 @@
 #include <cstdlib>
 #include <vector>
 
+#ifdef FQB_CHOL_PROBE
+__device__ long long g_stamps[512];
+__device__ __forceinline__ void chol_probe_stamp(int k) { g_stamps[k] = clock64(); }
+#endif
 #include "smallla.cu"
 
+namespace farqb {
+bool pdl_enabled() { return false; }   // engine.cu owns the real switch
+}
+
 int main(int argc, char** argv) {
-    const int b = argc > 1 ? std::atoi(argv[1]) : 50;
+  for (int b : {16, 32, 50, 64, 100, 128}) {
     const int reps = 200;
     std::vector<double> h(size_t(b) * b), w(size_t(b) * 4 * b);
     srand(1);
@@ -63,5 +71,13 @@ int main(int argc, char** argv) {
     cudaMemcpy(&hst, st, sizeof(unsigned), cudaMemcpyDeviceToHost);
     printf("b=%d: %.2f us per factorization  |R'R-S|=%.2e |R Ri - I|=%.2e status=%u  (%s)\n", b, 1e3 * ms / reps,
            e1max, e2max, hst, cudaGetErrorString(cudaGetLastError()));
+#ifdef FQB_CHOL_PROBE
+    long long hs[512];
+    cudaMemcpyFromSymbol(hs, g_stamps, sizeof hs);
+    double work = 0, wait = 0;
+    for (int j = 1; j < b; ++j) { work += hs[2 * j] - hs[2 * j - 1]; wait += hs[2 * j + 1] - hs[2 * j]; }
+    printf("   thread %d: per step %.0f cycles of work, %.0f cycles at the barrier\n", FQB_CHOL_PROBE, work / (b - 1), wait / (b - 1));
+#endif
+  }
     return 0;
 }
