@@ -491,13 +491,22 @@ __global__ void __launch_bounds__(256) k_slice_a(const T* __restrict__ a, int64_
     __shared__ double t[64][65];   // t[j][i]
     const int64_t i0 = int64_t(blockIdx.x) * 64, j0 = int64_t(blockIdx.y) * 64;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int jj = warp; jj < 64; jj += 8) {
-        const int64_t j = j0 + jj;
+    // all 16 loads of a thread in flight before the first shared store (a rolled
+    // loop here left the kernel latency-bound at ~50% of HBM)
+    double x[8][2];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const int64_t j = j0 + warp + 8 * k;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const int64_t i = i0 + lane + 32 * h;
-            t[jj][lane + 32 * h] = (i < m && j < n) ? double(a[j * ld + i]) : 0.0;
+            x[k][h] = (i < m && j < n) ? double(__ldcs(a + j * ld + i)) : 0.0;
         }
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) t[warp + 8 * k][lane + 32 * h] = x[k][h];
     }
     __syncthreads();
     const int line = threadIdx.x >> 2, q = threadIdx.x & 3;   // 64 lines x 4 chunks of 16
