@@ -170,8 +170,18 @@ class QbRun {
     // --- setup: ||A||^2 and (StdBernoulli) the centering column -----------------
     void setup() {
         FQB_CUDA(cudaMemsetAsync(scal_, 0, kScalarCount * sizeof(double), s_));
-        if (af_) launch_sumsq(af_, m_, n_, lda_, h_.ws.partial.ptr, scal_ + kNormA, s_, h_.lc);
-        else launch_sumsq(a_, m_, n_, lda_, h_.ws.partial.ptr, scal_ + kNormA, s_, h_.lc);
+        // With the emulation on, A is sliced now and ||A||^2 comes out of the
+        // slicing's line-max pass (one read of A fewer)
+        bool norm_done = false;
+        if (oz_on_) {
+            oz_ready_ = true;
+            norm_done = prepare_ozaki(scal_ + kNormA);
+            if (!norm_done) oz_on_ = false;
+        }
+        if (!norm_done) {
+            if (af_) launch_sumsq(af_, m_, n_, lda_, h_.ws.partial.ptr, scal_ + kNormA, s_, h_.lc);
+            else launch_sumsq(a_, m_, n_, lda_, h_.ws.partial.ptr, scal_ + kNormA, s_, h_.lc);
+        }
         comm_allreduce_sum(h_, scal_ + kNormA, 1, s_);
         // z = A (p 1_n) exists when the reference would build it (driver.cpp:364-365);
         // it is only computed once a sparse centered block actually needs it.
@@ -179,6 +189,8 @@ class QbRun {
         FQB_CUDA(cudaMemcpyAsync(h_.host_scalars, scal_ + kNormA, sizeof(double), cudaMemcpyDeviceToHost, s_));
         FQB_CUDA(cudaStreamSynchronize(s_));
         norm_a_sq_ = h_.host_scalars[0];
+        // non-finite A: DMMA, whose Inf/NaN propagation is the reference's
+        if (oz_on_ && !std::isfinite(norm_a_sq_)) oz_on_ = false;
     }
 
     double norm_a_sq() const { return norm_a_sq_; }
@@ -260,7 +272,7 @@ class QbRun {
 
     // Slice A once per run into the handle's buffers; false (and DMMA from then on)
     // when the two slice layouts do not fit in device memory.
-    bool prepare_ozaki() {
+    bool prepare_ozaki(double* norm_out = nullptr) {
         Workspace& w = h_.ws;
         try {
             w.oz_x_nn.ensure(size_t(ozaki_x_bytes(m_, n_)), s_);
@@ -274,12 +286,14 @@ class QbRun {
         w.oz_e_nn.ensure(size_t(m_), s_);
         w.oz_e_tn.ensure(size_t(n_), s_);
         w.oz_line_max.ensure(size_t(ozaki_line_max_words(m_, n_)), s_);
+        if (norm_out) w.oz_norm_partial.ensure(size_t(std::max<int64_t>(1, ozaki_norm_partials(m_, n_))), s_);
+        double* np = norm_out ? w.oz_norm_partial.ptr : nullptr;
         if (af_)
             ozaki_slice_a(af_, m_, n_, lda_, w.oz_line_max.ptr, w.oz_x_tn.ptr, w.oz_e_tn.ptr, w.oz_x_nn.ptr,
-                          w.oz_e_nn.ptr, s_, h_.lc);
+                          w.oz_e_nn.ptr, s_, h_.lc, np, norm_out);
         else
             ozaki_slice_a(a_, m_, n_, lda_, w.oz_line_max.ptr, w.oz_x_tn.ptr, w.oz_e_tn.ptr, w.oz_x_nn.ptr,
-                          w.oz_e_nn.ptr, s_, h_.lc);
+                          w.oz_e_nn.ptr, s_, h_.lc, np, norm_out);
         return true;
     }
 
@@ -304,8 +318,7 @@ class QbRun {
         const int64_t M = ta ? n_ : m_, K = ta ? m_ : n_;
         if (!oz_ready_) {
             oz_ready_ = true;
-            // non-finite A: DMMA, whose Inf/NaN propagation is the reference's
-            if (!std::isfinite(norm_a_sq_) || !prepare_ozaki()) {
+            if (!prepare_ozaki()) {
                 oz_on_ = false;
                 a_gemm(ta, N, B, ldb, C, ldc);
                 return;

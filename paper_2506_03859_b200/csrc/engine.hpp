@@ -49,7 +49,7 @@ struct DeviceArray {
 // Per-handle reusable workspace (everything except the Q and B' outputs).
 struct Workspace {
     DeviceArray<double> omega, y0, ys, wp, wraw, g, t, cd, c2, small, zc, rowsum_b, splitk, partial,
-        scalars, scratch, a_copy;
+        scalars, scratch, a_copy, oz_norm_partial;
     DeviceArray<float> a_copy_f32;   // FP32 input mode staging
     DeviceArray<int> col_ptr, row_idx, counts;
     DeviceArray<double> values;
@@ -64,7 +64,7 @@ struct Workspace {
     // every member, while the stream the frees are ordered on still exists
     void release_all() {
         for (auto* d : {&omega, &y0, &ys, &wp, &wraw, &g, &t, &cd, &c2, &small, &zc, &rowsum_b, &splitk, &partial,
-                        &scalars, &scratch, &a_copy, &values})
+                        &scalars, &scratch, &a_copy, &values, &oz_norm_partial})
             d->release();
         for (auto* d : {&col_ptr, &row_idx, &counts, &oz_e_nn, &oz_e_tn, &oz_ez}) d->release();
         for (auto* d : {&status, &gemm_flags, &oz_line_max}) d->release();

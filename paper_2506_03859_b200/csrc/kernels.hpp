@@ -124,12 +124,16 @@ int64_t ozaki_workspace_doubles(int num_sms);
 // Slices of A (m x n, ld) in both layouts from one pass (either may be null):
 //   x_tn / e_tn: operand rows = columns of A, K = m   (A' Y)
 //   x_nn / e_nn: operand rows = rows of A,    K = n   (A G)
-// line_max: ozaki_line_max_words(m, n) words of scratch.
+// line_max: ozaki_line_max_words(m, n) words of scratch.  With norm_out, ||A||_F^2
+// comes out of the same read of A (norm_partial: ozaki_norm_partials(m, n) doubles).
 int64_t ozaki_line_max_words(int64_t m, int64_t n);
+int64_t ozaki_norm_partials(int64_t m, int64_t n);
 void ozaki_slice_a(const double* a, int64_t m, int64_t n, int64_t ld, unsigned* line_max, int8_t* x_tn, int* e_tn,
-                   int8_t* x_nn, int* e_nn, cudaStream_t s, LaunchCounter& lc);
+                   int8_t* x_nn, int* e_nn, cudaStream_t s, LaunchCounter& lc, double* norm_partial = nullptr,
+                   double* norm_out = nullptr);
 void ozaki_slice_a(const float* a, int64_t m, int64_t n, int64_t ld, unsigned* line_max, int8_t* x_tn, int* e_tn,
-                   int8_t* x_nn, int* e_nn, cudaStream_t s, LaunchCounter& lc);
+                   int8_t* x_nn, int* e_nn, cudaStream_t s, LaunchCounter& lc, double* norm_partial = nullptr,
+                   double* norm_out = nullptr);
 // Z (k x n, ld)
 void ozaki_slice_z(const double* b, int64_t k, int64_t n, int64_t ld, int* e, int8_t* out, cudaStream_t s,
                    LaunchCounter& lc);

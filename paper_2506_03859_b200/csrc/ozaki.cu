@@ -449,31 +449,67 @@ __device__ __forceinline__ void put_chunk16(const double (&v)[16], int e, int8_t
 }
 
 // Row and column maxima (high words) of A (m x n, ld) in one pass; rmax / cmax
-// must be zeroed.  CTA: 256 rows x 128 columns, a thread walks one row.
+// must be zeroed.  CTA: 256 rows x 128 columns, a thread walks one row.  With
+// norm_partial it also writes the CTA's sum of squares (||A||_F^2, reduced by
+// ozaki_slice_a in CTA order), so the engine does not read A a third time.
 template <typename T>   // double, or float A (FP32 input mode: widened exactly)
 __global__ void __launch_bounds__(256) k_line_max(const T* __restrict__ a, int64_t m, int64_t n, int64_t ld,
-                                                  unsigned* rmax, unsigned* cmax) {
+                                                  unsigned* rmax, unsigned* cmax, double* norm_partial) {
     FQB_PDL_ENTRY();
     __shared__ unsigned cm[8][128];
+    __shared__ double red[8];
     const int64_t i = int64_t(blockIdx.x) * 256 + threadIdx.x;
     const int64_t j0 = int64_t(blockIdx.y) * 128;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     unsigned rm = 0;
+    double sq[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll 4
     for (int c = 0; c < 128; ++c) {
         const int64_t j = j0 + c;
-        const unsigned h = (i < m && j < n) ? abs_hi(double(a[j * ld + i])) : 0u;
+        const double x = (i < m && j < n) ? double(a[j * ld + i]) : 0.0;
+        const unsigned h = abs_hi(x);
+        sq[c & 3] = fma(x, x, sq[c & 3]);
         rm = max(rm, h);
         const unsigned wm = __reduce_max_sync(0xFFFFFFFFu, h);
         if (lane == 0) cm[warp][c] = wm;
     }
     if (i < m && rm) atomicMax(rmax + i, rm);
+    if (norm_partial) {
+        double t = (sq[0] + sq[1]) + (sq[2] + sq[3]);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) t += __shfl_down_sync(0xFFFFFFFFu, t, off);
+        if (lane == 0) red[warp] = t;
+    }
     __syncthreads();
+    if (norm_partial && threadIdx.x == 0) {
+        double t = 0.0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) t += red[w];
+        norm_partial[int64_t(blockIdx.y) * gridDim.x + blockIdx.x] = t;
+    }
     if (threadIdx.x < 128 && j0 + threadIdx.x < n) {
         unsigned v = 0;
 #pragma unroll
         for (int w = 0; w < 8; ++w) v = max(v, cm[w][threadIdx.x]);
         if (v) atomicMax(cmax + j0 + threadIdx.x, v);
+    }
+}
+
+// Sum of the per-CTA partials in index order (one CTA; deterministic)
+__global__ void __launch_bounds__(1024) k_sum_ordered(const double* __restrict__ partial, int64_t count,
+                                                      double* out) {
+    FQB_PDL_ENTRY();
+    __shared__ double red[32];
+    double t = 0.0;
+    for (int64_t k = threadIdx.x; k < count; k += blockDim.x) t += partial[k];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) t += __shfl_down_sync(0xFFFFFFFFu, t, off);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = t;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double u = 0.0;
+        for (int w = 0; w < int(blockDim.x >> 5); ++w) u += red[w];
+        *out = u;
     }
 }
 
@@ -625,16 +661,27 @@ int64_t ozaki_x_bytes(int64_t rows, int64_t k) { return ceil_div(rows, OZ_BM) * 
 int64_t ozaki_z_bytes(int64_t n, int64_t k) { return ceil_div(k, OZ_BK) * S * int64_t(ozaki_bn(n)) * OZ_BK; }
 
 int64_t ozaki_line_max_words(int64_t m, int64_t n) { return m + n; }
+int64_t ozaki_norm_partials(int64_t m, int64_t n) { return ceil_div(m, 256) * ceil_div(n, 128); }
 
 template <typename T>
 static void slice_a_impl(const T* a, int64_t m, int64_t n, int64_t ld, unsigned* line_max, int8_t* x_tn, int* e_tn,
-                         int8_t* x_nn, int* e_nn, cudaStream_t s, LaunchCounter& lc) {
-    if (m <= 0 || n <= 0) return;
+                         int8_t* x_nn, int* e_nn, double* norm_partial, double* norm_out, cudaStream_t s,
+                         LaunchCounter& lc) {
+    if (m <= 0 || n <= 0) {
+        if (norm_out) FQB_CUDA(cudaMemsetAsync(norm_out, 0, sizeof(double), s));
+        return;
+    }
     unsigned* rmax = line_max;
     unsigned* cmax = line_max + m;
     FQB_CUDA(cudaMemsetAsync(line_max, 0, sizeof(unsigned) * size_t(m + n), s));
-    launch_k(k_line_max<T>, dim3(unsigned(ceil_div(m, 256)), unsigned(ceil_div(n, 128))), 256, 0, s, a, m, n, ld, rmax, cmax);
+    launch_k(k_line_max<T>, dim3(unsigned(ceil_div(m, 256)), unsigned(ceil_div(n, 128))), 256, 0, s, a, m, n, ld, rmax,
+             cmax, norm_out ? norm_partial : nullptr);
     FQB_LAUNCHED();
+    if (norm_out) {
+        launch_k(k_sum_ordered, 1, 1024, 0, s, norm_partial, ozaki_norm_partials(m, n), norm_out);
+        FQB_LAUNCHED();
+        lc.bump();
+    }
     // cover the padded operand rows of both layouts (multiples of OZ_BM)
     const dim3 g(unsigned(ceil_div(m, OZ_BM) * (OZ_BM / 64)), unsigned(ceil_div(n, OZ_BM) * (OZ_BM / 64)));
     launch_k(k_slice_a<T>, g, 256, 0, s, a, m, n, ld, rmax, cmax, x_tn, e_tn, x_nn, e_nn);
@@ -643,12 +690,14 @@ static void slice_a_impl(const T* a, int64_t m, int64_t n, int64_t ld, unsigned*
 }
 
 void ozaki_slice_a(const double* a, int64_t m, int64_t n, int64_t ld, unsigned* line_max, int8_t* x_tn, int* e_tn,
-                   int8_t* x_nn, int* e_nn, cudaStream_t s, LaunchCounter& lc) {
-    slice_a_impl(a, m, n, ld, line_max, x_tn, e_tn, x_nn, e_nn, s, lc);
+                   int8_t* x_nn, int* e_nn, cudaStream_t s, LaunchCounter& lc, double* norm_partial,
+                   double* norm_out) {
+    slice_a_impl(a, m, n, ld, line_max, x_tn, e_tn, x_nn, e_nn, norm_partial, norm_out, s, lc);
 }
 void ozaki_slice_a(const float* a, int64_t m, int64_t n, int64_t ld, unsigned* line_max, int8_t* x_tn, int* e_tn,
-                   int8_t* x_nn, int* e_nn, cudaStream_t s, LaunchCounter& lc) {
-    slice_a_impl(a, m, n, ld, line_max, x_tn, e_tn, x_nn, e_nn, s, lc);
+                   int8_t* x_nn, int* e_nn, cudaStream_t s, LaunchCounter& lc, double* norm_partial,
+                   double* norm_out) {
+    slice_a_impl(a, m, n, ld, line_max, x_tn, e_tn, x_nn, e_nn, norm_partial, norm_out, s, lc);
 }
 
 void ozaki_slice_z(const double* b, int64_t k, int64_t n, int64_t ld, int* e, int8_t* out, cudaStream_t s,
