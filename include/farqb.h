@@ -22,6 +22,8 @@
  *   fqb_centering_column    <- rsvd::centering_column (driver.hpp:78, driver.cpp:178-183)
  *   fqb_frob_norm_sq        <- rsvd::frob_norm_sq (matrix_core.hpp:59, matrix_core.cpp:46-48)
  *   fqb_relative_error      <- rsvd::relative_error (experiment.hpp, experiment.cpp:317-342)
+ *   fqb_sym_eig             <- rsvd::sym_eig (matrix_core.hpp, matrix_core.cpp:50-115) as used by
+ *                              assemble_svd (driver.cpp:296-345) for the l x l Gram matrices
  *   fqb_gemm                <- rsvd::kern::Ops::gemm_nn / gemm_tn (kernels.hpp:9-19)
  *   fqb_philox_u32          <- rsvd::Philox::next_u32 (rng.hpp:21-24)
  *   fqb_random_orthonormal  <- rsvd::random_orthonormal (synthetic.hpp, synthetic.cpp:121-126)
@@ -247,6 +249,14 @@ fqb_status fqb_centering_column(fqb_handle h, const double* a, int64_t m, int64_
 /* ||A||_F^2 into *host_out */
 fqb_status fqb_frob_norm_sq(fqb_handle h, const double* a, int64_t m, int64_t n, int64_t lda,
                             double* host_out);
+/* Symmetric eigendecomposition (device pointers; both triangles of A read):
+ * eigenvalues ascending into w (n), eigenvectors into V (n x n, ldv).  The solver of
+ * the SVD assembly: cuSOLVER syevd by default; with FQB_EIG=small and n <= 224 a
+ * tridiagonal bisection / inverse-iteration solver verified a posteriori (residual
+ * and orthogonality at 64 n u, syevd when the check fails).  *used_small (nullable)
+ * = 1 when the latter produced the result. */
+fqb_status fqb_sym_eig(fqb_handle h, const double* a, int n, int64_t lda, double* w, double* v, int64_t ldv,
+                       int* used_small);
 /* Exact relative error ||A - U diag(sigma) V'||_F / ||A||_F (experiment.cpp:317-342),
  * one pass over A in column strips on the device.  U is m x r (ldu), V is n x r (ldv);
  * sigma (host, r values) may be NULL for a QB pair (U = Q, V = B').  A and the factors

@@ -396,6 +396,29 @@ fqb_status fqb_frob_norm_sq(fqb_handle h, const double* a, int64_t m, int64_t n,
     });
 }
 
+fqb_status fqb_sym_eig(fqb_handle h, const double* a, int n, int64_t lda, double* w, double* v, int64_t ldv,
+                       int* used_small) {
+    return guarded([&]() -> fqb_status {
+        bind(h);
+        if (!a || !w || !v) throw farqb::Error(FQB_ERR_INVALID_ARGUMENT, "null pointer");
+        if (n < 0) throw farqb::Error(FQB_ERR_DIMENSION, "negative dimension");
+        if (n > 0 && (lda < n || ldv < n)) throw farqb::Error(FQB_ERR_DIMENSION, "leading dimension below n");
+        if (used_small) *used_small = 0;
+        if (n == 0) return FQB_OK;
+        cudaStream_t s = h->h.stream;
+        farqb::DeviceArray<double> mat;
+        mat.ensure(size_t(n) * n, s);
+        FQB_CUDA(cudaMemcpy2DAsync(mat.ptr, sizeof(double) * n, a, sizeof(double) * lda, sizeof(double) * n, n,
+                                   cudaMemcpyDeviceToDevice, s));
+        const bool small = farqb::eigh_inplace(h->h, mat.ptr, n, w);
+        FQB_CUDA(cudaMemcpy2DAsync(v, sizeof(double) * ldv, mat.ptr, sizeof(double) * n, sizeof(double) * n, n,
+                                   cudaMemcpyDeviceToDevice, s));
+        FQB_CUDA(cudaStreamSynchronize(s));
+        if (used_small) *used_small = small ? 1 : 0;
+        return FQB_OK;
+    });
+}
+
 fqb_status fqb_relative_error(fqb_handle h, const double* a, int64_t m, int64_t n, int64_t lda, int a_on_device,
                               const double* u, int64_t ldu, const double* sigma, const double* v, int64_t ldv,
                               int r, int factors_on_device, double* host_out) {

@@ -799,12 +799,20 @@ int run_qb(Handle& h, const void* a, bool a_f32, int64_t m, int64_t n, int64_t l
             out->v_flagged[i] = flg[drop + i];
         }
         if (svd_r > 0 && (flags & FQB_OUT_DEVICE)) {
-            // the kept columns are the last svd_r (ascending order): move them to the front
+            // the kept columns are the last svd_r (ascending order): into fresh buffers
+            // (source and destination would overlap in place -- undefined for memcpy)
             if (drop > 0) {
-                FQB_CUDA(cudaMemcpyAsync(u_dev.ptr, u_dev.ptr + int64_t(drop) * run.ldq(),
+                DeviceArray<double> uk, vk;
+                uk.ensure(size_t(run.ldq()) * svd_r, s);
+                vk.ensure(size_t(run.ldbt()) * svd_r, s);
+                FQB_CUDA(cudaMemcpyAsync(uk.ptr, u_dev.ptr + int64_t(drop) * run.ldq(),
                                          sizeof(double) * run.ldq() * svd_r, cudaMemcpyDeviceToDevice, s));
-                FQB_CUDA(cudaMemcpyAsync(v_dev.ptr, v_dev.ptr + int64_t(drop) * run.ldbt(),
+                FQB_CUDA(cudaMemcpyAsync(vk.ptr, v_dev.ptr + int64_t(drop) * run.ldbt(),
                                          sizeof(double) * run.ldbt() * svd_r, cudaMemcpyDeviceToDevice, s));
+                u_dev.release();
+                v_dev.release();
+                u_dev.ptr = uk.detach();
+                v_dev.ptr = vk.detach();
             }
             out->u = u_dev.detach();
             out->v = v_dev.detach();

@@ -95,6 +95,7 @@ struct Handle {
 };
 
 // svd.cu: U = Q U~, V = Bt U~ Sigma^-1 from eig(B B'); sigma ascending
+bool eigh_inplace(Handle& h, double* mat, int l, double* w);
 void assemble_svd(Handle& h, const double* q, int64_t ldq, const double* bt, int64_t ldbt, int64_t m, int64_t n,
                   int l, double* u, int64_t ldu, double* v, int64_t ldv, std::vector<double>& sigma,
                   std::vector<char>& flagged);

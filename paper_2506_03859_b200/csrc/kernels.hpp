@@ -160,6 +160,14 @@ void launch_chol_upper_inv(const double* S, int b, int64_t lds, double tol, doub
 // eigenvalues (ascending) of a b x b symmetric matrix (cyclic Jacobi,
 // matrix_core.cpp:50-115) and optionally eigenvectors (ld = b).
 // vtmp: b x b doubles of scratch when vectors are wanted.
+// eigsmall.cu: symmetric eigensolver for the SVD assembly's l x l matrix, l <= kSmallEighMax.
+// mat: full symmetric n x n (col-major, ld n, left intact); eigenvalues ascending into w,
+// eigenvectors into x (n x n, ld n).  false when its a-posteriori residual /
+// orthogonality check fails -- the caller then uses cuSOLVER.  Synchronizes s.
+constexpr int kSmallEighMax = 224;
+int64_t small_eigh_scratch_doubles(int n);
+bool small_eigh(const double* mat, int n, double* w, double* x, double* scratch, GemmWorkspace& gws, int num_sms,
+                cudaStream_t s, LaunchCounter& lc);
 void launch_sym_eig(const double* S, int b, int64_t lds, double* values, double* vectors,
                     double* vtmp, unsigned* status, unsigned fail_bit, cudaStream_t s,
                     LaunchCounter& lc);

@@ -185,13 +185,24 @@ double relative_error(Handle& h, const double* a, int64_t m, int64_t n, int64_t 
     return std::sqrt(err_sq / norm_sq);
 }
 
-void assemble_svd(Handle& h, const double* q, int64_t ldq, const double* bt, int64_t ldbt, int64_t m, int64_t n,
-                  int l, double* u, int64_t ldu, double* v, int64_t ldv, std::vector<double>& sigma,
-                  std::vector<char>& flagged) {
-    sigma.assign(l, 0.0);
-    flagged.assign(l, 0);
-    if (l == 0) return;
+// Symmetric eigendecomposition of mat (l x l, ld l, both triangles) in place:
+// eigenvalues ascending into w, eigenvectors into mat.  FQB_EIG: unset / "syevd" =
+// cuSOLVER syevd (measured fastest at l = 200: 1.9 ms), "syevj" = cuSOLVER Jacobi,
+// "small" = the l <= kSmallEighMax solver of eigsmall.cu (its own residual /
+// orthogonality check falls back to syevd; 2.0 ms at l = 200).
+// Returns true when the small-l solver produced the result.
+bool eigh_inplace(Handle& h, double* mat, int l, double* w) {
     cudaStream_t s = h.stream;
+    ensure_gemm_workspace(h);
+    const char* env = std::getenv("FQB_EIG");
+    const int eig_mode = !env ? 1 : std::string(env) == "syevj" ? 2 : std::string(env) == "small" ? 0 : 1;
+    if (eig_mode == 0 && l <= kSmallEighMax) {
+        DeviceArray<double> es;
+        es.ensure(size_t(small_eigh_scratch_doubles(l)), s);
+        const bool ok = small_eigh(mat, l, w, mat, es.ptr, h.gws, h.num_sms, s, h.lc);
+        FQB_CUDA(cudaStreamSynchronize(s));   // es is released on scope exit
+        if (ok) return true;
+    }
     CusolverApi& api = cusolver();
     if (!h.cusolver) {
         cusolverDnHandle_t ch = nullptr;
@@ -200,21 +211,11 @@ void assemble_svd(Handle& h, const double* q, int64_t ldq, const double* bt, int
     }
     auto ch = static_cast<cusolverDnHandle_t>(h.cusolver);
     cs_check(api.set_stream(ch, s), "cusolverDnSetStream");
-    ensure_gemm_workspace(h);
-
-    DeviceArray<double> mat, w, work, scale, us;
+    DeviceArray<double> work;
     DeviceArray<int> info;
-    mat.ensure(size_t(l) * l, s);
-    w.ensure(size_t(l), s);
     info.ensure(1, s);
-    // B B' = Bt' Bt  (l x l)
-    gemm(true, l, l, n, 1.0, bt, ldbt, bt, ldbt, 0.0, mat.ptr, l, h.gws, h.num_sms, s, h.lc);
     int lwork = 0;
-    static const bool use_syevj = [] {
-        const char* e = std::getenv("FQB_EIG");
-        return e && std::string(e) == "syevj";  // measured: syevd 2.1 ms, syevj 3.3 ms at l = 200
-    }();
-    if (use_syevj) {
+    if (eig_mode == 2) {   // measured: syevd 2.1 ms, syevj 3.3 ms at l = 200
         // GPU-resident Jacobi (no host round trips), converged to working precision
         static syevjInfo_t params = nullptr;
         if (!params) {
@@ -222,27 +223,44 @@ void assemble_svd(Handle& h, const double* q, int64_t ldq, const double* bt, int
             cs_check(api.syevj_tol(params, 0.0), "cusolverDnXsyevjSetTolerance");   // 0 = machine precision
             cs_check(api.syevj_sweeps(params, 100), "cusolverDnXsyevjSetMaxSweeps");
         }
-        cs_check(api.syevj_buffer(ch, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, l, mat.ptr, l, w.ptr, &lwork,
-                                  params),
+        cs_check(api.syevj_buffer(ch, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, l, mat, l, w, &lwork, params),
                  "cusolverDnDsyevj_bufferSize");
         work.ensure(size_t(std::max(lwork, 1)), s);
-        cs_check(api.syevj(ch, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, l, mat.ptr, l, w.ptr, work.ptr,
-                           lwork, info.ptr, params),
+        cs_check(api.syevj(ch, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, l, mat, l, w, work.ptr, lwork,
+                           info.ptr, params),
                  "cusolverDnDsyevj");
     } else {
-        cs_check(api.syevd_buffer(ch, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, l, mat.ptr, l, w.ptr, &lwork),
+        cs_check(api.syevd_buffer(ch, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, l, mat, l, w, &lwork),
                  "cusolverDnDsyevd_bufferSize");
         work.ensure(size_t(std::max(lwork, 1)), s);
-        cs_check(api.syevd(ch, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, l, mat.ptr, l, w.ptr, work.ptr,
-                           lwork, info.ptr),
+        cs_check(api.syevd(ch, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, l, mat, l, w, work.ptr, lwork,
+                           info.ptr),
                  "cusolverDnDsyevd");
     }
-    std::vector<double> lam(l);
     int hinfo = 0;
-    FQB_CUDA(cudaMemcpyAsync(lam.data(), w.ptr, sizeof(double) * l, cudaMemcpyDeviceToHost, s));
     FQB_CUDA(cudaMemcpyAsync(&hinfo, info.ptr, sizeof(int), cudaMemcpyDeviceToHost, s));
     FQB_CUDA(cudaStreamSynchronize(s));
     if (hinfo != 0) throw Error(kStatusConvergence, "syevd did not converge (info " + std::to_string(hinfo) + ")");
+    return false;
+}
+
+void assemble_svd(Handle& h, const double* q, int64_t ldq, const double* bt, int64_t ldbt, int64_t m, int64_t n,
+                  int l, double* u, int64_t ldu, double* v, int64_t ldv, std::vector<double>& sigma,
+                  std::vector<char>& flagged) {
+    sigma.assign(l, 0.0);
+    flagged.assign(l, 0);
+    if (l == 0) return;
+    cudaStream_t s = h.stream;
+    ensure_gemm_workspace(h);
+    DeviceArray<double> mat, w, scale, us;
+    mat.ensure(size_t(l) * l, s);
+    w.ensure(size_t(l), s);
+    // B B' = Bt' Bt  (l x l)
+    gemm(true, l, l, n, 1.0, bt, ldbt, bt, ldbt, 0.0, mat.ptr, l, h.gws, h.num_sms, s, h.lc);
+    eigh_inplace(h, mat.ptr, l, w.ptr);
+    std::vector<double> lam(l);
+    FQB_CUDA(cudaMemcpyAsync(lam.data(), w.ptr, sizeof(double) * l, cudaMemcpyDeviceToHost, s));
+    FQB_CUDA(cudaStreamSynchronize(s));
     std::vector<double> inv(l);
     for (int j = 0; j < l; ++j) sigma[j] = std::sqrt(std::max(lam[j], 0.0));
     const double smax = sigma[l - 1];

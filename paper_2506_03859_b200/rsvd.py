@@ -613,6 +613,22 @@ class Engine:
             _raise(st, "fqb_relative_error")
         return out.value
 
+    def sym_eig(self, a):
+        """Symmetric eigendecomposition on the device (fqb_sym_eig, the SVD assembly's solver):
+        a torch float64 n x n (CUDA) -> (w ascending, V) as torch tensors, and whether the
+        small-l solver (rather than cuSOLVER) produced them."""
+        import torch
+        n = int(a.shape[0])
+        ac = a.t().contiguous().t() if a.stride(0) != 1 else a
+        w = torch.empty(n, dtype=torch.float64, device=a.device)
+        v = torch.empty((n, n), dtype=torch.float64, device=a.device).t()
+        used = C.c_int(0)
+        st = self._lib.fqb_sym_eig(self._h, ac.data_ptr(), n, max(n, 1) if n <= 1 else ac.stride(1), w.data_ptr(),
+                                   v.data_ptr(), max(n, 1), C.byref(used))
+        if st:
+            _raise(st, "fqb_sym_eig")
+        return w, v, bool(used.value)
+
     # ---- test matrices on the device (reference synthetic.cpp) -------------------
     def random_orthonormal(self, n: int, r: int, seed: int, stream: int = 0xFA000001):
         """rsvd::random_orthonormal on the device -> torch float64 n x r (column-major)."""
