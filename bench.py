@@ -3,9 +3,10 @@
 
 Workload (BASELINE.json configs[1], the metric's single-GPU config "C2"):
   A = U diag(sigma) V', 8000 x 8000 FP64, sigma_i = 10^(-i/50) (i = 1..900; smaller
-  values drop below 1e-18 sigma_1 as in synthetic.cpp:21), U, V from QR of seeded
-  N(0,1) matrices (synthetic stand-in, torch.Generator seed 42);
-  standardized-Bernoulli Omega (p = 1/2), b = 50, P = 2, eps = 1e-3 relative.
+  values drop below 1e-18 sigma_1 as in synthetic.cpp:21), U, V = random_orthonormal
+  (8000, 900, seed 42) on the reference's factor streams, generated on the device by
+  fqb_gen_lowrank (make_matrix); standardized-Bernoulli Omega (p = 1/2), b = 50, P = 2,
+  eps = 1e-3 relative.
 
 One step = one full run_fixed_precision to eps (rank 200, 4 blocks) through the
 engine -- the blocked QB loop plus the assembly of U, sigma, V, exactly what the
@@ -400,7 +401,9 @@ def run_reference(args):
         if i == 0 and args.warmup > 0:
             continue
     v = statistics.mean(times)
-    line = {"metric": "farPCA time-to-eps (s)", "value": v, "unit": "s", "n_gpus": 0,
+    # n_gpus echoes the launch (--gpus N) so the line pairs with our arm's; the work itself
+    # runs on host cores (cpu_baseline.cores)
+    line = {"metric": "farPCA time-to-eps (s)", "value": v, "unit": "s", "n_gpus": args.gpus,
             "steps": len(times), "warmup": min(args.warmup, 1), "ms_per_step": v * 1000,
             "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (same A as the ours arm)", "impl": "reference",
