@@ -86,6 +86,20 @@ __global__ void k_scale_cols(const double* src, int64_t lds, const double* scale
     if (i < rows && c < cols) dst[int64_t(c) * ldd + i] = src[int64_t(c) * lds + i] * scale[c];
 }
 
+// sigma = sqrt(max(lambda, 0)) (ascending), the pseudo-inverse scale and the flags of
+// assemble_svd (sigma <= 1e-14 sigma_max: v column zeroed and flagged), one CTA
+__global__ void k_sigma(const double* __restrict__ lam, int l, double* sigma, double* inv, char* flagged) {
+    FQB_PDL_ENTRY();
+    const double smax = sqrt(fmax(lam[l - 1], 0.0));
+    for (int j = threadIdx.x; j < l; j += blockDim.x) {
+        const double sg = sqrt(fmax(lam[j], 0.0));
+        const bool keep = sg > 1e-14 * smax;
+        sigma[j] = sg;
+        inv[j] = keep ? 1.0 / sg : 0.0;
+        flagged[j] = keep ? 0 : 1;
+    }
+}
+
 // T (r x w, ld r) = (V[s:s+w, :] diag(sigma))'   (sigma null: unscaled)
 __global__ void k_strip_t(const double* v, int64_t ldv, const double* sigma, int r, int64_t s, int w, double* t) {
     FQB_PDL_ENTRY();
@@ -191,7 +205,9 @@ double relative_error(Handle& h, const double* a, int64_t m, int64_t n, int64_t 
 // "small" = the l <= kSmallEighMax solver of eigsmall.cu (its own residual /
 // orthogonality check falls back to syevd; 2.0 ms at l = 200).
 // Returns true when the small-l solver produced the result.
-bool eigh_inplace(Handle& h, double* mat, int l, double* w) {
+// info_dev != null: cuSOLVER's status goes there and nothing is synchronized (the
+// caller checks it); null: checked here.
+static bool eigh_core(Handle& h, double* mat, int l, double* w, int* info_dev) {
     cudaStream_t s = h.stream;
     ensure_gemm_workspace(h);
     const char* env = std::getenv("FQB_EIG");
@@ -214,6 +230,7 @@ bool eigh_inplace(Handle& h, double* mat, int l, double* w) {
     DeviceArray<double> work;
     DeviceArray<int> info;
     info.ensure(1, s);
+    int* info_ptr = info_dev ? info_dev : info.ptr;
     int lwork = 0;
     if (eig_mode == 2) {   // measured: syevd 2.1 ms, syevj 3.3 ms at l = 200
         // GPU-resident Jacobi (no host round trips), converged to working precision
@@ -227,22 +244,25 @@ bool eigh_inplace(Handle& h, double* mat, int l, double* w) {
                  "cusolverDnDsyevj_bufferSize");
         work.ensure(size_t(std::max(lwork, 1)), s);
         cs_check(api.syevj(ch, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, l, mat, l, w, work.ptr, lwork,
-                           info.ptr, params),
+                           info_ptr, params),
                  "cusolverDnDsyevj");
     } else {
         cs_check(api.syevd_buffer(ch, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, l, mat, l, w, &lwork),
                  "cusolverDnDsyevd_bufferSize");
         work.ensure(size_t(std::max(lwork, 1)), s);
         cs_check(api.syevd(ch, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, l, mat, l, w, work.ptr, lwork,
-                           info.ptr),
+                           info_ptr),
                  "cusolverDnDsyevd");
     }
+    if (info_dev) return false;   // work / info are released stream-ordered
     int hinfo = 0;
     FQB_CUDA(cudaMemcpyAsync(&hinfo, info.ptr, sizeof(int), cudaMemcpyDeviceToHost, s));
     FQB_CUDA(cudaStreamSynchronize(s));
     if (hinfo != 0) throw Error(kStatusConvergence, "syevd did not converge (info " + std::to_string(hinfo) + ")");
     return false;
 }
+
+bool eigh_inplace(Handle& h, double* mat, int l, double* w) { return eigh_core(h, mat, l, w, nullptr); }
 
 void assemble_svd(Handle& h, const double* q, int64_t ldq, const double* bt, int64_t ldbt, int64_t m, int64_t n,
                   int l, double* u, int64_t ldu, double* v, int64_t ldv, std::vector<double>& sigma,
@@ -257,32 +277,32 @@ void assemble_svd(Handle& h, const double* q, int64_t ldq, const double* bt, int
     w.ensure(size_t(l), s);
     // B B' = Bt' Bt  (l x l)
     gemm(true, l, l, n, 1.0, bt, ldbt, bt, ldbt, 0.0, mat.ptr, l, h.gws, h.num_sms, s, h.lc);
-    eigh_inplace(h, mat.ptr, l, w.ptr);
-    std::vector<double> lam(l);
-    FQB_CUDA(cudaMemcpyAsync(lam.data(), w.ptr, sizeof(double) * l, cudaMemcpyDeviceToHost, s));
-    FQB_CUDA(cudaStreamSynchronize(s));
-    std::vector<double> inv(l);
-    for (int j = 0; j < l; ++j) sigma[j] = std::sqrt(std::max(lam[j], 0.0));
-    const double smax = sigma[l - 1];
-    for (int j = 0; j < l; ++j) {
-        if (sigma[j] > 1e-14 * smax) {
-            inv[j] = 1.0 / sigma[j];
-        } else {
-            inv[j] = 0.0;  // pseudo-inverse convention, v column zeroed and flagged
-            flagged[j] = 1;
-        }
-    }
-    scale.ensure(size_t(l), s);
+    // eigendecomposition, sigma / flags / pseudo-inverse scale and both GEMMs are queued
+    // without a host round trip; the one synchronization at the end also brings back
+    // sigma, the flags and cuSOLVER's status
+    DeviceArray<int> info;
+    DeviceArray<char> flg;
+    info.ensure(1, s);
+    FQB_CUDA(cudaMemsetAsync(info.ptr, 0, sizeof(int), s));
+    eigh_core(h, mat.ptr, l, w.ptr, info.ptr);
+    scale.ensure(size_t(2) * l, s);   // [sigma | 1/sigma]
+    flg.ensure(size_t(l), s);
     us.ensure(size_t(l) * l, s);
-    FQB_CUDA(cudaMemcpyAsync(scale.ptr, inv.data(), sizeof(double) * l, cudaMemcpyHostToDevice, s));
-    dim3 grid(unsigned(ceil_div(l, 256)), unsigned(l));
-    launch_k(k_scale_cols, grid, 256, 0, s, mat.ptr, l, scale.ptr, l, l, us.ptr, l);
+    launch_k(k_sigma, 1, 256, 0, s, w.ptr, l, scale.ptr, scale.ptr + l, flg.ptr);
     FQB_LAUNCHED();
-    h.lc.bump();
+    dim3 grid(unsigned(ceil_div(l, 256)), unsigned(l));
+    launch_k(k_scale_cols, grid, 256, 0, s, mat.ptr, l, scale.ptr + l, l, l, us.ptr, l);
+    FQB_LAUNCHED();
+    h.lc.bump(2);
     // U = Q U~ (this rank's rows), V = Bt (U~ Sigma^-1)
     gemm(false, m, l, l, 1.0, q, ldq, mat.ptr, l, 0.0, u, ldu, h.gws, h.num_sms, s, h.lc);
     gemm(false, n, l, l, 1.0, bt, ldbt, us.ptr, l, 0.0, v, ldv, h.gws, h.num_sms, s, h.lc);
+    int hinfo = 0;
+    FQB_CUDA(cudaMemcpyAsync(sigma.data(), scale.ptr, sizeof(double) * l, cudaMemcpyDeviceToHost, s));
+    FQB_CUDA(cudaMemcpyAsync(flagged.data(), flg.ptr, size_t(l), cudaMemcpyDeviceToHost, s));
+    FQB_CUDA(cudaMemcpyAsync(&hinfo, info.ptr, sizeof(int), cudaMemcpyDeviceToHost, s));
     FQB_CUDA(cudaStreamSynchronize(s));  // the temporaries above are released on return
+    if (hinfo != 0) throw Error(kStatusConvergence, "syevd did not converge (info " + std::to_string(hinfo) + ")");
 }
 
 void destroy_cusolver(Handle& h) {

@@ -53,12 +53,18 @@ for ev in prof.events():
         rt[ev.name][0] += 1
         rt[ev.name][1] += ev.cpu_time_total
     elif ev.device_type == torch.autograd.DeviceType.CUDA:
-        kern.append((ev.time_range.start, ev.time_range.end))
+        nm = ev.name
+        for junk in ("void ", "farqb::", "(anonymous namespace)::", "<unnamed>::"):
+            nm = nm.replace(junk, "")
+        kern.append((ev.time_range.start, ev.time_range.end, nm.split("(")[0][:50]))
 print("host CUDA runtime calls per run:")
 for k, (c, us) in sorted(rt.items(), key=lambda x: -x[1][1])[:8]:
     print(f"  {us / args.runs:9.1f} us  {c // args.runs:5d}x  {k}")
 kern.sort()
-gaps = [b[0] - a[1] for a, b in zip(kern, kern[1:]) if b[0] > a[1]]
-gaps.sort(reverse=True)
+gl = [(b[0] - a[1], a[2], b[2]) for a, b in zip(kern, kern[1:]) if b[0] > a[1]]
+gaps = sorted((g[0] for g in gl), reverse=True)
 print(f"GPU idle between kernels per run: {sum(gaps) / args.runs:.1f} us over {len(gaps) // args.runs} gaps; "
-      f"largest {[round(g, 1) for g in gaps[:8]]}")
+      f"largest {[round(g, 1) for g in gaps[:8]]}  (includes the gaps between runs)")
+print("largest gaps (after -> before):")
+for g, a_, b_ in sorted(gl, reverse=True)[:14]:
+    print(f"  {g:8.1f} us  {a_}  ->  {b_}")

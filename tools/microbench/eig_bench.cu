@@ -84,6 +84,17 @@ int main() {
             CK(cusolverDnXsyevBatched(h, params, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, CUDA_R_64F, A, n,
                                       CUDA_R_64F, W, CUDA_R_64F, work, dbytes, hbuf.data(), hbytes, info, 1));
         });
+        size_t xd = 0, xh = 0;
+        CK(cusolverDnXsyevd_bufferSize(h, params, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, CUDA_R_64F, A, n,
+                                       CUDA_R_64F, W, CUDA_R_64F, &xd, &xh));
+        double* xwork;
+        cudaMalloc(&xwork, std::max<size_t>(xd, 8));
+        std::vector<char> xhb(xh + 1);
+        timeit("Xsyevd", [&] {
+            CK(cusolverDnXsyevd(h, params, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, CUDA_R_64F, A, n,
+                                CUDA_R_64F, W, CUDA_R_64F, xwork, xd, xhb.data(), xh, info));
+        });
+        timeit("Dsyevd UPPER", [&] { CK(cusolverDnDsyevd(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_UPPER, n, A, n, W, work, lw, info)); });
         timeit("Dsyevj tol 1e-14", [&] { CK(cusolverDnDsyevj(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, A, n, W, work, lw2, info, sj)); });
         timeit("Dsytrd only", [&] { CK(cusolverDnDsytrd(h, CUBLAS_FILL_MODE_LOWER, n, A, n, d_, e_, tau, work, lw3, info)); });
         cudaFree(A); cudaFree(A0); cudaFree(W); cudaFree(work); cudaFree(d_); cudaFree(e_); cudaFree(tau);
