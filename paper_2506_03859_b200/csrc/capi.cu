@@ -123,6 +123,8 @@ fqb_status fqb_destroy(fqb_handle h) {
         cudaEventDestroy(h->h.ev1);
         if (h->h.copy_stream) cudaStreamDestroy(h->h.copy_stream);
         if (h->h.ev_qb) cudaEventDestroy(h->h.ev_qb);
+        if (h->h.ev_u) cudaEventDestroy(h->h.ev_u);
+        if (h->h.ev_v) cudaEventDestroy(h->h.ev_v);
         cudaStreamDestroy(h->h.own_stream);
         delete h;
         return FQB_OK;

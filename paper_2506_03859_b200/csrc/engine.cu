@@ -727,11 +727,13 @@ int run_qb(Handle& h, const void* a, bool a_f32, int64_t m, int64_t n, int64_t l
     struct HostGuard {   // returns the blocks to the pool if the assembly below throws
         double** a;
         double** b;
+        cudaStream_t* copies;   // drained first: async copies may still target the blocks
         ~HostGuard() {
+            if ((*a || *b) && *copies) cudaStreamSynchronize(*copies);
             if (*a) host_free(*a);
             if (*b) host_free(*b);
         }
-    } host_guard{&host_q, &host_bt};
+    } host_guard{&host_q, &host_bt, &h.copy_stream};
     const bool host_out = l_qb > 0 && !(flags & FQB_OUT_DEVICE) && (flags & FQB_OUT_HOST);
     if (host_out) {
         host_q = static_cast<double*>(host_alloc(sizeof(double) * size_t(m) * l_qb));
@@ -757,14 +759,31 @@ int run_qb(Handle& h, const void* a, bool a_f32, int64_t m, int64_t n, int64_t l
     int svd_r = 0, drop = 0;
     double svd_res = run.residual();
     const int l_final = run.rank();
+    // host U / V (FQB_OUT_HOST): allocated up front and filled on the copy stream
+    // while the rest of the assembly runs
+    double *host_u = nullptr, *host_v = nullptr;
+    HostGuard uv_guard{&host_u, &host_v, &h.copy_stream};
+    bool uv_to_host = false;
     if ((flags & FQB_OUT_SVD) && status != kStatusDegenerate && l_final > 0) {
         u_dev.ensure(size_t(run.ldq()) * l_final, s);
         v_dev.ensure(size_t(run.ldbt()) * l_final, s);
-        assemble_svd(h, run.q().ptr, run.ldq(), run.bt().ptr, run.ldbt(), m, n, l_final, u_dev.ptr, run.ldq(),
-                     v_dev.ptr, run.ldbt(), sig, flg);
         if (!fixed_precision) drop = std::max(0, l_final - rank);  // drop_smallest (driver.cpp:85-106)
-        for (int i = 0; i < drop; ++i) svd_res += sig[i] * sig[i];
         svd_r = l_final - drop;
+        HostSvdCopy hc{};
+        const bool uv_host = svd_r > 0 && !(flags & FQB_OUT_DEVICE) && (flags & FQB_OUT_HOST);
+        if (uv_host) {
+            host_u = static_cast<double*>(host_alloc(sizeof(double) * size_t(m) * svd_r));
+            host_v = static_cast<double*>(host_alloc(sizeof(double) * size_t(n) * svd_r));
+            if (!host_u || !host_v) throw Error(kStatusAlloc, "host result allocation failed");
+            if (!h.copy_stream) FQB_CUDA(cudaStreamCreateWithFlags(&h.copy_stream, cudaStreamNonBlocking));
+            if (!h.ev_u) FQB_CUDA(cudaEventCreateWithFlags(&h.ev_u, cudaEventDisableTiming));
+            if (!h.ev_v) FQB_CUDA(cudaEventCreateWithFlags(&h.ev_v, cudaEventDisableTiming));
+            hc = HostSvdCopy{h.copy_stream, h.ev_u, h.ev_v, host_u, host_v, drop};
+        }
+        assemble_svd(h, run.q().ptr, run.ldq(), run.bt().ptr, run.ldbt(), m, n, l_final, u_dev.ptr, run.ldq(),
+                     v_dev.ptr, run.ldbt(), sig, flg, uv_host ? &hc : nullptr);
+        uv_to_host = uv_host;
+        for (int i = 0; i < drop; ++i) svd_res += sig[i] * sig[i];
     }
     FQB_CUDA(cudaEventRecord(h.ev1, s));
 
@@ -818,22 +837,16 @@ int run_qb(Handle& h, const void* a, bool a_f32, int64_t m, int64_t n, int64_t l
             out->v = v_dev.detach();
             out->ldu = run.ldq();
             out->ldv = run.ldbt();
-        } else if (svd_r > 0 && (flags & FQB_OUT_HOST)) {
-            out->u = static_cast<double*>(host_alloc(sizeof(double) * size_t(m) * svd_r));
-            out->v = static_cast<double*>(host_alloc(sizeof(double) * size_t(n) * svd_r));
-            if (!out->u || !out->v) throw Error(kStatusAlloc, "host result allocation failed");
-            FQB_CUDA(cudaMemcpy2DAsync(out->u, m * sizeof(double), u_dev.ptr + int64_t(drop) * run.ldq(),
-                                       run.ldq() * sizeof(double), m * sizeof(double), svd_r,
-                                       cudaMemcpyDeviceToHost, s));
-            FQB_CUDA(cudaMemcpy2DAsync(out->v, n * sizeof(double), v_dev.ptr + int64_t(drop) * run.ldbt(),
-                                       run.ldbt() * sizeof(double), n * sizeof(double), svd_r,
-                                       cudaMemcpyDeviceToHost, s));
+        } else if (svd_r > 0 && host_u) {
+            out->u = host_u;    // copied on the copy stream during the assembly
+            out->v = host_v;
+            host_u = host_v = nullptr;   // owned by the result now
             out->ldu = m;
             out->ldv = n;
         }
     }
     FQB_CUDA(cudaStreamSynchronize(s));
-    if (host_out) FQB_CUDA(cudaStreamSynchronize(h.copy_stream));
+    if (host_out || uv_to_host) FQB_CUDA(cudaStreamSynchronize(h.copy_stream));
     float ms = 0.f;
     cudaEventElapsedTime(&ms, h.ev0, h.ev1);
     out->elapsed_ms = ms;

@@ -92,13 +92,23 @@ struct Handle {
     // D2H of host results overlapped with the SVD assembly (created on first use)
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t ev_qb = nullptr;
+    cudaEvent_t ev_u = nullptr, ev_v = nullptr;   // host U / V copies of the SVD assembly
 };
 
 // svd.cu: U = Q U~, V = Bt U~ Sigma^-1 from eig(B B'); sigma ascending
 bool eigh_inplace(Handle& h, double* mat, int l, double* w);
+// Host copies of U / V's kept columns (the last l - drop), issued on `stream` right
+// after each factor's GEMM (events ev_u / ev_v order them after it); null u / v skip.
+struct HostSvdCopy {
+    cudaStream_t stream;
+    cudaEvent_t ev_u, ev_v;
+    double* u;
+    double* v;
+    int drop;
+};
 void assemble_svd(Handle& h, const double* q, int64_t ldq, const double* bt, int64_t ldbt, int64_t m, int64_t n,
                   int l, double* u, int64_t ldu, double* v, int64_t ldv, std::vector<double>& sigma,
-                  std::vector<char>& flagged);
+                  std::vector<char>& flagged, const HostSvdCopy* hc = nullptr);
 void destroy_cusolver(Handle& h);
 // synthetic.cu: test matrices on the device (reference synthetic.cpp)
 void random_orthonormal_dev(Handle& h, int64_t n, int r, uint64_t seed, uint32_t stream, int first_col, double* q,

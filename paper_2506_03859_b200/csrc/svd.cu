@@ -266,7 +266,7 @@ bool eigh_inplace(Handle& h, double* mat, int l, double* w) { return eigh_core(h
 
 void assemble_svd(Handle& h, const double* q, int64_t ldq, const double* bt, int64_t ldbt, int64_t m, int64_t n,
                   int l, double* u, int64_t ldu, double* v, int64_t ldv, std::vector<double>& sigma,
-                  std::vector<char>& flagged) {
+                  std::vector<char>& flagged, const HostSvdCopy* hc) {
     sigma.assign(l, 0.0);
     flagged.assign(l, 0);
     if (l == 0) return;
@@ -294,9 +294,18 @@ void assemble_svd(Handle& h, const double* q, int64_t ldq, const double* bt, int
     launch_k(k_scale_cols, grid, 256, 0, s, mat.ptr, l, scale.ptr + l, l, l, us.ptr, l);
     FQB_LAUNCHED();
     h.lc.bump(2);
-    // U = Q U~ (this rank's rows), V = Bt (U~ Sigma^-1)
+    // U = Q U~ (this rank's rows), V = Bt (U~ Sigma^-1); with hc, each factor's kept
+    // columns go to the host on the copy stream as soon as its GEMM is done
+    auto copy_out = [&](const double* src, int64_t lds, int64_t rows, double* dst, cudaEvent_t ev) {
+        FQB_CUDA(cudaEventRecord(ev, s));
+        FQB_CUDA(cudaStreamWaitEvent(hc->stream, ev, 0));
+        FQB_CUDA(cudaMemcpy2DAsync(dst, rows * sizeof(double), src + int64_t(hc->drop) * lds, lds * sizeof(double),
+                                   rows * sizeof(double), l - hc->drop, cudaMemcpyDeviceToHost, hc->stream));
+    };
     gemm(false, m, l, l, 1.0, q, ldq, mat.ptr, l, 0.0, u, ldu, h.gws, h.num_sms, s, h.lc);
+    if (hc && hc->u) copy_out(u, ldu, m, hc->u, hc->ev_u);
     gemm(false, n, l, l, 1.0, bt, ldbt, us.ptr, l, 0.0, v, ldv, h.gws, h.num_sms, s, h.lc);
+    if (hc && hc->v) copy_out(v, ldv, n, hc->v, hc->ev_v);
     int hinfo = 0;
     FQB_CUDA(cudaMemcpyAsync(sigma.data(), scale.ptr, sizeof(double) * l, cudaMemcpyDeviceToHost, s));
     FQB_CUDA(cudaMemcpyAsync(flagged.data(), flg.ptr, size_t(l), cudaMemcpyDeviceToHost, s));
