@@ -466,9 +466,9 @@ fqb_status fqb_gemm_emulated(fqb_handle h, int trans_a, int64_t m, int64_t n, in
         farqb::DeviceArray<int8_t> xs, zs;
         farqb::DeviceArray<int> ex, ez;
         xs.ensure(size_t(farqb::ozaki_x_bytes(m, k)), s);
-        zs.ensure(size_t(farqb::ozaki_z_bytes(farqb::ozaki_max_n(), k)), s);
+        zs.ensure(size_t(farqb::ozaki_apply_z_bytes(k)), s);
         ex.ensure(size_t(m), s);
-        ez.ensure(size_t(farqb::ozaki_max_n()), s);
+        ez.ensure(size_t(farqb::ozaki_apply_ez_count()), s);
         farqb::DeviceArray<unsigned> line_max;
         line_max.ensure(size_t(farqb::ozaki_line_max_words(m, k)), s);
         if (trans_a) farqb::ozaki_slice_a(a, k, m, lda, line_max.ptr, xs.ptr, ex.ptr, nullptr, nullptr, s, h->h.lc);
@@ -506,7 +506,7 @@ fqb_status fqb_slice_operand(fqb_handle h, const double* a, int64_t m, int64_t n
             sl->x_tn.ensure(size_t(farqb::ozaki_x_bytes(n, m)), s);
             sl->e_nn.ensure(size_t(m), s);
             sl->e_tn.ensure(size_t(n), s);
-            sl->ez.ensure(size_t(farqb::ozaki_max_n()), s);
+            sl->ez.ensure(size_t(farqb::ozaki_apply_ez_count()), s);
             farqb::DeviceArray<unsigned> line_max;
             line_max.ensure(size_t(farqb::ozaki_line_max_words(m, n)), s);
             farqb::ozaki_slice_a(a, m, n, lda, line_max.ptr, sl->x_tn.ptr, sl->e_tn.ptr, sl->x_nn.ptr, sl->e_nn.ptr, s,
@@ -531,7 +531,7 @@ fqb_status fqb_sliced_gemm(fqb_handle h, fqb_sliced sl, int trans_a, int64_t nb,
         if (nb == 0) return FQB_OK;
         cudaStream_t s = h->h.stream;
         farqb::ensure_gemm_workspace(h->h);
-        sl->z.ensure(size_t(farqb::ozaki_z_bytes(farqb::ozaki_max_n(), K)), s);
+        sl->z.ensure(size_t(farqb::ozaki_apply_z_bytes(K)), s);
         farqb::ozaki_apply(M, nb, K, alpha, trans_a ? sl->x_tn.ptr : sl->x_nn.ptr,
                            trans_a ? sl->e_tn.ptr : sl->e_nn.ptr, b, ldb, beta, c, ldc, sl->z.ptr, sl->ez.ptr,
                            h->h.gws.work, h->h.num_sms, s, h->h.lc);

@@ -325,8 +325,8 @@ class QbRun {
             }
         }
         Workspace& w = h_.ws;
-        w.oz_z.ensure(size_t(ozaki_z_bytes(ozaki_max_n(), K)), s_);
-        w.oz_ez.ensure(size_t(ozaki_max_n()), s_);
+        w.oz_z.ensure(size_t(ozaki_apply_z_bytes(K)), s_);
+        w.oz_ez.ensure(size_t(ozaki_apply_ez_count()), s_);
         ozaki_apply(M, N, K, 1.0, ta ? w.oz_x_tn.ptr : w.oz_x_nn.ptr, ta ? w.oz_e_tn.ptr : w.oz_e_nn.ptr, B, ldb, 0.0,
                     C, ldc, w.oz_z.ptr, w.oz_ez.ptr, h_.gws.work, h_.num_sms, s_, h_.lc);
     }

@@ -120,6 +120,8 @@ int ozaki_max_n();
 int ozaki_bn(int64_t n);
 int64_t ozaki_x_bytes(int64_t rows, int64_t k);
 int64_t ozaki_z_bytes(int64_t n, int64_t k);
+int64_t ozaki_apply_z_bytes(int64_t k);
+int ozaki_apply_ez_count();
 int64_t ozaki_workspace_doubles(int num_sms);
 // Slices of A (m x n, ld) in both layouts from one pass (either may be null):
 //   x_tn / e_tn: operand rows = columns of A, K = m   (A' Y)
@@ -138,7 +140,8 @@ void ozaki_slice_a(const float* a, int64_t m, int64_t n, int64_t ld, unsigned* l
 void ozaki_slice_z(const double* b, int64_t k, int64_t n, int64_t ld, int* e, int8_t* out, cudaStream_t s,
                    LaunchCounter& lc);
 // C = alpha X' B + beta C for any N: B (K x N, ld, FP64) sliced in chunks of <= 64
-// columns into z (ozaki_z_bytes(64, K)) / ez (64)
+// columns into z (ozaki_apply_z_bytes(K)) / ez (ozaki_apply_ez_count()); N > 64
+// runs two chunks at a time on CTA pairs sharing the A tiles (FQB_OZ_PAIR=0: off)
 void ozaki_apply(int64_t M, int64_t N, int64_t K, double alpha, const int8_t* xs, const int* ex, const double* b,
                  int64_t ldb, double beta, double* C, int64_t ldc, int8_t* z, int* ez, double* work, int num_sms,
                  cudaStream_t s, LaunchCounter& lc);

@@ -107,7 +107,26 @@ struct OzArgs {
     int64_t iters;        // tiles * kblocks
     int kblocks, mtiles, grid, bn;
     double inv_grid, inv_kblocks, inv_iters;
+    // paired launch (pair = 1): clusters of two CTAs stream the same A tiles, each
+    // loading half of every k-block's slices multicast into both; CTA rank r
+    // computes column chunk r: zs + r zs_stride, ez + 64 r, C + r cw ldc, N_r =
+    // min(cw, N - r cw), work + r work_stride.  grid counts clusters.
+    int pair;
+    int64_t zs_stride, cw, work_stride;
 };
+
+// this CTA's (or fixup block's) column chunk of a paired launch
+__device__ __forceinline__ OzArgs chunk_args(const OzArgs& p, int r) {
+    OzArgs q = p;
+    if (p.pair) {
+        q.zs = p.zs + r * p.zs_stride;
+        q.ez = p.ez + r * OZ_BN;
+        q.C = p.C + r * p.cw * p.ldc;
+        q.N = min(p.cw, p.N - r * p.cw);
+        q.work = p.work + r * p.work_stride;
+    }
+    return q;
+}
 
 __device__ __forceinline__ int64_t range_begin(const OzArgs& p, int c) { return qdiv(p.iters * c, p.grid, p.inv_grid); }
 // the CTA whose range holds iteration it: largest c with range_begin(c) <= it
@@ -134,6 +153,18 @@ __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
         "@!p bra WAIT_%=;\n\t}\n" ::"r"(bar), "r"(parity) : "memory");
 }
+// one 1-D bulk copy landing at the same offset in both CTAs of the pair, completing
+// transaction bytes on the mbarrier at the same offset in each
+__device__ __forceinline__ void bulk_load_mc2(unsigned dst, const void* src, unsigned bytes, unsigned bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], "
+        "%4;\n" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(bar), "h"((unsigned short)3)
+        : "memory");
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
 __device__ __forceinline__ void bulk_load(unsigned dst, const void* src, unsigned bytes, unsigned bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
                  ::"r"(dst), "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(bar) : "memory");
@@ -158,6 +189,14 @@ __device__ __forceinline__ void umma_i8(unsigned tmem_d, unsigned da_lo, unsigne
 __device__ __forceinline__ void umma_commit(unsigned bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(bar)
                  : "memory");
+}
+// arrive on the mbarrier at this offset in both CTAs of the pair
+__device__ __forceinline__ void umma_commit_mc2(unsigned bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+            bar),
+        "h"((unsigned short)3)
+        : "memory");
 }
 __device__ __forceinline__ void tmem_ld16(unsigned taddr, unsigned (&v)[16]) {
     asm volatile(
@@ -195,10 +234,12 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
     const unsigned b_full = a_empty + 8 * A_STAGES, b_empty = b_full + 8 * B_STAGES;
     const unsigned t_full = b_empty + 8 * B_STAGES, t_empty = t_full + 8;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int rank = p.pair ? int(blockIdx.x & 1) : 0;
+    const OzArgs q = chunk_args(p, rank);
     if (threadIdx.x == 0) {
         for (int s = 0; s < A_STAGES; ++s) {
             mbar_init(a_full + 8 * s, 1);
-            mbar_init(a_empty + 8 * s, 1);
+            mbar_init(a_empty + 8 * s, p.pair ? 2 : 1);   // both consumers release a shared stage
         }
         for (int s = 0; s < B_STAGES; ++s) {
             mbar_init(b_full + 8 * s, 1);
@@ -208,7 +249,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
         mbar_init(t_empty, 128);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
-    if (threadIdx.x < OZ_BN) ez_s[threadIdx.x] = int(threadIdx.x) < p.N ? p.ez[threadIdx.x] : 0;
+    if (threadIdx.x < OZ_BN) ez_s[threadIdx.x] = int(threadIdx.x) < q.N ? q.ez[threadIdx.x] : 0;
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
             smem_u32(&tmem_base_s)));
@@ -216,10 +257,11 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n");
     __syncthreads();
+    if (p.pair) cluster_sync();   // the peer's barriers exist before any multicast / remote arrive
     asm volatile("tcgen05.fence::after_thread_sync;\n");
     const unsigned tmem = tmem_base_s;
 
-    const int c = blockIdx.x;
+    const int c = p.pair ? int(blockIdx.x >> 1) : int(blockIdx.x);
     const Walk wk(range_begin(p, c), range_begin(p, c + 1), p.kblocks, p.inv_kblocks);
     const int bn = p.bn;
 
@@ -234,13 +276,16 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
                     const int sb = int(jb % B_STAGES);
                     mbar_wait(b_empty + 8 * sb, unsigned((jb / B_STAGES) & 1) ^ 1u);
                     mbar_expect_tx(b_full + 8 * sb, zbytes);
-                    bulk_load(b_base + sb * B_STAGE, p.zs + int64_t(kb) * zbytes, zbytes, b_full + 8 * sb);
+                    bulk_load(b_base + sb * B_STAGE, q.zs + int64_t(kb) * zbytes, zbytes, b_full + 8 * sb);
                     const int8_t* xt = p.xs + (mt * p.kblocks + kb) * int64_t(S * A_TILE);
                     for (int sp = 0; sp < S; ++sp, ++ja) {
                         const int sa = int(ja % A_STAGES);
                         mbar_wait(a_empty + 8 * sa, unsigned((ja / A_STAGES) & 1) ^ 1u);
                         mbar_expect_tx(a_full + 8 * sa, unsigned(A_TILE));
-                        bulk_load(a_base + sa * A_TILE, xt + sp * A_TILE, unsigned(A_TILE), a_full + 8 * sa);
+                        if (!p.pair)
+                            bulk_load(a_base + sa * A_TILE, xt + sp * A_TILE, unsigned(A_TILE), a_full + 8 * sa);
+                        else if ((sp & 1) == rank)   // the pair splits the slices, each lands in both
+                            bulk_load_mc2(a_base + sa * A_TILE, xt + sp * A_TILE, unsigned(A_TILE), a_full + 8 * sa);
                     }
                 }
             }
@@ -286,7 +331,8 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
                                 for (int k = 1; k < OZ_BK / 32; ++k)
                                     umma_i8(dt, da_lo + k * kstep, bl + k * kstep, d_hi, id, 1u);
                             }
-                            umma_commit(a_empty + 8 * sa);
+                            if (p.pair) umma_commit_mc2(a_empty + 8 * sa);
+                            else umma_commit(a_empty + 8 * sa);
                             if (++sa == A_STAGES) sa = 0, pa ^= 1u;
                         }
                         umma_commit(b_empty + 8 * sb);
@@ -307,14 +353,14 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
         const int quarter = warp & 3;           // TMEM lanes 32*quarter .. +31
         const int r_loc = quarter * 32 + lane;  // tile row of this thread
         const unsigned lane_addr = tmem + (unsigned(quarter * 32) << 16);
-        double* carry = p.work + (3 * int64_t(c) + 2) * OZ_PARTIAL;
+        double* carry = q.work + (3 * int64_t(c) + 2) * OZ_PARTIAL;
         unsigned ph = 0;
         for (int64_t si = 0; si < wk.nseg; ++si) {
             const int64_t t = wk.tile(si);
             const int kb0 = wk.kb(t), kb1 = wk.ke(t);
             const int64_t row = t * OZ_BM + r_loc;
             const bool full_tile = kb0 == 0 && kb1 == p.kblocks;
-            double* piece = p.work + (3 * int64_t(c) + (t == wk.t_last ? 0 : 1)) * OZ_PARTIAL;
+            double* piece = q.work + (3 * int64_t(c) + (t == wk.t_last ? 0 : 1)) * OZ_PARTIAL;
             const int er = row < p.M ? p.ex[row] : 0;   // loaded while the MMAs run
             for (int cb = kb0; cb < kb1; cb += CHUNK_KB) {
                 const bool first_chunk = cb == kb0, last_chunk = cb + CHUNK_KB >= kb1;
@@ -358,13 +404,13 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
                         if (p.beta != 0.0) {
 #pragma unroll
                             for (int j = 0; j < 16; ++j)
-                                old_c[j] = g + j < p.N ? p.C[int64_t(g + j) * p.ldc + row] : 0.0;
+                                old_c[j] = g + j < q.N ? q.C[int64_t(g + j) * p.ldc + row] : 0.0;
                         }
 #pragma unroll
                         for (int j = 0; j < 16; ++j) {
-                            if (g + j < p.N) {
+                            if (g + j < q.N) {
                                 const double val = p.alpha * mul_pow2(acc[j], er + ez_s[g + j]);
-                                p.C[int64_t(g + j) * p.ldc + row] = p.beta != 0.0 ? fma(p.beta, old_c[j], val) : val;
+                                q.C[int64_t(g + j) * p.ldc + row] = p.beta != 0.0 ? fma(p.beta, old_c[j], val) : val;
                             }
                         }
                     }
@@ -376,6 +422,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n");
     __syncthreads();
+    if (p.pair) cluster_sync();   // no CTA leaves while its peer may still arrive on its barriers
     if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
 }
 
@@ -613,8 +660,9 @@ __global__ void __launch_bounds__(ZT) k_slice_z(const double* __restrict__ b, in
 // Pieces were written already scaled by 2^(ex + ez).  Block (tile, 8 columns),
 // one thread per tile row; up to 4 pieces x 8 columns of loads in flight.
 constexpr int FIX_COLS = 8;
-__global__ void __launch_bounds__(OZ_BM) k_ozaki_fixup(const OzArgs p) {
+__global__ void __launch_bounds__(OZ_BM) k_ozaki_fixup(const OzArgs p0) {
     FQB_PDL_ENTRY();
+    const OzArgs p = chunk_args(p0, int(blockIdx.z));   // blockIdx.z = column chunk of a paired launch
     const int64_t t = blockIdx.x;
     const int j0 = blockIdx.y * FIX_COLS, r = threadIdx.x;
     const int c0 = cta_of(p, t * p.kblocks), c1 = cta_of(p, t * p.kblocks + p.kblocks - 1);
@@ -709,17 +757,19 @@ void ozaki_slice_z(const double* b, int64_t k, int64_t n, int64_t ld, int* e, in
     lc.bump();
 }
 
-void ozaki_gemm(int64_t M, int64_t N, int64_t K, double alpha, const int8_t* xs, const int* ex, const int8_t* zs,
-                const int* ez, double beta, double* C, int64_t ldc, double* work, int num_sms, cudaStream_t s,
-                LaunchCounter& lc) {
-    if (N > OZ_BN) throw Error(kStatusInvalid, "ozaki_gemm: N > 64");
+// paired (pair_cw > 0): N = 2 chunks of pair_cw columns at most, zs / ez hold both
+static void launch_ozaki(int64_t M, int64_t N, int64_t K, double alpha, const int8_t* xs, const int* ex,
+                         const int8_t* zs, const int* ez, double beta, double* C, int64_t ldc, double* work,
+                         int num_sms, int64_t pair_cw, cudaStream_t s, LaunchCounter& lc) {
     static bool configured[64] = {};
     int dev = 0;
     FQB_CUDA(cudaGetDevice(&dev));
     if (dev < 0 || dev >= 64 || !configured[dev]) {
         FQB_CUDA(cudaFuncSetAttribute(k_ozaki, cudaFuncAttributeMaxDynamicSharedMemorySize, int(OZ_SMEM)));
+        FQB_CUDA(cudaFuncSetAttribute(k_ozaki, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
         if (dev >= 0 && dev < 64) configured[dev] = true;
     }
+    const bool pair = pair_cw > 0;
     OzArgs a{};
     a.xs = xs;
     a.zs = zs;
@@ -733,41 +783,91 @@ void ozaki_gemm(int64_t M, int64_t N, int64_t K, double alpha, const int8_t* xs,
     a.ex = ex;
     a.ez = ez;
     a.work = work;
-    a.bn = ozaki_bn(N);
-
+    a.bn = OZ_BN;
     a.mtiles = int(ceil_div(M, OZ_BM));
     a.kblocks = int(ceil_div(K, OZ_BK));
     a.iters = int64_t(a.mtiles) * a.kblocks;
-    a.grid = int(std::max<int64_t>(1, std::min<int64_t>(num_sms, a.iters / 4)));
+    const int slots = pair ? num_sms / 2 : num_sms;   // CTAs (pairs) streaming distinct A ranges
+    a.grid = int(std::max<int64_t>(1, std::min<int64_t>(slots, a.iters / 4)));
     a.inv_grid = 1.0 / double(a.grid);
     a.inv_kblocks = 1.0 / double(a.kblocks);
     a.inv_iters = 1.0 / double(a.iters);
-    launch_k(k_ozaki, a.grid, OZ_THREADS, OZ_SMEM, s, a);
+    a.pair = pair ? 1 : 0;
+    a.cw = pair_cw;
+    a.zs_stride = ozaki_z_bytes(OZ_BN, K);
+    a.work_stride = 3 * int64_t(a.grid) * OZ_PARTIAL;
+    if (!pair) {
+        launch_k(k_ozaki, a.grid, OZ_THREADS, OZ_SMEM, s, a);
+    } else {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(unsigned(2 * a.grid));
+        cfg.blockDim = dim3(OZ_THREADS);
+        cfg.dynamicSmemBytes = OZ_SMEM;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[2];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[1].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = pdl_enabled() ? 2 : 1;
+        FQB_CUDA(cudaLaunchKernelEx(&cfg, k_ozaki, a));
+    }
     FQB_LAUNCHED();
     lc.bump();
-    bool split = false;   // does any CTA boundary fall inside a tile?
+    bool split = false;   // does any CTA (pair) boundary fall inside a tile?
     for (int c = 1; c < a.grid && !split; ++c) split = (a.iters * c / a.grid) % a.kblocks != 0;
     if (split) {
-        launch_k(k_ozaki_fixup, dim3(unsigned(a.mtiles), unsigned(ceil_div(N, FIX_COLS))), OZ_BM, 0, s, a);
+        const int64_t ncols = pair ? pair_cw : N;
+        launch_k(k_ozaki_fixup, dim3(unsigned(a.mtiles), unsigned(ceil_div(ncols, FIX_COLS)), pair ? 2u : 1u), OZ_BM,
+                 0, s, a);
         FQB_LAUNCHED();
         lc.bump();
     }
 }
 
-// N > 64 right-hand columns: balanced chunks of <= 64 (one pass over the A slices each)
+void ozaki_gemm(int64_t M, int64_t N, int64_t K, double alpha, const int8_t* xs, const int* ex, const int8_t* zs,
+                const int* ez, double beta, double* C, int64_t ldc, double* work, int num_sms, cudaStream_t s,
+                LaunchCounter& lc) {
+    if (N > OZ_BN) throw Error(kStatusInvalid, "ozaki_gemm: N > 64");
+    launch_ozaki(M, N, K, alpha, xs, ex, zs, ez, beta, C, ldc, work, num_sms, 0, s, lc);
+}
+
+static bool pairs_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("FQB_OZ_PAIR");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 void ozaki_apply(int64_t M, int64_t N, int64_t K, double alpha, const int8_t* xs, const int* ex, const double* b,
                  int64_t ldb, double beta, double* C, int64_t ldc, int8_t* z, int* ez, double* work, int num_sms,
                  cudaStream_t s, LaunchCounter& lc) {
     if (N <= 0) return;
     const int64_t chunks = ceil_div(N, OZ_BN);
     const int64_t cw = ceil_div(N, chunks);
-    for (int64_t c0 = 0; c0 < N; c0 += cw) {
+    const int64_t zstride = ozaki_z_bytes(OZ_BN, K);
+    int64_t c0 = 0;
+    // two chunks at a time on CTA pairs that share every A tile (multicast): A is
+    // streamed once per pair of chunks instead of once per chunk
+    while (pairs_enabled() && num_sms >= 2 && N - c0 > cw) {
+        const int64_t nb = std::min(2 * cw, N - c0);
+        ozaki_slice_z(b + c0 * ldb, K, cw, ldb, ez, z, s, lc);
+        ozaki_slice_z(b + (c0 + cw) * ldb, K, nb - cw, ldb, ez + OZ_BN, z + zstride, s, lc);
+        launch_ozaki(M, nb, K, alpha, xs, ex, z, ez, beta, C + c0 * ldc, ldc, work, num_sms, cw, s, lc);
+        c0 += nb;
+    }
+    for (; c0 < N; c0 += cw) {
         const int64_t nb = std::min(cw, N - c0);
         ozaki_slice_z(b + c0 * ldb, K, nb, ldb, ez, z, s, lc);
         ozaki_gemm(M, nb, K, alpha, xs, ex, z, ez, beta, C + c0 * ldc, ldc, work, num_sms, s, lc);
     }
 }
-
+int64_t ozaki_apply_z_bytes(int64_t K) { return 2 * ozaki_z_bytes(OZ_BN, K); }
+int ozaki_apply_ez_count() { return 2 * OZ_BN; }
 int64_t ozaki_workspace_doubles(int num_sms) { return 3 * int64_t(num_sms) * OZ_PARTIAL; }  // 2 pieces + carry
 
 }  // namespace farqb
