@@ -137,10 +137,15 @@ def apass_roofline(eng, a, stream):
     sl = eng.slice_operand(a.data_ptr(), M, N, a.stride(1))
     for name, trans, outp, bp in (("tn", True, w, y), ("nn", False, yn, g)):
         k, rows = (M, N) if trans else (N, M)
-        for kind in ("ozaki", "dmma"):
+        for kind in ("ozaki", "kernel", "dmma"):
+            if kind == "kernel":   # k_ozaki (+ its stream-K fixup) alone, on the B slices just made
+                sl.gemm(trans, BLOCK, 1.0, bp.data_ptr(), bp.stride(1), 0.0, outp.data_ptr(), outp.stride(1))
+
             def call():
                 if kind == "ozaki":
                     sl.gemm(trans, BLOCK, 1.0, bp.data_ptr(), bp.stride(1), 0.0, outp.data_ptr(), outp.stride(1))
+                elif kind == "kernel":
+                    sl.gemm_again(1.0, 0.0, outp.data_ptr(), outp.stride(1))
                 else:
                     eng.gemm(trans, rows, BLOCK, k, 1.0, a.data_ptr(), a.stride(1), bp.data_ptr(), bp.stride(1),
                              0.0, outp.data_ptr(), outp.stride(1))
@@ -327,7 +332,8 @@ def run_ours(args):
     a_full = None
     torch.cuda.empty_cache()
     sketch = sketch_roofline(eng, dev)
-    dom = roof["tn_ozaki"]
+    dom = roof["tn_kernel"]   # the dominant kernel by itself (k_ozaki + its stream-K fixup)
+    pas = roof["tn_ozaki"]    # the whole A pass as the engine runs it (+ k_slice_z of Y)
     traffic = load_traffic()
     line = {
         "metric": "farPCA time-to-eps (s)",
@@ -350,12 +356,15 @@ def run_ours(args):
         "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,
         "roofline": {"bound": "hbm",
-                     "kernel": "A pass W=A'Y 8000x50x8000: k_slice_z + k_ozaki (tcgen05 kind::i8 FP64 emulation) "
-                               "+ k_ozaki_fixup",
+                     "kernel": "k_ozaki (tcgen05 kind::i8 FP64 emulation, + k_ozaki_fixup of the split tiles), "
+                               "W=A'Y 8000x50x8000 on pre-sliced A and Y (fqb_sliced_gemm_again)",
                      "achieved": dom["gbs"], "peak": HBM_PEAK_GBS, "unit": "GB/s", "frac": dom["gbs"] / HBM_PEAK_GBS,
                      "bytes_per_launch": dom["bytes"], "bytes_formula": "8*m*n (A slices) + 8*m*b (Y) + 8*n*b (W)",
-                     "launch_ms": dom["ms"], "nn_achieved": roof["nn_ozaki"]["gbs"],
-                     "nn_launch_ms": roof["nn_ozaki"]["ms"],
+                     "launch_ms": dom["ms"], "nn_achieved": roof["nn_kernel"]["gbs"],
+                     "nn_launch_ms": roof["nn_kernel"]["ms"],
+                     "pass": {"what": "the whole A pass as the QB loop runs it: k_slice_z (Y) + k_ozaki + fixup",
+                              "tn_ms": pas["ms"], "tn_achieved": pas["gbs"], "tn_frac": pas["gbs"] / HBM_PEAK_GBS,
+                              "nn_ms": roof["nn_ozaki"]["ms"], "nn_achieved": roof["nn_ozaki"]["gbs"]},
                      "fp64_tflops_equiv": dom["tflops"],
                      "dmma_same_product": {"tn_ms": roof["tn_dmma"]["ms"], "tn_tflops": roof["tn_dmma"]["tflops"],
                                            "nn_ms": roof["nn_dmma"]["ms"], "peak_tflops": FP64_PEAK_TFLOPS},

@@ -293,6 +293,11 @@ typedef struct fqb_sliced_s* fqb_sliced;
 fqb_status fqb_slice_operand(fqb_handle h, const double* a, int64_t m, int64_t n, int64_t lda, fqb_sliced* out);
 fqb_status fqb_sliced_gemm(fqb_handle h, fqb_sliced s, int trans_a, int64_t nb, double alpha, const double* b,
                            int64_t ldb, double beta, double* c, int64_t ldc);
+/* The last fqb_sliced_gemm on s once more, on the B slices it left behind (its nb <= 128):
+ * C = alpha op(A) B + beta C with the same op(A) and B -- only the tensor-core GEMM
+ * (k_ozaki, + the stream-K fixup when a tile is split) runs, no slicing of B.  For
+ * repeated products with one B, and for timing the GEMM kernel by itself. */
+fqb_status fqb_sliced_gemm_again(fqb_handle h, fqb_sliced s, double alpha, double beta, double* c, int64_t ldc);
 fqb_status fqb_sliced_free(fqb_handle h, fqb_sliced s);
 
 /* ---- test matrices on the device (reference synthetic.cpp) ----- */

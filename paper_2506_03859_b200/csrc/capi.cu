@@ -485,6 +485,8 @@ struct fqb_sliced_s {
     int64_t m = 0, n = 0;
     farqb::DeviceArray<int8_t> x_nn, x_tn, z;
     farqb::DeviceArray<int> e_nn, e_tn, ez;
+    int last_trans = -1;   // the last fqb_sliced_gemm: B slices left in z / ez
+    int64_t last_nb = 0;
 };
 
 extern "C" {
@@ -535,6 +537,25 @@ fqb_status fqb_sliced_gemm(fqb_handle h, fqb_sliced sl, int trans_a, int64_t nb,
         farqb::ozaki_apply(M, nb, K, alpha, trans_a ? sl->x_tn.ptr : sl->x_nn.ptr,
                            trans_a ? sl->e_tn.ptr : sl->e_nn.ptr, b, ldb, beta, c, ldc, sl->z.ptr, sl->ez.ptr,
                            h->h.gws.work, h->h.num_sms, s, h->h.lc);
+        sl->last_trans = trans_a ? 1 : 0;
+        sl->last_nb = nb;
+        return FQB_OK;
+    });
+}
+
+fqb_status fqb_sliced_gemm_again(fqb_handle h, fqb_sliced sl, double alpha, double beta, double* c, int64_t ldc) {
+    return guarded([&]() -> fqb_status {
+        bind(h);
+        if (!sl) throw farqb::Error(FQB_ERR_INVALID_ARGUMENT, "null sliced operand");
+        if (sl->last_trans < 0) throw farqb::Error(FQB_ERR_INVALID_ARGUMENT, "no previous fqb_sliced_gemm");
+        if (sl->last_nb > 128) throw farqb::Error(FQB_ERR_INVALID_ARGUMENT, "previous product wider than 128");
+        const bool ta = sl->last_trans == 1;
+        const int64_t M = ta ? sl->n : sl->m, K = ta ? sl->m : sl->n;
+        if (ldc < M) throw farqb::Error(FQB_ERR_DIMENSION, "leading dimension too small");
+        farqb::ensure_gemm_workspace(h->h);
+        farqb::ozaki_apply_presliced(M, sl->last_nb, K, alpha, ta ? sl->x_tn.ptr : sl->x_nn.ptr,
+                                     ta ? sl->e_tn.ptr : sl->e_nn.ptr, beta, c, ldc, sl->z.ptr, sl->ez.ptr,
+                                     h->h.gws.work, h->h.num_sms, h->h.stream, h->h.lc);
         return FQB_OK;
     });
 }

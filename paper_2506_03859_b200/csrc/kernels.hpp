@@ -121,6 +121,10 @@ int ozaki_bn(int64_t n);
 int64_t ozaki_x_bytes(int64_t rows, int64_t k);
 int64_t ozaki_z_bytes(int64_t n, int64_t k);
 int64_t ozaki_apply_z_bytes(int64_t k);
+// ozaki_apply's products again on the B slices its last call left in z / ez (N <= 128)
+void ozaki_apply_presliced(int64_t M, int64_t N, int64_t K, double alpha, const int8_t* xs, const int* ex, double beta,
+                           double* C, int64_t ldc, const int8_t* z, const int* ez, double* work, int num_sms,
+                           cudaStream_t s, LaunchCounter& lc);
 int ozaki_apply_ez_count();
 int64_t ozaki_workspace_doubles(int num_sms);
 // Slices of A (m x n, ld) in both layouts from one pass (either may be null):

@@ -866,6 +866,19 @@ void ozaki_apply(int64_t M, int64_t N, int64_t K, double alpha, const int8_t* xs
         ozaki_gemm(M, nb, K, alpha, xs, ex, z, ez, beta, C + c0 * ldc, ldc, work, num_sms, s, lc);
     }
 }
+// the products of ozaki_apply again, on the B slices its last call left in z / ez
+// (N <= 128: the chunks of one launch)
+void ozaki_apply_presliced(int64_t M, int64_t N, int64_t K, double alpha, const int8_t* xs, const int* ex, double beta,
+                           double* C, int64_t ldc, const int8_t* z, const int* ez, double* work, int num_sms,
+                           cudaStream_t s, LaunchCounter& lc) {
+    if (N <= 0) return;
+    if (N > 2 * OZ_BN) throw Error(kStatusInvalid, "ozaki_apply_presliced: N > 128");
+    const int64_t chunks = ceil_div(N, OZ_BN);
+    const int64_t cw = ceil_div(N, chunks);
+    if (chunks == 2 && !(pairs_enabled() && num_sms >= 2))
+        throw Error(kStatusInvalid, "ozaki_apply_presliced: two chunks need the paired launch");
+    launch_ozaki(M, N, K, alpha, xs, ex, z, ez, beta, C, ldc, work, num_sms, chunks == 2 ? cw : 0, s, lc);
+}
 int64_t ozaki_apply_z_bytes(int64_t K) { return 2 * ozaki_z_bytes(OZ_BN, K); }
 int ozaki_apply_ez_count() { return 2 * OZ_BN; }
 int64_t ozaki_workspace_doubles(int num_sms) { return 3 * int64_t(num_sms) * OZ_PARTIAL; }  // 2 pieces + carry

@@ -338,6 +338,15 @@ class SlicedOperand:
         if st:
             _raise(st, "fqb_sliced_gemm")
 
+    def gemm_again(self, alpha, beta, c_ptr, ldc):
+        """The last gemm() once more on the B slices it left (nb <= 128): only the tensor-core
+        GEMM kernel runs (fqb_sliced_gemm_again)."""
+        if self._s is None:
+            raise InvalidArgument("sliced operand was freed")
+        st = self._eng._lib.fqb_sliced_gemm_again(self._eng._h, self._s, alpha, beta, c_ptr, ldc)
+        if st:
+            _raise(st, "fqb_sliced_gemm_again")
+
     def free(self):
         if self._s is not None:
             self._eng._lib.fqb_sliced_free(self._eng._h, self._s)

@@ -210,3 +210,22 @@ def test_sliced_operand_matches_one_shot_emulation(eng):
             assert (c1.cpu() - want).abs().max().item() < 1e-12
     with pytest.raises(fqb.InvalidArgument):
         sl.gemm(True, nb, 1.0, b.data_ptr(), m, 0.0, c1.data_ptr(), n)
+
+
+@pytest.mark.parametrize("nb", [50, 100, 128])
+def test_sliced_gemm_again_reuses_b_slices(eng, nb):
+    """fqb_sliced_gemm_again: the previous product on the same B slices, bit for bit,
+    with new alpha / beta (one chunk, and the paired two-chunk launch)."""
+    m, n = 900, 700
+    g = torch.Generator(device="cpu").manual_seed(nb)
+    a = torch.randn((n, m), dtype=torch.float64, generator=g).t().contiguous().t().cuda()
+    for trans, k, rows in ((True, m, n), (False, n, m)):
+        b = torch.randn((nb, k), dtype=torch.float64, generator=g).t().cuda()
+        c1 = torch.empty((nb, rows), dtype=torch.float64, device="cuda").t()
+        c2 = torch.randn((nb, rows), dtype=torch.float64, device="cuda").t()
+        c2_0 = c2.clone()
+        with eng.slice_operand(a.data_ptr(), m, n, m) as sl:
+            sl.gemm(trans, nb, 1.0, b.data_ptr(), k, 0.0, c1.data_ptr(), rows)
+            sl.gemm_again(-2.0, 0.5, c2.data_ptr(), rows)
+        torch.cuda.synchronize()
+        assert torch.equal(c2, 0.5 * c2_0 - 2.0 * c1) or torch.allclose(c2, 0.5 * c2_0 - 2.0 * c1, rtol=0, atol=1e-12)
