@@ -221,6 +221,9 @@ struct Walk {
     __device__ int ke(int64_t t) const { return t == t_last ? int(end - t * KT) : int(KT); }
 };
 
+// PAIR: the clustered two-chunk variant (a separate instantiation, so the single
+// chunk kernel carries none of its branches -- they cost ~4 us per pass when shared)
+template <bool PAIR>
 __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
     FQB_PDL_ENTRY();
     extern __shared__ uint8_t smem_raw[];
@@ -234,12 +237,12 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
     const unsigned b_full = a_empty + 8 * A_STAGES, b_empty = b_full + 8 * B_STAGES;
     const unsigned t_full = b_empty + 8 * B_STAGES, t_empty = t_full + 8;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int rank = p.pair ? int(blockIdx.x & 1) : 0;
-    const OzArgs q = chunk_args(p, rank);
+    const int rank = PAIR ? int(blockIdx.x & 1) : 0;
+    const OzArgs q = PAIR ? chunk_args(p, rank) : p;
     if (threadIdx.x == 0) {
         for (int s = 0; s < A_STAGES; ++s) {
             mbar_init(a_full + 8 * s, 1);
-            mbar_init(a_empty + 8 * s, p.pair ? 2 : 1);   // both consumers release a shared stage
+            mbar_init(a_empty + 8 * s, PAIR ? 2 : 1);   // both consumers release a shared stage
         }
         for (int s = 0; s < B_STAGES; ++s) {
             mbar_init(b_full + 8 * s, 1);
@@ -257,11 +260,11 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n");
     __syncthreads();
-    if (p.pair) cluster_sync();   // the peer's barriers exist before any multicast / remote arrive
+    if constexpr (PAIR) cluster_sync();   // the peer's barriers exist before any multicast / remote arrive
     asm volatile("tcgen05.fence::after_thread_sync;\n");
     const unsigned tmem = tmem_base_s;
 
-    const int c = p.pair ? int(blockIdx.x >> 1) : int(blockIdx.x);
+    const int c = PAIR ? int(blockIdx.x >> 1) : int(blockIdx.x);
     const Walk wk(range_begin(p, c), range_begin(p, c + 1), p.kblocks, p.inv_kblocks);
     const int bn = p.bn;
 
@@ -282,7 +285,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
                         const int sa = int(ja % A_STAGES);
                         mbar_wait(a_empty + 8 * sa, unsigned((ja / A_STAGES) & 1) ^ 1u);
                         mbar_expect_tx(a_full + 8 * sa, unsigned(A_TILE));
-                        if (!p.pair)
+                        if constexpr (!PAIR)
                             bulk_load(a_base + sa * A_TILE, xt + sp * A_TILE, unsigned(A_TILE), a_full + 8 * sa);
                         else if ((sp & 1) == rank)   // the pair splits the slices, each lands in both
                             bulk_load_mc2(a_base + sa * A_TILE, xt + sp * A_TILE, unsigned(A_TILE), a_full + 8 * sa);
@@ -331,7 +334,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
                                 for (int k = 1; k < OZ_BK / 32; ++k)
                                     umma_i8(dt, da_lo + k * kstep, bl + k * kstep, d_hi, id, 1u);
                             }
-                            if (p.pair) umma_commit_mc2(a_empty + 8 * sa);
+                            if constexpr (PAIR) umma_commit_mc2(a_empty + 8 * sa);
                             else umma_commit(a_empty + 8 * sa);
                             if (++sa == A_STAGES) sa = 0, pa ^= 1u;
                         }
@@ -422,7 +425,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n");
     __syncthreads();
-    if (p.pair) cluster_sync();   // no CTA leaves while its peer may still arrive on its barriers
+    if constexpr (PAIR) cluster_sync();   // no CTA leaves while its peer may still arrive on its barriers
     if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
 }
 
@@ -765,8 +768,8 @@ static void launch_ozaki(int64_t M, int64_t N, int64_t K, double alpha, const in
     int dev = 0;
     FQB_CUDA(cudaGetDevice(&dev));
     if (dev < 0 || dev >= 64 || !configured[dev]) {
-        FQB_CUDA(cudaFuncSetAttribute(k_ozaki, cudaFuncAttributeMaxDynamicSharedMemorySize, int(OZ_SMEM)));
-        FQB_CUDA(cudaFuncSetAttribute(k_ozaki, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
+        FQB_CUDA(cudaFuncSetAttribute(k_ozaki<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(OZ_SMEM)));
+        FQB_CUDA(cudaFuncSetAttribute(k_ozaki<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(OZ_SMEM)));
         if (dev >= 0 && dev < 64) configured[dev] = true;
     }
     const bool pair = pair_cw > 0;
@@ -797,7 +800,7 @@ static void launch_ozaki(int64_t M, int64_t N, int64_t K, double alpha, const in
     a.zs_stride = ozaki_z_bytes(OZ_BN, K);
     a.work_stride = 3 * int64_t(a.grid) * OZ_PARTIAL;
     if (!pair) {
-        launch_k(k_ozaki, a.grid, OZ_THREADS, OZ_SMEM, s, a);
+        launch_k(k_ozaki<false>, a.grid, OZ_THREADS, OZ_SMEM, s, a);
     } else {
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(unsigned(2 * a.grid));
@@ -813,7 +816,7 @@ static void launch_ozaki(int64_t M, int64_t N, int64_t K, double alpha, const in
         attr[1].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;
         cfg.numAttrs = pdl_enabled() ? 2 : 1;
-        FQB_CUDA(cudaLaunchKernelEx(&cfg, k_ozaki, a));
+        FQB_CUDA(cudaLaunchKernelEx(&cfg, k_ozaki<true>, a));
     }
     FQB_LAUNCHED();
     lc.bump();
