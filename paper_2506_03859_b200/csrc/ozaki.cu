@@ -238,7 +238,13 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
     const unsigned t_full = b_empty + 8 * B_STAGES, t_empty = t_full + 8;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int rank = PAIR ? int(blockIdx.x & 1) : 0;
-    const OzArgs q = PAIR ? chunk_args(p, rank) : p;
+    // this CTA's column chunk (PAIR), else the launch's own operands -- scalars, not a
+    // copy of the parameter block (which would pin it in registers)
+    const int8_t* const q_zs = PAIR ? p.zs + rank * p.zs_stride : p.zs;
+    const int* const q_ez = PAIR ? p.ez + rank * OZ_BN : p.ez;
+    double* const q_C = PAIR ? p.C + rank * p.cw * p.ldc : p.C;
+    const int64_t q_N = PAIR ? min(p.cw, p.N - rank * p.cw) : p.N;
+    double* const q_work = PAIR ? p.work + rank * p.work_stride : p.work;
     if (threadIdx.x == 0) {
         for (int s = 0; s < A_STAGES; ++s) {
             mbar_init(a_full + 8 * s, 1);
@@ -252,7 +258,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
         mbar_init(t_empty, 128);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
-    if (threadIdx.x < OZ_BN) ez_s[threadIdx.x] = int(threadIdx.x) < q.N ? q.ez[threadIdx.x] : 0;
+    if (threadIdx.x < OZ_BN) ez_s[threadIdx.x] = int(threadIdx.x) < q_N ? q_ez[threadIdx.x] : 0;
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
             smem_u32(&tmem_base_s)));
@@ -279,7 +285,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
                     const int sb = int(jb % B_STAGES);
                     mbar_wait(b_empty + 8 * sb, unsigned((jb / B_STAGES) & 1) ^ 1u);
                     mbar_expect_tx(b_full + 8 * sb, zbytes);
-                    bulk_load(b_base + sb * B_STAGE, q.zs + int64_t(kb) * zbytes, zbytes, b_full + 8 * sb);
+                    bulk_load(b_base + sb * B_STAGE, q_zs + int64_t(kb) * zbytes, zbytes, b_full + 8 * sb);
                     const int8_t* xt = p.xs + (mt * p.kblocks + kb) * int64_t(S * A_TILE);
                     for (int sp = 0; sp < S; ++sp, ++ja) {
                         const int sa = int(ja % A_STAGES);
@@ -356,14 +362,14 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
         const int quarter = warp & 3;           // TMEM lanes 32*quarter .. +31
         const int r_loc = quarter * 32 + lane;  // tile row of this thread
         const unsigned lane_addr = tmem + (unsigned(quarter * 32) << 16);
-        double* carry = q.work + (3 * int64_t(c) + 2) * OZ_PARTIAL;
+        double* carry = q_work + (3 * int64_t(c) + 2) * OZ_PARTIAL;
         unsigned ph = 0;
         for (int64_t si = 0; si < wk.nseg; ++si) {
             const int64_t t = wk.tile(si);
             const int kb0 = wk.kb(t), kb1 = wk.ke(t);
             const int64_t row = t * OZ_BM + r_loc;
             const bool full_tile = kb0 == 0 && kb1 == p.kblocks;
-            double* piece = q.work + (3 * int64_t(c) + (t == wk.t_last ? 0 : 1)) * OZ_PARTIAL;
+            double* piece = q_work + (3 * int64_t(c) + (t == wk.t_last ? 0 : 1)) * OZ_PARTIAL;
             const int er = row < p.M ? p.ex[row] : 0;   // loaded while the MMAs run
             for (int cb = kb0; cb < kb1; cb += CHUNK_KB) {
                 const bool first_chunk = cb == kb0, last_chunk = cb + CHUNK_KB >= kb1;
@@ -407,13 +413,13 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
                         if (p.beta != 0.0) {
 #pragma unroll
                             for (int j = 0; j < 16; ++j)
-                                old_c[j] = g + j < q.N ? q.C[int64_t(g + j) * p.ldc + row] : 0.0;
+                                old_c[j] = g + j < q_N ? q_C[int64_t(g + j) * p.ldc + row] : 0.0;
                         }
 #pragma unroll
                         for (int j = 0; j < 16; ++j) {
-                            if (g + j < q.N) {
+                            if (g + j < q_N) {
                                 const double val = p.alpha * mul_pow2(acc[j], er + ez_s[g + j]);
-                                q.C[int64_t(g + j) * p.ldc + row] = p.beta != 0.0 ? fma(p.beta, old_c[j], val) : val;
+                                q_C[int64_t(g + j) * p.ldc + row] = p.beta != 0.0 ? fma(p.beta, old_c[j], val) : val;
                             }
                         }
                     }
