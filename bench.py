@@ -216,7 +216,7 @@ def sketch_roofline(eng, dev):
 
 
 def load_traffic():
-    path = os.path.join(ROOT, "profiles", "traffic_r02.json")
+    path = os.path.join(ROOT, "profiles", "traffic_r04.json")
     try:
         with open(path) as f:
             return json.load(f)
