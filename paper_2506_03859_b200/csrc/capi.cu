@@ -398,6 +398,15 @@ fqb_status fqb_frob_norm_sq(fqb_handle h, const double* a, int64_t m, int64_t n,
     });
 }
 
+fqb_status fqb_set_fp32_slices(fqb_handle h, int slices) {
+    return guarded([&]() -> fqb_status {
+        if (!h) throw farqb::Error(FQB_ERR_INVALID_ARGUMENT, "null handle");
+        if (slices != 4 && slices != 8) throw farqb::Error(FQB_ERR_INVALID_ARGUMENT, "slices must be 4 or 8");
+        h->h.fp32_slices = slices;
+        return FQB_OK;
+    });
+}
+
 fqb_status fqb_sym_eig(fqb_handle h, const double* a, int n, int64_t lda, double* w, double* v, int64_t ldv,
                        int* used_small) {
     return guarded([&]() -> fqb_status {

@@ -149,6 +149,8 @@ class QbRun {
         w.counts.ensure(size_t(b), s_);
         ensure_gemm_workspace(h_);
         oz_on_ = ozaki_default(m_, n_, b_);
+        // FP32 input may opt into FP32-class A passes (4 slices: half the bytes)
+        oz_nsl_ = (af_ && h_.fp32_slices == 4) ? 4 : 8;
         double* sm = w.small.ptr;
         S_ = sm;
         S2_ = sm + 1 * b * b;
@@ -275,8 +277,8 @@ class QbRun {
     bool prepare_ozaki(double* norm_out = nullptr) {
         Workspace& w = h_.ws;
         try {
-            w.oz_x_nn.ensure(size_t(ozaki_x_bytes(m_, n_)), s_);
-            w.oz_x_tn.ensure(size_t(ozaki_x_bytes(n_, m_)), s_);
+            w.oz_x_nn.ensure(size_t(ozaki_x_bytes(m_, n_, oz_nsl_)), s_);
+            w.oz_x_tn.ensure(size_t(ozaki_x_bytes(n_, m_, oz_nsl_)), s_);
         } catch (const Error&) {
             cudaGetLastError();   // clear the allocation failure
             w.oz_x_nn.release();
@@ -290,10 +292,10 @@ class QbRun {
         double* np = norm_out ? w.oz_norm_partial.ptr : nullptr;
         if (af_)
             ozaki_slice_a(af_, m_, n_, lda_, w.oz_line_max.ptr, w.oz_x_tn.ptr, w.oz_e_tn.ptr, w.oz_x_nn.ptr,
-                          w.oz_e_nn.ptr, s_, h_.lc, np, norm_out);
+                          w.oz_e_nn.ptr, s_, h_.lc, np, norm_out, oz_nsl_);
         else
             ozaki_slice_a(a_, m_, n_, lda_, w.oz_line_max.ptr, w.oz_x_tn.ptr, w.oz_e_tn.ptr, w.oz_x_nn.ptr,
-                          w.oz_e_nn.ptr, s_, h_.lc, np, norm_out);
+                          w.oz_e_nn.ptr, s_, h_.lc, np, norm_out, oz_nsl_);
         return true;
     }
 
@@ -325,10 +327,10 @@ class QbRun {
             }
         }
         Workspace& w = h_.ws;
-        w.oz_z.ensure(size_t(ozaki_apply_z_bytes(K)), s_);
+        w.oz_z.ensure(size_t(ozaki_apply_z_bytes(K, oz_nsl_)), s_);
         w.oz_ez.ensure(size_t(ozaki_apply_ez_count()), s_);
         ozaki_apply(M, N, K, 1.0, ta ? w.oz_x_tn.ptr : w.oz_x_nn.ptr, ta ? w.oz_e_tn.ptr : w.oz_e_nn.ptr, B, ldb, 0.0,
-                    C, ldc, w.oz_z.ptr, w.oz_ez.ptr, h_.gws.work, h_.num_sms, s_, h_.lc);
+                    C, ldc, w.oz_z.ptr, w.oz_ez.ptr, h_.gws.work, h_.num_sms, s_, h_.lc, oz_nsl_);
     }
 
     // ---- Omega ----------------------------------------------------------------
@@ -618,6 +620,7 @@ class QbRun {
     double om_p_ = 0.0;
     DeviceArray<double> q_, bt_, rowsum_;
     bool oz_on_ = false;              // A-pass products on the INT8 tensor cores (a_gemm)
+    int oz_nsl_ = 8;                  // slices per operand of the A passes (8: FP64-class, 4: FP32-class)
     bool oz_ready_ = false;           // A sliced for this run (buffers live in the handle workspace)
     std::vector<double> residuals_;
     std::vector<int> ids_;

@@ -59,11 +59,19 @@ constexpr int OZ_BN = 64;                // max N (8 diagonals x 64 = 512 TMEM c
 constexpr int B_STAGES = 2;
 constexpr int A_TILE = OZ_BM * OZ_BK;             // 8 KB, one slice
 constexpr int B_TILE = OZ_BN * OZ_BK;             // 4 KB per slice (bn = 64)
-constexpr int B_STAGE = S * B_TILE;               // 32 KB: all slices of a k-block
-constexpr int A_STAGES = (225 * 1024 - B_STAGES * B_STAGE) / A_TILE;   // 20: 160 KB of A in flight
+// Per slice count NSL (8: FP64-class, 4: FP32-class for FP32 input): the Z stage holds
+// all NSL slices of a k-block, the rest of 225 KB is the A ring, TMEM holds NSL diagonals.
+template <int NSL>
+struct Sl {
+    static constexpr int B_STAGE = NSL * B_TILE;                                   // 32 / 16 KB
+    static constexpr int A_STAGES = (225 * 1024 - B_STAGES * B_STAGE) / A_TILE;     // 20 / 24
+    static constexpr size_t SMEM = size_t(A_STAGES) * A_TILE + size_t(B_STAGES) * B_STAGE + 1024;
+    static constexpr unsigned TMEM_COLS = unsigned(NSL * OZ_BN);                    // 512 / 256
+};
+constexpr int B_STAGE = Sl<S>::B_STAGE;
+constexpr int A_STAGES = Sl<S>::A_STAGES;
 constexpr int CHUNK_KB = 32768 / OZ_BK;           // int32 safety: 8 * 64^2 * 32768 < 2^31
 constexpr int OZ_THREADS = 192;                   // producer, MMA, 4 epilogue warps
-constexpr size_t OZ_SMEM = size_t(A_STAGES) * A_TILE + size_t(B_STAGES) * B_STAGE + 1024;
 constexpr int OZ_PARTIAL = OZ_BM * OZ_BN;         // doubles per CTA partial slot
 
 // 64-bit quotient through a double reciprocal and one correction step (operands are
@@ -223,8 +231,10 @@ struct Walk {
 
 // PAIR: the clustered two-chunk variant (a separate instantiation, so the single
 // chunk kernel carries none of its branches -- they cost ~4 us per pass when shared)
-template <bool PAIR>
+template <bool PAIR, int NSL>
 __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
+    constexpr int A_STAGES = Sl<NSL>::A_STAGES;
+    constexpr int B_STAGE = Sl<NSL>::B_STAGE;
     FQB_PDL_ENTRY();
     extern __shared__ uint8_t smem_raw[];
     __shared__ uint64_t bars[2 * A_STAGES + 2 * B_STAGES + 2];
@@ -260,8 +270,8 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
     }
     if (threadIdx.x < OZ_BN) ez_s[threadIdx.x] = int(threadIdx.x) < q_N ? q_ez[threadIdx.x] : 0;
     if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
-            smem_u32(&tmem_base_s)));
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+            smem_u32(&tmem_base_s)), "n"(Sl<NSL>::TMEM_COLS));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n");
@@ -276,7 +286,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
 
     if (warp == 0) {
         if (lane == 0) {
-            const unsigned zbytes = unsigned(S * bn * OZ_BK);
+            const unsigned zbytes = unsigned(NSL * bn * OZ_BK);
             int64_t ja = 0, jb = 0;
             for (int64_t si = 0; si < wk.nseg; ++si) {
                 const int64_t t = wk.tile(si);
@@ -286,8 +296,8 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
                     mbar_wait(b_empty + 8 * sb, unsigned((jb / B_STAGES) & 1) ^ 1u);
                     mbar_expect_tx(b_full + 8 * sb, zbytes);
                     bulk_load(b_base + sb * B_STAGE, q_zs + int64_t(kb) * zbytes, zbytes, b_full + 8 * sb);
-                    const int8_t* xt = p.xs + (mt * p.kblocks + kb) * int64_t(S * A_TILE);
-                    for (int sp = 0; sp < S; ++sp, ++ja) {
+                    const int8_t* xt = p.xs + (mt * p.kblocks + kb) * int64_t(NSL * A_TILE);
+                    for (int sp = 0; sp < NSL; ++sp, ++ja) {
                         const int sa = int(ja % A_STAGES);
                         mbar_wait(a_empty + 8 * sa, unsigned((ja / A_STAGES) & 1) ^ 1u);
                         mbar_expect_tx(a_full + 8 * sa, unsigned(A_TILE));
@@ -322,17 +332,17 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
                         mbar_wait(b_full + 8 * sb, pb);
                         const unsigned db_lo = db_lo0 + sb * unsigned(B_STAGE >> 4);
 #pragma unroll
-                        for (int sp = 0; sp < S; ++sp) {
+                        for (int sp = 0; sp < NSL; ++sp) {
                             mbar_wait(a_full + 8 * sa, pa);
                             asm volatile("tcgen05.fence::after_thread_sync;\n");
                             const unsigned da_lo = da_lo0 + sa * unsigned(A_TILE >> 4);
                             // products (sp, sq), sq = sq0 .. sq0+3, land on the consecutive
                             // diagonals sp+sq: one N = 64 * slices MMA covers them (A read once)
 #pragma unroll
-                            for (int sq0 = 0; sq0 < S - sp; sq0 += 4) {
+                            for (int sq0 = 0; sq0 < NSL - sp; sq0 += 4) {
                                 constexpr unsigned kstep = 32 >> 4;   // 32 bytes of K per MMA
                                 const unsigned id =
-                                    idesc | (unsigned((S - sp - sq0 < 4 ? S - sp - sq0 : 4) * (OZ_BN >> 3)) << 17);
+                                    idesc | (unsigned((NSL - sp - sq0 < 4 ? NSL - sp - sq0 : 4) * (OZ_BN >> 3)) << 17);
                                 const unsigned dt = tmem + unsigned((sp + sq0) * OZ_BN);
                                 const unsigned bl = db_lo + unsigned((sq0 * OZ_BN * OZ_BK) >> 4);
                                 umma_i8(dt, da_lo, bl, d_hi, id, sp == 0 ? unsigned(kb != cb) : 1u);
@@ -379,16 +389,16 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
 #pragma unroll 1
                 for (int g = 0; g < OZ_BN; g += 16) {
                     // all 8 diagonals in flight, one wait
-                    unsigned v[S][16];
+                    unsigned v[NSL][16];
 #pragma unroll
-                    for (int d = 0; d < S; ++d) tmem_ld16(lane_addr + unsigned(d * OZ_BN + g), v[d]);
+                    for (int d = 0; d < NSL; ++d) tmem_ld16(lane_addr + unsigned(d * OZ_BN + g), v[d]);
                     asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
                     double acc[16];
 #pragma unroll
                     for (int j = 0; j < 16; ++j) acc[j] = 0.0;
                     // least significant diagonal first: d = S-1 .. 0 (scale 2^-12-7d)
 #pragma unroll
-                    for (int d = S - 1; d >= 0; --d) {
+                    for (int d = NSL - 1; d >= 0; --d) {
                         const double sc = pow2i(-12 - 7 * d);
 #pragma unroll
                         for (int j = 0; j < 16; ++j) acc[j] = fma(double(int(v[d][j])), sc, acc[j]);
@@ -432,7 +442,8 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
     asm volatile("tcgen05.fence::before_thread_sync;\n");
     __syncthreads();
     if constexpr (PAIR) cluster_sync();   // no CTA leaves while its peer may still arrive on its barriers
-    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(Sl<NSL>::TMEM_COLS));
 }
 
 // ---------------------------------------------------------------------------
@@ -463,7 +474,7 @@ __device__ __forceinline__ int exp_of_hi(unsigned hi) {
 
 // the 8 digits of x in line scale e, as raw fields d_p + 64 in [0, 128]: the 7-bit
 // fields of U = R + sum_p 64 2^(49-7p), read from its two 32-bit halves
-__device__ __forceinline__ void digits8(double x, int e, unsigned (&d)[S]) {
+__device__ __forceinline__ void digits8(double x, int e, unsigned (&d)[8]) {
     const unsigned long long U = static_cast<unsigned long long>(__double2ll_rn(mul_pow2(x, 55 - e)) + kDigitBias);
     const unsigned hi = unsigned(U >> 32), lo = unsigned(U);
     d[0] = hi >> 17;
@@ -476,31 +487,48 @@ __device__ __forceinline__ void digits8(double x, int e, unsigned (&d)[S]) {
     d[7] = lo & 127u;
 }
 
+// NSL = 4 (FP32-class): R = rint(x 2^(27-e)), |R| <= 2^27, four digits of the same
+// weights 2^(e-6-7p), p = 0..3, from the 32-bit U = R + 64 (2^21 + 2^14 + 2^7 + 1)
+constexpr int kDigitBias4 = (64 << 21) + (64 << 14) + (64 << 7) + 64;
+__device__ __forceinline__ void digits4(double x, int e, unsigned (&d)[4]) {
+    const unsigned U = unsigned(__double2int_rn(mul_pow2(x, 27 - e)) + kDigitBias4);
+    d[0] = (U >> 21) & 255u;
+    d[1] = (U >> 14) & 127u;
+    d[2] = (U >> 7) & 127u;
+    d[3] = U & 127u;
+}
+template <int NSL>
+__device__ __forceinline__ void digits(double x, int e, unsigned (&d)[NSL]) {
+    if constexpr (NSL == 8) digits8(x, e, d);
+    else digits4(x, e, d);
+}
+
 // byte offset of (row r, byte c) inside a swizzled TR x OZ_BK byte tile
 // (64B swizzle: the 16-byte chunk index c>>4 is XORed with address bits 7-8 = (r >> 1) & 3)
 __device__ __forceinline__ int swz(int r, int c) { return r * OZ_BK + ((((c >> 4) ^ ((r >> 1) & 3)) << 4) | (c & 15)); }
 
 // 16 consecutive K-values of one operand row -> one 16-byte chunk per slice
+template <int NSL>
 __device__ __forceinline__ void put_chunk16(const double (&v)[16], int e, int8_t* tile0, int64_t slice_stride, int r,
                                             int c) {
-    uint32_t w[S][4];
+    uint32_t w[NSL][4];
 #pragma unroll
-    for (int sl = 0; sl < S; ++sl) w[sl][0] = w[sl][1] = w[sl][2] = w[sl][3] = 0;
+    for (int sl = 0; sl < NSL; ++sl) w[sl][0] = w[sl][1] = w[sl][2] = w[sl][3] = 0;
 #pragma unroll
     for (int u = 0; u < 16; ++u) {
-        unsigned d[S];
-        digits8(v[u], e, d);
+        unsigned d[NSL];
+        digits<NSL>(v[u], e, d);
 #pragma unroll
-        for (int sl = 0; sl < S; ++sl) w[sl][u >> 2] |= d[sl] << (8 * (u & 3));
+        for (int sl = 0; sl < NSL; ++sl) w[sl][u >> 2] |= d[sl] << (8 * (u & 3));
     }
     // raw fields -> signed digits: (d - 64) mod 256 per byte, four at a time
 #pragma unroll
-    for (int sl = 0; sl < S; ++sl)
+    for (int sl = 0; sl < NSL; ++sl)
 #pragma unroll
         for (int q = 0; q < 4; ++q) w[sl][q] = __vadd4(w[sl][q], 0xC0C0C0C0u);
     int8_t* dst = tile0 + swz(r, c);
 #pragma unroll
-    for (int sl = 0; sl < S; ++sl)
+    for (int sl = 0; sl < NSL; ++sl)
         *reinterpret_cast<uint4*>(dst + sl * slice_stride) = make_uint4(w[sl][0], w[sl][1], w[sl][2], w[sl][3]);
 }
 
@@ -575,7 +603,7 @@ __global__ void __launch_bounds__(1024) k_sum_ordered(const double* __restrict__
 //   x_nn: operand rows = rows of A,    K = n (A G),   e_nn per row
 // Either may be null.  The grid covers the padded operand rows, so every byte of
 // both slice buffers is written (zeros outside A) and no memset is needed.
-template <typename T>
+template <typename T, int NSL>
 __global__ void __launch_bounds__(256) k_slice_a(const T* __restrict__ a, int64_t m, int64_t n, int64_t ld,
                                                  const unsigned* __restrict__ rmax, const unsigned* __restrict__ cmax,
                                                  int8_t* x_tn, int* e_tn, int8_t* x_nn, int* e_nn) {
@@ -610,8 +638,8 @@ __global__ void __launch_bounds__(256) k_slice_a(const T* __restrict__ a, int64_
 #pragma unroll
         for (int u = 0; u < 16; ++u) v[u] = t[line][q * 16 + u];
         const int64_t kb_count = (m + OZ_BK - 1) / OZ_BK;
-        int8_t* tile0 = x_tn + ((j / OZ_BM) * kb_count + i0 / OZ_BK) * S * int64_t(A_TILE);
-        put_chunk16(v, e, tile0, A_TILE, int(j % OZ_BM), q * 16);
+        int8_t* tile0 = x_tn + ((j / OZ_BM) * kb_count + i0 / OZ_BK) * NSL * int64_t(A_TILE);
+        put_chunk16<NSL>(v, e, tile0, A_TILE, int(j % OZ_BM), q * 16);
     }
     if (x_nn && j0 < round_up_dev(n, OZ_BK)) {                  // rows of A: rows i, K = j
         const int64_t i = i0 + line;
@@ -621,8 +649,8 @@ __global__ void __launch_bounds__(256) k_slice_a(const T* __restrict__ a, int64_
 #pragma unroll
         for (int u = 0; u < 16; ++u) v[u] = t[q * 16 + u][line];
         const int64_t kb_count = (n + OZ_BK - 1) / OZ_BK;
-        int8_t* tile0 = x_nn + ((i / OZ_BM) * kb_count + j0 / OZ_BK) * S * int64_t(A_TILE);
-        put_chunk16(v, e, tile0, A_TILE, int(i % OZ_BM), q * 16);
+        int8_t* tile0 = x_nn + ((i / OZ_BM) * kb_count + j0 / OZ_BK) * NSL * int64_t(A_TILE);
+        put_chunk16<NSL>(v, e, tile0, A_TILE, int(i % OZ_BM), q * 16);
     }
 }
 
@@ -631,6 +659,7 @@ __global__ void __launch_bounds__(256) k_slice_a(const T* __restrict__ a, int64_
 // column max itself (the column is small and L2-resident), so one launch does it;
 // (ZT = 256 measured faster than 512 at C2: 7.7 vs 9.6 us)
 constexpr int ZT = 256;
+template <int NSL>
 __global__ void __launch_bounds__(ZT) k_slice_z(const double* __restrict__ b, int64_t k, int64_t n, int64_t ld,
                                                 int* ez, int8_t* out) {
     FQB_PDL_ENTRY();
@@ -662,7 +691,7 @@ __global__ void __launch_bounds__(ZT) k_slice_z(const double* __restrict__ b, in
     double v[16];
 #pragma unroll
     for (int u = 0; u < 16; ++u) v[u] = (live && k0 + u < k) ? col[k0 + u] : 0.0;
-    put_chunk16(v, e, out + (k0 / OZ_BK) * S * z_tile, z_tile, j, int(k0 % OZ_BK));
+    put_chunk16<NSL>(v, e, out + (k0 / OZ_BK) * NSL * z_tile, z_tile, j, int(k0 % OZ_BK));
 }
 
 // Sum the pieces of every split tile in CTA order (deterministic) into C.
@@ -714,16 +743,22 @@ __global__ void __launch_bounds__(OZ_BM) k_ozaki_fixup(const OzArgs p0) {
 int ozaki_slices() { return S; }
 int ozaki_max_n() { return OZ_BN; }
 int ozaki_bn(int64_t) { return OZ_BN; }   // Z slices padded to 64 rows: slice sq sits at TMEM diagonal spacing
-int64_t ozaki_x_bytes(int64_t rows, int64_t k) { return ceil_div(rows, OZ_BM) * ceil_div(k, OZ_BK) * S * OZ_BM * OZ_BK; }
-int64_t ozaki_z_bytes(int64_t n, int64_t k) { return ceil_div(k, OZ_BK) * S * int64_t(ozaki_bn(n)) * OZ_BK; }
+int64_t ozaki_x_bytes(int64_t rows, int64_t k, int nsl) {
+    return ceil_div(rows, OZ_BM) * ceil_div(k, OZ_BK) * nsl * OZ_BM * OZ_BK;
+}
+int64_t ozaki_z_bytes(int64_t n, int64_t k, int nsl) { return ceil_div(k, OZ_BK) * nsl * int64_t(ozaki_bn(n)) * OZ_BK; }
+static void check_nsl(int nsl) {
+    if (nsl != 8 && nsl != 4) throw Error(kStatusInvalid, "ozaki: slices per operand must be 8 or 4");
+}
 
 int64_t ozaki_line_max_words(int64_t m, int64_t n) { return m + n; }
 int64_t ozaki_norm_partials(int64_t m, int64_t n) { return ceil_div(m, 256) * ceil_div(n, 128); }
 
 template <typename T>
 static void slice_a_impl(const T* a, int64_t m, int64_t n, int64_t ld, unsigned* line_max, int8_t* x_tn, int* e_tn,
-                         int8_t* x_nn, int* e_nn, double* norm_partial, double* norm_out, cudaStream_t s,
+                         int8_t* x_nn, int* e_nn, double* norm_partial, double* norm_out, int nsl, cudaStream_t s,
                          LaunchCounter& lc) {
+    check_nsl(nsl);
     if (m <= 0 || n <= 0) {
         if (norm_out) FQB_CUDA(cudaMemsetAsync(norm_out, 0, sizeof(double), s));
         return;
@@ -741,43 +776,52 @@ static void slice_a_impl(const T* a, int64_t m, int64_t n, int64_t ld, unsigned*
     }
     // cover the padded operand rows of both layouts (multiples of OZ_BM)
     const dim3 g(unsigned(ceil_div(m, OZ_BM) * (OZ_BM / 64)), unsigned(ceil_div(n, OZ_BM) * (OZ_BM / 64)));
-    launch_k(k_slice_a<T>, g, 256, 0, s, a, m, n, ld, rmax, cmax, x_tn, e_tn, x_nn, e_nn);
+    if (nsl == 8) launch_k(k_slice_a<T, 8>, g, 256, 0, s, a, m, n, ld, rmax, cmax, x_tn, e_tn, x_nn, e_nn);
+    else launch_k(k_slice_a<T, 4>, g, 256, 0, s, a, m, n, ld, rmax, cmax, x_tn, e_tn, x_nn, e_nn);
     FQB_LAUNCHED();
     lc.bump(2);
 }
 
 void ozaki_slice_a(const double* a, int64_t m, int64_t n, int64_t ld, unsigned* line_max, int8_t* x_tn, int* e_tn,
                    int8_t* x_nn, int* e_nn, cudaStream_t s, LaunchCounter& lc, double* norm_partial,
-                   double* norm_out) {
-    slice_a_impl(a, m, n, ld, line_max, x_tn, e_tn, x_nn, e_nn, norm_partial, norm_out, s, lc);
+                   double* norm_out, int nsl) {
+    slice_a_impl(a, m, n, ld, line_max, x_tn, e_tn, x_nn, e_nn, norm_partial, norm_out, nsl, s, lc);
 }
 void ozaki_slice_a(const float* a, int64_t m, int64_t n, int64_t ld, unsigned* line_max, int8_t* x_tn, int* e_tn,
                    int8_t* x_nn, int* e_nn, cudaStream_t s, LaunchCounter& lc, double* norm_partial,
-                   double* norm_out) {
-    slice_a_impl(a, m, n, ld, line_max, x_tn, e_tn, x_nn, e_nn, norm_partial, norm_out, s, lc);
+                   double* norm_out, int nsl) {
+    slice_a_impl(a, m, n, ld, line_max, x_tn, e_tn, x_nn, e_nn, norm_partial, norm_out, nsl, s, lc);
 }
 
 void ozaki_slice_z(const double* b, int64_t k, int64_t n, int64_t ld, int* e, int8_t* out, cudaStream_t s,
-                   LaunchCounter& lc) {
+                   LaunchCounter& lc, int nsl) {
     if (n <= 0 || k <= 0) return;
+    check_nsl(nsl);
     const int64_t chunks = ceil_div(k, OZ_BK) * (OZ_BK / 16);
-    launch_k(k_slice_z, dim3(OZ_BN, unsigned(ceil_div(chunks, ZT))), ZT, 0, s, b, k, n, ld, e, out);
+    const dim3 g(OZ_BN, unsigned(ceil_div(chunks, ZT)));
+    if (nsl == 8) launch_k(k_slice_z<8>, g, ZT, 0, s, b, k, n, ld, e, out);
+    else launch_k(k_slice_z<4>, g, ZT, 0, s, b, k, n, ld, e, out);
     FQB_LAUNCHED();
     lc.bump();
 }
 
 // paired (pair_cw > 0): N = 2 chunks of pair_cw columns at most, zs / ez hold both
-static void launch_ozaki(int64_t M, int64_t N, int64_t K, double alpha, const int8_t* xs, const int* ex,
-                         const int8_t* zs, const int* ez, double beta, double* C, int64_t ldc, double* work,
-                         int num_sms, int64_t pair_cw, cudaStream_t s, LaunchCounter& lc) {
+template <bool PAIR, int NSL>
+static void configure_ozaki() {
     static bool configured[64] = {};
     int dev = 0;
     FQB_CUDA(cudaGetDevice(&dev));
     if (dev < 0 || dev >= 64 || !configured[dev]) {
-        FQB_CUDA(cudaFuncSetAttribute(k_ozaki<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(OZ_SMEM)));
-        FQB_CUDA(cudaFuncSetAttribute(k_ozaki<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(OZ_SMEM)));
+        FQB_CUDA(cudaFuncSetAttribute(k_ozaki<PAIR, NSL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(Sl<NSL>::SMEM)));
         if (dev >= 0 && dev < 64) configured[dev] = true;
     }
+}
+
+static void launch_ozaki(int64_t M, int64_t N, int64_t K, double alpha, const int8_t* xs, const int* ex,
+                         const int8_t* zs, const int* ez, double beta, double* C, int64_t ldc, double* work,
+                         int num_sms, int64_t pair_cw, int nsl, cudaStream_t s, LaunchCounter& lc) {
+    check_nsl(nsl);
     const bool pair = pair_cw > 0;
     OzArgs a{};
     a.xs = xs;
@@ -803,15 +847,21 @@ static void launch_ozaki(int64_t M, int64_t N, int64_t K, double alpha, const in
     a.inv_iters = 1.0 / double(a.iters);
     a.pair = pair ? 1 : 0;
     a.cw = pair_cw;
-    a.zs_stride = ozaki_z_bytes(OZ_BN, K);
+    a.zs_stride = ozaki_z_bytes(OZ_BN, K, nsl);
     a.work_stride = 3 * int64_t(a.grid) * OZ_PARTIAL;
     if (!pair) {
-        launch_k(k_ozaki<false>, a.grid, OZ_THREADS, OZ_SMEM, s, a);
+        if (nsl == 8) {
+            configure_ozaki<false, 8>();
+            launch_k(k_ozaki<false, 8>, a.grid, OZ_THREADS, Sl<8>::SMEM, s, a);
+        } else {
+            configure_ozaki<false, 4>();
+            launch_k(k_ozaki<false, 4>, a.grid, OZ_THREADS, Sl<4>::SMEM, s, a);
+        }
     } else {
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(unsigned(2 * a.grid));
         cfg.blockDim = dim3(OZ_THREADS);
-        cfg.dynamicSmemBytes = OZ_SMEM;
+        cfg.dynamicSmemBytes = nsl == 8 ? Sl<8>::SMEM : Sl<4>::SMEM;
         cfg.stream = s;
         cudaLaunchAttribute attr[2];
         attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -822,7 +872,13 @@ static void launch_ozaki(int64_t M, int64_t N, int64_t K, double alpha, const in
         attr[1].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;
         cfg.numAttrs = pdl_enabled() ? 2 : 1;
-        FQB_CUDA(cudaLaunchKernelEx(&cfg, k_ozaki<true>, a));
+        if (nsl == 8) {
+            configure_ozaki<true, 8>();
+            FQB_CUDA(cudaLaunchKernelEx(&cfg, k_ozaki<true, 8>, a));
+        } else {
+            configure_ozaki<true, 4>();
+            FQB_CUDA(cudaLaunchKernelEx(&cfg, k_ozaki<true, 4>, a));
+        }
     }
     FQB_LAUNCHED();
     lc.bump();
@@ -839,9 +895,9 @@ static void launch_ozaki(int64_t M, int64_t N, int64_t K, double alpha, const in
 
 void ozaki_gemm(int64_t M, int64_t N, int64_t K, double alpha, const int8_t* xs, const int* ex, const int8_t* zs,
                 const int* ez, double beta, double* C, int64_t ldc, double* work, int num_sms, cudaStream_t s,
-                LaunchCounter& lc) {
+                LaunchCounter& lc, int nsl) {
     if (N > OZ_BN) throw Error(kStatusInvalid, "ozaki_gemm: N > 64");
-    launch_ozaki(M, N, K, alpha, xs, ex, zs, ez, beta, C, ldc, work, num_sms, 0, s, lc);
+    launch_ozaki(M, N, K, alpha, xs, ex, zs, ez, beta, C, ldc, work, num_sms, 0, nsl, s, lc);
 }
 
 static bool pairs_enabled() {
@@ -854,41 +910,41 @@ static bool pairs_enabled() {
 
 void ozaki_apply(int64_t M, int64_t N, int64_t K, double alpha, const int8_t* xs, const int* ex, const double* b,
                  int64_t ldb, double beta, double* C, int64_t ldc, int8_t* z, int* ez, double* work, int num_sms,
-                 cudaStream_t s, LaunchCounter& lc) {
+                 cudaStream_t s, LaunchCounter& lc, int nsl) {
     if (N <= 0) return;
     const int64_t chunks = ceil_div(N, OZ_BN);
     const int64_t cw = ceil_div(N, chunks);
-    const int64_t zstride = ozaki_z_bytes(OZ_BN, K);
+    const int64_t zstride = ozaki_z_bytes(OZ_BN, K, nsl);
     int64_t c0 = 0;
     // two chunks at a time on CTA pairs that share every A tile (multicast): A is
     // streamed once per pair of chunks instead of once per chunk
     while (pairs_enabled() && num_sms >= 2 && N - c0 > cw) {
         const int64_t nb = std::min(2 * cw, N - c0);
-        ozaki_slice_z(b + c0 * ldb, K, cw, ldb, ez, z, s, lc);
-        ozaki_slice_z(b + (c0 + cw) * ldb, K, nb - cw, ldb, ez + OZ_BN, z + zstride, s, lc);
-        launch_ozaki(M, nb, K, alpha, xs, ex, z, ez, beta, C + c0 * ldc, ldc, work, num_sms, cw, s, lc);
+        ozaki_slice_z(b + c0 * ldb, K, cw, ldb, ez, z, s, lc, nsl);
+        ozaki_slice_z(b + (c0 + cw) * ldb, K, nb - cw, ldb, ez + OZ_BN, z + zstride, s, lc, nsl);
+        launch_ozaki(M, nb, K, alpha, xs, ex, z, ez, beta, C + c0 * ldc, ldc, work, num_sms, cw, nsl, s, lc);
         c0 += nb;
     }
     for (; c0 < N; c0 += cw) {
         const int64_t nb = std::min(cw, N - c0);
-        ozaki_slice_z(b + c0 * ldb, K, nb, ldb, ez, z, s, lc);
-        ozaki_gemm(M, nb, K, alpha, xs, ex, z, ez, beta, C + c0 * ldc, ldc, work, num_sms, s, lc);
+        ozaki_slice_z(b + c0 * ldb, K, nb, ldb, ez, z, s, lc, nsl);
+        ozaki_gemm(M, nb, K, alpha, xs, ex, z, ez, beta, C + c0 * ldc, ldc, work, num_sms, s, lc, nsl);
     }
 }
 // the products of ozaki_apply again, on the B slices its last call left in z / ez
 // (N <= 128: the chunks of one launch)
 void ozaki_apply_presliced(int64_t M, int64_t N, int64_t K, double alpha, const int8_t* xs, const int* ex, double beta,
                            double* C, int64_t ldc, const int8_t* z, const int* ez, double* work, int num_sms,
-                           cudaStream_t s, LaunchCounter& lc) {
+                           cudaStream_t s, LaunchCounter& lc, int nsl) {
     if (N <= 0) return;
     if (N > 2 * OZ_BN) throw Error(kStatusInvalid, "ozaki_apply_presliced: N > 128");
     const int64_t chunks = ceil_div(N, OZ_BN);
     const int64_t cw = ceil_div(N, chunks);
     if (chunks == 2 && !(pairs_enabled() && num_sms >= 2))
         throw Error(kStatusInvalid, "ozaki_apply_presliced: two chunks need the paired launch");
-    launch_ozaki(M, N, K, alpha, xs, ex, z, ez, beta, C, ldc, work, num_sms, chunks == 2 ? cw : 0, s, lc);
+    launch_ozaki(M, N, K, alpha, xs, ex, z, ez, beta, C, ldc, work, num_sms, chunks == 2 ? cw : 0, nsl, s, lc);
 }
-int64_t ozaki_apply_z_bytes(int64_t K) { return 2 * ozaki_z_bytes(OZ_BN, K); }
+int64_t ozaki_apply_z_bytes(int64_t K, int nsl) { return 2 * ozaki_z_bytes(OZ_BN, K, nsl); }
 int ozaki_apply_ez_count() { return 2 * OZ_BN; }
 int64_t ozaki_workspace_doubles(int num_sms) { return 3 * int64_t(num_sms) * OZ_PARTIAL; }  // 2 pieces + carry
 

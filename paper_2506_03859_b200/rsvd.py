@@ -622,6 +622,13 @@ class Engine:
             _raise(st, "fqb_relative_error")
         return out.value
 
+    def set_fp32_slices(self, slices: int) -> None:
+        """FP32 inputs: 8 slices per operand (FP64-class A passes, default) or 4 (FP32-class,
+        about twice as fast; fqb_set_fp32_slices)."""
+        st = self._lib.fqb_set_fp32_slices(self._h, int(slices))
+        if st:
+            _raise(st, "fqb_set_fp32_slices")
+
     def sym_eig(self, a):
         """Symmetric eigendecomposition on the device (fqb_sym_eig, the SVD assembly's solver):
         a torch float64 n x n (CUDA) -> (w ascending, V) as torch tensors, and whether the

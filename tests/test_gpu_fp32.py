@@ -117,3 +117,48 @@ def test_c5_shape_slice_fp32(eng):
         d = a[:, c0:c0 + 1024].double() - q @ bt[c0:c0 + 1024].t()
         tot += float((d * d).sum())
     assert abs(res.residual_sq - tot) <= 1e-10 * res.norm_a_sq
+
+
+@pytest.fixture
+def eng4():
+    """A separate engine with FP32-class A passes (fqb_set_fp32_slices(4))."""
+    e = fqb.Engine(0)
+    e.set_fp32_slices(4)
+    yield e
+    e.close()
+
+
+@pytest.mark.parametrize("kind,zeta", [(0, 0), (2, 0), (3, 4), (4, 4)])
+def test_fp32_four_slices_within_the_fp32_contract(eng, eng4, port, monkeypatch, kind, zeta):
+    """4 slices per operand: FP32-class products.  Against the FP64 oracle on double(A):
+    the same rank / blocks / ids and E within the FP32-mode bar (1e-4 relative); against
+    the 8-slice run on the same A and Omega: Q B within 1e-6 of A's scale (the QB of one
+    sketch is unique, so this isolates the precision of the products)."""
+    monkeypatch.setenv("FQB_OZAKI", "1")
+    a32 = _lowrank32(900, 600, 1.0 / np.arange(1, 121), seed=70 + kind, noise=1e-3)
+    p = 0.0 if kind == 0 or zeta else 0.5
+    spec = SketchSpec(kind, p, 9, zeta=zeta)
+    cfg = FarpcaConfig(eps=5e-2, power=1, block=32, sketch=spec, relative=True)
+    res = eng4.run_fixed_precision(a32, cfg, output="host")
+    a64 = np.asfortranarray(a32.astype(np.float64))
+    ref = port.run(a64, eps=5e-2, power=1, block=32, kind=kind, p=p, seed=9, zeta=zeta, relative=True,
+                   source=_src(eng4, spec))
+    assert ref.status == 0 and res.converged
+    assert (res.rank, res.blocks, res.block_ids) == (ref.rank, ref.blocks, ref.block_ids)
+    na = ref.norm_a_sq
+    assert abs(res.residual_sq - ref.residual_sq) <= 1e-4 * ref.residual_sq
+    assert np.abs(res.q.T @ res.q - np.eye(res.rank)).max() < 1e-10
+    r8 = eng.run_fixed_precision(a32, cfg, output="host")
+    diff = np.abs(res.q @ res.bt.T - r8.q @ r8.bt.T).max()
+    assert diff <= 1e-6 * np.abs(a64).max(), diff
+    assert diff > 0.0   # different arithmetic really ran
+
+
+def test_fp32_four_slices_default_is_eight(eng, monkeypatch):
+    """The default engine keeps FP64-class passes for FP32 input (bit-equal to double(A))."""
+    monkeypatch.setenv("FQB_OZAKI", "1")
+    a32 = _lowrank32(700, 500, 0.9 ** np.arange(100), seed=4)
+    cfg = FarpcaConfig(eps=1e-2, power=1, block=20, sketch=SketchSpec(0, 0.0, 3), relative=True)
+    r32 = eng.run_fixed_precision(a32, cfg, output="host")
+    r64 = eng.run_fixed_precision(np.asfortranarray(a32.astype(np.float64)), cfg, output="host")
+    assert np.array_equal(r32.bt, r64.bt)
