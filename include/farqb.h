@@ -258,10 +258,10 @@ fqb_status fqb_set_fp32_slices(fqb_handle h, int slices);
 
 /* Symmetric eigendecomposition (device pointers; both triangles of A read):
  * eigenvalues ascending into w (n), eigenvectors into V (n x n, ldv).  The solver of
- * the SVD assembly: cuSOLVER syevd by default; with FQB_EIG=small and n <= 224 a
- * tridiagonal bisection / inverse-iteration solver verified a posteriori (residual
- * and orthogonality at 64 n u, syevd when the check fails).  *used_small (nullable)
- * = 1 when the latter produced the result. */
+ * the SVD assembly: for n <= 224 a one-CTA Householder tridiagonalisation + bisection /
+ * inverse-iteration solver verified a posteriori (residual and orthogonality at 64 n u;
+ * cuSOLVER syevd when the check fails or FQB_EIG=syevd), cuSOLVER syevd above.
+ * *used_small (nullable) = 1 when the former produced the result. */
 fqb_status fqb_sym_eig(fqb_handle h, const double* a, int n, int64_t lda, double* w, double* v, int64_t ldv,
                        int* used_small);
 /* Exact relative error ||A - U diag(sigma) V'||_F / ||A||_F (experiment.cpp:317-342),

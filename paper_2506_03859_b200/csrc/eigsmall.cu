@@ -174,6 +174,228 @@ __global__ void __launch_bounds__(kTrdThreads) k_sytrd(const double* __restrict_
 }
 
 // ---------------------------------------------------------------------------
+// Tridiagonalisation, register-vector form (n <= kTrd4Max): 16 warps, warp w owns rows
+// t0 + w, t0 + w + 16, ...; a lane owns columns j = 32 q + lane, q = 0..6, and keeps
+// v_j, w_j and its column-sum share of p = A22 v in registers, so a row costs one
+// load + two FMAs per 32-column chunk and one warp reduction, and the strict-lower
+// column sums need no atomics: each warp's 224 column partials go to shared memory
+// once per step.  A row's chunk count qi = i / 32 selects a specialised, fully
+// unrolled body (no per-chunk branches); the window start t0 enters as a per-lane
+// mask fixed for the step.  (A first version with per-chunk guards spent 29 % of its
+// 18k instructions per step on integer compares; 1.06 ms at n = 200.)
+constexpr int kTrd4Max = 208;     // packed A + 16 x 224 partials fit in 227 KB
+constexpr int kTrd4Warps = 16;
+constexpr int kTrd4Q = 7;         // 7 x 32 = 224 >= kTrd4Max columns
+
+// p-row: racc = sum_{t0 <= j <= i} A(i,j) v_j;  colacc[q] += A(i,j) v_i (j < i)
+template <int QI>
+__device__ __forceinline__ double trd_row_p(const double* __restrict__ row, const double (&vreg)[kTrd4Q],
+                                            const double (&lom)[kTrd4Q], double (&colacc)[kTrd4Q], int lane,
+                                            int li, double vi) {
+    double racc = 0.0;
+#pragma unroll
+    for (int q = 0; q <= QI; ++q) {
+        double a = row[32 * q + lane] * lom[q];              // lom: 1 for j >= t0, else 0
+        if (q == QI) a = lane <= li ? a : 0.0;               // j <= i
+        racc = fma(a, vreg[q], racc);
+        const double as = (q == QI && lane == li) ? 0.0 : a;   // strict lower for the column part
+        colacc[q] = fma(as, vi, colacc[q]);
+    }
+    return racc;
+}
+template <int QI>
+__device__ __forceinline__ void trd_row_u(double* __restrict__ row, const double (&vreg)[kTrd4Q],
+                                          const double (&wreg)[kTrd4Q], const double (&lom)[kTrd4Q], int lane,
+                                          int li, double vi, double wi) {
+    // all loads of the row first: interleaved with the stores, the possible aliasing
+    // would serialise every chunk on its load latency
+    double x[QI + 1];
+#pragma unroll
+    for (int q = 0; q <= QI; ++q) x[q] = row[32 * q + lane];
+#pragma unroll
+    for (int q = 0; q <= QI; ++q) {
+        const bool in = lom[q] != 0.0 && (q < QI || lane <= li);
+        if (in) row[32 * q + lane] = fma(-vi, wreg[q], fma(-wi, vreg[q], x[q]));
+    }
+}
+
+__global__ void __launch_bounds__(kTrd4Warps * 32, 1) k_sytrd4(const double* __restrict__ mat, int n, double* d,
+                                                               double* e, double* tau_out, double* vh) {
+    FQB_PDL_ENTRY();
+    extern __shared__ double sm[];
+    double* A = sm;                                   // packed lower, row-major (+ slack for over-reads)
+    double* vv = A + ri(n) + 224;                     // v (absolute index), zero outside [t0, n)
+    double* ww = vv + 224;                            // w
+    double* rs = ww + 224;                            // row sums of A22 v
+    double* part = rs + 224;                          // [16][224] column partials
+    __shared__ double red[kTrd4Warps];
+    __shared__ double sc[2];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int NT = kTrd4Warps * 32;
+    for (int i = warp; i < n; i += kTrd4Warps)
+        for (int j = lane; j <= i; j += 32) A[ri(i) + j] = mat[int64_t(j) * n + i];
+    for (int i = tid; i < 224; i += NT) vv[i] = ww[i] = 0.0;
+    __syncthreads();
+#ifdef FQB_TRD_PROBE
+    long long tp[6] = {0, 0, 0, 0, 0, 0};
+    long long tl = clock64();
+#define TRD_STAMP(x)                       \
+    {                                      \
+        const long long tn_ = clock64();   \
+        tp[x] += tn_ - tl;                 \
+        tl = tn_;                          \
+    }
+#else
+#define TRD_STAMP(x)
+#endif
+    for (int k = 0; k + 2 < n; ++k) {
+        const int t0 = k + 1;
+        if (warp == 0) {
+            // the column below the diagonal, read once (7 strided loads per lane at most)
+            double xc[kTrd4Q];
+            double ss = 0.0;
+#pragma unroll
+            for (int q = 0; q < kTrd4Q; ++q) {
+                const int i = t0 + 1 + 32 * q + lane;
+                xc[q] = i < n ? A[ri(i) + k] : 0.0;
+                ss = fma(xc[q], xc[q], ss);
+            }
+            ss = warp_sum(ss);
+            const double alpha = A[ri(t0) + k];
+            double tau = 0.0, beta = alpha, scal = 0.0;
+            if (ss > 0.0) {
+                beta = -copysign(sqrt(fma(alpha, alpha, ss)), alpha);
+                tau = (beta - alpha) / beta;
+                scal = 1.0 / (alpha - beta);
+            }
+#pragma unroll
+            for (int q = 0; q < kTrd4Q; ++q) {
+                const int i = t0 + 1 + 32 * q + lane;
+                if (i < n) {
+                    const double v = xc[q] * scal;   // scal = 0 when tau = 0
+                    if (tau != 0.0) A[ri(i) + k] = v;
+                    vv[i] = v;
+                }
+            }
+            if (lane == 0) {
+                vv[t0] = 1.0;
+                vv[k] = 0.0;   // the previous step's leading entry leaves the window
+                sc[0] = tau;
+                d[k] = A[ri(k) + k];
+                e[k] = beta;
+                tau_out[k] = tau;
+            }
+        }
+        __syncthreads();
+        TRD_STAMP(0)
+        const double tau = sc[0];
+        if (tau == 0.0) continue;   // uniform
+        double vreg[kTrd4Q], colacc[kTrd4Q], lom[kTrd4Q];
+#pragma unroll
+        for (int q = 0; q < kTrd4Q; ++q) {
+            vreg[q] = vv[32 * q + lane];   // zero outside [t0, n)
+            colacc[q] = 0.0;
+            lom[q] = 32 * q + lane >= t0 ? 1.0 : 0.0;
+        }
+        // ---- p = A22 v: row sums (lower incl. diagonal) + strict-lower column sums
+        // rows in pairs (i, i + 16): the two row reductions run as interleaved shuffle chains
+        auto row_p = [&](int i) -> double {
+            const double vi = vv[i];
+            const double* row = A + ri(i);
+            const int li = i & 31;
+            switch (i >> 5) {
+                case 0: return trd_row_p<0>(row, vreg, lom, colacc, lane, li, vi);
+                case 1: return trd_row_p<1>(row, vreg, lom, colacc, lane, li, vi);
+                case 2: return trd_row_p<2>(row, vreg, lom, colacc, lane, li, vi);
+                case 3: return trd_row_p<3>(row, vreg, lom, colacc, lane, li, vi);
+                case 4: return trd_row_p<4>(row, vreg, lom, colacc, lane, li, vi);
+                case 5: return trd_row_p<5>(row, vreg, lom, colacc, lane, li, vi);
+                default: return trd_row_p<6>(row, vreg, lom, colacc, lane, li, vi);
+            }
+        };
+        for (int i = t0 + warp; i < n; i += 2 * kTrd4Warps) {
+            const int i2 = i + kTrd4Warps;
+            double r1 = row_p(i);
+            double r2 = i2 < n ? row_p(i2) : 0.0;
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                r1 += __shfl_xor_sync(0xFFFFFFFFu, r1, off);
+                r2 += __shfl_xor_sync(0xFFFFFFFFu, r2, off);
+            }
+            if (lane == 0) {
+                rs[i] = r1;
+                if (i2 < n) rs[i2] = r2;
+            }
+        }
+        TRD_STAMP(1)
+#pragma unroll
+        for (int q = 0; q < kTrd4Q; ++q) part[warp * 224 + 32 * q + lane] = colacc[q];
+        __syncthreads();
+        TRD_STAMP(2)
+        // ---- p, K = (tau / 2) p'v, w = p - K v
+        double pv = 0.0, pt = 0.0;
+        if (tid >= t0 && tid < n) {
+            double acc = rs[tid];
+#pragma unroll
+            for (int w = 0; w < kTrd4Warps; ++w) acc += part[w * 224 + tid];
+            pt = tau * acc;
+            pv = pt * vv[tid];
+        }
+        pv = warp_sum(pv);
+        if (lane == 0) red[warp] = pv;
+        __syncthreads();
+        if (warp == 0) {
+            const double t = warp_sum(lane < kTrd4Warps ? red[lane] : 0.0);
+            if (lane == 0) sc[1] = 0.5 * tau * t;
+        }
+        __syncthreads();
+        if (tid >= t0 && tid < n) ww[tid] = fma(-sc[1], vv[tid], pt);
+        else if (tid < 224) ww[tid] = 0.0;
+        __syncthreads();
+        TRD_STAMP(3)
+        // ---- A22 -= v w' + w v'
+        double wreg[kTrd4Q];
+#pragma unroll
+        for (int q = 0; q < kTrd4Q; ++q) wreg[q] = ww[32 * q + lane];
+        for (int i = t0 + warp; i < n; i += kTrd4Warps) {
+            const double vi = vv[i], wi = ww[i];
+            double* row = A + ri(i);
+            const int li = i & 31;
+            switch (i >> 5) {
+                case 0: trd_row_u<0>(row, vreg, wreg, lom, lane, li, vi, wi); break;
+                case 1: trd_row_u<1>(row, vreg, wreg, lom, lane, li, vi, wi); break;
+                case 2: trd_row_u<2>(row, vreg, wreg, lom, lane, li, vi, wi); break;
+                case 3: trd_row_u<3>(row, vreg, wreg, lom, lane, li, vi, wi); break;
+                case 4: trd_row_u<4>(row, vreg, wreg, lom, lane, li, vi, wi); break;
+                case 5: trd_row_u<5>(row, vreg, wreg, lom, lane, li, vi, wi); break;
+                default: trd_row_u<6>(row, vreg, wreg, lom, lane, li, vi, wi); break;
+            }
+        }
+        TRD_STAMP(4)
+        __syncthreads();
+        TRD_STAMP(5)
+    }
+#ifdef FQB_TRD_PROBE
+    if (tid == FQB_TRD_PROBE)
+        for (int x = 0; x < 6; ++x) trd_probe_out[x] = tp[x];
+#endif
+    if (tid == 0) {
+        if (n >= 2) {
+            d[n - 2] = A[ri(n - 2) + n - 2];
+            e[n - 2] = A[ri(n - 1) + n - 2];
+            tau_out[n - 2] = 0.0;
+        }
+        d[n - 1] = A[ri(n - 1) + n - 1];
+    }
+    for (int k = warp; k < n; k += kTrd4Warps)
+        for (int i = lane; i < n; i += 32) {
+            double v = 0.0;
+            if (k + 2 < n) v = i == k + 1 ? 1.0 : (i > k + 1 ? A[ri(i) + k] : 0.0);
+            vh[int64_t(k) * n + i] = v;
+        }
+}
+
+// ---------------------------------------------------------------------------
 // eigenvalues: warp per index k (k-th smallest), 65-section on Sturm counts (two
 // points per lane, interleaved chains).  The recurrence's division is a hardware
 // reciprocal estimate refined by two Newton steps (full precision, ~half the
@@ -521,7 +743,18 @@ bool small_eigh(const double* mat, int n, double* w, double* x, double* scratch,
         FQB_CUDA(cudaFuncSetAttribute(k_sytrd, cudaFuncAttributeMaxDynamicSharedMemorySize, int(mx)));
         configured = true;
     }
-    launch_k(k_sytrd, 1, kTrdThreads, smem, s, mat, n, d, e, tau, vh);
+    if (n <= kTrd4Max) {
+        const size_t smem4 = sizeof(double) * size_t(n * (n + 1) / 2 + 4 * 224 + kTrd4Warps * 224);
+        static bool cfg4 = false;
+        if (!cfg4) {
+            const size_t mx4 = sizeof(double) * size_t(kTrd4Max * (kTrd4Max + 1) / 2 + 4 * 224 + kTrd4Warps * 224);
+            FQB_CUDA(cudaFuncSetAttribute(k_sytrd4, cudaFuncAttributeMaxDynamicSharedMemorySize, int(mx4)));
+            cfg4 = true;
+        }
+        launch_k(k_sytrd4, 1, kTrd4Warps * 32, smem4, s, mat, n, d, e, tau, vh);
+    } else {
+        launch_k(k_sytrd, 1, kTrdThreads, smem, s, mat, n, d, e, tau, vh);
+    }
     FQB_LAUNCHED();
     launch_k(k_tri_bisect, unsigned(ceil_div(n, 8)), 256, 0, s, d, e, n, w);
     FQB_LAUNCHED();

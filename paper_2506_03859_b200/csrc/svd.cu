@@ -200,10 +200,10 @@ double relative_error(Handle& h, const double* a, int64_t m, int64_t n, int64_t 
 }
 
 // Symmetric eigendecomposition of mat (l x l, ld l, both triangles) in place:
-// eigenvalues ascending into w, eigenvectors into mat.  FQB_EIG: unset / "syevd" =
-// cuSOLVER syevd (measured fastest at l = 200: 1.9 ms), "syevj" = cuSOLVER Jacobi,
-// "small" = the l <= kSmallEighMax solver of eigsmall.cu (its own residual /
-// orthogonality check falls back to syevd; 2.0 ms at l = 200).
+// eigenvalues ascending into w, eigenvectors into mat.  FQB_EIG: unset / "small" =
+// the l <= kSmallEighMax solver of eigsmall.cu (1.56 ms at l = 200; its own residual /
+// orthogonality check falls back to syevd), "syevd" = cuSOLVER syevd only (1.9 ms),
+// "syevj" = cuSOLVER Jacobi.
 // Returns true when the small-l solver produced the result.
 // info_dev != null: cuSOLVER's status goes there and nothing is synchronized (the
 // caller checks it); null: checked here.
@@ -211,7 +211,7 @@ static bool eigh_core(Handle& h, double* mat, int l, double* w, int* info_dev) {
     cudaStream_t s = h.stream;
     ensure_gemm_workspace(h);
     const char* env = std::getenv("FQB_EIG");
-    const int eig_mode = !env ? 1 : std::string(env) == "syevj" ? 2 : std::string(env) == "small" ? 0 : 1;
+    const int eig_mode = !env ? 0 : std::string(env) == "syevj" ? 2 : std::string(env) == "syevd" ? 1 : 0;
     if (eig_mode == 0 && l <= kSmallEighMax) {
         DeviceArray<double> es;
         es.ensure(size_t(small_eigh_scratch_doubles(l)), s);

@@ -1,6 +1,7 @@
-"""The SVD assembly's symmetric eigensolver (fqb_sym_eig): cuSOLVER syevd by default, and
-with FQB_EIG=small (opt-in, l <= 224) the tridiagonal bisection / inverse-iteration
-solver of eigsmall.cu, checked a posteriori with syevd as its fallback.  Bar: eigenvalues within 64 n u ||M|| of numpy's (LAPACK dsyevd),
+"""The SVD assembly's symmetric eigensolver (fqb_sym_eig): for l <= 224 the tridiagonal
+bisection / inverse-iteration solver of eigsmall.cu (the default; FQB_EIG=small forces it
+in these tests), checked a posteriori with cuSOLVER syevd as its fallback; FQB_EIG=syevd
+selects cuSOLVER only.  Bar: eigenvalues within 64 n u ||M|| of numpy's (LAPACK dsyevd),
 residual ||M V - V diag(w)||_F <= 64 n u ||M||_F and ||V'V - I||_F <= 64 n u -- the same
 bound the solver's own check enforces -- and the small path actually taken for the
 spectra the QB loop produces."""
@@ -110,6 +111,8 @@ def test_qb_svd_matches_numpy_and_syevd(eng, monkeypatch):
     assert np.linalg.norm(r1.u.T @ r1.u - np.eye(r1.rank)) <= 1e-12
 
 
-def test_default_is_cusolver(eng, monkeypatch):
+def test_default_is_the_small_solver_and_syevd_on_request(eng, monkeypatch):
     monkeypatch.delenv("FQB_EIG", raising=False)
+    assert _check(eng, _spd(50, np.linspace(1, 2, 50), seed=1))
+    monkeypatch.setenv("FQB_EIG", "syevd")
     assert not _check(eng, _spd(50, np.linspace(1, 2, 50), seed=1), expect_small=False)
