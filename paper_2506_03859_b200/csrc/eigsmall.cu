@@ -219,6 +219,244 @@ __device__ __forceinline__ void trd_row_u(double* __restrict__ row, const double
     }
 }
 
+// fused step body of k_sytrd5: the rank-2 update of step k on row i, then the row's
+// contributions to p of step k + 1 from the updated values
+template <int QI>
+__device__ __forceinline__ double trd_row_f(double* __restrict__ row, const double (&vk)[kTrd4Q],
+                                            const double (&wk)[kTrd4Q], const double (&vn)[kTrd4Q],
+                                            const double (&lom)[kTrd4Q], double (&colacc)[kTrd4Q], int lane, int li,
+                                            double vki, double wki, double vni) {
+    double x[QI + 1];
+#pragma unroll
+    for (int q = 0; q <= QI; ++q) x[q] = row[32 * q + lane];
+    double racc = 0.0;
+#pragma unroll
+    for (int q = 0; q <= QI; ++q) {
+        const bool in = lom[q] != 0.0 && (q < QI || lane <= li);
+        const double a = fma(-vki, wk[q], fma(-wki, vk[q], x[q]));
+        if (in) row[32 * q + lane] = a;
+        const double am = in ? a : 0.0;
+        racc = fma(am, vn[q], racc);
+        colacc[q] = fma((q == QI && lane == li) ? 0.0 : am, vni, colacc[q]);
+    }
+    return racc;
+}
+
+// Tridiagonalisation with a one-column lookahead (n <= kTrd4Max): per step the
+// reflector of column k+1 is formed as soon as that column has step k's update, and
+// one fused sweep then applies step k's rank-2 update to the rest of the trailing
+// matrix AND accumulates p = A22 v of step k+1 from the updated values -- one pass
+// over the matrix per step instead of two.
+__global__ void __launch_bounds__(kTrd4Warps * 32, 1) k_sytrd5(const double* __restrict__ mat, int n, double* d,
+                                                               double* e, double* tau_out, double* vh) {
+    FQB_PDL_ENTRY();
+    extern __shared__ double sm[];
+    double* A = sm;                                   // packed lower, row-major (+ slack for over-reads)
+    double* vb = A + ri(n) + 224;                     // two v buffers (steps k, k+1), zero outside their window
+    double* ww = vb + 2 * 224;                        // w of step k
+    double* rs = ww + 224;                            // row sums of A22 v
+    double* part = rs + 224;                          // [16][224] column partials
+    __shared__ double red[kTrd4Warps];
+    __shared__ double sc[4];                          // tau(k), K, tau(k+1)
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int NT = kTrd4Warps * 32;
+    for (int i = warp; i < n; i += kTrd4Warps)
+        for (int j = lane; j <= i; j += 32) A[ri(i) + j] = mat[int64_t(j) * n + i];
+    for (int i = tid; i < 3 * 224; i += NT) vb[i] = 0.0;   // vb[0..447], ww
+    __syncthreads();
+
+    // reflector of column c (rows c+1 ..) into v buffer vbuf by warp 0; tau to sc[slot]
+    auto house = [&](int c, double* vbuf, int slot) {
+        if (warp == 0) {
+            const int t0 = c + 1;
+            double xc[kTrd4Q];
+            double ss = 0.0;
+#pragma unroll
+            for (int q = 0; q < kTrd4Q; ++q) {
+                const int i = t0 + 1 + 32 * q + lane;
+                xc[q] = i < n ? A[ri(i) + c] : 0.0;
+                ss = fma(xc[q], xc[q], ss);
+            }
+            ss = warp_sum(ss);
+            const double alpha = A[ri(t0) + c];
+            double tau = 0.0, beta = alpha, scal = 0.0;
+            if (ss > 0.0) {
+                beta = -copysign(sqrt(fma(alpha, alpha, ss)), alpha);
+                tau = (beta - alpha) / beta;
+                scal = 1.0 / (alpha - beta);
+            }
+            // clear the buffer's previous window (two steps back), then write this one
+            for (int i = lane; i < t0; i += 32) vbuf[i] = 0.0;
+#pragma unroll
+            for (int q = 0; q < kTrd4Q; ++q) {
+                const int i = t0 + 1 + 32 * q + lane;
+                if (i < n) {
+                    const double v = xc[q] * scal;   // scal = 0 when tau = 0
+                    if (tau != 0.0) A[ri(i) + c] = v;
+                    vbuf[i] = v;
+                }
+            }
+            if (lane == 0) {
+                vbuf[t0] = 1.0;
+                sc[slot] = tau;
+                d[c] = A[ri(c) + c];
+                e[c] = beta;
+                tau_out[c] = tau;
+            }
+        }
+    };
+    auto lo_mask = [&](int j0, double (&lom)[kTrd4Q]) {
+#pragma unroll
+        for (int q = 0; q < kTrd4Q; ++q) lom[q] = 32 * q + lane >= j0 ? 1.0 : 0.0;
+    };
+
+    if (n >= 3) {
+        // ---- prologue: reflector 0 and p of step 0 (plain symmetric product)
+        house(0, vb, 0);
+        __syncthreads();
+        {
+            const double* v0 = vb;
+            double vreg[kTrd4Q], colacc[kTrd4Q], lom[kTrd4Q];
+#pragma unroll
+            for (int q = 0; q < kTrd4Q; ++q) {
+                vreg[q] = v0[32 * q + lane];
+                colacc[q] = 0.0;
+            }
+            lo_mask(1, lom);
+            auto row_p = [&](int i) -> double {
+                const double vi = v0[i];
+                const double* row = A + ri(i);
+                const int li = i & 31;
+                switch (i >> 5) {
+                    case 0: return trd_row_p<0>(row, vreg, lom, colacc, lane, li, vi);
+                    case 1: return trd_row_p<1>(row, vreg, lom, colacc, lane, li, vi);
+                    case 2: return trd_row_p<2>(row, vreg, lom, colacc, lane, li, vi);
+                    case 3: return trd_row_p<3>(row, vreg, lom, colacc, lane, li, vi);
+                    case 4: return trd_row_p<4>(row, vreg, lom, colacc, lane, li, vi);
+                    case 5: return trd_row_p<5>(row, vreg, lom, colacc, lane, li, vi);
+                    default: return trd_row_p<6>(row, vreg, lom, colacc, lane, li, vi);
+                }
+            };
+            for (int i = 1 + warp; i < n; i += 2 * kTrd4Warps) {
+                const int i2 = i + kTrd4Warps;
+                double r1 = row_p(i);
+                double r2 = i2 < n ? row_p(i2) : 0.0;
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) {
+                    r1 += __shfl_xor_sync(0xFFFFFFFFu, r1, off);
+                    r2 += __shfl_xor_sync(0xFFFFFFFFu, r2, off);
+                }
+                if (lane == 0) {
+                    rs[i] = r1;
+                    if (i2 < n) rs[i2] = r2;
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < kTrd4Q; ++q) part[warp * 224 + 32 * q + lane] = colacc[q];
+        }
+        __syncthreads();
+    }
+    for (int k = 0; k + 2 < n; ++k) {
+        const int t0 = k + 1;
+        double* vk = vb + (k & 1) * 224;
+        double* vn = vb + ((k + 1) & 1) * 224;
+        // ---- P(k): p = tau A22 v, K = (tau / 2) p'v, w = p - K v
+        const double tau = sc[0];
+        double pv = 0.0, pt = 0.0;
+        if (tid >= t0 && tid < n) {
+            double acc = rs[tid];
+#pragma unroll
+            for (int w = 0; w < kTrd4Warps; ++w) acc += part[w * 224 + tid];
+            pt = tau * acc;
+            pv = pt * vk[tid];
+        }
+        pv = warp_sum(pv);
+        if (lane == 0) red[warp] = pv;
+        __syncthreads();
+        if (warp == 0) {
+            const double t = warp_sum(lane < kTrd4Warps ? red[lane] : 0.0);
+            if (lane == 0) sc[1] = 0.5 * tau * t;
+        }
+        __syncthreads();
+        if (tid >= t0 && tid < n) ww[tid] = fma(-sc[1], vk[tid], pt);
+        else if (tid < 224) ww[tid] = 0.0;
+        __syncthreads();
+        if (k + 3 >= n) {
+            // last reflector: its update touches only the trailing 2 x 2 block
+            if (tid >= t0 && tid < n) {
+                const int i = tid;
+                for (int j = t0; j <= i; ++j)
+                    A[ri(i) + j] = fma(-vk[i], ww[j], fma(-ww[i], vk[j], A[ri(i) + j]));
+            }
+            __syncthreads();
+            break;
+        }
+        // ---- L(k): column k+1 (rows >= k+1) gets step k's update; then reflector k+1
+        if (tid >= t0 && tid < n) {
+            const int i = tid, j = t0;
+            A[ri(i) + j] = fma(-vk[i], ww[j], fma(-ww[i], vk[j], A[ri(i) + j]));
+        }
+        __syncthreads();
+        house(k + 1, vn, 0);
+        __syncthreads();
+        // ---- F(k): rows >= k+2, columns >= k+2: update(k) + p(k+1)
+        double vkr[kTrd4Q], wkr[kTrd4Q], vnr[kTrd4Q], colacc[kTrd4Q], lom[kTrd4Q];
+#pragma unroll
+        for (int q = 0; q < kTrd4Q; ++q) {
+            vkr[q] = vk[32 * q + lane];
+            wkr[q] = ww[32 * q + lane];
+            vnr[q] = vn[32 * q + lane];
+            colacc[q] = 0.0;
+        }
+        lo_mask(k + 2, lom);
+        auto row_f = [&](int i) -> double {
+            double* row = A + ri(i);
+            const double vki = vk[i], wki = ww[i], vni = vn[i];
+            const int li = i & 31;
+            switch (i >> 5) {
+                case 0: return trd_row_f<0>(row, vkr, wkr, vnr, lom, colacc, lane, li, vki, wki, vni);
+                case 1: return trd_row_f<1>(row, vkr, wkr, vnr, lom, colacc, lane, li, vki, wki, vni);
+                case 2: return trd_row_f<2>(row, vkr, wkr, vnr, lom, colacc, lane, li, vki, wki, vni);
+                case 3: return trd_row_f<3>(row, vkr, wkr, vnr, lom, colacc, lane, li, vki, wki, vni);
+                case 4: return trd_row_f<4>(row, vkr, wkr, vnr, lom, colacc, lane, li, vki, wki, vni);
+                case 5: return trd_row_f<5>(row, vkr, wkr, vnr, lom, colacc, lane, li, vki, wki, vni);
+                default: return trd_row_f<6>(row, vkr, wkr, vnr, lom, colacc, lane, li, vki, wki, vni);
+            }
+        };
+        for (int i = k + 2 + warp; i < n; i += 2 * kTrd4Warps) {
+            const int i2 = i + kTrd4Warps;
+            double r1 = row_f(i);
+            double r2 = i2 < n ? row_f(i2) : 0.0;
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                r1 += __shfl_xor_sync(0xFFFFFFFFu, r1, off);
+                r2 += __shfl_xor_sync(0xFFFFFFFFu, r2, off);
+            }
+            if (lane == 0) {
+                rs[i] = r1;
+                if (i2 < n) rs[i2] = r2;
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < kTrd4Q; ++q) part[warp * 224 + 32 * q + lane] = colacc[q];
+        __syncthreads();
+    }
+    if (tid == 0) {
+        if (n >= 2) {
+            d[n - 2] = A[ri(n - 2) + n - 2];
+            e[n - 2] = A[ri(n - 1) + n - 2];
+            tau_out[n - 2] = 0.0;
+        }
+        d[n - 1] = A[ri(n - 1) + n - 1];
+    }
+    for (int k = warp; k < n; k += kTrd4Warps)
+        for (int i = lane; i < n; i += 32) {
+            double v = 0.0;
+            if (k + 2 < n) v = i == k + 1 ? 1.0 : (i > k + 1 ? A[ri(i) + k] : 0.0);
+            vh[int64_t(k) * n + i] = v;
+        }
+}
+
 __global__ void __launch_bounds__(kTrd4Warps * 32, 1) k_sytrd4(const double* __restrict__ mat, int n, double* d,
                                                                double* e, double* tau_out, double* vh) {
     FQB_PDL_ENTRY();
@@ -744,14 +982,14 @@ bool small_eigh(const double* mat, int n, double* w, double* x, double* scratch,
         configured = true;
     }
     if (n <= kTrd4Max) {
-        const size_t smem4 = sizeof(double) * size_t(n * (n + 1) / 2 + 4 * 224 + kTrd4Warps * 224);
+        const size_t smem4 = sizeof(double) * size_t(n * (n + 1) / 2 + 5 * 224 + kTrd4Warps * 224);
         static bool cfg4 = false;
         if (!cfg4) {
-            const size_t mx4 = sizeof(double) * size_t(kTrd4Max * (kTrd4Max + 1) / 2 + 4 * 224 + kTrd4Warps * 224);
-            FQB_CUDA(cudaFuncSetAttribute(k_sytrd4, cudaFuncAttributeMaxDynamicSharedMemorySize, int(mx4)));
+            const size_t mx4 = sizeof(double) * size_t(kTrd4Max * (kTrd4Max + 1) / 2 + 5 * 224 + kTrd4Warps * 224);
+            FQB_CUDA(cudaFuncSetAttribute(k_sytrd5, cudaFuncAttributeMaxDynamicSharedMemorySize, int(mx4)));
             cfg4 = true;
         }
-        launch_k(k_sytrd4, 1, kTrd4Warps * 32, smem4, s, mat, n, d, e, tau, vh);
+        launch_k(k_sytrd5, 1, kTrd4Warps * 32, smem4, s, mat, n, d, e, tau, vh);
     } else {
         launch_k(k_sytrd, 1, kTrdThreads, smem, s, mat, n, d, e, tau, vh);
     }

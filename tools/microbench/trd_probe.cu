@@ -19,9 +19,9 @@ int main() {
     double *m, *d, *e, *tau, *vh;
     cudaMalloc(&m, 8 * n * n); cudaMalloc(&d, 8 * n); cudaMalloc(&e, 8 * n); cudaMalloc(&tau, 8 * n); cudaMalloc(&vh, 8 * n * n);
     cudaMemcpy(m, h.data(), 8 * n * n, cudaMemcpyHostToDevice);
-    const size_t smem4 = sizeof(double) * size_t(n * (n + 1) / 2 + 4 * 224 + farqb::kTrd4Warps * 224);
-    cudaFuncSetAttribute(farqb::k_sytrd4, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem4));
-    for (int r = 0; r < 3; ++r) farqb::k_sytrd4<<<1, farqb::kTrd4Warps * 32, smem4>>>(m, n, d, e, tau, vh);
+    const size_t smem4 = sizeof(double) * size_t(n * (n + 1) / 2 + 4 * 224 + farqb::kTrd4Warps * 224 + 224);
+    cudaFuncSetAttribute(farqb::k_sytrd5, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem4));
+    for (int r = 0; r < 3; ++r) farqb::k_sytrd5<<<1, farqb::kTrd4Warps * 32, smem4>>>(m, n, d, e, tau, vh);
     cudaDeviceSynchronize();
     long long t[6];
     cudaMemcpyFromSymbol(t, trd_probe_out, sizeof t);
