@@ -391,14 +391,46 @@ __global__ void __launch_bounds__(kTrd4Warps * 32, 1) k_sytrd5(const double* __r
             __syncthreads();
             break;
         }
-        // ---- L(k): column k+1 (rows >= k+1) gets step k's update; then reflector k+1
-        if (tid >= t0 && tid < n) {
-            const int i = tid, j = t0;
-            A[ri(i) + j] = fma(-vk[i], ww[j], fma(-ww[i], vk[j], A[ri(i) + j]));
+        // ---- L(k): column k+1 (rows >= k+1) gets step k's update, and every thread
+        // then forms reflector k+1 itself from the block-reduced norm (no serial warp)
+        {
+            const int c = t0, c1 = c + 1;   // column, first row of the reflector
+            double x = 0.0;
+            if (tid >= c && tid < n) {
+                const int i = tid;
+                x = fma(-vk[i], ww[c], fma(-ww[i], vk[c], A[ri(i) + c]));
+                A[ri(i) + c] = x;
+            }
+            const double sq = tid > c1 && tid < n ? x * x : 0.0;
+            const double wsum = warp_sum(sq);
+            if (lane == 0) red[warp] = wsum;
+            if (tid == c1) sc[2] = x;   // alpha
+            __syncthreads();
+            double ss = 0.0;
+#pragma unroll
+            for (int w = 0; w < kTrd4Warps; ++w) ss += red[w];
+            const double alpha = sc[2];
+            double tau = 0.0, beta = alpha, scal = 0.0;
+            if (ss > 0.0) {
+                beta = -copysign(sqrt(fma(alpha, alpha, ss)), alpha);
+                tau = (beta - alpha) / beta;
+                scal = 1.0 / (alpha - beta);
+            }
+            if (tid < c1) vn[tid] = 0.0;
+            else if (tid == c1) vn[tid] = 1.0;
+            else if (tid < n) {
+                const double v = x * scal;   // scal = 0 when tau = 0
+                if (tau != 0.0) A[ri(tid) + c] = v;
+                vn[tid] = v;
+            }
+            if (tid == 0) {
+                sc[0] = tau;
+                d[c] = A[ri(c) + c];
+                e[c] = beta;
+                tau_out[c] = tau;
+            }
+            __syncthreads();
         }
-        __syncthreads();
-        house(k + 1, vn, 0);
-        __syncthreads();
         // ---- F(k): rows >= k+2, columns >= k+2: update(k) + p(k+1)
         double vkr[kTrd4Q], wkr[kTrd4Q], vnr[kTrd4Q], colacc[kTrd4Q], lom[kTrd4Q];
 #pragma unroll
