@@ -35,6 +35,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 #include <utility>
 
 #include "kernels.hpp"
@@ -203,41 +204,36 @@ __device__ __forceinline__ double trd_row_p(const double* __restrict__ row, cons
     }
     return racc;
 }
-template <int QI>
-__device__ __forceinline__ void trd_row_u(double* __restrict__ row, const double (&vreg)[kTrd4Q],
-                                          const double (&wreg)[kTrd4Q], const double (&lom)[kTrd4Q], int lane,
-                                          int li, double vi, double wi) {
-    // all loads of the row first: interleaved with the stores, the possible aliasing
-    // would serialise every chunk on its load latency
-    double x[QI + 1];
-#pragma unroll
-    for (int q = 0; q <= QI; ++q) x[q] = row[32 * q + lane];
-#pragma unroll
-    for (int q = 0; q <= QI; ++q) {
-        const bool in = lom[q] != 0.0 && (q < QI || lane <= li);
-        if (in) row[32 * q + lane] = fma(-vi, wreg[q], fma(-wi, vreg[q], x[q]));
-    }
-}
 
 // fused step body of k_sytrd5: the rank-2 update of step k on row i, then the row's
-// contributions to p of step k + 1 from the updated values
+// contributions to p of step k + 1 from the updated values.  No masks below the last
+// chunk: vk / wk are zero outside step k's window and at its first column (updated
+// already by the lookahead), so those columns are rewritten unchanged; vn is zero
+// below step k+1's window, so they add nothing to the row sum; their column sums land
+// on p_j for j below the window, which nothing reads.  Only the chunk holding the
+// diagonal needs masks (j <= i, and j < i for the column part).
 template <int QI>
 __device__ __forceinline__ double trd_row_f(double* __restrict__ row, const double (&vk)[kTrd4Q],
                                             const double (&wk)[kTrd4Q], const double (&vn)[kTrd4Q],
-                                            const double (&lom)[kTrd4Q], double (&colacc)[kTrd4Q], int lane, int li,
-                                            double vki, double wki, double vni) {
+                                            double (&colacc)[kTrd4Q], int lane, int li, double vki, double wki,
+                                            double vni) {
     double x[QI + 1];
 #pragma unroll
     for (int q = 0; q <= QI; ++q) x[q] = row[32 * q + lane];
     double racc = 0.0;
 #pragma unroll
-    for (int q = 0; q <= QI; ++q) {
-        const bool in = lom[q] != 0.0 && (q < QI || lane <= li);
+    for (int q = 0; q < QI; ++q) {
         const double a = fma(-vki, wk[q], fma(-wki, vk[q], x[q]));
-        if (in) row[32 * q + lane] = a;
-        const double am = in ? a : 0.0;
-        racc = fma(am, vn[q], racc);
-        colacc[q] = fma((q == QI && lane == li) ? 0.0 : am, vni, colacc[q]);
+        row[32 * q + lane] = a;
+        racc = fma(a, vn[q], racc);
+        colacc[q] = fma(a, vni, colacc[q]);
+    }
+    {
+        const bool in = lane <= li;
+        const double a = fma(-vki, wk[QI], fma(-wki, vk[QI], x[QI]));
+        if (in) row[32 * QI + lane] = a;
+        racc = fma(in ? a : 0.0, vn[QI], racc);
+        colacc[QI] = fma(lane < li ? a : 0.0, vni, colacc[QI]);
     }
     return racc;
 }
@@ -356,6 +352,18 @@ __global__ void __launch_bounds__(kTrd4Warps * 32, 1) k_sytrd5(const double* __r
         }
         __syncthreads();
     }
+#ifdef FQB_TRD_PROBE
+    long long tp5[6] = {0, 0, 0, 0, 0, 0};
+    long long tl5 = clock64();
+#define TRD5_STAMP(x)                      \
+    {                                      \
+        const long long tn_ = clock64();   \
+        tp5[x] += tn_ - tl5;               \
+        tl5 = tn_;                         \
+    }
+#else
+#define TRD5_STAMP(x)
+#endif
     for (int k = 0; k + 2 < n; ++k) {
         const int t0 = k + 1;
         double* vk = vb + (k & 1) * 224;
@@ -381,6 +389,7 @@ __global__ void __launch_bounds__(kTrd4Warps * 32, 1) k_sytrd5(const double* __r
         if (tid >= t0 && tid < n) ww[tid] = fma(-sc[1], vk[tid], pt);
         else if (tid < 224) ww[tid] = 0.0;
         __syncthreads();
+        TRD5_STAMP(0)
         if (k + 3 >= n) {
             // last reflector: its update touches only the trailing 2 x 2 block
             if (tid >= t0 && tid < n) {
@@ -431,223 +440,55 @@ __global__ void __launch_bounds__(kTrd4Warps * 32, 1) k_sytrd5(const double* __r
             }
             __syncthreads();
         }
+        TRD5_STAMP(1)
         // ---- F(k): rows >= k+2, columns >= k+2: update(k) + p(k+1)
-        double vkr[kTrd4Q], wkr[kTrd4Q], vnr[kTrd4Q], colacc[kTrd4Q], lom[kTrd4Q];
+        double vkr[kTrd4Q], wkr[kTrd4Q], vnr[kTrd4Q], colacc[kTrd4Q];
 #pragma unroll
         for (int q = 0; q < kTrd4Q; ++q) {
-            vkr[q] = vk[32 * q + lane];
-            wkr[q] = ww[32 * q + lane];
-            vnr[q] = vn[32 * q + lane];
+            const int j = 32 * q + lane;
+            vkr[q] = j == t0 ? 0.0 : vk[j];   // column t0 already has step k's update (L)
+            wkr[q] = j == t0 ? 0.0 : ww[j];
+            vnr[q] = vn[j];
             colacc[q] = 0.0;
         }
-        lo_mask(k + 2, lom);
-        auto row_f = [&](int i) -> double {
-            double* row = A + ri(i);
-            const double vki = vk[i], wki = ww[i], vni = vn[i];
-            const int li = i & 31;
-            switch (i >> 5) {
-                case 0: return trd_row_f<0>(row, vkr, wkr, vnr, lom, colacc, lane, li, vki, wki, vni);
-                case 1: return trd_row_f<1>(row, vkr, wkr, vnr, lom, colacc, lane, li, vki, wki, vni);
-                case 2: return trd_row_f<2>(row, vkr, wkr, vnr, lom, colacc, lane, li, vki, wki, vni);
-                case 3: return trd_row_f<3>(row, vkr, wkr, vnr, lom, colacc, lane, li, vki, wki, vni);
-                case 4: return trd_row_f<4>(row, vkr, wkr, vnr, lom, colacc, lane, li, vki, wki, vni);
-                case 5: return trd_row_f<5>(row, vkr, wkr, vnr, lom, colacc, lane, li, vki, wki, vni);
-                default: return trd_row_f<6>(row, vkr, wkr, vnr, lom, colacc, lane, li, vki, wki, vni);
-            }
-        };
-        for (int i = k + 2 + warp; i < n; i += 2 * kTrd4Warps) {
-            const int i2 = i + kTrd4Warps;
-            double r1 = row_f(i);
-            double r2 = i2 < n ? row_f(i2) : 0.0;
+        // rows by 32-row blocks (QI = i / 32 a compile-time constant per block -- no
+        // indirect branch per row); a warp has at most two rows (i, i + 16) in a block
+        const int r0 = (k + 2 + warp) & 15;
+        auto block_f = [&](auto qi_c) {
+            constexpr int QI = decltype(qi_c)::value;
+            const int lo = max(k + 2, 32 * QI), hi = min(n, 32 * QI + 32);
+            if (lo >= hi) return;
+            const int i1 = lo + ((r0 - lo) & 15), i2 = i1 + 16;
+            const bool h1 = i1 < hi, h2 = i2 < hi;
+            double ra = 0.0, rb = 0.0;
+            if (h1) ra = trd_row_f<QI>(A + ri(i1), vkr, wkr, vnr, colacc, lane, i1 & 31, vk[i1], ww[i1], vn[i1]);
+            if (h2) rb = trd_row_f<QI>(A + ri(i2), vkr, wkr, vnr, colacc, lane, i2 & 31, vk[i2], ww[i2], vn[i2]);
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) {
-                r1 += __shfl_xor_sync(0xFFFFFFFFu, r1, off);
-                r2 += __shfl_xor_sync(0xFFFFFFFFu, r2, off);
+                ra += __shfl_xor_sync(0xFFFFFFFFu, ra, off);
+                rb += __shfl_xor_sync(0xFFFFFFFFu, rb, off);
             }
             if (lane == 0) {
-                rs[i] = r1;
-                if (i2 < n) rs[i2] = r2;
+                if (h1) rs[i1] = ra;
+                if (h2) rs[i2] = rb;
             }
-        }
+        };
+        block_f(std::integral_constant<int, 0>{});
+        block_f(std::integral_constant<int, 1>{});
+        block_f(std::integral_constant<int, 2>{});
+        block_f(std::integral_constant<int, 3>{});
+        block_f(std::integral_constant<int, 4>{});
+        block_f(std::integral_constant<int, 5>{});
+        block_f(std::integral_constant<int, 6>{});
+        TRD5_STAMP(2)
 #pragma unroll
         for (int q = 0; q < kTrd4Q; ++q) part[warp * 224 + 32 * q + lane] = colacc[q];
         __syncthreads();
-    }
-    if (tid == 0) {
-        if (n >= 2) {
-            d[n - 2] = A[ri(n - 2) + n - 2];
-            e[n - 2] = A[ri(n - 1) + n - 2];
-            tau_out[n - 2] = 0.0;
-        }
-        d[n - 1] = A[ri(n - 1) + n - 1];
-    }
-    for (int k = warp; k < n; k += kTrd4Warps)
-        for (int i = lane; i < n; i += 32) {
-            double v = 0.0;
-            if (k + 2 < n) v = i == k + 1 ? 1.0 : (i > k + 1 ? A[ri(i) + k] : 0.0);
-            vh[int64_t(k) * n + i] = v;
-        }
-}
-
-__global__ void __launch_bounds__(kTrd4Warps * 32, 1) k_sytrd4(const double* __restrict__ mat, int n, double* d,
-                                                               double* e, double* tau_out, double* vh) {
-    FQB_PDL_ENTRY();
-    extern __shared__ double sm[];
-    double* A = sm;                                   // packed lower, row-major (+ slack for over-reads)
-    double* vv = A + ri(n) + 224;                     // v (absolute index), zero outside [t0, n)
-    double* ww = vv + 224;                            // w
-    double* rs = ww + 224;                            // row sums of A22 v
-    double* part = rs + 224;                          // [16][224] column partials
-    __shared__ double red[kTrd4Warps];
-    __shared__ double sc[2];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    constexpr int NT = kTrd4Warps * 32;
-    for (int i = warp; i < n; i += kTrd4Warps)
-        for (int j = lane; j <= i; j += 32) A[ri(i) + j] = mat[int64_t(j) * n + i];
-    for (int i = tid; i < 224; i += NT) vv[i] = ww[i] = 0.0;
-    __syncthreads();
-#ifdef FQB_TRD_PROBE
-    long long tp[6] = {0, 0, 0, 0, 0, 0};
-    long long tl = clock64();
-#define TRD_STAMP(x)                       \
-    {                                      \
-        const long long tn_ = clock64();   \
-        tp[x] += tn_ - tl;                 \
-        tl = tn_;                          \
-    }
-#else
-#define TRD_STAMP(x)
-#endif
-    for (int k = 0; k + 2 < n; ++k) {
-        const int t0 = k + 1;
-        if (warp == 0) {
-            // the column below the diagonal, read once (7 strided loads per lane at most)
-            double xc[kTrd4Q];
-            double ss = 0.0;
-#pragma unroll
-            for (int q = 0; q < kTrd4Q; ++q) {
-                const int i = t0 + 1 + 32 * q + lane;
-                xc[q] = i < n ? A[ri(i) + k] : 0.0;
-                ss = fma(xc[q], xc[q], ss);
-            }
-            ss = warp_sum(ss);
-            const double alpha = A[ri(t0) + k];
-            double tau = 0.0, beta = alpha, scal = 0.0;
-            if (ss > 0.0) {
-                beta = -copysign(sqrt(fma(alpha, alpha, ss)), alpha);
-                tau = (beta - alpha) / beta;
-                scal = 1.0 / (alpha - beta);
-            }
-#pragma unroll
-            for (int q = 0; q < kTrd4Q; ++q) {
-                const int i = t0 + 1 + 32 * q + lane;
-                if (i < n) {
-                    const double v = xc[q] * scal;   // scal = 0 when tau = 0
-                    if (tau != 0.0) A[ri(i) + k] = v;
-                    vv[i] = v;
-                }
-            }
-            if (lane == 0) {
-                vv[t0] = 1.0;
-                vv[k] = 0.0;   // the previous step's leading entry leaves the window
-                sc[0] = tau;
-                d[k] = A[ri(k) + k];
-                e[k] = beta;
-                tau_out[k] = tau;
-            }
-        }
-        __syncthreads();
-        TRD_STAMP(0)
-        const double tau = sc[0];
-        if (tau == 0.0) continue;   // uniform
-        double vreg[kTrd4Q], colacc[kTrd4Q], lom[kTrd4Q];
-#pragma unroll
-        for (int q = 0; q < kTrd4Q; ++q) {
-            vreg[q] = vv[32 * q + lane];   // zero outside [t0, n)
-            colacc[q] = 0.0;
-            lom[q] = 32 * q + lane >= t0 ? 1.0 : 0.0;
-        }
-        // ---- p = A22 v: row sums (lower incl. diagonal) + strict-lower column sums
-        // rows in pairs (i, i + 16): the two row reductions run as interleaved shuffle chains
-        auto row_p = [&](int i) -> double {
-            const double vi = vv[i];
-            const double* row = A + ri(i);
-            const int li = i & 31;
-            switch (i >> 5) {
-                case 0: return trd_row_p<0>(row, vreg, lom, colacc, lane, li, vi);
-                case 1: return trd_row_p<1>(row, vreg, lom, colacc, lane, li, vi);
-                case 2: return trd_row_p<2>(row, vreg, lom, colacc, lane, li, vi);
-                case 3: return trd_row_p<3>(row, vreg, lom, colacc, lane, li, vi);
-                case 4: return trd_row_p<4>(row, vreg, lom, colacc, lane, li, vi);
-                case 5: return trd_row_p<5>(row, vreg, lom, colacc, lane, li, vi);
-                default: return trd_row_p<6>(row, vreg, lom, colacc, lane, li, vi);
-            }
-        };
-        for (int i = t0 + warp; i < n; i += 2 * kTrd4Warps) {
-            const int i2 = i + kTrd4Warps;
-            double r1 = row_p(i);
-            double r2 = i2 < n ? row_p(i2) : 0.0;
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) {
-                r1 += __shfl_xor_sync(0xFFFFFFFFu, r1, off);
-                r2 += __shfl_xor_sync(0xFFFFFFFFu, r2, off);
-            }
-            if (lane == 0) {
-                rs[i] = r1;
-                if (i2 < n) rs[i2] = r2;
-            }
-        }
-        TRD_STAMP(1)
-#pragma unroll
-        for (int q = 0; q < kTrd4Q; ++q) part[warp * 224 + 32 * q + lane] = colacc[q];
-        __syncthreads();
-        TRD_STAMP(2)
-        // ---- p, K = (tau / 2) p'v, w = p - K v
-        double pv = 0.0, pt = 0.0;
-        if (tid >= t0 && tid < n) {
-            double acc = rs[tid];
-#pragma unroll
-            for (int w = 0; w < kTrd4Warps; ++w) acc += part[w * 224 + tid];
-            pt = tau * acc;
-            pv = pt * vv[tid];
-        }
-        pv = warp_sum(pv);
-        if (lane == 0) red[warp] = pv;
-        __syncthreads();
-        if (warp == 0) {
-            const double t = warp_sum(lane < kTrd4Warps ? red[lane] : 0.0);
-            if (lane == 0) sc[1] = 0.5 * tau * t;
-        }
-        __syncthreads();
-        if (tid >= t0 && tid < n) ww[tid] = fma(-sc[1], vv[tid], pt);
-        else if (tid < 224) ww[tid] = 0.0;
-        __syncthreads();
-        TRD_STAMP(3)
-        // ---- A22 -= v w' + w v'
-        double wreg[kTrd4Q];
-#pragma unroll
-        for (int q = 0; q < kTrd4Q; ++q) wreg[q] = ww[32 * q + lane];
-        for (int i = t0 + warp; i < n; i += kTrd4Warps) {
-            const double vi = vv[i], wi = ww[i];
-            double* row = A + ri(i);
-            const int li = i & 31;
-            switch (i >> 5) {
-                case 0: trd_row_u<0>(row, vreg, wreg, lom, lane, li, vi, wi); break;
-                case 1: trd_row_u<1>(row, vreg, wreg, lom, lane, li, vi, wi); break;
-                case 2: trd_row_u<2>(row, vreg, wreg, lom, lane, li, vi, wi); break;
-                case 3: trd_row_u<3>(row, vreg, wreg, lom, lane, li, vi, wi); break;
-                case 4: trd_row_u<4>(row, vreg, wreg, lom, lane, li, vi, wi); break;
-                case 5: trd_row_u<5>(row, vreg, wreg, lom, lane, li, vi, wi); break;
-                default: trd_row_u<6>(row, vreg, wreg, lom, lane, li, vi, wi); break;
-            }
-        }
-        TRD_STAMP(4)
-        __syncthreads();
-        TRD_STAMP(5)
+        TRD5_STAMP(3)
     }
 #ifdef FQB_TRD_PROBE
     if (tid == FQB_TRD_PROBE)
-        for (int x = 0; x < 6; ++x) trd_probe_out[x] = tp[x];
+        for (int x = 0; x < 6; ++x) trd_probe_out[x] = tp5[x];
 #endif
     if (tid == 0) {
         if (n >= 2) {

@@ -25,7 +25,7 @@ int main() {
     cudaDeviceSynchronize();
     long long t[6];
     cudaMemcpyFromSymbol(t, trd_probe_out, sizeof t);
-    const char* nm[6] = {"H+bar", "S sweep", "S bar", "P (p,K,w)", "U sweep", "U bar"};
+    const char* nm[6] = {"P (p,K,w)", "L (col+refl)", "F sweep", "F bar", "-", "-"};
     long long tot = 0;
     for (int x = 0; x < 6; ++x) tot += t[x];
     for (int x = 0; x < 6; ++x) printf("%-10s %8.0f cycles/step  %5.1f%%\n", nm[x], double(t[x]) / (n - 2), 100.0 * t[x] / tot);
