@@ -124,8 +124,8 @@ def apass_roofline(eng, a, stream):
     W = A' Y (TN) and Y = A G (NN) at 8000 x 50 x 8000, as the engine runs it --
     k_slice_z + k_ozaki (INT8 tcgen05 FP64 emulation) + k_ozaki_fixup on a
     persistent sliced A (fqb_slice_operand / fqb_sliced_gemm), CUDA events on the
-    stream the kernels are launched on.  HBM bound: the A slices are 8 bytes per
-    element of A, streamed once per pass.  The FP64 DMMA GEMM of the same product
+    stream the kernels are launched on.  HBM bound: the A slices are nsl bytes per
+    element of A (fqb_fp64_slices: 7 by default), streamed once per pass.  The FP64 DMMA GEMM of the same product
     is timed beside it for reference."""
     import torch
     y = torch.randn(BLOCK, M, dtype=torch.float64, device=a.device).t()   # m x b col-major
@@ -133,7 +133,9 @@ def apass_roofline(eng, a, stream):
     yn = torch.empty(BLOCK, M, dtype=torch.float64, device=a.device).t()
     g = torch.randn(BLOCK, N, dtype=torch.float64, device=a.device).t()
     reps = 20
-    out = {}
+    from paper_2506_03859_b200 import _native
+    nsl = int(_native.lib().fqb_fp64_slices())
+    out = {"nsl": nsl}
     sl = eng.slice_operand(a.data_ptr(), M, N, a.stride(1))
     for name, trans, outp, bp in (("tn", True, w, y), ("nn", False, yn, g)):
         k, rows = (M, N) if trans else (N, M)
@@ -159,7 +161,7 @@ def apass_roofline(eng, a, stream):
                 e1.record()
             e1.synchronize()
             ms = e0.elapsed_time(e1) / reps
-            alg_bytes = 8.0 * M * N + 8.0 * k * BLOCK + 8.0 * rows * BLOCK   # A (as slices), B, C
+            alg_bytes = float(nsl) * M * N + 8.0 * k * BLOCK + 8.0 * rows * BLOCK   # A (as slices), B, C
             out[f"{name}_{kind}"] = {"ms": ms, "gbs": alg_bytes / ms / 1e6, "bytes": alg_bytes,
                                      "tflops": 2.0 * M * N * BLOCK / ms / 1e9}
     sl.free()
@@ -359,7 +361,7 @@ def run_ours(args):
                      "kernel": "k_ozaki (tcgen05 kind::i8 FP64 emulation, + k_ozaki_fixup of the split tiles), "
                                "W=A'Y 8000x50x8000 on pre-sliced A and Y (fqb_sliced_gemm_again)",
                      "achieved": dom["gbs"], "peak": HBM_PEAK_GBS, "unit": "GB/s", "frac": dom["gbs"] / HBM_PEAK_GBS,
-                     "bytes_per_launch": dom["bytes"], "bytes_formula": "8*m*n (A slices) + 8*m*b (Y) + 8*n*b (W)",
+                     "bytes_per_launch": dom["bytes"], "bytes_formula": f"{roof['nsl']}*m*n (A slices, fqb_fp64_slices) + 8*m*b (Y) + 8*n*b (W)",
                      "launch_ms": dom["ms"], "nn_achieved": roof["nn_kernel"]["gbs"],
                      "nn_launch_ms": roof["nn_kernel"]["ms"],
                      "pass": {"what": "the whole A pass as the QB loop runs it: k_slice_z (Y) + k_ozaki + fixup",

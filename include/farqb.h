@@ -250,11 +250,16 @@ fqb_status fqb_centering_column(fqb_handle h, const double* a, int64_t m, int64_
 fqb_status fqb_frob_norm_sq(fqb_handle h, const double* a, int64_t m, int64_t n, int64_t lda,
                             double* host_out);
 /* FP32 input mode (fqb_qb_*_f32): slices per operand of the A passes on the INT8 tensor
- * cores.  8 (default): every product FP64-class, the run equals the FP64 run on the
- * widened A to ~1e-15.  4: FP32-class products (~2^-26 of max|row| max|col|, ten int8
- * products instead of 36, half the slice bytes -- A passes about twice as fast), within
- * the FP32-mode parity bar of 1e-4.  Applies to runs started after the call. */
+ * cores.  8 (default): every product FP64-class (the FP64 scheme, fqb_fp64_slices), the
+ * run equals the FP64 run on the widened A to ~1e-15.  4: FP32-class products (~2^-26 of
+ * max|row| max|col|, ten int8 products, about half the slice bytes -- A passes about
+ * twice as fast), within the FP32-mode parity bar of 1e-4.  Applies to runs started
+ * after the call. */
 fqb_status fqb_set_fp32_slices(fqb_handle h, int slices);
+/* int8 slices per element of A in the FP64-class A passes: 7 (8-bit digits, 34 int8
+ * products per output; the default) or 8 (7-bit digits, 36 products; environment
+ * FQB_OZ_SLICES=8).  Also the bytes per element of A each pass streams from HBM. */
+int fqb_fp64_slices(void);
 
 /* Symmetric eigendecomposition (device pointers; both triangles of A read):
  * eigenvalues ascending into w (n), eigenvectors into V (n x n, ldv).  The solver of

@@ -407,6 +407,8 @@ fqb_status fqb_set_fp32_slices(fqb_handle h, int slices) {
     });
 }
 
+int fqb_fp64_slices(void) { return farqb::ozaki_fp64_slices(); }
+
 fqb_status fqb_sym_eig(fqb_handle h, const double* a, int n, int64_t lda, double* w, double* v, int64_t ldv,
                        int* used_small) {
     return guarded([&]() -> fqb_status {

@@ -150,7 +150,7 @@ class QbRun {
         ensure_gemm_workspace(h_);
         oz_on_ = ozaki_default(m_, n_, b_);
         // FP32 input may opt into FP32-class A passes (4 slices: half the bytes)
-        oz_nsl_ = (af_ && h_.fp32_slices == 4) ? 4 : 8;
+        oz_nsl_ = (af_ && h_.fp32_slices == 4) ? 4 : ozaki_fp64_slices();
         double* sm = w.small.ptr;
         S_ = sm;
         S2_ = sm + 1 * b * b;
@@ -620,7 +620,7 @@ class QbRun {
     double om_p_ = 0.0;
     DeviceArray<double> q_, bt_, rowsum_;
     bool oz_on_ = false;              // A-pass products on the INT8 tensor cores (a_gemm)
-    int oz_nsl_ = 8;                  // slices per operand of the A passes (8: FP64-class, 4: FP32-class)
+    int oz_nsl_ = 7;                  // slices per operand of the A passes (7 / 8: FP64-class, 4: FP32-class)
     bool oz_ready_ = false;           // A sliced for this run (buffers live in the handle workspace)
     std::vector<double> residuals_;
     std::vector<int> ids_;

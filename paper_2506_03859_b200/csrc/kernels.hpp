@@ -115,18 +115,20 @@ void gemm_tma(bool trans_a, int64_t M, int64_t N, int64_t K, double alpha, const
 // Operands are int8 slices with one power-of-two exponent per operand row, stored
 // pre-tiled and pre-swizzled (ozaki_x_bytes / ozaki_z_bytes).  C (M x N) =
 // alpha X' Z + beta C with X the K x M operand, Z the K x N operand, N <= 64.
-// nsl = slices per operand: 8 (FP64-class, the default) or 4 (FP32-class: half the
-// slice bytes, 10 instead of 36 products; FP32 inputs on request).
+// nsl = slices per operand: 7 (FP64-class, 8-bit digits: 7 bytes of slices per element,
+// 34 products; the default), 8 (FP64-class, 7-bit digits, 36 products; FQB_OZ_SLICES=8
+// makes it the default) or 4 (FP32-class: 10 products; FP32 inputs on request).
+int ozaki_fp64_slices();
 int ozaki_slices();
 int ozaki_max_n();
 int ozaki_bn(int64_t n);
-int64_t ozaki_x_bytes(int64_t rows, int64_t k, int nsl = 8);
-int64_t ozaki_z_bytes(int64_t n, int64_t k, int nsl = 8);
-int64_t ozaki_apply_z_bytes(int64_t k, int nsl = 8);
+int64_t ozaki_x_bytes(int64_t rows, int64_t k, int nsl = ozaki_fp64_slices());
+int64_t ozaki_z_bytes(int64_t n, int64_t k, int nsl = ozaki_fp64_slices());
+int64_t ozaki_apply_z_bytes(int64_t k, int nsl = ozaki_fp64_slices());
 // ozaki_apply's products again on the B slices its last call left in z / ez (N <= 128)
 void ozaki_apply_presliced(int64_t M, int64_t N, int64_t K, double alpha, const int8_t* xs, const int* ex, double beta,
                            double* C, int64_t ldc, const int8_t* z, const int* ez, double* work, int num_sms,
-                           cudaStream_t s, LaunchCounter& lc, int nsl = 8);
+                           cudaStream_t s, LaunchCounter& lc, int nsl = ozaki_fp64_slices());
 int ozaki_apply_ez_count();
 int64_t ozaki_workspace_doubles(int num_sms);
 // Slices of A (m x n, ld) in both layouts from one pass (either may be null):
@@ -138,22 +140,22 @@ int64_t ozaki_line_max_words(int64_t m, int64_t n);
 int64_t ozaki_norm_partials(int64_t m, int64_t n);
 void ozaki_slice_a(const double* a, int64_t m, int64_t n, int64_t ld, unsigned* line_max, int8_t* x_tn, int* e_tn,
                    int8_t* x_nn, int* e_nn, cudaStream_t s, LaunchCounter& lc, double* norm_partial = nullptr,
-                   double* norm_out = nullptr, int nsl = 8);
+                   double* norm_out = nullptr, int nsl = ozaki_fp64_slices());
 void ozaki_slice_a(const float* a, int64_t m, int64_t n, int64_t ld, unsigned* line_max, int8_t* x_tn, int* e_tn,
                    int8_t* x_nn, int* e_nn, cudaStream_t s, LaunchCounter& lc, double* norm_partial = nullptr,
-                   double* norm_out = nullptr, int nsl = 8);
+                   double* norm_out = nullptr, int nsl = ozaki_fp64_slices());
 // Z (k x n, ld)
 void ozaki_slice_z(const double* b, int64_t k, int64_t n, int64_t ld, int* e, int8_t* out, cudaStream_t s,
-                   LaunchCounter& lc, int nsl = 8);
+                   LaunchCounter& lc, int nsl = ozaki_fp64_slices());
 // C = alpha X' B + beta C for any N: B (K x N, ld, FP64) sliced in chunks of <= 64
 // columns into z (ozaki_apply_z_bytes(K)) / ez (ozaki_apply_ez_count()); N > 64
 // runs two chunks at a time on CTA pairs sharing the A tiles (FQB_OZ_PAIR=0: off)
 void ozaki_apply(int64_t M, int64_t N, int64_t K, double alpha, const int8_t* xs, const int* ex, const double* b,
                  int64_t ldb, double beta, double* C, int64_t ldc, int8_t* z, int* ez, double* work, int num_sms,
-                 cudaStream_t s, LaunchCounter& lc, int nsl = 8);
+                 cudaStream_t s, LaunchCounter& lc, int nsl = ozaki_fp64_slices());
 void ozaki_gemm(int64_t M, int64_t N, int64_t K, double alpha, const int8_t* xs, const int* ex, const int8_t* zs,
                 const int* ez, double beta, double* C, int64_t ldc, double* work, int num_sms, cudaStream_t s,
-                LaunchCounter& lc, int nsl = 8);
+                LaunchCounter& lc, int nsl = ozaki_fp64_slices());
 
 // ---- smallla.cu --------------------------------------------------------------
 // Cholesky of the b x b SPD matrix S (ld = lds) with the reference pivot rule

@@ -2,30 +2,32 @@
 //
 // For the passes over A the FP64 DMMA pipe (37 TFLOP/s) is the bound; B200's INT8
 // tensor cores (tcgen05 kind::i8, 4.5 POPS dense) are not.  Each operand is cut
-// into S = 8 signed 7-bit slices with a power-of-two scale per output row /
-// column, e.g. for a row x of A with 2^(e-1) <= max|x| < 2^e:
-//     x = 2^e ( 2^-6 x_1 + 2^-13 x_2 + ... + 2^-55 x_8 ) + r,   |x_p| <= 64,
-//     |r| <= 2^(e-56)
-// (each step exact in FP64: x_p = rint(r * 2^6 or 2^7), r -= x_p).  Then
-//     (A Z)_ij = 2^(e_i + f_j) sum_{p+q <= 9} 2^(-12 - 7(p+q-2)) (A_p Z_q)_ij
-// where every A_p Z_q is an exact int32 product on the tensor cores and the 36
+// into signed integer slices with a power-of-two scale per output row / column.
+// Default (NSL = 7): for a row x of A with 2^(e-1) <= max|x| < 2^e,
+//     x = 2^e ( 2^-6 x_0 + 2^-14 x_1 + ... + 2^-54 x_6 ) + r,
+//     |x_0| <= 64, |x_p| <= 128, |r| <= 2^(e-55)
+// (8-bit digits of R = rint(x 2^(54-e)), see digits7).  Then
+//     (A Z)_ij = 2^(e_i + f_j) sum_{p+q <= 7} 2^(-12 - 8(p+q)) (A_p Z_q)_ij
+// where every A_p Z_q is an exact int32 product on the tensor cores and the 34
 // products collapse into 8 diagonals d = p+q (same power of two), accumulated
 // in TMEM (8 x 64 int32 columns = all 512).  The epilogue adds the diagonals
 // from the least significant up in FP64 and applies the exponents.  The
-// dropped terms and r are ~2^-55 relative to max|row| * max|col|, i.e. the
-// accuracy class of an FP64 GEMM.
+// dropped terms (d >= 8: 5 products, ~2^-59) and r are below 2^-54 relative to
+// max|row| * max|col|, i.e. the accuracy class of an FP64 GEMM.  NSL = 8 is the
+// same with 7-bit digits (R = rint(x 2^(55-e)), 36 products, 8 bytes per element);
+// NSL = 4 the FP32-class variant for FP32 input.
 //
 // The slices of A are made once per run (A is fixed for all 2P+2 passes), in
 // two layouts: scaled per column for A'Y (K = m contiguous, A's own layout)
 // and per row, transposed, for A G (K = n contiguous).  A pass then streams
-// 8 bytes of slices per element of A -- the same bytes as FP64 -- so it becomes
+// 7 bytes of slices per element of A -- less than FP64's 8 -- so it becomes
 // HBM bound instead of FP64 bound.
 //
 // Slices are stored pre-tiled and pre-swizzled: tile (row tile, k-block, slice)
 // is one contiguous TR x 64 B block already in the 64B-swizzle arrangement
 // tcgen05 expects, so every pipeline stage is a single 1-D bulk copy
 // (cp.async.bulk) -- no per-row TMA requests.  Kernel: one producer warp (8 KB
-// A-slice tiles, all 8 Z slices of a k-block in one 32 KB copy, 160 KB of A in
+// A-slice tiles, all Z slices of a k-block in one copy, ~165 KB of A in
 // flight), one MMA warp (tcgen05.mma.cta_group::1.kind::i8, M=128, K=32, N = 64
 // per Z slice: the products of one A slice with up to 4 consecutive Z slices
 // land on consecutive TMEM diagonals, so one N<=256 MMA covers them and A is
@@ -34,8 +36,8 @@
 // stream-K style; a CTA writes pieces of split tiles, already scaled, to its
 // partial slots and k_ozaki_fixup sums them in CTA order (deterministic).
 //
-// Measured (C2, A'Y 8000x50x8000, B200): 104 us + 3 us fixup, vs 235 us for the
-// FP64 DMMA GEMM; HBM floor for the 512 MB of A slices ~80 us.
+// Measured (C2, A'Y 8000x50x8000, B200, NSL = 8): 104 us + 3 us fixup, vs 235 us
+// for the FP64 DMMA GEMM; HBM floor for the 512 MB of A slices ~80 us.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -49,7 +51,6 @@
 namespace farqb {
 namespace {
 
-constexpr int S = 8;                     // slices per operand
 constexpr int OZ_BM = 128;               // rows per tile (UMMA M)
 // K bytes per k-block: one 64-byte swizzle row.  64 rather than 128 halves the Z
 // stage (all 8 slices of a k-block) and so doubles the A-slice bytes in flight.
@@ -59,18 +60,22 @@ constexpr int OZ_BN = 64;                // max N (8 diagonals x 64 = 512 TMEM c
 constexpr int B_STAGES = 2;
 constexpr int A_TILE = OZ_BM * OZ_BK;             // 8 KB, one slice
 constexpr int B_TILE = OZ_BN * OZ_BK;             // 4 KB per slice (bn = 64)
-// Per slice count NSL (8: FP64-class, 4: FP32-class for FP32 input): the Z stage holds
-// all NSL slices of a k-block, the rest of 225 KB is the A ring, TMEM holds NSL diagonals.
+// Per slice count NSL: 7 (FP64-class, the default: 8-bit digits, diagonals d = p+q <= 7,
+// 34 products), 8 (FP64-class, 7-bit digits, d <= 7, 36 products), 4 (FP32-class for FP32
+// input, 7-bit digits, d <= 3).  The Z stage holds all NSL slices of a k-block, the rest
+// of 225 KB is the A ring, TMEM holds ND diagonals of 64 columns.
 template <int NSL>
 struct Sl {
-    static constexpr int B_STAGE = NSL * B_TILE;                                   // 32 / 16 KB
-    static constexpr int A_STAGES = (225 * 1024 - B_STAGES * B_STAGE) / A_TILE;     // 20 / 24
+    static constexpr int W = NSL == 7 ? 8 : 7;                                      // bits per digit
+    static constexpr int ND = NSL == 7 ? 8 : NSL;                                    // diagonals kept
+    static constexpr int B_STAGE = NSL * B_TILE;                                   // 28 / 32 / 16 KB
+    static constexpr int A_STAGES = (225 * 1024 - B_STAGES * B_STAGE) / A_TILE;     // 21 / 20 / 24
     static constexpr size_t SMEM = size_t(A_STAGES) * A_TILE + size_t(B_STAGES) * B_STAGE + 1024;
-    static constexpr unsigned TMEM_COLS = unsigned(NSL * OZ_BN);                    // 512 / 256
+    static constexpr unsigned TMEM_COLS = unsigned(ND * OZ_BN);                     // 512 / 512 / 256
+    // k-blocks per TMEM accumulation (int32 headroom): a diagonal sums at most ND
+    // products of |digits| <= 2^(W-1): 8 * 64^2 * 32768 = 2^30 and 7 * 128^2 * 16384 < 2^31
+    static constexpr int CHUNK_KB = (W == 8 ? 16384 : 32768) / OZ_BK;
 };
-constexpr int B_STAGE = Sl<S>::B_STAGE;
-constexpr int A_STAGES = Sl<S>::A_STAGES;
-constexpr int CHUNK_KB = 32768 / OZ_BK;           // int32 safety: 8 * 64^2 * 32768 < 2^31
 constexpr int OZ_THREADS = 192;                   // producer, MMA, 4 epilogue warps
 constexpr int OZ_PARTIAL = OZ_BM * OZ_BN;         // doubles per CTA partial slot
 
@@ -235,6 +240,7 @@ template <bool PAIR, int NSL>
 __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
     constexpr int A_STAGES = Sl<NSL>::A_STAGES;
     constexpr int B_STAGE = Sl<NSL>::B_STAGE;
+    constexpr int ND = Sl<NSL>::ND, CHUNK_KB = Sl<NSL>::CHUNK_KB;
     FQB_PDL_ENTRY();
     extern __shared__ uint8_t smem_raw[];
     __shared__ uint64_t bars[2 * A_STAGES + 2 * B_STAGES + 2];
@@ -337,15 +343,29 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
                             asm volatile("tcgen05.fence::after_thread_sync;\n");
                             const unsigned da_lo = da_lo0 + sa * unsigned(A_TILE >> 4);
                             // products (sp, sq), sq = sq0 .. sq0+3, land on the consecutive
-                            // diagonals sp+sq: one N = 64 * slices MMA covers them (A read once)
+                            // diagonals sp+sq: one N = 64 * slices MMA covers them (A read once).
+                            // Diagonals d < NSL start (accumulate = 0) with sp = 0; with ND > NSL
+                            // the top diagonal ND-1 starts with (ND-NSL, NSL-1), issued alone.
+                            constexpr unsigned kstep = 32 >> 4;   // 32 bytes of K per MMA
+                            const int nq_all = min(NSL, ND - sp);
+                            const bool split_top = ND > NSL && sp == ND - NSL;
+                            const int nq_main = split_top ? nq_all - 1 : nq_all;
 #pragma unroll
-                            for (int sq0 = 0; sq0 < NSL - sp; sq0 += 4) {
-                                constexpr unsigned kstep = 32 >> 4;   // 32 bytes of K per MMA
-                                const unsigned id =
-                                    idesc | (unsigned((NSL - sp - sq0 < 4 ? NSL - sp - sq0 : 4) * (OZ_BN >> 3)) << 17);
+                            for (int sq0 = 0; sq0 < nq_main; sq0 += 4) {
+                                const int nq = nq_main - sq0;
+                                const unsigned id = idesc | (unsigned((nq < 4 ? nq : 4) * (OZ_BN >> 3)) << 17);
                                 const unsigned dt = tmem + unsigned((sp + sq0) * OZ_BN);
                                 const unsigned bl = db_lo + unsigned((sq0 * OZ_BN * OZ_BK) >> 4);
                                 umma_i8(dt, da_lo, bl, d_hi, id, sp == 0 ? unsigned(kb != cb) : 1u);
+#pragma unroll
+                                for (int k = 1; k < OZ_BK / 32; ++k)
+                                    umma_i8(dt, da_lo + k * kstep, bl + k * kstep, d_hi, id, 1u);
+                            }
+                            if (split_top) {
+                                const unsigned id = idesc | (unsigned(OZ_BN >> 3) << 17);
+                                const unsigned dt = tmem + unsigned((ND - 1) * OZ_BN);
+                                const unsigned bl = db_lo + unsigned(((NSL - 1) * OZ_BN * OZ_BK) >> 4);
+                                umma_i8(dt, da_lo, bl, d_hi, id, unsigned(kb != cb));
 #pragma unroll
                                 for (int k = 1; k < OZ_BK / 32; ++k)
                                     umma_i8(dt, da_lo + k * kstep, bl + k * kstep, d_hi, id, 1u);
@@ -388,18 +408,18 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
                 asm volatile("tcgen05.fence::after_thread_sync;\n");
 #pragma unroll 1
                 for (int g = 0; g < OZ_BN; g += 16) {
-                    // all 8 diagonals in flight, one wait
-                    unsigned v[NSL][16];
+                    // all diagonals in flight, one wait
+                    unsigned v[ND][16];
 #pragma unroll
-                    for (int d = 0; d < NSL; ++d) tmem_ld16(lane_addr + unsigned(d * OZ_BN + g), v[d]);
+                    for (int d = 0; d < ND; ++d) tmem_ld16(lane_addr + unsigned(d * OZ_BN + g), v[d]);
                     asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
                     double acc[16];
 #pragma unroll
                     for (int j = 0; j < 16; ++j) acc[j] = 0.0;
-                    // least significant diagonal first: d = S-1 .. 0 (scale 2^-12-7d)
+                    // least significant diagonal first: d = ND-1 .. 0 (scale 2^(-12-W d))
 #pragma unroll
-                    for (int d = NSL - 1; d >= 0; --d) {
-                        const double sc = pow2i(-12 - 7 * d);
+                    for (int d = ND - 1; d >= 0; --d) {
+                        const double sc = pow2i(-12 - Sl<NSL>::W * d);
 #pragma unroll
                         for (int j = 0; j < 16; ++j) acc[j] = fma(double(int(v[d][j])), sc, acc[j]);
                     }
@@ -497,9 +517,28 @@ __device__ __forceinline__ void digits4(double x, int e, unsigned (&d)[4]) {
     d[2] = (U >> 7) & 127u;
     d[3] = U & 127u;
 }
+// NSL = 7 (8-bit digits): R = rint(x 2^(54-e)), |R| <= 2^54, in balanced base 256,
+//     R = sum_p d_p 2^(48-8p),  d_0 in [-64, 64],  d_1..d_6 in [-128, 127],
+// the bytes of U = R + 0x80 80 80 80 80 80 80 (byte 6-p is d_p + 128): so
+// x = 2^e sum_p d_p 2^(-6-8p) up to the rounding of R (2^(e-55)), one bit coarser
+// than NSL = 8 but the products of 7 slices of 8 bits reach 2^-56 below 2^e with 34
+// products instead of 36 and the A slices are 7 bytes per element instead of 8.
+constexpr long long kDigitBias7 = 0x80808080808080LL;
+__device__ __forceinline__ void digits7(double x, int e, unsigned (&d)[7]) {
+    const unsigned long long U = static_cast<unsigned long long>(__double2ll_rn(mul_pow2(x, 54 - e)) + kDigitBias7);
+    const unsigned hi = unsigned(U >> 32), lo = unsigned(U);
+    d[0] = hi >> 16;
+    d[1] = (hi >> 8) & 255u;
+    d[2] = hi & 255u;
+    d[3] = lo >> 24;
+    d[4] = (lo >> 16) & 255u;
+    d[5] = (lo >> 8) & 255u;
+    d[6] = lo & 255u;
+}
 template <int NSL>
 __device__ __forceinline__ void digits(double x, int e, unsigned (&d)[NSL]) {
     if constexpr (NSL == 8) digits8(x, e, d);
+    else if constexpr (NSL == 7) digits7(x, e, d);
     else digits4(x, e, d);
 }
 
@@ -521,11 +560,12 @@ __device__ __forceinline__ void put_chunk16(const double (&v)[16], int e, int8_t
 #pragma unroll
         for (int sl = 0; sl < NSL; ++sl) w[sl][u >> 2] |= d[sl] << (8 * (u & 3));
     }
-    // raw fields -> signed digits: (d - 64) mod 256 per byte, four at a time
+    // raw fields -> signed digits: (d - 2^(W-1)) mod 256 per byte, four at a time
+    constexpr unsigned kOff = Sl<NSL>::W == 8 ? 0x80808080u : 0xC0C0C0C0u;
 #pragma unroll
     for (int sl = 0; sl < NSL; ++sl)
 #pragma unroll
-        for (int q = 0; q < 4; ++q) w[sl][q] = __vadd4(w[sl][q], 0xC0C0C0C0u);
+        for (int q = 0; q < 4; ++q) w[sl][q] = __vadd4(w[sl][q], kOff);
     int8_t* dst = tile0 + swz(r, c);
 #pragma unroll
     for (int sl = 0; sl < NSL; ++sl)
@@ -740,7 +780,14 @@ __global__ void __launch_bounds__(OZ_BM) k_ozaki_fixup(const OzArgs p0) {
 
 }  // namespace
 
-int ozaki_slices() { return S; }
+int ozaki_slices() { return ozaki_fp64_slices(); }
+int ozaki_fp64_slices() {
+    static const int v = [] {
+        const char* e = std::getenv("FQB_OZ_SLICES");   // 8: the 7-bit-digit FP64 scheme
+        return e && std::atoi(e) == 8 ? 8 : 7;
+    }();
+    return v;
+}
 int ozaki_max_n() { return OZ_BN; }
 int ozaki_bn(int64_t) { return OZ_BN; }   // Z slices padded to 64 rows: slice sq sits at TMEM diagonal spacing
 int64_t ozaki_x_bytes(int64_t rows, int64_t k, int nsl) {
@@ -748,7 +795,7 @@ int64_t ozaki_x_bytes(int64_t rows, int64_t k, int nsl) {
 }
 int64_t ozaki_z_bytes(int64_t n, int64_t k, int nsl) { return ceil_div(k, OZ_BK) * nsl * int64_t(ozaki_bn(n)) * OZ_BK; }
 static void check_nsl(int nsl) {
-    if (nsl != 8 && nsl != 4) throw Error(kStatusInvalid, "ozaki: slices per operand must be 8 or 4");
+    if (nsl != 8 && nsl != 7 && nsl != 4) throw Error(kStatusInvalid, "ozaki: slices per operand must be 8, 7 or 4");
 }
 
 int64_t ozaki_line_max_words(int64_t m, int64_t n) { return m + n; }
@@ -777,6 +824,7 @@ static void slice_a_impl(const T* a, int64_t m, int64_t n, int64_t ld, unsigned*
     // cover the padded operand rows of both layouts (multiples of OZ_BM)
     const dim3 g(unsigned(ceil_div(m, OZ_BM) * (OZ_BM / 64)), unsigned(ceil_div(n, OZ_BM) * (OZ_BM / 64)));
     if (nsl == 8) launch_k(k_slice_a<T, 8>, g, 256, 0, s, a, m, n, ld, rmax, cmax, x_tn, e_tn, x_nn, e_nn);
+    else if (nsl == 7) launch_k(k_slice_a<T, 7>, g, 256, 0, s, a, m, n, ld, rmax, cmax, x_tn, e_tn, x_nn, e_nn);
     else launch_k(k_slice_a<T, 4>, g, 256, 0, s, a, m, n, ld, rmax, cmax, x_tn, e_tn, x_nn, e_nn);
     FQB_LAUNCHED();
     lc.bump(2);
@@ -800,6 +848,7 @@ void ozaki_slice_z(const double* b, int64_t k, int64_t n, int64_t ld, int* e, in
     const int64_t chunks = ceil_div(k, OZ_BK) * (OZ_BK / 16);
     const dim3 g(OZ_BN, unsigned(ceil_div(chunks, ZT)));
     if (nsl == 8) launch_k(k_slice_z<8>, g, ZT, 0, s, b, k, n, ld, e, out);
+    else if (nsl == 7) launch_k(k_slice_z<7>, g, ZT, 0, s, b, k, n, ld, e, out);
     else launch_k(k_slice_z<4>, g, ZT, 0, s, b, k, n, ld, e, out);
     FQB_LAUNCHED();
     lc.bump();
@@ -853,6 +902,9 @@ static void launch_ozaki(int64_t M, int64_t N, int64_t K, double alpha, const in
         if (nsl == 8) {
             configure_ozaki<false, 8>();
             launch_k(k_ozaki<false, 8>, a.grid, OZ_THREADS, Sl<8>::SMEM, s, a);
+        } else if (nsl == 7) {
+            configure_ozaki<false, 7>();
+            launch_k(k_ozaki<false, 7>, a.grid, OZ_THREADS, Sl<7>::SMEM, s, a);
         } else {
             configure_ozaki<false, 4>();
             launch_k(k_ozaki<false, 4>, a.grid, OZ_THREADS, Sl<4>::SMEM, s, a);
@@ -861,7 +913,7 @@ static void launch_ozaki(int64_t M, int64_t N, int64_t K, double alpha, const in
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(unsigned(2 * a.grid));
         cfg.blockDim = dim3(OZ_THREADS);
-        cfg.dynamicSmemBytes = nsl == 8 ? Sl<8>::SMEM : Sl<4>::SMEM;
+        cfg.dynamicSmemBytes = nsl == 8 ? Sl<8>::SMEM : nsl == 7 ? Sl<7>::SMEM : Sl<4>::SMEM;
         cfg.stream = s;
         cudaLaunchAttribute attr[2];
         attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -875,6 +927,9 @@ static void launch_ozaki(int64_t M, int64_t N, int64_t K, double alpha, const in
         if (nsl == 8) {
             configure_ozaki<true, 8>();
             FQB_CUDA(cudaLaunchKernelEx(&cfg, k_ozaki<true, 8>, a));
+        } else if (nsl == 7) {
+            configure_ozaki<true, 7>();
+            FQB_CUDA(cudaLaunchKernelEx(&cfg, k_ozaki<true, 7>, a));
         } else {
             configure_ozaki<true, 4>();
             FQB_CUDA(cudaLaunchKernelEx(&cfg, k_ozaki<true, 4>, a));

@@ -229,3 +229,20 @@ def test_sliced_gemm_again_reuses_b_slices(eng, nb):
             sl.gemm_again(-2.0, 0.5, c2.data_ptr(), rows)
         torch.cuda.synchronize()
         assert torch.equal(c2, 0.5 * c2_0 - 2.0 * c1) or torch.allclose(c2, 0.5 * c2_0 - 2.0 * c1, rtol=0, atol=1e-12)
+
+
+def test_tile_result_independent_of_tmem_history(eng):
+    """Every accumulator diagonal is (re)initialised per tile: a CTA's 4th tile equals the
+    same rows computed alone (the top diagonal of the 7-slice scheme has no sp = 0 product
+    and once accumulated onto the previous tile's sum)."""
+    M, K, N = 296 * 128, 64, 50          # 296 row tiles, one k-block: 74 CTAs x 4 whole tiles
+    g = torch.Generator(device="cpu").manual_seed(5)
+    a = torch.randn((K, M), dtype=torch.float64, generator=g).cuda().t()      # M x K column-major
+    b = torch.randn((N, K), dtype=torch.float64, generator=g).cuda().t()      # K x N
+    full = torch.empty((N, M), dtype=torch.float64, device="cuda").t()
+    eng.gemm_emulated(False, M, N, K, 1.0, a.data_ptr(), M, b.data_ptr(), K, 0.0, full.data_ptr(), M)
+    for t in (3, 7, 150, 295):
+        part = torch.empty((N, 128), dtype=torch.float64, device="cuda").t()
+        eng.gemm_emulated(False, 128, N, K, 1.0, a[t * 128:].data_ptr(), M, b.data_ptr(), K, 0.0, part.data_ptr(), 128)
+        torch.cuda.synchronize()
+        assert torch.equal(part, full[t * 128:(t + 1) * 128]), t
