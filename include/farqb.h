@@ -252,9 +252,10 @@ fqb_status fqb_frob_norm_sq(fqb_handle h, const double* a, int64_t m, int64_t n,
 /* FP32 input mode (fqb_qb_*_f32): slices per operand of the A passes on the INT8 tensor
  * cores.  8 (default): every product FP64-class (the FP64 scheme, fqb_fp64_slices), the
  * run equals the FP64 run on the widened A to ~1e-15.  4: FP32-class products (~2^-26 of
- * max|row| max|col|, ten int8 products, about half the slice bytes -- A passes about
- * twice as fast), within the FP32-mode parity bar of 1e-4.  Applies to runs started
- * after the call. */
+ * max|row| max|col|, ten int8 products on 7-bit digits, 4 bytes per element of A);
+ * 3: FP32-class on 8-bit digits (8 products, 3 bytes per element, representation 2^-23
+ * of the line max) -- both within the FP32-mode parity bar of 1e-4 and about twice as
+ * fast as 8.  Applies to runs started after the call. */
 fqb_status fqb_set_fp32_slices(fqb_handle h, int slices);
 /* int8 slices per element of A in the FP64-class A passes: 7 (8-bit digits, 34 int8
  * products per output; the default) or 8 (7-bit digits, 36 products; environment

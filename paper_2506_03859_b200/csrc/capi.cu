@@ -401,7 +401,8 @@ fqb_status fqb_frob_norm_sq(fqb_handle h, const double* a, int64_t m, int64_t n,
 fqb_status fqb_set_fp32_slices(fqb_handle h, int slices) {
     return guarded([&]() -> fqb_status {
         if (!h) throw farqb::Error(FQB_ERR_INVALID_ARGUMENT, "null handle");
-        if (slices != 4 && slices != 8) throw farqb::Error(FQB_ERR_INVALID_ARGUMENT, "slices must be 4 or 8");
+        if (slices != 3 && slices != 4 && slices != 8)
+            throw farqb::Error(FQB_ERR_INVALID_ARGUMENT, "slices must be 3, 4 or 8");
         h->h.fp32_slices = slices;
         return FQB_OK;
     });

@@ -150,7 +150,7 @@ class QbRun {
         ensure_gemm_workspace(h_);
         oz_on_ = ozaki_default(m_, n_, b_);
         // FP32 input may opt into FP32-class A passes (4 slices: half the bytes)
-        oz_nsl_ = (af_ && h_.fp32_slices == 4) ? 4 : ozaki_fp64_slices();
+        oz_nsl_ = (af_ && h_.fp32_slices < 7) ? h_.fp32_slices : ozaki_fp64_slices();
         double* sm = w.small.ptr;
         S_ = sm;
         S2_ = sm + 1 * b * b;

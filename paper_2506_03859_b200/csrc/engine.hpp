@@ -76,7 +76,7 @@ struct Workspace {
 struct Handle {
     int device = 0;
     int num_sms = 148;
-    int fp32_slices = 8;              // FP32 input: 8 (FP64-class A passes) or 4 (FP32-class, fqb_set_fp32_slices)
+    int fp32_slices = 8;              // FP32 input: 8 (FP64-class A passes), 4 or 3 (FP32-class, fqb_set_fp32_slices)
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;
     LaunchCounter lc;

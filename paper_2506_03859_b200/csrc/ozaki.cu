@@ -62,12 +62,12 @@ constexpr int A_TILE = OZ_BM * OZ_BK;             // 8 KB, one slice
 constexpr int B_TILE = OZ_BN * OZ_BK;             // 4 KB per slice (bn = 64)
 // Per slice count NSL: 7 (FP64-class, the default: 8-bit digits, diagonals d = p+q <= 7,
 // 34 products), 8 (FP64-class, 7-bit digits, d <= 7, 36 products), 4 (FP32-class for FP32
-// input, 7-bit digits, d <= 3).  The Z stage holds all NSL slices of a k-block, the rest
+// input, 7-bit digits, d <= 3, 10 products), 3 (FP32-class, 8-bit digits, d <= 3, 8 products).  The Z stage holds all NSL slices of a k-block, the rest
 // of 225 KB is the A ring, TMEM holds ND diagonals of 64 columns.
 template <int NSL>
 struct Sl {
-    static constexpr int W = NSL == 7 ? 8 : 7;                                      // bits per digit
-    static constexpr int ND = NSL == 7 ? 8 : NSL;                                    // diagonals kept
+    static constexpr int W = (NSL == 7 || NSL == 3) ? 8 : 7;                        // bits per digit
+    static constexpr int ND = NSL == 7 ? 8 : NSL == 3 ? 4 : NSL;                     // diagonals kept
     static constexpr int B_STAGE = NSL * B_TILE;                                   // 28 / 32 / 16 KB
     static constexpr int A_STAGES = (225 * 1024 - B_STAGES * B_STAGE) / A_TILE;     // 21 / 20 / 24
     static constexpr size_t SMEM = size_t(A_STAGES) * A_TILE + size_t(B_STAGES) * B_STAGE + 1024;
@@ -535,10 +535,19 @@ __device__ __forceinline__ void digits7(double x, int e, unsigned (&d)[7]) {
     d[5] = (lo >> 8) & 255u;
     d[6] = lo & 255u;
 }
+// NSL = 3 (FP32-class, 8-bit digits): R = rint(x 2^(22-e)), |R| <= 2^22, the bytes of
+// U = R + 0x808080: x = 2^e sum_p d_p 2^(-6-8p), p = 0..2, up to 2^(e-23)
+__device__ __forceinline__ void digits3(double x, int e, unsigned (&d)[3]) {
+    const unsigned U = unsigned(__double2int_rn(mul_pow2(x, 22 - e)) + 0x808080);
+    d[0] = U >> 16;
+    d[1] = (U >> 8) & 255u;
+    d[2] = U & 255u;
+}
 template <int NSL>
 __device__ __forceinline__ void digits(double x, int e, unsigned (&d)[NSL]) {
     if constexpr (NSL == 8) digits8(x, e, d);
     else if constexpr (NSL == 7) digits7(x, e, d);
+    else if constexpr (NSL == 3) digits3(x, e, d);
     else digits4(x, e, d);
 }
 
@@ -795,7 +804,8 @@ int64_t ozaki_x_bytes(int64_t rows, int64_t k, int nsl) {
 }
 int64_t ozaki_z_bytes(int64_t n, int64_t k, int nsl) { return ceil_div(k, OZ_BK) * nsl * int64_t(ozaki_bn(n)) * OZ_BK; }
 static void check_nsl(int nsl) {
-    if (nsl != 8 && nsl != 7 && nsl != 4) throw Error(kStatusInvalid, "ozaki: slices per operand must be 8, 7 or 4");
+    if (nsl != 8 && nsl != 7 && nsl != 4 && nsl != 3)
+        throw Error(kStatusInvalid, "ozaki: slices per operand must be 8, 7, 4 or 3");
 }
 
 int64_t ozaki_line_max_words(int64_t m, int64_t n) { return m + n; }
@@ -825,6 +835,7 @@ static void slice_a_impl(const T* a, int64_t m, int64_t n, int64_t ld, unsigned*
     const dim3 g(unsigned(ceil_div(m, OZ_BM) * (OZ_BM / 64)), unsigned(ceil_div(n, OZ_BM) * (OZ_BM / 64)));
     if (nsl == 8) launch_k(k_slice_a<T, 8>, g, 256, 0, s, a, m, n, ld, rmax, cmax, x_tn, e_tn, x_nn, e_nn);
     else if (nsl == 7) launch_k(k_slice_a<T, 7>, g, 256, 0, s, a, m, n, ld, rmax, cmax, x_tn, e_tn, x_nn, e_nn);
+    else if (nsl == 3) launch_k(k_slice_a<T, 3>, g, 256, 0, s, a, m, n, ld, rmax, cmax, x_tn, e_tn, x_nn, e_nn);
     else launch_k(k_slice_a<T, 4>, g, 256, 0, s, a, m, n, ld, rmax, cmax, x_tn, e_tn, x_nn, e_nn);
     FQB_LAUNCHED();
     lc.bump(2);
@@ -849,6 +860,7 @@ void ozaki_slice_z(const double* b, int64_t k, int64_t n, int64_t ld, int* e, in
     const dim3 g(OZ_BN, unsigned(ceil_div(chunks, ZT)));
     if (nsl == 8) launch_k(k_slice_z<8>, g, ZT, 0, s, b, k, n, ld, e, out);
     else if (nsl == 7) launch_k(k_slice_z<7>, g, ZT, 0, s, b, k, n, ld, e, out);
+    else if (nsl == 3) launch_k(k_slice_z<3>, g, ZT, 0, s, b, k, n, ld, e, out);
     else launch_k(k_slice_z<4>, g, ZT, 0, s, b, k, n, ld, e, out);
     FQB_LAUNCHED();
     lc.bump();
@@ -905,6 +917,9 @@ static void launch_ozaki(int64_t M, int64_t N, int64_t K, double alpha, const in
         } else if (nsl == 7) {
             configure_ozaki<false, 7>();
             launch_k(k_ozaki<false, 7>, a.grid, OZ_THREADS, Sl<7>::SMEM, s, a);
+        } else if (nsl == 3) {
+            configure_ozaki<false, 3>();
+            launch_k(k_ozaki<false, 3>, a.grid, OZ_THREADS, Sl<3>::SMEM, s, a);
         } else {
             configure_ozaki<false, 4>();
             launch_k(k_ozaki<false, 4>, a.grid, OZ_THREADS, Sl<4>::SMEM, s, a);
@@ -913,7 +928,7 @@ static void launch_ozaki(int64_t M, int64_t N, int64_t K, double alpha, const in
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(unsigned(2 * a.grid));
         cfg.blockDim = dim3(OZ_THREADS);
-        cfg.dynamicSmemBytes = nsl == 8 ? Sl<8>::SMEM : nsl == 7 ? Sl<7>::SMEM : Sl<4>::SMEM;
+        cfg.dynamicSmemBytes = nsl == 8 ? Sl<8>::SMEM : nsl == 7 ? Sl<7>::SMEM : nsl == 3 ? Sl<3>::SMEM : Sl<4>::SMEM;
         cfg.stream = s;
         cudaLaunchAttribute attr[2];
         attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -930,6 +945,9 @@ static void launch_ozaki(int64_t M, int64_t N, int64_t K, double alpha, const in
         } else if (nsl == 7) {
             configure_ozaki<true, 7>();
             FQB_CUDA(cudaLaunchKernelEx(&cfg, k_ozaki<true, 7>, a));
+        } else if (nsl == 3) {
+            configure_ozaki<true, 3>();
+            FQB_CUDA(cudaLaunchKernelEx(&cfg, k_ozaki<true, 3>, a));
         } else {
             configure_ozaki<true, 4>();
             FQB_CUDA(cudaLaunchKernelEx(&cfg, k_ozaki<true, 4>, a));

@@ -623,7 +623,7 @@ class Engine:
         return out.value
 
     def set_fp32_slices(self, slices: int) -> None:
-        """FP32 inputs: 8 slices per operand (FP64-class A passes, default) or 4 (FP32-class,
+        """FP32 inputs: 8 slices per operand (FP64-class A passes, default), 4 or 3 (FP32-class,
         about twice as fast; fqb_set_fp32_slices)."""
         st = self._lib.fqb_set_fp32_slices(self._h, int(slices))
         if st:

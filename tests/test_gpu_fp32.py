@@ -119,18 +119,19 @@ def test_c5_shape_slice_fp32(eng):
     assert abs(res.residual_sq - tot) <= 1e-10 * res.norm_a_sq
 
 
-@pytest.fixture
-def eng4():
-    """A separate engine with FP32-class A passes (fqb_set_fp32_slices(4))."""
+@pytest.fixture(params=[4, 3])
+def eng4(request):
+    """A separate engine with FP32-class A passes (fqb_set_fp32_slices(4): 7-bit digits,
+    10 products; (3): 8-bit digits, 8 products)."""
     e = fqb.Engine(0)
-    e.set_fp32_slices(4)
+    e.set_fp32_slices(request.param)
     yield e
     e.close()
 
 
 @pytest.mark.parametrize("kind,zeta", [(0, 0), (2, 0), (3, 4), (4, 4)])
 def test_fp32_four_slices_within_the_fp32_contract(eng, eng4, port, monkeypatch, kind, zeta):
-    """4 slices per operand: FP32-class products.  Against the FP64 oracle on double(A):
+    """4 or 3 slices per operand: FP32-class products.  Against the FP64 oracle on double(A):
     the same rank / blocks / ids and E within the FP32-mode bar (1e-4 relative); against
     the 8-slice run on the same A and Omega: Q B within 1e-6 of A's scale (the QB of one
     sketch is unique, so this isolates the precision of the products)."""

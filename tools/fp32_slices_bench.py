@@ -1,4 +1,4 @@
-"""FP32 input: QB time-to-eps with FP64-class (8 slices) vs FP32-class (4 slices) A passes,
+"""FP32 input: QB time-to-eps with FP64-class (8) vs FP32-class (4 or 3 slices) A passes,
 on a config-5-like low-rank-plus-noise FP32 matrix (rows x cols given), b = 128,
 sparse sign zeta = 4, P = 1, eps = 5e-2 (the config-5 settings) with a block cap."""
 import sys
@@ -19,7 +19,7 @@ a = eng.gen_lowrank(m, n, sig, seed=42, noise=1e-3).float()
 a = a.t().contiguous().t()
 cfg = FarpcaConfig(eps=5e-2, power=1, block=128, sketch=SketchSpec(3, 0.0, 7, zeta=4), relative=True,
                    max_iters=12)
-for nsl in (8, 4):
+for nsl in (8, 4, 3):
     e = fqb.Engine(0)
     e.set_fp32_slices(nsl)
     out = []
