@@ -218,7 +218,7 @@ def sketch_roofline(eng, dev):
 
 
 def load_traffic():
-    path = os.path.join(ROOT, "profiles", "traffic_r04.json")
+    path = os.path.join(ROOT, "profiles", "traffic_r05.json")
     try:
         with open(path) as f:
             return json.load(f)
