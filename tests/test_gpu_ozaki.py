@@ -55,7 +55,8 @@ def _check_rows(got, aa, b, c0, alpha, beta, rows):
 
 @pytest.mark.parametrize("trans", [True, False])
 @pytest.mark.parametrize("m,n,k", [(8000, 50, 8000), (257, 33, 999), (128, 64, 64), (129, 1, 65), (1, 17, 3),
-                                   (300, 64, 5000), (1000, 20, 127)])
+                                   (300, 64, 5000), (1000, 20, 127), (500, 56, 700), (500, 57, 700),
+                                   (200, 49, 4096)])
 def test_emulated_gemm_fp64_accuracy(eng, trans, m, n, k):
     g = torch.Generator(device="cpu").manual_seed(m + 3 * n + 7 * k + int(trans))
     a = torch.randn((k, m) if trans else (m, k), dtype=torch.float64, generator=g)
@@ -126,7 +127,7 @@ def test_emulated_gemm_is_deterministic(eng):
     assert torch.equal(r1, r2)
 
 
-@pytest.mark.parametrize("n", [65, 100, 128, 200])
+@pytest.mark.parametrize("n", [65, 100, 112, 113, 128, 200])
 def test_emulated_gemm_wide_n_in_chunks(eng, n):
     """n > 64 runs as balanced chunks of <= 64 columns (config 4 has b = 100)."""
     m, k = 700, 900
