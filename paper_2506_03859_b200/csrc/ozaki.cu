@@ -719,10 +719,20 @@ __global__ void __launch_bounds__(ZT) k_slice_z(const double* __restrict__ b, in
     const bool live = j < n;
     unsigned h = 0;
     if (live) {
+        // eight loads in flight per thread (k = 8000: four round trips instead of eight)
         int64_t r = threadIdx.x;
-        for (; r + 3 * ZT < k; r += 4 * ZT)
-            h = max(max(max(h, abs_hi(col[r])), abs_hi(col[r + ZT])), max(abs_hi(col[r + 2 * ZT]), abs_hi(col[r + 3 * ZT])));
-        for (; r < k; r += ZT) h = max(h, abs_hi(col[r]));
+        for (; r + 7 * ZT < k; r += 8 * ZT) {
+            unsigned x[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) x[u] = abs_hi(col[r + u * ZT]);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) h = max(h, x[u]);
+        }
+        unsigned x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) x[u] = r + u * ZT < k ? abs_hi(col[r + u * ZT]) : 0u;   // the tail, also in flight
+#pragma unroll
+        for (int u = 0; u < 8; ++u) h = max(h, x[u]);
     }
     h = __reduce_max_sync(0xFFFFFFFFu, h);
     if (lane == 0) wmax[warp] = h;
