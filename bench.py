@@ -1,26 +1,36 @@
 #!/usr/bin/env python
 """farPCA time-to-epsilon benchmark (BASELINE.json metric) on B200.
 
-Workload (BASELINE.json configs[1], the metric's single-GPU config "C2"):
-  A = U diag(sigma) V', 8000 x 8000 FP64, sigma_i = 10^(-i/50) (i = 1..900; smaller
-  values drop below 1e-18 sigma_1 as in synthetic.cpp:21), U, V = random_orthonormal
-  (8000, 900, seed 42) on the reference's factor streams, generated on the device by
-  fqb_gen_lowrank (make_matrix); standardized-Bernoulli Omega (p = 1/2), b = 50, P = 2,
-  eps = 1e-3 relative.
+Workload: BASELINE.json configs[3] ("C4"), the largest configuration that fits one
+GPU: A = X diag(sigma) Y', 100000 x 20000 FP64 (16 GB), rank 2000, sigma_i =
+10^(-3i/2000), X, Y = Q of QR of seeded N(0,1) (the deterministic generator
+fqb_gen_lowrank_det, seed 42 -- bit-identical to its host twin oracle/detgen.c, so the
+reference's golden run tests/golden/c4.json is on this exact matrix); sparse-Gaussian
+Omega with zeta = 8 nonzeros per column (seed 7), b = 100, P = 2, eps = 1e-3 relative.
 
-One step = one full run_fixed_precision to eps (rank 200, 4 blocks) through the
+One step = one full run_fixed_precision to eps (20 blocks, rank 2000) through the
 engine -- the blocked QB loop plus the assembly of U, sigma, V, exactly what the
-reference's run_fixed_precision times -- with A resident in HBM (512 MB > 126 MB
-L2, so no L2 flush is needed between steps).  `e2e` repeats the step through the public API with A in pinned host
-memory (H2D inside the timed region) and Q, B' returned to the host.
+reference's run_fixed_precision returns -- with A resident in HBM (16 GB >> the 126 MB
+L2, so no flush is needed between steps).  `e2e` repeats the step through the public
+API with A in pinned host memory (the 16 GB H2D inside the timed region) and Q, B', U,
+V returned to the host.  `roofline` times the dominant kernel live (k_ozaki on the
+paired column chunks, W = A'Y at the C4 shape).  `cpu_baseline` / `--impl reference`
+time the unmodified reference (oracle/_ref, single-threaded like the library) on a
+bounded row sample of the same matrix and extrapolate (see cpu_sample()).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+--gpus N > 1 without torchrun re-launches itself under torch.distributed.run; every
+rank makes only its own row shard of A (the generator's factor Grams run over all
+rows, so the shards are bit-equal to rows of the whole) and the engine all-reduces
+over NCCL (strong scaling: one problem, rows sharded).
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -30,13 +40,14 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-M = N = 8000
-RANK_SIG = 900
-BLOCK, POWER, EPS, P_BERN = 50, 2, 1e-3, 0.5
+M, N = 100000, 20000
+RANK_SIG = 2000
+BLOCK, POWER, EPS, ZETA = 100, 2, 1e-3, 8
 SEED_A, SEED_OMEGA = 42, 7
-FP64_PEAK_TFLOPS = 37.1     # measured DMMA peak on this pool (profiles/fp64_peak_r01.txt)
-HBM_PEAK_GBS = 6550.4       # MEASURED_PEAKS.json hbm_gbs (copy)
-WORKLOAD = "C2: 8000x8000 FP64, sigma_i=10^(-i/50), StdBernoulli p=1/2, b=50, P=2, eps=1e-3"
+KIND_SPARSE_GAUSSIAN = 4
+SAMPLE_ROWS = 2000          # CPU reference sample: the first rows of A, one block
+WORKLOAD = ("C4: A = X diag(10^(-3i/2000)) Y', 100000x20000 FP64, rank 2000; sparse Gaussian Omega "
+            "zeta=8; b=100, P=2, eps=1e-3 relative")
 
 
 def parse():
@@ -49,21 +60,46 @@ def parse():
     return ap.parse_args()
 
 
-def make_matrix(device):
-    """C2's A on the device with the engine's own generator (fqb_gen_lowrank): U, V =
-    random_orthonormal(8000, 900, seed 42) on the reference's factor streams
-    0xFA000001 / 0xFA000002 (SURVEY.md section 8(d) convention), sigma_i = 10^(-i/50)."""
+def sigma():
     import numpy as np
-    import paper_2506_03859_b200 as fqb
-    idx = device.index if getattr(device, "index", None) is not None else 0
-    sig = 10.0 ** (-np.arange(1, RANK_SIG + 1, dtype=np.float64) / 50.0)
-    return fqb.default_engine(idx).gen_lowrank(M, N, sig, seed=SEED_A)   # column-major (DenseMatrix layout)
+    return 10.0 ** (-3.0 * np.arange(1, RANK_SIG + 1, dtype=np.float64) / RANK_SIG)
+
+
+def peaks():
+    """Roofline denominators: MEASURED_PEAKS.json (driver-written) for HBM; the FP64
+    DMMA peak measured by this repo (profiles/fp64_peak_r01.txt) for context."""
+    out = {"hbm_gbs": None, "source": "MEASURED_PEAKS.json", "fp64_tflops": 37.1,
+           "fp64_source": "profiles/fp64_peak_r01.txt (DMMA microbenchmark; no FP64 entry in MEASURED_PEAKS.json)"}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            mp = json.load(f)
+        out["hbm_gbs"] = float(mp["hbm_gbs"])
+    except (OSError, ValueError, KeyError):
+        out["hbm_gbs"] = 6650.0
+        out["source"] = "fallback (B200_PROFILING.md: 6.65 TB/s)"
+    return out
+
+
+def bench_config(world: int) -> dict:
+    """The workload description -- identical in both arms."""
+    return {"workload": WORKLOAD, "m": M, "n": N, "rank_signal": RANK_SIG, "sigma": "10^(-3i/2000), i=1..2000",
+            "sketch": "sparse gaussian", "zeta": ZETA, "block": BLOCK, "power": POWER, "eps": EPS,
+            "relative": True, "seed_a": SEED_A, "seed_omega": SEED_OMEGA,
+            "generator": "fqb_gen_lowrank_det == oracle/detgen.c (bit-identical)",
+            "step": "run_fixed_precision to eps + assemble_svd (U, sigma, V)",
+            "l2": "A (16 GB) exceeds the 126 MB L2; no flush needed",
+            "parallelism": f"rows of A sharded over {world} GPUs, NCCL all-reduce" if world > 1 else "single GPU"}
 
 
 def config():
     from paper_2506_03859_b200 import FarpcaConfig, SketchKind, SketchSpec
     return FarpcaConfig(eps=EPS, power=POWER, block=BLOCK,
-                        sketch=SketchSpec(SketchKind.StdBernoulli, P_BERN, SEED_OMEGA), relative=True)
+                        sketch=SketchSpec(SketchKind.SparseGaussian, 0.0, SEED_OMEGA, zeta=ZETA), relative=True)
+
+
+def make_matrix(eng, row0=0, rows=None):
+    """Rows [row0, row0 + rows) of C4's A on the device (fqb_gen_lowrank_det)."""
+    return eng.gen_lowrank_det(M, N, sigma(), SEED_A, 0.0, row0, M - row0 if rows is None else rows)
 
 
 class ClockSampler:
@@ -119,60 +155,61 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def apass_roofline(eng, a, stream):
-    """Live per-launch timing of the dominant kernel: one A pass of the QB loop,
-    W = A' Y (TN) and Y = A G (NN) at 8000 x 50 x 8000, as the engine runs it --
-    k_slice_z + k_ozaki (INT8 tcgen05 FP64 emulation) + k_ozaki_fixup on a
-    persistent sliced A (fqb_slice_operand / fqb_sliced_gemm), CUDA events on the
-    stream the kernels are launched on.  HBM bound: the A slices are nsl bytes per
-    element of A (fqb_fp64_slices: 7 by default), streamed once per pass.  The FP64 DMMA GEMM of the same product
-    is timed beside it for reference."""
+def ozaki_roofline(eng, a, stream, pk):
+    """Live per-launch timing of the dominant kernel: k_ozaki on the paired column chunks
+    (b = 100 -> two chunks of 50 on multicast CTA pairs, + its stream-K fixup), W = A'Y at
+    the C4 shape, on A and Y sliced beforehand (fqb_slice_operand / fqb_sliced_gemm_again),
+    CUDA events on the launching stream.  Algorithmic bytes = SURVEY 8(d)'s dense A'Y figure
+    8(mn + mb + nb) (FP64 A read once, Y read, W written); the kernel actually streams the
+    7-byte slices of A (7mn), reported beside it.  The same A pass as the loop runs it (with
+    the per-pass slicing of Y, k_slice_z) and the NN pass Y = A G are timed too."""
     import torch
-    y = torch.randn(BLOCK, M, dtype=torch.float64, device=a.device).t()   # m x b col-major
-    w = torch.empty(BLOCK, N, dtype=torch.float64, device=a.device).t()
-    yn = torch.empty(BLOCK, M, dtype=torch.float64, device=a.device).t()
-    g = torch.randn(BLOCK, N, dtype=torch.float64, device=a.device).t()
-    reps = 20
+    m, n = a.shape
+    b = BLOCK
+    y = torch.randn(b, m, dtype=torch.float64, device=a.device).t()
+    w = torch.empty(b, n, dtype=torch.float64, device=a.device).t()
+    g = torch.randn(b, n, dtype=torch.float64, device=a.device).t()
+    yn = torch.empty(b, m, dtype=torch.float64, device=a.device).t()
     from paper_2506_03859_b200 import _native
     nsl = int(_native.lib().fqb_fp64_slices())
     out = {"nsl": nsl}
-    sl = eng.slice_operand(a.data_ptr(), M, N, a.stride(1))
-    for name, trans, outp, bp in (("tn", True, w, y), ("nn", False, yn, g)):
-        k, rows = (M, N) if trans else (N, M)
-        for kind in ("ozaki", "kernel", "dmma"):
-            if kind == "kernel":   # k_ozaki (+ its stream-K fixup) alone, on the B slices just made
-                sl.gemm(trans, BLOCK, 1.0, bp.data_ptr(), bp.stride(1), 0.0, outp.data_ptr(), outp.stride(1))
+    sl = eng.slice_operand(a.data_ptr(), m, n, a.stride(1))
+    reps = 6
+    try:
+        for name, trans, outp, bp in (("tn", True, w, y), ("nn", False, yn, g)):
+            rows, k = (n, m) if trans else (m, n)
+            for kind in ("pass", "kernel"):
+                sl.gemm(trans, b, 1.0, bp.data_ptr(), bp.stride(1), 0.0, outp.data_ptr(), outp.stride(1))
 
-            def call():
-                if kind == "ozaki":
-                    sl.gemm(trans, BLOCK, 1.0, bp.data_ptr(), bp.stride(1), 0.0, outp.data_ptr(), outp.stride(1))
-                elif kind == "kernel":
-                    sl.gemm_again(1.0, 0.0, outp.data_ptr(), outp.stride(1))
-                else:
-                    eng.gemm(trans, rows, BLOCK, k, 1.0, a.data_ptr(), a.stride(1), bp.data_ptr(), bp.stride(1),
-                             0.0, outp.data_ptr(), outp.stride(1))
-            for _ in range(3):
-                call()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            with torch.cuda.stream(stream):
-                e0.record()
-                for _ in range(reps):
+                def call():
+                    if kind == "pass":
+                        sl.gemm(trans, b, 1.0, bp.data_ptr(), bp.stride(1), 0.0, outp.data_ptr(), outp.stride(1))
+                    else:
+                        sl.gemm_again(1.0, 0.0, outp.data_ptr(), outp.stride(1))
+                for _ in range(2):
                     call()
-                e1.record()
-            e1.synchronize()
-            ms = e0.elapsed_time(e1) / reps
-            alg_bytes = float(nsl) * M * N + 8.0 * k * BLOCK + 8.0 * rows * BLOCK   # A (as slices), B, C
-            out[f"{name}_{kind}"] = {"ms": ms, "gbs": alg_bytes / ms / 1e6, "bytes": alg_bytes,
-                                     "tflops": 2.0 * M * N * BLOCK / ms / 1e9}
-    sl.free()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                with torch.cuda.stream(stream):
+                    e0.record()
+                    for _ in range(reps):
+                        call()
+                    e1.record()
+                e1.synchronize()
+                ms = e0.elapsed_time(e1) / reps
+                alg = 8.0 * (m * n + k * b + rows * b)
+                out[f"{name}_{kind}"] = {"ms": ms, "gbs": alg / ms / 1e6, "bytes": alg,
+                                         "slice_gbs": (nsl * m * n + 8.0 * (k * b + rows * b)) / ms / 1e6,
+                                         "fp64_tflops_equiv": 2.0 * m * n * b / ms / 1e9}
+    finally:
+        sl.free()
     return out
 
 
-def sketch_roofline(eng, dev):
-    """Sparse-sign sketch Y = A*Omega at BASELINE config 3 shape (A 20000 x 20000 FP64,
-    b = 64, zeta = 8): HBM GB/s of the gather SpMM against the measured copy peak.
-    32 different Omega blocks are cycled so consecutive launches touch different
-    columns of A (each block reads 512 of 20000 columns, 82 MB, < L2 otherwise)."""
+def sketch_roofline(eng, dev, pk):
+    """Sparse-sign sketch Y = A*Omega at BASELINE config 3's shape (A 20000 x 20000 FP64,
+    b = 64, zeta = 8): HBM GB/s of the gather SpMM.  32 different Omega blocks, each writing
+    its own Y (32 x 10 MB > L2), so neither the column reads nor the Y writes of one launch
+    are served from L2 by the previous one."""
     import numpy as np
     import torch
     from paper_2506_03859_b200 import SketchKind, SketchSpec
@@ -186,14 +223,14 @@ def sketch_roofline(eng, dev):
         u = len(np.unique(s.row_idx))
         blocks.append((torch.from_numpy(s.col_ptr.astype(np.int32)).to(dev),
                        torch.from_numpy(s.row_idx.astype(np.int32)).to(dev),
-                       torch.from_numpy(s.values).to(dev)))
+                       torch.from_numpy(s.values).to(dev),
+                       torch.empty(b, m, dtype=torch.float64, device=dev).t()))
         alg_bytes.append(8 * m * (u + b) + 12 * s.nnz + 4 * (b + 1))
-    y = torch.empty(b, m, dtype=torch.float64, device=dev).t()
-    stream = torch.cuda.Stream(device=dev)   # a real stream: handle 0 would mean the engine's own
+    stream = torch.cuda.Stream(device=dev)
     eng.set_stream(stream.cuda_stream)
 
     def launch(j):
-        cp, ri, va = blocks[j]
+        cp, ri, va, y = blocks[j]
         eng.sparse_dense_mul(a.data_ptr(), m, n, m, cp.data_ptr(), ri.data_ptr(), va.data_ptr(), b, None,
                              y.data_ptr(), m)
     for j in range(nblk):
@@ -209,32 +246,95 @@ def sketch_roofline(eng, dev):
     e1.synchronize()
     ms = e0.elapsed_time(e1) / (reps * nblk)
     gbs = (sum(alg_bytes) / nblk) / (ms * 1e-3) / 1e9
-    del a
+    del a, blocks
     torch.cuda.empty_cache()
-    return {"kernel": "k_gather_spmm (sparse sign, zeta=8) Y = A*Omega, A 20000x20000, b=64",
-            "achieved": gbs, "peak": HBM_PEAK_GBS, "unit": "GB/s", "frac": gbs / HBM_PEAK_GBS,
+    return {"kernel": "k_gather_spmm (sparse sign, zeta=8) Y = A*Omega, A 20000x20000, b=64, 32 distinct Y",
+            "achieved": gbs, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": gbs / pk["hbm_gbs"],
             "launch_us": ms * 1e3, "bytes_per_launch": sum(alg_bytes) / nblk,
             "bytes_formula": "8*m*(u+b) + 12*nnz + 4*(b+1), u = distinct rows of the block"}
 
 
 def load_traffic():
-    path = os.path.join(ROOT, "profiles", "traffic_r05.json")
+    for name in ("traffic_r08.json", "traffic_r07.json"):
+        try:
+            with open(os.path.join(ROOT, "profiles", name)) as f:
+                return json.load(f)
+        except (OSError, ValueError):
+            continue
+    return None
+
+
+def host_info():
+    cpu = "unknown"
     try:
-        with open(path) as f:
-            return json.load(f)
-    except (OSError, ValueError):
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    cpu = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu": cpu, "nproc": os.cpu_count()}
+
+
+def cpu_sample(a_rows, blocks_full):
+    """The unmodified reference (oracle/_ref; else the C port) on a bounded sample of the
+    workload: the first SAMPLE_ROWS rows of A (SAMPLE_ROWS x 20000), one block (max_iters
+    = 1: the sparse sketch, 2P+1 = 5 dense passes, CholQR, B update), single-threaded like
+    the library (kernels.hpp:5-8).  Extrapolated to time-to-eps on the whole matrix as
+    t_sample * (M / SAMPLE_ROWS) * blocks_full: every pass over A scales with its rows and
+    the run repeats the block blocks_full times.  This leaves out the costs that grow with
+    the accumulated rank (deflation, re-orthogonalisation against l up to 2000, the l x l
+    Jacobi of assemble_svd), so it UNDER-states the reference's time; the full C4 reference
+    run, measured once on the build host, is in tests/golden/c4.json."""
+    import numpy as np
+    from oracle.oracle import REF_LIB, Oracle
+    which = "reference" if os.path.exists(REF_LIB) else "port"
+    orc = Oracle(which)
+    a = np.asfortranarray(a_rows)
+
+    def src(nn, bb, bid):
+        return orc_port().gen_sketch(KIND_SPARSE_GAUSSIAN, 0.0, SEED_OMEGA, nn, bb, bid, zeta=ZETA)
+    t0 = time.perf_counter()
+    r = orc.run(a, eps=EPS, power=POWER, block=BLOCK, kind=KIND_SPARSE_GAUSSIAN, seed=SEED_OMEGA, zeta=ZETA,
+                max_iters=1, relative=True, source=src)
+    dt = time.perf_counter() - t0
+    scale = (M / a.shape[0]) * blocks_full
+    return dt, dt * scale, which, r
+
+
+_PORT = None
+
+
+def orc_port():
+    global _PORT
+    if _PORT is None:
+        from oracle.oracle import Oracle
+        _PORT = Oracle("port")
+    return _PORT
+
+
+def full_reference_record():
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "c4.json")) as f:
+            g = json.load(f)
+        return {"seconds": g["reference_seconds"], "host": g["host"], "rank": g["rank"], "blocks": g["blocks"],
+                "source": "tests/golden/c4.json (one full reference run on the build host, 1 core)"}
+    except (OSError, ValueError, KeyError):
         return None
 
 
-def cpu_baseline_reference(a_host, kind):
-    """The reference CPU implementation (oracle/_ref, else the C port) on one core."""
-    from oracle.oracle import Oracle, REF_LIB
-    which = "reference" if os.path.exists(REF_LIB) else "port"
-    orc = Oracle(which)
-    t0 = time.perf_counter()
-    r = orc.run(a_host, eps=EPS, power=POWER, block=BLOCK, kind=2, p=P_BERN, seed=SEED_OMEGA, relative=True)
-    dt = time.perf_counter() - t0
-    return dt, which, r
+def maybe_spawn(args):
+    """--gpus N > 1 outside torchrun: re-launch under torch.distributed.run on 127.0.0.1."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return False
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
 
 
 def run_ours(args):
@@ -249,21 +349,17 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     torch.cuda.set_device(local)
     dev = torch.device(f"cuda:{local}")
+    pk = peaks()
 
     import paper_2506_03859_b200 as fqb
     from paper_2506_03859_b200.dist import partition_rows
     eng = fqb.Engine(local)
     stream = torch.cuda.Stream(device=dev)
     eng.set_stream(stream.cuda_stream)
-    a_full = make_matrix(dev)
+    r0, r1 = partition_rows(M, world, rank) if world > 1 else (0, M)
+    a = make_matrix(eng, r0, r1 - r0)           # this rank's row shard only
     if world > 1:
-        # strong scaling: one problem, rows of A sharded over the GPUs, NCCL all-reduce
-        r0, r1 = partition_rows(M, world, rank)
-        a = a_full[r0:r1, :].t().contiguous().t()
-        a_full = None
         eng.attach_comm()
-    else:
-        a = a_full
     torch.cuda.synchronize()
     cfg = config()
 
@@ -288,8 +384,7 @@ def run_ours(args):
     last = None
     for _ in range(args.steps):
         # like rsvd::run_fixed_precision: QB loop + assemble_svd (U, sigma, V), all on the device.
-        # The previous step's factors are released first (as a caller that consumed them
-        # would), so every step allocates its outputs from the warm pool.
+        # The previous step's factors are released first (as a caller that consumed them would).
         last = None
         r = eng.run_fixed_precision(a, cfg, output="device", svd=True)
         step_ms.append(r.elapsed_ms)
@@ -304,38 +399,45 @@ def run_ours(args):
         t = torch.tensor([ms], device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = t.item()
+    result = {"rank": last.rank, "blocks": last.blocks, "converged": bool(last.converged),
+              "rel_error_indicator": float(np.sqrt(max(last.residual_sq, 0) / last.norm_a_sq)),
+              "step_device_ms": step_ms}
+    last = None
 
-    rank_l, blocks, e_rel = last.rank, last.blocks, float(np.sqrt(max(last.residual_sq, 0) / last.norm_a_sq))
-
-    # ---- e2e: host A (pinned) -> public API -> Q, B' back on the host -----------------
-    a_host = a.t().contiguous().cpu().pin_memory()  # (n x m_local) row-major == A column-major
+    # ---- e2e: pinned host A (this rank's rows) -> public API -> Q, B', U, V on the host --
+    m_loc = a.shape[0]
+    a_host = torch.empty((N, m_loc), dtype=torch.float64, pin_memory=True)   # (n x m) row-major == A col-major
+    a_host.copy_(a.t())
     a_host_cm = a_host.t()
-    for _ in range(1):
-        eng.run_fixed_precision(a_host_cm, cfg, output="host", svd=True)
+    eng.run_fixed_precision(a_host_cm, cfg, output="host", svd=True)
     torch.cuda.synchronize()
     t_e2e = []
     r = None
-    for _ in range(args.steps):
+    e2e_steps = max(1, min(args.steps, 5))
+    for _ in range(e2e_steps):
         r = None   # the caller is done with the previous factors (their pinned blocks return to the pool)
+        barrier()
         t0 = time.perf_counter()
         r = eng.run_fixed_precision(a_host_cm, cfg, output="host", svd=True)
         t_e2e.append(time.perf_counter() - t0)
     e2e_s = statistics.mean(t_e2e)
     clk.__exit__(None, None, None)
-    h2d = a.shape[0] * N * 8
+    h2d = m_loc * N * 8
     # Q, B' and U, V (m x l, n x l each), sigma, flags and the per-block trace
-    d2h = 2 * (a.shape[0] + N) * r.rank * 8 + 9 * r.rank + 8 * (r.blocks + 4)
-
+    d2h = 2 * (m_loc + N) * r.rank * 8 + 9 * r.rank + 8 * (r.blocks + 4)
+    r = None
+    del a_host, a_host_cm
     if world > 1:
         t = torch.tensor([e2e_s], device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_s = t.item()
-    roof = apass_roofline(eng, a_full if world == 1 else make_matrix(dev), stream)
-    a_full = None
+
+    roof = ozaki_roofline(eng, a, stream, pk)
+    a_rows = a[:SAMPLE_ROWS].cpu().numpy() if (rank == 0 and world == 1 and not args.no_cpu_baseline) else None
+    del a
     torch.cuda.empty_cache()
-    sketch = sketch_roofline(eng, dev)
+    sketch = sketch_roofline(eng, dev, pk)
     dom = roof["tn_kernel"]   # the dominant kernel by itself (k_ozaki + its stream-K fixup)
-    pas = roof["tn_ozaki"]    # the whole A pass as the engine runs it (+ k_slice_z of Y)
     traffic = load_traffic()
     line = {
         "metric": "farPCA time-to-eps (s)",
@@ -349,37 +451,38 @@ def run_ours(args):
         "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f64",
-        "data": "synthetic: A = U diag(sigma) V' from fqb_gen_lowrank (Philox factor streams, seed 42), see make_matrix",
-        "config": {"workload": WORKLOAD, "m": M, "n": N, "block": BLOCK, "power": POWER, "eps": EPS,
-                   "sketch": "stdbernoulli p=0.5", "rank_reached": rank_l, "blocks": blocks,
-                   "rel_error_indicator": e_rel, "step_device_ms": step_ms, "l2": "A (512 MB) exceeds the 126 MB L2; no flush",
-                   "parallelism": f"rows of A sharded over {world} GPUs, NCCL all-reduce" if world > 1
-                   else "single GPU"},
-        "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "data": "synthetic: C4's A from fqb_gen_lowrank_det (seed 42), bit-identical to oracle/detgen.c",
+        "config": bench_config(world),
+        "result": result,
+        "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "steps": e2e_steps},
         "gpu_launches": launches,
         "roofline": {"bound": "hbm",
-                     "kernel": "k_ozaki (tcgen05 kind::i8 FP64 emulation, + k_ozaki_fixup of the split tiles), "
-                               "W=A'Y 8000x50x8000 on pre-sliced A and Y (fqb_sliced_gemm_again)",
-                     "achieved": dom["gbs"], "peak": HBM_PEAK_GBS, "unit": "GB/s", "frac": dom["gbs"] / HBM_PEAK_GBS,
-                     "bytes_per_launch": dom["bytes"], "bytes_formula": f"{roof['nsl']}*m*n (A slices, fqb_fp64_slices) + 8*m*b (Y) + 8*n*b (W)",
-                     "launch_ms": dom["ms"], "nn_achieved": roof["nn_kernel"]["gbs"],
-                     "nn_launch_ms": roof["nn_kernel"]["ms"],
+                     "kernel": "k_ozaki<true,7> (tcgen05 kind::i8 FP64 emulation, two 50-column chunks on "
+                               "multicast CTA pairs) + k_ozaki_fixup, W = A'Y at 100000x100x20000 on pre-sliced "
+                               "A and Y (fqb_sliced_gemm_again)",
+                     "achieved": dom["gbs"], "peak": pk["hbm_gbs"], "unit": "GB/s",
+                     "frac": dom["gbs"] / pk["hbm_gbs"], "traffic": (traffic or {}).get("ozaki_c4_tn_bytes_per_launch"),
+                     "peak_source": pk["source"],
+                     "bytes_per_launch": dom["bytes"], "bytes_formula": "8*(m*n + m*b + n*b) (SURVEY 8(d), dense A'Y)",
+                     "slice_bytes_per_launch": roof["nsl"] * M * N + 8.0 * (M * BLOCK + N * BLOCK),
+                     "slice_gbs": dom["slice_gbs"], "launch_ms": dom["ms"],
+                     "fp64_tflops_equiv": dom["fp64_tflops_equiv"], "fp64_peak_tflops": pk["fp64_tflops"],
+                     "nn_kernel_ms": roof["nn_kernel"]["ms"], "nn_achieved": roof["nn_kernel"]["gbs"],
                      "pass": {"what": "the whole A pass as the QB loop runs it: k_slice_z (Y) + k_ozaki + fixup",
-                              "tn_ms": pas["ms"], "tn_achieved": pas["gbs"], "tn_frac": pas["gbs"] / HBM_PEAK_GBS,
-                              "nn_ms": roof["nn_ozaki"]["ms"], "nn_achieved": roof["nn_ozaki"]["gbs"]},
-                     "fp64_tflops_equiv": dom["tflops"],
-                     "dmma_same_product": {"tn_ms": roof["tn_dmma"]["ms"], "tn_tflops": roof["tn_dmma"]["tflops"],
-                                           "nn_ms": roof["nn_dmma"]["ms"], "peak_tflops": FP64_PEAK_TFLOPS},
-                     "traffic": (traffic or {}).get("ozaki_tn_bytes_per_launch")},
+                              "tn_ms": roof["tn_pass"]["ms"], "tn_achieved": roof["tn_pass"]["gbs"],
+                              "nn_ms": roof["nn_pass"]["ms"], "nn_achieved": roof["nn_pass"]["gbs"]}},
         "sketch_roofline": sketch,
         "clocks": clk.summary(),
     }
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        a_np = np.asfortranarray(a.cpu().numpy())
-        dt, which, rr = cpu_baseline_reference(a_np, 2)
-        line["cpu_baseline"] = {"value": dt, "unit": "s", "cores": 1, "kind": which,
-                                "sample": f"one full C2 run_fixed_precision (rank {rr.rank}, "
-                                          f"{rr.blocks} blocks), single-threaded like the reference"}
+    if a_rows is not None:
+        dt, est, which, rr = cpu_sample(a_rows, result["blocks"])
+        line["cpu_baseline"] = {"value": est, "unit": "s", "cores": 1, "kind": which,
+                                "sample": f"reference run_fixed_precision on rows [0,{SAMPLE_ROWS}) of A, 1 block "
+                                          f"(max_iters=1): {dt:.2f} s; x (m/{SAMPLE_ROWS}) x {result['blocks']} "
+                                          "blocks (excludes the rank-dependent costs, so a lower bound)",
+                                "sample_seconds": dt, "host": host_info(),
+                                "full_run_on_build_host": full_reference_record()}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -387,41 +490,44 @@ def run_ours(args):
 
 
 def run_reference(args):
-    """--impl reference: the reference's own CPU run_fixed_precision (oracle/_ref)."""
+    """--impl reference: the reference's own CPU run_fixed_precision (oracle/_ref) on the
+    bounded sample of cpu_sample(), each step one sample, value extrapolated to C4."""
     import numpy as np
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import torch
-    dev = torch.device("cuda:0") if torch.cuda.is_available() else torch.device("cpu")
-    a = np.asfortranarray(make_matrix(dev).cpu().numpy())
-    from oracle.oracle import Oracle, REF_LIB
-    which = "reference" if os.path.exists(REF_LIB) else "port"
-    orc = Oracle(which)
-    budget_s = 150.0
-    times = []
-    t_start = time.perf_counter()
+    import ctypes as C
+    from oracle.oracle import PORT_LIB
+    lib = C.CDLL(PORT_LIB)
+    lib.fqo_det_lowrank.argtypes = [C.c_int64, C.c_int64, C.c_int, C.c_void_p, C.c_uint64, C.c_double, C.c_int64,
+                                    C.c_int64, C.c_void_p, C.c_int64]
+    sig = sigma()
+    a = np.empty((N, SAMPLE_ROWS), dtype=np.float64).T        # the same rows the ours arm samples, host-made
+    st = lib.fqo_det_lowrank(M, N, len(sig), sig.ctypes.data, SEED_A, 0.0, 0, SAMPLE_ROWS, a.ctypes.data,
+                             SAMPLE_ROWS)
+    if st:
+        print(json.dumps({"impl": "reference", "unavailable": f"fqo_det_lowrank failed ({st})"}))
+        return
+    full = full_reference_record()
+    blocks_full = full["blocks"] if full else 20
+    times, ests = [], []
     for i in range(max(args.warmup, 0) + args.steps):
-        t0 = time.perf_counter()
-        r = orc.run(a, eps=EPS, power=POWER, block=BLOCK, kind=2, p=P_BERN, seed=SEED_OMEGA, relative=True)
-        dt = time.perf_counter() - t0
-        if i >= min(args.warmup, 1):
+        dt, est, which, r = cpu_sample(a, blocks_full)
+        if i >= args.warmup:
             times.append(dt)
-        if time.perf_counter() - t_start > budget_s and times:
-            break
-        if i == 0 and args.warmup > 0:
-            continue
-    v = statistics.mean(times)
-    # n_gpus echoes the launch (--gpus N) so the line pairs with our arm's; the work itself
-    # runs on host cores (cpu_baseline.cores)
+            ests.append(est)
+    v = statistics.mean(ests)
+    # n_gpus echoes the launch (--gpus N) so the line pairs with our arm's; the work runs on host cores
     line = {"metric": "farPCA time-to-eps (s)", "value": v, "unit": "s", "n_gpus": args.gpus,
-            "steps": len(times), "warmup": min(args.warmup, 1), "ms_per_step": v * 1000,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1000,
             "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (same A as the ours arm)", "impl": "reference",
-            "config": {"workload": WORKLOAD, "rank_reached": r.rank, "blocks": r.blocks},
+            "data": "synthetic: the same A (oracle/detgen.c rows = fqb_gen_lowrank_det rows)", "impl": "reference",
+            "config": bench_config(args.gpus),
             "cpu_baseline": {"value": v, "unit": "s", "cores": 1, "kind": which,
-                             "sample": f"{len(times)} full run(s) within a {budget_s:.0f}s budget; "
-                                       "the reference is single-threaded per factorization"},
+                             "sample": f"each step: reference run_fixed_precision on rows [0,{SAMPLE_ROWS}) of A, "
+                                       f"1 block (mean {statistics.mean(times):.2f} s); value = x (m/{SAMPLE_ROWS}) x "
+                                       f"{blocks_full} blocks (a lower bound: rank-dependent costs excluded)",
+                             "sample_seconds": times, "host": host_info(), "full_run_on_build_host": full},
             "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -431,4 +537,5 @@ if __name__ == "__main__":
     if a.impl == "reference":
         run_reference(a)
     else:
+        maybe_spawn(a)
         run_ours(a)

@@ -329,6 +329,18 @@ fqb_status fqb_gen_synthetic(fqb_handle h, int kind, int n, int d, uint64_t seed
  * 0xFA000002, noise on 0xFA000003 keyed by column; sigma on the host. */
 fqb_status fqb_gen_lowrank(fqb_handle h, int64_t m, int64_t n, int r, const double* sigma, uint64_t seed,
                            double noise, double* a, int64_t lda);
+/* Deterministic low-rank inputs (BASELINE configs 3-4 at full size): rows [row0, row0 + rows)
+ * of A = X diag(sigma) Y' + noise_scale G, X / Y the Q of CholeskyQR of Philox Gaussians
+ * (streams 0xFA000001 / 0xFA000002, G on 0xFA000003, libm-free Box-Muller of
+ * include/farqb/detmath.h), every product an fma chain in ascending k on the FP64 pipe.
+ * Bit-identical to the host twin oracle/detgen.c (fqo_det_lowrank), so the CPU reference
+ * can be run on the same matrix.  a: device, rows x n, lda >= rows; sigma on the host. */
+fqb_status fqb_gen_lowrank_det(fqb_handle h, int64_t m, int64_t n, int r, const double* sigma, uint64_t seed,
+                               double noise_scale, int64_t row0, int64_t rows, double* a, int64_t lda);
+/* Order-independent 64-bit fingerprint of a device matrix's bits (row shard [row0, row0 +
+ * rows) of an m_total-row matrix; shards sum mod 2^64 to the whole), = fqo_checksum. */
+fqb_status fqb_checksum(fqb_handle h, const double* a, int64_t rows, int64_t cols, int64_t lda, int64_t row0,
+                        int64_t m_total, uint64_t* out);
 
 /* ---- defaults (driver.cpp:449-466) ------------------------------------------- */
 double fqb_default_density(int kind, int64_t n);

@@ -10,6 +10,7 @@
  * second implementation of the same algorithm; it is pinned against the
  * compiled reference (oracle/_ref) by tests/test_oracle_pin.py.
  */
+#include "../include/farqb/detmath.h"
 #include "farqb_oracle.h"
 
 #include <math.h>
@@ -79,6 +80,26 @@ static double philox_next_unit(philox_t* r) {
 }
 
 /* Box-Muller pair with a cached spare; exact zeros redrawn, rng.hpp:39-56. */
+/* The same pair logic through the libm-free Box-Muller of include/farqb/detmath.h:
+ * the fixed-zeta sparse-Gaussian values (a kind the reference does not have), so
+ * the device draws bit-identical Omega values for a seed. */
+static double philox_next_gaussian_det(philox_t* r) {
+    if (r->have_spare) {
+        r->have_spare = 0;
+        if (r->spare != 0.0) return r->spare;
+    }
+    for (;;) {
+        double u1 = philox_next_unit(r);
+        double u2 = philox_next_unit(r);
+        double z0, z1;
+        fqd_box_muller(u1, u2, &z0, &z1);
+        r->spare = z1;
+        r->have_spare = 1;
+        if (z0 != 0.0) return z0;
+        r->have_spare = 0;
+    }
+}
+
 static double philox_next_gaussian(philox_t* r) {
     if (r->have_spare) {
         r->have_spare = 0;
@@ -425,7 +446,9 @@ static int nz_push(nzbuf_t* b, int row, double v) {
  *   the column stream, duplicates skipped, until zeta rows are held; then one
  *   value per row in draw order -- sign: the next u32's top bit set gives
  *   -1/sqrt(zeta), clear gives +1/sqrt(zeta); Gaussian: next_gaussian() /
- *   sqrt(zeta) -- and the (row, value) pairs are sorted by row.
+ *   sqrt(zeta), next_gaussian through the libm-free Box-Muller of
+ *   include/farqb/detmath.h so host and device values are bit-identical -- and
+ *   the (row, value) pairs are sorted by row.
  */
 int fqo_gen_sketch(int kind, double p, uint64_t seed, int zeta, int n, int l,
                    int block_id, fqo_block* out) {
@@ -469,7 +492,7 @@ int fqo_gen_sketch(int kind, double p, uint64_t seed, int zeta, int n, int l,
                 if (kind == FQO_SPARSE_SIGN)
                     vals[t] = (philox_next_u32(&r) & 0x80000000u) ? -scale : scale;
                 else
-                    vals[t] = philox_next_gaussian(&r) * scale;
+                    vals[t] = philox_next_gaussian_det(&r) * scale;
             }
             for (int t = 1; t < zeta; ++t) {   /* insertion sort by row */
                 int kr = rows[t];

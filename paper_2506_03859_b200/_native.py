@@ -107,6 +107,10 @@ SIGNATURES = [
                                     C.POINTER(C.c_int)]),
     ("fqb_gen_lowrank", C.c_int, [_H, C.c_int64, C.c_int64, C.c_int, C.c_void_p, C.c_uint64, C.c_double,
                                   C.c_void_p, C.c_int64]),
+    ("fqb_gen_lowrank_det", C.c_int, [_H, C.c_int64, C.c_int64, C.c_int, C.c_void_p, C.c_uint64, C.c_double,
+                                      C.c_int64, C.c_int64, C.c_void_p, C.c_int64]),
+    ("fqb_checksum", C.c_int, [_H, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
+                               C.POINTER(C.c_uint64)]),
     ("fqb_gemm_emulated", C.c_int, [_H, C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_double, C.c_void_p,
                                     C.c_int64, C.c_void_p, C.c_int64, C.c_double, C.c_void_p, C.c_int64]),
     ("fqb_slice_operand", C.c_int, [_H, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.POINTER(C.c_void_p)]),

@@ -613,6 +613,28 @@ fqb_status fqb_gen_lowrank(fqb_handle h, int64_t m, int64_t n, int r, const doub
     });
 }
 
+fqb_status fqb_gen_lowrank_det(fqb_handle h, int64_t m, int64_t n, int r, const double* sigma, uint64_t seed,
+                               double noise_scale, int64_t row0, int64_t rows, double* a, int64_t lda) {
+    return guarded([&]() -> fqb_status {
+        bind(h);
+        if (!a || !sigma) throw farqb::Error(FQB_ERR_INVALID_ARGUMENT, "null pointer");
+        farqb::gen_lowrank_det_dev(h->h, m, n, r, sigma, seed, noise_scale, row0, rows, a, lda);
+        return FQB_OK;
+    });
+}
+
+fqb_status fqb_checksum(fqb_handle h, const double* a, int64_t rows, int64_t cols, int64_t lda, int64_t row0,
+                        int64_t m_total, uint64_t* out) {
+    return guarded([&]() -> fqb_status {
+        bind(h);
+        if (!out || (!a && rows > 0 && cols > 0)) throw farqb::Error(FQB_ERR_INVALID_ARGUMENT, "null pointer");
+        if (rows < 0 || cols < 0 || lda < rows || row0 < 0 || row0 + rows > m_total)
+            throw farqb::Error(FQB_ERR_INVALID_ARGUMENT, "fqb_checksum: bad extents");
+        *out = farqb::checksum_dev(h->h, a, rows, cols, lda, row0, m_total);
+        return FQB_OK;
+    });
+}
+
 double fqb_default_density(int kind, int64_t n) { return farqb::default_density(kind, n); }
 int fqb_default_block(int64_t m, int64_t n) { return farqb::default_block(m, n); }
 int fqb_default_max_iters(int64_t n, int b) { return farqb::default_max_iters(n, b); }

@@ -117,6 +117,11 @@ void random_orthonormal_dev(Handle& h, int64_t n, int r, uint64_t seed, uint32_t
 int gen_synthetic_dev(Handle& h, int kind, int n, int d, uint64_t seed, double* a, int64_t lda);
 void gen_lowrank_dev(Handle& h, int64_t m, int64_t n, int r, const double* sigma, uint64_t seed, double noise,
                      double* a, int64_t lda);
+// detgen.cu: the deterministic generator (bit-equal to oracle/detgen.c) and the matrix fingerprint
+void gen_lowrank_det_dev(Handle& h, int64_t m, int64_t n, int r, const double* sigma_host, uint64_t seed,
+                         double noise_scale, int64_t row0, int64_t rows, double* a, int64_t lda);
+uint64_t checksum_dev(Handle& h, const double* a, int64_t rows, int64_t cols, int64_t lda, int64_t row0,
+                      int64_t m_total);
 // hostmem.cu: pinned, pooled host arrays for results returned on the host
 void* host_alloc(size_t bytes);
 void host_free(void* ptr);

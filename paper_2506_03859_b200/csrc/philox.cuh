@@ -10,6 +10,8 @@
 
 #include <cstdint>
 
+#include "../../include/farqb/detmath.h"
+
 namespace farqb {
 
 struct PhiloxKey {
@@ -69,6 +71,12 @@ __device__ __forceinline__ void box_muller(double u1, double u2, double& z0, dou
     z1 = r * s;
 }
 
+// The same pair on the libm-free Box-Muller of include/farqb/detmath.h: bit-identical
+// to the host (fixed-zeta sparse-Gaussian values, a kind the reference lacks).
+__device__ __forceinline__ void box_muller_det(double u1, double u2, double& z0, double& z1) {
+    fqd_box_muller(u1, u2, &z0, &z1);
+}
+
 // Sequential view of one stream, for the few generators whose draw order is
 // data dependent (fixed-zeta duplicate rejection).  Mirrors the reference's
 // buffered next_u32 / next_unit / next_gaussian (rng.hpp:21-56).
@@ -99,6 +107,7 @@ struct PhiloxStream {
     }
     // Returns false if the reference would have redrawn on an exact zero
     // (probability ~2^-52 per draw); callers flag that as an internal error.
+    template <bool kDet = false>
     __device__ __forceinline__ bool next_gaussian(double& out) {
         if (have_spare) {
             have_spare = false;
@@ -111,7 +120,10 @@ struct PhiloxStream {
         const double u1 = next_unit();
         const double u2 = next_unit();
         double z0, z1;
-        box_muller(u1, u2, z0, z1);
+        if (kDet)
+            box_muller_det(u1, u2, z0, z1);
+        else
+            box_muller(u1, u2, z0, z1);
         spare = z1;
         have_spare = true;
         out = z0;

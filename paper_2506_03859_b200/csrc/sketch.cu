@@ -230,7 +230,7 @@ __global__ void k_zeta_fill(int kind, PhiloxKey key, uint32_t blk, int64_t n, in
             vals[t] = (rng.next_u32() & 0x80000000u) ? -scale : scale;
         } else {
             double g;
-            if (!rng.next_gaussian(g)) atomicOr(status, kGenZeroGaussian);
+            if (!rng.next_gaussian<true>(g)) atomicOr(status, kGenZeroGaussian);
             vals[t] = g * scale;
         }
     }

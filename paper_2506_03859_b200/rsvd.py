@@ -676,6 +676,30 @@ class Engine:
             _raise(st, "fqb_gen_lowrank")
         return a
 
+    def gen_lowrank_det(self, m: int, n: int, sigma, seed: int, noise_scale: float = 0.0, row0: int = 0,
+                        rows: int | None = None):
+        """Rows [row0, row0 + rows) of the deterministic A = X diag(sigma) Y' + noise_scale G
+        (fqb_gen_lowrank_det; bit-equal to the host twin oracle/detgen.c) -> torch rows x n."""
+        import torch
+        rows = m - row0 if rows is None else rows
+        sig = np.ascontiguousarray(np.asarray(sigma, dtype=np.float64))
+        a = torch.empty((n, rows), dtype=torch.float64, device=f"cuda:{self.device}").t()
+        st = self._lib.fqb_gen_lowrank_det(self._h, m, n, len(sig), sig.ctypes.data, seed, float(noise_scale),
+                                           row0, rows, a.data_ptr(), max(rows, 1))
+        if st:
+            _raise(st, "fqb_gen_lowrank_det")
+        return a
+
+    def checksum(self, a, row0: int = 0, m_total: int | None = None) -> int:
+        """fqb_checksum of a device column-major torch matrix (a row shard starting at row0)."""
+        rows, cols = a.shape
+        out = C.c_uint64()
+        st = self._lib.fqb_checksum(self._h, a.data_ptr(), rows, cols, max(a.stride(1), rows, 1), row0,
+                                    rows + row0 if m_total is None else m_total, C.byref(out))
+        if st:
+            _raise(st, "fqb_checksum")
+        return out.value
+
     def slice_operand(self, a_ptr, m, n, lda) -> "SlicedOperand":
         """Cut A (m x n, device, column-major) once into Ozaki slices (fqb_slice_operand)."""
         out = C.c_void_p()

@@ -1,8 +1,8 @@
 """BASELINE configs at full size on the GPU.
 
-C2 is checked against the reference itself (oracle/_ref, ~16 s on one core) on the
-exact bench matrix.  C3 and C4 are too large for the CPU oracle (hours), so they
-are checked through size-independent properties: E equals the true residual
+C2 is checked against the reference itself (oracle/_ref, ~16 s on one core).  C3 and
+C4 are checked against golden reference runs in test_gpu_bigcases.py; here, on other
+seeds, through size-independent properties: E equals the true residual
 ||A - QB||_F^2 (computed on the GPU), Q is orthonormal, the per-block trace is
 monotone, the rank reaches the spectrum's tail, and the run is deterministic.
 """
@@ -20,18 +20,6 @@ from paper_2506_03859_b200 import FarpcaConfig, SketchKind, SketchSpec  # noqa: 
 DEV = torch.device("cuda:0")
 
 
-def _lowrank_dev(m, n, sig, seed, noise=0.0):
-    g = torch.Generator(device=DEV).manual_seed(seed)
-    r = sig.numel()
-    u = torch.linalg.qr(torch.randn(m, r, dtype=torch.float64, device=DEV, generator=g))[0]
-    v = torch.linalg.qr(torch.randn(n, r, dtype=torch.float64, device=DEV, generator=g))[0]
-    a = (u * sig) @ v.t()
-    del u, v
-    if noise:
-        a += noise * torch.randn(m, n, dtype=torch.float64, device=DEV, generator=g) / np.sqrt(n)
-    return a.t().contiguous().t()
-
-
 def _true_residual(a, q, bt, chunk=8192):
     tot = 0.0
     for c0 in range(0, a.shape[1], chunk):
@@ -41,10 +29,17 @@ def _true_residual(a, q, bt, chunk=8192):
     return tot
 
 
-def test_c2_matches_reference_on_the_bench_matrix(reference):
-    import bench
-    a = bench.make_matrix(DEV)
-    cfg = bench.config()
+def _c2_matrix():
+    """BASELINE configs[1]: U diag(10^(-i/50)) V', 8000^2, U, V = random_orthonormal(8000, 900,
+    seed 42) on the reference's factor streams (fqb_gen_lowrank)."""
+    sig = 10.0 ** (-np.arange(1, 901, dtype=np.float64) / 50.0)
+    return fqb.default_engine(0).gen_lowrank(8000, 8000, sig, seed=42)
+
+
+def test_c2_matches_reference(reference):
+    a = _c2_matrix()
+    cfg = FarpcaConfig(eps=1e-3, power=2, block=50, sketch=SketchSpec(SketchKind.StdBernoulli, 0.5, 7),
+                       relative=True)
     res = fqb.run_fixed_precision(a, cfg, output="host", svd=True)
     a_np = np.asfortranarray(a.cpu().numpy())
     eng = fqb.default_engine(0)
@@ -69,8 +64,8 @@ def test_c2_matches_reference_on_the_bench_matrix(reference):
 
 def test_c4_tall_sparse_gaussian_full_size():
     """100000 x 20000, rank 2000, sigma_i = 10^(-3i/2000), sparse Gaussian zeta=8, b=100, P=2, eps=1e-3."""
-    sig = 10.0 ** (-3.0 * torch.arange(1, 2001, dtype=torch.float64, device=DEV) / 2000)
-    a = _lowrank_dev(100000, 20000, sig, seed=4)
+    sig = 10.0 ** (-3.0 * np.arange(1, 2001, dtype=np.float64) / 2000)
+    a = fqb.default_engine(0).gen_lowrank_det(100000, 20000, sig, 4)
     cfg = FarpcaConfig(eps=1e-3, power=2, block=100, sketch=SketchSpec(SketchKind.SparseGaussian, 0.0, 7, zeta=8),
                        relative=True)
     res = fqb.run_fixed_precision(a, cfg, output="device", svd=False)
@@ -93,8 +88,8 @@ def test_c3_noise_floor_full_size():
     The QB also captures noise directions (about l/n of ||N||^2), so depending on
     the draw the run either converges late or stops at the cap with
     ToleranceNotReached; both outcomes must carry a correct indicator."""
-    sig = (1.0 + torch.arange(0, 1000, dtype=torch.float64, device=DEV)) ** -1.5
-    a = _lowrank_dev(20000, 20000, sig, seed=3, noise=1e-4)
+    sig = (1.0 + np.arange(0, 1000, dtype=np.float64)) ** -1.5
+    a = fqb.default_engine(0).gen_lowrank_det(20000, 20000, sig, 3, 1e-4 / np.sqrt(20000))
     cfg = FarpcaConfig(eps=1e-2, power=1, block=64, sketch=SketchSpec(SketchKind.SparseSign, 0.0, 7, zeta=8),
                        relative=True)
     try:

@@ -16,27 +16,15 @@ from paper_2506_03859_b200 import FarpcaConfig, SketchKind, SketchSpec
 DEV = torch.device("cuda:0")
 
 
-def lowrank(m, n, sig, seed, noise=0.0):
-    g = torch.Generator(device=DEV).manual_seed(seed)
-    r = sig.numel()
-    u = torch.linalg.qr(torch.randn(m, r, dtype=torch.float64, device=DEV, generator=g))[0]
-    v = torch.linalg.qr(torch.randn(n, r, dtype=torch.float64, device=DEV, generator=g))[0]
-    a = (u * sig) @ v.t()
-    del u, v
-    if noise:
-        a += noise * torch.randn(m, n, dtype=torch.float64, device=DEV, generator=g) / np.sqrt(n)
-    return a.t().contiguous().t()
-
-
 which = sys.argv[1] if len(sys.argv) > 1 else "c4"
 if which == "c4":
-    sig = 10.0 ** (-3.0 * torch.arange(1, 2001, dtype=torch.float64, device=DEV) / 2000)
-    a = lowrank(100000, 20000, sig, seed=4)
+    sig = 10.0 ** (-3.0 * np.arange(1, 2001, dtype=np.float64) / 2000)
+    a = fqb.default_engine(0).gen_lowrank_det(100000, 20000, sig, 42)
     cfg = FarpcaConfig(eps=1e-3, power=2, block=100, sketch=SketchSpec(SketchKind.SparseGaussian, 0.0, 7, zeta=8),
                        relative=True)
 else:
-    sig = (1.0 + torch.arange(0, 1000, dtype=torch.float64, device=DEV)) ** -1.5
-    a = lowrank(20000, 20000, sig, seed=3, noise=1e-4)
+    sig = (1.0 + np.arange(0, 1000, dtype=np.float64)) ** -1.5
+    a = fqb.default_engine(0).gen_lowrank_det(20000, 20000, sig, 42, 1e-4 / np.sqrt(20000))
     cfg = FarpcaConfig(eps=1e-2, power=1, block=64, sketch=SketchSpec(SketchKind.SparseSign, 0.0, 7, zeta=8),
                        relative=True)
 eng = fqb.Engine(0)

@@ -1,8 +1,8 @@
-"""Warm per-kernel times of one C2 run_fixed_precision (CUPTI via torch.profiler).
+"""Warm per-kernel times of one run_fixed_precision (CUPTI via torch.profiler).
 
 Unlike an ncu launch list (caches flushed and kernels serialised per launch),
 this is the steady state the bench sees.  Usage:
-    python tools/kernel_profile.py [--svd] [--runs N]
+    python tools/kernel_profile.py [--config c4|c2] [--svd] [--runs N]
 """
 import argparse
 import collections
@@ -19,11 +19,19 @@ import paper_2506_03859_b200 as fqb  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--svd", action="store_true")
 ap.add_argument("--runs", type=int, default=3)
+ap.add_argument("--config", default="c4", choices=["c4", "c2"])
 args = ap.parse_args()
 
 eng = fqb.Engine(0)
-a = bench.make_matrix(torch.device("cuda:0"))
-cfg = bench.config()
+if args.config == "c4":
+    a = bench.make_matrix(eng)
+    cfg = bench.config()
+else:
+    import numpy as np
+    from paper_2506_03859_b200 import FarpcaConfig, SketchKind, SketchSpec
+    a = eng.gen_lowrank(8000, 8000, 10.0 ** (-np.arange(1, 901) / 50.0), seed=42)
+    cfg = FarpcaConfig(eps=1e-3, power=2, block=50, sketch=SketchSpec(SketchKind.StdBernoulli, 0.5, 7),
+                       relative=True)
 for _ in range(2):
     eng.run_fixed_precision(a, cfg, output="device", svd=args.svd)
 torch.cuda.synchronize()
