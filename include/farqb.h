@@ -203,6 +203,11 @@ void fqb_result_free(fqb_qb_result* r);
  * faults).  A caller that keeps one of those arrays beyond the result frees it
  * with fqb_host_free and sets the field to NULL before fqb_result_free. */
 void fqb_host_free(void* p);
+/* Host results live in a process-wide pool of pinned blocks, reused across runs; at most
+ * FQB_HOST_POOL_MB (environment, default 4096) MB of free blocks stay cached.  This
+ * releases every cached free block now (also done when the last handle is destroyed);
+ * returns the bytes released. */
+size_t fqb_host_pool_trim(void);
 
 /* ---- row-sharded multi-GPU (one rank per GPU, NCCL over NVLink) ------------- */
 /* Rank 0 creates a 128-byte id, the caller distributes it (e.g. with
@@ -250,8 +255,9 @@ fqb_status fqb_centering_column(fqb_handle h, const double* a, int64_t m, int64_
 fqb_status fqb_frob_norm_sq(fqb_handle h, const double* a, int64_t m, int64_t n, int64_t lda,
                             double* host_out);
 /* FP32 input mode (fqb_qb_*_f32): slices per operand of the A passes on the INT8 tensor
- * cores.  8 (default): every product FP64-class (the FP64 scheme, fqb_fp64_slices), the
- * run equals the FP64 run on the widened A to ~1e-15.  4: FP32-class products (~2^-26 of
+ * cores.  Any value >= 7 (the default sentinel is 8): every product FP64-class -- the FP64
+ * scheme with fqb_fp64_slices() slices (7 by default) -- and the run equals the FP64 run on
+ * the widened A to ~1e-15.  4: FP32-class products (~2^-26 of
  * max|row| max|col|, ten int8 products on 7-bit digits, 4 bytes per element of A);
  * 3: FP32-class on 8-bit digits (8 products, 3 bytes per element, representation 2^-23
  * of the line max) -- both within the FP32-mode parity bar of 1e-4 and about twice as

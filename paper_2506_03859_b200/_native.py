@@ -107,6 +107,7 @@ SIGNATURES = [
                                     C.POINTER(C.c_int)]),
     ("fqb_gen_lowrank", C.c_int, [_H, C.c_int64, C.c_int64, C.c_int, C.c_void_p, C.c_uint64, C.c_double,
                                   C.c_void_p, C.c_int64]),
+    ("fqb_host_pool_trim", C.c_size_t, []),
     ("fqb_gen_lowrank_det", C.c_int, [_H, C.c_int64, C.c_int64, C.c_int, C.c_void_p, C.c_uint64, C.c_double,
                                       C.c_int64, C.c_int64, C.c_void_p, C.c_int64]),
     ("fqb_checksum", C.c_int, [_H, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int64,

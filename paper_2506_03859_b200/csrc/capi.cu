@@ -4,6 +4,7 @@
 // and a thread-local message; no C++ exception crosses the boundary.  There is
 // no host compute path: without a CUDA device every compute call fails with
 // FQB_ERR_CUDA.
+#include <atomic>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -24,6 +25,7 @@ struct fqb_handle_s {
 namespace {
 
 thread_local std::string g_last_error;
+std::atomic<int> g_live_handles{0};   // the pinned host pool is trimmed when the last handle goes
 
 fqb_status set_error(int status, const std::string& msg) {
     g_last_error = msg;
@@ -57,6 +59,8 @@ extern "C" {
 int fqb_abi_version(void) { return FARQB_ABI_VERSION; }
 
 const char* fqb_last_error(void) { return g_last_error.c_str(); }
+
+size_t fqb_host_pool_trim(void) { return farqb::host_pool_trim(); }
 
 const char* fqb_status_name(int status) {
     switch (status) {
@@ -104,6 +108,7 @@ fqb_status fqb_create(int device, fqb_handle* out) {
         uint64_t threshold = UINT64_MAX;
         FQB_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold));
         *out = hs;
+        g_live_handles.fetch_add(1);
         return FQB_OK;
     });
 }
@@ -127,6 +132,7 @@ fqb_status fqb_destroy(fqb_handle h) {
         if (h->h.ev_v) cudaEventDestroy(h->h.ev_v);
         cudaStreamDestroy(h->h.own_stream);
         delete h;
+        if (g_live_handles.fetch_sub(1) == 1) farqb::host_pool_trim();
         return FQB_OK;
     });
 }

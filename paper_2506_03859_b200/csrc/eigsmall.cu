@@ -32,6 +32,8 @@
 // 64 n u ||M||_F and 64 n u -- decides; a failed check returns false and the
 // caller runs cuSOLVER instead, so this path can only be faster, never worse.
 #include <cmath>
+#include <mutex>
+#include <vector>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -804,10 +806,14 @@ __global__ void __launch_bounds__(128) k_apply_house(const double* __restrict__ 
     }
 }
 
-// sums[0] += ||R - X diag(w)||^2, sums[1] += ||M||^2, sums[2] += ||O - I||^2
+// Per-CTA partial sums, in a fixed order (warp shuffles, then warps 0..7), written to
+// part[3 * cta + {0, 1, 2}] = ||R - X diag(w)||^2, ||M||^2, ||O - I||^2 over the CTA's
+// elements; the host adds the CTAs in index order -- so the accept / fallback decision
+// is bitwise reproducible (no floating-point atomics).
 __global__ void k_eig_check(const double* __restrict__ r, const double* __restrict__ x, const double* __restrict__ w,
-                            const double* __restrict__ mat, const double* __restrict__ o, int n, double* sums) {
+                            const double* __restrict__ mat, const double* __restrict__ o, int n, double* part) {
     FQB_PDL_ENTRY();
+    __shared__ double red[3][8];
     const int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;
     double a = 0.0, b = 0.0, c = 0.0;
     if (i < n) {
@@ -821,10 +827,17 @@ __global__ void k_eig_check(const double* __restrict__ r, const double* __restri
     a = warp_sum(a);
     b = warp_sum(b);
     c = warp_sum(c);
+    const int warp = threadIdx.x >> 5;
     if ((threadIdx.x & 31) == 0) {
-        atomicAdd(sums + 0, a);
-        atomicAdd(sums + 1, b);
-        atomicAdd(sums + 2, c);
+        red[0][warp] = a;
+        red[1][warp] = b;
+        red[2][warp] = c;
+    }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+        double t = 0.0;
+        for (int q = 0; q < int(blockDim.x >> 5); ++q) t += red[threadIdx.x][q];
+        part[3 * (int64_t(blockIdx.y) * gridDim.x + blockIdx.x) + threadIdx.x] = t;
     }
 }
 
@@ -847,21 +860,27 @@ bool small_eigh(const double* mat, int n, double* w, double* x, double* scratch,
     double* tau = e + n;
     double* sums = tau + n + n;    // 4 (8-aligned slack above)
     const size_t smem = sizeof(double) * size_t(n * (n + 1) / 2 + 4 * kSmallEighMax + 4 * 256);
-    static bool configured = false;
-    if (!configured) {
-        FQB_CUDA(cudaFuncSetAttribute(k_tri_invit, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kInvitSmem)));
-        const size_t mx = sizeof(double) * size_t(kSmallEighMax * (kSmallEighMax + 1) / 2 + 4 * kSmallEighMax + 4 * 256);
-        FQB_CUDA(cudaFuncSetAttribute(k_sytrd, cudaFuncAttributeMaxDynamicSharedMemorySize, int(mx)));
-        configured = true;
+    // The dynamic shared-memory limits are per-device function attributes: raise them
+    // once on every device a handle lives on (a process may drive several GPUs, from
+    // several threads).
+    {
+        static std::mutex mu;
+        static bool configured[64] = {};
+        int dev = 0;
+        FQB_CUDA(cudaGetDevice(&dev));
+        std::lock_guard<std::mutex> lock(mu);
+        if (dev < 0 || dev >= 64 || !configured[dev]) {
+            FQB_CUDA(cudaFuncSetAttribute(k_tri_invit, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kInvitSmem)));
+            const size_t mx =
+                sizeof(double) * size_t(kSmallEighMax * (kSmallEighMax + 1) / 2 + 4 * kSmallEighMax + 4 * 256);
+            FQB_CUDA(cudaFuncSetAttribute(k_sytrd, cudaFuncAttributeMaxDynamicSharedMemorySize, int(mx)));
+            const size_t mx4 = sizeof(double) * size_t(kTrd4Max * (kTrd4Max + 1) / 2 + 5 * 224 + kTrd4Warps * 224);
+            FQB_CUDA(cudaFuncSetAttribute(k_sytrd5, cudaFuncAttributeMaxDynamicSharedMemorySize, int(mx4)));
+            if (dev >= 0 && dev < 64) configured[dev] = true;
+        }
     }
     if (n <= kTrd4Max) {
         const size_t smem4 = sizeof(double) * size_t(n * (n + 1) / 2 + 5 * 224 + kTrd4Warps * 224);
-        static bool cfg4 = false;
-        if (!cfg4) {
-            const size_t mx4 = sizeof(double) * size_t(kTrd4Max * (kTrd4Max + 1) / 2 + 5 * 224 + kTrd4Warps * 224);
-            FQB_CUDA(cudaFuncSetAttribute(k_sytrd5, cudaFuncAttributeMaxDynamicSharedMemorySize, int(mx4)));
-            cfg4 = true;
-        }
         launch_k(k_sytrd5, 1, kTrd4Warps * 32, smem4, s, mat, n, d, e, tau, vh);
     } else {
         launch_k(k_sytrd, 1, kTrdThreads, smem, s, mat, n, d, e, tau, vh);
@@ -891,13 +910,16 @@ bool small_eigh(const double* mat, int n, double* w, double* x, double* scratch,
     // a-posteriori check: R = M X, O = X'X
     gemm(false, n, n, n, 1.0, mat, n, cur, n, 0.0, r, n, gws, num_sms, s, lc);
     gemm(true, n, n, n, 1.0, cur, n, cur, n, 0.0, g, n, gws, num_sms, s, lc);
-    FQB_CUDA(cudaMemsetAsync(sums, 0, 4 * sizeof(double), s));
-    launch_k(k_eig_check, dim3(unsigned(ceil_div(n, 256)), unsigned(n)), 256, 0, s, r, cur, w, mat, g, n, sums);
+    const int check_ctas = int(ceil_div(n, 256)) * n;   // <= 224 partial triples, in inv (6 n^2 doubles)
+    launch_k(k_eig_check, dim3(unsigned(ceil_div(n, 256)), unsigned(n)), 256, 0, s, r, cur, w, mat, g, n, inv);
     FQB_LAUNCHED();
     lc.bump();
-    double hs[4];
-    FQB_CUDA(cudaMemcpyAsync(hs, sums, 3 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    std::vector<double> part(size_t(3) * check_ctas);
+    FQB_CUDA(cudaMemcpyAsync(part.data(), inv, sizeof(double) * part.size(), cudaMemcpyDeviceToHost, s));
     FQB_CUDA(cudaStreamSynchronize(s));
+    double hs[3] = {0.0, 0.0, 0.0};
+    for (int c = 0; c < check_ctas; ++c)
+        for (int q = 0; q < 3; ++q) hs[q] += part[size_t(3) * c + q];
     const double u = 1.1102230246251565e-16;
     const double res = std::sqrt(hs[0]), mnorm = std::sqrt(hs[1]), orth = std::sqrt(hs[2]);
     const bool ok = std::isfinite(res) && std::isfinite(orth) && res <= 64.0 * n * u * mnorm && orth <= 64.0 * n * u;

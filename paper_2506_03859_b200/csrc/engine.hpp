@@ -125,6 +125,7 @@ uint64_t checksum_dev(Handle& h, const double* a, int64_t rows, int64_t cols, in
 // hostmem.cu: pinned, pooled host arrays for results returned on the host
 void* host_alloc(size_t bytes);
 void host_free(void* ptr);
+size_t host_pool_trim();   // release every cached free block; returns the bytes released
 // ||A - U diag(sigma) V'||_F / ||A||_F (sigma host or null = unscaled), strips of A on the device
 double relative_error(Handle& h, const double* a, int64_t m, int64_t n, int64_t lda, bool a_on_device,
                       const double* u, int64_t ldu, const double* sigma, const double* v, int64_t ldv, int r,

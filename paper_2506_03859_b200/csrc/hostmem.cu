@@ -5,7 +5,9 @@
 // 51 MB, took ~24 ms that way against ~1 ms into pinned memory), so host results
 // live in page-locked blocks from a process-wide pool: cudaMallocHost once, reused
 // after fqb_result_free / fqb_host_free.  Blocks not from the pool (never, unless
-// pinning failed) are plain malloc/free.
+// pinning failed) are plain malloc/free.  At most FQB_HOST_POOL_MB (default 4096) MB
+// of free blocks stay cached; fqb_host_pool_trim() returns them all to the OS, and
+// so does destroying the last handle.
 #include <cuda_runtime.h>
 
 #include <cstdlib>
@@ -28,7 +30,14 @@ Pool& pool() {
     static Pool* p = new Pool();   // never destroyed: blocks may be freed during static teardown
     return *p;
 }
-constexpr size_t kMaxCached = size_t(16) << 30;   // keep at most 16 GB of free pinned blocks
+size_t max_cached() {
+    static const size_t cap = [] {
+        const char* e = std::getenv("FQB_HOST_POOL_MB");
+        const long long mb = e ? std::atoll(e) : 4096;
+        return size_t(mb < 0 ? 0 : mb) << 20;
+    }();
+    return cap;
+}
 
 }  // namespace
 
@@ -67,12 +76,25 @@ void host_free(void* ptr) {
     }
     const size_t bytes = it->second;
     p.live.erase(it);
-    if (p.cached + bytes > kMaxCached) {
+    if (p.cached + bytes > max_cached()) {
         cudaFreeHost(ptr);
         return;
     }
     p.free_blocks.emplace(bytes, ptr);
     p.cached += bytes;
+}
+
+size_t host_pool_trim() {
+    Pool& p = pool();
+    std::lock_guard<std::mutex> lk(p.mu);
+    size_t freed = 0;
+    for (auto& kv : p.free_blocks) {
+        cudaFreeHost(kv.second);
+        freed += kv.first;
+    }
+    p.free_blocks.clear();
+    p.cached = 0;
+    return freed;
 }
 
 }  // namespace farqb

@@ -13,7 +13,12 @@
 // in TMEM (8 x 64 int32 columns = all 512).  The epilogue adds the diagonals
 // from the least significant up in FP64 and applies the exponents.  The
 // dropped terms (d >= 8: 5 products, ~2^-59) and r are below 2^-54 relative to
-// max|row| * max|col|, i.e. the accuracy class of an FP64 GEMM.  NSL = 8 is the
+// max|row| * max|col|.  The bound is NORMWISE per line, not elementwise: an entry
+// much smaller than its line's maximum keeps only ~54 - log2(max/|x|) bits, so a
+// product is FP64-class relative to max|row_i(A)| * max|col_j(Z)|, which is the
+// class of the normwise FP64 GEMM bound K u |A_i| |Z_j| the QB loop's parity bars
+// rest on (tests/test_gpu_ozaki.py: graded-line products and QB runs on matrices
+// whose lines span 1e-8..1, against the oracle).  NSL = 8 is the
 // same with 7-bit digits (R = rint(x 2^(55-e)), 36 products, 8 bytes per element);
 // NSL = 4 the FP32-class variant for FP32 input.
 //
@@ -36,8 +41,8 @@
 // stream-K style; a CTA writes pieces of split tiles, already scaled, to its
 // partial slots and k_ozaki_fixup sums them in CTA order (deterministic).
 //
-// Measured (C2, A'Y 8000x50x8000, B200, NSL = 8): 104 us + 3 us fixup, vs 235 us
-// for the FP64 DMMA GEMM; HBM floor for the 512 MB of A slices ~80 us.
+// Measured (C2, A'Y 8000x50x8000, B200, NSL = 7): 104-106 us + 3 us fixup, vs 235 us
+// for the FP64 DMMA GEMM; HBM floor for the 448 MB of A slices ~70 us.
 #include <cuda.h>
 #include <cuda_runtime.h>
 

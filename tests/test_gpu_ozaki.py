@@ -247,3 +247,83 @@ def test_tile_result_independent_of_tmem_history(eng):
         eng.gemm_emulated(False, 128, N, K, 1.0, a[t * 128:].data_ptr(), M, b.data_ptr(), K, 0.0, part.data_ptr(), 128)
         torch.cuda.synchronize()
         assert torch.equal(part, full[t * 128:(t + 1) * 128]), t
+
+
+# ---------------------------------------------------------------- graded lines (the scheme's weak case)
+
+def _check_rows_normwise(got, aa, b, c0, alpha, beta, rows):
+    """The emulation's bound: per output (i, j), 2^-54-class relative to max|row_i(op A)| *
+    sum_k |b_kj| (plus the final rounding) -- the normwise FP64 GEMM class, NOT elementwise."""
+    ar = aa[rows].numpy().astype(np.longdouble)
+    bl = b.numpy().astype(np.longdouble)
+    exact = alpha * (ar @ bl) + beta * c0[rows].numpy().astype(np.longdouble)
+    rowmax = np.abs(ar).max(axis=1, keepdims=True)
+    colmax = np.abs(bl).max(axis=0, keepdims=True)
+    k = ar.shape[1]
+    # slice rounding of op(A) (<= 2^-55 rowmax per element) and of B (<= 2^-55 colmax), summed over k
+    bound = abs(alpha) * (2.0 ** -54) * (rowmax @ np.abs(bl).sum(axis=0, keepdims=True)
+                                         + np.abs(ar).sum(axis=1, keepdims=True) @ colmax)
+    err = np.abs(got[rows].numpy().astype(np.longdouble) - exact)
+    tol = bound + 4e-16 * abs(beta) * np.abs(c0[rows].numpy()) + 2.0 ** -53 * np.abs(exact) + 1e-300
+    assert (err <= tol).all(), float(np.max(err / tol))
+    # and how far from elementwise FP64 accuracy the small entries are (informational)
+    elem = abs(alpha) * (np.abs(ar) @ np.abs(bl)) + 1e-300
+    return float(np.max(err / elem))
+
+
+@pytest.mark.parametrize("trans", [True, False])
+def test_emulated_gemm_graded_within_lines(eng, trans):
+    """Every line of op(A) spans 1e-8 .. 1 (columns of A graded for the row-scaled A G
+    layout, rows graded for the column-scaled A'Y one) plus a few spikes: the normwise
+    bound holds for every element."""
+    m, n, k = 600, 64, 3000
+    g = torch.Generator(device="cpu").manual_seed(31 + int(trans))
+    opa = torch.randn((m, k), dtype=torch.float64, generator=g) * torch.logspace(-8, 0, k, dtype=torch.float64)
+    opa[:, ::997] *= 1e3    # spikes
+    b = torch.randn((k, n), dtype=torch.float64, generator=g)
+    c0 = torch.zeros((m, n), dtype=torch.float64)
+    a = opa.t().contiguous() if trans else opa       # trans: A is k x m with op(A) = A'
+    got = _run_emulated(eng, trans, a, b, c0, 1.0, 0.0)
+    rel = _check_rows_normwise(got, opa, b, c0, 1.0, 0.0, np.arange(0, m, 5))
+    assert rel > 0.0
+
+
+def _graded(m, n, sig, seed, rows: bool):
+    a = _lowrank(m, n, sig, seed)
+    d = np.logspace(-8, 0, m if rows else n)
+    np.random.default_rng(seed).shuffle(d)
+    return np.asfortranarray(a * d[:, None] if rows else a * d[None, :])
+
+
+@pytest.mark.parametrize("rows", [False, True])
+@pytest.mark.parametrize("kind,zeta,power", [(3, 8, 1), (0, 0, 2), (2, 0, 1)])
+def test_qb_emulation_on_graded_matrix_matches_oracle(eng, port, monkeypatch, rows, kind, zeta, power):
+    """A with its columns (rows) scaled by 1e-8 .. 1 -- every row (column) of A then spans
+    eight decades, the emulation's weak case -- through the QB loop with every A pass on
+    the INT8 tensor cores, against the oracle on the same Omega: same rank / blocks / ids,
+    E within 1e-10 ||A||^2, top sigma within 1e-10 sigma_max, Q B within 1e-10 ||A||_F."""
+    monkeypatch.setenv("FQB_OZAKI", "1")
+    a = _graded(1600, 1300, 0.9 ** np.arange(400), 90 + kind + 3 * int(rows), rows)
+    p = 0.5 if kind == 2 else 0.0
+    spec = SketchSpec(kind, p, 17, zeta=zeta)
+    cfg = FarpcaConfig(eps=1e-3, power=power, block=32, sketch=spec, relative=True)
+    res = eng.run_fixed_precision(a, cfg, output="host", svd=True)
+
+    def src(n, b, bid):
+        s = eng.gen_sketch(spec, n, b, bid)
+        if s.is_dense:
+            return SketchArrays(True, s.rows, s.cols, dense=s.dense, p=s.p)
+        return SketchArrays(False, s.rows, s.cols, col_ptr=s.col_ptr, row_idx=s.row_idx, values=s.values,
+                            centered=s.centered, p=s.p, std_scale=s.std_scale)
+    ref = port.run(a, eps=1e-3, power=power, block=32, kind=kind, p=p, seed=17, zeta=zeta, relative=True,
+                   source=src, want_vectors=True)
+    assert ref.status == 0 and res.converged
+    assert (res.rank, res.blocks, res.block_ids) == (ref.rank, ref.blocks, ref.block_ids)
+    na = ref.norm_a_sq
+    assert abs(res.residual_sq - ref.residual_sq) <= 1e-10 * na
+    assert np.max(np.abs(res.block_residuals - ref.block_residuals)) <= 1e-10 * na
+    top = ref.sigma >= 1e-3 * ref.sigma[-1]
+    assert np.max(np.abs(res.sigma[top] - ref.sigma[top])) <= 1e-10 * ref.sigma[-1]
+    qb = res.q @ res.bt.T
+    usv = (ref.u * ref.sigma) @ ref.v.T
+    assert np.linalg.norm(qb - usv) <= 1e-10 * np.sqrt(na)

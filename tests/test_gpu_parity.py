@@ -281,6 +281,30 @@ def test_qb_injected_block_source_matches_reference(reference, port):
         _check_run(res, ref, power, f"injected P={power}")
 
 
+@pytest.mark.parametrize("kind,zeta,p", [(0, 0, 0.0), (2, 0, 0.5), (3, 8, 0.0), (4, 8, 0.0)])
+@pytest.mark.parametrize("power", [1, 2])
+def test_qb_product_matches_reference_usv(eng, reference, kind, zeta, p, power):
+    """North-star Q.B parity: ||Q_gpu B_gpu - U_ref diag(sigma_ref) V_ref'||_F <= 1e-10 ||A||_F
+    against the unmodified reference (oracle/_ref, want_vectors) on the same Omega, for all
+    four test-matrix kinds (driver.hpp:45-58: ApproxSvd u, sigma, v)."""
+    a = _lowrank(1100, 800, 0.95 ** np.arange(300), seed=200 + 10 * kind + power)
+    spec = SketchSpec(kind, p, 23, zeta=zeta)
+    cfg = FarpcaConfig(eps=1e-3, power=power, block=30, sketch=spec, relative=True)
+    res = eng.run_fixed_precision(a, cfg, output="host", svd=True)
+
+    def src(n, b, bid):
+        return _arr(eng.gen_sketch(spec, n, b, bid))
+    ref = reference.run(a, eps=1e-3, power=power, block=30, kind=kind, p=p, seed=23, zeta=0, relative=True,
+                        source=src, want_vectors=True, traced=True)
+    assert ref.status == 0 and res.converged
+    assert (res.rank, res.blocks, res.block_ids) == (ref.rank, ref.blocks, ref.block_ids)
+    norm_a = np.sqrt(ref.norm_a_sq)
+    usv = (ref.u * ref.sigma) @ ref.v.T
+    assert np.linalg.norm(res.q @ res.bt.T - usv) <= 1e-10 * norm_a
+    # and the GPU's own ApproxSvd reproduces the same product
+    assert np.linalg.norm((res.u * res.sigma) @ res.v.T - usv) <= 1e-10 * norm_a
+
+
 def test_c1_reference_matrix(reference):
     """BASELINE config 1 exactly: gen_synthetic(SlowDecay, 2000, seed 42), Gaussian, b=20, P=1, eps=1e-2."""
     a = reference.gen_synthetic(0, 2000, 42)
