@@ -62,18 +62,23 @@ constexpr int OZ_BM = 128;               // rows per tile (UMMA M)
 constexpr int OZ_BK = 64;
 constexpr int SWZ_ROWS = 1024 / 128;     // the swizzle pattern repeats every 8 rows (SBO = 8 rows)
 constexpr int OZ_BN = 64;                // max N (8 diagonals x 64 = 512 TMEM columns)
-constexpr int B_STAGES = 2;
 constexpr int A_TILE = OZ_BM * OZ_BK;             // 8 KB, one slice
 constexpr int B_TILE = OZ_BN * OZ_BK;             // 4 KB per slice (bn = 64)
 // Per slice count NSL: 7 (FP64-class, the default: 8-bit digits, diagonals d = p+q <= 7,
 // 34 products), 8 (FP64-class, 7-bit digits, d <= 7, 36 products), 4 (FP32-class for FP32
 // input, 7-bit digits, d <= 3, 10 products), 3 (FP32-class, 8-bit digits, d <= 3, 8 products).  The Z stage holds all NSL slices of a k-block, the rest
 // of 225 KB is the A ring, TMEM holds ND diagonals of 64 columns.
-template <int NSL>
+// Z rows per k-block of the slices of one column chunk: NSL slices of S rows each (S = 64,
+// or S = 56 for chunks of <= 56 columns, then with 8 zero rows after the last slice that
+// the N = 64 lone products of the S = 56 schedule read past it)
+__host__ __device__ constexpr int z_block_rows(int nsl, int S) { return nsl * S + (S == 56 ? 8 : 0); }
+
+template <int NSL, int BS = 2, int S = 64>
 struct Sl {
+    static constexpr int B_STAGES = BS;                                            // Z stages (2 or 3)
     static constexpr int W = (NSL == 7 || NSL == 3) ? 8 : 7;                        // bits per digit
     static constexpr int ND = NSL == 7 ? 8 : NSL == 3 ? 4 : NSL;                     // diagonals kept
-    static constexpr int B_STAGE = NSL * B_TILE;                                   // 28 / 32 / 16 KB
+    static constexpr int B_STAGE = z_block_rows(NSL, S) * OZ_BK;                   // 28 / 32 / 16 KB (25 KB at S = 56)
     static constexpr int A_STAGES = (225 * 1024 - B_STAGES * B_STAGE) / A_TILE;     // 21 / 20 / 24
     static constexpr size_t SMEM = size_t(A_STAGES) * A_TILE + size_t(B_STAGES) * B_STAGE + 1024;
     static constexpr unsigned TMEM_COLS = unsigned(ND * OZ_BN);                     // 512 / 512 / 256
@@ -131,6 +136,9 @@ struct OzArgs {
     // min(cw, N - r cw), work + r work_stride.  grid counts clusters.
     int pair;
     int64_t zs_stride, cw, work_stride;
+    // L2 policy of the bulk copies: A slices evict-first (streamed once per pass), Z
+    // slices evict-last (re-read by every row tile; the pairs walk different k ranges)
+    int l2hint;
 };
 
 // this CTA's (or fixup block's) column chunk of a paired launch
@@ -179,6 +187,30 @@ __device__ __forceinline__ void bulk_load_mc2(unsigned dst, const void* src, uns
         "%4;\n" ::"r"(dst),
         "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(bar), "h"((unsigned short)3)
         : "memory");
+}
+__device__ __forceinline__ void bulk_load_mc2_hint(unsigned dst, const void* src, unsigned bytes, unsigned bar,
+                                                   uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster.L2::cache_hint [%0], "
+        "[%1], %2, [%3], %4, %5;\n" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(bar), "h"((unsigned short)3), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_load_hint(unsigned dst, const void* src, unsigned bytes, unsigned bar,
+                                               uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;\n"
+        ::"r"(dst), "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(bar), "l"(pol) : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol));
+    return pol;
 }
 __device__ __forceinline__ void cluster_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
@@ -241,11 +273,41 @@ struct Walk {
 
 // PAIR: the clustered two-chunk variant (a separate instantiation, so the single
 // chunk kernel carries none of its branches -- they cost ~4 us per pass when shared)
-template <bool PAIR, int NSL>
+// One k-step (32 bytes of K) of the S = 56 schedule for A slice SP (NSL = 7): 34 products
+// in 14 MMAs.  Z slice q sits at B rows 56 q, its products with A slice SP accumulate on
+// TMEM diagonal SP + q at column 56 (SP + q).  Runs of 4 / 2 slices are N = 224 / 112
+// MMAs; a lone product is an N = 64 MMA whose last 8 columns read the next slice (or the
+// 8 zero rows after slice 6) into the next diagonal -- placed so that spill is either
+// zero or lands on diagonal 8 (columns 448..511, never read).  `init` (first k-step of an
+// accumulation) starts a diagonal at its first writer: (0, 0..6) for diagonals 0..6,
+// (1, 6) for diagonal 7 (issued after (0, 6), whose spill into diagonal 7 is zero).
+template <int SP>
+__device__ __forceinline__ void issue_s56(unsigned tmem, unsigned da_lo, unsigned db_lo, unsigned d_hi,
+                                          unsigned idesc, bool init) {
+    constexpr unsigned kstep = 32 >> 4;
+    auto mma = [&](int q0, int n, bool first_writer) {
+        const unsigned id = idesc | (unsigned(n >> 3) << 17);
+        const unsigned dt = tmem + unsigned((SP + q0) * 56);
+        const unsigned bl = db_lo + unsigned((q0 * 56 * OZ_BK) >> 4);
+        umma_i8(dt, da_lo, bl, d_hi, id, (first_writer && init) ? 0u : 1u);
+        umma_i8(dt, da_lo + kstep, bl + kstep, d_hi, id, 1u);
+    };
+    if constexpr (SP == 0) { mma(0, 224, true); mma(4, 112, true); mma(6, 64, true); }
+    else if constexpr (SP == 1) { mma(0, 224, false); mma(4, 112, false); mma(6, 64, true); }
+    else if constexpr (SP == 2) { mma(0, 224, false); mma(4, 112, false); }
+    else if constexpr (SP == 3) { mma(0, 224, false); mma(4, 64, false); }
+    else if constexpr (SP == 4) { mma(0, 224, false); }
+    else if constexpr (SP == 5) { mma(0, 112, false); mma(2, 64, false); }
+    else { mma(0, 112, false); }
+}
+
+template <bool PAIR, int NSL, int BS, int S>
 __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
-    constexpr int A_STAGES = Sl<NSL>::A_STAGES;
-    constexpr int B_STAGE = Sl<NSL>::B_STAGE;
-    constexpr int ND = Sl<NSL>::ND, CHUNK_KB = Sl<NSL>::CHUNK_KB;
+    static_assert(S == 64 || (S == 56 && NSL == 7), "the 56-row spacing is scheduled for 7 slices");
+    constexpr int A_STAGES = Sl<NSL, BS, S>::A_STAGES;
+    constexpr int B_STAGES = Sl<NSL, BS, S>::B_STAGES;
+    constexpr int B_STAGE = Sl<NSL, BS, S>::B_STAGE;
+    constexpr int ND = Sl<NSL, BS, S>::ND, CHUNK_KB = Sl<NSL, BS, S>::CHUNK_KB;
     FQB_PDL_ENTRY();
     extern __shared__ uint8_t smem_raw[];
     __shared__ uint64_t bars[2 * A_STAGES + 2 * B_STAGES + 2];
@@ -282,7 +344,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
     if (threadIdx.x < OZ_BN) ez_s[threadIdx.x] = int(threadIdx.x) < q_N ? q_ez[threadIdx.x] : 0;
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
-            smem_u32(&tmem_base_s)), "n"(Sl<NSL>::TMEM_COLS));
+            smem_u32(&tmem_base_s)), "n"(Sl<NSL, BS, S>::TMEM_COLS));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n");
@@ -293,11 +355,12 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
 
     const int c = PAIR ? int(blockIdx.x >> 1) : int(blockIdx.x);
     const Walk wk(range_begin(p, c), range_begin(p, c + 1), p.kblocks, p.inv_kblocks);
-    const int bn = p.bn;
 
     if (warp == 0) {
         if (lane == 0) {
-            const unsigned zbytes = unsigned(NSL * bn * OZ_BK);
+            const unsigned zbytes = unsigned(z_block_rows(NSL, S) * OZ_BK);
+            const bool hint = p.l2hint != 0;
+            const uint64_t pol_a = policy_evict_first(), pol_z = policy_evict_last();
             int64_t ja = 0, jb = 0;
             for (int64_t si = 0; si < wk.nseg; ++si) {
                 const int64_t t = wk.tile(si);
@@ -306,16 +369,30 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
                     const int sb = int(jb % B_STAGES);
                     mbar_wait(b_empty + 8 * sb, unsigned((jb / B_STAGES) & 1) ^ 1u);
                     mbar_expect_tx(b_full + 8 * sb, zbytes);
-                    bulk_load(b_base + sb * B_STAGE, q_zs + int64_t(kb) * zbytes, zbytes, b_full + 8 * sb);
+                    if (hint)
+                        bulk_load_hint(b_base + sb * B_STAGE, q_zs + int64_t(kb) * zbytes, zbytes, b_full + 8 * sb,
+                                       pol_z);
+                    else
+                        bulk_load(b_base + sb * B_STAGE, q_zs + int64_t(kb) * zbytes, zbytes, b_full + 8 * sb);
                     const int8_t* xt = p.xs + (mt * p.kblocks + kb) * int64_t(NSL * A_TILE);
                     for (int sp = 0; sp < NSL; ++sp, ++ja) {
                         const int sa = int(ja % A_STAGES);
                         mbar_wait(a_empty + 8 * sa, unsigned((ja / A_STAGES) & 1) ^ 1u);
                         mbar_expect_tx(a_full + 8 * sa, unsigned(A_TILE));
-                        if constexpr (!PAIR)
-                            bulk_load(a_base + sa * A_TILE, xt + sp * A_TILE, unsigned(A_TILE), a_full + 8 * sa);
-                        else if ((sp & 1) == rank)   // the pair splits the slices, each lands in both
-                            bulk_load_mc2(a_base + sa * A_TILE, xt + sp * A_TILE, unsigned(A_TILE), a_full + 8 * sa);
+                        if constexpr (!PAIR) {
+                            if (hint)
+                                bulk_load_hint(a_base + sa * A_TILE, xt + sp * A_TILE, unsigned(A_TILE),
+                                               a_full + 8 * sa, pol_a);
+                            else
+                                bulk_load(a_base + sa * A_TILE, xt + sp * A_TILE, unsigned(A_TILE), a_full + 8 * sa);
+                        } else if ((sp & 1) == rank) {   // the pair splits the slices, each lands in both
+                            if (hint)
+                                bulk_load_mc2_hint(a_base + sa * A_TILE, xt + sp * A_TILE, unsigned(A_TILE),
+                                                   a_full + 8 * sa, pol_a);
+                            else
+                                bulk_load_mc2(a_base + sa * A_TILE, xt + sp * A_TILE, unsigned(A_TILE),
+                                              a_full + 8 * sa);
+                        }
                     }
                 }
             }
@@ -351,6 +428,20 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
                             // diagonals sp+sq: one N = 64 * slices MMA covers them (A read once).
                             // Diagonals d < NSL start (accumulate = 0) with sp = 0; with ND > NSL
                             // the top diagonal ND-1 starts with (ND-NSL, NSL-1), issued alone.
+                            if constexpr (S == 56) {
+                                const bool init = kb == cb;
+                                if (sp == 0) issue_s56<0>(tmem, da_lo, db_lo, d_hi, idesc, init);
+                                else if (sp == 1) issue_s56<1>(tmem, da_lo, db_lo, d_hi, idesc, init);
+                                else if (sp == 2) issue_s56<2>(tmem, da_lo, db_lo, d_hi, idesc, init);
+                                else if (sp == 3) issue_s56<3>(tmem, da_lo, db_lo, d_hi, idesc, init);
+                                else if (sp == 4) issue_s56<4>(tmem, da_lo, db_lo, d_hi, idesc, init);
+                                else if (sp == 5) issue_s56<5>(tmem, da_lo, db_lo, d_hi, idesc, init);
+                                else issue_s56<6>(tmem, da_lo, db_lo, d_hi, idesc, init);
+                                if constexpr (PAIR) umma_commit_mc2(a_empty + 8 * sa);
+                                else umma_commit(a_empty + 8 * sa);
+                                if (++sa == A_STAGES) sa = 0, pa ^= 1u;
+                                continue;
+                            }
                             constexpr unsigned kstep = 32 >> 4;   // 32 bytes of K per MMA
                             const int nq_all = min(NSL, ND - sp);
                             const bool split_top = ND > NSL && sp == ND - NSL;
@@ -412,11 +503,11 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
                 ph ^= 1u;
                 asm volatile("tcgen05.fence::after_thread_sync;\n");
 #pragma unroll 1
-                for (int g = 0; g < OZ_BN; g += 16) {
+                for (int g = 0; g < S; g += 16) {   // S = 56: the last group reads 8 spare columns
                     // all diagonals in flight, one wait
                     unsigned v[ND][16];
 #pragma unroll
-                    for (int d = 0; d < ND; ++d) tmem_ld16(lane_addr + unsigned(d * OZ_BN + g), v[d]);
+                    for (int d = 0; d < ND; ++d) tmem_ld16(lane_addr + unsigned(d * S + g), v[d]);
                     asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
                     double acc[16];
 #pragma unroll
@@ -424,7 +515,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
                     // least significant diagonal first: d = ND-1 .. 0 (scale 2^(-12-W d))
 #pragma unroll
                     for (int d = ND - 1; d >= 0; --d) {
-                        const double sc = pow2i(-12 - Sl<NSL>::W * d);
+                        const double sc = pow2i(-12 - Sl<NSL, BS, S>::W * d);
 #pragma unroll
                         for (int j = 0; j < 16; ++j) acc[j] = fma(double(int(v[d][j])), sc, acc[j]);
                     }
@@ -468,7 +559,8 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
     __syncthreads();
     if constexpr (PAIR) cluster_sync();   // no CTA leaves while its peer may still arrive on its barriers
     if (warp == 1)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(Sl<NSL>::TMEM_COLS));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
+                     "n"(Sl<NSL, BS, S>::TMEM_COLS));
 }
 
 // ---------------------------------------------------------------------------
@@ -713,12 +805,22 @@ __global__ void __launch_bounds__(256) k_slice_a(const T* __restrict__ a, int64_
 // column max itself (the column is small and L2-resident), so one launch does it;
 // (ZT = 256 measured faster than 512 at C2: 7.7 vs 9.6 us)
 constexpr int ZT = 256;
-template <int NSL>
+template <int NSL, int S>
 __global__ void __launch_bounds__(ZT) k_slice_z(const double* __restrict__ b, int64_t k, int64_t n, int64_t ld,
                                                 int* ez, int8_t* out) {
     FQB_PDL_ENTRY();
     __shared__ unsigned wmax[ZT / 32];
     const int j = blockIdx.x;
+    constexpr int ZR = z_block_rows(NSL, S);
+    if (j >= S) {   // S = 56: the 8 zero rows after the last slice, row NSL S + (j - S)
+        const int64_t kb_count = (k + OZ_BK - 1) / OZ_BK;
+        const int64_t c16 = int64_t(blockIdx.y) * ZT + threadIdx.x;
+        if (c16 >= kb_count * (OZ_BK / 16)) return;
+        const int64_t k0 = c16 * 16;
+        *reinterpret_cast<uint4*>(out + (k0 / OZ_BK) * int64_t(ZR) * OZ_BK + swz(NSL * S + (j - S), int(k0 % OZ_BK))) =
+            make_uint4(0u, 0u, 0u, 0u);
+        return;
+    }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const double* col = b + int64_t(j) * ld;
     const bool live = j < n;
@@ -748,14 +850,14 @@ __global__ void __launch_bounds__(ZT) k_slice_z(const double* __restrict__ b, in
     const int e = exp_of_hi(mx);
     if (live && blockIdx.y == 0 && threadIdx.x == 0) ez[j] = e;
     const int64_t kb_count = (k + OZ_BK - 1) / OZ_BK;
-    const int64_t z_tile = int64_t(OZ_BN) * OZ_BK;
+    const int64_t z_tile = int64_t(S) * OZ_BK;   // one slice of a k-block
     const int64_t c16 = int64_t(blockIdx.y) * ZT + threadIdx.x;
     if (c16 >= kb_count * (OZ_BK / 16)) return;
     const int64_t k0 = c16 * 16;
     double v[16];
 #pragma unroll
     for (int u = 0; u < 16; ++u) v[u] = (live && k0 + u < k) ? col[k0 + u] : 0.0;
-    put_chunk16<NSL>(v, e, out + (k0 / OZ_BK) * NSL * z_tile, z_tile, j, int(k0 % OZ_BK));
+    put_chunk16<NSL>(v, e, out + (k0 / OZ_BK) * int64_t(ZR) * OZ_BK, z_tile, j, int(k0 % OZ_BK));
 }
 
 // Sum the pieces of every split tile in CTA order (deterministic) into C.
@@ -867,36 +969,97 @@ void ozaki_slice_a(const float* a, int64_t m, int64_t n, int64_t ld, unsigned* l
     slice_a_impl(a, m, n, ld, line_max, x_tn, e_tn, x_nn, e_nn, norm_partial, norm_out, nsl, s, lc);
 }
 
-void ozaki_slice_z(const double* b, int64_t k, int64_t n, int64_t ld, int* e, int8_t* out, cudaStream_t s,
-                   LaunchCounter& lc, int nsl) {
+// Z slices with row spacing S (64, or 56 for chunks of <= 56 columns of the 7-slice scheme)
+static void slice_z_s(const double* b, int64_t k, int64_t n, int64_t ld, int* e, int8_t* out, cudaStream_t s,
+                      LaunchCounter& lc, int nsl, int S) {
     if (n <= 0 || k <= 0) return;
     check_nsl(nsl);
     const int64_t chunks = ceil_div(k, OZ_BK) * (OZ_BK / 16);
-    const dim3 g(OZ_BN, unsigned(ceil_div(chunks, ZT)));
-    if (nsl == 8) launch_k(k_slice_z<8>, g, ZT, 0, s, b, k, n, ld, e, out);
-    else if (nsl == 7) launch_k(k_slice_z<7>, g, ZT, 0, s, b, k, n, ld, e, out);
-    else if (nsl == 3) launch_k(k_slice_z<3>, g, ZT, 0, s, b, k, n, ld, e, out);
-    else launch_k(k_slice_z<4>, g, ZT, 0, s, b, k, n, ld, e, out);
+    const dim3 g(unsigned(S == 56 ? S + 8 : S), unsigned(ceil_div(chunks, ZT)));
+    if (nsl == 7 && S == 56) launch_k(k_slice_z<7, 56>, g, ZT, 0, s, b, k, n, ld, e, out);
+    else if (nsl == 8) launch_k(k_slice_z<8, 64>, g, ZT, 0, s, b, k, n, ld, e, out);
+    else if (nsl == 7) launch_k(k_slice_z<7, 64>, g, ZT, 0, s, b, k, n, ld, e, out);
+    else if (nsl == 3) launch_k(k_slice_z<3, 64>, g, ZT, 0, s, b, k, n, ld, e, out);
+    else launch_k(k_slice_z<4, 64>, g, ZT, 0, s, b, k, n, ld, e, out);
     FQB_LAUNCHED();
     lc.bump();
 }
 
+void ozaki_slice_z(const double* b, int64_t k, int64_t n, int64_t ld, int* e, int8_t* out, cudaStream_t s,
+                   LaunchCounter& lc, int nsl) {
+    slice_z_s(b, k, n, ld, e, out, s, lc, nsl, OZ_BN);
+}
+
 // paired (pair_cw > 0): N = 2 chunks of pair_cw columns at most, zs / ez hold both
-template <bool PAIR, int NSL>
-static void configure_ozaki() {
+template <bool PAIR, int NSL, int BS, int S = 64>
+static void launch_variant(const OzArgs& a, cudaStream_t s) {
     static bool configured[64] = {};
     int dev = 0;
     FQB_CUDA(cudaGetDevice(&dev));
     if (dev < 0 || dev >= 64 || !configured[dev]) {
-        FQB_CUDA(cudaFuncSetAttribute(k_ozaki<PAIR, NSL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      int(Sl<NSL>::SMEM)));
+        FQB_CUDA(cudaFuncSetAttribute(k_ozaki<PAIR, NSL, BS, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(Sl<NSL, BS, S>::SMEM)));
         if (dev >= 0 && dev < 64) configured[dev] = true;
     }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(unsigned(PAIR ? 2 * a.grid : a.grid));
+    cfg.blockDim = dim3(OZ_THREADS);
+    cfg.dynamicSmemBytes = Sl<NSL, BS, S>::SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (PAIR) {
+        attr[na].id = cudaLaunchAttributeClusterDimension;
+        attr[na].val.clusterDim.x = 2;
+        attr[na].val.clusterDim.y = 1;
+        attr[na].val.clusterDim.z = 1;
+        ++na;
+    }
+    if (pdl_enabled()) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = na;
+    FQB_CUDA(cudaLaunchKernelEx(&cfg, k_ozaki<PAIR, NSL, BS, S>, a));
+}
+
+// A/B switches of the A-pass kernel (read once): FQB_OZ_L2HINT=0 plain bulk copies,
+// FQB_OZ_BSTAGES=2|3 Z-slice stages of the 7-slice scheme
+static int env_int(const char* name, int dflt) {
+    const char* e = std::getenv(name);
+    return e && *e ? std::atoi(e) : dflt;
+}
+static int l2hint_default() {
+    static const int v = env_int("FQB_OZ_L2HINT", 1) != 0 ? 1 : 0;
+    return v;
+}
+static int zstages_default() {
+    static const int v = env_int("FQB_OZ_BSTAGES", 2) == 3 ? 3 : 2;
+    return v;
+}
+// Z slice spacing of a chunk of cw columns: 56 rows (11 % fewer int8 MACs, 14 MMAs per
+// k-step) for cw <= 56 on the 7-slice scheme; FQB_OZ_S56=0 keeps 64
+static int z_spacing(int64_t cw, int nsl) {
+    static const bool on = env_int("FQB_OZ_S56", 1) != 0;
+    return (on && nsl == 7 && cw <= 56) ? 56 : 64;
+}
+static int64_t z_chunk_bytes(int64_t K, int nsl, int S) { return ceil_div(K, OZ_BK) * z_block_rows(nsl, S) * OZ_BK; }
+
+template <bool PAIR>
+static void launch_pair_or_not(const OzArgs& a, int nsl, int S, cudaStream_t s) {
+    if (nsl == 7 && S == 56) launch_variant<PAIR, 7, 2, 56>(a, s);
+    else if (nsl == 8) launch_variant<PAIR, 8, 2>(a, s);
+    else if (nsl == 7 && zstages_default() == 3) launch_variant<PAIR, 7, 3>(a, s);
+    else if (nsl == 7) launch_variant<PAIR, 7, 2>(a, s);
+    else if (nsl == 3) launch_variant<PAIR, 3, 2>(a, s);
+    else launch_variant<PAIR, 4, 2>(a, s);
 }
 
 static void launch_ozaki(int64_t M, int64_t N, int64_t K, double alpha, const int8_t* xs, const int* ex,
                          const int8_t* zs, const int* ez, double beta, double* C, int64_t ldc, double* work,
-                         int num_sms, int64_t pair_cw, int nsl, cudaStream_t s, LaunchCounter& lc) {
+                         int num_sms, int64_t pair_cw, int nsl, int S, cudaStream_t s, LaunchCounter& lc) {
     check_nsl(nsl);
     const bool pair = pair_cw > 0;
     OzArgs a{};
@@ -912,7 +1075,7 @@ static void launch_ozaki(int64_t M, int64_t N, int64_t K, double alpha, const in
     a.ex = ex;
     a.ez = ez;
     a.work = work;
-    a.bn = OZ_BN;
+    a.bn = S;
     a.mtiles = int(ceil_div(M, OZ_BM));
     a.kblocks = int(ceil_div(K, OZ_BK));
     a.iters = int64_t(a.mtiles) * a.kblocks;
@@ -923,51 +1086,11 @@ static void launch_ozaki(int64_t M, int64_t N, int64_t K, double alpha, const in
     a.inv_iters = 1.0 / double(a.iters);
     a.pair = pair ? 1 : 0;
     a.cw = pair_cw;
-    a.zs_stride = ozaki_z_bytes(OZ_BN, K, nsl);
+    a.zs_stride = z_chunk_bytes(K, nsl, S);
     a.work_stride = 3 * int64_t(a.grid) * OZ_PARTIAL;
-    if (!pair) {
-        if (nsl == 8) {
-            configure_ozaki<false, 8>();
-            launch_k(k_ozaki<false, 8>, a.grid, OZ_THREADS, Sl<8>::SMEM, s, a);
-        } else if (nsl == 7) {
-            configure_ozaki<false, 7>();
-            launch_k(k_ozaki<false, 7>, a.grid, OZ_THREADS, Sl<7>::SMEM, s, a);
-        } else if (nsl == 3) {
-            configure_ozaki<false, 3>();
-            launch_k(k_ozaki<false, 3>, a.grid, OZ_THREADS, Sl<3>::SMEM, s, a);
-        } else {
-            configure_ozaki<false, 4>();
-            launch_k(k_ozaki<false, 4>, a.grid, OZ_THREADS, Sl<4>::SMEM, s, a);
-        }
-    } else {
-        cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3(unsigned(2 * a.grid));
-        cfg.blockDim = dim3(OZ_THREADS);
-        cfg.dynamicSmemBytes = nsl == 8 ? Sl<8>::SMEM : nsl == 7 ? Sl<7>::SMEM : nsl == 3 ? Sl<3>::SMEM : Sl<4>::SMEM;
-        cfg.stream = s;
-        cudaLaunchAttribute attr[2];
-        attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = 2;
-        attr[0].val.clusterDim.y = 1;
-        attr[0].val.clusterDim.z = 1;
-        attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        attr[1].val.programmaticStreamSerializationAllowed = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = pdl_enabled() ? 2 : 1;
-        if (nsl == 8) {
-            configure_ozaki<true, 8>();
-            FQB_CUDA(cudaLaunchKernelEx(&cfg, k_ozaki<true, 8>, a));
-        } else if (nsl == 7) {
-            configure_ozaki<true, 7>();
-            FQB_CUDA(cudaLaunchKernelEx(&cfg, k_ozaki<true, 7>, a));
-        } else if (nsl == 3) {
-            configure_ozaki<true, 3>();
-            FQB_CUDA(cudaLaunchKernelEx(&cfg, k_ozaki<true, 3>, a));
-        } else {
-            configure_ozaki<true, 4>();
-            FQB_CUDA(cudaLaunchKernelEx(&cfg, k_ozaki<true, 4>, a));
-        }
-    }
+    a.l2hint = l2hint_default();
+    if (pair) launch_pair_or_not<true>(a, nsl, S, s);
+    else launch_pair_or_not<false>(a, nsl, S, s);
     FQB_LAUNCHED();
     lc.bump();
     bool split = false;   // does any CTA (pair) boundary fall inside a tile?
@@ -985,7 +1108,7 @@ void ozaki_gemm(int64_t M, int64_t N, int64_t K, double alpha, const int8_t* xs,
                 const int* ez, double beta, double* C, int64_t ldc, double* work, int num_sms, cudaStream_t s,
                 LaunchCounter& lc, int nsl) {
     if (N > OZ_BN) throw Error(kStatusInvalid, "ozaki_gemm: N > 64");
-    launch_ozaki(M, N, K, alpha, xs, ex, zs, ez, beta, C, ldc, work, num_sms, 0, nsl, s, lc);
+    launch_ozaki(M, N, K, alpha, xs, ex, zs, ez, beta, C, ldc, work, num_sms, 0, nsl, OZ_BN, s, lc);
 }
 
 static bool pairs_enabled() {
@@ -1002,21 +1125,22 @@ void ozaki_apply(int64_t M, int64_t N, int64_t K, double alpha, const int8_t* xs
     if (N <= 0) return;
     const int64_t chunks = ceil_div(N, OZ_BN);
     const int64_t cw = ceil_div(N, chunks);
-    const int64_t zstride = ozaki_z_bytes(OZ_BN, K, nsl);
+    const int S = z_spacing(cw, nsl);
+    const int64_t zstride = z_chunk_bytes(K, nsl, S);
     int64_t c0 = 0;
     // two chunks at a time on CTA pairs that share every A tile (multicast): A is
     // streamed once per pair of chunks instead of once per chunk
     while (pairs_enabled() && num_sms >= 2 && N - c0 > cw) {
         const int64_t nb = std::min(2 * cw, N - c0);
-        ozaki_slice_z(b + c0 * ldb, K, cw, ldb, ez, z, s, lc, nsl);
-        ozaki_slice_z(b + (c0 + cw) * ldb, K, nb - cw, ldb, ez + OZ_BN, z + zstride, s, lc, nsl);
-        launch_ozaki(M, nb, K, alpha, xs, ex, z, ez, beta, C + c0 * ldc, ldc, work, num_sms, cw, nsl, s, lc);
+        slice_z_s(b + c0 * ldb, K, cw, ldb, ez, z, s, lc, nsl, S);
+        slice_z_s(b + (c0 + cw) * ldb, K, nb - cw, ldb, ez + OZ_BN, z + zstride, s, lc, nsl, S);
+        launch_ozaki(M, nb, K, alpha, xs, ex, z, ez, beta, C + c0 * ldc, ldc, work, num_sms, cw, nsl, S, s, lc);
         c0 += nb;
     }
     for (; c0 < N; c0 += cw) {
         const int64_t nb = std::min(cw, N - c0);
-        ozaki_slice_z(b + c0 * ldb, K, nb, ldb, ez, z, s, lc, nsl);
-        ozaki_gemm(M, nb, K, alpha, xs, ex, z, ez, beta, C + c0 * ldc, ldc, work, num_sms, s, lc, nsl);
+        slice_z_s(b + c0 * ldb, K, nb, ldb, ez, z, s, lc, nsl, S);
+        launch_ozaki(M, nb, K, alpha, xs, ex, z, ez, beta, C + c0 * ldc, ldc, work, num_sms, 0, nsl, S, s, lc);
     }
 }
 // the products of ozaki_apply again, on the B slices its last call left in z / ez
@@ -1030,7 +1154,8 @@ void ozaki_apply_presliced(int64_t M, int64_t N, int64_t K, double alpha, const 
     const int64_t cw = ceil_div(N, chunks);
     if (chunks == 2 && !(pairs_enabled() && num_sms >= 2))
         throw Error(kStatusInvalid, "ozaki_apply_presliced: two chunks need the paired launch");
-    launch_ozaki(M, N, K, alpha, xs, ex, z, ez, beta, C, ldc, work, num_sms, chunks == 2 ? cw : 0, nsl, s, lc);
+    launch_ozaki(M, N, K, alpha, xs, ex, z, ez, beta, C, ldc, work, num_sms, chunks == 2 ? cw : 0, nsl,
+                 z_spacing(cw, nsl), s, lc);
 }
 int64_t ozaki_apply_z_bytes(int64_t K, int nsl) { return 2 * ozaki_z_bytes(OZ_BN, K, nsl); }
 int ozaki_apply_ez_count() { return 2 * OZ_BN; }
