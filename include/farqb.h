@@ -218,6 +218,14 @@ size_t fqb_host_pool_trim(void);
 fqb_status fqb_comm_unique_id(void* out128);
 fqb_status fqb_comm_attach(fqb_handle h, const void* id128, int nranks, int rank);
 fqb_status fqb_comm_detach(fqb_handle h);
+/* The same row sharding over a host transport: at every reduction point the engine
+ * copies the partial sums to pinned host memory and calls fn(user, buf, count), which
+ * must sum `count` doubles in place across all ranks (MPI_Allreduce, a gloo all-reduce)
+ * and return 0; nonzero fails the run with FQB_ERR_NCCL.  Called on the thread that
+ * runs fqb_qb_*.  Slower than NCCL (a device sync per reduction), for hosts that bring
+ * their own transport and for multi-rank tests sharing one GPU. */
+typedef int (*fqb_host_allreduce_fn)(void* user, double* buf, int64_t count);
+fqb_status fqb_comm_attach_host(fqb_handle h, fqb_host_allreduce_fn fn, void* user, int nranks, int rank);
 /* collectives issued by this handle since creation */
 int64_t fqb_collective_count(fqb_handle h);
 

@@ -50,6 +50,7 @@ class SketchHostC(C.Structure):
 
 
 SOURCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_int, C.POINTER(BlockC))
+HOST_ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_int64)
 
 OUT_NONE, OUT_HOST, OUT_DEVICE, OUT_SVD = 0, 1, 2, 4
 
@@ -80,6 +81,7 @@ SIGNATURES = [
     ("fqb_result_free", None, [C.POINTER(ResultC)]),
     ("fqb_comm_unique_id", C.c_int, [C.c_void_p]),
     ("fqb_comm_attach", C.c_int, [_H, C.c_void_p, C.c_int, C.c_int]),
+    ("fqb_comm_attach_host", C.c_int, [_H, HOST_ALLREDUCE_FN, C.c_void_p, C.c_int, C.c_int]),
     ("fqb_comm_detach", C.c_int, [_H]),
     ("fqb_collective_count", C.c_int64, [_H]),
     ("fqb_philox_u32", C.c_int, [_H, C.c_uint64, C.c_uint32, C.c_uint32, C.c_int, C.c_void_p]),

@@ -174,6 +174,14 @@ fqb_status fqb_comm_attach(fqb_handle h, const void* id128, int nranks, int rank
     });
 }
 
+fqb_status fqb_comm_attach_host(fqb_handle h, fqb_host_allreduce_fn fn, void* user, int nranks, int rank) {
+    return guarded([&]() -> fqb_status {
+        bind(h);
+        farqb::comm_attach_host(h->h, fn, user, nranks, rank);
+        return FQB_OK;
+    });
+}
+
 fqb_status fqb_comm_detach(fqb_handle h) {
     return guarded([&]() -> fqb_status {
         bind(h);

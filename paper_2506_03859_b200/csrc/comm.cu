@@ -10,6 +10,12 @@
 //
 // libnccl.so.2 is dlopen()ed on first use (torch's bundled copy when it is
 // already loaded, else the system one): single-GPU users need no NCCL.
+//
+// The host backend (fqb_comm_attach_host) runs the same reduction points through a
+// caller's all-reduce on pinned host copies (D2H, callback, H2D on the handle's
+// stream).  It is what a host application with its own transport (MPI, gloo) binds,
+// and it lets several ranks share one GPU in a test without any kernel waiting on
+// another rank's kernel: every exchange is a host round trip.
 #include <dlfcn.h>
 #include <nccl.h>
 
@@ -85,13 +91,50 @@ void comm_detach(Handle& h) {
         cudaStreamSynchronize(h.stream);
         nccl().comm_destroy(static_cast<ncclComm_t>(h.comm));
     }
+    if (h.host_ar_buf) {
+        cudaStreamSynchronize(h.stream);
+        cudaFreeHost(h.host_ar_buf);
+    }
     h.comm = nullptr;
+    h.host_ar = nullptr;
+    h.host_ar_user = nullptr;
+    h.host_ar_buf = nullptr;
+    h.host_ar_cap = 0;
     h.nranks = 1;
     h.rank = 0;
 }
 
+void comm_attach_host(Handle& h, fqb_host_allreduce_fn fn, void* user, int nranks, int rank) {
+    if (!fn) throw Error(kStatusInvalid, "null all-reduce callback");
+    if (nranks < 1 || rank < 0 || rank >= nranks) throw Error(kStatusInvalid, "bad rank / nranks");
+    comm_detach(h);
+    h.host_ar = fn;
+    h.host_ar_user = user;
+    h.nranks = nranks;
+    h.rank = rank;
+}
+
 void comm_allreduce_sum(Handle& h, double* buf, size_t count, cudaStream_t s) {
-    if (!h.comm || count == 0) return;
+    if (count == 0) return;
+    if (h.host_ar) {
+        if (count > h.host_ar_cap) {
+            if (h.host_ar_buf) {
+                FQB_CUDA(cudaStreamSynchronize(s));
+                FQB_CUDA(cudaFreeHost(h.host_ar_buf));
+                h.host_ar_buf = nullptr;
+            }
+            FQB_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h.host_ar_buf), count * sizeof(double)));
+            h.host_ar_cap = count;
+        }
+        FQB_CUDA(cudaMemcpyAsync(h.host_ar_buf, buf, count * sizeof(double), cudaMemcpyDeviceToHost, s));
+        FQB_CUDA(cudaStreamSynchronize(s));
+        if (h.host_ar(h.host_ar_user, h.host_ar_buf, int64_t(count)) != 0)
+            throw Error(kStatusNccl, "host all-reduce callback failed");
+        FQB_CUDA(cudaMemcpyAsync(buf, h.host_ar_buf, count * sizeof(double), cudaMemcpyHostToDevice, s));
+        ++h.collectives;
+        return;
+    }
+    if (!h.comm) return;
     nccl_check(nccl().all_reduce(buf, buf, count, ncclFloat64, ncclSum, static_cast<ncclComm_t>(h.comm), s),
                "ncclAllReduce");
     ++h.collectives;

@@ -636,11 +636,11 @@ int run_qb(Handle& h, const void* a, bool a_f32, int64_t m, int64_t n, int64_t l
     std::memset(out, 0, sizeof *out);
     out->m = m;
     out->n = n;
-    if (!a && !(h.comm && m == 0)) throw Error(kStatusInvalid, "null matrix pointer");
+    if (!a && !(sharded(h) && m == 0)) throw Error(kStatusInvalid, "null matrix pointer");
     if (lda < m) throw Error(kStatusDimension, "lda < m");
     // with a communicator, (a, m, lda) is this rank's row block of A
     int64_t m_global = m;
-    if (h.comm) {
+    if (sharded(h)) {
         h.ws.scalars.ensure(8, h.stream);
         const double local = double(m);
         FQB_CUDA(cudaMemcpyAsync(h.ws.scalars.ptr, &local, sizeof(double), cudaMemcpyHostToDevice, h.stream));

@@ -87,6 +87,12 @@ struct Handle {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     // row-sharded multi-GPU (comm.cu); nullptr = single GPU
     void* comm = nullptr;
+    // ... or the host reduction backend (fqb_comm_attach_host): sums staged through
+    // pinned host memory and handed to a caller-supplied all-reduce
+    fqb_host_allreduce_fn host_ar = nullptr;
+    void* host_ar_user = nullptr;
+    double* host_ar_buf = nullptr;
+    size_t host_ar_cap = 0;
     int nranks = 1, rank = 0;
     int64_t collectives = 0;
     void* cusolver = nullptr;  // svd.cu
@@ -136,6 +142,8 @@ void comm_unique_id(void* out128);
 void comm_attach(Handle& h, const void* id128, int nranks, int rank);
 void comm_detach(Handle& h);
 void comm_allreduce_sum(Handle& h, double* buf, size_t count, cudaStream_t s);
+void comm_attach_host(Handle& h, fqb_host_allreduce_fn fn, void* user, int nranks, int rank);
+inline bool sharded(const Handle& h) { return h.comm != nullptr || h.host_ar != nullptr; }
 
 struct ResolvedConfig {
     fqb_config cfg;

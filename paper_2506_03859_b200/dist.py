@@ -49,3 +49,31 @@ def attach(engine, group=None) -> None:
     st = _native.lib().fqb_comm_attach(engine._h, buf, dist.get_world_size(group), dist.get_rank(group))
     if st:
         _raise(st, "fqb_comm_attach")
+
+
+def attach_host(engine, group=None) -> None:
+    """Attach the host reduction backend (fqb_comm_attach_host): every reduction point of
+    the engine becomes a torch.distributed all-reduce of a CPU tensor (gloo), so the row-
+    sharded loop runs with any process group -- several ranks may even share one GPU, as
+    no kernel waits on another rank.  Collective call."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from . import _native
+    from .rsvd import _raise
+
+    def cb(_user, buf, count):
+        try:
+            t = torch.from_numpy(np.ctypeslib.as_array(buf, (int(count),)))
+            dist.all_reduce(t, group=group)
+            # every rank must take the same decisions from the same bits: rank 0's sum wins
+            dist.broadcast(t, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+            return 0
+        except Exception:  # noqa: BLE001 - reported through the status
+            return 1
+
+    fn = _native.HOST_ALLREDUCE_FN(cb)
+    engine._host_ar_fn = fn          # kept alive as long as the engine uses it
+    st = _native.lib().fqb_comm_attach_host(engine._h, fn, None, dist.get_world_size(group), dist.get_rank(group))
+    if st:
+        _raise(st, "fqb_comm_attach_host")

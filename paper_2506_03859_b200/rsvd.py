@@ -396,11 +396,16 @@ class Engine:
     def collective_count(self) -> int:
         return self._lib.fqb_collective_count(self._h)
 
-    def attach_comm(self, group=None) -> None:
+    def attach_comm(self, group=None, backend: str = "nccl") -> None:
         """Row-sharded mode: subsequent runs take this rank's row block of A
-        (see paper_2506_03859_b200.dist.partition_rows)."""
+        (see paper_2506_03859_b200.dist.partition_rows).  backend "nccl": the engine's
+        own NCCL communicator over NVLink; "host": the reduction points go through
+        torch.distributed on the host (any process group, e.g. gloo)."""
         from . import dist
-        dist.attach(self, group)
+        if backend == "host":
+            dist.attach_host(self, group)
+        else:
+            dist.attach(self, group)
 
     def detach_comm(self) -> None:
         st = self._lib.fqb_comm_detach(self._h)
