@@ -65,7 +65,35 @@ def build(verbose: bool = False) -> str:
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+    build_dropin(verbose)
     return LIB
+
+
+REF_INCLUDE = os.environ.get("FARQB_REF_INCLUDE", "/root/reference/proj/include")
+DROPIN_SRC = os.path.join(PKG, "dropin", "rsvd_link.cpp")
+DROPIN_LIB = os.path.join(LIB_DIR, "librsvd_b200.so")
+
+
+def build_dropin(verbose: bool = False) -> str | None:
+    """lib/librsvd_b200.so: rsvd::run_fixed_precision / run_fixed_rank with the reference's
+    exact C++ signatures on the engine (dropin/rsvd_link.cpp).  Needs the reference's
+    public headers at build time (FARQB_REF_INCLUDE); skipped without them (the built .so
+    travels with the tree)."""
+    if not os.path.isdir(os.path.join(REF_INCLUDE, "rsvd")):
+        return None
+    if os.path.exists(DROPIN_LIB) and os.path.getmtime(DROPIN_LIB) >= max(
+            os.path.getmtime(DROPIN_SRC), os.path.getmtime(LIB), os.path.getmtime(os.path.join(ROOT, "include", "farqb.h"))):
+        return DROPIN_LIB
+    cxx = shutil.which("g++") or "g++"
+    cmd = [cxx, "-std=c++20", "-O2", "-fPIC", "-shared", "-Wall", "-Wextra", "-I" + REF_INCLUDE,
+           "-I" + os.path.join(ROOT, "include"), DROPIN_SRC, "-L" + LIB_DIR, "-lfarqb", "-Wl,-rpath,$ORIGIN",
+           "-o", DROPIN_LIB]
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"drop-in build failed:\n{r.stdout}\n{r.stderr}")
+    return DROPIN_LIB
 
 
 if __name__ == "__main__":
