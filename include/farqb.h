@@ -64,7 +64,8 @@ typedef enum fqb_status {
     FQB_ERR_INVALID_ARGUMENT = 7,       /* null pointer, bad handle, bad enum    */
     FQB_ERR_CONVERGENCE = 8,            /* rsvd::ConvergenceFailure              */
     FQB_ERR_CALLBACK = 9,               /* block source returned non-zero        */
-    FQB_ERR_ALLOC = 10                  /* device or host allocation failed      */
+    FQB_ERR_ALLOC = 10,                 /* device or host allocation failed      */
+    FQB_ERR_FORMAT = 11                 /* rsvd::FormatError (matrix file); byte offset returned */
 } fqb_status;
 
 /* rsvd::SketchKind, same numbering (sketch.hpp:11). */
@@ -226,6 +227,18 @@ fqb_status fqb_comm_detach(fqb_handle h);
  * their own transport and for multi-rank tests sharing one GPU. */
 typedef int (*fqb_host_allreduce_fn)(void* user, double* buf, int64_t count);
 fqb_status fqb_comm_attach_host(fqb_handle h, fqb_host_allreduce_fn fn, void* user, int nranks, int rank);
+/* ---- RawF64 matrix files (matrix_io.cpp:141-200, rsvd::load_matrix RawF64) ---- */
+/* Validates a "SKLR" file exactly like the reference's loader: on a malformed file
+ * FQB_ERR_FORMAT, the reference's FormatError message in fqb_last_error() and its byte
+ * offset in *err_offset (may be NULL). */
+fqb_status fqb_raw_header(const char* path, int64_t* rows, int64_t* cols, int64_t* err_offset);
+/* Rows [row0, row0 + rows) of every column (a rank's row shard; all rows: row0 = 0,
+ * rows = m) into dst (rows x cols, ld >= rows), device memory when dst_on_device (pinned
+ * staging panels, reads overlapped with the uploads on the handle's stream; returns when
+ * the data has landed), else host memory (h may then be NULL).  Multi-threaded pread. */
+fqb_status fqb_load_raw_rows(fqb_handle h, const char* path, int64_t row0, int64_t rows, double* dst, int64_t ld,
+                             int dst_on_device, int64_t* err_offset);
+
 /* collectives issued by this handle since creation */
 int64_t fqb_collective_count(fqb_handle h);
 

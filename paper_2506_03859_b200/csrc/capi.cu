@@ -75,6 +75,7 @@ const char* fqb_status_name(int status) {
         case FQB_ERR_CONVERGENCE: return "convergence";
         case FQB_ERR_CALLBACK: return "callback";
         case FQB_ERR_ALLOC: return "alloc";
+        case FQB_ERR_FORMAT: return "format";
         default: return "unknown";
     }
 }
@@ -647,6 +648,40 @@ fqb_status fqb_checksum(fqb_handle h, const double* a, int64_t rows, int64_t col
         *out = farqb::checksum_dev(h->h, a, rows, cols, lda, row0, m_total);
         return FQB_OK;
     });
+}
+
+fqb_status fqb_raw_header(const char* path, int64_t* rows, int64_t* cols, int64_t* err_offset) {
+    if (err_offset) *err_offset = -1;
+    try {
+        if (!path || !rows || !cols) throw farqb::Error(FQB_ERR_INVALID_ARGUMENT, "null argument");
+        farqb::raw_header(path, rows, cols);
+        return FQB_OK;
+    } catch (const farqb::FormatFailure& e) {
+        if (err_offset) *err_offset = e.offset;
+        return set_error(e.status, e.what());
+    } catch (const farqb::Error& e) {
+        return set_error(e.status, e.what());
+    } catch (const std::exception& e) {
+        return set_error(FQB_ERR_INVALID_ARGUMENT, e.what());
+    }
+}
+
+fqb_status fqb_load_raw_rows(fqb_handle h, const char* path, int64_t row0, int64_t rows, double* dst, int64_t ld,
+                             int dst_on_device, int64_t* err_offset) {
+    if (err_offset) *err_offset = -1;
+    try {
+        if (!path || (!dst && rows > 0)) throw farqb::Error(FQB_ERR_INVALID_ARGUMENT, "null argument");
+        if (dst_on_device) bind(h);
+        farqb::load_raw_rows(h ? &h->h : nullptr, path, row0, rows, dst, ld, dst_on_device != 0);
+        return FQB_OK;
+    } catch (const farqb::FormatFailure& e) {
+        if (err_offset) *err_offset = e.offset;
+        return set_error(e.status, e.what());
+    } catch (const farqb::Error& e) {
+        return set_error(e.status, e.what());
+    } catch (const std::exception& e) {
+        return set_error(FQB_ERR_INVALID_ARGUMENT, e.what());
+    }
 }
 
 double fqb_default_density(int kind, int64_t n) { return farqb::default_density(kind, n); }

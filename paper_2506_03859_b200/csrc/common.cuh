@@ -26,6 +26,7 @@ constexpr int kStatusInvalid = 7;
 constexpr int kStatusConvergence = 8;
 constexpr int kStatusCallback = 9;
 constexpr int kStatusAlloc = 10;
+constexpr int kStatusFormat = 11;
 
 inline void cuda_check(cudaError_t e, const char* what) {
     if (e != cudaSuccess)

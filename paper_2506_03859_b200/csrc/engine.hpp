@@ -137,6 +137,15 @@ double relative_error(Handle& h, const double* a, int64_t m, int64_t n, int64_t 
                       const double* u, int64_t ldu, const double* sigma, const double* v, int64_t ldv, int r,
                       bool factors_on_device);
 
+// rawio.cu: RawF64 files (matrix_io.cpp:141-200); FormatFailure carries the byte offset
+struct FormatFailure : Error {
+    int64_t offset;
+    FormatFailure(const std::string& m, int64_t off) : Error(kStatusFormat, m), offset(off) {}
+};
+void raw_header(const char* path, int64_t* rows, int64_t* cols);
+void load_raw_rows(Handle* h, const char* path, int64_t row0, int64_t rows, double* dst, int64_t ld,
+                   bool dst_on_device);
+
 // comm.cu
 void comm_unique_id(void* out128);
 void comm_attach(Handle& h, const void* id128, int nranks, int rank);

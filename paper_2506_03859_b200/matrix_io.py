@@ -341,3 +341,50 @@ def load_raw(path: str | os.PathLike) -> np.ndarray:
 
 def save_raw(path: str | os.PathLike, a) -> None:
     save_matrix(a, path, RAW)
+
+
+# ---- native RawF64 reads (csrc/rawio.cu): row shards, straight to the device ----------
+def _native_check(st: int, off, what: str) -> None:
+    if st == 0:
+        return
+    from . import _native
+    msg = _native.lib().fqb_last_error().decode(errors="replace")
+    if st == 11:   # FQB_ERR_FORMAT: the reference's FormatError and byte offset
+        raise FormatError(msg, int(off.value))
+    from .rsvd import _raise
+    _raise(st, f"{what}: {msg}")
+
+
+def raw_header(path: str | os.PathLike) -> tuple[int, int]:
+    """(rows, cols) of a RawF64 file, validated like the reference's loader (FormatError)."""
+    import ctypes as C
+    from . import _native
+    r, c, off = C.c_int64(), C.c_int64(), C.c_int64()
+    st = _native.lib().fqb_raw_header(os.fsencode(path), C.byref(r), C.byref(c), C.byref(off))
+    _native_check(st, off, "fqb_raw_header")
+    return r.value, c.value
+
+
+def load_raw_rows(path: str | os.PathLike, row0: int = 0, rows: int | None = None, engine=None):
+    """Rows [row0, row0 + rows) of a RawF64 file (a rank's row shard; default all rows).
+
+    engine=None: a host float64 array (Fortran order), read by parallel preads.
+    engine=Engine: a column-major torch tensor on that engine's device, uploaded through
+    pinned staging panels overlapped with the reads (fqb_load_raw_rows)."""
+    import ctypes as C
+    from . import _native
+    m, n = raw_header(path)
+    rows = m - row0 if rows is None else rows
+    off = C.c_int64()
+    if engine is None:
+        out = np.empty((n, rows), dtype=np.float64).T    # column-major rows x n
+        st = _native.lib().fqb_load_raw_rows(None, os.fsencode(path), row0, rows, out.ctypes.data, max(rows, 1), 0,
+                                             C.byref(off))
+        _native_check(st, off, "fqb_load_raw_rows")
+        return out
+    import torch
+    out = torch.empty((n, rows), dtype=torch.float64, device=f"cuda:{engine.device}").t()
+    st = _native.lib().fqb_load_raw_rows(engine._h, os.fsencode(path), row0, rows, out.data_ptr(), max(rows, 1), 1,
+                                         C.byref(off))
+    _native_check(st, off, "fqb_load_raw_rows")
+    return out

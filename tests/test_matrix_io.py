@@ -158,3 +158,48 @@ def test_raw_payload_size_overflow_matches_reference(reference, tmp_path):
     with pytest.raises(fqb.FormatError) as e:
         fqb.loads_raw(buf)
     assert (1, e.value.msg, e.value.offset) == ref_err
+
+
+# ---- the native RawF64 reader (csrc/rawio.cu, fqb_raw_header / fqb_load_raw_rows) ----------
+from paper_2506_03859_b200 import matrix_io as mio  # noqa: E402
+
+
+@pytest.mark.parametrize("m,n", [(1, 1), (7, 3), (1000, 37), (4097, 5)])
+def test_native_raw_rows_equal_the_file(tmp_path, m, n):
+    a = np.asfortranarray(np.random.default_rng(m * n).standard_normal((m, n)))
+    p = tmp_path / "a.raw"
+    fqb.save_raw(p, a)
+    assert mio.raw_header(p) == (m, n)
+    assert np.array_equal(mio.load_raw_rows(p), a)
+    for r0, r1 in ((0, m), (m // 3, m // 3 + (m + 1) // 2), (m - 1, m)):
+        got = mio.load_raw_rows(p, r0, r1 - r0)
+        assert got.flags.f_contiguous and np.array_equal(got, a[r0:r1])
+    # row shards of a partition reassemble the matrix
+    from paper_2506_03859_b200.dist import partition_rows
+    parts = [mio.load_raw_rows(p, *(lambda r: (r[0], r[1] - r[0]))(partition_rows(m, 3, k))) for k in range(3)]
+    assert np.array_equal(np.vstack(parts), a)
+
+
+@pytest.mark.parametrize("mutate", [
+    lambda r: r[:10], lambda r: b"SKLX" + r[4:], lambda r: r[:-8], lambda r: r + b"\0",
+    lambda r: r[:4] + struct.pack("<I", 2**31) + r[8:], lambda r: r[:8] + struct.pack("<I", 2**31) + r[12:],
+    lambda r: b"SKLR" + struct.pack("<III", 2**31 - 1, 2**31 - 1, 0), lambda r: b"",
+])
+def test_native_raw_errors_match_the_reference(reference, tmp_path, mutate):
+    """Same FormatError message and byte offset as the reference's load_matrix (oracle/_ref)."""
+    p = tmp_path / "bad.raw"
+    p.write_bytes(mutate(fqb.dumps_raw(np.ones((2, 3)))))
+    _, ref_err = reference.load_matrix(p, "raw")
+    assert ref_err is not None
+    with pytest.raises(fqb.FormatError) as e:
+        mio.raw_header(p)
+    assert (1, e.value.msg, e.value.offset) == ref_err
+    with pytest.raises(fqb.FormatError):
+        mio.load_raw_rows(p)
+
+
+def test_native_raw_bad_row_range(tmp_path):
+    p = tmp_path / "a.raw"
+    fqb.save_raw(p, np.ones((5, 2)))
+    with pytest.raises(fqb.RsvdError):
+        mio.load_raw_rows(p, 3, 4)
