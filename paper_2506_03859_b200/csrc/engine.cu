@@ -568,7 +568,9 @@ class QbRun {
         for (int pass = 0; pass < 2; ++pass) {
             pending_rowsum_ = false;
             FQB_CUDA(cudaMemsetAsync(status_, 0, sizeof(unsigned), s_));
-            make_block(id);
+            // the eigSVD retry reuses the block already on the device: the reference asks
+            // its source once per attempt (driver.cpp:141-143)
+            if (pass == 0) make_block(id);
             if (cfg_.power >= 1) power_iterate(eig_mode);
             accept(cfg_.power >= 1);
             FQB_CUDA(cudaMemcpyAsync(h_.host_status, status_, sizeof(unsigned), cudaMemcpyDeviceToHost, s_));

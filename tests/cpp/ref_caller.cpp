@@ -145,8 +145,8 @@ int main() {
     // 5. degenerate blocks: redraw ids j + 1000 attempt, BlockDegenerate after 3 redraws
     {
         DegenerateSource src;
-        src.bad_below = 2000;   // block 0 fails twice, then succeeds at id 2000
-        const ApproxSvd s = run_fixed_precision(f, config(SketchKind::Gaussian, 0.0, 1, 10, 1e-2, 1), &src);
+        src.bad_below = 2000;   // every block fails twice, then succeeds at id j + 2000
+        const ApproxSvd s = run_fixed_precision(f, config(SketchKind::Gaussian, 0.0, 1, 10, 1e-1, 1), &src);
         print_svd("redraw", s, &src.seen);
     }
     try {
