@@ -209,6 +209,12 @@ void fqb_host_free(void* p);
  * releases every cached free block now (also done when the last handle is destroyed);
  * returns the bytes released. */
 size_t fqb_host_pool_trim(void);
+/* Device blocks of >= 16 MB (Q, B', U, V, the A slices, A copies) come from a per-device
+ * cache of cudaMalloc'd blocks (a multi-GB cudaMallocAsync costs milliseconds, sometimes
+ * hundreds); device results freed with fqb_result_free return to it.  At most
+ * FQB_DEVICE_CACHE_MB (default half the device memory) stays cached; this releases every
+ * cached block now (also done when the last handle is destroyed); returns the bytes. */
+size_t fqb_device_cache_trim(void);
 
 /* ---- row-sharded multi-GPU (one rank per GPU, NCCL over NVLink) ------------- */
 /* Rank 0 creates a 128-byte id, the caller distributes it (e.g. with

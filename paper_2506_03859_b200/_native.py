@@ -110,6 +110,7 @@ SIGNATURES = [
     ("fqb_gen_lowrank", C.c_int, [_H, C.c_int64, C.c_int64, C.c_int, C.c_void_p, C.c_uint64, C.c_double,
                                   C.c_void_p, C.c_int64]),
     ("fqb_host_pool_trim", C.c_size_t, []),
+    ("fqb_device_cache_trim", C.c_size_t, []),
     ("fqb_raw_header", C.c_int, [C.c_char_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     ("fqb_load_raw_rows", C.c_int, [_H, C.c_char_p, C.c_int64, C.c_int64, C.c_void_p, C.c_int64, C.c_int,
                                     C.POINTER(C.c_int64)]),

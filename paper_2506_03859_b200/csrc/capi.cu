@@ -62,6 +62,8 @@ const char* fqb_last_error(void) { return g_last_error.c_str(); }
 
 size_t fqb_host_pool_trim(void) { return farqb::host_pool_trim(); }
 
+size_t fqb_device_cache_trim(void) { return farqb::device_cache_trim(); }
+
 const char* fqb_status_name(int status) {
     switch (status) {
         case FQB_OK: return "ok";
@@ -133,7 +135,10 @@ fqb_status fqb_destroy(fqb_handle h) {
         if (h->h.ev_v) cudaEventDestroy(h->h.ev_v);
         cudaStreamDestroy(h->h.own_stream);
         delete h;
-        if (g_live_handles.fetch_sub(1) == 1) farqb::host_pool_trim();
+        if (g_live_handles.fetch_sub(1) == 1) {
+            farqb::host_pool_trim();
+            farqb::device_cache_trim();
+        }
         return FQB_OK;
     });
 }
@@ -244,17 +249,16 @@ void fqb_host_free(void* p) { farqb::host_free(p); }
 
 void fqb_result_free(fqb_qb_result* r) {
     if (!r) return;
-    if (r->on_device) {
-        if (r->q) cudaFree(r->q);
-        if (r->bt) cudaFree(r->bt);
-    } else {
+    if (r->on_device && (r->q || r->bt || r->u || r->v)) {
+        // like cudaFree: no work still queued anywhere may use the blocks afterwards
+        cudaDeviceSynchronize();
+        for (double* p : {r->q, r->bt, r->u, r->v})
+            if (p && !farqb::device_free_large(p, nullptr)) cudaFree(p);
+    } else if (!r->on_device) {
         farqb::host_free(r->q);
         farqb::host_free(r->bt);
     }
-    if (r->on_device) {
-        if (r->u) cudaFree(r->u);
-        if (r->v) cudaFree(r->v);
-    } else {
+    if (!r->on_device) {
         farqb::host_free(r->u);
         farqb::host_free(r->v);
     }

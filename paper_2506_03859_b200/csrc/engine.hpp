@@ -3,7 +3,10 @@
 
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -13,7 +16,23 @@
 
 namespace farqb {
 
-// Stream-ordered device allocation (cudaMallocAsync pool), grown on demand.
+// FQB_ALLOC_STATS=1: report slow pool allocations on stderr (diagnostics)
+inline bool alloc_stats_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("FQB_ALLOC_STATS");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+
+// devmem.cu: cached large device blocks (>= kLargeBlock bytes), see there
+constexpr size_t kLargeBlock = size_t(16) << 20;
+void* device_alloc_large(size_t bytes, cudaStream_t s);
+bool device_free_large(void* p, cudaStream_t s);   // false: not a cached-path block
+size_t device_cache_trim();
+
+// Stream-ordered device allocation, grown on demand: the cudaMallocAsync pool for small
+// buffers, the large-block cache (devmem.cu) from kLargeBlock bytes up.
 template <typename T>
 struct DeviceArray {
     T* ptr = nullptr;
@@ -24,7 +43,7 @@ struct DeviceArray {
     DeviceArray& operator=(const DeviceArray&) = delete;
     ~DeviceArray() { release(); }
     void release() {
-        if (ptr) cudaFreeAsync(ptr, stream);
+        if (ptr && !device_free_large(ptr, stream)) cudaFreeAsync(ptr, stream);
         ptr = nullptr;
         count = 0;
     }
@@ -33,8 +52,18 @@ struct DeviceArray {
         if (n <= count && ptr) return ptr;
         release();
         stream = s;
-        FQB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ptr), std::max<size_t>(n, 1) * sizeof(T), s));
+        const auto t0 = std::chrono::steady_clock::now();
+        const size_t bytes = std::max<size_t>(n, 1) * sizeof(T);
+        if (bytes >= kLargeBlock)
+            ptr = static_cast<T*>(device_alloc_large(bytes, s));
+        else
+            FQB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ptr), bytes, s));
         count = std::max<size_t>(n, 1);
+        if (alloc_stats_enabled()) {
+            const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+            if (ms > 0.2) std::fprintf(stderr, "[farqb] device allocation %.3f GB took %.2f ms\n",
+                                       double(count * sizeof(T)) / 1e9, ms);
+        }
         return ptr;
     }
     // hand ownership to the caller
