@@ -193,6 +193,8 @@ class QbRun {
         norm_a_sq_ = h_.host_scalars[0];
         // non-finite A: DMMA, whose Inf/NaN propagation is the reference's
         if (oz_on_ && !std::isfinite(norm_a_sq_)) oz_on_ = false;
+        // Q'X products on the INT8 path when the A passes are there and the rows are many
+        q_oz_on_ = oz_on_ && q_oz_default() && m_ >= 4096;
     }
 
     double norm_a_sq() const { return norm_a_sq_; }
@@ -247,6 +249,28 @@ class QbRun {
         regrow(q_, ldq_);
         regrow(bt_, ldbt_);
         if (z_allowed_) regrow(rowsum_, 1);
+        if (q_oz_on_) {   // the slices of the committed Q columns move with Q
+            Workspace& w = h_.ws;
+            const int nsl = ozaki_fp64_slices();
+            DeviceArray<int8_t> fresh;
+            fresh.ensure(size_t(ozaki_x_bytes(nc, m_, nsl)), s_);
+            if (q_sliced_ > 0)
+                FQB_CUDA(cudaMemcpyAsync(fresh.ptr, w.oz_q_tn.ptr, size_t(ozaki_x_bytes(q_sliced_, m_, nsl)),
+                                         cudaMemcpyDeviceToDevice, s_));
+            w.oz_q_tn.release();
+            w.oz_q_tn.ptr = fresh.detach();
+            w.oz_q_tn.count = size_t(ozaki_x_bytes(nc, m_, nsl));
+            w.oz_q_tn.stream = s_;
+            DeviceArray<int> fe;
+            fe.ensure(size_t(nc), s_);
+            if (q_sliced_ > 0)
+                FQB_CUDA(cudaMemcpyAsync(fe.ptr, w.oz_q_e.ptr, sizeof(int) * size_t(q_sliced_), cudaMemcpyDeviceToDevice,
+                                         s_));
+            w.oz_q_e.release();
+            w.oz_q_e.ptr = fe.detach();
+            w.oz_q_e.count = size_t(nc);
+            w.oz_q_e.stream = s_;
+        }
         cap_ = nc;
         Workspace& w = h_.ws;
         w.t.ensure(size_t(nc) * b_, s_);
@@ -331,6 +355,38 @@ class QbRun {
         w.oz_ez.ensure(size_t(ozaki_apply_ez_count()), s_);
         ozaki_apply(M, N, K, 1.0, ta ? w.oz_x_tn.ptr : w.oz_x_nn.ptr, ta ? w.oz_e_tn.ptr : w.oz_e_nn.ptr, B, ldb, 0.0,
                     C, ldc, w.oz_z.ptr, w.oz_ez.ptr, h_.gws.work, h_.num_sms, s_, h_.lc, oz_nsl_);
+    }
+
+    // ---- the block Gram-Schmidt products Q' X on the INT8 tensor cores --------
+    // Q's columns are final once committed, so their slices (A'Y layout: one operand row
+    // per column of Q, K = m, a power-of-two scale per column) are made once: each block
+    // slices from the 128-column tile holding column l through l + b (Y_j / Q_j in place)
+    // and [Q|Y]'Y, Q'Y_s become one k_ozaki pass each instead of a DMMA GEMM (2 m l b
+    // flops per product; FP64-class like the A passes).  FQB_OZ_Q=0 keeps them on DMMA.
+    static bool q_oz_default() {
+        const char* e = std::getenv("FQB_OZ_Q");
+        return !(e && e[0] == '0');
+    }
+    bool use_q_oz(int64_t l) const { return q_oz_on_ && l >= kQOzMinCols; }
+    void slice_q(int64_t upto) {   // slices of q_ columns [floor(l_/128)*128, upto)
+        Workspace& w = h_.ws;
+        const int nsl = ozaki_fp64_slices();
+        const int64_t c0 = (l_ / 128) * 128;
+        const int64_t cols = upto - c0;
+        if (cols <= 0) return;
+        w.oz_q_line_max.ensure(size_t(ozaki_line_max_words(m_, cols)), s_);
+        ozaki_slice_a(q_.ptr + c0 * ldq_, m_, cols, ldq_, w.oz_q_line_max.ptr,
+                      w.oz_q_tn.ptr + (c0 / 128) * (ozaki_x_bytes(128, m_, nsl)), w.oz_q_e.ptr + c0, nullptr, nullptr,
+                      s_, h_.lc, nullptr, nullptr, nsl);
+        q_sliced_ = l_;   // committed columns with valid slices (the rest is redone next block)
+    }
+    void q_tn(int64_t M, const double* B, double* C, int64_t ldc) {   // C (M x b) = Q(:, :M)' B
+        Workspace& w = h_.ws;
+        const int nsl = ozaki_fp64_slices();
+        w.oz_z.ensure(size_t(ozaki_apply_z_bytes(m_, nsl)), s_);
+        w.oz_ez.ensure(size_t(ozaki_apply_ez_count()), s_);
+        ozaki_apply(M, b_, m_, 1.0, w.oz_q_tn.ptr, w.oz_q_e.ptr, B, ldq_, 0.0, C, ldc, w.oz_z.ptr, w.oz_ez.ptr,
+                    h_.gws.work, h_.num_sms, s_, h_.lc, nsl);
     }
 
     // ---- Omega ----------------------------------------------------------------
@@ -525,7 +581,12 @@ class QbRun {
         const int64_t ldcd = l + b;
         double* cd = w.cd.ptr;
         // [C1; D] = [Q_old | Y_j]' Y_j
-        gemm_(true, l + b, b, m_, 1.0, q_.ptr, ldq_, yj, ldq_, 0.0, cd, ldcd);
+        if (use_q_oz(l)) {
+            slice_q(l + b);
+            q_tn(l + b, yj, cd, ldcd);
+        } else {
+            gemm_(true, l + b, b, m_, 1.0, q_.ptr, ldq_, yj, ldq_, 0.0, cd, ldcd);
+        }
         comm_allreduce_sum(h_, cd, size_t(ldcd) * b, s_);
         double* dblk = cd + l;  // rows l..l+b-1, ld = l+b
         if (l == 0) {
@@ -539,7 +600,8 @@ class QbRun {
             launch_chol_upper_inv(S_, b, b, 1e-12, diag_max_, dblk, ldcd, R1_, R1i_, scal_ + kDMax,
                                   w.scratch.ptr, status_, kStAcceptPivot, s_, h_.lc);
             gemm_(false, m_, b, b, 1.0, yj, ldq_, R1i_, b, 0.0, w.ys.ptr, ldq_);
-            gemm_(true, l, b, m_, 1.0, q_.ptr, ldq_, w.ys.ptr, ldq_, 0.0, w.c2.ptr, l);
+            if (use_q_oz(l)) q_tn(l, w.ys.ptr, w.c2.ptr, l);
+            else gemm_(true, l, b, m_, 1.0, q_.ptr, ldq_, w.ys.ptr, ldq_, 0.0, w.c2.ptr, l);
             comm_allreduce_sum(h_, w.c2.ptr, size_t(l) * b, s_);
             gemm_(false, m_, b, l, -1.0, q_.ptr, ldq_, w.c2.ptr, l, 1.0, w.ys.ptr, ldq_);
         }
@@ -624,6 +686,9 @@ class QbRun {
     bool oz_on_ = false;              // A-pass products on the INT8 tensor cores (a_gemm)
     int oz_nsl_ = 7;                  // slices per operand of the A passes (7 / 8: FP64-class, 4: FP32-class)
     bool oz_ready_ = false;           // A sliced for this run (buffers live in the handle workspace)
+    bool q_oz_on_ = false;            // Q'X products of the accept step on the INT8 tensor cores
+    int64_t q_sliced_ = 0;            // columns of Q whose slices in ws.oz_q_tn are valid
+    static constexpr int64_t kQOzMinCols = 200;
     std::vector<double> residuals_;
     std::vector<int> ids_;
     double *S_, *S2_, *R1_, *R1i_, *R2_, *R2i_, *R_, *Ri_, *V_, *VS_, *VT_, *eig_, *sig_, *scal_;
