@@ -368,10 +368,12 @@ class QbRun {
         return !(e && e[0] == '0');
     }
     bool use_q_oz(int64_t l) const { return q_oz_on_ && l >= kQOzMinCols; }
-    void slice_q(int64_t upto) {   // slices of q_ columns [floor(l_/128)*128, upto)
+    // slices of q_ columns [floor(q_sliced_ / 128) * 128, upto): every committed column not
+    // sliced yet, the current block's Y_j, and the rest of the 128-column tile they start in
+    void slice_q(int64_t upto) {
         Workspace& w = h_.ws;
         const int nsl = ozaki_fp64_slices();
-        const int64_t c0 = (l_ / 128) * 128;
+        const int64_t c0 = (std::min(q_sliced_, l_) / 128) * 128;
         const int64_t cols = upto - c0;
         if (cols <= 0) return;
         w.oz_q_line_max.ensure(size_t(ozaki_line_max_words(m_, cols)), s_);
