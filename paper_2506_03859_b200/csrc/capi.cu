@@ -500,12 +500,13 @@ fqb_status fqb_gemm_emulated(fqb_handle h, int trans_a, int64_t m, int64_t n, in
         zs.ensure(size_t(farqb::ozaki_apply_z_bytes(k)), s);
         ex.ensure(size_t(m), s);
         ez.ensure(size_t(farqb::ozaki_apply_ez_count()), s);
-        farqb::DeviceArray<unsigned> line_max;
+        farqb::DeviceArray<unsigned> line_max, zmax;
         line_max.ensure(size_t(farqb::ozaki_line_max_words(m, k)), s);
+        zmax.ensure(size_t(farqb::ozaki_apply_ez_count()), s);
         if (trans_a) farqb::ozaki_slice_a(a, k, m, lda, line_max.ptr, xs.ptr, ex.ptr, nullptr, nullptr, s, h->h.lc);
         else farqb::ozaki_slice_a(a, m, k, lda, line_max.ptr, nullptr, nullptr, xs.ptr, ex.ptr, s, h->h.lc);
         farqb::ozaki_apply(m, n, k, alpha, xs.ptr, ex.ptr, b, ldb, beta, c, ldc, zs.ptr, ez.ptr, h->h.gws.work,
-                           h->h.num_sms, s, h->h.lc);
+                           h->h.num_sms, s, h->h.lc, farqb::ozaki_fp64_slices(), zmax.ptr);
         return FQB_OK;   // temporaries are freed stream-ordered, after the kernels
     });
 }
@@ -516,6 +517,7 @@ struct fqb_sliced_s {
     int64_t m = 0, n = 0;
     farqb::DeviceArray<int8_t> x_nn, x_tn, z;
     farqb::DeviceArray<int> e_nn, e_tn, ez;
+    farqb::DeviceArray<unsigned> zmax;
     int last_trans = -1;   // the last fqb_sliced_gemm: B slices left in z / ez
     int64_t last_nb = 0;
 };
@@ -565,9 +567,10 @@ fqb_status fqb_sliced_gemm(fqb_handle h, fqb_sliced sl, int trans_a, int64_t nb,
         cudaStream_t s = h->h.stream;
         farqb::ensure_gemm_workspace(h->h);
         sl->z.ensure(size_t(farqb::ozaki_apply_z_bytes(K)), s);
+        sl->zmax.ensure(size_t(farqb::ozaki_apply_ez_count()), s);
         farqb::ozaki_apply(M, nb, K, alpha, trans_a ? sl->x_tn.ptr : sl->x_nn.ptr,
                            trans_a ? sl->e_tn.ptr : sl->e_nn.ptr, b, ldb, beta, c, ldc, sl->z.ptr, sl->ez.ptr,
-                           h->h.gws.work, h->h.num_sms, s, h->h.lc);
+                           h->h.gws.work, h->h.num_sms, s, h->h.lc, farqb::ozaki_fp64_slices(), sl->zmax.ptr);
         sl->last_trans = trans_a ? 1 : 0;
         sl->last_nb = nb;
         return FQB_OK;

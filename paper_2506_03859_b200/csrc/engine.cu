@@ -353,8 +353,9 @@ class QbRun {
         Workspace& w = h_.ws;
         w.oz_z.ensure(size_t(ozaki_apply_z_bytes(K, oz_nsl_)), s_);
         w.oz_ez.ensure(size_t(ozaki_apply_ez_count()), s_);
+        w.oz_zmax.ensure(size_t(ozaki_apply_ez_count()), s_);
         ozaki_apply(M, N, K, 1.0, ta ? w.oz_x_tn.ptr : w.oz_x_nn.ptr, ta ? w.oz_e_tn.ptr : w.oz_e_nn.ptr, B, ldb, 0.0,
-                    C, ldc, w.oz_z.ptr, w.oz_ez.ptr, h_.gws.work, h_.num_sms, s_, h_.lc, oz_nsl_);
+                    C, ldc, w.oz_z.ptr, w.oz_ez.ptr, h_.gws.work, h_.num_sms, s_, h_.lc, oz_nsl_, w.oz_zmax.ptr);
     }
 
     // ---- the block Gram-Schmidt products Q' X on the INT8 tensor cores --------
@@ -387,8 +388,9 @@ class QbRun {
         const int nsl = ozaki_fp64_slices();
         w.oz_z.ensure(size_t(ozaki_apply_z_bytes(m_, nsl)), s_);
         w.oz_ez.ensure(size_t(ozaki_apply_ez_count()), s_);
+        w.oz_zmax.ensure(size_t(ozaki_apply_ez_count()), s_);
         ozaki_apply(M, b_, m_, 1.0, w.oz_q_tn.ptr, w.oz_q_e.ptr, B, ldq_, 0.0, C, ldc, w.oz_z.ptr, w.oz_ez.ptr,
-                    h_.gws.work, h_.num_sms, s_, h_.lc, nsl);
+                    h_.gws.work, h_.num_sms, s_, h_.lc, nsl, w.oz_zmax.ptr);
     }
 
     // ---- Omega ----------------------------------------------------------------

@@ -93,7 +93,7 @@ struct Workspace {
     // for the block Gram-Schmidt products [Q|Y]'Y and Q'Y_s (engine.cu, accept)
     DeviceArray<int8_t> oz_q_tn;
     DeviceArray<int> oz_q_e;
-    DeviceArray<unsigned> oz_q_line_max;
+    DeviceArray<unsigned> oz_q_line_max, oz_zmax;
 
     // every member, while the stream the frees are ordered on still exists
     void release_all() {
@@ -101,7 +101,7 @@ struct Workspace {
                         &scalars, &scratch, &a_copy, &values, &oz_norm_partial})
             d->release();
         for (auto* d : {&col_ptr, &row_idx, &counts, &oz_e_nn, &oz_e_tn, &oz_ez, &oz_q_e}) d->release();
-        for (auto* d : {&status, &gemm_flags, &oz_line_max, &oz_q_line_max}) d->release();
+        for (auto* d : {&status, &gemm_flags, &oz_line_max, &oz_q_line_max, &oz_zmax}) d->release();
         a_copy_f32.release();
         for (auto* d : {&oz_x_nn, &oz_x_tn, &oz_z, &oz_q_tn}) d->release();
     }

@@ -150,9 +150,11 @@ void ozaki_slice_z(const double* b, int64_t k, int64_t n, int64_t ld, int* e, in
 // C = alpha X' B + beta C for any N: B (K x N, ld, FP64) sliced in chunks of <= 64
 // columns into z (ozaki_apply_z_bytes(K)) / ez (ozaki_apply_ez_count()); N > 64
 // runs two chunks at a time on CTA pairs sharing the A tiles (FQB_OZ_PAIR=0: off)
+// zmax: ozaki_apply_ez_count() words of scratch; lets a long B (K > 16384 rows) take its
+// column maxima in one pass before slicing (null: the one-kernel slicer)
 void ozaki_apply(int64_t M, int64_t N, int64_t K, double alpha, const int8_t* xs, const int* ex, const double* b,
                  int64_t ldb, double beta, double* C, int64_t ldc, int8_t* z, int* ez, double* work, int num_sms,
-                 cudaStream_t s, LaunchCounter& lc, int nsl = ozaki_fp64_slices());
+                 cudaStream_t s, LaunchCounter& lc, int nsl = ozaki_fp64_slices(), unsigned* zmax = nullptr);
 void ozaki_gemm(int64_t M, int64_t N, int64_t K, double alpha, const int8_t* xs, const int* ex, const int8_t* zs,
                 const int* ez, double beta, double* C, int64_t ldc, double* work, int num_sms, cudaStream_t s,
                 LaunchCounter& lc, int nsl = ozaki_fp64_slices());

@@ -860,6 +860,67 @@ __global__ void __launch_bounds__(ZT) k_slice_z(const double* __restrict__ b, in
     put_chunk16<NSL>(v, e, out + (k0 / OZ_BK) * int64_t(ZR) * OZ_BK, z_tile, j, int(k0 % OZ_BK));
 }
 
+// Long Z operands (k > kZFused rows: the Y of config 4's A'Y, k = m = 100000): every CTA
+// of k_slice_z re-reads its whole column for the max (25x at k = 100000), so the maxima
+// come from one pass first (k_zcol_max: atomicMax of the high words) and the slicer is a
+// k-block per CTA with a warp per 8 rows -- each warp's stores are a contiguous 512 B.
+constexpr int64_t kZFused = 16384;
+constexpr int ZMAX_PER_CTA = 8192;
+__global__ void __launch_bounds__(256) k_zcol_max(const double* __restrict__ b, int64_t k, int64_t n, int64_t ld,
+                                                  unsigned* cmax) {
+    FQB_PDL_ENTRY();
+    __shared__ unsigned wmax[8];
+    const int j = blockIdx.x;
+    if (j >= n) return;
+    const double* col = b + int64_t(j) * ld;
+    const int64_t r0 = int64_t(blockIdx.y) * ZMAX_PER_CTA;
+    unsigned h = 0;
+    unsigned x[8];
+#pragma unroll
+    for (int g = 0; g < ZMAX_PER_CTA / (256 * 8); ++g) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int64_t r = r0 + (int64_t(g) * 8 + u) * 256 + threadIdx.x;
+            x[u] = r < k ? abs_hi(col[r]) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) h = max(h, x[u]);
+    }
+    h = __reduce_max_sync(0xFFFFFFFFu, h);
+    if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = h;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned mx = 0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) mx = max(mx, wmax[w]);
+        if (mx) atomicMax(cmax + j, mx);
+    }
+}
+
+template <int NSL, int S>
+__global__ void __launch_bounds__(256) k_slice_z_kb(const double* __restrict__ b, int64_t k, int64_t n, int64_t ld,
+                                                    const unsigned* __restrict__ cmax, int* ez, int8_t* out) {
+    FQB_PDL_ENTRY();
+    constexpr int ZR = z_block_rows(NSL, S);
+    const int kb = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int j = warp * 8 + (lane >> 2), q = lane & 3;   // row j of the tile, 16-byte chunk q
+    const int64_t k0 = int64_t(kb) * OZ_BK + q * 16;
+    int8_t* tile0 = out + int64_t(kb) * ZR * OZ_BK;
+    if (j >= S) {   // S = 56: the 8 zero rows after the last slice
+        if (S == 56) *reinterpret_cast<uint4*>(tile0 + swz(NSL * S + (j - S), q * 16)) = make_uint4(0u, 0u, 0u, 0u);
+        return;
+    }
+    const bool live = j < n;
+    const int e = live ? exp_of_hi(cmax[j]) : exp_of_hi(0u);
+    if (live && kb == 0 && q == 0) ez[j] = e;
+    const double* col = b + int64_t(j) * ld;
+    double v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) v[u] = (live && k0 + u < k) ? col[k0 + u] : 0.0;
+    put_chunk16<NSL>(v, e, tile0, int64_t(S) * OZ_BK, j, q * 16);
+}
+
 // Sum the pieces of every split tile in CTA order (deterministic) into C.
 // Pieces were written already scaled by 2^(ex + ez).  Block (tile, 8 columns),
 // one thread per tile row; up to 4 pieces x 8 columns of loads in flight.
@@ -970,10 +1031,29 @@ void ozaki_slice_a(const float* a, int64_t m, int64_t n, int64_t ld, unsigned* l
 }
 
 // Z slices with row spacing S (64, or 56 for chunks of <= 56 columns of the 7-slice scheme)
+template <int NSL, int S>
+static void slice_z_long(const double* b, int64_t k, int64_t n, int64_t ld, int* e, int8_t* out, unsigned* cmax,
+                         cudaStream_t s, LaunchCounter& lc) {
+    FQB_CUDA(cudaMemsetAsync(cmax, 0, sizeof(unsigned) * OZ_BN, s));
+    launch_k(k_zcol_max, dim3(unsigned(n), unsigned(ceil_div(k, ZMAX_PER_CTA))), 256, 0, s, b, k, n, ld, cmax);
+    FQB_LAUNCHED();
+    launch_k(k_slice_z_kb<NSL, S>, dim3(unsigned(ceil_div(k, OZ_BK))), 256, 0, s, b, k, n, ld, cmax, e, out);
+    FQB_LAUNCHED();
+    lc.bump(2);
+}
+
 static void slice_z_s(const double* b, int64_t k, int64_t n, int64_t ld, int* e, int8_t* out, cudaStream_t s,
-                      LaunchCounter& lc, int nsl, int S) {
+                      LaunchCounter& lc, int nsl, int S, unsigned* cmax = nullptr) {
     if (n <= 0 || k <= 0) return;
     check_nsl(nsl);
+    if (cmax && k > kZFused) {
+        if (nsl == 7 && S == 56) slice_z_long<7, 56>(b, k, n, ld, e, out, cmax, s, lc);
+        else if (nsl == 7) slice_z_long<7, 64>(b, k, n, ld, e, out, cmax, s, lc);
+        else if (nsl == 8) slice_z_long<8, 64>(b, k, n, ld, e, out, cmax, s, lc);
+        else if (nsl == 3) slice_z_long<3, 64>(b, k, n, ld, e, out, cmax, s, lc);
+        else slice_z_long<4, 64>(b, k, n, ld, e, out, cmax, s, lc);
+        return;
+    }
     const int64_t chunks = ceil_div(k, OZ_BK) * (OZ_BK / 16);
     const dim3 g(unsigned(S == 56 ? S + 8 : S), unsigned(ceil_div(chunks, ZT)));
     if (nsl == 7 && S == 56) launch_k(k_slice_z<7, 56>, g, ZT, 0, s, b, k, n, ld, e, out);
@@ -1121,7 +1201,7 @@ static bool pairs_enabled() {
 
 void ozaki_apply(int64_t M, int64_t N, int64_t K, double alpha, const int8_t* xs, const int* ex, const double* b,
                  int64_t ldb, double beta, double* C, int64_t ldc, int8_t* z, int* ez, double* work, int num_sms,
-                 cudaStream_t s, LaunchCounter& lc, int nsl) {
+                 cudaStream_t s, LaunchCounter& lc, int nsl, unsigned* zmax) {
     if (N <= 0) return;
     const int64_t chunks = ceil_div(N, OZ_BN);
     const int64_t cw = ceil_div(N, chunks);
@@ -1132,14 +1212,15 @@ void ozaki_apply(int64_t M, int64_t N, int64_t K, double alpha, const int8_t* xs
     // streamed once per pair of chunks instead of once per chunk
     while (pairs_enabled() && num_sms >= 2 && N - c0 > cw) {
         const int64_t nb = std::min(2 * cw, N - c0);
-        slice_z_s(b + c0 * ldb, K, cw, ldb, ez, z, s, lc, nsl, S);
-        slice_z_s(b + (c0 + cw) * ldb, K, nb - cw, ldb, ez + OZ_BN, z + zstride, s, lc, nsl, S);
+        slice_z_s(b + c0 * ldb, K, cw, ldb, ez, z, s, lc, nsl, S, zmax);
+        slice_z_s(b + (c0 + cw) * ldb, K, nb - cw, ldb, ez + OZ_BN, z + zstride, s, lc, nsl, S,
+                  zmax ? zmax + OZ_BN : nullptr);
         launch_ozaki(M, nb, K, alpha, xs, ex, z, ez, beta, C + c0 * ldc, ldc, work, num_sms, cw, nsl, S, s, lc);
         c0 += nb;
     }
     for (; c0 < N; c0 += cw) {
         const int64_t nb = std::min(cw, N - c0);
-        slice_z_s(b + c0 * ldb, K, nb, ldb, ez, z, s, lc, nsl, S);
+        slice_z_s(b + c0 * ldb, K, nb, ldb, ez, z, s, lc, nsl, S, zmax);
         launch_ozaki(M, nb, K, alpha, xs, ex, z, ez, beta, C + c0 * ldc, ldc, work, num_sms, 0, nsl, S, s, lc);
     }
 }

@@ -56,7 +56,7 @@ def _check_rows(got, aa, b, c0, alpha, beta, rows):
 @pytest.mark.parametrize("trans", [True, False])
 @pytest.mark.parametrize("m,n,k", [(8000, 50, 8000), (257, 33, 999), (128, 64, 64), (129, 1, 65), (1, 17, 3),
                                    (300, 64, 5000), (1000, 20, 127), (500, 56, 700), (500, 57, 700),
-                                   (200, 49, 4096)])
+                                   (200, 49, 4096), (300, 50, 40000), (130, 100, 20000), (129, 7, 16385)])
 def test_emulated_gemm_fp64_accuracy(eng, trans, m, n, k):
     g = torch.Generator(device="cpu").manual_seed(m + 3 * n + 7 * k + int(trans))
     a = torch.randn((k, m) if trans else (m, k), dtype=torch.float64, generator=g)
