@@ -855,7 +855,7 @@ int run_qb(Handle& h, const void* a, bool a_f32, int64_t m, int64_t n, int64_t l
             hc = HostSvdCopy{h.copy_stream, h.ev_u, h.ev_v, host_u, host_v, drop};
         }
         assemble_svd(h, run.q().ptr, run.ldq(), run.bt().ptr, run.ldbt(), m, n, l_final, u_dev.ptr, run.ldq(),
-                     v_dev.ptr, run.ldbt(), sig, flg, uv_host ? &hc : nullptr);
+                     v_dev.ptr, run.ldbt(), sig, flg, uv_host ? &hc : nullptr, run.ozaki() && l_final >= 256);
         uv_to_host = uv_host;
         for (int i = 0; i < drop; ++i) svd_res += sig[i] * sig[i];
     }

@@ -149,7 +149,7 @@ struct HostSvdCopy {
 };
 void assemble_svd(Handle& h, const double* q, int64_t ldq, const double* bt, int64_t ldbt, int64_t m, int64_t n,
                   int l, double* u, int64_t ldu, double* v, int64_t ldv, std::vector<double>& sigma,
-                  std::vector<char>& flagged, const HostSvdCopy* hc = nullptr);
+                  std::vector<char>& flagged, const HostSvdCopy* hc = nullptr, bool emulate = false);
 void destroy_cusolver(Handle& h);
 // synthetic.cu: test matrices on the device (reference synthetic.cpp)
 void random_orthonormal_dev(Handle& h, int64_t n, int r, uint64_t seed, uint32_t stream, int first_col, double* q,

@@ -7,7 +7,8 @@
 //     sigma = sqrt(max(lambda, 0))              ascending, like ApproxSvd
 //     U = Q U~,   V = B' U~ diag(1/sigma)       (sigma <= 1e-14 sigma_max: zero
 //                                                column, v_flagged, driver.cpp:331-341)
-// B B' is a DMMA GEMM; the l x l eigensolver is cuSOLVER's syevd (dlopen()ed,
+// B B', Q U~ and B' U~ Sigma^-1 are DMMA GEMMs, or (emulate: the run's A passes ran on the
+// INT8 tensor cores and l >= 256) k_ozaki products; the l x l eigensolver is cuSOLVER's syevd (dlopen()ed,
 // like NCCL: a library call for a once-per-run O(l^3) step, not the hot loop).
 #include <cusolverDn.h>
 #include <dlfcn.h>
@@ -266,7 +267,7 @@ bool eigh_inplace(Handle& h, double* mat, int l, double* w) { return eigh_core(h
 
 void assemble_svd(Handle& h, const double* q, int64_t ldq, const double* bt, int64_t ldbt, int64_t m, int64_t n,
                   int l, double* u, int64_t ldu, double* v, int64_t ldv, std::vector<double>& sigma,
-                  std::vector<char>& flagged, const HostSvdCopy* hc) {
+                  std::vector<char>& flagged, const HostSvdCopy* hc, bool emulate) {
     sigma.assign(l, 0.0);
     flagged.assign(l, 0);
     if (l == 0) return;
@@ -275,8 +276,32 @@ void assemble_svd(Handle& h, const double* q, int64_t ldq, const double* bt, int
     DeviceArray<double> mat, w, scale, us;
     mat.ensure(size_t(l) * l, s);
     w.ensure(size_t(l), s);
-    // B B' = Bt' Bt  (l x l)
-    gemm(true, l, l, n, 1.0, bt, ldbt, bt, ldbt, 0.0, mat.ptr, l, h.gws, h.num_sms, s, h.lc);
+    // emulate: the three products on the INT8 tensor cores (the run's A passes were there):
+    // B' sliced once in both layouts, Q row-scaled (K = l); FP64-class like the A passes
+    const int nsl = ozaki_fp64_slices();
+    DeviceArray<int8_t> bt_tn, bt_nn, q_nn, oz_z;
+    DeviceArray<int> bt_etn, bt_enn, q_enn, oz_ez;
+    DeviceArray<unsigned> oz_lm, oz_zmax;
+    if (emulate) {
+        oz_lm.ensure(size_t(ozaki_line_max_words(std::max<int64_t>(m, n), l)), s);
+        bt_tn.ensure(size_t(ozaki_x_bytes(l, n, nsl)), s);
+        bt_nn.ensure(size_t(ozaki_x_bytes(n, l, nsl)), s);
+        bt_etn.ensure(size_t(l), s);
+        bt_enn.ensure(size_t(n), s);
+        ozaki_slice_a(bt, n, l, ldbt, oz_lm.ptr, bt_tn.ptr, bt_etn.ptr, bt_nn.ptr, bt_enn.ptr, s, h.lc, nullptr,
+                      nullptr, nsl);
+        oz_z.ensure(size_t(ozaki_apply_z_bytes(std::max<int64_t>(n, l), nsl)), s);
+        oz_ez.ensure(size_t(ozaki_apply_ez_count()), s);
+        oz_zmax.ensure(size_t(ozaki_apply_ez_count()), s);
+    }
+    auto oz = [&](int64_t M, int64_t K, const int8_t* xs, const int* ex, const double* B, int64_t ldb, double* C,
+                  int64_t ldc) {
+        ozaki_apply(M, l, K, 1.0, xs, ex, B, ldb, 0.0, C, ldc, oz_z.ptr, oz_ez.ptr, h.gws.work, h.num_sms, s, h.lc,
+                    nsl, oz_zmax.ptr);
+    };
+    // B B' = Bt' Bt  (l x l; the eigensolvers read its lower triangle)
+    if (emulate) oz(l, n, bt_tn.ptr, bt_etn.ptr, bt, ldbt, mat.ptr, l);
+    else gemm(true, l, l, n, 1.0, bt, ldbt, bt, ldbt, 0.0, mat.ptr, l, h.gws, h.num_sms, s, h.lc);
     // eigendecomposition, sigma / flags / pseudo-inverse scale and both GEMMs are queued
     // without a host round trip; the one synchronization at the end also brings back
     // sigma, the flags and cuSOLVER's status
@@ -302,9 +327,17 @@ void assemble_svd(Handle& h, const double* q, int64_t ldq, const double* bt, int
         FQB_CUDA(cudaMemcpy2DAsync(dst, rows * sizeof(double), src + int64_t(hc->drop) * lds, lds * sizeof(double),
                                    rows * sizeof(double), l - hc->drop, cudaMemcpyDeviceToHost, hc->stream));
     };
-    gemm(false, m, l, l, 1.0, q, ldq, mat.ptr, l, 0.0, u, ldu, h.gws, h.num_sms, s, h.lc);
+    if (emulate) {
+        q_nn.ensure(size_t(ozaki_x_bytes(m, l, nsl)), s);
+        q_enn.ensure(size_t(std::max<int64_t>(m, 1)), s);
+        ozaki_slice_a(q, m, l, ldq, oz_lm.ptr, nullptr, nullptr, q_nn.ptr, q_enn.ptr, s, h.lc, nullptr, nullptr, nsl);
+        oz(m, l, q_nn.ptr, q_enn.ptr, mat.ptr, l, u, ldu);
+    } else {
+        gemm(false, m, l, l, 1.0, q, ldq, mat.ptr, l, 0.0, u, ldu, h.gws, h.num_sms, s, h.lc);
+    }
     if (hc && hc->u) copy_out(u, ldu, m, hc->u, hc->ev_u);
-    gemm(false, n, l, l, 1.0, bt, ldbt, us.ptr, l, 0.0, v, ldv, h.gws, h.num_sms, s, h.lc);
+    if (emulate) oz(n, l, bt_nn.ptr, bt_enn.ptr, us.ptr, l, v, ldv);
+    else gemm(false, n, l, l, 1.0, bt, ldbt, us.ptr, l, 0.0, v, ldv, h.gws, h.num_sms, s, h.lc);
     if (hc && hc->v) copy_out(v, ldv, n, hc->v, hc->ev_v);
     int hinfo = 0;
     FQB_CUDA(cudaMemcpyAsync(sigma.data(), scale.ptr, sizeof(double) * l, cudaMemcpyDeviceToHost, s));
