@@ -383,6 +383,27 @@ class QbRun {
                       s_, h_.lc, nullptr, nullptr, nsl);
         q_sliced_ = l_;   // committed columns with valid slices (the rest is redone next block)
     }
+    // Q (m x l) in the A G layout (row-scaled, K = l): a row's scale depends on every
+    // column, so it is made anew per block (one read of Q) for the two projections
+    // Y -= Q C of the block
+    void slice_q_nn(int64_t l) {
+        Workspace& w = h_.ws;
+        const int nsl = ozaki_fp64_slices();
+        w.oz_q_nn.ensure(size_t(ozaki_x_bytes(m_, cap_, nsl)), s_);
+        w.oz_q_enn.ensure(size_t(m_), s_);
+        w.oz_q_line_max.ensure(size_t(ozaki_line_max_words(m_, cap_ + b_)), s_);
+        ozaki_slice_a(q_.ptr, m_, l, ldq_, w.oz_q_line_max.ptr, nullptr, nullptr, w.oz_q_nn.ptr, w.oz_q_enn.ptr, s_,
+                      h_.lc, nullptr, nullptr, nsl);
+    }
+    void q_nn_sub(int64_t l, const double* Cm, int64_t ldcm, double* Y) {   // Y (m x b) -= Q(:, :l) Cm
+        Workspace& w = h_.ws;
+        const int nsl = ozaki_fp64_slices();
+        w.oz_z.ensure(size_t(std::max(ozaki_apply_z_bytes(m_, nsl), ozaki_apply_z_bytes(l, nsl))), s_);
+        w.oz_ez.ensure(size_t(ozaki_apply_ez_count()), s_);
+        w.oz_zmax.ensure(size_t(ozaki_apply_ez_count()), s_);
+        ozaki_apply(m_, b_, l, -1.0, w.oz_q_nn.ptr, w.oz_q_enn.ptr, Cm, ldcm, 1.0, Y, ldq_, w.oz_z.ptr, w.oz_ez.ptr,
+                    h_.gws.work, h_.num_sms, s_, h_.lc, nsl, w.oz_zmax.ptr);
+    }
     void q_tn(int64_t M, const double* B, double* C, int64_t ldc) {   // C (M x b) = Q(:, :M)' B
         Workspace& w = h_.ws;
         const int nsl = ozaki_fp64_slices();
@@ -466,7 +487,8 @@ class QbRun {
         launch_exclusive_scan(w.counts.ptr, b, w.col_ptr.ptr, s_, h_.lc);
         launch_iid_fill_csc(kind, seed, id, n_, b, denom, scale, w.col_ptr.ptr, w.row_idx.ptr, w.values.ptr,
                             status_, s_, h_.lc);
-        om_dense_ = false;
+        // sparse (p <= kDenseThreshold): a centered block needs z = p A 1 and B's row sums
+        finish_sparse(p);
     }
 
     void finish_sparse(double density) {
@@ -598,7 +620,12 @@ class QbRun {
                                   w.scratch.ptr, status_, kStAcceptPivot, s_, h_.lc);
             gemm_(false, m_, b, b, 1.0, yj, ldq_, R1i_, b, 0.0, w.ys.ptr, ldq_);
         } else {
-            gemm_(false, m_, b, l, -1.0, q_.ptr, ldq_, cd, ldcd, 1.0, yj, ldq_);
+            if (use_q_oz(l)) {
+                slice_q_nn(l);
+                q_nn_sub(l, cd, ldcd, yj);
+            } else {
+                gemm_(false, m_, b, l, -1.0, q_.ptr, ldq_, cd, ldcd, 1.0, yj, ldq_);
+            }
             gemm_(true, b, b, m_, 1.0, yj, ldq_, yj, ldq_, 0.0, S_, b);
             comm_allreduce_sum(h_, S_, size_t(b) * b, s_);
             launch_chol_upper_inv(S_, b, b, 1e-12, diag_max_, dblk, ldcd, R1_, R1i_, scal_ + kDMax,
@@ -607,7 +634,8 @@ class QbRun {
             if (use_q_oz(l)) q_tn(l, w.ys.ptr, w.c2.ptr, l);
             else gemm_(true, l, b, m_, 1.0, q_.ptr, ldq_, w.ys.ptr, ldq_, 0.0, w.c2.ptr, l);
             comm_allreduce_sum(h_, w.c2.ptr, size_t(l) * b, s_);
-            gemm_(false, m_, b, l, -1.0, q_.ptr, ldq_, w.c2.ptr, l, 1.0, w.ys.ptr, ldq_);
+            if (use_q_oz(l)) q_nn_sub(l, w.c2.ptr, l, w.ys.ptr);
+            else gemm_(false, m_, b, l, -1.0, q_.ptr, ldq_, w.c2.ptr, l, 1.0, w.ys.ptr, ldq_);
         }
         gemm_(true, b, b, m_, 1.0, w.ys.ptr, ldq_, w.ys.ptr, ldq_, 0.0, S2_, b);
         comm_allreduce_sum(h_, S2_, size_t(b) * b, s_);

@@ -265,6 +265,30 @@ def test_qb_matches_oracle_same_omega(eng, port, kind, zeta, power):
     _check_run(res, ref, power, f"kind={kind} zeta={zeta} P={power}")
 
 
+@pytest.mark.parametrize("p", [0.0, 0.01, 0.03])
+@pytest.mark.parametrize("power", [0, 1, 2])
+def test_qb_sparse_centered_stdbernoulli_matches_reference(eng, reference, p, power):
+    """StdBernoulli at densities <= 1/32 (the default max(1e-3, ln n / n) for n >= ~150): the
+    Omega block stays sparse and the centering (z = p A 1, B's row sums in the deflation)
+    is applied in the gather products -- against the reference on the same Omega, with the
+    first run of a fresh engine (no workspace left over from an earlier run)."""
+    a = _lowrank(800, 600, 0.95 ** np.arange(200), seed=31 + power)
+    spec = SketchSpec(2, p, 19)
+    cfg = FarpcaConfig(eps=1e-2, power=power, block=24, sketch=spec, relative=True)
+    fresh = fqb.Engine(0)
+    res = fresh.run_fixed_precision(a, cfg, output="host")
+    res2 = fresh.run_fixed_precision(a, cfg, output="host")
+    assert res.residual_sq == res2.residual_sq and np.array_equal(res.bt, res2.bt)
+
+    def src(n, b, bid):
+        return _arr(eng.gen_sketch(spec, n, b, bid))
+    ref = reference.run(a, eps=1e-2, power=power, block=24, kind=2, p=p, seed=19, relative=True, source=src,
+                        traced=True)
+    assert ref.status == 0 and res.converged and res.rank == ref.rank
+    _check_run(res, ref, power, f"stdbernoulli p={p} P={power}")
+    fresh.close()
+
+
 def test_qb_injected_block_source_matches_reference(reference, port):
     """BlockSource plugin: host-supplied fixed-zeta blocks, identical on GPU and reference."""
     a = _lowrank(900, 600, 1.0 / np.arange(1, 301), seed=5)
