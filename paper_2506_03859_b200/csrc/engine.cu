@@ -369,6 +369,15 @@ class QbRun {
         return !(e && e[0] == '0');
     }
     bool use_q_oz(int64_t l) const { return q_oz_on_ && l >= kQOzMinCols; }
+    // the projections Y -= Q C (K = l) only pay on the INT8 path once l is long enough to
+    // amortize each 128-row tile's accumulator drain (FQB_OZ_QNN_MIN, 0: never)
+    bool use_q_oz_nn(int64_t l) const {
+        static const int64_t min_cols = [] {
+            const char* e = std::getenv("FQB_OZ_QNN_MIN");
+            return e && *e ? int64_t(std::atoll(e)) : int64_t(1024);
+        }();
+        return q_oz_on_ && min_cols > 0 && l >= min_cols;
+    }
     // slices of q_ columns [floor(q_sliced_ / 128) * 128, upto): every committed column not
     // sliced yet, the current block's Y_j, and the rest of the 128-column tile they start in
     void slice_q(int64_t upto) {
@@ -620,7 +629,7 @@ class QbRun {
                                   w.scratch.ptr, status_, kStAcceptPivot, s_, h_.lc);
             gemm_(false, m_, b, b, 1.0, yj, ldq_, R1i_, b, 0.0, w.ys.ptr, ldq_);
         } else {
-            if (use_q_oz(l)) {
+            if (use_q_oz_nn(l)) {
                 slice_q_nn(l);
                 q_nn_sub(l, cd, ldcd, yj);
             } else {
@@ -634,7 +643,7 @@ class QbRun {
             if (use_q_oz(l)) q_tn(l, w.ys.ptr, w.c2.ptr, l);
             else gemm_(true, l, b, m_, 1.0, q_.ptr, ldq_, w.ys.ptr, ldq_, 0.0, w.c2.ptr, l);
             comm_allreduce_sum(h_, w.c2.ptr, size_t(l) * b, s_);
-            if (use_q_oz(l)) q_nn_sub(l, w.c2.ptr, l, w.ys.ptr);
+            if (use_q_oz_nn(l)) q_nn_sub(l, w.c2.ptr, l, w.ys.ptr);
             else gemm_(false, m_, b, l, -1.0, q_.ptr, ldq_, w.c2.ptr, l, 1.0, w.ys.ptr, ldq_);
         }
         gemm_(true, b, b, m_, 1.0, w.ys.ptr, ldq_, w.ys.ptr, ldq_, 0.0, S2_, b);

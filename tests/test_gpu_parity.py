@@ -273,6 +273,8 @@ def test_qb_sparse_centered_stdbernoulli_matches_reference(eng, reference, p, po
     is applied in the gather products -- against the reference on the same Omega, with the
     first run of a fresh engine (no workspace left over from an earlier run)."""
     a = _lowrank(800, 600, 0.95 ** np.arange(200), seed=31 + power)
+    p = p or fqb.default_density(SketchKind.StdBernoulli, 600)   # resolved like driver.cpp:449-455
+    assert p <= 1.0 / 32
     spec = SketchSpec(2, p, 19)
     cfg = FarpcaConfig(eps=1e-2, power=power, block=24, sketch=spec, relative=True)
     fresh = fqb.Engine(0)
