@@ -369,12 +369,14 @@ class QbRun {
         return !(e && e[0] == '0');
     }
     bool use_q_oz(int64_t l) const { return q_oz_on_ && l >= kQOzMinCols; }
-    // the projections Y -= Q C (K = l) only pay on the INT8 path once l is long enough to
-    // amortize each 128-row tile's accumulator drain (FQB_OZ_QNN_MIN, 0: never)
+    // the projections Y -= Q C (K = l) on the INT8 path from l >= FQB_OZ_QNN_MIN (default 0:
+    // never).  Measured on config 4 (r13): 745-747 ms per step with or without it at any
+    // threshold -- a tile has only l / 64 k-blocks to amortize its accumulator drain, and
+    // the per-block re-slicing of Q (row scales change as Q grows) eats the rest; DMMA stays
     bool use_q_oz_nn(int64_t l) const {
         static const int64_t min_cols = [] {
             const char* e = std::getenv("FQB_OZ_QNN_MIN");
-            return e && *e ? int64_t(std::atoll(e)) : int64_t(1024);
+            return e && *e ? int64_t(std::atoll(e)) : int64_t(0);
         }();
         return q_oz_on_ && min_cols > 0 && l >= min_cols;
     }
