@@ -130,6 +130,9 @@ fqb_status fqb_destroy(fqb_handle h) {
         cudaEventDestroy(h->h.ev0);
         cudaEventDestroy(h->h.ev1);
         if (h->h.copy_stream) cudaStreamDestroy(h->h.copy_stream);
+        if (h->h.comm_stream) cudaStreamDestroy(h->h.comm_stream);
+        if (h->h.ev_half) cudaEventDestroy(h->h.ev_half);
+        if (h->h.ev_reduced) cudaEventDestroy(h->h.ev_reduced);
         if (h->h.ev_qb) cudaEventDestroy(h->h.ev_qb);
         if (h->h.ev_u) cudaEventDestroy(h->h.ev_u);
         if (h->h.ev_v) cudaEventDestroy(h->h.ev_v);

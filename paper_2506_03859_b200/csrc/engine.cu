@@ -358,6 +358,76 @@ class QbRun {
                     C, ldc, w.oz_z.ptr, w.oz_ez.ptr, h_.gws.work, h_.num_sms, s_, h_.lc, oz_nsl_, w.oz_zmax.ptr);
     }
 
+    // W (n x N) = sum over ranks of A_g' B (the A'Y passes).  With a NCCL communicator
+    // the product runs in two halves of W's rows (A's columns, split on a 128 multiple):
+    // the all-reduce of the first half, on a second stream, overlaps the second half's
+    // product (16 MB per pass at config 4).  Otherwise product, then sum.
+    void a_tn_reduced(int N, const double* B, int64_t ldb, double* C, int64_t ldc) {
+        const int64_t n1 = (n_ / 2 / 128) * 128;
+        if (!h_.comm || n1 == 0) {
+            a_gemm(true, N, B, ldb, C, ldc);
+            comm_allreduce_sum(h_, C, size_t(ldc) * N, s_);
+            return;
+        }
+        if (!h_.comm_stream) {
+            FQB_CUDA(cudaStreamCreateWithFlags(&h_.comm_stream, cudaStreamNonBlocking));
+            FQB_CUDA(cudaEventCreateWithFlags(&h_.ev_half, cudaEventDisableTiming));
+            FQB_CUDA(cudaEventCreateWithFlags(&h_.ev_reduced, cudaEventDisableTiming));
+        }
+        // the halves are C rows [0, n1) and [n1, n) of every column: each is packed into a
+        // contiguous buffer for one all-reduce and unpacked after it
+        double* buf = h_.ws.w_half.ensure(size_t(n_) * N, s_);
+        auto reduce_rows = [&](int64_t r0, int64_t rows, cudaStream_t st) {
+            double* pk = buf + r0 * N;
+            FQB_CUDA(cudaMemcpy2DAsync(pk, rows * sizeof(double), C + r0, ldc * sizeof(double), rows * sizeof(double),
+                                       N, cudaMemcpyDeviceToDevice, st));
+            comm_allreduce_sum(h_, pk, size_t(rows) * N, st);
+            FQB_CUDA(cudaMemcpy2DAsync(C + r0, ldc * sizeof(double), pk, rows * sizeof(double), rows * sizeof(double),
+                                       N, cudaMemcpyDeviceToDevice, st));
+        };
+        a_gemm_rows(0, n1, N, B, ldb, C, ldc, false);
+        FQB_CUDA(cudaEventRecord(h_.ev_half, s_));
+        FQB_CUDA(cudaStreamWaitEvent(h_.comm_stream, h_.ev_half, 0));
+        reduce_rows(0, n1, h_.comm_stream);
+        a_gemm_rows(n1, n_ - n1, N, B, ldb, C, ldc, true);
+        FQB_CUDA(cudaEventRecord(h_.ev_half, s_));
+        FQB_CUDA(cudaStreamWaitEvent(h_.comm_stream, h_.ev_half, 0));
+        reduce_rows(n1, n_ - n1, h_.comm_stream);   // same communicator: issued in order on one stream
+        FQB_CUDA(cudaEventRecord(h_.ev_reduced, h_.comm_stream));
+        FQB_CUDA(cudaStreamWaitEvent(s_, h_.ev_reduced, 0));
+    }
+    // rows [r0, r0 + rows) of A' B (A's columns r0..): the Ozaki TN slices start at a
+    // 128-row tile boundary; `again` reuses the B slices the first half made
+    void a_gemm_rows(int64_t r0, int64_t rows, int N, const double* B, int64_t ldb, double* C, int64_t ldc,
+                     bool again) {
+        if (!oz_on_) {
+            ensure_fp64_a();
+            const int64_t lda = a_ld64_ ? a_ld64_ : lda_;
+            gemm_(true, rows, N, m_, 1.0, a_ + r0 * lda, lda, B, ldb, 0.0, C + r0, ldc);
+            return;
+        }
+        if (!oz_ready_) {
+            oz_ready_ = true;
+            if (!prepare_ozaki()) {
+                oz_on_ = false;
+                a_gemm_rows(r0, rows, N, B, ldb, C, ldc, false);
+                return;
+            }
+        }
+        Workspace& w = h_.ws;
+        const int8_t* xs = w.oz_x_tn.ptr + (r0 / 128) * ozaki_x_bytes(128, m_, oz_nsl_);
+        if (again && N <= 128) {
+            ozaki_apply_presliced(rows, N, m_, 1.0, xs, w.oz_e_tn.ptr + r0, 0.0, C + r0, ldc, w.oz_z.ptr, w.oz_ez.ptr,
+                                  h_.gws.work, h_.num_sms, s_, h_.lc, oz_nsl_);
+            return;
+        }
+        w.oz_z.ensure(size_t(ozaki_apply_z_bytes(m_, oz_nsl_)), s_);
+        w.oz_ez.ensure(size_t(ozaki_apply_ez_count()), s_);
+        w.oz_zmax.ensure(size_t(ozaki_apply_ez_count()), s_);
+        ozaki_apply(rows, N, m_, 1.0, xs, w.oz_e_tn.ptr + r0, B, ldb, 0.0, C + r0, ldc, w.oz_z.ptr, w.oz_ez.ptr,
+                    h_.gws.work, h_.num_sms, s_, h_.lc, oz_nsl_, w.oz_zmax.ptr);
+    }
+
     // ---- the block Gram-Schmidt products Q' X on the INT8 tensor cores --------
     // Q's columns are final once committed, so their slices (A'Y layout: one operand row
     // per column of Q, K = m, a power-of-two scale per column) are made once: each block
@@ -589,8 +659,7 @@ class QbRun {
         for (int k = 1; k <= P; ++k) {
             if (k == 1) apply_omega(w.y0.ptr, ldq_);
             else a_gemm(false, b_, w.g.ptr, ldbt_, w.y0.ptr, ldq_);
-            a_gemm(true, b_, w.y0.ptr, ldq_, w.wp.ptr, ldbt_);
-            comm_allreduce_sum(h_, w.wp.ptr, size_t(ldbt_) * b_, s_);   // W = sum_g A_g' Y_g
+            a_tn_reduced(b_, w.y0.ptr, ldq_, w.wp.ptr, ldbt_);   // W = sum_g A_g' Y_g
             if (l_ > 0) {
                 if (k == 1) tmul_omega(w.t.ptr, l_);
                 else gemm_(true, l_, b_, n_, 1.0, bt_.ptr, ldbt_, w.g.ptr, ldbt_, 0.0, w.t.ptr, l_);
@@ -613,8 +682,7 @@ class QbRun {
         double* btj = bt_.ptr + l * ldbt_;
         if (from_iterate) a_gemm(false, b, w.g.ptr, ldbt_, yj, ldq_);
         else apply_omega(yj, ldq_);
-        a_gemm(true, b, yj, ldq_, w.wraw.ptr, ldbt_);
-        comm_allreduce_sum(h_, w.wraw.ptr, size_t(ldbt_) * b, s_);
+        a_tn_reduced(b, yj, ldq_, w.wraw.ptr, ldbt_);
         const int64_t ldcd = l + b;
         double* cd = w.cd.ptr;
         // [C1; D] = [Q_old | Y_j]' Y_j

@@ -78,7 +78,7 @@ struct DeviceArray {
 // Per-handle reusable workspace (everything except the Q and B' outputs).
 struct Workspace {
     DeviceArray<double> omega, y0, ys, wp, wraw, g, t, cd, c2, small, zc, rowsum_b, splitk, partial,
-        scalars, scratch, a_copy, oz_norm_partial;
+        scalars, scratch, a_copy, oz_norm_partial, w_half;
     DeviceArray<float> a_copy_f32;   // FP32 input mode staging
     DeviceArray<int> col_ptr, row_idx, counts;
     DeviceArray<double> values;
@@ -98,7 +98,7 @@ struct Workspace {
     // every member, while the stream the frees are ordered on still exists
     void release_all() {
         for (auto* d : {&omega, &y0, &ys, &wp, &wraw, &g, &t, &cd, &c2, &small, &zc, &rowsum_b, &splitk, &partial,
-                        &scalars, &scratch, &a_copy, &values, &oz_norm_partial})
+                        &scalars, &scratch, &a_copy, &values, &oz_norm_partial, &w_half})
             d->release();
         for (auto* d : {&col_ptr, &row_idx, &counts, &oz_e_nn, &oz_e_tn, &oz_ez, &oz_q_e, &oz_q_enn}) d->release();
         for (auto* d : {&status, &gemm_flags, &oz_line_max, &oz_q_line_max, &oz_zmax}) d->release();
@@ -132,6 +132,9 @@ struct Handle {
     void* cusolver = nullptr;  // svd.cu
     // D2H of host results overlapped with the SVD assembly (created on first use)
     cudaStream_t copy_stream = nullptr;
+    // NCCL all-reduce of the first half of W = A'Y overlapped with the second half's product
+    cudaStream_t comm_stream = nullptr;
+    cudaEvent_t ev_half = nullptr, ev_reduced = nullptr;
     cudaEvent_t ev_qb = nullptr;
     cudaEvent_t ev_u = nullptr, ev_v = nullptr;   // host U / V copies of the SVD assembly
 };

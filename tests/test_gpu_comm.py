@@ -1,6 +1,9 @@
 """Row-sharded (NCCL) engine path on the one GPU this run has: a 1-rank
-communicator exercises every all-reduce point of csrc/engine.cu and must leave
-the factorization bit-identical to the single-GPU run."""
+communicator exercises every all-reduce point of csrc/engine.cu, including the
+A'Y passes split in two row halves whose first all-reduce overlaps the second half's
+product.  The halves change the products' internal summation order (split-K / stream-K
+partitions follow the shape), so the factorization must equal the single-GPU run to
+rounding: same rank / blocks / ids, E within 1e-12 ||A||^2, Q B within 1e-12 ||A||_F."""
 import socket
 
 import numpy as np
@@ -23,12 +26,13 @@ def _port():
         return s.getsockname()[1]
 
 
-def test_one_rank_nccl_comm_is_transparent():
+@pytest.mark.parametrize("m,n,b", [(1600, 1200, 32), (6000, 3000, 100)])   # DMMA / INT8 (paired) A passes
+def test_one_rank_nccl_comm_is_transparent(m, n, b):
     rng = np.random.default_rng(0)
-    u, _ = np.linalg.qr(rng.standard_normal((1600, 300)))
-    v, _ = np.linalg.qr(rng.standard_normal((1200, 300)))
+    u, _ = np.linalg.qr(rng.standard_normal((m, 300)))
+    v, _ = np.linalg.qr(rng.standard_normal((n, 300)))
     a = np.asfortranarray((u * 10.0 ** (-np.arange(300) / 60)) @ v.T)
-    cfg = FarpcaConfig(eps=1e-4, power=2, block=32, sketch=SketchSpec(4, 0.0, 3, zeta=8), relative=True)
+    cfg = FarpcaConfig(eps=1e-4, power=2, block=b, sketch=SketchSpec(4, 0.0, 3, zeta=8), relative=True)
     plain = fqb.Engine(0)
     r0 = plain.run_fixed_precision(a, cfg, output="host")
     dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{_port()}", rank=0, world_size=1,
@@ -42,6 +46,6 @@ def test_one_rank_nccl_comm_is_transparent():
         eng.detach_comm()
     finally:
         dist.destroy_process_group()
-    assert r1.rank == r0.rank and r1.blocks == r0.blocks
-    assert r1.residual_sq == r0.residual_sq
-    assert np.array_equal(r1.q, r0.q) and np.array_equal(r1.bt, r0.bt)
+    assert (r1.rank, r1.blocks, r1.block_ids) == (r0.rank, r0.blocks, r0.block_ids)
+    assert abs(r1.residual_sq - r0.residual_sq) <= 1e-12 * r0.norm_a_sq
+    assert np.linalg.norm(r1.q @ r1.bt.T - r0.q @ r0.bt.T) <= 1e-12 * np.sqrt(r0.norm_a_sq)
