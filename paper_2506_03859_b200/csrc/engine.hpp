@@ -139,6 +139,8 @@ struct Handle {
     cudaEvent_t ev_u = nullptr, ev_v = nullptr;   // host U / V copies of the SVD assembly
 };
 
+// eiglarge.cu: l x l symmetric eigensolver for 224 < l <= 8192 (a-posteriori checked; false: use syevd)
+bool large_eigh(Handle& h, const double* mat, int n, double* w, double* x);
 // svd.cu: U = Q U~, V = Bt U~ Sigma^-1 from eig(B B'); sigma ascending
 bool eigh_inplace(Handle& h, double* mat, int l, double* w);
 // Host copies of U / V's kept columns (the last l - drop), issued on `stream` right

@@ -212,13 +212,27 @@ static bool eigh_core(Handle& h, double* mat, int l, double* w, int* info_dev) {
     cudaStream_t s = h.stream;
     ensure_gemm_workspace(h);
     const char* env = std::getenv("FQB_EIG");
+    // unset / "small": the own solver for l <= 224 (eigsmall.cu), syevd above; "large": also the
+    // own solver above 224 (eiglarge.cu: correct, but 3.4x slower than syevd at l = 2000 -- its
+    // one-stage tridiagonalisation is a chain of 2000 grid barriers, 17 us per column)
     const int eig_mode = !env ? 0 : std::string(env) == "syevj" ? 2 : std::string(env) == "syevd" ? 1 : 0;
+    const bool own_large = env && std::string(env) == "large";
     if (eig_mode == 0 && l <= kSmallEighMax) {
         DeviceArray<double> es;
         es.ensure(size_t(small_eigh_scratch_doubles(l)), s);
         const bool ok = small_eigh(mat, l, w, mat, es.ptr, h.gws, h.num_sms, s, h.lc);
         FQB_CUDA(cudaStreamSynchronize(s));   // es is released on scope exit
         if (ok) return true;
+    }
+    if (own_large && l > kSmallEighMax) {
+        // own solver for large l (eiglarge.cu): cooperative tridiagonalisation, bisection,
+        // inverse iteration, WY back-transformation; checked a posteriori, syevd if not
+        DeviceArray<double> keep;   // the input survives a failed attempt
+        keep.ensure(size_t(l) * l, s);
+        FQB_CUDA(cudaMemcpyAsync(keep.ptr, mat, sizeof(double) * size_t(l) * l, cudaMemcpyDeviceToDevice, s));
+        if (large_eigh(h, keep.ptr, l, w, mat)) return true;
+        FQB_CUDA(cudaMemcpyAsync(mat, keep.ptr, sizeof(double) * size_t(l) * l, cudaMemcpyDeviceToDevice, s));
+        FQB_CUDA(cudaStreamSynchronize(s));
     }
     CusolverApi& api = cusolver();
     if (!h.cusolver) {

@@ -82,9 +82,13 @@ def test_tight_clusters_fall_back_or_pass(eng):
     _check(eng, _spd(60, spec, seed=9), expect_small=False)
 
 
-def test_large_l_uses_cusolver(eng):
-    small = _check(eng, _spd(300, np.linspace(0, 1, 300), seed=3), expect_small=False)
-    assert not small
+def test_large_l_uses_the_own_solver(eng, monkeypatch):
+    """l > 224 with FQB_EIG=large runs eiglarge.cu (not cuSOLVER) on a well-separated spectrum;
+    by default syevd (measured faster there)."""
+    monkeypatch.setenv("FQB_EIG", "large")
+    assert _check(eng, _spd(300, np.linspace(0, 1, 300), seed=3), expect_small=False)
+    monkeypatch.delenv("FQB_EIG")
+    assert not _check(eng, _spd(300, np.linspace(0, 1, 300), seed=3), expect_small=False)
 
 
 def test_qb_svd_matches_numpy_and_syevd(eng, monkeypatch):
@@ -116,3 +120,52 @@ def test_default_is_the_small_solver_and_syevd_on_request(eng, monkeypatch):
     assert _check(eng, _spd(50, np.linspace(1, 2, 50), seed=1))
     monkeypatch.setenv("FQB_EIG", "syevd")
     assert not _check(eng, _spd(50, np.linspace(1, 2, 50), seed=1), expect_small=False)
+
+
+# ---- l > 224: the cooperative tridiagonalisation solver of eiglarge.cu (FQB_EIG=large) --------
+
+@pytest.fixture
+def large_solver(monkeypatch):
+    monkeypatch.setenv("FQB_EIG", "large")
+
+
+@pytest.mark.parametrize("n", [225, 257, 600, 1024, 2000])
+def test_large_decaying_spectrum(eng, large_solver, n):
+    """Config 4's assembly: lambda_i = sigma_i^2, sigma_i = 10^(-3i/2000) (l = 2000)."""
+    _check(eng, _spd(n, 10.0 ** (-6.0 * np.arange(n) / 2000.0), seed=n))
+
+
+@pytest.mark.parametrize("n", [300, 1500])
+def test_large_indefinite(eng, large_solver, n):
+    rng = np.random.default_rng(n)
+    _check(eng, _spd(n, rng.standard_normal(n), seed=n + 1))
+
+
+@pytest.mark.parametrize("n", [300, 1500])
+def test_large_big_cluster_falls_back_correctly(eng, large_solver, n):
+    """Half the spectrum one exact cluster: inverse iteration cannot separate it, the check
+    rejects the own result and syevd answers -- within the bar either way."""
+    rng = np.random.default_rng(n)
+    spec = np.concatenate([rng.standard_normal(n // 2), np.full(n - n // 2, 0.25)])
+    _check(eng, _spd(n, spec, seed=n + 1), expect_small=False)
+
+
+def test_large_matches_syevd_in_the_qb_assembly(eng, monkeypatch):
+    """A QB run with l = 400 (> 224): the own large solver vs FQB_EIG=syevd -- sigma within
+    1e-12 sigma_max, U orthonormal, U S V' identical to rounding."""
+    from paper_2506_03859_b200 import FarpcaConfig, SketchSpec
+    rng = np.random.default_rng(3)
+    u, _ = np.linalg.qr(rng.standard_normal((3000, 500)))
+    v, _ = np.linalg.qr(rng.standard_normal((1200, 500)))
+    a = np.asfortranarray((u * 0.99 ** np.arange(500)) @ v.T)
+    cfg = FarpcaConfig(eps=1e-3, power=1, block=50, sketch=SketchSpec(3, 0.0, 5, zeta=8), relative=True)
+    monkeypatch.setenv("FQB_EIG", "large")
+    r_own = eng.run_fixed_precision(a, cfg, output="host", svd=True)
+    monkeypatch.setenv("FQB_EIG", "syevd")
+    r_ref = eng.run_fixed_precision(a, cfg, output="host", svd=True)
+    assert r_own.rank == r_ref.rank > 224
+    assert np.max(np.abs(r_own.sigma - r_ref.sigma)) <= 1e-12 * r_ref.sigma[-1]
+    assert np.abs(r_own.u.T @ r_own.u - np.eye(r_own.rank)).max() < 1e-11
+    us_own = (r_own.u * r_own.sigma) @ r_own.v.T
+    us_ref = (r_ref.u * r_ref.sigma) @ r_ref.v.T
+    assert np.linalg.norm(us_own - us_ref) <= 1e-10 * np.linalg.norm(us_ref)
