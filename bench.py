@@ -69,15 +69,27 @@ def peaks():
     """Roofline denominators: MEASURED_PEAKS.json (driver-written) for HBM; the FP64
     DMMA peak measured by this repo (profiles/fp64_peak_r01.txt) for context."""
     out = {"hbm_gbs": None, "source": "MEASURED_PEAKS.json", "fp64_tflops": 37.1,
-           "fp64_source": "profiles/fp64_peak_r01.txt (DMMA microbenchmark; no FP64 entry in MEASURED_PEAKS.json)"}
+           "fp64_source": "profiles/fp64_peak_r01.txt (DMMA microbenchmark; no FP64 entry in MEASURED_PEAKS.json)",
+           "bf16_tflops": None}
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             mp = json.load(f)
         out["hbm_gbs"] = float(mp["hbm_gbs"])
+        out["bf16_tflops"] = float(mp["bf16_tflops"])
     except (OSError, ValueError, KeyError):
         out["hbm_gbs"] = 6650.0
         out["source"] = "fallback (B200_PROFILING.md: 6.65 TB/s)"
     return out
+
+
+def ozaki_int8_ops(rows_out: int, k: int, b: int) -> float:
+    """INT8 tensor-core operations one k_ozaki<*,7,*,56> launch executes (2 per MAC): per
+    128-row output tile, per 64-byte k-block and per column chunk (<= 56 columns) the
+    issue_s56 schedule runs MMAs of N = 400+400+336+288+224+176+112 = 1936 (ozaki.cu)."""
+    tiles = -(-rows_out // 128)
+    kblocks = -(-k // 64)
+    chunks = -(-b // 56)
+    return 2.0 * tiles * kblocks * chunks * 1936 * 128 * 64
 
 
 def bench_config(world: int) -> dict:
@@ -205,6 +217,20 @@ def ozaki_roofline(eng, a, stream, pk):
     return out
 
 
+def tensor_view(ms: float, pk: dict) -> dict:
+    """The same launch against the INT8 tensor pipe, the unit that actually bounds it
+    (DESIGN.md 4a): executed INT8 ops / launch time, against the dense INT8 rate (2x bf16
+    per clock on B200: 4.5 POPS nominal, and 2x the MEASURED bf16 cuBLAS rate, i.e. the
+    same power-capped clocks)."""
+    ops = ozaki_int8_ops(N, M, BLOCK)
+    tops = ops / ms / 1e9
+    meas = 2.0 * pk["bf16_tflops"] if pk.get("bf16_tflops") else None
+    return {"int8_ops_per_launch": ops, "achieved_tops": tops, "peak_nominal_tops": 4500.0,
+            "frac_nominal": tops / 4500.0, "peak_measured_equiv_tops": meas,
+            "frac_measured_equiv": (tops / meas) if meas else None,
+            "note": "peak_measured_equiv = 2 x MEASURED_PEAKS bf16_tflops (no INT8 entry there)"}
+
+
 def sketch_roofline(eng, dev, pk):
     """Sparse-sign sketch Y = A*Omega at BASELINE config 3's shape (A 20000 x 20000 FP64,
     b = 64, zeta = 8): HBM GB/s of the gather SpMM.  32 different Omega blocks, each writing
@@ -255,7 +281,7 @@ def sketch_roofline(eng, dev, pk):
 
 
 def load_traffic():
-    for name in ("traffic_r08.json", "traffic_r07.json"):
+    for name in ("R2_traffic.json",):
         try:
             with open(os.path.join(ROOT, "profiles", name)) as f:
                 return json.load(f)
@@ -376,6 +402,7 @@ def run_ours(args):
         r = eng.run_fixed_precision(a, cfg, output="device", svd=True)
         del r
     barrier()
+    eng.set_pass_timing(True)    # CUDA events around every A-pass k_ozaki launch inside the timed steps
     launches0 = eng.launch_count
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     step_ms = []
@@ -394,6 +421,8 @@ def run_ours(args):
     e1.synchronize()
     barrier()
     launches = eng.launch_count - launches0
+    live_ms, live_n, live_bytes = eng.pass_timing()
+    eng.set_pass_timing(False)
     ms = e0.elapsed_time(e1) / args.steps
     if world > 1:
         t = torch.tensor([ms], device=dev)
@@ -438,6 +467,8 @@ def run_ours(args):
     torch.cuda.empty_cache()
     sketch = sketch_roofline(eng, dev, pk)
     dom = roof["tn_kernel"]   # the dominant kernel by itself (k_ozaki + its stream-K fixup)
+    live_launch_ms = live_ms / max(live_n, 1)
+    live_gbs = (live_bytes / max(live_n, 1)) / live_launch_ms / 1e6 if live_n else 0.0
     traffic = load_traffic()
     line = {
         "metric": "farPCA time-to-eps (s)",
@@ -458,20 +489,27 @@ def run_ours(args):
                 "steps": e2e_steps},
         "gpu_launches": launches,
         "roofline": {"bound": "hbm",
-                     "kernel": "k_ozaki<true,7> (tcgen05 kind::i8 FP64 emulation, two 50-column chunks on "
-                               "multicast CTA pairs) + k_ozaki_fixup, W = A'Y at 100000x100x20000 on pre-sliced "
-                               "A and Y (fqb_sliced_gemm_again)",
-                     "achieved": dom["gbs"], "peak": pk["hbm_gbs"], "unit": "GB/s",
-                     "frac": dom["gbs"] / pk["hbm_gbs"], "traffic": (traffic or {}).get("ozaki_c4_tn_bytes_per_launch"),
+                     "kernel": "k_ozaki<true,7,2,56> (tcgen05 kind::i8 FP64 emulation, two 50-column chunks on "
+                               "multicast CTA pairs) + k_ozaki_fixup: the A passes W = A'Y and Y = A G of the timed "
+                               "steps",
+                     "achieved": live_gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                     "frac": live_gbs / pk["hbm_gbs"], "traffic": (traffic or {}).get("ozaki_c4_tn_bytes_per_launch"),
+                     "traffic_source": (traffic or {}).get("source"),
                      "peak_source": pk["source"],
-                     "bytes_per_launch": dom["bytes"], "bytes_formula": "8*(m*n + m*b + n*b) (SURVEY 8(d), dense A'Y)",
+                     "timing": "live: CUDA events on the engine's stream around every A-pass k_ozaki launch (+ fixup) "
+                               "inside the timed steps (fqb_set_pass_timing / fqb_pass_timing)",
+                     "launches_timed": live_n, "launch_ms": live_launch_ms,
+                     "bytes_per_launch": live_bytes / max(live_n, 1),
+                     "bytes_formula": "8*(M*K + K*b + M*b) per launch (SURVEY 8(d): FP64 A read once, Y read, W "
+                                      "written) = 8*(m*n + m*b + n*b) at C4",
                      "slice_bytes_per_launch": roof["nsl"] * M * N + 8.0 * (M * BLOCK + N * BLOCK),
-                     "slice_gbs": dom["slice_gbs"], "launch_ms": dom["ms"],
-                     "fp64_tflops_equiv": dom["fp64_tflops_equiv"], "fp64_peak_tflops": pk["fp64_tflops"],
-                     "nn_kernel_ms": roof["nn_kernel"]["ms"], "nn_achieved": roof["nn_kernel"]["gbs"],
-                     "pass": {"what": "the whole A pass as the QB loop runs it: k_slice_z (Y) + k_ozaki + fixup",
-                              "tn_ms": roof["tn_pass"]["ms"], "tn_achieved": roof["tn_pass"]["gbs"],
-                              "nn_ms": roof["nn_pass"]["ms"], "nn_achieved": roof["nn_pass"]["gbs"]}},
+                     "fp64_tflops_equiv": 2.0 * M * N * BLOCK / live_launch_ms / 1e9,
+                     "fp64_peak_tflops": pk["fp64_tflops"],
+                     "tensor_view": tensor_view(live_launch_ms, pk),
+                     "isolated": {"what": "the same products outside the loop on the bench matrix, 6 back-to-back "
+                                          "launches each (fqb_sliced_gemm / _again)",
+                                  "tn_kernel_ms": dom["ms"], "nn_kernel_ms": roof["nn_kernel"]["ms"],
+                                  "tn_pass_ms": roof["tn_pass"]["ms"], "nn_pass_ms": roof["nn_pass"]["ms"]}},
         "sketch_roofline": sketch,
         "clocks": clk.summary(),
     }

@@ -170,6 +170,13 @@ const char* fqb_last_error(void);
 const char* fqb_status_name(int status);
 /* Kernels launched by this handle since creation (launch accounting). */
 int64_t fqb_launch_count(fqb_handle h);
+/* Live timing of the dominant kernel: while on, every A-pass k_ozaki launch (with its
+ * stream-K fixup) of this handle's runs is bracketed by CUDA events on the handle's
+ * stream.  fqb_set_pass_timing synchronizes the stream and resets the record;
+ * fqb_pass_timing synchronizes and returns the summed launch time (ms), the number of
+ * launches and their algorithmic FP64 bytes 8 (MK + KN + MN) (any pointer may be NULL). */
+fqb_status fqb_set_pass_timing(fqb_handle h, int on);
+fqb_status fqb_pass_timing(fqb_handle h, double* total_ms, int64_t* launches, double* bytes);
 
 /* ---- the QB loop ----------------------------------------------------------- */
 /* A is m x n column-major with leading dimension lda, on the device when

@@ -65,6 +65,8 @@ SIGNATURES = [
     ("fqb_last_error", C.c_char_p, []),
     ("fqb_status_name", C.c_char_p, [C.c_int]),
     ("fqb_launch_count", C.c_int64, [_H]),
+    ("fqb_set_pass_timing", C.c_int, [_H, C.c_int]),
+    ("fqb_pass_timing", C.c_int, [_H, C.POINTER(C.c_double), C.POINTER(C.c_int64), C.POINTER(C.c_double)]),
     ("fqb_qb_fixed_precision", C.c_int, [_H, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_int,
                                          C.POINTER(ConfigC), SOURCE_FN, C.c_void_p, C.c_uint,
                                          C.POINTER(ResultC)]),

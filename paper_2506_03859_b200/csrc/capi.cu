@@ -136,6 +136,7 @@ fqb_status fqb_destroy(fqb_handle h) {
         if (h->h.ev_qb) cudaEventDestroy(h->h.ev_qb);
         if (h->h.ev_u) cudaEventDestroy(h->h.ev_u);
         if (h->h.ev_v) cudaEventDestroy(h->h.ev_v);
+        for (cudaEvent_t e : h->h.pass_timer.ev) cudaEventDestroy(e);
         cudaStreamDestroy(h->h.own_stream);
         delete h;
         if (g_live_handles.fetch_sub(1) == 1) {
@@ -165,6 +166,37 @@ fqb_status fqb_synchronize(fqb_handle h) {
 int64_t fqb_launch_count(fqb_handle h) { return h ? h->h.lc.total : 0; }
 
 int64_t fqb_collective_count(fqb_handle h) { return h ? h->h.collectives : 0; }
+
+fqb_status fqb_set_pass_timing(fqb_handle h, int on) {
+    return guarded([&]() -> fqb_status {
+        if (!h) throw farqb::Error(FQB_ERR_INVALID_ARGUMENT, "null handle");
+        bind(h);
+        FQB_CUDA(cudaStreamSynchronize(h->h.stream));   // no recorded event is still pending
+        h->h.pass_timer.on = on != 0;
+        h->h.pass_timer.used = 0;
+        h->h.pass_timer.bytes = 0.0;
+        return FQB_OK;
+    });
+}
+
+fqb_status fqb_pass_timing(fqb_handle h, double* total_ms, int64_t* launches, double* bytes) {
+    return guarded([&]() -> fqb_status {
+        if (!h) throw farqb::Error(FQB_ERR_INVALID_ARGUMENT, "null handle");
+        bind(h);
+        FQB_CUDA(cudaStreamSynchronize(h->h.stream));
+        const farqb::LaunchTimer& t = h->h.pass_timer;
+        double ms = 0.0;
+        for (size_t i = 0; i + 1 < t.used; i += 2) {
+            float e = 0.f;
+            FQB_CUDA(cudaEventElapsedTime(&e, t.ev[i], t.ev[i + 1]));
+            ms += double(e);
+        }
+        if (total_ms) *total_ms = ms;
+        if (launches) *launches = int64_t(t.used / 2);
+        if (bytes) *bytes = t.bytes;
+        return FQB_OK;
+    });
+}
 
 fqb_status fqb_comm_unique_id(void* out128) {
     return guarded([&]() -> fqb_status {

@@ -7,6 +7,7 @@
 #include <stdexcept>
 #include <string>
 #include <utility>
+#include <vector>
 
 namespace farqb {
 
@@ -81,6 +82,16 @@ inline void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t sme
 struct LaunchCounter {
     int64_t total = 0;
     void bump(int n = 1) { total += n; }
+};
+
+// CUDA-event brackets around the A-pass products (k_ozaki + its fixup) of a handle's
+// runs, read back by fqb_pass_timing: the dominant kernel timed live inside a caller's
+// timed region, on the stream it runs on (ozaki.cu records, engine.cu arms it)
+struct LaunchTimer {
+    bool on = false;
+    std::vector<cudaEvent_t> ev;   // pairs
+    size_t used = 0;               // events recorded since the last reset
+    double bytes = 0.0;            // algorithmic FP64 bytes 8 (MK + KN + MN) of the timed launches
 };
 
 }  // namespace farqb

@@ -333,6 +333,12 @@ class QbRun {
         a_ld64_ = ld;
     }
 
+    // the A passes' k_ozaki launches are bracketed by the handle's pass timer when armed
+    struct PassTimerScope {
+        explicit PassTimerScope(Handle& h) { ozaki_set_timer(h.pass_timer.on ? &h.pass_timer : nullptr); }
+        ~PassTimerScope() { ozaki_set_timer(nullptr); }
+    };
+
     void a_gemm(bool ta, int N, const double* B, int64_t ldb, double* C, int64_t ldc) {
         if (!oz_on_) {
             ensure_fp64_a();
@@ -354,6 +360,7 @@ class QbRun {
         w.oz_z.ensure(size_t(ozaki_apply_z_bytes(K, oz_nsl_)), s_);
         w.oz_ez.ensure(size_t(ozaki_apply_ez_count()), s_);
         w.oz_zmax.ensure(size_t(ozaki_apply_ez_count()), s_);
+        PassTimerScope timed(h_);
         ozaki_apply(M, N, K, 1.0, ta ? w.oz_x_tn.ptr : w.oz_x_nn.ptr, ta ? w.oz_e_tn.ptr : w.oz_e_nn.ptr, B, ldb, 0.0,
                     C, ldc, w.oz_z.ptr, w.oz_ez.ptr, h_.gws.work, h_.num_sms, s_, h_.lc, oz_nsl_, w.oz_zmax.ptr);
     }
@@ -416,6 +423,7 @@ class QbRun {
         }
         Workspace& w = h_.ws;
         const int8_t* xs = w.oz_x_tn.ptr + (r0 / 128) * ozaki_x_bytes(128, m_, oz_nsl_);
+        PassTimerScope timed(h_);
         if (again && N <= 128) {
             ozaki_apply_presliced(rows, N, m_, 1.0, xs, w.oz_e_tn.ptr + r0, 0.0, C + r0, ldc, w.oz_z.ptr, w.oz_ez.ptr,
                                   h_.gws.work, h_.num_sms, s_, h_.lc, oz_nsl_);

@@ -114,6 +114,7 @@ struct Handle {
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;
     LaunchCounter lc;
+    LaunchTimer pass_timer;           // fqb_set_pass_timing
     Workspace ws;
     GemmWorkspace gws;                // views into ws.splitk / ws.gemm_flags
     unsigned* host_status = nullptr;  // pinned readback slot

@@ -126,6 +126,9 @@ int64_t ozaki_x_bytes(int64_t rows, int64_t k, int nsl = ozaki_fp64_slices());
 int64_t ozaki_z_bytes(int64_t n, int64_t k, int nsl = ozaki_fp64_slices());
 int64_t ozaki_apply_z_bytes(int64_t k, int nsl = ozaki_fp64_slices());
 // ozaki_apply's products again on the B slices its last call left in z / ez (N <= 128)
+// while set (per thread), launch_ozaki brackets each k_ozaki (+ fixup) launch with a
+// pair of events from this timer
+void ozaki_set_timer(LaunchTimer* t);
 void ozaki_apply_presliced(int64_t M, int64_t N, int64_t K, double alpha, const int8_t* xs, const int* ex, double beta,
                            double* C, int64_t ldc, const int8_t* z, const int* ez, double* work, int num_sms,
                            cudaStream_t s, LaunchCounter& lc, int nsl = ozaki_fp64_slices());

@@ -73,15 +73,16 @@ constexpr int B_TILE = OZ_BN * OZ_BK;             // 4 KB per slice (bn = 64)
 // the N = 64 lone products of the S = 56 schedule read past it)
 __host__ __device__ constexpr int z_block_rows(int nsl, int S) { return nsl * S + (S == 56 ? 8 : 0); }
 
-template <int NSL, int BS = 2, int S = 64>
+template <int NSL, int BS = 2, int S = 64, int NDK = 0>
 struct Sl {
     static constexpr int B_STAGES = BS;                                            // Z stages (2 or 3)
     static constexpr int W = (NSL == 7 || NSL == 3) ? 8 : 7;                        // bits per digit
-    static constexpr int ND = NSL == 7 ? 8 : NSL == 3 ? 4 : NSL;                     // diagonals kept
+    // diagonals kept (NDK = 7 with NSL = 7: the trimmed variant, FQB_OZ_DIAGS=7)
+    static constexpr int ND = NDK ? NDK : NSL == 7 ? 8 : NSL == 3 ? 4 : NSL;
     static constexpr int B_STAGE = z_block_rows(NSL, S) * OZ_BK;                   // 28 / 32 / 16 KB (25 KB at S = 56)
     static constexpr int A_STAGES = (225 * 1024 - B_STAGES * B_STAGE) / A_TILE;     // 21 / 20 / 24
     static constexpr size_t SMEM = size_t(A_STAGES) * A_TILE + size_t(B_STAGES) * B_STAGE + 1024;
-    static constexpr unsigned TMEM_COLS = unsigned(ND * OZ_BN);                     // 512 / 512 / 256
+    static constexpr unsigned TMEM_COLS = ND > 4 ? 512u : unsigned(ND * OZ_BN);    // a power of two: 512 / 256
     // k-blocks per TMEM accumulation (int32 headroom): a diagonal sums at most ND
     // products of |digits| <= 2^(W-1): 8 * 64^2 * 32768 = 2^30 and 7 * 128^2 * 16384 < 2^31
     static constexpr int CHUNK_KB = (W == 8 ? 16384 : 32768) / OZ_BK;
@@ -281,7 +282,7 @@ struct Walk {
 // zero or lands on diagonal 8 (columns 448..511, never read).  `init` (first k-step of an
 // accumulation) starts a diagonal at its first writer: (0, 0..6) for diagonals 0..6,
 // (1, 6) for diagonal 7 (issued after (0, 6), whose spill into diagonal 7 is zero).
-template <int SP>
+template <int SP, int ND>
 __device__ __forceinline__ void issue_s56(unsigned tmem, unsigned da_lo, unsigned db_lo, unsigned d_hi,
                                           unsigned idesc, bool init) {
     constexpr unsigned kstep = 32 >> 4;
@@ -292,6 +293,18 @@ __device__ __forceinline__ void issue_s56(unsigned tmem, unsigned da_lo, unsigne
         umma_i8(dt, da_lo, bl, d_hi, id, (first_writer && init) ? 0u : 1u);
         umma_i8(dt, da_lo + kstep, bl + kstep, d_hi, id, 1u);
     };
+    if constexpr (ND == 7) {
+        // diagonals 0..6 only (p + q <= 6: 28 products in 11 MMAs); every diagonal starts
+        // with SP = 0, and the N = 64 spills land on diagonal 7, which is never read
+        if constexpr (SP == 0) { mma(0, 224, true); mma(4, 112, true); mma(6, 64, true); }
+        else if constexpr (SP == 1) { mma(0, 224, false); mma(4, 112, false); }
+        else if constexpr (SP == 2) { mma(0, 224, false); mma(4, 64, false); }
+        else if constexpr (SP == 3) { mma(0, 224, false); }
+        else if constexpr (SP == 4) { mma(0, 112, false); mma(2, 64, false); }
+        else if constexpr (SP == 5) { mma(0, 112, false); }
+        else { mma(0, 64, false); }
+        return;
+    }
     if constexpr (SP == 0) { mma(0, 224, true); mma(4, 112, true); mma(6, 64, true); }
     else if constexpr (SP == 1) { mma(0, 224, false); mma(4, 112, false); mma(6, 64, true); }
     else if constexpr (SP == 2) { mma(0, 224, false); mma(4, 112, false); }
@@ -301,13 +314,15 @@ __device__ __forceinline__ void issue_s56(unsigned tmem, unsigned da_lo, unsigne
     else { mma(0, 112, false); }
 }
 
-template <bool PAIR, int NSL, int BS, int S>
+template <bool PAIR, int NSL, int BS, int S, int NDK = 0>
 __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
+    using SL = Sl<NSL, BS, S, NDK>;
     static_assert(S == 64 || (S == 56 && NSL == 7), "the 56-row spacing is scheduled for 7 slices");
-    constexpr int A_STAGES = Sl<NSL, BS, S>::A_STAGES;
-    constexpr int B_STAGES = Sl<NSL, BS, S>::B_STAGES;
-    constexpr int B_STAGE = Sl<NSL, BS, S>::B_STAGE;
-    constexpr int ND = Sl<NSL, BS, S>::ND, CHUNK_KB = Sl<NSL, BS, S>::CHUNK_KB;
+    static_assert(NDK == 0 || (NDK == 7 && NSL == 7 && S == 56), "the trimmed variant is scheduled for S = 56");
+    constexpr int A_STAGES = SL::A_STAGES;
+    constexpr int B_STAGES = SL::B_STAGES;
+    constexpr int B_STAGE = SL::B_STAGE;
+    constexpr int ND = SL::ND, CHUNK_KB = SL::CHUNK_KB;
     FQB_PDL_ENTRY();
     extern __shared__ uint8_t smem_raw[];
     __shared__ uint64_t bars[2 * A_STAGES + 2 * B_STAGES + 2];
@@ -344,7 +359,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
     if (threadIdx.x < OZ_BN) ez_s[threadIdx.x] = int(threadIdx.x) < q_N ? q_ez[threadIdx.x] : 0;
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
-            smem_u32(&tmem_base_s)), "n"(Sl<NSL, BS, S>::TMEM_COLS));
+            smem_u32(&tmem_base_s)), "n"(SL::TMEM_COLS));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n");
@@ -430,13 +445,13 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
                             // the top diagonal ND-1 starts with (ND-NSL, NSL-1), issued alone.
                             if constexpr (S == 56) {
                                 const bool init = kb == cb;
-                                if (sp == 0) issue_s56<0>(tmem, da_lo, db_lo, d_hi, idesc, init);
-                                else if (sp == 1) issue_s56<1>(tmem, da_lo, db_lo, d_hi, idesc, init);
-                                else if (sp == 2) issue_s56<2>(tmem, da_lo, db_lo, d_hi, idesc, init);
-                                else if (sp == 3) issue_s56<3>(tmem, da_lo, db_lo, d_hi, idesc, init);
-                                else if (sp == 4) issue_s56<4>(tmem, da_lo, db_lo, d_hi, idesc, init);
-                                else if (sp == 5) issue_s56<5>(tmem, da_lo, db_lo, d_hi, idesc, init);
-                                else issue_s56<6>(tmem, da_lo, db_lo, d_hi, idesc, init);
+                                if (sp == 0) issue_s56<0, ND>(tmem, da_lo, db_lo, d_hi, idesc, init);
+                                else if (sp == 1) issue_s56<1, ND>(tmem, da_lo, db_lo, d_hi, idesc, init);
+                                else if (sp == 2) issue_s56<2, ND>(tmem, da_lo, db_lo, d_hi, idesc, init);
+                                else if (sp == 3) issue_s56<3, ND>(tmem, da_lo, db_lo, d_hi, idesc, init);
+                                else if (sp == 4) issue_s56<4, ND>(tmem, da_lo, db_lo, d_hi, idesc, init);
+                                else if (sp == 5) issue_s56<5, ND>(tmem, da_lo, db_lo, d_hi, idesc, init);
+                                else issue_s56<6, ND>(tmem, da_lo, db_lo, d_hi, idesc, init);
                                 if constexpr (PAIR) umma_commit_mc2(a_empty + 8 * sa);
                                 else umma_commit(a_empty + 8 * sa);
                                 if (++sa == A_STAGES) sa = 0, pa ^= 1u;
@@ -515,7 +530,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
                     // least significant diagonal first: d = ND-1 .. 0 (scale 2^(-12-W d))
 #pragma unroll
                     for (int d = ND - 1; d >= 0; --d) {
-                        const double sc = pow2i(-12 - Sl<NSL, BS, S>::W * d);
+                        const double sc = pow2i(-12 - SL::W * d);
 #pragma unroll
                         for (int j = 0; j < 16; ++j) acc[j] = fma(double(int(v[d][j])), sc, acc[j]);
                     }
@@ -560,7 +575,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
     if constexpr (PAIR) cluster_sync();   // no CTA leaves while its peer may still arrive on its barriers
     if (warp == 1)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
-                     "n"(Sl<NSL, BS, S>::TMEM_COLS));
+                     "n"(SL::TMEM_COLS));
 }
 
 // ---------------------------------------------------------------------------
@@ -1071,20 +1086,20 @@ void ozaki_slice_z(const double* b, int64_t k, int64_t n, int64_t ld, int* e, in
 }
 
 // paired (pair_cw > 0): N = 2 chunks of pair_cw columns at most, zs / ez hold both
-template <bool PAIR, int NSL, int BS, int S = 64>
+template <bool PAIR, int NSL, int BS, int S = 64, int NDK = 0>
 static void launch_variant(const OzArgs& a, cudaStream_t s) {
     static bool configured[64] = {};
     int dev = 0;
     FQB_CUDA(cudaGetDevice(&dev));
     if (dev < 0 || dev >= 64 || !configured[dev]) {
-        FQB_CUDA(cudaFuncSetAttribute(k_ozaki<PAIR, NSL, BS, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      int(Sl<NSL, BS, S>::SMEM)));
+        FQB_CUDA(cudaFuncSetAttribute(k_ozaki<PAIR, NSL, BS, S, NDK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(Sl<NSL, BS, S, NDK>::SMEM)));
         if (dev >= 0 && dev < 64) configured[dev] = true;
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(unsigned(PAIR ? 2 * a.grid : a.grid));
     cfg.blockDim = dim3(OZ_THREADS);
-    cfg.dynamicSmemBytes = Sl<NSL, BS, S>::SMEM;
+    cfg.dynamicSmemBytes = Sl<NSL, BS, S, NDK>::SMEM;
     cfg.stream = s;
     cudaLaunchAttribute attr[2];
     int na = 0;
@@ -1102,7 +1117,7 @@ static void launch_variant(const OzArgs& a, cudaStream_t s) {
     }
     cfg.attrs = attr;
     cfg.numAttrs = na;
-    FQB_CUDA(cudaLaunchKernelEx(&cfg, k_ozaki<PAIR, NSL, BS, S>, a));
+    FQB_CUDA(cudaLaunchKernelEx(&cfg, k_ozaki<PAIR, NSL, BS, S, NDK>, a));
 }
 
 // A/B switches of the A-pass kernel (read once): FQB_OZ_L2HINT=0 plain bulk copies,
@@ -1127,14 +1142,33 @@ static int z_spacing(int64_t cw, int nsl) {
 }
 static int64_t z_chunk_bytes(int64_t K, int nsl, int S) { return ceil_div(K, OZ_BK) * z_block_rows(nsl, S) * OZ_BK; }
 
+// FQB_OZ_DIAGS=7: the 7-slice scheme keeps diagonals p + q <= 6 only (28 of 34 products,
+// S = 56 chunks); see the DESIGN note on its error.  Default 8 (all d <= 7).
+static int diags_default() {
+    static const int v = env_int("FQB_OZ_DIAGS", 8) == 7 ? 7 : 8;
+    return v;
+}
+
 template <bool PAIR>
 static void launch_pair_or_not(const OzArgs& a, int nsl, int S, cudaStream_t s) {
-    if (nsl == 7 && S == 56) launch_variant<PAIR, 7, 2, 56>(a, s);
+    if (nsl == 7 && S == 56 && diags_default() == 7) launch_variant<PAIR, 7, 2, 56, 7>(a, s);
+    else if (nsl == 7 && S == 56) launch_variant<PAIR, 7, 2, 56>(a, s);
     else if (nsl == 8) launch_variant<PAIR, 8, 2>(a, s);
     else if (nsl == 7 && zstages_default() == 3) launch_variant<PAIR, 7, 3>(a, s);
     else if (nsl == 7) launch_variant<PAIR, 7, 2>(a, s);
     else if (nsl == 3) launch_variant<PAIR, 3, 2>(a, s);
     else launch_variant<PAIR, 4, 2>(a, s);
+}
+
+static thread_local LaunchTimer* t_timer = nullptr;
+void ozaki_set_timer(LaunchTimer* t) { t_timer = t; }
+static cudaEvent_t timer_event(LaunchTimer* t) {
+    if (t->used == t->ev.size()) {
+        cudaEvent_t e;
+        FQB_CUDA(cudaEventCreate(&e));
+        t->ev.push_back(e);
+    }
+    return t->ev[t->used++];
 }
 
 static void launch_ozaki(int64_t M, int64_t N, int64_t K, double alpha, const int8_t* xs, const int* ex,
@@ -1169,6 +1203,8 @@ static void launch_ozaki(int64_t M, int64_t N, int64_t K, double alpha, const in
     a.zs_stride = z_chunk_bytes(K, nsl, S);
     a.work_stride = 3 * int64_t(a.grid) * OZ_PARTIAL;
     a.l2hint = l2hint_default();
+    LaunchTimer* const tm = (t_timer && t_timer->on) ? t_timer : nullptr;
+    if (tm) FQB_CUDA(cudaEventRecord(timer_event(tm), s));
     if (pair) launch_pair_or_not<true>(a, nsl, S, s);
     else launch_pair_or_not<false>(a, nsl, S, s);
     FQB_LAUNCHED();
@@ -1181,6 +1217,10 @@ static void launch_ozaki(int64_t M, int64_t N, int64_t K, double alpha, const in
                  0, s, a);
         FQB_LAUNCHED();
         lc.bump();
+    }
+    if (tm) {
+        FQB_CUDA(cudaEventRecord(timer_event(tm), s));
+        tm->bytes += 8.0 * (double(M) * double(K) + double(K) * double(N) + double(M) * double(N));
     }
 }
 

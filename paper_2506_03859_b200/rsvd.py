@@ -396,6 +396,21 @@ class Engine:
     def collective_count(self) -> int:
         return self._lib.fqb_collective_count(self._h)
 
+    def set_pass_timing(self, on: bool = True) -> None:
+        """Arm (and reset) the CUDA-event timing of the A-pass k_ozaki launches
+        (fqb_set_pass_timing)."""
+        st = self._lib.fqb_set_pass_timing(self._h, 1 if on else 0)
+        if st:
+            _raise(st, "fqb_set_pass_timing")
+
+    def pass_timing(self) -> tuple[float, int, float]:
+        """(summed launch ms, launches, algorithmic FP64 bytes) since set_pass_timing."""
+        ms, n, by = C.c_double(), C.c_int64(), C.c_double()
+        st = self._lib.fqb_pass_timing(self._h, C.byref(ms), C.byref(n), C.byref(by))
+        if st:
+            _raise(st, "fqb_pass_timing")
+        return ms.value, n.value, by.value
+
     def attach_comm(self, group=None, backend: str = "nccl") -> None:
         """Row-sharded mode: subsequent runs take this rank's row block of A
         (see paper_2506_03859_b200.dist.partition_rows).  backend "nccl": the engine's

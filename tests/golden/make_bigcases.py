@@ -40,6 +40,10 @@ CASES = {
     # sparse Gaussian zeta = 8, b = 100, P = 2, eps = 1e-3 relative
     "c4": dict(m=100000, n=20000, sigma=("pow10", 2000, 3.0), noise=0.0, kind=SPARSE_GAUSSIAN, zeta=8, block=100,
                power=2, eps=1e-3, max_iters=0),
+    # config 4's matrix with the reference's own default StdBernoulli (p = ln n / n, sparse and
+    # centered: z = p A 1 and B's row sums in every product), b = 100, P = 1, first 4 blocks
+    "c4sb": dict(m=100000, n=20000, sigma=("pow10", 2000, 3.0), noise=0.0, kind=2, zeta=0, block=100,
+                 power=1, eps=1e-3, max_iters=4),
     # BASELINE configs[2]: 20000^2, rank-1000 signal sigma_i = (1+i)^-1.5 (i = 0..999) + 1e-4 N(0,1)/sqrt(n),
     # sparse sign zeta = 8, b = 64, P = 1, eps = 1e-2; unreachable, so capped at 6 blocks
     "c3": dict(m=20000, n=20000, sigma=("inv15", 1000), noise=1e-4, kind=SPARSE_SIGN, zeta=8, block=64, power=1,
@@ -65,6 +69,14 @@ def det_lib():
     return lib
 
 
+def port_default_density(kind: int, n: int) -> float:
+    """driver.cpp:449-455 (the oracle port's fqo_default_density)."""
+    lib = C.CDLL(PORT_LIB)
+    lib.fqo_default_density.restype = C.c_double
+    lib.fqo_default_density.argtypes = [C.c_int, C.c_int]
+    return float(lib.fqo_default_density(kind, n))
+
+
 def noise_scale(case) -> float:
     return float(case["noise"]) / float(np.sqrt(case["n"])) if case["noise"] else 0.0
 
@@ -88,8 +100,10 @@ def make(name: str) -> dict:
     port = Oracle("port")
     ref = Oracle("reference")
 
+    p_eff = 0.0 if case["zeta"] else port_default_density(case["kind"], n)
+
     def src(nn, bb, bid):
-        return port.gen_sketch(case["kind"], 0.0, SEED_OMEGA, nn, bb, bid, zeta=case["zeta"])
+        return port.gen_sketch(case["kind"], p_eff, SEED_OMEGA, nn, bb, bid, zeta=case["zeta"])
 
     t0 = time.perf_counter()
     res = ref.run(a, eps=case["eps"], power=case["power"], block=case["block"], kind=case["kind"], seed=SEED_OMEGA,
@@ -122,7 +136,7 @@ def make(name: str) -> dict:
     return {
         "case": name, "m": m, "n": n, "sigma_spec": list(case["sigma"]), "noise": case["noise"],
         "noise_scale": noise_scale(case), "seed_a": SEED_A, "seed_omega": SEED_OMEGA, "kind": case["kind"],
-        "zeta": case["zeta"], "block": case["block"], "power": case["power"], "eps": case["eps"],
+        "zeta": case["zeta"], "p": p_eff, "block": case["block"], "power": case["power"], "eps": case["eps"],
         "max_iters": case["max_iters"],
         "checksum": f"{csum:016x}", "a_samples": {"i": si.tolist(), "j": sj.tolist(), "v": samples},
         "status": res.status, "rank": res.rank, "blocks": res.blocks, "converged": res.converged,

@@ -125,3 +125,10 @@ def test_c4_matches_reference():
     g = _load("c4")
     res = _check_against_golden(g)
     assert res.converged
+
+
+def test_c4_default_stdbernoulli_capped_matches_reference():
+    """Config 4's matrix with the reference's default StdBernoulli (p = ln n / n: sparse and
+    centered -- the path round 1 got wrong), b = 100, P = 1, the first 4 blocks."""
+    g = _load("c4sb")
+    _check_against_golden(g)

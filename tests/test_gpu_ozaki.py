@@ -173,6 +173,25 @@ def test_qb_with_emulation_matches_oracle(eng, port, monkeypatch, kind, zeta, po
     assert np.max(np.abs(res.block_residuals - ref.block_residuals)) <= 1e-10 * na
 
 
+def test_pass_timing_counts_the_a_passes(eng, monkeypatch):
+    """fqb_set_pass_timing / fqb_pass_timing (the bench's live roofline timing): one event
+    pair per A-pass k_ozaki launch -- 2P + 1 per block with a sparse Omega (P = 2: 5), the
+    b = 100 block as one paired launch -- and 8 (MK + Kb + Mb) algorithmic bytes each."""
+    monkeypatch.setenv("FQB_OZAKI", "1")
+    m, n, b = 900, 700, 100
+    a = _lowrank(m, n, 1.0 / np.arange(1, 251) ** 1.5, seed=5)
+    cfg = FarpcaConfig(eps=1e-2, power=2, block=b, sketch=SketchSpec(4, 0.0, 13, zeta=8), relative=True)
+    eng.set_pass_timing(True)
+    res = eng.run_fixed_precision(a, cfg, output="host")
+    ms, launches, nbytes = eng.pass_timing()
+    eng.set_pass_timing(False)
+    assert launches == 5 * res.blocks
+    assert nbytes == pytest.approx(launches * 8.0 * (m * n + (m + n) * b), rel=1e-12)
+    assert ms > 0.0
+    eng.run_fixed_precision(a, cfg, output="host")            # disarmed: nothing more is recorded
+    assert eng.pass_timing()[1] == 0
+
+
 def test_emulation_on_and_off_agree(eng, monkeypatch):
     a = _lowrank(1500, 1200, 0.97 ** np.arange(300), seed=77)
     cfg = FarpcaConfig(eps=1e-3, power=2, block=40, sketch=SketchSpec(2, 0.5, 5), relative=True)
