@@ -36,8 +36,9 @@
 // flight), one MMA warp (tcgen05.mma.cta_group::1.kind::i8, M=128, K=32, N = 64
 // per Z slice: the products of one A slice with up to 4 consecutive Z slices
 // land on consecutive TMEM diagonals, so one N<=256 MMA covers them and A is
-// read from shared memory once per 4 products), four epilogue warps
-// (tcgen05.ld 32x32b -> FP64).  Tiles are split over the persistent grid
+// read from shared memory once per 4 products; chunks of <= 56 columns use 56-row Z
+// slices and the wide schedule of issue_s56: 12 MMAs of N <= 256 per k-step for all 34
+// products), four epilogue warps (tcgen05.ld 32x32b -> FP64).  Tiles are split over the persistent grid
 // stream-K style; a CTA writes pieces of split tiles, already scaled, to its
 // partial slots and k_ozaki_fixup sums them in CTA order (deterministic).
 //
@@ -282,10 +283,39 @@ struct Walk {
 // zero or lands on diagonal 8 (columns 448..511, never read).  `init` (first k-step of an
 // accumulation) starts a diagonal at its first writer: (0, 0..6) for diagonals 0..6,
 // (1, 6) for diagonal 7 (issued after (0, 6), whose spill into diagonal 7 is zero).
-template <int SP, int ND>
+//
+// WIDE (the default; FQB_OZ_WIDE=0 for the schedule above): the same products in fewer, wider MMAs -- a slice's Z rows are
+// covered by N = 256 MMAs split at row 256 (a swizzle-atom boundary inside slice 4), so
+// A is read from shared memory 12 (ND = 8) / 10 (ND = 7) times per k-step instead of
+// 14 / 11.  Spilled rows (past the slices a product needs) land on diagonal 8 (ND = 8) or
+// 7 (ND = 7), never read; diagonal 7 of ND = 8 starts with its own lone MMA in SP = 1.
+template <int SP, int ND, bool WIDE>
 __device__ __forceinline__ void issue_s56(unsigned tmem, unsigned da_lo, unsigned db_lo, unsigned d_hi,
                                           unsigned idesc, bool init) {
     constexpr unsigned kstep = 32 >> 4;
+    if constexpr (WIDE) {
+        // rows [r0, r0 + n) of the Z stage -> TMEM columns 56 SP + r0 ..
+        auto mmr = [&](int r0, int n, bool first_writer) {
+            const unsigned id = idesc | (unsigned(n >> 3) << 17);
+            const unsigned dt = tmem + unsigned(SP * 56 + r0);
+            const unsigned bl = db_lo + unsigned((r0 * OZ_BK) >> 4);
+            umma_i8(dt, da_lo, bl, d_hi, id, (first_writer && init) ? 0u : 1u);
+            umma_i8(dt, da_lo + kstep, bl + kstep, d_hi, id, 1u);
+        };
+        if constexpr (SP == 0) { mmr(0, 256, true); mmr(256, 144, true); }
+        else if constexpr (SP == 1) {
+            mmr(0, 256, false);
+            mmr(256, 80, false);
+            if constexpr (ND == 8) mmr(336, 64, true);
+        } else if constexpr (SP == 2) { mmr(0, 256, false); mmr(256, ND == 8 ? 80 : 32, false); }
+        else if constexpr (SP == 3) {
+            if constexpr (ND == 8) { mmr(0, 256, false); mmr(256, 32, false); }
+            else mmr(0, 224, false);
+        } else if constexpr (SP == 4) mmr(0, ND == 8 ? 224 : 176, false);
+        else if constexpr (SP == 5) mmr(0, ND == 8 ? 176 : 112, false);
+        else mmr(0, ND == 8 ? 112 : 64, false);
+        return;
+    }
     auto mma = [&](int q0, int n, bool first_writer) {
         const unsigned id = idesc | (unsigned(n >> 3) << 17);
         const unsigned dt = tmem + unsigned((SP + q0) * 56);
@@ -314,7 +344,7 @@ __device__ __forceinline__ void issue_s56(unsigned tmem, unsigned da_lo, unsigne
     else { mma(0, 112, false); }
 }
 
-template <bool PAIR, int NSL, int BS, int S, int NDK = 0>
+template <bool PAIR, int NSL, int BS, int S, int NDK = 0, bool WIDE = false>
 __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
     using SL = Sl<NSL, BS, S, NDK>;
     static_assert(S == 64 || (S == 56 && NSL == 7), "the 56-row spacing is scheduled for 7 slices");
@@ -445,13 +475,13 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
                             // the top diagonal ND-1 starts with (ND-NSL, NSL-1), issued alone.
                             if constexpr (S == 56) {
                                 const bool init = kb == cb;
-                                if (sp == 0) issue_s56<0, ND>(tmem, da_lo, db_lo, d_hi, idesc, init);
-                                else if (sp == 1) issue_s56<1, ND>(tmem, da_lo, db_lo, d_hi, idesc, init);
-                                else if (sp == 2) issue_s56<2, ND>(tmem, da_lo, db_lo, d_hi, idesc, init);
-                                else if (sp == 3) issue_s56<3, ND>(tmem, da_lo, db_lo, d_hi, idesc, init);
-                                else if (sp == 4) issue_s56<4, ND>(tmem, da_lo, db_lo, d_hi, idesc, init);
-                                else if (sp == 5) issue_s56<5, ND>(tmem, da_lo, db_lo, d_hi, idesc, init);
-                                else issue_s56<6, ND>(tmem, da_lo, db_lo, d_hi, idesc, init);
+                                if (sp == 0) issue_s56<0, ND, WIDE>(tmem, da_lo, db_lo, d_hi, idesc, init);
+                                else if (sp == 1) issue_s56<1, ND, WIDE>(tmem, da_lo, db_lo, d_hi, idesc, init);
+                                else if (sp == 2) issue_s56<2, ND, WIDE>(tmem, da_lo, db_lo, d_hi, idesc, init);
+                                else if (sp == 3) issue_s56<3, ND, WIDE>(tmem, da_lo, db_lo, d_hi, idesc, init);
+                                else if (sp == 4) issue_s56<4, ND, WIDE>(tmem, da_lo, db_lo, d_hi, idesc, init);
+                                else if (sp == 5) issue_s56<5, ND, WIDE>(tmem, da_lo, db_lo, d_hi, idesc, init);
+                                else issue_s56<6, ND, WIDE>(tmem, da_lo, db_lo, d_hi, idesc, init);
                                 if constexpr (PAIR) umma_commit_mc2(a_empty + 8 * sa);
                                 else umma_commit(a_empty + 8 * sa);
                                 if (++sa == A_STAGES) sa = 0, pa ^= 1u;
@@ -1086,13 +1116,13 @@ void ozaki_slice_z(const double* b, int64_t k, int64_t n, int64_t ld, int* e, in
 }
 
 // paired (pair_cw > 0): N = 2 chunks of pair_cw columns at most, zs / ez hold both
-template <bool PAIR, int NSL, int BS, int S = 64, int NDK = 0>
+template <bool PAIR, int NSL, int BS, int S = 64, int NDK = 0, bool WIDE = false>
 static void launch_variant(const OzArgs& a, cudaStream_t s) {
     static bool configured[64] = {};
     int dev = 0;
     FQB_CUDA(cudaGetDevice(&dev));
     if (dev < 0 || dev >= 64 || !configured[dev]) {
-        FQB_CUDA(cudaFuncSetAttribute(k_ozaki<PAIR, NSL, BS, S, NDK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        FQB_CUDA(cudaFuncSetAttribute(k_ozaki<PAIR, NSL, BS, S, NDK, WIDE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       int(Sl<NSL, BS, S, NDK>::SMEM)));
         if (dev >= 0 && dev < 64) configured[dev] = true;
     }
@@ -1117,7 +1147,7 @@ static void launch_variant(const OzArgs& a, cudaStream_t s) {
     }
     cfg.attrs = attr;
     cfg.numAttrs = na;
-    FQB_CUDA(cudaLaunchKernelEx(&cfg, k_ozaki<PAIR, NSL, BS, S, NDK>, a));
+    FQB_CUDA(cudaLaunchKernelEx(&cfg, k_ozaki<PAIR, NSL, BS, S, NDK, WIDE>, a));
 }
 
 // A/B switches of the A-pass kernel (read once): FQB_OZ_L2HINT=0 plain bulk copies,
@@ -1149,10 +1179,20 @@ static int diags_default() {
     return v;
 }
 
+// the S = 56 schedule in wide MMAs (default; FQB_OZ_WIDE=0: the 14-MMA schedule).  The
+// int32 sums are exact either way, so both give identical bits.
+static bool wide_default() {
+    static const bool v = env_int("FQB_OZ_WIDE", 1) != 0;
+    return v;
+}
+
 template <bool PAIR>
 static void launch_pair_or_not(const OzArgs& a, int nsl, int S, cudaStream_t s) {
-    if (nsl == 7 && S == 56 && diags_default() == 7) launch_variant<PAIR, 7, 2, 56, 7>(a, s);
-    else if (nsl == 7 && S == 56) launch_variant<PAIR, 7, 2, 56>(a, s);
+    const bool s56 = nsl == 7 && S == 56;
+    if (s56 && diags_default() == 7 && wide_default()) launch_variant<PAIR, 7, 2, 56, 7, true>(a, s);
+    else if (s56 && diags_default() == 7) launch_variant<PAIR, 7, 2, 56, 7>(a, s);
+    else if (s56 && wide_default()) launch_variant<PAIR, 7, 2, 56, 0, true>(a, s);
+    else if (s56) launch_variant<PAIR, 7, 2, 56>(a, s);
     else if (nsl == 8) launch_variant<PAIR, 8, 2>(a, s);
     else if (nsl == 7 && zstages_default() == 3) launch_variant<PAIR, 7, 3>(a, s);
     else if (nsl == 7) launch_variant<PAIR, 7, 2>(a, s);
