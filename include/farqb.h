@@ -351,6 +351,13 @@ fqb_status fqb_sliced_gemm(fqb_handle h, fqb_sliced s, int trans_a, int64_t nb, 
  * (k_ozaki, + the stream-K fixup when a tile is split) runs, no slicing of B.  For
  * repeated products with one B, and for timing the GEMM kernel by itself. */
 fqb_status fqb_sliced_gemm_again(fqb_handle h, fqb_sliced s, double alpha, double beta, double* c, int64_t ldc);
+/* C (m x nb) = alpha A B + beta C (B n x nb) computed from the A'Y-layout slices alone,
+ * read MN-major by the kernel (B's rows are first scaled by A's column scales) -- the
+ * product the engine's block Gram-Schmidt uses for Y -= Q C on the slices of Q its
+ * Q'Y products made.  Same accuracy class as fqb_sliced_gemm(trans_a = 0), different
+ * rounding (per-column instead of per-row scales of A). */
+fqb_status fqb_sliced_gemm_mn(fqb_handle h, fqb_sliced s, int64_t nb, double alpha, const double* b, int64_t ldb,
+                              double beta, double* c, int64_t ldc);
 fqb_status fqb_sliced_free(fqb_handle h, fqb_sliced s);
 
 /* ---- test matrices on the device (reference synthetic.cpp) ----- */

@@ -127,6 +127,8 @@ SIGNATURES = [
                                   C.c_double, C.c_void_p, C.c_int64]),
     ("fqb_sliced_free", C.c_int, [_H, C.c_void_p]),
     ("fqb_sliced_gemm_again", C.c_int, [_H, C.c_void_p, C.c_double, C.c_double, C.c_void_p, C.c_int64]),
+    ("fqb_sliced_gemm_mn", C.c_int, [_H, C.c_void_p, C.c_int64, C.c_double, C.c_void_p, C.c_int64, C.c_double,
+                                     C.c_void_p, C.c_int64]),
     ("fqb_default_density", C.c_double, [C.c_int, C.c_int64]),
     ("fqb_default_block", C.c_int, [C.c_int64, C.c_int64]),
     ("fqb_default_max_iters", C.c_int, [C.c_int64, C.c_int]),

@@ -553,6 +553,7 @@ struct fqb_sliced_s {
     farqb::DeviceArray<int8_t> x_nn, x_tn, z;
     farqb::DeviceArray<int> e_nn, e_tn, ez;
     farqb::DeviceArray<unsigned> zmax;
+    farqb::DeviceArray<double> cs;   // fqb_sliced_gemm_mn: B with its rows scaled by A's column scales
     int last_trans = -1;   // the last fqb_sliced_gemm: B slices left in z / ez
     int64_t last_nb = 0;
 };
@@ -608,6 +609,28 @@ fqb_status fqb_sliced_gemm(fqb_handle h, fqb_sliced sl, int trans_a, int64_t nb,
                            h->h.gws.work, h->h.num_sms, s, h->h.lc, farqb::ozaki_fp64_slices(), sl->zmax.ptr);
         sl->last_trans = trans_a ? 1 : 0;
         sl->last_nb = nb;
+        return FQB_OK;
+    });
+}
+
+fqb_status fqb_sliced_gemm_mn(fqb_handle h, fqb_sliced sl, int64_t nb, double alpha, const double* b, int64_t ldb,
+                              double beta, double* c, int64_t ldc) {
+    return guarded([&]() -> fqb_status {
+        bind(h);
+        if (!sl) throw farqb::Error(FQB_ERR_INVALID_ARGUMENT, "null sliced operand");
+        if (nb < 0) throw farqb::Error(FQB_ERR_DIMENSION, "fqb_sliced_gemm_mn: negative nb");
+        const int64_t M = sl->m, K = sl->n;
+        if (ldb < K || ldc < M) throw farqb::Error(FQB_ERR_DIMENSION, "leading dimension too small");
+        if (nb == 0) return FQB_OK;
+        cudaStream_t s = h->h.stream;
+        farqb::ensure_gemm_workspace(h->h);
+        sl->z.ensure(size_t(farqb::ozaki_apply_z_bytes(K)), s);
+        sl->zmax.ensure(size_t(farqb::ozaki_apply_ez_count()), s);
+        sl->cs.ensure(size_t(K) * size_t(nb), s);
+        farqb::ozaki_apply_mn(M, nb, K, alpha, sl->x_tn.ptr, sl->e_tn.ptr, b, ldb, beta, c, ldc, sl->cs.ptr,
+                              sl->z.ptr, sl->ez.ptr, h->h.gws.work, h->h.num_sms, s, h->h.lc,
+                              farqb::ozaki_fp64_slices(), sl->zmax.ptr);
+        sl->last_trans = -1;   // z holds the scaled B's slices: no fqb_sliced_gemm_again after this
         return FQB_OK;
     });
 }

@@ -458,6 +458,26 @@ class QbRun {
         }();
         return q_oz_on_ && min_cols > 0 && l >= min_cols;
     }
+    // the projections Y -= Q C (K = l) on the INT8 path reading the A'Y-layout slices of Q
+    // (the ones slice_q made for Q'Y) MN-major, C's rows scaled by Q's column scales --
+    // nothing is re-sliced.  FQB_OZ_QMN=0 keeps them on DMMA.
+    bool use_q_mn(int64_t l) const {
+        static const bool on = [] {
+            const char* e = std::getenv("FQB_OZ_QMN");
+            return !(e && e[0] == '0');
+        }();
+        return on && use_q_oz(l);
+    }
+    void q_mn_sub(int64_t l, const double* Cm, int64_t ldcm, double* Y) {   // Y (m x b) -= Q(:, :l) Cm
+        Workspace& w = h_.ws;
+        const int nsl = ozaki_fp64_slices();
+        w.oz_z.ensure(size_t(std::max(ozaki_apply_z_bytes(m_, nsl), ozaki_apply_z_bytes(l, nsl))), s_);
+        w.oz_ez.ensure(size_t(ozaki_apply_ez_count()), s_);
+        w.oz_zmax.ensure(size_t(ozaki_apply_ez_count()), s_);
+        w.oz_q_cs.ensure(size_t(l) * size_t(b_), s_);
+        ozaki_apply_mn(m_, b_, l, -1.0, w.oz_q_tn.ptr, w.oz_q_e.ptr, Cm, ldcm, 1.0, Y, ldq_, w.oz_q_cs.ptr,
+                       w.oz_z.ptr, w.oz_ez.ptr, h_.gws.work, h_.num_sms, s_, h_.lc, nsl, w.oz_zmax.ptr);
+    }
     // slices of q_ columns [floor(q_sliced_ / 128) * 128, upto): every committed column not
     // sliced yet, the current block's Y_j, and the rest of the 128-column tile they start in
     void slice_q(int64_t upto) {
@@ -707,7 +727,9 @@ class QbRun {
                                   w.scratch.ptr, status_, kStAcceptPivot, s_, h_.lc);
             gemm_(false, m_, b, b, 1.0, yj, ldq_, R1i_, b, 0.0, w.ys.ptr, ldq_);
         } else {
-            if (use_q_oz_nn(l)) {
+            if (use_q_mn(l)) {
+                q_mn_sub(l, cd, ldcd, yj);
+            } else if (use_q_oz_nn(l)) {
                 slice_q_nn(l);
                 q_nn_sub(l, cd, ldcd, yj);
             } else {
@@ -721,7 +743,8 @@ class QbRun {
             if (use_q_oz(l)) q_tn(l, w.ys.ptr, w.c2.ptr, l);
             else gemm_(true, l, b, m_, 1.0, q_.ptr, ldq_, w.ys.ptr, ldq_, 0.0, w.c2.ptr, l);
             comm_allreduce_sum(h_, w.c2.ptr, size_t(l) * b, s_);
-            if (use_q_oz_nn(l)) q_nn_sub(l, w.c2.ptr, l, w.ys.ptr);
+            if (use_q_mn(l)) q_mn_sub(l, w.c2.ptr, l, w.ys.ptr);
+            else if (use_q_oz_nn(l)) q_nn_sub(l, w.c2.ptr, l, w.ys.ptr);
             else gemm_(false, m_, b, l, -1.0, q_.ptr, ldq_, w.c2.ptr, l, 1.0, w.ys.ptr, ldq_);
         }
         gemm_(true, b, b, m_, 1.0, w.ys.ptr, ldq_, w.ys.ptr, ldq_, 0.0, S2_, b);

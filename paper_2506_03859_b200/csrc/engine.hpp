@@ -78,7 +78,7 @@ struct DeviceArray {
 // Per-handle reusable workspace (everything except the Q and B' outputs).
 struct Workspace {
     DeviceArray<double> omega, y0, ys, wp, wraw, g, t, cd, c2, small, zc, rowsum_b, splitk, partial,
-        scalars, scratch, a_copy, oz_norm_partial, w_half;
+        scalars, scratch, a_copy, oz_norm_partial, w_half, oz_q_cs;
     DeviceArray<float> a_copy_f32;   // FP32 input mode staging
     DeviceArray<int> col_ptr, row_idx, counts;
     DeviceArray<double> values;
@@ -98,7 +98,7 @@ struct Workspace {
     // every member, while the stream the frees are ordered on still exists
     void release_all() {
         for (auto* d : {&omega, &y0, &ys, &wp, &wraw, &g, &t, &cd, &c2, &small, &zc, &rowsum_b, &splitk, &partial,
-                        &scalars, &scratch, &a_copy, &values, &oz_norm_partial, &w_half})
+                        &scalars, &scratch, &a_copy, &values, &oz_norm_partial, &w_half, &oz_q_cs})
             d->release();
         for (auto* d : {&col_ptr, &row_idx, &counts, &oz_e_nn, &oz_e_tn, &oz_ez, &oz_q_e, &oz_q_enn}) d->release();
         for (auto* d : {&status, &gemm_flags, &oz_line_max, &oz_q_line_max, &oz_zmax}) d->release();

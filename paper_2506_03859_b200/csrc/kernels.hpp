@@ -126,6 +126,14 @@ int64_t ozaki_x_bytes(int64_t rows, int64_t k, int nsl = ozaki_fp64_slices());
 int64_t ozaki_z_bytes(int64_t n, int64_t k, int nsl = ozaki_fp64_slices());
 int64_t ozaki_apply_z_bytes(int64_t k, int nsl = ozaki_fp64_slices());
 // ozaki_apply's products again on the B slices its last call left in z / ez (N <= 128)
+// Y (M x N) = alpha X C + beta Y for an X (M x K) held as its A'Y-layout slices xs_tn
+// (column exponents xe, as made by ozaki_slice_a for the A'Y layout): C's rows scaled by
+// 2^xe into cs (K x N scratch), sliced per column into z, and multiplied reading the
+// slices MN-major (no slices of X in the A G layout are needed)
+void ozaki_apply_mn(int64_t M, int64_t N, int64_t K, double alpha, const int8_t* xs_tn, const int* xe,
+                    const double* c, int64_t ldc_in, double beta, double* Y, int64_t ldy, double* cs, int8_t* z,
+                    int* ez, double* work, int num_sms, cudaStream_t s, LaunchCounter& lc, int nsl,
+                    unsigned* zmax);
 // while set (per thread), launch_ozaki brackets each k_ozaki (+ fixup) launch with a
 // pair of events from this timer
 void ozaki_set_timer(LaunchTimer* t);

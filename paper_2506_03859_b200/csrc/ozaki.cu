@@ -141,6 +141,9 @@ struct OzArgs {
     // L2 policy of the bulk copies: A slices evict-first (streamed once per pass), Z
     // slices evict-last (re-read by every row tile; the pairs walk different k ranges)
     int l2hint;
+    // AMN launches: xs are the A'Y-layout (column-scaled, K-major) slices of an operand X
+    // (rows = K of this product, x_kb k-blocks of 64 of them), read MN-major as A = X
+    int64_t x_kb;
 };
 
 // this CTA's (or fixup block's) column chunk of a paired launch
@@ -289,7 +292,9 @@ struct Walk {
 // A is read from shared memory 12 (ND = 8) / 10 (ND = 7) times per k-step instead of
 // 14 / 11.  Spilled rows (past the slices a product needs) land on diagonal 8 (ND = 8) or
 // 7 (ND = 7), never read; diagonal 7 of ND = 8 starts with its own lone MMA in SP = 1.
-template <int SP, int ND, bool WIDE>
+// AK: advance of the A descriptor per 32-element k-step (16-byte units): 2 (K-major), 128
+// (MN-major: 32 K rows of 64 bytes)
+template <int SP, int ND, bool WIDE, unsigned AK = (32 >> 4)>
 __device__ __forceinline__ void issue_s56(unsigned tmem, unsigned da_lo, unsigned db_lo, unsigned d_hi,
                                           unsigned idesc, bool init) {
     constexpr unsigned kstep = 32 >> 4;
@@ -300,7 +305,7 @@ __device__ __forceinline__ void issue_s56(unsigned tmem, unsigned da_lo, unsigne
             const unsigned dt = tmem + unsigned(SP * 56 + r0);
             const unsigned bl = db_lo + unsigned((r0 * OZ_BK) >> 4);
             umma_i8(dt, da_lo, bl, d_hi, id, (first_writer && init) ? 0u : 1u);
-            umma_i8(dt, da_lo + kstep, bl + kstep, d_hi, id, 1u);
+            umma_i8(dt, da_lo + AK, bl + kstep, d_hi, id, 1u);
         };
         if constexpr (SP == 0) { mmr(0, 256, true); mmr(256, 144, true); }
         else if constexpr (SP == 1) {
@@ -321,7 +326,7 @@ __device__ __forceinline__ void issue_s56(unsigned tmem, unsigned da_lo, unsigne
         const unsigned dt = tmem + unsigned((SP + q0) * 56);
         const unsigned bl = db_lo + unsigned((q0 * 56 * OZ_BK) >> 4);
         umma_i8(dt, da_lo, bl, d_hi, id, (first_writer && init) ? 0u : 1u);
-        umma_i8(dt, da_lo + kstep, bl + kstep, d_hi, id, 1u);
+        umma_i8(dt, da_lo + AK, bl + kstep, d_hi, id, 1u);
     };
     if constexpr (ND == 7) {
         // diagonals 0..6 only (p + q <= 6: 28 products in 11 MMAs); every diagonal starts
@@ -344,9 +349,16 @@ __device__ __forceinline__ void issue_s56(unsigned tmem, unsigned da_lo, unsigne
     else { mma(0, 112, false); }
 }
 
-template <bool PAIR, int NSL, int BS, int S, int NDK = 0, bool WIDE = false>
+// AMN: A is read MN-major from the A'Y-layout slices of an operand X (p.x_kb): the
+// products Y (rows of X) = X C with K = columns of X, e.g. Y -= Q C in the block
+// Gram-Schmidt, on the slices of Q the Q'Y products already made.  A k-block (64 columns
+// of X, 128 rows) per slice is two 4 KB halves of A'Y tiles: the rows 0..63 and 64..127
+// halves sit 4 KB apart (LBO), 8 columns per 512-byte swizzle atom (SBO); the row
+// exponents are 0 (each column's scale is folded into C by the caller).
+template <bool PAIR, int NSL, int BS, int S, int NDK = 0, bool WIDE = false, bool AMN = false>
 __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
     using SL = Sl<NSL, BS, S, NDK>;
+    constexpr unsigned AK = AMN ? (32u * 64u) >> 4 : 32u >> 4;
     static_assert(S == 64 || (S == 56 && NSL == 7), "the 56-row spacing is scheduled for 7 slices");
     static_assert(NDK == 0 || (NDK == 7 && NSL == 7 && S == 56), "the trimmed variant is scheduled for S = 56");
     constexpr int A_STAGES = SL::A_STAGES;
@@ -419,6 +431,27 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
                                        pol_z);
                     else
                         bulk_load(b_base + sb * B_STAGE, q_zs + int64_t(kb) * zbytes, zbytes, b_full + 8 * sb);
+                    if constexpr (AMN) {
+                        // columns 64 kb.. of X = half (kb & 1) of row tile kb / 2 of its A'Y
+                        // slices, at X-row k-blocks 2 mt (rows 0..63) and 2 mt + 1 (64..127)
+                        const int64_t kb0 = 2 * mt;
+                        const bool two = kb0 + 1 < p.x_kb;
+                        const int8_t* xt = p.xs + ((int64_t(kb >> 1) * p.x_kb + kb0) * NSL) * int64_t(A_TILE) +
+                                           (kb & 1) * (A_TILE / 2);
+                        for (int sp = 0; sp < NSL; ++sp, ++ja) {
+                            const int sa = int(ja % A_STAGES);
+                            mbar_wait(a_empty + 8 * sa, unsigned((ja / A_STAGES) & 1) ^ 1u);
+                            mbar_expect_tx(a_full + 8 * sa, unsigned(two ? A_TILE : A_TILE / 2));
+                            if (PAIR && (sp & 1) != rank) continue;
+                            for (int hf = 0; hf < (two ? 2 : 1); ++hf) {
+                                const int8_t* src = xt + (int64_t(hf) * NSL + sp) * A_TILE;
+                                const unsigned dst = a_base + sa * A_TILE + hf * (A_TILE / 2);
+                                if constexpr (PAIR) bulk_load_mc2_hint(dst, src, unsigned(A_TILE / 2), a_full + 8 * sa, pol_a);
+                                else bulk_load_hint(dst, src, unsigned(A_TILE / 2), a_full + 8 * sa, pol_a);
+                            }
+                        }
+                        continue;
+                    }
                     const int8_t* xt = p.xs + (mt * p.kblocks + kb) * int64_t(NSL * A_TILE);
                     for (int sp = 0; sp < NSL; ++sp, ++ja) {
                         const int sa = int(ja % A_STAGES);
@@ -448,8 +481,12 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
             // Everything below stays 32-bit and the slice loops are unrolled, so the
             // descriptors live in uniform registers (a per-MMA register->uniform
             // broadcast made the issue loop, not the tensor core, the bottleneck).
-            constexpr unsigned idesc = (2u << 4) | (1u << 7) | (1u << 10) | (unsigned(OZ_BM >> 4) << 24);
-            const uint64_t da0 = smem_desc(a_base), db0 = smem_desc(b_base);
+            constexpr unsigned idesc =
+                (2u << 4) | (1u << 7) | (1u << 10) | (AMN ? 1u << 15 : 0u) | (unsigned(OZ_BM >> 4) << 24);
+            // MN-major A: LBO = 4 KB between the two 64-row halves (SBO = 512 B as for K-major)
+            const uint64_t da0 = AMN ? (smem_desc(a_base) & ~(uint64_t(0x3FFF) << 16)) | (uint64_t(4096 >> 4) << 16)
+                                     : smem_desc(a_base);
+            const uint64_t db0 = smem_desc(b_base);
             const unsigned da_lo0 = unsigned(da0), db_lo0 = unsigned(db0);
             const unsigned d_hi = unsigned(da0 >> 32);   // identical for both operands
             unsigned sa = 0, pa = 0, sb = 0, pb = 0, pt = 0;
@@ -475,13 +512,13 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
                             // the top diagonal ND-1 starts with (ND-NSL, NSL-1), issued alone.
                             if constexpr (S == 56) {
                                 const bool init = kb == cb;
-                                if (sp == 0) issue_s56<0, ND, WIDE>(tmem, da_lo, db_lo, d_hi, idesc, init);
-                                else if (sp == 1) issue_s56<1, ND, WIDE>(tmem, da_lo, db_lo, d_hi, idesc, init);
-                                else if (sp == 2) issue_s56<2, ND, WIDE>(tmem, da_lo, db_lo, d_hi, idesc, init);
-                                else if (sp == 3) issue_s56<3, ND, WIDE>(tmem, da_lo, db_lo, d_hi, idesc, init);
-                                else if (sp == 4) issue_s56<4, ND, WIDE>(tmem, da_lo, db_lo, d_hi, idesc, init);
-                                else if (sp == 5) issue_s56<5, ND, WIDE>(tmem, da_lo, db_lo, d_hi, idesc, init);
-                                else issue_s56<6, ND, WIDE>(tmem, da_lo, db_lo, d_hi, idesc, init);
+                                if (sp == 0) issue_s56<0, ND, WIDE, AK>(tmem, da_lo, db_lo, d_hi, idesc, init);
+                                else if (sp == 1) issue_s56<1, ND, WIDE, AK>(tmem, da_lo, db_lo, d_hi, idesc, init);
+                                else if (sp == 2) issue_s56<2, ND, WIDE, AK>(tmem, da_lo, db_lo, d_hi, idesc, init);
+                                else if (sp == 3) issue_s56<3, ND, WIDE, AK>(tmem, da_lo, db_lo, d_hi, idesc, init);
+                                else if (sp == 4) issue_s56<4, ND, WIDE, AK>(tmem, da_lo, db_lo, d_hi, idesc, init);
+                                else if (sp == 5) issue_s56<5, ND, WIDE, AK>(tmem, da_lo, db_lo, d_hi, idesc, init);
+                                else issue_s56<6, ND, WIDE, AK>(tmem, da_lo, db_lo, d_hi, idesc, init);
                                 if constexpr (PAIR) umma_commit_mc2(a_empty + 8 * sa);
                                 else umma_commit(a_empty + 8 * sa);
                                 if (++sa == A_STAGES) sa = 0, pa ^= 1u;
@@ -500,7 +537,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
                                 umma_i8(dt, da_lo, bl, d_hi, id, sp == 0 ? unsigned(kb != cb) : 1u);
 #pragma unroll
                                 for (int k = 1; k < OZ_BK / 32; ++k)
-                                    umma_i8(dt, da_lo + k * kstep, bl + k * kstep, d_hi, id, 1u);
+                                    umma_i8(dt, da_lo + k * AK, bl + k * kstep, d_hi, id, 1u);
                             }
                             if (split_top) {
                                 const unsigned id = idesc | (unsigned(OZ_BN >> 3) << 17);
@@ -509,7 +546,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
                                 umma_i8(dt, da_lo, bl, d_hi, id, unsigned(kb != cb));
 #pragma unroll
                                 for (int k = 1; k < OZ_BK / 32; ++k)
-                                    umma_i8(dt, da_lo + k * kstep, bl + k * kstep, d_hi, id, 1u);
+                                    umma_i8(dt, da_lo + k * AK, bl + k * kstep, d_hi, id, 1u);
                             }
                             if constexpr (PAIR) umma_commit_mc2(a_empty + 8 * sa);
                             else umma_commit(a_empty + 8 * sa);
@@ -541,7 +578,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
             const int64_t row = t * OZ_BM + r_loc;
             const bool full_tile = kb0 == 0 && kb1 == p.kblocks;
             double* piece = q_work + (3 * int64_t(c) + (t == wk.t_last ? 0 : 1)) * OZ_PARTIAL;
-            const int er = row < p.M ? p.ex[row] : 0;   // loaded while the MMAs run
+            const int er = (!AMN && row < p.M) ? p.ex[row] : 0;   // loaded while the MMAs run
             for (int cb = kb0; cb < kb1; cb += CHUNK_KB) {
                 const bool first_chunk = cb == kb0, last_chunk = cb + CHUNK_KB >= kb1;
                 mbar_wait(t_full, ph);
@@ -1116,13 +1153,13 @@ void ozaki_slice_z(const double* b, int64_t k, int64_t n, int64_t ld, int* e, in
 }
 
 // paired (pair_cw > 0): N = 2 chunks of pair_cw columns at most, zs / ez hold both
-template <bool PAIR, int NSL, int BS, int S = 64, int NDK = 0, bool WIDE = false>
+template <bool PAIR, int NSL, int BS, int S = 64, int NDK = 0, bool WIDE = false, bool AMN = false>
 static void launch_variant(const OzArgs& a, cudaStream_t s) {
     static bool configured[64] = {};
     int dev = 0;
     FQB_CUDA(cudaGetDevice(&dev));
     if (dev < 0 || dev >= 64 || !configured[dev]) {
-        FQB_CUDA(cudaFuncSetAttribute(k_ozaki<PAIR, NSL, BS, S, NDK, WIDE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        FQB_CUDA(cudaFuncSetAttribute(k_ozaki<PAIR, NSL, BS, S, NDK, WIDE, AMN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       int(Sl<NSL, BS, S, NDK>::SMEM)));
         if (dev >= 0 && dev < 64) configured[dev] = true;
     }
@@ -1147,7 +1184,7 @@ static void launch_variant(const OzArgs& a, cudaStream_t s) {
     }
     cfg.attrs = attr;
     cfg.numAttrs = na;
-    FQB_CUDA(cudaLaunchKernelEx(&cfg, k_ozaki<PAIR, NSL, BS, S, NDK, WIDE>, a));
+    FQB_CUDA(cudaLaunchKernelEx(&cfg, k_ozaki<PAIR, NSL, BS, S, NDK, WIDE, AMN>, a));
 }
 
 // A/B switches of the A-pass kernel (read once): FQB_OZ_L2HINT=0 plain bulk copies,
@@ -1187,8 +1224,14 @@ static bool wide_default() {
 }
 
 template <bool PAIR>
-static void launch_pair_or_not(const OzArgs& a, int nsl, int S, cudaStream_t s) {
+static void launch_pair_or_not(const OzArgs& a, int nsl, int S, cudaStream_t s, bool amn) {
     const bool s56 = nsl == 7 && S == 56;
+    if (amn) {   // the MN-major reads of A'Y-layout slices: FP64-class, default schedules only
+        if (s56 && wide_default()) launch_variant<PAIR, 7, 2, 56, 0, true, true>(a, s);
+        else if (nsl == 7 && S == 64) launch_variant<PAIR, 7, 2, 64, 0, false, true>(a, s);
+        else throw Error(kStatusInvalid, "ozaki_apply_mn: unsupported slice scheme");
+        return;
+    }
     if (s56 && diags_default() == 7 && wide_default()) launch_variant<PAIR, 7, 2, 56, 7, true>(a, s);
     else if (s56 && diags_default() == 7) launch_variant<PAIR, 7, 2, 56, 7>(a, s);
     else if (s56 && wide_default()) launch_variant<PAIR, 7, 2, 56, 0, true>(a, s);
@@ -1213,7 +1256,8 @@ static cudaEvent_t timer_event(LaunchTimer* t) {
 
 static void launch_ozaki(int64_t M, int64_t N, int64_t K, double alpha, const int8_t* xs, const int* ex,
                          const int8_t* zs, const int* ez, double beta, double* C, int64_t ldc, double* work,
-                         int num_sms, int64_t pair_cw, int nsl, int S, cudaStream_t s, LaunchCounter& lc) {
+                         int num_sms, int64_t pair_cw, int nsl, int S, cudaStream_t s, LaunchCounter& lc,
+                         int64_t x_kb = 0) {
     check_nsl(nsl);
     const bool pair = pair_cw > 0;
     OzArgs a{};
@@ -1245,8 +1289,9 @@ static void launch_ozaki(int64_t M, int64_t N, int64_t K, double alpha, const in
     a.l2hint = l2hint_default();
     LaunchTimer* const tm = (t_timer && t_timer->on) ? t_timer : nullptr;
     if (tm) FQB_CUDA(cudaEventRecord(timer_event(tm), s));
-    if (pair) launch_pair_or_not<true>(a, nsl, S, s);
-    else launch_pair_or_not<false>(a, nsl, S, s);
+    a.x_kb = x_kb;
+    if (pair) launch_pair_or_not<true>(a, nsl, S, s, x_kb > 0);
+    else launch_pair_or_not<false>(a, nsl, S, s, x_kb > 0);
     FQB_LAUNCHED();
     lc.bump();
     bool split = false;   // does any CTA (pair) boundary fall inside a tile?
@@ -1279,9 +1324,47 @@ static bool pairs_enabled() {
     return on;
 }
 
+static void apply_chunks(int64_t M, int64_t N, int64_t K, double alpha, const int8_t* xs, const int* ex,
+                         const double* b, int64_t ldb, double beta, double* C, int64_t ldc, int8_t* z, int* ez,
+                         double* work, int num_sms, cudaStream_t s, LaunchCounter& lc, int nsl, unsigned* zmax,
+                         int64_t x_kb);
+
 void ozaki_apply(int64_t M, int64_t N, int64_t K, double alpha, const int8_t* xs, const int* ex, const double* b,
                  int64_t ldb, double beta, double* C, int64_t ldc, int8_t* z, int* ez, double* work, int num_sms,
                  cudaStream_t s, LaunchCounter& lc, int nsl, unsigned* zmax) {
+    apply_chunks(M, N, K, alpha, xs, ex, b, ldb, beta, C, ldc, z, ez, work, num_sms, s, lc, nsl, zmax, 0);
+}
+
+// cs (K x N, ld K) = diag(2^e) c: row k of C times 2^e_k (exact; NaN for a non-finite line)
+__global__ void k_scale_rows_pow2(const double* __restrict__ c, int64_t K, int64_t N, int64_t ldc,
+                                  const int* __restrict__ e, double* __restrict__ cs) {
+    FQB_PDL_ENTRY();
+    const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= K) return;
+    const int ek = e[k];
+    for (int64_t j = blockIdx.y; j < N; j += gridDim.y) cs[j * K + k] = mul_pow2(c[j * ldc + k], ek);
+}
+
+void ozaki_apply_mn(int64_t M, int64_t N, int64_t K, double alpha, const int8_t* xs_tn, const int* xe,
+                    const double* c, int64_t ldc_in, double beta, double* Y, int64_t ldy, double* cs, int8_t* z,
+                    int* ez, double* work, int num_sms, cudaStream_t s, LaunchCounter& lc, int nsl,
+                    unsigned* zmax) {
+    if (N <= 0 || M <= 0) return;
+    if (K <= 0) {   // empty sum: Y = beta Y
+        throw Error(kStatusInvalid, "ozaki_apply_mn: K = 0");
+    }
+    launch_k(k_scale_rows_pow2, dim3(unsigned(ceil_div(K, 128)), unsigned(std::min<int64_t>(N, 64))), 128, 0, s, c,
+             K, N, ldc_in, xe, cs);
+    FQB_LAUNCHED();
+    lc.bump();
+    apply_chunks(M, N, K, alpha, xs_tn, nullptr, cs, K, beta, Y, ldy, z, ez, work, num_sms, s, lc, nsl, zmax,
+                 ceil_div(M, OZ_BK));
+}
+
+static void apply_chunks(int64_t M, int64_t N, int64_t K, double alpha, const int8_t* xs, const int* ex,
+                         const double* b, int64_t ldb, double beta, double* C, int64_t ldc, int8_t* z, int* ez,
+                         double* work, int num_sms, cudaStream_t s, LaunchCounter& lc, int nsl, unsigned* zmax,
+                         int64_t x_kb) {
     if (N <= 0) return;
     const int64_t chunks = ceil_div(N, OZ_BN);
     const int64_t cw = ceil_div(N, chunks);
@@ -1295,13 +1378,13 @@ void ozaki_apply(int64_t M, int64_t N, int64_t K, double alpha, const int8_t* xs
         slice_z_s(b + c0 * ldb, K, cw, ldb, ez, z, s, lc, nsl, S, zmax);
         slice_z_s(b + (c0 + cw) * ldb, K, nb - cw, ldb, ez + OZ_BN, z + zstride, s, lc, nsl, S,
                   zmax ? zmax + OZ_BN : nullptr);
-        launch_ozaki(M, nb, K, alpha, xs, ex, z, ez, beta, C + c0 * ldc, ldc, work, num_sms, cw, nsl, S, s, lc);
+        launch_ozaki(M, nb, K, alpha, xs, ex, z, ez, beta, C + c0 * ldc, ldc, work, num_sms, cw, nsl, S, s, lc, x_kb);
         c0 += nb;
     }
     for (; c0 < N; c0 += cw) {
         const int64_t nb = std::min(cw, N - c0);
         slice_z_s(b + c0 * ldb, K, nb, ldb, ez, z, s, lc, nsl, S, zmax);
-        launch_ozaki(M, nb, K, alpha, xs, ex, z, ez, beta, C + c0 * ldc, ldc, work, num_sms, 0, nsl, S, s, lc);
+        launch_ozaki(M, nb, K, alpha, xs, ex, z, ez, beta, C + c0 * ldc, ldc, work, num_sms, 0, nsl, S, s, lc, x_kb);
     }
 }
 // the products of ozaki_apply again, on the B slices its last call left in z / ez

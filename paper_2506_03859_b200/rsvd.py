@@ -347,6 +347,15 @@ class SlicedOperand:
         if st:
             _raise(st, "fqb_sliced_gemm_again")
 
+    def gemm_mn(self, nb, alpha, b_ptr, ldb, beta, c_ptr, ldc):
+        """C (m x nb) = alpha A B + beta C from the A'Y-layout slices read MN-major
+        (fqb_sliced_gemm_mn; the engine's Y -= Q C)."""
+        if self._s is None:
+            raise InvalidArgument("sliced operand was freed")
+        st = self._eng._lib.fqb_sliced_gemm_mn(self._eng._h, self._s, nb, alpha, b_ptr, ldb, beta, c_ptr, ldc)
+        if st:
+            _raise(st, "fqb_sliced_gemm_mn")
+
     def free(self):
         if self._s is not None:
             self._eng._lib.fqb_sliced_free(self._eng._h, self._s)

@@ -232,6 +232,40 @@ def test_sliced_operand_matches_one_shot_emulation(eng):
         sl.gemm(True, nb, 1.0, b.data_ptr(), m, 0.0, c1.data_ptr(), n)
 
 
+@pytest.mark.parametrize("m,n,nb", [(1100, 900, 37), (1000, 200, 100), (960, 130, 60), (64, 65, 8),
+                                    (3000, 2000, 100), (1088, 1, 50), (5000, 257, 128)])
+def test_sliced_gemm_mn_fp64_accuracy(eng, m, n, nb):
+    """fqb_sliced_gemm_mn: A B from the A'Y-layout slices read MN-major (the engine's
+    Y -= Q C), against an extended-precision product: odd numbers of 64-row k-blocks (the
+    last row tile's second half absent), K not a multiple of 64, one chunk (S = 56 and
+    S = 64) and paired chunks, alpha / beta.
+    The scales are per column of A here, so the bound is normwise per column:
+    |err_ij| <= 4e-16 sum_k max_i|A_ik| |B_kj| (+ 2^-53 |C_ij|) -- a row much smaller than
+    its columns' maxima keeps absolute, not relative, accuracy (the engine's Q rows: the
+    projection Y -= Q C only needs ||err|| small against ||C||)."""
+    g = torch.Generator(device="cpu").manual_seed(m + n + nb)
+    a = torch.randn((m, n), dtype=torch.float64, generator=g)
+    a[:, ::7] *= 1e-3                                    # column scales differ
+    a[::5, :] *= 1e-2                                    # and row scales
+    b = torch.randn((n, nb), dtype=torch.float64, generator=g)
+    c0 = torch.randn((m, nb), dtype=torch.float64, generator=g)
+    ad = a.t().contiguous().t().cuda()
+    bd = b.t().contiguous().t().cuda()
+    c = c0.t().contiguous().t().cuda()
+    with eng.slice_operand(ad.data_ptr(), m, n, m) as sl:
+        sl.gemm_mn(nb, 0.75, bd.data_ptr(), n, -0.5, c.data_ptr(), m)
+        torch.cuda.synchronize()
+    rows = np.unique(np.linspace(0, m - 1, min(m, 64)).astype(int))
+    an = a.numpy().astype(np.longdouble)
+    bn = b.numpy().astype(np.longdouble)
+    exact = 0.75 * (an[rows] @ bn) - 0.5 * c0.numpy()[rows].astype(np.longdouble)
+    cmax = np.abs(an).max(axis=0)                          # per column of A
+    bound = 0.75 * (cmax @ np.abs(bn))[None, :] + 0.5 * np.abs(c0.numpy()[rows])
+    err = np.abs(c.cpu().numpy()[rows].astype(np.longdouble) - exact)
+    tol = 4e-16 * bound + 2.0 ** -53 * np.abs(exact) + 1e-300
+    assert (err <= tol).all(), float(np.max(err / tol))
+
+
 @pytest.mark.parametrize("nb", [50, 100, 128])
 def test_sliced_gemm_again_reuses_b_slices(eng, nb):
     """fqb_sliced_gemm_again: the previous product on the same B slices, bit for bit,

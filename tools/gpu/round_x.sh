@@ -1,0 +1,4 @@
+set -x
+mkdir -p gpurun_out
+timeout 900 python tools/kernel_profile.py --config c4 --svd --runs 2 > gpurun_out/r25_kprof_c4.txt 2>&1
+timeout 900 python tools/kernel_profile.py --config c2 --svd --runs 5 > gpurun_out/r25_kprof_c2.txt 2>&1
