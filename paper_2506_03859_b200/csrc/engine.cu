@@ -447,17 +447,6 @@ class QbRun {
         return !(e && e[0] == '0');
     }
     bool use_q_oz(int64_t l) const { return q_oz_on_ && l >= kQOzMinCols; }
-    // the projections Y -= Q C (K = l) on the INT8 path from l >= FQB_OZ_QNN_MIN (default 0:
-    // never).  Measured on config 4 (r13): 745-747 ms per step with or without it at any
-    // threshold -- a tile has only l / 64 k-blocks to amortize its accumulator drain, and
-    // the per-block re-slicing of Q (row scales change as Q grows) eats the rest; DMMA stays
-    bool use_q_oz_nn(int64_t l) const {
-        static const int64_t min_cols = [] {
-            const char* e = std::getenv("FQB_OZ_QNN_MIN");
-            return e && *e ? int64_t(std::atoll(e)) : int64_t(0);
-        }();
-        return q_oz_on_ && min_cols > 0 && l >= min_cols;
-    }
     // the projections Y -= Q C (K = l) on the INT8 path reading the A'Y-layout slices of Q
     // (the ones slice_q made for Q'Y) MN-major, C's rows scaled by Q's column scales --
     // nothing is re-sliced.  FQB_OZ_QMN=0 keeps them on DMMA.
@@ -491,27 +480,6 @@ class QbRun {
                       w.oz_q_tn.ptr + (c0 / 128) * (ozaki_x_bytes(128, m_, nsl)), w.oz_q_e.ptr + c0, nullptr, nullptr,
                       s_, h_.lc, nullptr, nullptr, nsl);
         q_sliced_ = l_;   // committed columns with valid slices (the rest is redone next block)
-    }
-    // Q (m x l) in the A G layout (row-scaled, K = l): a row's scale depends on every
-    // column, so it is made anew per block (one read of Q) for the two projections
-    // Y -= Q C of the block
-    void slice_q_nn(int64_t l) {
-        Workspace& w = h_.ws;
-        const int nsl = ozaki_fp64_slices();
-        w.oz_q_nn.ensure(size_t(ozaki_x_bytes(m_, cap_, nsl)), s_);
-        w.oz_q_enn.ensure(size_t(m_), s_);
-        w.oz_q_line_max.ensure(size_t(ozaki_line_max_words(m_, cap_ + b_)), s_);
-        ozaki_slice_a(q_.ptr, m_, l, ldq_, w.oz_q_line_max.ptr, nullptr, nullptr, w.oz_q_nn.ptr, w.oz_q_enn.ptr, s_,
-                      h_.lc, nullptr, nullptr, nsl);
-    }
-    void q_nn_sub(int64_t l, const double* Cm, int64_t ldcm, double* Y) {   // Y (m x b) -= Q(:, :l) Cm
-        Workspace& w = h_.ws;
-        const int nsl = ozaki_fp64_slices();
-        w.oz_z.ensure(size_t(std::max(ozaki_apply_z_bytes(m_, nsl), ozaki_apply_z_bytes(l, nsl))), s_);
-        w.oz_ez.ensure(size_t(ozaki_apply_ez_count()), s_);
-        w.oz_zmax.ensure(size_t(ozaki_apply_ez_count()), s_);
-        ozaki_apply(m_, b_, l, -1.0, w.oz_q_nn.ptr, w.oz_q_enn.ptr, Cm, ldcm, 1.0, Y, ldq_, w.oz_z.ptr, w.oz_ez.ptr,
-                    h_.gws.work, h_.num_sms, s_, h_.lc, nsl, w.oz_zmax.ptr);
     }
     void q_tn(int64_t M, const double* B, double* C, int64_t ldc) {   // C (M x b) = Q(:, :M)' B
         Workspace& w = h_.ws;
@@ -729,9 +697,6 @@ class QbRun {
         } else {
             if (use_q_mn(l)) {
                 q_mn_sub(l, cd, ldcd, yj);
-            } else if (use_q_oz_nn(l)) {
-                slice_q_nn(l);
-                q_nn_sub(l, cd, ldcd, yj);
             } else {
                 gemm_(false, m_, b, l, -1.0, q_.ptr, ldq_, cd, ldcd, 1.0, yj, ldq_);
             }
@@ -744,7 +709,6 @@ class QbRun {
             else gemm_(true, l, b, m_, 1.0, q_.ptr, ldq_, w.ys.ptr, ldq_, 0.0, w.c2.ptr, l);
             comm_allreduce_sum(h_, w.c2.ptr, size_t(l) * b, s_);
             if (use_q_mn(l)) q_mn_sub(l, w.c2.ptr, l, w.ys.ptr);
-            else if (use_q_oz_nn(l)) q_nn_sub(l, w.c2.ptr, l, w.ys.ptr);
             else gemm_(false, m_, b, l, -1.0, q_.ptr, ldq_, w.c2.ptr, l, 1.0, w.ys.ptr, ldq_);
         }
         gemm_(true, b, b, m_, 1.0, w.ys.ptr, ldq_, w.ys.ptr, ldq_, 0.0, S2_, b);

@@ -91,8 +91,8 @@ struct Workspace {
     DeviceArray<unsigned> oz_line_max;
     // Ozaki slices of Q in the A'Y layout (operand rows = columns of Q), grown with Q,
     // for the block Gram-Schmidt products [Q|Y]'Y and Q'Y_s (engine.cu, accept)
-    DeviceArray<int8_t> oz_q_tn, oz_q_nn;   // Q in the A'Y layout (grown) and the A G layout (per block)
-    DeviceArray<int> oz_q_e, oz_q_enn;
+    DeviceArray<int8_t> oz_q_tn;   // Q in the A'Y layout (grown with Q; also read MN-major for Y -= Q C)
+    DeviceArray<int> oz_q_e;
     DeviceArray<unsigned> oz_q_line_max, oz_zmax;
 
     // every member, while the stream the frees are ordered on still exists
@@ -100,10 +100,10 @@ struct Workspace {
         for (auto* d : {&omega, &y0, &ys, &wp, &wraw, &g, &t, &cd, &c2, &small, &zc, &rowsum_b, &splitk, &partial,
                         &scalars, &scratch, &a_copy, &values, &oz_norm_partial, &w_half, &oz_q_cs})
             d->release();
-        for (auto* d : {&col_ptr, &row_idx, &counts, &oz_e_nn, &oz_e_tn, &oz_ez, &oz_q_e, &oz_q_enn}) d->release();
+        for (auto* d : {&col_ptr, &row_idx, &counts, &oz_e_nn, &oz_e_tn, &oz_ez, &oz_q_e}) d->release();
         for (auto* d : {&status, &gemm_flags, &oz_line_max, &oz_q_line_max, &oz_zmax}) d->release();
         a_copy_f32.release();
-        for (auto* d : {&oz_x_nn, &oz_x_tn, &oz_z, &oz_q_tn, &oz_q_nn}) d->release();
+        for (auto* d : {&oz_x_nn, &oz_x_tn, &oz_z, &oz_q_tn}) d->release();
     }
 };
 
