@@ -579,8 +579,20 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
             const bool full_tile = kb0 == 0 && kb1 == p.kblocks;
             double* piece = q_work + (3 * int64_t(c) + (t == wk.t_last ? 0 : 1)) * OZ_PARTIAL;
             const int er = (!AMN && row < p.M) ? p.ex[row] : 0;   // loaded while the MMAs run
+            // AMN (short K, beta != 0: Y -= Q C): each group's old C is loaded one group
+            // ahead -- the first before the accumulators are ready -- so the drain, which
+            // the single-buffered TMEM puts on the MMA's critical path, does not wait on it
+            double pre[16];
+            const bool pre_on = AMN && p.beta != 0.0 && full_tile && row < p.M;
+            auto load_old = [&](int g0) {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) pre[j] = g0 + j < q_N ? q_C[int64_t(g0 + j) * p.ldc + row] : 0.0;
+            };
             for (int cb = kb0; cb < kb1; cb += CHUNK_KB) {
                 const bool first_chunk = cb == kb0, last_chunk = cb + CHUNK_KB >= kb1;
+                if constexpr (AMN) {
+                    if (pre_on && last_chunk) load_old(0);
+                }
                 mbar_wait(t_full, ph);
                 ph ^= 1u;
                 asm volatile("tcgen05.fence::after_thread_sync;\n");
@@ -618,7 +630,11 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
                     }
                     if (row < p.M) {
                         double old_c[16];
-                        if (p.beta != 0.0) {
+                        if (AMN && pre_on) {
+#pragma unroll
+                            for (int j = 0; j < 16; ++j) old_c[j] = pre[j];
+                            if (g + 16 < S) load_old(g + 16);
+                        } else if (p.beta != 0.0) {
 #pragma unroll
                             for (int j = 0; j < 16; ++j)
                                 old_c[j] = g + j < q_N ? q_C[int64_t(g + j) * p.ldc + row] : 0.0;
