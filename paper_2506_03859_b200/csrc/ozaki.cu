@@ -72,7 +72,10 @@ constexpr int B_TILE = OZ_BN * OZ_BK;             // 4 KB per slice (bn = 64)
 // Z rows per k-block of the slices of one column chunk: NSL slices of S rows each (S = 64,
 // or S = 56 for chunks of <= 56 columns, then with 8 zero rows after the last slice that
 // the N = 64 lone products of the S = 56 schedule read past it)
-__host__ __device__ constexpr int z_block_rows(int nsl, int S) { return nsl * S + (S == 56 ? 8 : 0); }
+// Zero rows after the last slice that the schedules read past it: 8 for S = 56 (the N = 64
+// lone products), 2 for S = 50 (the N = 96 MMAs of slices 0 / 1 cover rows 256..351).
+__host__ __device__ constexpr int z_pad_rows(int S) { return S == 56 ? 8 : S == 50 ? 2 : 0; }
+__host__ __device__ constexpr int z_block_rows(int nsl, int S) { return nsl * S + z_pad_rows(S); }
 
 template <int NSL, int BS = 2, int S = 64, int NDK = 0>
 struct Sl {
@@ -261,6 +264,14 @@ __device__ __forceinline__ void tmem_ld16(unsigned taddr, unsigned (&v)[16]) {
         : "r"(taddr));
 }
 
+// zero 16 columns of this warp's 32 TMEM lanes
+__device__ __forceinline__ void tmem_st16_zero(unsigned taddr) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};\n" ::"r"(taddr),
+        "r"(0u)
+        : "memory");
+}
+
 // Work item sequence shared by the three roles: the CTA's iteration range is cut
 // into segments (one per tile, processed last tile first, as in gemm_tma.cu) and
 // each segment into chunks of at most CHUNK_KB k-blocks (int32 headroom).
@@ -349,6 +360,38 @@ __device__ __forceinline__ void issue_s56(unsigned tmem, unsigned da_lo, unsigne
     else { mma(0, 112, false); }
 }
 
+// One k-step of the S = 50 schedule (chunks of <= 50 columns, NSL = 7, all 8 diagonals):
+// Z slice q sits at B rows 50 q (2 zero rows after slice 6), diagonal d at TMEM columns
+// 50 d .. 50 d + 49.  Every MMA starts at B row 0 or 256 (swizzle-atom aligned) and covers
+// the rows a slice's products need, N rounded up to a multiple of 16:
+//     SP 0, 1: rows 0..255, 256..351    SP 2: 0..255, 256..303    SP 3: 0..255
+//     SP 4: 0..207    SP 5: 0..159    SP 6: 0..111
+// 10 MMAs, 1744 B rows per k-step (S = 56 wide: 12 MMAs, 1936 rows).  Rows past the needed
+// slices read the zero pad rows (SP 0, 1) or land on diagonal 8 (columns 400..411, never
+// read).  SP 0 writes columns 0..351 first (accumulate = 0 at `init`); the rest of
+// diagonal 7 (columns 352..399) is zeroed by the epilogue (tcgen05.st) before each
+// accumulation, so every other MMA accumulates.
+template <int SP, unsigned AK = (32 >> 4)>
+__device__ __forceinline__ void issue_s50(unsigned tmem, unsigned da_lo, unsigned db_lo, unsigned d_hi,
+                                          unsigned idesc, bool init) {
+    constexpr unsigned kstep = 32 >> 4;
+    auto mmr = [&](int r0, int n) {
+        const unsigned id = idesc | (unsigned(n >> 3) << 17);
+        const unsigned dt = tmem + unsigned(SP * 50 + r0);
+        const unsigned bl = db_lo + unsigned((r0 * OZ_BK) >> 4);
+        umma_i8(dt, da_lo, bl, d_hi, id, (SP == 0 && init) ? 0u : 1u);
+        umma_i8(dt, da_lo + AK, bl + kstep, d_hi, id, 1u);
+    };
+    if constexpr (SP <= 1) { mmr(0, 256); mmr(256, 96); }
+    else if constexpr (SP == 2) { mmr(0, 256); mmr(256, 48); }
+    else if constexpr (SP == 3) mmr(0, 256);
+    else if constexpr (SP == 4) mmr(0, 208);
+    else if constexpr (SP == 5) mmr(0, 160);
+    else mmr(0, 112);
+}
+// diagonal 7's columns the S = 50 schedule does not initialise (352..399, in 16s)
+constexpr int kS50ZeroCol = 352, kS50ZeroGroups = 3;
+
 // AMN: A is read MN-major from the A'Y-layout slices of an operand X (p.x_kb): the
 // products Y (rows of X) = X C with K = columns of X, e.g. Y -= Q C in the block
 // Gram-Schmidt, on the slices of Q the Q'Y products already made.  A k-block (64 columns
@@ -359,7 +402,8 @@ template <bool PAIR, int NSL, int BS, int S, int NDK = 0, bool WIDE = false, boo
 __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
     using SL = Sl<NSL, BS, S, NDK>;
     constexpr unsigned AK = AMN ? (32u * 64u) >> 4 : 32u >> 4;
-    static_assert(S == 64 || (S == 56 && NSL == 7), "the 56-row spacing is scheduled for 7 slices");
+    static_assert(S == 64 || ((S == 56 || S == 50) && NSL == 7), "the 56 / 50-row spacings are scheduled for 7 slices");
+    static_assert(S != 50 || (NDK == 0 && WIDE), "the 50-row spacing has one (wide, 8-diagonal) schedule");
     static_assert(NDK == 0 || (NDK == 7 && NSL == 7 && S == 56), "the trimmed variant is scheduled for S = 56");
     constexpr int A_STAGES = SL::A_STAGES;
     constexpr int B_STAGES = SL::B_STAGES;
@@ -489,7 +533,9 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
             const uint64_t db0 = smem_desc(b_base);
             const unsigned da_lo0 = unsigned(da0), db_lo0 = unsigned(db0);
             const unsigned d_hi = unsigned(da0 >> 32);   // identical for both operands
-            unsigned sa = 0, pa = 0, sb = 0, pb = 0, pt = 0;
+            // S = 50: the epilogue zeroes part of diagonal 7 before the first accumulation
+            // too (one extra phase of t_empty), so the first wait is on phase 0
+            unsigned sa = 0, pa = 0, sb = 0, pb = 0, pt = S == 50 ? 1u : 0u;
             for (int64_t si = 0; si < wk.nseg; ++si) {
                 const int64_t t = wk.tile(si);
                 const int kb0 = wk.kb(t), kb1 = wk.ke(t);
@@ -510,6 +556,20 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
                             // diagonals sp+sq: one N = 64 * slices MMA covers them (A read once).
                             // Diagonals d < NSL start (accumulate = 0) with sp = 0; with ND > NSL
                             // the top diagonal ND-1 starts with (ND-NSL, NSL-1), issued alone.
+                            if constexpr (S == 50) {
+                                const bool init = kb == cb;
+                                if (sp == 0) issue_s50<0, AK>(tmem, da_lo, db_lo, d_hi, idesc, init);
+                                else if (sp == 1) issue_s50<1, AK>(tmem, da_lo, db_lo, d_hi, idesc, init);
+                                else if (sp == 2) issue_s50<2, AK>(tmem, da_lo, db_lo, d_hi, idesc, init);
+                                else if (sp == 3) issue_s50<3, AK>(tmem, da_lo, db_lo, d_hi, idesc, init);
+                                else if (sp == 4) issue_s50<4, AK>(tmem, da_lo, db_lo, d_hi, idesc, init);
+                                else if (sp == 5) issue_s50<5, AK>(tmem, da_lo, db_lo, d_hi, idesc, init);
+                                else issue_s50<6, AK>(tmem, da_lo, db_lo, d_hi, idesc, init);
+                                if constexpr (PAIR) umma_commit_mc2(a_empty + 8 * sa);
+                                else umma_commit(a_empty + 8 * sa);
+                                if (++sa == A_STAGES) sa = 0, pa ^= 1u;
+                                continue;
+                            }
                             if constexpr (S == 56) {
                                 const bool init = kb == cb;
                                 if (sp == 0) issue_s56<0, ND, WIDE, AK>(tmem, da_lo, db_lo, d_hi, idesc, init);
@@ -572,6 +632,16 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
         const unsigned lane_addr = tmem + (unsigned(quarter * 32) << 16);
         double* carry = q_work + (3 * int64_t(c) + 2) * OZ_PARTIAL;
         unsigned ph = 0;
+        // S = 50: diagonal 7's columns no MMA initialises are zeroed before every
+        // accumulation (here for the first, after each drain for the next)
+        auto zero_d7 = [&]() {
+#pragma unroll
+            for (int z = 0; z < kS50ZeroGroups; ++z) tmem_st16_zero(lane_addr + unsigned(kS50ZeroCol + 16 * z));
+            asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+            asm volatile("tcgen05.fence::before_thread_sync;\n");
+            mbar_arrive(t_empty);
+        };
+        if constexpr (S == 50) zero_d7();
         for (int64_t si = 0; si < wk.nseg; ++si) {
             const int64_t t = wk.tile(si);
             const int kb0 = wk.kb(t), kb1 = wk.ke(t);
@@ -648,8 +718,12 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
                         }
                     }
                 }
-                asm volatile("tcgen05.fence::before_thread_sync;\n");
-                mbar_arrive(t_empty);
+                if constexpr (S == 50) {
+                    zero_d7();
+                } else {
+                    asm volatile("tcgen05.fence::before_thread_sync;\n");
+                    mbar_arrive(t_empty);
+                }
             }
         }
     }
@@ -774,6 +848,34 @@ __device__ __forceinline__ void put_chunk16(const double (&v)[16], int e, int8_t
 #pragma unroll
     for (int sl = 0; sl < NSL; ++sl)
         *reinterpret_cast<uint4*>(dst + sl * slice_stride) = make_uint4(w[sl][0], w[sl][1], w[sl][2], w[sl][3]);
+}
+
+// the same for a Z stage of NSL slices spaced S rows apart: slice sl's row r is stage row
+// S sl + r, swizzled by its stage row (S = 50 is not a multiple of the 8-row atom)
+template <int NSL, int S>
+__device__ __forceinline__ void put_chunk16_z(const double (&v)[16], int e, int8_t* tile0, int r, int c) {
+    if constexpr (S % 8 == 0) {
+        put_chunk16<NSL>(v, e, tile0, int64_t(S) * OZ_BK, r, c);
+    } else {
+        uint32_t w[NSL][4];
+#pragma unroll
+        for (int sl = 0; sl < NSL; ++sl) w[sl][0] = w[sl][1] = w[sl][2] = w[sl][3] = 0;
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            unsigned d[NSL];
+            digits<NSL>(v[u], e, d);
+#pragma unroll
+            for (int sl = 0; sl < NSL; ++sl) w[sl][u >> 2] |= d[sl] << (8 * (u & 3));
+        }
+        constexpr unsigned kOff = Sl<NSL>::W == 8 ? 0x80808080u : 0xC0C0C0C0u;
+#pragma unroll
+        for (int sl = 0; sl < NSL; ++sl)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) w[sl][q] = __vadd4(w[sl][q], kOff);
+#pragma unroll
+        for (int sl = 0; sl < NSL; ++sl)
+            *reinterpret_cast<uint4*>(tile0 + swz(S * sl + r, c)) = make_uint4(w[sl][0], w[sl][1], w[sl][2], w[sl][3]);
+    }
 }
 
 // Row and column maxima (high words) of A (m x n, ld) in one pass; rmax / cmax
@@ -910,7 +1012,7 @@ __global__ void __launch_bounds__(ZT) k_slice_z(const double* __restrict__ b, in
     __shared__ unsigned wmax[ZT / 32];
     const int j = blockIdx.x;
     constexpr int ZR = z_block_rows(NSL, S);
-    if (j >= S) {   // S = 56: the 8 zero rows after the last slice, row NSL S + (j - S)
+    if (j >= S) {   // S = 56 / 50: the 8 / 2 zero rows after the last slice, row NSL S + (j - S)
         const int64_t kb_count = (k + OZ_BK - 1) / OZ_BK;
         const int64_t c16 = int64_t(blockIdx.y) * ZT + threadIdx.x;
         if (c16 >= kb_count * (OZ_BK / 16)) return;
@@ -948,14 +1050,13 @@ __global__ void __launch_bounds__(ZT) k_slice_z(const double* __restrict__ b, in
     const int e = exp_of_hi(mx);
     if (live && blockIdx.y == 0 && threadIdx.x == 0) ez[j] = e;
     const int64_t kb_count = (k + OZ_BK - 1) / OZ_BK;
-    const int64_t z_tile = int64_t(S) * OZ_BK;   // one slice of a k-block
     const int64_t c16 = int64_t(blockIdx.y) * ZT + threadIdx.x;
     if (c16 >= kb_count * (OZ_BK / 16)) return;
     const int64_t k0 = c16 * 16;
     double v[16];
 #pragma unroll
     for (int u = 0; u < 16; ++u) v[u] = (live && k0 + u < k) ? col[k0 + u] : 0.0;
-    put_chunk16<NSL>(v, e, out + (k0 / OZ_BK) * int64_t(ZR) * OZ_BK, z_tile, j, int(k0 % OZ_BK));
+    put_chunk16_z<NSL, S>(v, e, out + (k0 / OZ_BK) * int64_t(ZR) * OZ_BK, j, int(k0 % OZ_BK));
 }
 
 // Long Z operands (k > kZFused rows: the Y of config 4's A'Y, k = m = 100000): every CTA
@@ -1005,8 +1106,9 @@ __global__ void __launch_bounds__(256) k_slice_z_kb(const double* __restrict__ b
     const int j = warp * 8 + (lane >> 2), q = lane & 3;   // row j of the tile, 16-byte chunk q
     const int64_t k0 = int64_t(kb) * OZ_BK + q * 16;
     int8_t* tile0 = out + int64_t(kb) * ZR * OZ_BK;
-    if (j >= S) {   // S = 56: the 8 zero rows after the last slice
-        if (S == 56) *reinterpret_cast<uint4*>(tile0 + swz(NSL * S + (j - S), q * 16)) = make_uint4(0u, 0u, 0u, 0u);
+    if (j >= S) {   // S = 56 / 50: the 8 / 2 zero rows after the last slice
+        if (j - S < z_pad_rows(S))
+            *reinterpret_cast<uint4*>(tile0 + swz(NSL * S + (j - S), q * 16)) = make_uint4(0u, 0u, 0u, 0u);
         return;
     }
     const bool live = j < n;
@@ -1016,7 +1118,7 @@ __global__ void __launch_bounds__(256) k_slice_z_kb(const double* __restrict__ b
     double v[16];
 #pragma unroll
     for (int u = 0; u < 16; ++u) v[u] = (live && k0 + u < k) ? col[k0 + u] : 0.0;
-    put_chunk16<NSL>(v, e, tile0, int64_t(S) * OZ_BK, j, q * 16);
+    put_chunk16_z<NSL, S>(v, e, tile0, j, q * 16);
 }
 
 // Sum the pieces of every split tile in CTA order (deterministic) into C.
@@ -1145,7 +1247,8 @@ static void slice_z_s(const double* b, int64_t k, int64_t n, int64_t ld, int* e,
     if (n <= 0 || k <= 0) return;
     check_nsl(nsl);
     if (cmax && k > kZFused) {
-        if (nsl == 7 && S == 56) slice_z_long<7, 56>(b, k, n, ld, e, out, cmax, s, lc);
+        if (nsl == 7 && S == 50) slice_z_long<7, 50>(b, k, n, ld, e, out, cmax, s, lc);
+        else if (nsl == 7 && S == 56) slice_z_long<7, 56>(b, k, n, ld, e, out, cmax, s, lc);
         else if (nsl == 7) slice_z_long<7, 64>(b, k, n, ld, e, out, cmax, s, lc);
         else if (nsl == 8) slice_z_long<8, 64>(b, k, n, ld, e, out, cmax, s, lc);
         else if (nsl == 3) slice_z_long<3, 64>(b, k, n, ld, e, out, cmax, s, lc);
@@ -1153,8 +1256,9 @@ static void slice_z_s(const double* b, int64_t k, int64_t n, int64_t ld, int* e,
         return;
     }
     const int64_t chunks = ceil_div(k, OZ_BK) * (OZ_BK / 16);
-    const dim3 g(unsigned(S == 56 ? S + 8 : S), unsigned(ceil_div(chunks, ZT)));
-    if (nsl == 7 && S == 56) launch_k(k_slice_z<7, 56>, g, ZT, 0, s, b, k, n, ld, e, out);
+    const dim3 g(unsigned(S + z_pad_rows(S)), unsigned(ceil_div(chunks, ZT)));
+    if (nsl == 7 && S == 50) launch_k(k_slice_z<7, 50>, g, ZT, 0, s, b, k, n, ld, e, out);
+    else if (nsl == 7 && S == 56) launch_k(k_slice_z<7, 56>, g, ZT, 0, s, b, k, n, ld, e, out);
     else if (nsl == 8) launch_k(k_slice_z<8, 64>, g, ZT, 0, s, b, k, n, ld, e, out);
     else if (nsl == 7) launch_k(k_slice_z<7, 64>, g, ZT, 0, s, b, k, n, ld, e, out);
     else if (nsl == 3) launch_k(k_slice_z<3, 64>, g, ZT, 0, s, b, k, n, ld, e, out);
@@ -1217,12 +1321,6 @@ static int zstages_default() {
     static const int v = env_int("FQB_OZ_BSTAGES", 2) == 3 ? 3 : 2;
     return v;
 }
-// Z slice spacing of a chunk of cw columns: 56 rows (11 % fewer int8 MACs, 14 MMAs per
-// k-step) for cw <= 56 on the 7-slice scheme; FQB_OZ_S56=0 keeps 64
-static int z_spacing(int64_t cw, int nsl) {
-    static const bool on = env_int("FQB_OZ_S56", 1) != 0;
-    return (on && nsl == 7 && cw <= 56) ? 56 : 64;
-}
 static int64_t z_chunk_bytes(int64_t K, int nsl, int S) { return ceil_div(K, OZ_BK) * z_block_rows(nsl, S) * OZ_BK; }
 
 // FQB_OZ_DIAGS=7: the 7-slice scheme keeps diagonals p + q <= 6 only (28 of 34 products,
@@ -1239,9 +1337,25 @@ static bool wide_default() {
     return v;
 }
 
+// Z slice spacing of a chunk of cw columns on the 7-slice scheme: 50 rows for cw <= 50 (the
+// wide 8-diagonal schedule: 10 MMAs, 1744 B rows per k-step), 56 for cw <= 56 (12 MMAs,
+// 1936 rows), else 64.  FQB_OZ_S50=0 / FQB_OZ_S56=0 turn the narrower spacings off.
+static int z_spacing(int64_t cw, int nsl) {
+    static const bool on56 = env_int("FQB_OZ_S56", 1) != 0;
+    static const bool on50 = on56 && env_int("FQB_OZ_S50", 1) != 0 && wide_default() && diags_default() == 8;
+    if (nsl != 7) return 64;
+    if (on50 && cw <= 50) return 50;
+    return (on56 && cw <= 56) ? 56 : 64;
+}
+
 template <bool PAIR>
 static void launch_pair_or_not(const OzArgs& a, int nsl, int S, cudaStream_t s, bool amn) {
     const bool s56 = nsl == 7 && S == 56;
+    if (nsl == 7 && S == 50) {
+        if (amn) launch_variant<PAIR, 7, 2, 50, 0, true, true>(a, s);
+        else launch_variant<PAIR, 7, 2, 50, 0, true>(a, s);
+        return;
+    }
     if (amn) {   // the MN-major reads of A'Y-layout slices: FP64-class, default schedules only
         if (s56 && wide_default()) launch_variant<PAIR, 7, 2, 56, 0, true, true>(a, s);
         else if (nsl == 7 && S == 64) launch_variant<PAIR, 7, 2, 64, 0, false, true>(a, s);

@@ -80,3 +80,13 @@ def test_trimmed_diagonals_stay_fp64_class(tmp_path, wide):
         assert float(e7.max()) <= 8 * u           # measured up to ~5.4 u at k = 65
         assert float(e8.max()) <= 3.6 * u         # the full scheme (test_gpu_ozaki's 4e-16 bar)
         assert not np.array_equal(c7, c8)          # the trimmed kernel really ran
+
+
+def test_s50_and_s56_spacings_give_identical_bits(tmp_path):
+    """Chunks of <= 50 columns on 50-row Z slices (10 MMAs per k-step, diagonal 7 partly
+    zeroed by tcgen05.st) against the 56-row spacing: the same exact int32 sums, so the same
+    bits -- paired (n = 100), single (n = 50) and ragged (n = 37, k = 65) launches."""
+    s50 = _run(tmp_path, {"FQB_OZ_S50": "1"}, "s50")
+    s56 = _run(tmp_path, {"FQB_OZ_S50": "0"}, "s56")
+    for a, b in zip(s50, s56):
+        assert np.array_equal(a.view(np.uint64), b.view(np.uint64))
