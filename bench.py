@@ -76,6 +76,8 @@ def peaks():
             mp = json.load(f)
         out["hbm_gbs"] = float(mp["hbm_gbs"])
         out["bf16_tflops"] = float(mp["bf16_tflops"])
+        if mp.get("bf16_tflops_sustained"):
+            out["bf16_tflops_sustained"] = float(mp["bf16_tflops_sustained"])
     except (OSError, ValueError, KeyError):
         out["hbm_gbs"] = 6650.0
         out["source"] = "fallback (B200_PROFILING.md: 6.65 TB/s)"
@@ -83,13 +85,17 @@ def peaks():
 
 
 def ozaki_int8_ops(rows_out: int, k: int, b: int) -> float:
-    """INT8 tensor-core operations one k_ozaki<*,7,*,56> launch executes (2 per MAC): per
-    128-row output tile, per 64-byte k-block and per column chunk (<= 56 columns) the
-    issue_s56 schedule runs MMAs of N = 400+400+336+288+224+176+112 = 1936 (ozaki.cu)."""
+    """INT8 tensor-core operations one k_ozaki<*,7,*,50|56> launch executes (2 per MAC): per
+    128-row output tile, per 64-byte k-block and per column chunk the schedule runs MMAs
+    of total N = 1744 for chunks of <= 50 columns (50-row Z spacing, 10 MMAs per 32-byte
+    k-step) or 1936 for chunks of <= 56 (ozaki.cu).  Equals ncu's
+    sm__ops_path_tensor_op_utcimma_src_int8_sparsity_off.sum (profiles/R3_ncu_ozaki_c4_s50_tn.txt)."""
     tiles = -(-rows_out // 128)
     kblocks = -(-k // 64)
     chunks = -(-b // 56)
-    return 2.0 * tiles * kblocks * chunks * 1936 * 128 * 64
+    width = -(-b // chunks)
+    n_rows = 1744 if width <= 50 else 1936
+    return 2.0 * tiles * kblocks * chunks * n_rows * 128 * 64
 
 
 def bench_config(world: int) -> dict:
@@ -225,10 +231,15 @@ def tensor_view(ms: float, pk: dict) -> dict:
     ops = ozaki_int8_ops(N, M, BLOCK)
     tops = ops / ms / 1e9
     meas = 2.0 * pk["bf16_tflops"] if pk.get("bf16_tflops") else None
+    sus = 2.0 * pk["bf16_tflops_sustained"] if pk.get("bf16_tflops_sustained") else None
     return {"int8_ops_per_launch": ops, "achieved_tops": tops, "peak_nominal_tops": 4500.0,
             "frac_nominal": tops / 4500.0, "peak_measured_equiv_tops": meas,
             "frac_measured_equiv": (tops / meas) if meas else None,
-            "note": "peak_measured_equiv = 2 x MEASURED_PEAKS bf16_tflops (no INT8 entry there)"}
+            "peak_measured_sustained_equiv_tops": sus,
+            "frac_measured_sustained_equiv": (tops / sus) if sus else None,
+            "note": "peak_measured_equiv = 2 x MEASURED_PEAKS bf16_tflops (burst), _sustained_ = 2 x "
+                    "bf16_tflops_sustained (seconds-long, power-capped: the regime of the timed step); "
+                    "no INT8 entry in MEASURED_PEAKS.json"}
 
 
 def sketch_roofline(eng, dev, pk):
@@ -281,7 +292,7 @@ def sketch_roofline(eng, dev, pk):
 
 
 def load_traffic():
-    for name in ("R2_traffic.json",):
+    for name in ("R3_traffic.json", "R2_traffic.json"):
         try:
             with open(os.path.join(ROOT, "profiles", name)) as f:
                 return json.load(f)
@@ -489,7 +500,7 @@ def run_ours(args):
                 "steps": e2e_steps},
         "gpu_launches": launches,
         "roofline": {"bound": "hbm",
-                     "kernel": "k_ozaki<true,7,2,56> (tcgen05 kind::i8 FP64 emulation, two 50-column chunks on "
+                     "kernel": "k_ozaki<true,7,2,50> (tcgen05 kind::i8 FP64 emulation, two 50-column chunks on "
                                "multicast CTA pairs) + k_ozaki_fixup: the A passes W = A'Y and Y = A G of the timed "
                                "steps",
                      "achieved": live_gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
