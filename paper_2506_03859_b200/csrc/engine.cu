@@ -195,6 +195,8 @@ class QbRun {
         if (oz_on_ && !std::isfinite(norm_a_sq_)) oz_on_ = false;
         // Q'X products on the INT8 path when the A passes are there and the rows are many
         q_oz_on_ = oz_on_ && q_oz_default() && m_ >= 4096;
+        // B G and B' T likewise (K = n, resp. the l columns of B')
+        b_oz_on_ = oz_on_ && b_oz_default() && n_ >= 4096;
     }
 
     double norm_a_sq() const { return norm_a_sq_; }
@@ -249,28 +251,29 @@ class QbRun {
         regrow(q_, ldq_);
         regrow(bt_, ldbt_);
         if (z_allowed_) regrow(rowsum_, 1);
-        if (q_oz_on_) {   // the slices of the committed Q columns move with Q
-            Workspace& w = h_.ws;
+        // the slices of the committed Q (B') columns move with Q (B')
+        auto regrow_slices = [&](DeviceArray<int8_t>& xs, DeviceArray<int>& xe, int64_t sliced, int64_t k) {
             const int nsl = ozaki_fp64_slices();
             DeviceArray<int8_t> fresh;
-            fresh.ensure(size_t(ozaki_x_bytes(nc, m_, nsl)), s_);
-            if (q_sliced_ > 0)
-                FQB_CUDA(cudaMemcpyAsync(fresh.ptr, w.oz_q_tn.ptr, size_t(ozaki_x_bytes(q_sliced_, m_, nsl)),
+            fresh.ensure(size_t(ozaki_x_bytes(nc, k, nsl)), s_);
+            if (sliced > 0)
+                FQB_CUDA(cudaMemcpyAsync(fresh.ptr, xs.ptr, size_t(ozaki_x_bytes(sliced, k, nsl)),
                                          cudaMemcpyDeviceToDevice, s_));
-            w.oz_q_tn.release();
-            w.oz_q_tn.ptr = fresh.detach();
-            w.oz_q_tn.count = size_t(ozaki_x_bytes(nc, m_, nsl));
-            w.oz_q_tn.stream = s_;
+            xs.release();
+            xs.ptr = fresh.detach();
+            xs.count = size_t(ozaki_x_bytes(nc, k, nsl));
+            xs.stream = s_;
             DeviceArray<int> fe;
             fe.ensure(size_t(nc), s_);
-            if (q_sliced_ > 0)
-                FQB_CUDA(cudaMemcpyAsync(fe.ptr, w.oz_q_e.ptr, sizeof(int) * size_t(q_sliced_), cudaMemcpyDeviceToDevice,
-                                         s_));
-            w.oz_q_e.release();
-            w.oz_q_e.ptr = fe.detach();
-            w.oz_q_e.count = size_t(nc);
-            w.oz_q_e.stream = s_;
-        }
+            if (sliced > 0)
+                FQB_CUDA(cudaMemcpyAsync(fe.ptr, xe.ptr, sizeof(int) * size_t(sliced), cudaMemcpyDeviceToDevice, s_));
+            xe.release();
+            xe.ptr = fe.detach();
+            xe.count = size_t(nc);
+            xe.stream = s_;
+        };
+        if (q_oz_on_) regrow_slices(h_.ws.oz_q_tn, h_.ws.oz_q_e, q_sliced_, m_);
+        if (b_oz_on_) regrow_slices(h_.ws.oz_b_tn, h_.ws.oz_b_e, b_sliced_, n_);
         cap_ = nc;
         Workspace& w = h_.ws;
         w.t.ensure(size_t(nc) * b_, s_);
@@ -491,6 +494,60 @@ class QbRun {
                     h_.gws.work, h_.num_sms, s_, h_.lc, nsl, w.oz_zmax.ptr);
     }
 
+    // ---- the B-side products on the INT8 tensor cores ---------------------------
+    // T = B G (K = n) and W -= B' T (K = l) for every committed column of B' -- 2 n l b
+    // flops each, three to four per block -- read B' from slices made once per committed
+    // column like Q's (A'Y layout: one operand row per column of B', a power-of-two scale
+    // per column; B' T reads them MN-major with T's rows scaled).  FQB_OZ_B=0: DMMA.
+    static bool b_oz_default() {
+        const char* e = std::getenv("FQB_OZ_B");
+        return !(e && e[0] == '0');
+    }
+    bool use_b_oz(int64_t l) const { return b_oz_on_ && l >= kQOzMinCols; }
+    void slice_b() {   // every committed column of B' not sliced yet (from its 128-column tile)
+        Workspace& w = h_.ws;
+        const int nsl = ozaki_fp64_slices();
+        const int64_t c0 = (std::min(b_sliced_, l_) / 128) * 128;
+        const int64_t cols = l_ - c0;
+        if (cols <= 0) return;
+        w.oz_q_line_max.ensure(size_t(ozaki_line_max_words(n_, cols)), s_);
+        ozaki_slice_a(bt_.ptr + c0 * ldbt_, n_, cols, ldbt_, w.oz_q_line_max.ptr,
+                      w.oz_b_tn.ptr + (c0 / 128) * (ozaki_x_bytes(128, n_, nsl)), w.oz_b_e.ptr + c0, nullptr, nullptr,
+                      s_, h_.lc, nullptr, nullptr, nsl);
+        b_sliced_ = l_;
+    }
+    // T (l x b, ldt) = B(:l, :) G   (G: n x b, ldg)
+    void b_tn(int64_t l, const double* G, int64_t ldg, double* T, int64_t ldt) {
+        if (!use_b_oz(l)) {
+            gemm_(true, l, b_, n_, 1.0, bt_.ptr, ldbt_, G, ldg, 0.0, T, ldt);
+            return;
+        }
+        slice_b();
+        Workspace& w = h_.ws;
+        const int nsl = ozaki_fp64_slices();
+        w.oz_z.ensure(size_t(ozaki_apply_z_bytes(n_, nsl)), s_);
+        w.oz_ez.ensure(size_t(ozaki_apply_ez_count()), s_);
+        w.oz_zmax.ensure(size_t(ozaki_apply_ez_count()), s_);
+        ozaki_apply(l, b_, n_, 1.0, w.oz_b_tn.ptr, w.oz_b_e.ptr, G, ldg, 0.0, T, ldt, w.oz_z.ptr, w.oz_ez.ptr,
+                    h_.gws.work, h_.num_sms, s_, h_.lc, nsl, w.oz_zmax.ptr);
+    }
+    // W (n x b, ldw) -= B(:l, :)' C   (C: l x b, ldc)
+    void b_mn_sub(int64_t l, const double* Cm, int64_t ldcm, double* W, int64_t ldw) {
+        if (!use_b_oz(l)) {
+            gemm_(false, n_, b_, l, -1.0, bt_.ptr, ldbt_, Cm, ldcm, 1.0, W, ldw);
+            return;
+        }
+        slice_b();
+        Workspace& w = h_.ws;
+        const int nsl = ozaki_fp64_slices();
+        w.oz_z.ensure(size_t(std::max(ozaki_apply_z_bytes(n_, nsl), ozaki_apply_z_bytes(l, nsl))), s_);
+        w.oz_ez.ensure(size_t(ozaki_apply_ez_count()), s_);
+        w.oz_zmax.ensure(size_t(ozaki_apply_ez_count()), s_);
+        w.oz_q_cs.ensure(size_t(l) * size_t(b_), s_);
+        ozaki_apply_mn(n_, b_, l, -1.0, w.oz_b_tn.ptr, w.oz_b_e.ptr, Cm, ldcm, 1.0, W, ldw, w.oz_q_cs.ptr, w.oz_z.ptr,
+                       w.oz_ez.ptr, h_.gws.work, h_.num_sms, s_, h_.lc, nsl, w.oz_zmax.ptr);
+    }
+
     // ---- Omega ----------------------------------------------------------------
     void make_block(int id) {
         Workspace& w = h_.ws;
@@ -617,7 +674,7 @@ class QbRun {
     void tmul_omega(double* t, int64_t ldt) {
         Workspace& w = h_.ws;
         if (om_dense_) {
-            gemm_(true, l_, b_, n_, 1.0, bt_.ptr, ldbt_, w.omega.ptr, ldo_, 0.0, t, ldt);
+            b_tn(l_, w.omega.ptr, ldo_, t, ldt);
             if (om_centered_ && !om_shift_folded_) {
                 // a dense block flagged centered: subtract p * rowsum(B) like the reference
                 throw Error(kStatusConfig, "dense centered blocks are not supported");
@@ -658,8 +715,8 @@ class QbRun {
             a_tn_reduced(b_, w.y0.ptr, ldq_, w.wp.ptr, ldbt_);   // W = sum_g A_g' Y_g
             if (l_ > 0) {
                 if (k == 1) tmul_omega(w.t.ptr, l_);
-                else gemm_(true, l_, b_, n_, 1.0, bt_.ptr, ldbt_, w.g.ptr, ldbt_, 0.0, w.t.ptr, l_);
-                gemm_(false, n_, b_, l_, -1.0, bt_.ptr, ldbt_, w.t.ptr, l_, 1.0, w.wp.ptr, ldbt_);
+                else b_tn(l_, w.g.ptr, ldbt_, w.t.ptr, l_);
+                b_mn_sub(l_, w.t.ptr, l_, w.wp.ptr, ldbt_);
             }
             if (k > 1 && P >= 3)
                 launch_axpy_cols_dev(scal_ + kAlpha, w.g.ptr, ldbt_, w.wp.ptr, ldbt_, n_, b_, s_, h_.lc);
@@ -719,7 +776,7 @@ class QbRun {
         gemm_(false, b, b, b, 1.0, R1i_, b, R2i_, b, 0.0, Ri_, b);              // R^-1 = R1^-1 R2^-1
         if (l > 0) {
             gemm_(false, l, b, b, 1.0, w.c2.ptr, l, R1_, b, 1.0, cd, ldcd);     // C = C1 + C2 R1
-            gemm_(false, n_, b, l, -1.0, bt_.ptr, ldbt_, cd, ldcd, 1.0, w.wraw.ptr, ldbt_);
+            b_mn_sub(l, cd, ldcd, w.wraw.ptr, ldbt_);
         }
         gemm_(false, n_, b, b, 1.0, w.wraw.ptr, ldbt_, Ri_, b, 0.0, btj, ldbt_);  // B_j'
         launch_sumsq(btj, n_, b, ldbt_, w.partial.ptr, scal_ + kBNorm, s_, h_.lc);
@@ -794,6 +851,8 @@ class QbRun {
     bool oz_ready_ = false;           // A sliced for this run (buffers live in the handle workspace)
     bool q_oz_on_ = false;            // Q'X products of the accept step on the INT8 tensor cores
     int64_t q_sliced_ = 0;            // columns of Q whose slices in ws.oz_q_tn are valid
+    bool b_oz_on_ = false;            // B G and B' T products on the INT8 tensor cores
+    int64_t b_sliced_ = 0;            // columns of B' whose slices in ws.oz_b_tn are valid
     static constexpr int64_t kQOzMinCols = 200;
     std::vector<double> residuals_;
     std::vector<int> ids_;

@@ -94,16 +94,20 @@ struct Workspace {
     DeviceArray<int8_t> oz_q_tn;   // Q in the A'Y layout (grown with Q; also read MN-major for Y -= Q C)
     DeviceArray<int> oz_q_e;
     DeviceArray<unsigned> oz_q_line_max, oz_zmax;
+    // B' (n x l) in the same layout (operand rows = rows of B, K = n), grown with B', for
+    // T = B G and W -= B' T (engine.cu, power_iterate / accept)
+    DeviceArray<int8_t> oz_b_tn;
+    DeviceArray<int> oz_b_e;
 
     // every member, while the stream the frees are ordered on still exists
     void release_all() {
         for (auto* d : {&omega, &y0, &ys, &wp, &wraw, &g, &t, &cd, &c2, &small, &zc, &rowsum_b, &splitk, &partial,
                         &scalars, &scratch, &a_copy, &values, &oz_norm_partial, &w_half, &oz_q_cs})
             d->release();
-        for (auto* d : {&col_ptr, &row_idx, &counts, &oz_e_nn, &oz_e_tn, &oz_ez, &oz_q_e}) d->release();
+        for (auto* d : {&col_ptr, &row_idx, &counts, &oz_e_nn, &oz_e_tn, &oz_ez, &oz_q_e, &oz_b_e}) d->release();
         for (auto* d : {&status, &gemm_flags, &oz_line_max, &oz_q_line_max, &oz_zmax}) d->release();
         a_copy_f32.release();
-        for (auto* d : {&oz_x_nn, &oz_x_tn, &oz_z, &oz_q_tn}) d->release();
+        for (auto* d : {&oz_x_nn, &oz_x_tn, &oz_z, &oz_q_tn, &oz_b_tn}) d->release();
     }
 };
 
