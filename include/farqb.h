@@ -25,6 +25,8 @@
  *   fqb_sym_eig             <- rsvd::sym_eig (matrix_core.hpp, matrix_core.cpp:50-115) as used by
  *                              assemble_svd (driver.cpp:296-345) for the l x l Gram matrices
  *   fqb_gemm                <- rsvd::kern::Ops::gemm_nn / gemm_tn (kernels.hpp:9-19)
+ *   fqb_chol_factor         <- rsvd::chol_factor (matrix_core.hpp:36-38, matrix_core.cpp:117-140),
+ *                              the b x b factorizations of the CholeskyQR steps
  *   fqb_philox_u32          <- rsvd::Philox::next_u32 (rng.hpp:21-24)
  *   fqb_random_orthonormal  <- rsvd::random_orthonormal (synthetic.hpp, synthetic.cpp:121-126)
  *   fqb_gen_synthetic       <- rsvd::gen_synthetic (synthetic.hpp, synthetic.cpp:159-180)
@@ -318,6 +320,15 @@ fqb_status fqb_sym_eig(fqb_handle h, const double* a, int n, int64_t lda, double
 fqb_status fqb_relative_error(fqb_handle h, const double* a, int64_t m, int64_t n, int64_t lda, int a_on_device,
                               const double* u, int64_t ldu, const double* sigma, const double* v, int64_t ldv,
                               int r, int factors_on_device, double* host_out);
+/* Cholesky of a symmetric n x n matrix Z (device pointers; Z must be symmetric), the
+ * reference's chol_factor: with max_diag = diag_ref if > 0, else max_i Z(i,i), a pivot
+ * (the Schur complement diagonal l(j,j)^2) at or below pivot_tol * max_diag makes
+ * *rank_deficient = 1 (the reference's RankDeficient) and R = R^-1 = I; otherwise
+ * *rank_deficient = 0, R (n x n, ldr) = L' (upper) and Rinv (ldri) = L'^-1 (upper) --
+ * the forms the CholeskyQR steps use.  One CTA, n <= 1024 (registers + one barrier per
+ * column for n <= 128, shared / global memory above). */
+fqb_status fqb_chol_factor(fqb_handle h, const double* z, int n, int64_t ldz, double pivot_tol, double diag_ref,
+                           double* r, int64_t ldr, double* rinv, int64_t ldri, int* rank_deficient);
 /* C (m x n) = alpha * op(A) * B + beta * C, op(A) = A (trans_a = 0, A is m x k)
  * or A' (trans_a = 1, A is k x m); B is k x n.  FP64 on the DMMA tensor pipe. */
 fqb_status fqb_gemm(fqb_handle h, int trans_a, int64_t m, int64_t n, int64_t k, double alpha,

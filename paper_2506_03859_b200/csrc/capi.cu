@@ -502,6 +502,39 @@ fqb_status fqb_relative_error(fqb_handle h, const double* a, int64_t m, int64_t 
     });
 }
 
+fqb_status fqb_chol_factor(fqb_handle h, const double* z, int n, int64_t ldz, double pivot_tol, double diag_ref,
+                           double* r, int64_t ldr, double* rinv, int64_t ldri, int* rank_deficient) {
+    return guarded([&]() -> fqb_status {
+        bind(h);
+        if (!z || !r || !rinv) throw farqb::Error(FQB_ERR_INVALID_ARGUMENT, "null pointer");
+        if (n < 0) throw farqb::Error(FQB_ERR_DIMENSION, "negative dimension");
+        if (n > 1024) throw farqb::Error(FQB_ERR_CONFIG, "fqb_chol_factor: n above 1024");
+        if (n > 0 && (ldz < n || ldr < n || ldri < n))
+            throw farqb::Error(FQB_ERR_DIMENSION, "leading dimension below n");
+        if (rank_deficient) *rank_deficient = 0;
+        if (n == 0) return FQB_OK;
+        cudaStream_t s = h->h.stream;
+        farqb::DeviceArray<double> rr, ri, scratch;
+        farqb::DeviceArray<unsigned> st;
+        rr.ensure(size_t(n) * n, s);
+        ri.ensure(size_t(n) * n, s);
+        scratch.ensure(size_t(n) * (n + 1), s);
+        st.ensure(1, s);
+        FQB_CUDA(cudaMemsetAsync(st.ptr, 0, sizeof(unsigned), s));
+        farqb::launch_chol_upper_inv(z, n, ldz, pivot_tol, diag_ref, nullptr, 0, rr.ptr, ri.ptr, nullptr,
+                                     scratch.ptr, st.ptr, 1u, s, h->h.lc);
+        FQB_CUDA(cudaMemcpy2DAsync(r, sizeof(double) * ldr, rr.ptr, sizeof(double) * n, sizeof(double) * n, n,
+                                   cudaMemcpyDeviceToDevice, s));
+        FQB_CUDA(cudaMemcpy2DAsync(rinv, sizeof(double) * ldri, ri.ptr, sizeof(double) * n, sizeof(double) * n, n,
+                                   cudaMemcpyDeviceToDevice, s));
+        unsigned hs = 0;
+        FQB_CUDA(cudaMemcpyAsync(&hs, st.ptr, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+        FQB_CUDA(cudaStreamSynchronize(s));
+        if (rank_deficient) *rank_deficient = hs ? 1 : 0;
+        return FQB_OK;
+    });
+}
+
 fqb_status fqb_gemm(fqb_handle h, int trans_a, int64_t m, int64_t n, int64_t k, double alpha,
                     const double* a, int64_t lda, const double* b, int64_t ldb, double beta, double* c,
                     int64_t ldc) {

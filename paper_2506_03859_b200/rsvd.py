@@ -674,6 +674,23 @@ class Engine:
             _raise(st, "fqb_sym_eig")
         return w, v, bool(used.value)
 
+    def chol_factor(self, z, pivot_tol: float = 1e-12, diag_ref: float = 0.0):
+        """rsvd::chol_factor on the device (fqb_chol_factor): a symmetric torch float64 n x n
+        (CUDA) -> (R = L', R^-1, rank_deficient) -- rank_deficient (R = R^-1 = I) when a pivot
+        falls to pivot_tol * max_diag, the reference's RankDeficient."""
+        import torch
+        n = int(z.shape[0])
+        zc = z.t().contiguous().t() if z.stride(0) != 1 else z
+        r = torch.empty((n, n), dtype=torch.float64, device=z.device).t()
+        ri = torch.empty((n, n), dtype=torch.float64, device=z.device).t()
+        bad = C.c_int(0)
+        st = self._lib.fqb_chol_factor(self._h, zc.data_ptr(), n, max(n, 1) if n <= 1 else zc.stride(1),
+                                       float(pivot_tol), float(diag_ref), r.data_ptr(), max(n, 1), ri.data_ptr(),
+                                       max(n, 1), C.byref(bad))
+        if st:
+            _raise(st, "fqb_chol_factor")
+        return r, ri, bool(bad.value)
+
     # ---- test matrices on the device (reference synthetic.cpp) -------------------
     def random_orthonormal(self, n: int, r: int, seed: int, stream: int = 0xFA000001):
         """rsvd::random_orthonormal on the device -> torch float64 n x r (column-major)."""
