@@ -27,6 +27,8 @@
  *   fqb_gemm                <- rsvd::kern::Ops::gemm_nn / gemm_tn (kernels.hpp:9-19)
  *   fqb_chol_factor         <- rsvd::chol_factor (matrix_core.hpp:36-38, matrix_core.cpp:117-140),
  *                              the b x b factorizations of the CholeskyQR steps
+ *   fqb_gram                <- rsvd::matmul_tn(y, y) (matrix_core.cpp:28-35) for the b x b Grams
+ *                              of accept_block / eig_svd (driver.cpp:230-294, matrix_core.cpp:193-215)
  *   fqb_philox_u32          <- rsvd::Philox::next_u32 (rng.hpp:21-24)
  *   fqb_random_orthonormal  <- rsvd::random_orthonormal (synthetic.hpp, synthetic.cpp:121-126)
  *   fqb_gen_synthetic       <- rsvd::gen_synthetic (synthetic.hpp, synthetic.cpp:159-180)
@@ -329,6 +331,10 @@ fqb_status fqb_relative_error(fqb_handle h, const double* a, int64_t m, int64_t 
  * column for n <= 128, shared / global memory above). */
 fqb_status fqb_chol_factor(fqb_handle h, const double* z, int n, int64_t ldz, double pivot_tol, double diag_ref,
                            double* r, int64_t ldr, double* rinv, int64_t ldri, int* rank_deficient);
+/* S (b x b, lds) = Y' Y for a tall Y (K x b, ldy), device pointers: for b <= 128 only the
+ * 8 x 8 tiles on and above the diagonal are formed and mirrored (S exactly symmetric),
+ * rows split over the SMs and the partials summed in a fixed order (deterministic). */
+fqb_status fqb_gram(fqb_handle h, const double* y, int64_t k, int b, int64_t ldy, double* s, int64_t lds);
 /* C (m x n) = alpha * op(A) * B + beta * C, op(A) = A (trans_a = 0, A is m x k)
  * or A' (trans_a = 1, A is k x m); B is k x n.  FP64 on the DMMA tensor pipe. */
 fqb_status fqb_gemm(fqb_handle h, int trans_a, int64_t m, int64_t n, int64_t k, double alpha,

@@ -535,6 +535,25 @@ fqb_status fqb_chol_factor(fqb_handle h, const double* z, int n, int64_t ldz, do
     });
 }
 
+fqb_status fqb_gram(fqb_handle h, const double* y, int64_t k, int b, int64_t ldy, double* s_out, int64_t lds) {
+    return guarded([&]() -> fqb_status {
+        bind(h);
+        if (!y || !s_out) throw farqb::Error(FQB_ERR_INVALID_ARGUMENT, "null pointer");
+        if (k < 0 || b < 0) throw farqb::Error(FQB_ERR_DIMENSION, "negative dimension");
+        if (b > 0 && (ldy < std::max<int64_t>(k, 1) || lds < b))
+            throw farqb::Error(FQB_ERR_DIMENSION, "leading dimension too small");
+        if (b == 0) return FQB_OK;
+        cudaStream_t s = h->h.stream;
+        farqb::ensure_gemm_workspace(h->h);
+        if (b <= 128 && k > 0)
+            farqb::ts_gram(y, k, b, ldy, 1.0, 0.0, s_out, lds, h->h.gws.work, h->h.gws.work_doubles, h->h.num_sms, s,
+                           h->h.lc);
+        else
+            farqb::gemm(true, b, b, k, 1.0, y, ldy, y, ldy, 0.0, s_out, lds, h->h.gws, h->h.num_sms, s, h->h.lc);
+        return FQB_OK;
+    });
+}
+
 fqb_status fqb_gemm(fqb_handle h, int trans_a, int64_t m, int64_t n, int64_t k, double alpha,
                     const double* a, int64_t lda, const double* b, int64_t ldb, double beta, double* c,
                     int64_t ldc) {

@@ -285,6 +285,19 @@ class QbRun {
                const double* B, int64_t ldb, double beta, double* C, int64_t ldc) {
         gemm(ta, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, h_.gws, h_.num_sms, s_, h_.lc);
     }
+    // S (b x b) = Y'Y for a tall Y (K x b): the symmetric tall-skinny kernel (tsmm.cu)
+    void gram_(const double* Y, int64_t K, int64_t ldy, double* S) {
+        if (ts_enabled() && b_ <= 128 &&
+            h_.gws.work_doubles >= ts_gram_workspace_doubles(b_, std::min<int>(h_.num_sms, 8))) {
+            ts_gram(Y, K, b_, ldy, 1.0, 0.0, S, b_, h_.gws.work, h_.gws.work_doubles, h_.num_sms, s_, h_.lc);
+            return;
+        }
+        gemm_(true, b_, b_, K, 1.0, Y, ldy, Y, ldy, 0.0, S, b_);
+    }
+    // Z (M x b) = Y R for a b x b R (the upper-triangular R^-1 factors)
+    void trmm_(const double* Y, int64_t M, int64_t ldy, const double* R, double* Z, int64_t ldz) {
+        gemm_(false, M, b_, b_, 1.0, Y, ldy, R, b_, 0.0, Z, ldz);
+    }
 
     // ---- A-pass products ------------------------------------------------------
     // C = A' B (ta) or A B with B of N <= b columns: the passes over A that dominate
@@ -688,7 +701,7 @@ class QbRun {
     // ---- orth(W) -> G (n x b) ---------------------------------------------------
     void orth_power(const double* wsrc, double* gdst, bool eig_mode, bool need_sigma) {
         const int b = b_;
-        gemm_(true, b, b, n_, 1.0, wsrc, ldbt_, wsrc, ldbt_, 0.0, S_, b);
+        gram_(wsrc, n_, ldbt_, S_);
         if (need_sigma || eig_mode) {
             launch_sym_eig(S_, b, b, eig_, eig_mode ? V_ : nullptr, VT_, status_, kStEigConv, s_, h_.lc);
         }
@@ -700,7 +713,7 @@ class QbRun {
             // one CholeskyQR pass: same span, orthonormal to the same u*cond^2 as eigSVD
             launch_chol_upper_inv(S_, b, b, 0.0, 0.0, nullptr, 0, R1_, R1i_, nullptr, h_.ws.scratch.ptr,
                                   status_, kStPowerChol, s_, h_.lc);
-            gemm_(false, n_, b, b, 1.0, wsrc, ldbt_, R1i_, b, 0.0, gdst, ldbt_);
+            trmm_(wsrc, n_, ldbt_, R1i_, gdst, ldbt_);
         }
     }
 
@@ -750,35 +763,35 @@ class QbRun {
         if (l == 0) {
             launch_chol_upper_inv(dblk, b, ldcd, 1e-12, 0.0, dblk, ldcd, R1_, R1i_, scal_ + kDMax,
                                   w.scratch.ptr, status_, kStAcceptPivot, s_, h_.lc);
-            gemm_(false, m_, b, b, 1.0, yj, ldq_, R1i_, b, 0.0, w.ys.ptr, ldq_);
+            trmm_(yj, m_, ldq_, R1i_, w.ys.ptr, ldq_);
         } else {
             if (use_q_mn(l)) {
                 q_mn_sub(l, cd, ldcd, yj);
             } else {
                 gemm_(false, m_, b, l, -1.0, q_.ptr, ldq_, cd, ldcd, 1.0, yj, ldq_);
             }
-            gemm_(true, b, b, m_, 1.0, yj, ldq_, yj, ldq_, 0.0, S_, b);
+            gram_(yj, m_, ldq_, S_);
             comm_allreduce_sum(h_, S_, size_t(b) * b, s_);
             launch_chol_upper_inv(S_, b, b, 1e-12, diag_max_, dblk, ldcd, R1_, R1i_, scal_ + kDMax,
                                   w.scratch.ptr, status_, kStAcceptPivot, s_, h_.lc);
-            gemm_(false, m_, b, b, 1.0, yj, ldq_, R1i_, b, 0.0, w.ys.ptr, ldq_);
+            trmm_(yj, m_, ldq_, R1i_, w.ys.ptr, ldq_);
             if (use_q_oz(l)) q_tn(l, w.ys.ptr, w.c2.ptr, l);
             else gemm_(true, l, b, m_, 1.0, q_.ptr, ldq_, w.ys.ptr, ldq_, 0.0, w.c2.ptr, l);
             comm_allreduce_sum(h_, w.c2.ptr, size_t(l) * b, s_);
             if (use_q_mn(l)) q_mn_sub(l, w.c2.ptr, l, w.ys.ptr);
             else gemm_(false, m_, b, l, -1.0, q_.ptr, ldq_, w.c2.ptr, l, 1.0, w.ys.ptr, ldq_);
         }
-        gemm_(true, b, b, m_, 1.0, w.ys.ptr, ldq_, w.ys.ptr, ldq_, 0.0, S2_, b);
+        gram_(w.ys.ptr, m_, ldq_, S2_);
         comm_allreduce_sum(h_, S2_, size_t(b) * b, s_);
         launch_chol_upper_inv(S2_, b, b, 0.0, 0.0, nullptr, 0, R2_, R2i_, nullptr, w.scratch.ptr, status_,
                               kStAcceptChol2, s_, h_.lc);
-        gemm_(false, m_, b, b, 1.0, w.ys.ptr, ldq_, R2i_, b, 0.0, yj, ldq_);  // Q_j
+        trmm_(w.ys.ptr, m_, ldq_, R2i_, yj, ldq_);  // Q_j
         gemm_(false, b, b, b, 1.0, R1i_, b, R2i_, b, 0.0, Ri_, b);              // R^-1 = R1^-1 R2^-1
         if (l > 0) {
             gemm_(false, l, b, b, 1.0, w.c2.ptr, l, R1_, b, 1.0, cd, ldcd);     // C = C1 + C2 R1
             b_mn_sub(l, cd, ldcd, w.wraw.ptr, ldbt_);
         }
-        gemm_(false, n_, b, b, 1.0, w.wraw.ptr, ldbt_, Ri_, b, 0.0, btj, ldbt_);  // B_j'
+        trmm_(w.wraw.ptr, n_, ldbt_, Ri_, btj, ldbt_);  // B_j'
         launch_sumsq(btj, n_, b, ldbt_, w.partial.ptr, scal_ + kBNorm, s_, h_.lc);
         if (need_rowsum_ && rowsum_cols_ == l) {
             launch_colsum(btj, n_, b, ldbt_, rowsum_.ptr + l, s_, h_.lc);

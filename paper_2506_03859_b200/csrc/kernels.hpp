@@ -111,6 +111,14 @@ void gemm_tma(bool trans_a, int64_t M, int64_t N, int64_t K, double alpha, const
               const double* B, int64_t ldb, double beta, double* C, int64_t ldc, double* work, unsigned* flags,
               unsigned epoch, int num_sms, cudaStream_t s, bool a3d_slack = false);
 
+// ---- tsmm.cu: the b x b Grams of the CholeskyQR steps (b <= 128) ----------------
+// S (b x b) = alpha Y'Y + beta S for Y (K x b): upper tiles only, mirrored, deterministic
+// (per-CTA partials in work, ts_gram_workspace_doubles, summed in CTA order)
+bool ts_enabled();   // FQB_TSMM=0: the general GEMMs instead
+int64_t ts_gram_workspace_doubles(int b, int num_sms);
+void ts_gram(const double* Y, int64_t K, int b, int64_t ldy, double alpha, double beta, double* S, int64_t lds,
+             double* work, int64_t work_doubles, int num_sms, cudaStream_t s, LaunchCounter& lc);
+
 // ---- ozaki.cu: FP64 GEMM on the INT8 tensor cores ------------------------------
 // Operands are int8 slices with one power-of-two exponent per operand row, stored
 // pre-tiled and pre-swizzled (ozaki_x_bytes / ozaki_z_bytes).  C (M x N) =

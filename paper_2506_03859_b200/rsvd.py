@@ -674,6 +674,21 @@ class Engine:
             _raise(st, "fqb_sym_eig")
         return w, v, bool(used.value)
 
+    def gram(self, y, out=None, sync: bool = True):
+        """S = y' y (fqb_gram) for a tall column-major torch float64 y (CUDA) -> torch b x b."""
+        import torch
+        k, b = int(y.shape[0]), int(y.shape[1])
+        ldy = y.stride(1) if (y.stride(0) == 1 and b > 1) else max(k, 1)
+        if y.stride(0) != 1:
+            raise InvalidArgument("gram: y must be column-major")
+        s = out if out is not None else torch.empty((b, b), dtype=torch.float64, device=y.device).t()
+        st = self._lib.fqb_gram(self._h, y.data_ptr(), k, b, ldy, s.data_ptr(), s.stride(1) if b > 1 else 1)
+        if st:
+            _raise(st, "fqb_gram")
+        if sync:
+            torch.cuda.synchronize(y.device)
+        return s
+
     def chol_factor(self, z, pivot_tol: float = 1e-12, diag_ref: float = 0.0):
         """rsvd::chol_factor on the device (fqb_chol_factor): a symmetric torch float64 n x n
         (CUDA) -> (R = L', R^-1, rank_deficient) -- rank_deficient (R = R^-1 = I) when a pivot

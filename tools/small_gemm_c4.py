@@ -57,6 +57,13 @@ for name, tr, M, N, K, cnt in shapes:
     print(f"{name:22s} {'TN' if tr else 'NN'} {M}x{N}x{K}: {us:7.1f} us  {2*M*N*K/us/1e6:6.2f} TF/s  x{cnt}/block")
 print(f"DMMA products per block at l={l}: {tot:.0f} us")
 
+# the Grams on the tall-skinny kernel (tsmm.cu: upper tiles only)
+for name, K in (("ts_gram S = W'W", n), ("ts_gram S = Y'Y (m)", m)):
+    y = cm(K, b)
+    s_out = cm(b, b)
+    us = timed(lambda: eng.gram(y, out=s_out, sync=False))
+    print(f"{name:22s} {K}x{b}: {us:7.1f} us ({2*K*b*b/us/1e6:6.2f} TF/s full-product equivalent)")
+
 # B-side products on the INT8 path: B' (n x l) sliced once
 bt = cm(n, l)
 g = cm(n, b)
