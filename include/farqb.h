@@ -29,6 +29,8 @@
  *                              the b x b factorizations of the CholeskyQR steps
  *   fqb_gram                <- rsvd::matmul_tn(y, y) (matrix_core.cpp:28-35) for the b x b Grams
  *                              of accept_block / eig_svd (driver.cpp:230-294, matrix_core.cpp:193-215)
+ *   fqb_mul_upper           <- trsm_right_lower_trans (matrix_core.cpp:167-179) given the inverse
+ *                              factor: Y R^-1 with R^-1 upper triangular
  *   fqb_philox_u32          <- rsvd::Philox::next_u32 (rng.hpp:21-24)
  *   fqb_random_orthonormal  <- rsvd::random_orthonormal (synthetic.hpp, synthetic.cpp:121-126)
  *   fqb_gen_synthetic       <- rsvd::gen_synthetic (synthetic.hpp, synthetic.cpp:159-180)
@@ -335,6 +337,10 @@ fqb_status fqb_chol_factor(fqb_handle h, const double* z, int n, int64_t ldz, do
  * 8 x 8 tiles on and above the diagonal are formed and mirrored (S exactly symmetric),
  * rows split over the SMs and the partials summed in a fixed order (deterministic). */
 fqb_status fqb_gram(fqb_handle h, const double* y, int64_t k, int b, int64_t ldy, double* s, int64_t lds);
+/* Z (M x b, ldz) = Y (M x b, ldy) * R with R (b x b, ldr) upper triangular -- its strictly
+ * lower part is not read.  Device pointers; Z must not overlap Y. */
+fqb_status fqb_mul_upper(fqb_handle h, const double* y, int64_t m, int b, int64_t ldy, const double* r, int64_t ldr,
+                         double* z, int64_t ldz);
 /* C (m x n) = alpha * op(A) * B + beta * C, op(A) = A (trans_a = 0, A is m x k)
  * or A' (trans_a = 1, A is k x m); B is k x n.  FP64 on the DMMA tensor pipe. */
 fqb_status fqb_gemm(fqb_handle h, int trans_a, int64_t m, int64_t n, int64_t k, double alpha,

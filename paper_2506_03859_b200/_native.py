@@ -105,6 +105,8 @@ SIGNATURES = [
     ("fqb_sym_eig", C.c_int, [_H, C.c_void_p, C.c_int, C.c_int64, C.c_void_p, C.c_void_p, C.c_int64,
                               C.POINTER(C.c_int)]),
     ("fqb_gram", C.c_int, [_H, C.c_void_p, C.c_int64, C.c_int, C.c_int64, C.c_void_p, C.c_int64]),
+    ("fqb_mul_upper", C.c_int, [_H, C.c_void_p, C.c_int64, C.c_int, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p,
+                                C.c_int64]),
     ("fqb_chol_factor", C.c_int, [_H, C.c_void_p, C.c_int, C.c_int64, C.c_double, C.c_double, C.c_void_p,
                                   C.c_int64, C.c_void_p, C.c_int64, C.POINTER(C.c_int)]),
     ("fqb_set_fp32_slices", C.c_int, [_H, C.c_int]),

@@ -554,6 +554,30 @@ fqb_status fqb_gram(fqb_handle h, const double* y, int64_t k, int b, int64_t ldy
     });
 }
 
+fqb_status fqb_mul_upper(fqb_handle h, const double* y, int64_t m, int b, int64_t ldy, const double* r, int64_t ldr,
+                         double* z, int64_t ldz) {
+    return guarded([&]() -> fqb_status {
+        bind(h);
+        if (!y || !r || !z) throw farqb::Error(FQB_ERR_INVALID_ARGUMENT, "null pointer");
+        if (m < 0 || b < 0) throw farqb::Error(FQB_ERR_DIMENSION, "negative dimension");
+        if (b > 0 && (ldy < std::max<int64_t>(m, 1) || ldz < std::max<int64_t>(m, 1) || ldr < b))
+            throw farqb::Error(FQB_ERR_DIMENSION, "leading dimension too small");
+        if (b == 0 || m == 0) return FQB_OK;
+        cudaStream_t s = h->h.stream;
+        if (farqb::ts_trmm(y, m, b, ldy, r, ldr, z, ldz, h->h.num_sms, s, h->h.lc)) return FQB_OK;
+        // b > 104: the general GEMM on a copy of R with its strictly lower part zeroed
+        farqb::ensure_gemm_workspace(h->h);
+        farqb::DeviceArray<double> ru;
+        ru.ensure(size_t(b) * b, s);
+        FQB_CUDA(cudaMemcpy2DAsync(ru.ptr, sizeof(double) * b, r, sizeof(double) * ldr, sizeof(double) * b, b,
+                                   cudaMemcpyDeviceToDevice, s));
+        for (int c = 0; c + 1 < b; ++c)
+            FQB_CUDA(cudaMemsetAsync(ru.ptr + int64_t(c) * b + c + 1, 0, sizeof(double) * (b - c - 1), s));
+        farqb::gemm(false, m, b, b, 1.0, y, ldy, ru.ptr, b, 0.0, z, ldz, h->h.gws, h->h.num_sms, s, h->h.lc);
+        return FQB_OK;
+    });
+}
+
 fqb_status fqb_gemm(fqb_handle h, int trans_a, int64_t m, int64_t n, int64_t k, double alpha,
                     const double* a, int64_t lda, const double* b, int64_t ldb, double beta, double* c,
                     int64_t ldc) {

@@ -294,8 +294,9 @@ class QbRun {
         }
         gemm_(true, b_, b_, K, 1.0, Y, ldy, Y, ldy, 0.0, S, b_);
     }
-    // Z (M x b) = Y R for a b x b R (the upper-triangular R^-1 factors)
+    // Z (M x b) = Y R for an upper-triangular b x b R (the R^-1 factors; tsmm.cu)
     void trmm_(const double* Y, int64_t M, int64_t ldy, const double* R, double* Z, int64_t ldz) {
+        if (ts_enabled() && ts_trmm(Y, M, b_, ldy, R, b_, Z, ldz, h_.num_sms, s_, h_.lc)) return;
         gemm_(false, M, b_, b_, 1.0, Y, ldy, R, b_, 0.0, Z, ldz);
     }
 

@@ -118,6 +118,10 @@ bool ts_enabled();   // FQB_TSMM=0: the general GEMMs instead
 int64_t ts_gram_workspace_doubles(int b, int num_sms);
 void ts_gram(const double* Y, int64_t K, int b, int64_t ldy, double alpha, double beta, double* S, int64_t lds,
              double* work, int64_t work_doubles, int num_sms, cudaStream_t s, LaunchCounter& lc);
+// Z (M x b) = Y R, R upper triangular b x b (its strictly lower part is not read);
+// false (nothing launched) when b > 104
+bool ts_trmm(const double* Y, int64_t M, int b, int64_t ldy, const double* R, int64_t ldr, double* Z, int64_t ldz,
+             int num_sms, cudaStream_t s, LaunchCounter& lc);
 
 // ---- ozaki.cu: FP64 GEMM on the INT8 tensor cores ------------------------------
 // Operands are int8 slices with one power-of-two exponent per operand row, stored

@@ -689,6 +689,21 @@ class Engine:
             torch.cuda.synchronize(y.device)
         return s
 
+    def mul_upper(self, y, r, sync: bool = True):
+        """Z = y r with r upper triangular (fqb_mul_upper; r's strictly lower part is not read)."""
+        import torch
+        m, b = int(y.shape[0]), int(y.shape[1])
+        if y.stride(0) != 1 or r.stride(0) != 1:
+            raise InvalidArgument("mul_upper: column-major operands")
+        z = torch.empty((b, m), dtype=torch.float64, device=y.device).t()
+        st = self._lib.fqb_mul_upper(self._h, y.data_ptr(), m, b, y.stride(1) if b > 1 else max(m, 1), r.data_ptr(),
+                                     r.stride(1) if b > 1 else 1, z.data_ptr(), max(m, 1))
+        if st:
+            _raise(st, "fqb_mul_upper")
+        if sync:
+            torch.cuda.synchronize(y.device)
+        return z
+
     def chol_factor(self, z, pivot_tol: float = 1e-12, diag_ref: float = 0.0):
         """rsvd::chol_factor on the device (fqb_chol_factor): a symmetric torch float64 n x n
         (CUDA) -> (R = L', R^-1, rank_deficient) -- rank_deficient (R = R^-1 = I) when a pivot

@@ -64,6 +64,12 @@ for name, K in (("ts_gram S = W'W", n), ("ts_gram S = Y'Y (m)", m)):
     us = timed(lambda: eng.gram(y, out=s_out, sync=False))
     print(f"{name:22s} {K}x{b}: {us:7.1f} us ({2*K*b*b/us/1e6:6.2f} TF/s full-product equivalent)")
 
+for name, M in (("ts_trmm G = W R^-1", n), ("ts_trmm ys = Y R^-1 (m)", m)):
+    y = cm(M, b)
+    r = torch.triu(cm(b, b)).t().contiguous().t()
+    us = timed(lambda: eng.mul_upper(y, r, sync=False))
+    print(f"{name:22s} {M}x{b}: {us:7.1f} us ({2*M*b*b/us/1e6:6.2f} TF/s full-product equivalent)")
+
 # B-side products on the INT8 path: B' (n x l) sliced once
 bt = cm(n, l)
 g = cm(n, b)

@@ -12,7 +12,9 @@ eng = fqb.Engine(0)
 b = 100
 for rows in (100000, 20000):
     y = torch.randn(b, rows, dtype=torch.float64, device="cuda").t()
+    r = torch.triu(torch.randn(b, b, dtype=torch.float64, device="cuda")).t().contiguous().t()
     for _ in range(2):
         s = eng.gram(y)
+        z = eng.mul_upper(y, r)
 torch.cuda.synchronize()
 print("done", float(s.abs().sum()))
