@@ -612,8 +612,8 @@ fqb_status fqb_gemm_emulated(fqb_handle h, int trans_a, int64_t m, int64_t n, in
         ex.ensure(size_t(m), s);
         ez.ensure(size_t(farqb::ozaki_apply_ez_count()), s);
         farqb::DeviceArray<unsigned> line_max, zmax;
-        line_max.ensure(size_t(farqb::ozaki_line_max_words(m, k)), s);
-        zmax.ensure(size_t(farqb::ozaki_apply_ez_count()), s);
+        line_max.ensure_zeroed(size_t(farqb::ozaki_line_max_words(m, k)), s);
+        zmax.ensure_zeroed(size_t(farqb::ozaki_apply_ez_count()), s);
         if (trans_a) farqb::ozaki_slice_a(a, k, m, lda, line_max.ptr, xs.ptr, ex.ptr, nullptr, nullptr, s, h->h.lc);
         else farqb::ozaki_slice_a(a, m, k, lda, line_max.ptr, nullptr, nullptr, xs.ptr, ex.ptr, s, h->h.lc);
         farqb::ozaki_apply(m, n, k, alpha, xs.ptr, ex.ptr, b, ldb, beta, c, ldc, zs.ptr, ez.ptr, h->h.gws.work,
@@ -655,7 +655,7 @@ fqb_status fqb_slice_operand(fqb_handle h, const double* a, int64_t m, int64_t n
             sl->e_tn.ensure(size_t(n), s);
             sl->ez.ensure(size_t(farqb::ozaki_apply_ez_count()), s);
             farqb::DeviceArray<unsigned> line_max;
-            line_max.ensure(size_t(farqb::ozaki_line_max_words(m, n)), s);
+            line_max.ensure_zeroed(size_t(farqb::ozaki_line_max_words(m, n)), s);
             farqb::ozaki_slice_a(a, m, n, lda, line_max.ptr, sl->x_tn.ptr, sl->e_tn.ptr, sl->x_nn.ptr, sl->e_nn.ptr, s,
                                  h->h.lc);
         } catch (...) {
@@ -679,7 +679,7 @@ fqb_status fqb_sliced_gemm(fqb_handle h, fqb_sliced sl, int trans_a, int64_t nb,
         cudaStream_t s = h->h.stream;
         farqb::ensure_gemm_workspace(h->h);
         sl->z.ensure(size_t(farqb::ozaki_apply_z_bytes(K)), s);
-        sl->zmax.ensure(size_t(farqb::ozaki_apply_ez_count()), s);
+        sl->zmax.ensure_zeroed(size_t(farqb::ozaki_apply_ez_count()), s);
         farqb::ozaki_apply(M, nb, K, alpha, trans_a ? sl->x_tn.ptr : sl->x_nn.ptr,
                            trans_a ? sl->e_tn.ptr : sl->e_nn.ptr, b, ldb, beta, c, ldc, sl->z.ptr, sl->ez.ptr,
                            h->h.gws.work, h->h.num_sms, s, h->h.lc, farqb::ozaki_fp64_slices(), sl->zmax.ptr);
@@ -701,7 +701,7 @@ fqb_status fqb_sliced_gemm_mn(fqb_handle h, fqb_sliced sl, int64_t nb, double al
         cudaStream_t s = h->h.stream;
         farqb::ensure_gemm_workspace(h->h);
         sl->z.ensure(size_t(farqb::ozaki_apply_z_bytes(K)), s);
-        sl->zmax.ensure(size_t(farqb::ozaki_apply_ez_count()), s);
+        sl->zmax.ensure_zeroed(size_t(farqb::ozaki_apply_ez_count()), s);
         sl->cs.ensure(size_t(K) * size_t(nb), s);
         farqb::ozaki_apply_mn(M, nb, K, alpha, sl->x_tn.ptr, sl->e_tn.ptr, b, ldb, beta, c, ldc, sl->cs.ptr,
                               sl->z.ptr, sl->ez.ptr, h->h.gws.work, h->h.num_sms, s, h->h.lc,

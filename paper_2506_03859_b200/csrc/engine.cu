@@ -328,7 +328,7 @@ class QbRun {
         }
         w.oz_e_nn.ensure(size_t(m_), s_);
         w.oz_e_tn.ensure(size_t(n_), s_);
-        w.oz_line_max.ensure(size_t(ozaki_line_max_words(m_, n_)), s_);
+        w.oz_line_max.ensure_zeroed(size_t(ozaki_line_max_words(m_, n_)), s_);
         if (norm_out) w.oz_norm_partial.ensure(size_t(std::max<int64_t>(1, ozaki_norm_partials(m_, n_))), s_);
         double* np = norm_out ? w.oz_norm_partial.ptr : nullptr;
         if (af_)
@@ -376,7 +376,7 @@ class QbRun {
         Workspace& w = h_.ws;
         w.oz_z.ensure(size_t(ozaki_apply_z_bytes(K, oz_nsl_)), s_);
         w.oz_ez.ensure(size_t(ozaki_apply_ez_count()), s_);
-        w.oz_zmax.ensure(size_t(ozaki_apply_ez_count()), s_);
+        w.oz_zmax.ensure_zeroed(size_t(ozaki_apply_ez_count()), s_);
         PassTimerScope timed(h_);
         ozaki_apply(M, N, K, 1.0, ta ? w.oz_x_tn.ptr : w.oz_x_nn.ptr, ta ? w.oz_e_tn.ptr : w.oz_e_nn.ptr, B, ldb, 0.0,
                     C, ldc, w.oz_z.ptr, w.oz_ez.ptr, h_.gws.work, h_.num_sms, s_, h_.lc, oz_nsl_, w.oz_zmax.ptr);
@@ -448,7 +448,7 @@ class QbRun {
         }
         w.oz_z.ensure(size_t(ozaki_apply_z_bytes(m_, oz_nsl_)), s_);
         w.oz_ez.ensure(size_t(ozaki_apply_ez_count()), s_);
-        w.oz_zmax.ensure(size_t(ozaki_apply_ez_count()), s_);
+        w.oz_zmax.ensure_zeroed(size_t(ozaki_apply_ez_count()), s_);
         ozaki_apply(rows, N, m_, 1.0, xs, w.oz_e_tn.ptr + r0, B, ldb, 0.0, C + r0, ldc, w.oz_z.ptr, w.oz_ez.ptr,
                     h_.gws.work, h_.num_sms, s_, h_.lc, oz_nsl_, w.oz_zmax.ptr);
     }
@@ -479,7 +479,7 @@ class QbRun {
         const int nsl = ozaki_fp64_slices();
         w.oz_z.ensure(size_t(std::max(ozaki_apply_z_bytes(m_, nsl), ozaki_apply_z_bytes(l, nsl))), s_);
         w.oz_ez.ensure(size_t(ozaki_apply_ez_count()), s_);
-        w.oz_zmax.ensure(size_t(ozaki_apply_ez_count()), s_);
+        w.oz_zmax.ensure_zeroed(size_t(ozaki_apply_ez_count()), s_);
         w.oz_q_cs.ensure(size_t(l) * size_t(b_), s_);
         ozaki_apply_mn(m_, b_, l, -1.0, w.oz_q_tn.ptr, w.oz_q_e.ptr, Cm, ldcm, 1.0, Y, ldq_, w.oz_q_cs.ptr,
                        w.oz_z.ptr, w.oz_ez.ptr, h_.gws.work, h_.num_sms, s_, h_.lc, nsl, w.oz_zmax.ptr);
@@ -492,7 +492,7 @@ class QbRun {
         const int64_t c0 = (std::min(q_sliced_, l_) / 128) * 128;
         const int64_t cols = upto - c0;
         if (cols <= 0) return;
-        w.oz_q_line_max.ensure(size_t(ozaki_line_max_words(m_, cols)), s_);
+        w.oz_q_line_max.ensure_zeroed(size_t(ozaki_line_max_words(m_, cols)), s_);
         ozaki_slice_a(q_.ptr + c0 * ldq_, m_, cols, ldq_, w.oz_q_line_max.ptr,
                       w.oz_q_tn.ptr + (c0 / 128) * (ozaki_x_bytes(128, m_, nsl)), w.oz_q_e.ptr + c0, nullptr, nullptr,
                       s_, h_.lc, nullptr, nullptr, nsl);
@@ -503,7 +503,7 @@ class QbRun {
         const int nsl = ozaki_fp64_slices();
         w.oz_z.ensure(size_t(ozaki_apply_z_bytes(m_, nsl)), s_);
         w.oz_ez.ensure(size_t(ozaki_apply_ez_count()), s_);
-        w.oz_zmax.ensure(size_t(ozaki_apply_ez_count()), s_);
+        w.oz_zmax.ensure_zeroed(size_t(ozaki_apply_ez_count()), s_);
         ozaki_apply(M, b_, m_, 1.0, w.oz_q_tn.ptr, w.oz_q_e.ptr, B, ldq_, 0.0, C, ldc, w.oz_z.ptr, w.oz_ez.ptr,
                     h_.gws.work, h_.num_sms, s_, h_.lc, nsl, w.oz_zmax.ptr);
     }
@@ -524,7 +524,7 @@ class QbRun {
         const int64_t c0 = (std::min(b_sliced_, l_) / 128) * 128;
         const int64_t cols = l_ - c0;
         if (cols <= 0) return;
-        w.oz_q_line_max.ensure(size_t(ozaki_line_max_words(n_, cols)), s_);
+        w.oz_q_line_max.ensure_zeroed(size_t(ozaki_line_max_words(n_, cols)), s_);
         ozaki_slice_a(bt_.ptr + c0 * ldbt_, n_, cols, ldbt_, w.oz_q_line_max.ptr,
                       w.oz_b_tn.ptr + (c0 / 128) * (ozaki_x_bytes(128, n_, nsl)), w.oz_b_e.ptr + c0, nullptr, nullptr,
                       s_, h_.lc, nullptr, nullptr, nsl);
@@ -541,7 +541,7 @@ class QbRun {
         const int nsl = ozaki_fp64_slices();
         w.oz_z.ensure(size_t(ozaki_apply_z_bytes(n_, nsl)), s_);
         w.oz_ez.ensure(size_t(ozaki_apply_ez_count()), s_);
-        w.oz_zmax.ensure(size_t(ozaki_apply_ez_count()), s_);
+        w.oz_zmax.ensure_zeroed(size_t(ozaki_apply_ez_count()), s_);
         ozaki_apply(l, b_, n_, 1.0, w.oz_b_tn.ptr, w.oz_b_e.ptr, G, ldg, 0.0, T, ldt, w.oz_z.ptr, w.oz_ez.ptr,
                     h_.gws.work, h_.num_sms, s_, h_.lc, nsl, w.oz_zmax.ptr);
     }
@@ -556,7 +556,7 @@ class QbRun {
         const int nsl = ozaki_fp64_slices();
         w.oz_z.ensure(size_t(std::max(ozaki_apply_z_bytes(n_, nsl), ozaki_apply_z_bytes(l, nsl))), s_);
         w.oz_ez.ensure(size_t(ozaki_apply_ez_count()), s_);
-        w.oz_zmax.ensure(size_t(ozaki_apply_ez_count()), s_);
+        w.oz_zmax.ensure_zeroed(size_t(ozaki_apply_ez_count()), s_);
         w.oz_q_cs.ensure(size_t(l) * size_t(b_), s_);
         ozaki_apply_mn(n_, b_, l, -1.0, w.oz_b_tn.ptr, w.oz_b_e.ptr, Cm, ldcm, 1.0, W, ldw, w.oz_q_cs.ptr, w.oz_z.ptr,
                        w.oz_ez.ptr, h_.gws.work, h_.num_sms, s_, h_.lc, nsl, w.oz_zmax.ptr);

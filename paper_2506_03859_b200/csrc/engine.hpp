@@ -66,6 +66,14 @@ struct DeviceArray {
         }
         return ptr;
     }
+    // as ensure, and a new allocation is zero-filled: the generation-tagged line maxima of
+    // ozaki.cu rely on never finding a word tagged above the current generation
+    T* ensure_zeroed(size_t n, cudaStream_t s) {
+        if (n <= count && ptr) return ptr;
+        ensure(n, s);
+        FQB_CUDA(cudaMemsetAsync(ptr, 0, count * sizeof(T), s));
+        return ptr;
+    }
     // hand ownership to the caller
     T* detach() {
         T* p = ptr;

@@ -157,7 +157,9 @@ int64_t ozaki_workspace_doubles(int num_sms);
 // Slices of A (m x n, ld) in both layouts from one pass (either may be null):
 //   x_tn / e_tn: operand rows = columns of A, K = m   (A' Y)
 //   x_nn / e_nn: operand rows = rows of A,    K = n   (A G)
-// line_max: ozaki_line_max_words(m, n) words of scratch.  With norm_out, ||A||_F^2
+// line_max: ozaki_line_max_words(m, n) words of scratch, zero-filled once when allocated
+// (DeviceArray::ensure_zeroed): the maxima are tagged with a per-call generation, so no
+// memset is needed between calls.  With norm_out, ||A||_F^2
 // comes out of the same read of A (norm_partial: ozaki_norm_partials(m, n) doubles).
 int64_t ozaki_line_max_words(int64_t m, int64_t n);
 int64_t ozaki_norm_partials(int64_t m, int64_t n);
@@ -173,8 +175,9 @@ void ozaki_slice_z(const double* b, int64_t k, int64_t n, int64_t ld, int* e, in
 // C = alpha X' B + beta C for any N: B (K x N, ld, FP64) sliced in chunks of <= 64
 // columns into z (ozaki_apply_z_bytes(K)) / ez (ozaki_apply_ez_count()); N > 64
 // runs two chunks at a time on CTA pairs sharing the A tiles (FQB_OZ_PAIR=0: off)
-// zmax: ozaki_apply_ez_count() words of scratch; lets a long B (K > 16384 rows) take its
-// column maxima in one pass before slicing (null: the one-kernel slicer)
+// zmax: ozaki_apply_ez_count() words of scratch, zero-filled once when allocated (as
+// line_max); lets a long B (K > 16384 rows) take its column maxima in one pass before
+// slicing (null: the one-kernel slicer)
 void ozaki_apply(int64_t M, int64_t N, int64_t K, double alpha, const int8_t* xs, const int* ex, const double* b,
                  int64_t ldb, double beta, double* C, int64_t ldc, int8_t* z, int* ez, double* work, int num_sms,
                  cudaStream_t s, LaunchCounter& lc, int nsl = ozaki_fp64_slices(), unsigned* zmax = nullptr);

@@ -48,6 +48,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
@@ -761,6 +762,15 @@ __device__ __forceinline__ int exp_of_hi(unsigned hi) {
     return hi >= 0x7FF00000u ? kNonFiniteE : hi >= 0x00100000u ? int(hi >> 20) - 1022 : -1021;
 }
 
+// Line maxima are atomicMax'ed as (generation << 32 | high word): a word left by an
+// earlier call carries a smaller generation and reads as 0, so the buffers need no
+// memset between calls (a memset node would also break the programmatic-launch chain).
+typedef unsigned long long u64;
+__device__ __forceinline__ void max_tagged(u64* w, unsigned gen, unsigned v) {
+    if (v) atomicMax(w, (u64(gen) << 32) | v);
+}
+__device__ __forceinline__ unsigned untag(u64 w, unsigned gen) { return unsigned(w >> 32) == gen ? unsigned(w) : 0u; }
+
 // the 8 digits of x in line scale e, as raw fields d_p + 64 in [0, 128]: the 7-bit
 // fields of U = R + sum_p 64 2^(49-7p), read from its two 32-bit halves
 __device__ __forceinline__ void digits8(double x, int e, unsigned (&d)[8]) {
@@ -878,13 +888,13 @@ __device__ __forceinline__ void put_chunk16_z(const double (&v)[16], int e, int8
     }
 }
 
-// Row and column maxima (high words) of A (m x n, ld) in one pass; rmax / cmax
-// must be zeroed.  CTA: 256 rows x 128 columns, a thread walks one row.  With
+// Row and column maxima (high words) of A (m x n, ld) in one pass, tagged with this
+// call's generation (max_tagged).  CTA: 256 rows x 128 columns, a thread walks one row.  With
 // norm_partial it also writes the CTA's sum of squares (||A||_F^2, reduced by
 // ozaki_slice_a in CTA order), so the engine does not read A a third time.
 template <typename T>   // double, or float A (FP32 input mode: widened exactly)
 __global__ void __launch_bounds__(256) k_line_max(const T* __restrict__ a, int64_t m, int64_t n, int64_t ld,
-                                                  unsigned* rmax, unsigned* cmax, double* norm_partial) {
+                                                  u64* rmax, u64* cmax, unsigned gen, double* norm_partial) {
     FQB_PDL_ENTRY();
     __shared__ unsigned cm[8][128];
     __shared__ double red[8];
@@ -903,7 +913,7 @@ __global__ void __launch_bounds__(256) k_line_max(const T* __restrict__ a, int64
         const unsigned wm = __reduce_max_sync(0xFFFFFFFFu, h);
         if (lane == 0) cm[warp][c] = wm;
     }
-    if (i < m && rm) atomicMax(rmax + i, rm);
+    if (i < m) max_tagged(rmax + i, gen, rm);
     if (norm_partial) {
         double t = (sq[0] + sq[1]) + (sq[2] + sq[3]);
 #pragma unroll
@@ -921,7 +931,7 @@ __global__ void __launch_bounds__(256) k_line_max(const T* __restrict__ a, int64
         unsigned v = 0;
 #pragma unroll
         for (int w = 0; w < 8; ++w) v = max(v, cm[w][threadIdx.x]);
-        if (v) atomicMax(cmax + j0 + threadIdx.x, v);
+        max_tagged(cmax + j0 + threadIdx.x, gen, v);
     }
 }
 
@@ -951,7 +961,7 @@ __global__ void __launch_bounds__(1024) k_sum_ordered(const double* __restrict__
 // both slice buffers is written (zeros outside A) and no memset is needed.
 template <typename T, int NSL>
 __global__ void __launch_bounds__(256) k_slice_a(const T* __restrict__ a, int64_t m, int64_t n, int64_t ld,
-                                                 const unsigned* __restrict__ rmax, const unsigned* __restrict__ cmax,
+                                                 const u64* __restrict__ rmax, const u64* __restrict__ cmax, unsigned gen,
                                                  int8_t* x_tn, int* e_tn, int8_t* x_nn, int* e_nn) {
     FQB_PDL_ENTRY();
     __shared__ double t[64][65];   // t[j][i]
@@ -978,7 +988,7 @@ __global__ void __launch_bounds__(256) k_slice_a(const T* __restrict__ a, int64_
     const int line = threadIdx.x >> 2, q = threadIdx.x & 3;   // 64 lines x 4 chunks of 16
     if (x_tn && i0 < round_up_dev(m, OZ_BK)) {                  // columns of A: rows j, K = i
         const int64_t j = j0 + line;
-        const int e = j < n ? exp_of_hi(cmax[j]) : -1021;
+        const int e = j < n ? exp_of_hi(untag(cmax[j], gen)) : -1021;
         if (e_tn && blockIdx.x == 0 && j < n && q == 0) e_tn[j] = e;
         double v[16];
 #pragma unroll
@@ -989,7 +999,7 @@ __global__ void __launch_bounds__(256) k_slice_a(const T* __restrict__ a, int64_
     }
     if (x_nn && j0 < round_up_dev(n, OZ_BK)) {                  // rows of A: rows i, K = j
         const int64_t i = i0 + line;
-        const int e = i < m ? exp_of_hi(rmax[i]) : -1021;
+        const int e = i < m ? exp_of_hi(untag(rmax[i], gen)) : -1021;
         if (e_nn && blockIdx.y == 0 && i < m && q == 0) e_nn[i] = e;
         double v[16];
 #pragma unroll
@@ -1066,7 +1076,7 @@ __global__ void __launch_bounds__(ZT) k_slice_z(const double* __restrict__ b, in
 constexpr int64_t kZFused = 16384;
 constexpr int ZMAX_PER_CTA = 8192;
 __global__ void __launch_bounds__(256) k_zcol_max(const double* __restrict__ b, int64_t k, int64_t n, int64_t ld,
-                                                  unsigned* cmax) {
+                                                  u64* cmax, unsigned gen) {
     FQB_PDL_ENTRY();
     __shared__ unsigned wmax[8];
     const int j = blockIdx.x;
@@ -1092,13 +1102,13 @@ __global__ void __launch_bounds__(256) k_zcol_max(const double* __restrict__ b, 
         unsigned mx = 0;
 #pragma unroll
         for (int w = 0; w < 8; ++w) mx = max(mx, wmax[w]);
-        if (mx) atomicMax(cmax + j, mx);
+        max_tagged(cmax + j, gen, mx);
     }
 }
 
 template <int NSL, int S>
 __global__ void __launch_bounds__(256) k_slice_z_kb(const double* __restrict__ b, int64_t k, int64_t n, int64_t ld,
-                                                    const unsigned* __restrict__ cmax, int* ez, int8_t* out) {
+                                                    const u64* __restrict__ cmax, unsigned gen, int* ez, int8_t* out) {
     FQB_PDL_ENTRY();
     constexpr int ZR = z_block_rows(NSL, S);
     const int kb = blockIdx.x;
@@ -1112,7 +1122,7 @@ __global__ void __launch_bounds__(256) k_slice_z_kb(const double* __restrict__ b
         return;
     }
     const bool live = j < n;
-    const int e = live ? exp_of_hi(cmax[j]) : exp_of_hi(0u);
+    const int e = live ? exp_of_hi(untag(cmax[j], gen)) : exp_of_hi(0u);
     if (live && kb == 0 && q == 0) ez[j] = e;
     const double* col = b + int64_t(j) * ld;
     double v[16];
@@ -1186,7 +1196,14 @@ static void check_nsl(int nsl) {
         throw Error(kStatusInvalid, "ozaki: slices per operand must be 8, 7, 4 or 3");
 }
 
-int64_t ozaki_line_max_words(int64_t m, int64_t n) { return m + n; }
+int64_t ozaki_line_max_words(int64_t m, int64_t n) { return 2 * (m + n); }   // generation-tagged 64-bit maxima
+// one generation per maxima pass (host-side, process-wide, never reused before 2^32 calls)
+static unsigned next_generation() {
+    static std::atomic<unsigned> g{0};
+    unsigned v = ++g;
+    if (v == 0) v = ++g;
+    return v;
+}
 int64_t ozaki_norm_partials(int64_t m, int64_t n) { return ceil_div(m, 256) * ceil_div(n, 128); }
 
 template <typename T>
@@ -1198,11 +1215,11 @@ static void slice_a_impl(const T* a, int64_t m, int64_t n, int64_t ld, unsigned*
         if (norm_out) FQB_CUDA(cudaMemsetAsync(norm_out, 0, sizeof(double), s));
         return;
     }
-    unsigned* rmax = line_max;
-    unsigned* cmax = line_max + m;
-    FQB_CUDA(cudaMemsetAsync(line_max, 0, sizeof(unsigned) * size_t(m + n), s));
+    u64* rmax = reinterpret_cast<u64*>(line_max);
+    u64* cmax = rmax + m;
+    const unsigned gen = next_generation();
     launch_k(k_line_max<T>, dim3(unsigned(ceil_div(m, 256)), unsigned(ceil_div(n, 128))), 256, 0, s, a, m, n, ld, rmax,
-             cmax, norm_out ? norm_partial : nullptr);
+             cmax, gen, norm_out ? norm_partial : nullptr);
     FQB_LAUNCHED();
     if (norm_out) {
         launch_k(k_sum_ordered, 1, 1024, 0, s, norm_partial, ozaki_norm_partials(m, n), norm_out);
@@ -1211,10 +1228,10 @@ static void slice_a_impl(const T* a, int64_t m, int64_t n, int64_t ld, unsigned*
     }
     // cover the padded operand rows of both layouts (multiples of OZ_BM)
     const dim3 g(unsigned(ceil_div(m, OZ_BM) * (OZ_BM / 64)), unsigned(ceil_div(n, OZ_BM) * (OZ_BM / 64)));
-    if (nsl == 8) launch_k(k_slice_a<T, 8>, g, 256, 0, s, a, m, n, ld, rmax, cmax, x_tn, e_tn, x_nn, e_nn);
-    else if (nsl == 7) launch_k(k_slice_a<T, 7>, g, 256, 0, s, a, m, n, ld, rmax, cmax, x_tn, e_tn, x_nn, e_nn);
-    else if (nsl == 3) launch_k(k_slice_a<T, 3>, g, 256, 0, s, a, m, n, ld, rmax, cmax, x_tn, e_tn, x_nn, e_nn);
-    else launch_k(k_slice_a<T, 4>, g, 256, 0, s, a, m, n, ld, rmax, cmax, x_tn, e_tn, x_nn, e_nn);
+    if (nsl == 8) launch_k(k_slice_a<T, 8>, g, 256, 0, s, a, m, n, ld, rmax, cmax, gen, x_tn, e_tn, x_nn, e_nn);
+    else if (nsl == 7) launch_k(k_slice_a<T, 7>, g, 256, 0, s, a, m, n, ld, rmax, cmax, gen, x_tn, e_tn, x_nn, e_nn);
+    else if (nsl == 3) launch_k(k_slice_a<T, 3>, g, 256, 0, s, a, m, n, ld, rmax, cmax, gen, x_tn, e_tn, x_nn, e_nn);
+    else launch_k(k_slice_a<T, 4>, g, 256, 0, s, a, m, n, ld, rmax, cmax, gen, x_tn, e_tn, x_nn, e_nn);
     FQB_LAUNCHED();
     lc.bump(2);
 }
@@ -1234,10 +1251,12 @@ void ozaki_slice_a(const float* a, int64_t m, int64_t n, int64_t ld, unsigned* l
 template <int NSL, int S>
 static void slice_z_long(const double* b, int64_t k, int64_t n, int64_t ld, int* e, int8_t* out, unsigned* cmax,
                          cudaStream_t s, LaunchCounter& lc) {
-    FQB_CUDA(cudaMemsetAsync(cmax, 0, sizeof(unsigned) * OZ_BN, s));
-    launch_k(k_zcol_max, dim3(unsigned(n), unsigned(ceil_div(k, ZMAX_PER_CTA))), 256, 0, s, b, k, n, ld, cmax);
+    u64* cm = reinterpret_cast<u64*>(cmax);   // OZ_BN tagged words (2 OZ_BN unsigned)
+    const unsigned gen = next_generation();
+    launch_k(k_zcol_max, dim3(unsigned(n), unsigned(ceil_div(k, ZMAX_PER_CTA))), 256, 0, s, b, k, n, ld, cm, gen);
     FQB_LAUNCHED();
-    launch_k(k_slice_z_kb<NSL, S>, dim3(unsigned(ceil_div(k, OZ_BK))), 256, 0, s, b, k, n, ld, cmax, e, out);
+    launch_k(k_slice_z_kb<NSL, S>, dim3(unsigned(ceil_div(k, OZ_BK))), 256, 0, s, b, k, n, ld,
+             static_cast<const u64*>(cm), gen, e, out);
     FQB_LAUNCHED();
     lc.bump(2);
 }
@@ -1507,7 +1526,7 @@ static void apply_chunks(int64_t M, int64_t N, int64_t K, double alpha, const in
         const int64_t nb = std::min(2 * cw, N - c0);
         slice_z_s(b + c0 * ldb, K, cw, ldb, ez, z, s, lc, nsl, S, zmax);
         slice_z_s(b + (c0 + cw) * ldb, K, nb - cw, ldb, ez + OZ_BN, z + zstride, s, lc, nsl, S,
-                  zmax ? zmax + OZ_BN : nullptr);
+                  zmax ? zmax + 2 * OZ_BN : nullptr);
         launch_ozaki(M, nb, K, alpha, xs, ex, z, ez, beta, C + c0 * ldc, ldc, work, num_sms, cw, nsl, S, s, lc, x_kb);
         c0 += nb;
     }
@@ -1532,7 +1551,7 @@ void ozaki_apply_presliced(int64_t M, int64_t N, int64_t K, double alpha, const 
                  z_spacing(cw, nsl), s, lc);
 }
 int64_t ozaki_apply_z_bytes(int64_t K, int nsl) { return 2 * ozaki_z_bytes(OZ_BN, K, nsl); }
-int ozaki_apply_ez_count() { return 2 * OZ_BN; }
+int ozaki_apply_ez_count() { return 4 * OZ_BN; }   // also the tagged 64-bit column maxima of two chunks
 int64_t ozaki_workspace_doubles(int num_sms) { return 3 * int64_t(num_sms) * OZ_PARTIAL; }  // 2 pieces + carry
 
 }  // namespace farqb

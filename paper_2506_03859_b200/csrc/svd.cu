@@ -297,7 +297,7 @@ void assemble_svd(Handle& h, const double* q, int64_t ldq, const double* bt, int
     DeviceArray<int> bt_etn, bt_enn, q_enn, oz_ez;
     DeviceArray<unsigned> oz_lm, oz_zmax;
     if (emulate) {
-        oz_lm.ensure(size_t(ozaki_line_max_words(std::max<int64_t>(m, n), l)), s);
+        oz_lm.ensure_zeroed(size_t(ozaki_line_max_words(std::max<int64_t>(m, n), l)), s);
         bt_tn.ensure(size_t(ozaki_x_bytes(l, n, nsl)), s);
         bt_nn.ensure(size_t(ozaki_x_bytes(n, l, nsl)), s);
         bt_etn.ensure(size_t(l), s);
@@ -306,7 +306,7 @@ void assemble_svd(Handle& h, const double* q, int64_t ldq, const double* bt, int
                       nullptr, nsl);
         oz_z.ensure(size_t(ozaki_apply_z_bytes(std::max<int64_t>(n, l), nsl)), s);
         oz_ez.ensure(size_t(ozaki_apply_ez_count()), s);
-        oz_zmax.ensure(size_t(ozaki_apply_ez_count()), s);
+        oz_zmax.ensure_zeroed(size_t(ozaki_apply_ez_count()), s);
     }
     auto oz = [&](int64_t M, int64_t K, const int8_t* xs, const int* ex, const double* B, int64_t ldb, double* C,
                   int64_t ldc) {
