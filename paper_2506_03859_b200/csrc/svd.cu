@@ -79,6 +79,25 @@ void cs_check(cusolverStatus_t st, const char* what) {
                                                                     std::to_string(int(st)) + ")");
 }
 
+// mat (n x n, ld n): upper triangle := lower triangle (32 x 32 tiles through shared memory)
+__global__ void k_mirror_lower(double* mat, int64_t n) {
+    FQB_PDL_ENTRY();
+    __shared__ double t[32][33];
+    const int64_t bi = blockIdx.x, bj = blockIdx.y;   // tile (row block bi, column block bj), bi >= bj sources
+    if (bi < bj) return;
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    for (int r = ty; r < 32; r += 8) {
+        const int64_t i = bi * 32 + r, j = bj * 32 + tx;
+        t[r][tx] = (i < n && j < n) ? mat[j * n + i] : 0.0;
+    }
+    __syncthreads();
+    // write the transpose into tile (bj, bi): element (j, i) = (i, j) for i > j
+    for (int r = ty; r < 32; r += 8) {
+        const int64_t j = bj * 32 + r, i = bi * 32 + tx;   // destination row j, column i
+        if (i < n && j < n && i > j) mat[i * n + j] = t[tx][r];
+    }
+}
+
 __global__ void k_scale_cols(const double* src, int64_t lds, const double* scale, int rows, int cols, double* dst,
                              int64_t ldd) {
     FQB_PDL_ENTRY();
@@ -313,9 +332,23 @@ void assemble_svd(Handle& h, const double* q, int64_t ldq, const double* bt, int
         ozaki_apply(M, l, K, 1.0, xs, ex, B, ldb, 0.0, C, ldc, oz_z.ptr, oz_ez.ptr, h.gws.work, h.num_sms, s, h.lc,
                     nsl, oz_zmax.ptr);
     };
-    // B B' = Bt' Bt  (l x l; the eigensolvers read its lower triangle)
-    if (emulate) oz(l, n, bt_tn.ptr, bt_etn.ptr, bt, ldbt, mat.ptr, l);
-    else gemm(true, l, l, n, 1.0, bt, ldbt, bt, ldbt, 0.0, mat.ptr, l, h.gws, h.num_sms, s, h.lc);
+    // B B' = Bt' Bt  (l x l).  Emulated: only the 128-column blocks on and below the
+    // diagonal (rows from the block's own first row: about half the products), then the
+    // lower triangle mirrored -- the eigensolvers get a symmetric matrix
+    if (emulate) {
+        for (int64_t c0 = 0; c0 < l; c0 += 128) {
+            const int64_t nb = std::min<int64_t>(128, l - c0);
+            ozaki_apply(l - c0, nb, n, 1.0, bt_tn.ptr + (c0 / 128) * ozaki_x_bytes(128, n, nsl), bt_etn.ptr + c0,
+                        bt + c0 * ldbt, ldbt, 0.0, mat.ptr + c0 + c0 * int64_t(l), l, oz_z.ptr, oz_ez.ptr, h.gws.work,
+                        h.num_sms, s, h.lc, nsl, oz_zmax.ptr);
+        }
+        launch_k(k_mirror_lower, dim3(unsigned(ceil_div(l, 32)), unsigned(ceil_div(l, 32))), dim3(32, 8), 0, s, mat.ptr,
+                 int64_t(l));
+        FQB_LAUNCHED();
+        h.lc.bump();
+    } else {
+        gemm(true, l, l, n, 1.0, bt, ldbt, bt, ldbt, 0.0, mat.ptr, l, h.gws, h.num_sms, s, h.lc);
+    }
     // eigendecomposition, sigma / flags / pseudo-inverse scale and both GEMMs are queued
     // without a host round trip; the one synchronization at the end also brings back
     // sigma, the flags and cuSOLVER's status
