@@ -149,16 +149,29 @@ __global__ void __launch_bounds__(1024) k_chol_inv(const double* __restrict__ S,
 // publication, the loads of a step issued together -- and the pivot column's
 // "store -f" is folded into the FMA (v keep + (-f) pc with keep = 0, pc = 1
 // there).  b = 50: 34.8 -> 18.3 us per call, b = 100: 125 -> 86 us
-// (tools/microbench/chol_bench.cu); a two-columns-per-thread form was slower.
+// (tools/microbench/chol_bench.cu); a two-columns-per-thread form was slower.  Since
+// then two pivots per barrier (below).
+// Two pivots per barrier: the owners of rows j and j + 1 publish both (row j + 1 as it
+// is before step j), and every thread forms row j + 1 after step j itself,
+//     f = M[j+1][j] / d_j,  M'[j+1][c] = M[j+1][c] - f M[j][c]  (-f at c = j),
+//     d_{j+1} = M'[j+1][j+1],
+// then applies steps j and j + 1 to its rows i > j + 1 (M[i][j] = M[j][i] and
+// M'[i][j+1] = M'[j+1][i] by the symmetry of the trailing Schur complements), and the
+// owner of row j + 1 stores M'[j+1][*].  The same pivots and the same pivot floor as one
+// step at a time; the published rows are double buffered per pair: a barrier per two
+// columns.
 template <int MAXS, int Q>
 __device__ __forceinline__ bool chol_group(double (&v)[MAXS], int b, double thresh, int rg, int c, bool active,
                                            double (*prow)[kSmemMaxB]) {
 #pragma unroll 1
-    for (int r = 0; r < 8; ++r) {
+    for (int r = 0; r < 8; r += 2) {
         const int j = 8 * Q + r;
         if (j >= b) return true;
-        double* pr = prow[j & 1];
-        if (active && rg == r) pr[c] = v[Q];
+        const bool two = j + 1 < b;
+        double* p0 = prow[((j >> 1) & 1) * 2];
+        double* p1 = prow[((j >> 1) & 1) * 2 + 1];
+        if (active && rg == r) p0[c] = v[Q];
+        if (two && active && rg == r + 1) p1[c] = v[Q];
 #ifdef FQB_CHOL_PROBE
         if (threadIdx.x == FQB_CHOL_PROBE) chol_probe_stamp(2 * j);
 #endif
@@ -166,21 +179,38 @@ __device__ __forceinline__ bool chol_group(double (&v)[MAXS], int b, double thre
 #ifdef FQB_CHOL_PROBE
         if (threadIdx.x == FQB_CHOL_PROBE) chol_probe_stamp(2 * j + 1);
 #endif
-        const double d = pr[j];
-        if (!(d > thresh)) return false;   // uniform: every thread reads the same pivot
-        double pv[MAXS - Q];
+        const double d0 = p0[j];
+        if (!(d0 > thresh)) return false;   // uniform: every thread reads the same pivot
+        const double inv0 = 1.0 / d0;
+        const double p0c = p0[c];
+        if (!two) {   // the last column of an odd b: one step
+            const bool piv = c == j;
+            const double pc = piv ? 1.0 : p0c;
+            const double keep = piv ? 0.0 : 1.0;
 #pragma unroll
-        for (int s = Q; s < MAXS; ++s) pv[s - Q] = pr[min(rg + 8 * s, b - 1)];
-        const bool piv = c == j;
-        const double pc = piv ? 1.0 : pr[c];
-        const double keep = piv ? 0.0 : 1.0;
-        const double invd = 1.0 / d;
+            for (int s = Q; s < MAXS; ++s) {
+                const double nv = fma(-(p0[min(rg + 8 * s, b - 1)] * inv0), pc, v[s] * keep);
+                if (s == Q) v[s] = rg > r ? nv : v[s];
+                else v[s] = nv;
+            }
+            return true;
+        }
+        const double f1 = p1[j] * inv0;
+        const double d1 = fma(-f1, p0[j + 1], p1[j + 1]);
+        if (!(d1 > thresh)) return false;
+        const double inv1 = 1.0 / d1;
+        const double p1c = c == j ? -f1 : fma(-f1, p0c, p1[c]);   // row j + 1 after step j, column c
 #pragma unroll
         for (int s = Q; s < MAXS; ++s) {
-            const double nv = fma(-(pv[s - Q] * invd), pc, v[s] * keep);
+            const int i = min(rg + 8 * s, b - 1);
+            const double a0 = p0[i], a1 = p1[i];
+            const double g0 = a0 * inv0;
+            const double g1 = fma(-f1, a0, a1) * inv1;
+            double x = c == j ? -g0 : fma(-g0, p0c, v[s]);
+            x = c == j + 1 ? -g1 : fma(-g1, p1c, x);
             // slots past row b - 1 collect garbage that is never published or stored
-            if (s == Q) v[s] = rg > r ? nv : v[s];
-            else v[s] = nv;
+            if (s == Q) v[s] = rg > r + 1 ? x : (rg == r + 1 ? p1c : v[s]);
+            else v[s] = x;
         }
     }
     return true;
@@ -201,7 +231,7 @@ __global__ void __launch_bounds__(1024) k_chol_inv_reg(const double* __restrict_
                                                        unsigned fail_bit) {
     FQB_PDL_ENTRY();
     extern __shared__ double smem[];        // final M, b x (b+1), row-major
-    __shared__ double prow[2][kSmemMaxB];
+    __shared__ double prow[4][kSmemMaxB];
     __shared__ double red[32];
     __shared__ double isd[kSmemMaxB];
     constexpr int RG = 8;
