@@ -393,10 +393,6 @@ void ts_gram(const double* Y, int64_t K, int b, int64_t ldy, double alpha, doubl
     lc.bump(2);
 }
 
-}  // namespace farqb
-
-namespace farqb {
-
 bool ts_trmm(const double* Y, int64_t M, int b, int64_t ldy, const double* R, int64_t ldr, double* Z, int64_t ldz,
              int num_sms, cudaStream_t s, LaunchCounter& lc) {
     if (b > kTrmmMaxB || b <= 0) return false;   // R and two Y stages no longer fit in shared memory
