@@ -366,26 +366,38 @@ void assemble_svd(Handle& h, const double* q, int64_t ldq, const double* bt, int
     launch_k(k_scale_cols, grid, 256, 0, s, mat.ptr, l, scale.ptr + l, l, l, us.ptr, l);
     FQB_LAUNCHED();
     h.lc.bump(2);
-    // U = Q U~ (this rank's rows), V = Bt (U~ Sigma^-1); with hc, each factor's kept
-    // columns go to the host on the copy stream as soon as its GEMM is done
-    auto copy_out = [&](const double* src, int64_t lds, int64_t rows, double* dst, cudaEvent_t ev) {
+    // V = Bt (U~ Sigma^-1) first (small), then U = Q U~ (this rank's rows); with hc, the kept
+    // columns (>= drop) go to the host on the copy stream as soon as they are computed -- U in
+    // blocks of 256 columns, so its download overlaps the rest of its product
+    auto copy_cols = [&](const double* src, int64_t lds, int64_t rows, double* dst, int64_t c0, int64_t c1,
+                         cudaEvent_t ev) {
+        const int64_t a0 = std::max<int64_t>(c0, hc->drop);
+        if (a0 >= c1) return;
         FQB_CUDA(cudaEventRecord(ev, s));
         FQB_CUDA(cudaStreamWaitEvent(hc->stream, ev, 0));
-        FQB_CUDA(cudaMemcpy2DAsync(dst, rows * sizeof(double), src + int64_t(hc->drop) * lds, lds * sizeof(double),
-                                   rows * sizeof(double), l - hc->drop, cudaMemcpyDeviceToHost, hc->stream));
+        FQB_CUDA(cudaMemcpy2DAsync(dst + (a0 - hc->drop) * rows, rows * sizeof(double), src + a0 * lds,
+                                   lds * sizeof(double), rows * sizeof(double), c1 - a0, cudaMemcpyDeviceToHost,
+                                   hc->stream));
     };
+    if (emulate) oz(n, l, bt_nn.ptr, bt_enn.ptr, us.ptr, l, v, ldv);
+    else gemm(false, n, l, l, 1.0, bt, ldbt, us.ptr, l, 0.0, v, ldv, h.gws, h.num_sms, s, h.lc);
+    if (hc && hc->v) copy_cols(v, ldv, n, hc->v, 0, l, hc->ev_v);
     if (emulate) {
         q_nn.ensure(size_t(ozaki_x_bytes(m, l, nsl)), s);
         q_enn.ensure(size_t(std::max<int64_t>(m, 1)), s);
         ozaki_slice_a(q, m, l, ldq, oz_lm.ptr, nullptr, nullptr, q_nn.ptr, q_enn.ptr, s, h.lc, nullptr, nullptr, nsl);
-        oz(m, l, q_nn.ptr, q_enn.ptr, mat.ptr, l, u, ldu);
-    } else {
-        gemm(false, m, l, l, 1.0, q, ldq, mat.ptr, l, 0.0, u, ldu, h.gws, h.num_sms, s, h.lc);
     }
-    if (hc && hc->u) copy_out(u, ldu, m, hc->u, hc->ev_u);
-    if (emulate) oz(n, l, bt_nn.ptr, bt_enn.ptr, us.ptr, l, v, ldv);
-    else gemm(false, n, l, l, 1.0, bt, ldbt, us.ptr, l, 0.0, v, ldv, h.gws, h.num_sms, s, h.lc);
-    if (hc && hc->v) copy_out(v, ldv, n, hc->v, hc->ev_v);
+    const int64_t ub = (hc && hc->u) ? 256 : l;
+    for (int64_t c0 = 0; c0 < l; c0 += ub) {
+        const int64_t nb = std::min<int64_t>(ub, l - c0);
+        if (emulate)
+            ozaki_apply(m, nb, l, 1.0, q_nn.ptr, q_enn.ptr, mat.ptr + c0 * l, l, 0.0, u + c0 * ldu, ldu, oz_z.ptr,
+                        oz_ez.ptr, h.gws.work, h.num_sms, s, h.lc, nsl, oz_zmax.ptr);
+        else
+            gemm(false, m, nb, l, 1.0, q, ldq, mat.ptr + c0 * l, l, 0.0, u + c0 * ldu, ldu, h.gws, h.num_sms, s,
+                 h.lc);
+        if (hc && hc->u) copy_cols(u, ldu, m, hc->u, c0, c0 + nb, hc->ev_u);
+    }
     int hinfo = 0;
     FQB_CUDA(cudaMemcpyAsync(sigma.data(), scale.ptr, sizeof(double) * l, cudaMemcpyDeviceToHost, s));
     FQB_CUDA(cudaMemcpyAsync(flagged.data(), flg.ptr, size_t(l), cudaMemcpyDeviceToHost, s));
