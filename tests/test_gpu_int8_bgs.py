@@ -87,3 +87,34 @@ def test_int8_bgs_and_b_products_match_oracle(eng, port, m, n, b, power, kind):
         results[tag] = res
     qb = [r.q @ r.bt.T for r in results.values()]
     assert np.linalg.norm(qb[0] - qb[1]) <= 1e-10 * np.sqrt(na)
+
+
+@pytest.mark.parametrize("rows", [False, True])
+def test_int8_products_on_graded_matrix_match_oracle(eng, port, rows):
+    """The emulation's weak case at sizes where the Q- and B-side products run on the INT8
+    tensor cores too: every row (column) of A spans eight decades (its columns (rows) scaled
+    by 1e-8 .. 1).  Same bars as above, plus Q B within 1e-10 ||A||_F of the oracle's."""
+    m, n, b = 4200, 4300, 64
+    a = _lowrank(m, n, 0.98 ** np.arange(420), seed=700 + int(rows))
+    d = np.logspace(-8, 0, m if rows else n)
+    np.random.default_rng(701).shuffle(d)
+    a = np.asfortranarray(a * d[:, None] if rows else a * d[None, :])
+    spec = SketchSpec(3, 0.0, 41, zeta=8)
+    cfg = FarpcaConfig(eps=2e-3, power=1, block=b, sketch=spec, relative=True)
+
+    def src(nn, bb, bid):
+        return _arr(eng.gen_sketch(spec, nn, bb, bid))
+    ref = port.run(a, eps=2e-3, power=1, block=b, kind=3, p=0.0, seed=41, zeta=8, relative=True, source=src,
+                   want_vectors=True)
+    assert ref.status == 0 and ref.rank >= 4 * b
+    res = _with_env({"FQB_OZAKI": "1", "FQB_OZ_Q": "1", "FQB_OZ_B": "1"},
+                    lambda: eng.run_fixed_precision(torch.from_numpy(a).cuda(), cfg, output="host", svd=True))
+    assert res.converged
+    assert (res.rank, res.blocks, res.block_ids) == (ref.rank, ref.blocks, ref.block_ids)
+    na = ref.norm_a_sq
+    assert abs(res.residual_sq - ref.residual_sq) <= 1e-10 * na
+    assert np.max(np.abs(res.block_residuals - np.asarray(ref.block_residuals))) <= 1e-10 * na
+    top = ref.sigma >= 1e-3 * ref.sigma[-1]
+    assert np.max(np.abs(res.sigma[top] - ref.sigma[top])) <= 1e-10 * ref.sigma[-1]
+    usv = (ref.u * ref.sigma) @ ref.v.T
+    assert np.linalg.norm(res.q @ res.bt.T - usv) <= 1e-10 * np.sqrt(na)
