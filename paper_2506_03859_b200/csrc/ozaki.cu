@@ -93,6 +93,10 @@ struct Sl {
     static constexpr int CHUNK_KB = (W == 8 ? 16384 : 32768) / OZ_BK;
 };
 constexpr int OZ_THREADS = 192;                   // producer, MMA, 4 epilogue warps
+// the MN-major (AMN) products have short K, so each row tile's TMEM drain is on the MMA's
+// critical path: they split it over 8 epilogue warps (two per TMEM lane quarter, each
+// draining half of the column groups)
+constexpr int oz_threads(bool amn) { return amn ? OZ_THREADS + 128 : OZ_THREADS; }
 constexpr int OZ_PARTIAL = OZ_BM * OZ_BN;         // doubles per CTA partial slot
 
 // 64-bit quotient through a double reciprocal and one correction step (operands are
@@ -265,6 +269,17 @@ __device__ __forceinline__ void tmem_ld16(unsigned taddr, unsigned (&v)[16]) {
         : "r"(taddr));
 }
 
+__device__ __forceinline__ void tmem_ld8(unsigned taddr, unsigned (&v)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "r"(taddr));
+}
+template <int GW>
+__device__ __forceinline__ void tmem_ld_g(unsigned taddr, unsigned (&v)[GW]) {
+    if constexpr (GW == 16) tmem_ld16(taddr, v);
+    else tmem_ld8(taddr, v);
+}
+
 // zero 16 columns of this warp's 32 TMEM lanes
 __device__ __forceinline__ void tmem_st16_zero(unsigned taddr) {
     asm volatile(
@@ -400,7 +415,7 @@ constexpr int kS50ZeroCol = 352, kS50ZeroGroups = 3;
 // halves sit 4 KB apart (LBO), 8 columns per 512-byte swizzle atom (SBO); the row
 // exponents are 0 (each column's scale is folded into C by the caller).
 template <bool PAIR, int NSL, int BS, int S, int NDK = 0, bool WIDE = false, bool AMN = false>
-__global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
+__global__ void __launch_bounds__(oz_threads(AMN), 1) k_ozaki(const OzArgs p) {
     using SL = Sl<NSL, BS, S, NDK>;
     constexpr unsigned AK = AMN ? (32u * 64u) >> 4 : 32u >> 4;
     static_assert(S == 64 || ((S == 56 || S == 50) && NSL == 7), "the 56 / 50-row spacings are scheduled for 7 slices");
@@ -440,7 +455,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
             mbar_init(b_empty + 8 * s, 1);
         }
         mbar_init(t_full, 1);
-        mbar_init(t_empty, 128);
+        mbar_init(t_empty, unsigned(oz_threads(AMN) - 64));   // every epilogue thread
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     if (threadIdx.x < OZ_BN) ez_s[threadIdx.x] = int(threadIdx.x) < q_N ? q_ez[threadIdx.x] : 0;
@@ -629,6 +644,11 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
         // pieces in CTA order afterwards -- no inter-CTA waiting inside this kernel.
         // A segment longer than CHUNK_KB k-blocks carries its running sum in slot 2.
         const int quarter = warp & 3;           // TMEM lanes 32*quarter .. +31
+        constexpr int EPI = (oz_threads(AMN) - 64) / 32;   // epilogue warps: 4, or 8 (AMN)
+        constexpr int GPH = EPI == 8 ? 32 : 64;             // columns drained per epilogue half
+        const int g_lo = EPI == 8 ? ((warp - 2) >> 2) * GPH : 0;   // this warp's column groups
+        const int g_hi = min(S, g_lo + GPH);
+        constexpr int GW = EPI == 8 ? 8 : 16;               // columns per drain step (registers)
         const int r_loc = quarter * 32 + lane;  // tile row of this thread
         const unsigned lane_addr = tmem + (unsigned(quarter * 32) << 16);
         double* carry = q_work + (3 * int64_t(c) + 2) * OZ_PARTIAL;
@@ -636,9 +656,20 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
         // S = 50: diagonal 7's columns no MMA initialises are zeroed before every
         // accumulation (here for the first, after each drain for the next)
         auto zero_d7 = [&]() {
+            if constexpr (EPI == 8) {
+                // both halves have read diagonal 7 before the first half zeroes it
+                asm volatile("bar.sync 1, %0;\n" ::"n"(EPI * 32) : "memory");
+                if (g_lo == 0) {
 #pragma unroll
-            for (int z = 0; z < kS50ZeroGroups; ++z) tmem_st16_zero(lane_addr + unsigned(kS50ZeroCol + 16 * z));
-            asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+                    for (int z = 0; z < kS50ZeroGroups; ++z)
+                        tmem_st16_zero(lane_addr + unsigned(kS50ZeroCol + 16 * z));
+                    asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+                }
+            } else {
+#pragma unroll
+                for (int z = 0; z < kS50ZeroGroups; ++z) tmem_st16_zero(lane_addr + unsigned(kS50ZeroCol + 16 * z));
+                asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+            }
             asm volatile("tcgen05.fence::before_thread_sync;\n");
             mbar_arrive(t_empty);
         };
@@ -653,65 +684,65 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_ozaki(const OzArgs p) {
             // AMN (short K, beta != 0: Y -= Q C): each group's old C is loaded one group
             // ahead -- the first before the accumulators are ready -- so the drain, which
             // the single-buffered TMEM puts on the MMA's critical path, does not wait on it
-            double pre[16];
+            double pre[GW];
             const bool pre_on = AMN && p.beta != 0.0 && full_tile && row < p.M;
             auto load_old = [&](int g0) {
 #pragma unroll
-                for (int j = 0; j < 16; ++j) pre[j] = g0 + j < q_N ? q_C[int64_t(g0 + j) * p.ldc + row] : 0.0;
+                for (int j = 0; j < GW; ++j) pre[j] = g0 + j < q_N ? q_C[int64_t(g0 + j) * p.ldc + row] : 0.0;
             };
             for (int cb = kb0; cb < kb1; cb += CHUNK_KB) {
                 const bool first_chunk = cb == kb0, last_chunk = cb + CHUNK_KB >= kb1;
                 if constexpr (AMN) {
-                    if (pre_on && last_chunk) load_old(0);
+                    if (pre_on && last_chunk) load_old(g_lo);
                 }
                 mbar_wait(t_full, ph);
                 ph ^= 1u;
                 asm volatile("tcgen05.fence::after_thread_sync;\n");
 #pragma unroll 1
-                for (int g = 0; g < S; g += 16) {   // S = 56: the last group reads 8 spare columns
+                for (int g = g_lo; g < g_hi; g += GW) {   // S = 56: the last group reads 8 spare columns
                     // all diagonals in flight, one wait
-                    unsigned v[ND][16];
+                    unsigned v[ND][GW];
 #pragma unroll
-                    for (int d = 0; d < ND; ++d) tmem_ld16(lane_addr + unsigned(d * S + g), v[d]);
+                    for (int d = 0; d < ND; ++d) tmem_ld_g<GW>(lane_addr + unsigned(d * S + g), v[d]);
                     asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-                    double acc[16];
+                    double acc[GW];
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) acc[j] = 0.0;
+                    for (int j = 0; j < GW; ++j) acc[j] = 0.0;
                     // least significant diagonal first: d = ND-1 .. 0 (scale 2^(-12-W d))
 #pragma unroll
                     for (int d = ND - 1; d >= 0; --d) {
                         const double sc = pow2i(-12 - SL::W * d);
 #pragma unroll
-                        for (int j = 0; j < 16; ++j) acc[j] = fma(double(int(v[d][j])), sc, acc[j]);
+                        for (int j = 0; j < GW; ++j) acc[j] = fma(double(int(v[d][j])), sc, acc[j]);
                     }
                     if (!first_chunk) {
 #pragma unroll
-                        for (int j = 0; j < 16; ++j) acc[j] += carry[(g + j) * OZ_BM + r_loc];
+                        for (int j = 0; j < GW; ++j) acc[j] += carry[(g + j) * OZ_BM + r_loc];
                     }
                     if (!last_chunk) {
 #pragma unroll
-                        for (int j = 0; j < 16; ++j) carry[(g + j) * OZ_BM + r_loc] = acc[j];
+                        for (int j = 0; j < GW; ++j) carry[(g + j) * OZ_BM + r_loc] = acc[j];
                         continue;
                     }
                     if (!full_tile) {
 #pragma unroll
-                        for (int j = 0; j < 16; ++j)
+                        for (int j = 0; j < GW; ++j)
                             piece[(g + j) * OZ_BM + r_loc] = mul_pow2(acc[j], er + ez_s[g + j]);
                         continue;
                     }
                     if (row < p.M) {
-                        double old_c[16];
+                        double old_c[GW];
                         if (AMN && pre_on) {
 #pragma unroll
-                            for (int j = 0; j < 16; ++j) old_c[j] = pre[j];
-                            if (g + 16 < S) load_old(g + 16);
+                            for (int j = 0; j < GW; ++j) old_c[j] = pre[j];
+                            if (g + GW < g_hi) load_old(g + GW);
                         } else if (p.beta != 0.0) {
 #pragma unroll
-                            for (int j = 0; j < 16; ++j)
+                            for (int j = 0; j < GW; ++j)
                                 old_c[j] = g + j < q_N ? q_C[int64_t(g + j) * p.ldc + row] : 0.0;
                         }
 #pragma unroll
-                        for (int j = 0; j < 16; ++j) {
+                        for (int j = 0; j < GW; ++j) {
                             if (g + j < q_N) {
                                 const double val = p.alpha * mul_pow2(acc[j], er + ez_s[g + j]);
                                 q_C[int64_t(g + j) * p.ldc + row] = p.beta != 0.0 ? fma(p.beta, old_c[j], val) : val;
@@ -1304,7 +1335,7 @@ static void launch_variant(const OzArgs& a, cudaStream_t s) {
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(unsigned(PAIR ? 2 * a.grid : a.grid));
-    cfg.blockDim = dim3(OZ_THREADS);
+    cfg.blockDim = dim3(oz_threads(AMN));
     cfg.dynamicSmemBytes = Sl<NSL, BS, S, NDK>::SMEM;
     cfg.stream = s;
     cudaLaunchAttribute attr[2];
