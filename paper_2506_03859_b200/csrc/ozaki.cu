@@ -88,9 +88,14 @@ struct Sl {
     static constexpr int A_STAGES = (225 * 1024 - B_STAGES * B_STAGE) / A_TILE;     // 21 / 20 / 24
     static constexpr size_t SMEM = size_t(A_STAGES) * A_TILE + size_t(B_STAGES) * B_STAGE + 1024;
     static constexpr unsigned TMEM_COLS = ND > 4 ? 512u : unsigned(ND * OZ_BN);    // a power of two: 512 / 256
-    // k-blocks per TMEM accumulation (int32 headroom): a diagonal sums at most ND
-    // products of |digits| <= 2^(W-1): 8 * 64^2 * 32768 = 2^30 and 7 * 128^2 * 16384 < 2^31
-    static constexpr int CHUNK_KB = (W == 8 ? 16384 : 32768) / OZ_BK;
+    // k-blocks per TMEM accumulation (int32 headroom).  7-bit digits: at most 8 products
+    // of |d| <= 64 per diagonal, 8 * 64^2 * 32768 = 2^30.  8-bit digits (|d| <= 128, the top
+    // digit |d_0| <= 64): diagonal d sums the products p + q = d, at most 6 of size 2^14
+    // (d = 6: two with the top digit, 2^13 each, plus five; d = 7: six) -> 6 * 2^14 per
+    // element of K, so K <= 21845; 336 k-blocks (21504) keep every diagonal < 2^31.  (What
+    // the schedules spill onto diagonal 8 is never read.)  The 4-diagonal FP32 scheme keeps
+    // the old 256.  336 puts a whole K = 20000 A G pass into one accumulation (two with 256).
+    static constexpr int CHUNK_KB = W == 7 ? 32768 / OZ_BK : (ND >= 7 ? 336 : 16384 / OZ_BK);
 };
 constexpr int OZ_THREADS = 192;                   // producer, MMA, 4 epilogue warps
 // the MN-major (AMN) products have short K, so each row tile's TMEM drain is on the MMA's
@@ -152,6 +157,8 @@ struct OzArgs {
     // AMN launches: xs are the A'Y-layout (column-scaled, K-major) slices of an operand X
     // (rows = K of this product, x_kb k-blocks of 64 of them), read MN-major as A = X
     int64_t x_kb;
+    // k-blocks per TMEM accumulation, <= Sl::CHUNK_KB (int32 headroom); FQB_OZ_CHUNK lowers it
+    int chunk_kb;
 };
 
 // this CTA's (or fixup block's) column chunk of a paired launch
@@ -424,7 +431,8 @@ __global__ void __launch_bounds__(oz_threads(AMN), 1) k_ozaki(const OzArgs p) {
     constexpr int A_STAGES = SL::A_STAGES;
     constexpr int B_STAGES = SL::B_STAGES;
     constexpr int B_STAGE = SL::B_STAGE;
-    constexpr int ND = SL::ND, CHUNK_KB = SL::CHUNK_KB;
+    constexpr int ND = SL::ND;
+    const int CHUNK_KB = p.chunk_kb;
     FQB_PDL_ENTRY();
     extern __shared__ uint8_t smem_raw[];
     __shared__ uint64_t bars[2 * A_STAGES + 2 * B_STAGES + 2];
@@ -1323,6 +1331,17 @@ void ozaki_slice_z(const double* b, int64_t k, int64_t n, int64_t ld, int* e, in
 }
 
 // paired (pair_cw > 0): N = 2 chunks of pair_cw columns at most, zs / ez hold both
+// FQB_OZ_CHUNK=<k-blocks>: a shorter TMEM accumulation than the int32 headroom allows
+// (A/B measurements; the default is the headroom, Sl::CHUNK_KB)
+static int chunk_kb_limit() {
+    static const int v = [] {
+        const char* e = std::getenv("FQB_OZ_CHUNK");
+        const int x = e ? std::atoi(e) : 0;
+        return x > 0 ? x : 1 << 30;
+    }();
+    return v;
+}
+
 template <bool PAIR, int NSL, int BS, int S = 64, int NDK = 0, bool WIDE = false, bool AMN = false>
 static void launch_variant(const OzArgs& a, cudaStream_t s) {
     static bool configured[64] = {};
@@ -1333,6 +1352,8 @@ static void launch_variant(const OzArgs& a, cudaStream_t s) {
                                       int(Sl<NSL, BS, S, NDK>::SMEM)));
         if (dev >= 0 && dev < 64) configured[dev] = true;
     }
+    OzArgs args = a;
+    args.chunk_kb = std::min(Sl<NSL, BS, S, NDK>::CHUNK_KB, chunk_kb_limit());
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(unsigned(PAIR ? 2 * a.grid : a.grid));
     cfg.blockDim = dim3(oz_threads(AMN));
@@ -1354,7 +1375,7 @@ static void launch_variant(const OzArgs& a, cudaStream_t s) {
     }
     cfg.attrs = attr;
     cfg.numAttrs = na;
-    FQB_CUDA(cudaLaunchKernelEx(&cfg, k_ozaki<PAIR, NSL, BS, S, NDK, WIDE, AMN>, a));
+    FQB_CUDA(cudaLaunchKernelEx(&cfg, k_ozaki<PAIR, NSL, BS, S, NDK, WIDE, AMN>, args));
 }
 
 // A/B switches of the A-pass kernel (read once): FQB_OZ_L2HINT=0 plain bulk copies,
