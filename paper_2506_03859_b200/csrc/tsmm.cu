@@ -32,7 +32,8 @@ constexpr int kMaxB = 128;
 constexpr int kGramRows = 32;      // rows of Y per stage
 constexpr int kGramPitch = kGramRows + 4;   // Ys[c][k]: fragment loads hit 2 wavefronts
 constexpr int kGramStages = 4;
-constexpr int kGramThreads = 256;
+constexpr int kGramThreads = 512;   // 16 warps: more independent DMMA chains per SM partition
+constexpr int kGramWarps = kGramThreads / 32;
 constexpr int kTrmmRows = 64;      // rows of Y per block
 constexpr int kTrmmThreads = 256;  // 4 row groups of 16 x 2 column-tile parities
 constexpr int kTrmmMaxB = 104;     // R (b x b+4) + 2 x Y (b x 72) within 227 KB
@@ -76,7 +77,7 @@ struct GramArgs {
     double* work;           // gridDim.x x tiles x 64
 };
 
-// MAXT: tiles per warp (ceil(tiles / 8))
+// MAXT: tiles per warp (ceil(tiles / kGramWarps))
 template <int MAXT>
 __global__ void __launch_bounds__(kGramThreads, 1) k_ts_gram(const GramArgs p) {
     FQB_PDL_ENTRY();
@@ -88,7 +89,7 @@ __global__ void __launch_bounds__(kGramThreads, 1) k_ts_gram(const GramArgs p) {
     const int64_t r1 = min(p.K, r0 + p.rows_per_cta);
     const int nsteps = r1 > r0 ? int((r1 - r0 + kGramRows - 1) / kGramRows) : 0;
     // this warp's contiguous run of upper tiles
-    const int per = (p.tiles + 7) / 8;
+    const int per = (p.tiles + kGramWarps - 1) / kGramWarps;
     const int t0 = warp * per;
     int ti[MAXT], tj[MAXT];
 #pragma unroll
@@ -381,10 +382,10 @@ void ts_gram(const double* Y, int64_t K, int b, int64_t ldy, double alpha, doubl
     if (grid < 1) grid = 1;
     a.work = work;
     const size_t smem = size_t(kGramStages) * a.nt * 8 * kGramPitch * sizeof(double);
-    const int per = (a.tiles + 7) / 8;
-    if (per <= 6) launch_gram<6>(a, grid, smem, s);          // b <= 48
-    else if (per <= 12) launch_gram<12>(a, grid, smem, s);   // b <= 104
-    else launch_gram<17>(a, grid, smem, s);                  // b <= 128
+    const int per = (a.tiles + kGramWarps - 1) / kGramWarps;
+    if (per <= 3) launch_gram<3>(a, grid, smem, s);          // b <= 48
+    else if (per <= 6) launch_gram<6>(a, grid, smem, s);     // b <= 104
+    else launch_gram<9>(a, grid, smem, s);                   // b <= 128
     FQB_LAUNCHED();
     const int64_t outs = int64_t(a.tiles) * 64;
     launch_k(k_ts_gram_reduce, unsigned((outs + 31) / 32), 256, 0, s, static_cast<const double*>(work), grid,
