@@ -35,7 +35,7 @@ constexpr int kGramStages = 4;
 constexpr int kGramThreads = 512;   // 16 warps: more independent DMMA chains per SM partition
 constexpr int kGramWarps = kGramThreads / 32;
 constexpr int kTrmmRows = 64;      // rows of Y per block
-constexpr int kTrmmThreads = 256;  // 4 row groups of 16 x 2 column-tile parities
+constexpr int kTrmmThreads = 512;  // 8 row groups of 8 x 2 column-tile parities
 constexpr int kTrmmMaxB = 104;     // R (b x b+4) + 2 x Y (b x 72) within 227 KB
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
@@ -226,7 +226,7 @@ struct TrmmArgs {
     bool vec2;
 };
 
-// One 64-row block of Z = Y R for warp (rows wm .. wm + 15, 8-column tiles j = WJ, WJ + 2,
+// One 64-row block of Z = Y R for warp (rows wm .. wm + 7, 8-column tiles j = WJ, WJ + 2,
 // ...): every tile / k-step pair is a compile-time constant, so the k-steps below R's
 // diagonal are not emitted at all (a predicated-off DMMA still occupies the pipe).
 template <int NT, int WJ>
@@ -234,15 +234,12 @@ __device__ __forceinline__ void trmm_block(const double* ys, const double* Rs, i
                                            const TrmmArgs& p) {
     constexpr int BP = NT * 8, RP = BP + 4, YP = kTrmmRows + 8;
     constexpr int JT = (NT - WJ + 1) / 2;
-    double acc[2][JT > 0 ? JT : 1][2];
+    double acc[JT > 0 ? JT : 1][2];
 #pragma unroll
-    for (int i = 0; i < 2; ++i)
-#pragma unroll
-        for (int q = 0; q < JT; ++q) acc[i][q][0] = acc[i][q][1] = 0.0;
+    for (int q = 0; q < JT; ++q) acc[q][0] = acc[q][1] = 0.0;
 #pragma unroll
     for (int kk = 0; kk < BP; kk += 4) {
         const double a0 = ys[(kk + t4) * YP + wm + g];
-        const double a1 = ys[(kk + t4) * YP + wm + 8 + g];
         double bf[JT > 0 ? JT : 1];
 #pragma unroll
         for (int q = 0; q < JT; ++q) {
@@ -253,27 +250,24 @@ __device__ __forceinline__ void trmm_block(const double* ys, const double* Rs, i
         for (int q = 0; q < JT; ++q) {
             const int j = 2 * q + WJ;
             if (j * 8 + 7 < kk) continue;   // R(k, n) = 0 for k > n: resolved at compile time
-            dmma(acc[0][q][0], acc[0][q][1], a0, bf[q]);
-            dmma(acc[1][q][0], acc[1][q][1], a1, bf[q]);
+            dmma(acc[q][0], acc[q][1], a0, bf[q]);
         }
     }
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-        const int64_t row = m0 + wm + i * 8 + g;
-        if (row >= p.M) continue;
+    const int64_t row = m0 + wm + g;
+    if (row < p.M) {
 #pragma unroll
         for (int q = 0; q < JT; ++q)
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 const int col = (2 * q + WJ) * 8 + 2 * t4 + h;
-                if (col < p.b) p.Z[int64_t(col) * p.ldz + row] = acc[i][q][h];
+                if (col < p.b) p.Z[int64_t(col) * p.ldz + row] = acc[q][h];
             }
     }
 }
 
 // NT: 8-column tiles of b (b <= 8 NT).  Persistent: R staged once per CTA as Rs[n][k]
 // (pitch 8 NT + 4, zero below the diagonal), 64-row blocks of Y double-buffered by
-// cp.async as Ys[k][m] (pitch 72).  8 warps: 4 row groups of 16 x the two parities of
+// cp.async as Ys[k][m] (pitch 72).  16 warps: 8 row groups of 8 x the two parities of
 // the column tiles (alternate tiles balance the triangle).
 template <int NT>
 __global__ void __launch_bounds__(kTrmmThreads, 1) k_ts_trmm(const TrmmArgs p) {
@@ -318,7 +312,7 @@ __global__ void __launch_bounds__(kTrmmThreads, 1) k_ts_trmm(const TrmmArgs p) {
     int64_t blk = blockIdx.x;
     if (blk < nblocks) load(blk, 0);
     cp_commit();
-    const int wm = (warp & 3) * 16;
+    const int wm = (warp & 7) * 8;
     for (int it = 0; blk < nblocks; ++it, blk += gridDim.x) {
         const int64_t nxt = blk + gridDim.x;
         if (nxt < nblocks) load(nxt, (it + 1) & 1);
@@ -326,7 +320,7 @@ __global__ void __launch_bounds__(kTrmmThreads, 1) k_ts_trmm(const TrmmArgs p) {
         cp_wait<1>();
         __syncthreads();
         const double* ys = Ys0 + (it & 1) * (BP * YP);
-        if (warp < 4) trmm_block<NT, 0>(ys, Rs, wm, g, t4, blk * kTrmmRows, p);
+        if (warp < 8) trmm_block<NT, 0>(ys, Rs, wm, g, t4, blk * kTrmmRows, p);
         else trmm_block<NT, 1>(ys, Rs, wm, g, t4, blk * kTrmmRows, p);
         __syncthreads();   // the stage is refilled next iteration
     }
