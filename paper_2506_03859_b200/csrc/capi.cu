@@ -134,6 +134,7 @@ fqb_status fqb_destroy(fqb_handle h) {
         if (h->h.ev_half) cudaEventDestroy(h->h.ev_half);
         if (h->h.ev_reduced) cudaEventDestroy(h->h.ev_reduced);
         if (h->h.ev_qb) cudaEventDestroy(h->h.ev_qb);
+        if (h->h.ev_copied) cudaEventDestroy(h->h.ev_copied);
         if (h->h.ev_u) cudaEventDestroy(h->h.ev_u);
         if (h->h.ev_v) cudaEventDestroy(h->h.ev_v);
         for (cudaEvent_t e : h->h.pass_timer.ev) cudaEventDestroy(e);

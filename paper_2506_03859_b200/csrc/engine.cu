@@ -208,6 +208,25 @@ class QbRun {
 
     void reserve_blocks(int nblocks) { grow(int64_t(nblocks) * b_); }
 
+    // Host Q, B' (FQB_OUT_HOST): each committed block's columns leave on the handle's
+    // copy stream while the next block runs, so only U, V are copied after the loop.
+    // Host capacity: the device's, or the rank the handle's last run of this shape
+    // reached; outgrowing it copies the committed columns again from the device.
+    void stream_out_host() { stream_out_ = true; }
+    bool streamed() const { return hq_ != nullptr; }
+    // the host arrays (ld m, n), every committed column queued on the copy stream
+    void take_host(double** q, double** bt) {
+        *q = hq_;
+        *bt = hbt_;
+        hq_ = hbt_ = nullptr;
+    }
+    ~QbRun() {
+        // queued copies read q_ / bt_, which are released on s_ below
+        if (hcopied_ > 0) cudaStreamSynchronize(h_.copy_stream);
+        host_free(hq_);
+        host_free(hbt_);
+    }
+
     // process_block (driver.cpp:134-160): up to 3 redraws with id + 1000 r
     void process_block(int index) {
         for (int attempt = 0;; ++attempt) {
@@ -238,6 +257,10 @@ class QbRun {
         if (need_cols <= cap_) return;
         int64_t nc = std::max<int64_t>(need_cols, cap_ ? 2 * cap_ : int64_t(b_) * 4);
         nc = std::min<int64_t>(std::max(nc, need_cols), std::max<int64_t>(need_cols, int64_t(cfg_.max_iters) * b_));
+        if (hcopied_ > 0) {   // host copies of the old Q / B' may still be in flight
+            FQB_CUDA(cudaEventRecord(h_.ev_copied, h_.copy_stream));
+            FQB_CUDA(cudaStreamWaitEvent(s_, h_.ev_copied, 0));
+        }
         auto regrow = [&](DeviceArray<double>& arr, int64_t ld) {
             DeviceArray<double> fresh;
             fresh.ensure(size_t(ld) * nc, s_);
@@ -279,6 +302,39 @@ class QbRun {
         w.t.ensure(size_t(nc) * b_, s_);
         w.cd.ensure(size_t(nc + b_) * b_, s_);
         w.c2.ensure(size_t(nc) * b_, s_);
+    }
+
+    void push_host() {
+        if (l_ > hcap_) {
+            // the first run of a shape on this handle copies after the loop (its final
+            // size is unknown; growing host blocks would leave odd sizes in the pool)
+            const bool hinted = h_.out_hint_m == m_ && h_.out_hint_n == n_ && h_.out_hint_l > 0;
+            if (!hinted) {
+                stream_out_ = false;
+                return;
+            }
+            const int64_t want = hcap_ == 0 ? std::max(l_, h_.out_hint_l) : std::max(cap_, l_);
+            if (hcopied_ > 0) FQB_CUDA(cudaStreamSynchronize(h_.copy_stream));
+            host_release(hq_);   // outgrown: unpinned, not cached
+            host_release(hbt_);
+            hq_ = static_cast<double*>(host_alloc(sizeof(double) * size_t(m_) * size_t(want)));
+            hbt_ = static_cast<double*>(host_alloc(sizeof(double) * size_t(n_) * size_t(want)));
+            if (!hq_ || !hbt_) throw Error(kStatusAlloc, "host result allocation failed");
+            hcap_ = want;
+            hcopied_ = 0;
+        }
+        if (!h_.copy_stream) FQB_CUDA(cudaStreamCreateWithFlags(&h_.copy_stream, cudaStreamNonBlocking));
+        if (!h_.ev_qb) FQB_CUDA(cudaEventCreateWithFlags(&h_.ev_qb, cudaEventDisableTiming));
+        if (!h_.ev_copied) FQB_CUDA(cudaEventCreateWithFlags(&h_.ev_copied, cudaEventDisableTiming));
+        FQB_CUDA(cudaEventRecord(h_.ev_qb, s_));
+        FQB_CUDA(cudaStreamWaitEvent(h_.copy_stream, h_.ev_qb, 0));
+        const int64_t c0 = hcopied_, nc = l_ - hcopied_;
+        FQB_CUDA(cudaMemcpy2DAsync(hq_ + c0 * m_, m_ * sizeof(double), q_.ptr + c0 * ldq_, ldq_ * sizeof(double),
+                                   m_ * sizeof(double), nc, cudaMemcpyDeviceToHost, h_.copy_stream));
+        FQB_CUDA(cudaMemcpy2DAsync(hbt_ + c0 * n_, n_ * sizeof(double), bt_.ptr + c0 * ldbt_,
+                                   ldbt_ * sizeof(double), n_ * sizeof(double), nc, cudaMemcpyDeviceToHost,
+                                   h_.copy_stream));
+        hcopied_ = l_;
     }
 
     void gemm_(bool ta, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
@@ -834,6 +890,7 @@ class QbRun {
             pending_rowsum_ = false;
             ++blocks_;
             residuals_.push_back(residual());
+            if (stream_out_) push_host();
             return 0;
         }
         return kStPowerDegenerate;
@@ -855,6 +912,9 @@ class QbRun {
     double norm_a_sq_ = 0.0, trace_ = 0.0, diag_max_ = 0.0;
     bool have_z_ = false, need_rowsum_ = false, z_allowed_ = false, pending_rowsum_ = false;
     int64_t rowsum_cols_ = 0;  // B' columns whose row sums are in rowsum_
+    bool stream_out_ = false;  // stream_out_host()
+    double *hq_ = nullptr, *hbt_ = nullptr;
+    int64_t hcap_ = 0, hcopied_ = 0;
   public:
     double host_wait_s_ = 0.0;  // time the host spent blocked on the device (FQB_HOST_STATS)
     bool om_dense_ = true, om_centered_ = false, om_shift_folded_ = false;
@@ -934,6 +994,7 @@ int run_qb(Handle& h, const void* a, bool a_f32, int64_t m, int64_t n, int64_t l
     const auto t_host0 = std::chrono::steady_clock::now();
     QbRun run(h, a_f32 ? nullptr : static_cast<const double*>(ad), a_f32 ? static_cast<const float*>(ad) : nullptr, m,
               n, ldad, cfg, src, user);
+    if (!(flags & FQB_OUT_DEVICE) && (flags & FQB_OUT_HOST) && !std::getenv("FQB_OUT_TAIL")) run.stream_out_host();
     run.setup();
     int status = 0;
     bool converged = false;
@@ -984,7 +1045,14 @@ int run_qb(Handle& h, const void* a, bool a_f32, int64_t m, int64_t n, int64_t l
         }
     } host_guard{&host_q, &host_bt, &h.copy_stream};
     const bool host_out = l_qb > 0 && !(flags & FQB_OUT_DEVICE) && (flags & FQB_OUT_HOST);
-    if (host_out) {
+    if (host_out) {   // host capacity for the next run of this shape (QbRun::push_host)
+        h.out_hint_m = m;
+        h.out_hint_n = n;
+        h.out_hint_l = l_qb;
+    }
+    if (host_out && run.streamed()) {
+        run.take_host(&host_q, &host_bt);   // every committed column already queued
+    } else if (host_out) {
         host_q = static_cast<double*>(host_alloc(sizeof(double) * size_t(m) * l_qb));
         host_bt = static_cast<double*>(host_alloc(sizeof(double) * size_t(n) * l_qb));
         if (!host_q || !host_bt) throw Error(kStatusAlloc, "host result allocation failed");

@@ -149,6 +149,8 @@ struct Handle {
     cudaStream_t comm_stream = nullptr;
     cudaEvent_t ev_half = nullptr, ev_reduced = nullptr;
     cudaEvent_t ev_qb = nullptr;
+    cudaEvent_t ev_copied = nullptr;                // copy stream -> engine stream (QbRun::grow)
+    int64_t out_hint_m = -1, out_hint_n = -1, out_hint_l = 0;   // host Q / B' capacity hint (QbRun::push_host)
     cudaEvent_t ev_u = nullptr, ev_v = nullptr;   // host U / V copies of the SVD assembly
 };
 
@@ -183,6 +185,7 @@ uint64_t checksum_dev(Handle& h, const double* a, int64_t rows, int64_t cols, in
 // hostmem.cu: pinned, pooled host arrays for results returned on the host
 void* host_alloc(size_t bytes);
 void host_free(void* ptr);
+void host_release(void* ptr);   // like host_free, never cached
 size_t host_pool_trim();   // release every cached free block; returns the bytes released
 // ||A - U diag(sigma) V'||_F / ||A||_F (sigma host or null = unscaled), strips of A on the device
 double relative_error(Handle& h, const double* a, int64_t m, int64_t n, int64_t lda, bool a_on_device,

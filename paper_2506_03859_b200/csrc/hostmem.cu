@@ -84,6 +84,19 @@ void host_free(void* ptr) {
     p.cached += bytes;
 }
 
+void host_release(void* ptr) {
+    if (!ptr) return;
+    Pool& p = pool();
+    std::lock_guard<std::mutex> lk(p.mu);
+    auto it = p.live.find(ptr);
+    if (it == p.live.end()) {
+        std::free(ptr);
+        return;
+    }
+    p.live.erase(it);
+    cudaFreeHost(ptr);
+}
+
 size_t host_pool_trim() {
     Pool& p = pool();
     std::lock_guard<std::mutex> lk(p.mu);
