@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", default="c4", choices=["c4", "c2"],
+                    help="c4: the headline (configs[3]); c2: configs[1], a secondary line (one GPU)")
     return ap.parse_args()
 
 
@@ -581,9 +583,156 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+# ---- secondary line: BASELINE configs[1] (C2), opt-in with --workload c2 ----------------
+C2_N, C2_RANK, C2_BLOCK, C2_POWER, C2_EPS = 8000, 900, 50, 2, 1e-3
+C2_WORKLOAD = ("C2: A = U diag(10^(-i/50)) V', 8000x8000 FP64 (fqb_gen_lowrank_det seed 42, 900 singular values "
+               "kept: sigma_900 = 1e-18); StdBernoulli Omega p=1/2; b=50, P=2, eps=1e-3 relative")
+
+
+def c2_sigma():
+    import numpy as np
+    return 10.0 ** (-np.arange(1, C2_RANK + 1, dtype=np.float64) / 50.0)
+
+
+def c2_config_dict():
+    return {"workload": C2_WORKLOAD, "m": C2_N, "n": C2_N, "block": C2_BLOCK, "power": C2_POWER, "eps": C2_EPS,
+            "relative": True, "sketch": "stdbernoulli", "p": 0.5, "seed_a": SEED_A, "seed_omega": SEED_OMEGA,
+            "step": "run_fixed_precision to eps + assemble_svd (U, sigma, V)",
+            "l2": "A (512 MB) exceeds the 126 MB L2; no flush needed", "parallelism": "single GPU"}
+
+
+def run_c2(args):
+    """C2 on one GPU: device time with A resident, e2e from pinned host A with Q, B', U, V
+    returned, and the unmodified reference (oracle/_ref, 1 core) timed on the whole run."""
+    import numpy as np
+    import torch
+    import paper_2506_03859_b200 as fqb
+    from paper_2506_03859_b200 import FarpcaConfig, SketchKind, SketchSpec
+    if int(os.environ.get("RANK", "0")) != 0:
+        return
+    dev = torch.device("cuda:0")
+    eng = fqb.Engine(0)
+    stream = torch.cuda.Stream(device=dev)
+    eng.set_stream(stream.cuda_stream)
+    a = eng.gen_lowrank_det(C2_N, C2_N, c2_sigma(), SEED_A)
+    cfg = FarpcaConfig(eps=C2_EPS, power=C2_POWER, block=C2_BLOCK,
+                       sketch=SketchSpec(SketchKind.StdBernoulli, 0.5, SEED_OMEGA), relative=True)
+    torch.cuda.synchronize()
+    clk = ClockSampler(0).__enter__()
+    t_wait = time.time()
+    while not clk.lines and time.time() - t_wait < 10.0:
+        time.sleep(0.05)
+    for _ in range(max(args.warmup, 0)):
+        eng.run_fixed_precision(a, cfg, output="device", svd=True)
+    torch.cuda.synchronize()
+    eng.set_pass_timing(True)
+    launches0 = eng.launch_count
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        e0.record()
+    last = None
+    for _ in range(args.steps):
+        last = None
+        last = eng.run_fixed_precision(a, cfg, output="device", svd=True)
+    with torch.cuda.stream(stream):
+        e1.record()
+    e1.synchronize()
+    launches = eng.launch_count - launches0
+    live_ms, live_n, _ = eng.pass_timing()
+    eng.set_pass_timing(False)
+    ms = e0.elapsed_time(e1) / args.steps
+    rank_l, blocks = last.rank, last.blocks
+    last = None
+    a_host = torch.empty((C2_N, C2_N), dtype=torch.float64, pin_memory=True)
+    a_host.copy_(a.t())
+    a_host_cm = a_host.t()
+    eng.run_fixed_precision(a_host_cm, cfg, output="host", svd=True)
+    t_e2e, r = [], None
+    for _ in range(max(1, args.steps)):
+        r = None
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = eng.run_fixed_precision(a_host_cm, cfg, output="host", svd=True)
+        t_e2e.append(time.perf_counter() - t0)
+    clk.__exit__(None, None, None)
+    d2h = 2 * (C2_N + C2_N) * r.rank * 8 + 9 * r.rank + 8 * (r.blocks + 4)
+    r = None
+    pk = peaks()
+    launch_ms = live_ms / max(live_n, 1)
+    bytes_launch = 8.0 * (C2_N * C2_N + 2 * C2_N * C2_BLOCK)
+    ref = None
+    if not args.no_cpu_baseline:
+        ref = c2_reference_time(a.cpu().numpy())
+    line = {"metric": "farPCA time-to-eps (s)", "value": ms / 1e3, "unit": "s", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: C2's A from fqb_gen_lowrank_det (seed 42), bit-identical to oracle/detgen.c",
+            "config": c2_config_dict(),
+            "result": {"rank": rank_l, "blocks": blocks},
+            "e2e": {"value": statistics.mean(t_e2e), "unit": "s", "h2d_bytes_per_step": C2_N * C2_N * 8,
+                    "d2h_bytes_per_step": d2h, "steps": len(t_e2e)},
+            "gpu_launches": int(launches),
+            "roofline": {"bound": "hbm", "kernel": "k_ozaki (A passes, one 50-column chunk) + fixup, live",
+                         "achieved": bytes_launch / (launch_ms * 1e-3) / 1e9, "peak": pk["hbm_gbs"],
+                         "unit": "GB/s", "frac": bytes_launch / (launch_ms * 1e-3) / 1e9 / pk["hbm_gbs"],
+                         "traffic": None, "launch_ms": launch_ms, "launches_timed": live_n,
+                         "bytes_formula": "8*(m*n + m*b + n*b) per launch"},
+            "clocks": clk.summary()}
+    if ref:
+        line["cpu_baseline"] = {"value": ref[0], "unit": "s", "cores": 1, "kind": ref[1],
+                                "sample": "the whole C2 run (run_fixed_precision + assemble_svd), one core",
+                                "host": host_info(), "rank": ref[2], "blocks": ref[3]}
+    print(json.dumps(line), flush=True)
+
+
+def c2_reference_time(a):
+    """The unmodified reference's run_fixed_precision on the whole C2 matrix (one core)."""
+    from oracle.oracle import REF_LIB, Oracle
+    which = "reference" if os.path.exists(REF_LIB) else "port"
+    orc = Oracle(which)
+    t0 = time.perf_counter()
+    r = orc.run(a, eps=C2_EPS, power=C2_POWER, block=C2_BLOCK, kind=2, p=0.5, seed=SEED_OMEGA, relative=True)
+    return time.perf_counter() - t0, which, r.rank, r.blocks
+
+
+def run_reference_c2(args):
+    import numpy as np
+    import ctypes as C
+    if int(os.environ.get("RANK", "0")) != 0:
+        return
+    from oracle.oracle import PORT_LIB
+    lib = C.CDLL(PORT_LIB)
+    lib.fqo_det_lowrank.argtypes = [C.c_int64, C.c_int64, C.c_int, C.c_void_p, C.c_uint64, C.c_double, C.c_int64,
+                                    C.c_int64, C.c_void_p, C.c_int64]
+    sig = c2_sigma()
+    a = np.empty((C2_N, C2_N), dtype=np.float64).T
+    st = lib.fqo_det_lowrank(C2_N, C2_N, len(sig), sig.ctypes.data, SEED_A, 0.0, 0, C2_N, a.ctypes.data, C2_N)
+    if st:
+        print(json.dumps({"impl": "reference", "unavailable": f"fqo_det_lowrank failed ({st})"}))
+        return
+    ts = []
+    for i in range(max(args.warmup, 0) + args.steps):
+        dt, which, rk, bl = c2_reference_time(a)
+        if i >= args.warmup:
+            ts.append(dt)
+    v = statistics.mean(ts)
+    print(json.dumps({"metric": "farPCA time-to-eps (s)", "value": v, "unit": "s", "n_gpus": args.gpus,
+                      "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False,
+                      "scaling": "strong", "vs_baseline": None, "dtype": "f64", "impl": "reference",
+                      "data": "synthetic: the same A (oracle/detgen.c == fqb_gen_lowrank_det)",
+                      "config": c2_config_dict(), "result": {"rank": rk, "blocks": bl},
+                      "cpu_baseline": {"value": v, "unit": "s", "cores": 1, "kind": which,
+                                       "sample": "each step the whole C2 run, one core", "sample_seconds": ts,
+                                       "host": host_info()},
+                      "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}),
+          flush=True)
+
+
 if __name__ == "__main__":
     a = parse()
-    if a.impl == "reference":
+    if a.workload == "c2":
+        run_reference_c2(a) if a.impl == "reference" else run_c2(a)
+    elif a.impl == "reference":
         run_reference(a)
     else:
         maybe_spawn(a)
