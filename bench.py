@@ -294,7 +294,7 @@ def sketch_roofline(eng, dev, pk):
 
 
 def load_traffic():
-    for name in ("R3_traffic.json", "R2_traffic.json"):
+    for name in ("R4_traffic.json", "R3_traffic.json", "R2_traffic.json"):
         try:
             with open(os.path.join(ROOT, "profiles", name)) as f:
                 return json.load(f)
@@ -675,7 +675,9 @@ def run_c2(args):
             "roofline": {"bound": "hbm", "kernel": "k_ozaki (A passes, one 50-column chunk) + fixup, live",
                          "achieved": bytes_launch / (launch_ms * 1e-3) / 1e9, "peak": pk["hbm_gbs"],
                          "unit": "GB/s", "frac": bytes_launch / (launch_ms * 1e-3) / 1e9 / pk["hbm_gbs"],
-                         "traffic": None, "launch_ms": launch_ms, "launches_timed": live_n,
+                         "traffic": ((load_traffic() or {}).get("c2") or {}).get("bytes_per_launch"),
+                         "traffic_source": ((load_traffic() or {}).get("c2") or {}).get("source"),
+                         "launch_ms": launch_ms, "launches_timed": live_n,
                          "bytes_formula": "8*(m*n + m*b + n*b) per launch"},
             "clocks": clk.summary()}
     if ref:
